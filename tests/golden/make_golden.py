@@ -1,0 +1,147 @@
+"""Generates tests/golden/* from the REFERENCE itself (oracle/_ref shim over the
+unmodified /root/reference headers).  Run in the build container:
+
+    make -C oracle && python tests/golden/make_golden.py
+
+Fixtures (all small):
+  geometry.json      tconv_geometry over n<=12, k<=7, p<=4 + rect cases
+                     (reference proj/tests/test_geometry.cpp:9-70)
+  counts.json        count_ops_naive/fused for BASELINE configs and tests
+                     (proj/include/segconv/analysis.hpp:31-67)
+  segregation.npz    sub-kernels of iota kernels (proj/tests/test_segregation.cpp)
+  frozen.npz         2x2 input, 3x3 ones, p=2 worked example
+                     (proj/tests/test_reference_ops.cpp:96-112)
+  verify_cases.npz   the first 200 run_verify cases, seed 20240911 (inputs +
+                     reference outputs; proj/include/segconv/verify.hpp:66-125)
+  real_cases.npz     U[-1,1] float cases incl. BASELINE-shaped reductions, with
+                     the reference's fused and naive outputs
+  f64_case.npz       a double-precision case (proj/tests/test_fused.cpp:61-70)
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+import oracle  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def iota(kh, kw, cin=1, cout=1):
+    return np.arange(1, kh * kw * cin * cout + 1, dtype=np.float32).reshape(kh, kw, cin, cout)
+
+
+def main():
+    # ---------------------------------------------------------------- geometry
+    geo = []
+    for n in range(1, 13):
+        for k in range(1, 8):
+            for p in range(0, 5):
+                try:
+                    g = oracle.ref_geometry(n, k, k, p)
+                    geo.append({"args": [n, k, k, p], "ok": True, "g": list(g.__dict__.values())})
+                except oracle.OracleError as e:
+                    geo.append({"args": [n, k, k, p], "ok": False, "code": e.code})
+    for args in ([8, 3, 4, 2], [28, 5, 5, 0], [0, 3, 3, 1], [4, 0, 3, 1], [4, 3, 3, -1],
+                 [1, 3, 3, 0], [32, 3, 3, 0], [64, 3, 3, 0], [16, 4, 4, 0], [256, 5, 5, 0],
+                 [4, 3, 3, 0], [5, 3, 3, 0], [7, 3, 3, 0], [11, 3, 3, 0]):
+        try:
+            g = oracle.ref_geometry(*args)
+            geo.append({"args": args, "ok": True, "g": list(g.__dict__.values())})
+        except oracle.OracleError as e:
+            geo.append({"args": args, "ok": False, "code": e.code})
+    with open(os.path.join(OUT, "geometry.json"), "w") as f:
+        json.dump(geo, f)
+
+    # ------------------------------------------------------------------ counts
+    shapes = [  # (n, cin, cout, kh, kw, p)
+        (32, 1, 1, 3, 3, 0), (64, 64, 32, 3, 3, 0), (16, 512, 256, 4, 4, 0),
+        (256, 64, 3, 5, 5, 0), (4, 1024, 512, 3, 3, 0), (5, 512, 256, 3, 3, 0),
+        (7, 256, 128, 3, 3, 0), (11, 128, 3, 3, 3, 0), (224, 3, 1, 5, 5, 3),
+        (4, 1024, 512, 4, 4, 2), (8, 512, 256, 4, 4, 2), (16, 256, 128, 4, 4, 2),
+        (32, 128, 3, 4, 4, 2), (6, 2, 3, 4, 4, 2), (5, 3, 2, 3, 3, 1), (7, 1, 2, 5, 5, 2),
+        (4, 2, 2, 7, 7, 3), (3, 2, 1, 1, 1, 0), (5, 2, 2, 3, 4, 2),
+    ]
+    counts = [{"shape": s, "ops": list(oracle.ref_count_ops(*s))} for s in shapes]
+    with open(os.path.join(OUT, "counts.json"), "w") as f:
+        json.dump(counts, f)
+
+    # ------------------------------------------------------------- segregation
+    seg = {}
+    for (kh, kw, cin, cout, p) in [(3, 3, 1, 1, 2), (3, 3, 1, 1, 1), (4, 4, 1, 1, 2),
+                                   (1, 1, 2, 3, 0), (5, 5, 2, 2, 3), (3, 4, 2, 3, 0),
+                                   (7, 2, 1, 2, 5), (5, 5, 1, 1, 0)]:
+        k = iota(kh, kw, cin, cout)
+        subs, offs = oracle.ref_segregate(k, p)
+        key = f"k{kh}x{kw}x{cin}x{cout}_p{p}"
+        seg[key + "_kernel"] = k
+        for q, s in enumerate(subs):
+            seg[f"{key}_sub{q}"] = s
+        seg[key + "_offs"] = np.array(offs, dtype=np.int32)
+    np.savez_compressed(os.path.join(OUT, "segregation.npz"), **seg)
+
+    # ------------------------------------------------------------------ frozen
+    x = np.array([1, 2, 3, 4], dtype=np.float32).reshape(2, 2, 1)
+    k = np.ones((3, 3, 1, 1), dtype=np.float32)
+    np.savez_compressed(os.path.join(OUT, "frozen.npz"), x=x, k=k, p=np.int32(2),
+                        naive=oracle.ref_tconv_naive(x, k, 2), fused=oracle.ref_tconv_fused(x, k, 2))
+
+    # ------------------------------------------------------------ verify cases
+    seed = 20240911
+    vc = {}
+    for i in range(200):
+        c = oracle.ref_verify_case(seed, i)
+        vc[f"c{i}_dims"] = np.array([c["n"], c["k"], c["p"], c["cin"], c["cout"]], dtype=np.int32)
+        vc[f"c{i}_x"] = c["x"].astype(np.int8)
+        vc[f"c{i}_k"] = c["kernel"].astype(np.int8)
+        vc[f"c{i}_y"] = c["y"]
+    summary = oracle.ref_run_verify(200, seed, -1)
+    fault = oracle.ref_run_verify(10, seed, 4)
+    vc["summary"] = np.array([summary["cases_run"], summary["failures"], summary["first_failure"],
+                              fault["cases_run"], fault["failures"], fault["first_failure"]],
+                             dtype=np.int32)
+    np.savez_compressed(os.path.join(OUT, "verify_cases.npz"), **vc)
+
+    # -------------------------------------------------------------- real cases
+    rng = np.random.default_rng(424242)
+    rc = {}
+    specs = []
+    for _ in range(60):
+        n = int(rng.integers(1, 9))
+        p = int(rng.integers(0, 5))
+        cap = min(7, 2 * n - 1 + 2 * p)
+        kh, kw = int(rng.integers(1, cap + 1)), int(rng.integers(1, cap + 1))
+        if 2 * n + 2 * p - kh < 1 or 2 * n + 2 * p - kw < 1:
+            continue
+        specs.append((1, n, int(rng.integers(1, 5)), int(rng.integers(1, 5)), kh, kw, p))
+    # BASELINE-shaped cases (full C1; the others reduced in batch / extent)
+    specs += [(1, 32, 1, 1, 3, 3, 0), (2, 12, 64, 32, 3, 3, 0), (1, 6, 128, 64, 4, 4, 0),
+              (1, 20, 64, 3, 5, 5, 0), (2, 4, 64, 32, 3, 3, 0), (2, 5, 32, 16, 3, 3, 0),
+              (1, 7, 16, 8, 3, 3, 0), (1, 11, 128, 3, 3, 3, 0), (1, 9, 2, 37, 3, 3, 1)]
+    for i, (b, n, cin, cout, kh, kw, p) in enumerate(specs):
+        x = rng.uniform(-1, 1, (b, n, n, cin)).astype(np.float32)
+        k = rng.uniform(-1, 1, (kh, kw, cin, cout)).astype(np.float32)
+        rc[f"r{i}_dims"] = np.array([b, n, cin, cout, kh, kw, p], dtype=np.int32)
+        rc[f"r{i}_x"] = x
+        rc[f"r{i}_k"] = k
+        rc[f"r{i}_fused"] = oracle.ref_tconv_fused(x, k, p)
+        rc[f"r{i}_naive"] = oracle.ref_tconv_naive(x, k, p)
+    rc["count"] = np.int32(len(specs))
+    np.savez_compressed(os.path.join(OUT, "real_cases.npz"), **rc)
+
+    # ---------------------------------------------------------------- double
+    r64 = np.random.default_rng(9)
+    x = r64.uniform(-1, 1, (6, 6, 2))
+    k = r64.uniform(-1, 1, (5, 5, 2, 3))
+    np.savez_compressed(os.path.join(OUT, "f64_case.npz"), x=x, k=k, p=np.int32(2),
+                        fused=oracle.ref_tconv_fused(x, k, 2), naive=oracle.ref_tconv_naive(x, k, 2))
+    print("golden fixtures written to", OUT)
+
+
+if __name__ == "__main__":
+    main()
