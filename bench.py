@@ -1,0 +1,540 @@
+#!/usr/bin/env python
+"""Benchmark of the segregated transpose convolution on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl segconv|reference]
+
+A step is one pass of the hot path (transpose_conv_fused, or the C5 stack)
+over one batch of synthetic input resident in HBM.  Weights are segregated
+once, untimed, as the reference bench does (proj/include/segconv/bench.hpp:83).
+Each timed step is bracketed by CUDA events on the launching stream; L2 is
+flushed (256 MiB write) between steps outside the events.  Multi-GPU: one
+process per GPU (torchrun), max over ranks.  Prints ONE JSON line on rank 0.
+
+Metric (BASELINE.json): useful GMAC/s (count_ops_fused numerator, reference
+analysis.hpp:48-67) with HBM GB/s / tensor TFLOP/s as a fraction of the
+measured roofline, vs the GPU upsample+conv path.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "useful GMAC/s & HBM GB/s (frac of roofline) vs upsample+conv, 1/2/4/8 B200"
+
+# BASELINE.json configs.  dist: u = U[-1,1]; n = N(0,1); he = N(0, sqrt(2/(cin*k*k)));
+# n02 = N(0, 0.02).
+CONFIGS = {
+    "C1": dict(batch=1, n=32, cin=1, cout=1, k=3, p=0, dtype="f32", xd="u", wd="u", act=None,
+               desc="single-channel fp32, 1x32x32x1 -> 61x61x1, n=3"),
+    "C2": dict(batch=16, n=64, cin=64, cout=32, k=3, p=0, dtype="f32", xd="u", wd="he", act=None,
+               desc="multi-channel fp32, 16x64x64x64 -> 16x125x125x32, n=3"),
+    "C3": dict(batch=128, n=16, cin=512, cout=256, k=4, p=0, dtype="bf16", xd="n", wd="n02",
+               act=None, desc="DCGAN-style bf16, 128x16x16x512 -> 128x28x28x256, n=4"),
+    "C4": dict(batch=32, n=256, cin=64, cout=3, k=5, p=0, dtype="f32", xd="u", wd="n02",
+               act="tanh", desc="low-channel fp32 + tanh, 32x256x256x64 -> 32x507x507x3, n=5"),
+    "C5": dict(batch=1024, stack=True, dtype="bf16",
+               desc="4-layer bf16 generator stack, batch 1024 sharded, 4->5->7->11->19"),
+}
+SEED = 20240911
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def gen(shape, dist, rng, fan_in=1):
+    if dist == "u":
+        return rng.uniform(-1.0, 1.0, shape).astype(np.float32)
+    if dist == "n":
+        return rng.standard_normal(shape, dtype=np.float32)
+    if dist == "he":
+        return (rng.standard_normal(shape, dtype=np.float32) * np.float32(np.sqrt(2.0 / fan_in)))
+    if dist == "n02":
+        return rng.standard_normal(shape, dtype=np.float32) * np.float32(0.02)
+    raise ValueError(dist)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm": d["hbm_gbs"], "bf16": d["bf16_tflops"], "src": "measured"}
+    return {"hbm": 6650.0, "bf16": 1590.0, "src": "fallback"}
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.terminate()
+            self.p.wait(timeout=5)
+
+    def summary(self):
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in rows if len(r) > 2 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 2 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for nm, v in zip(names, r[5:9]):
+                if v.strip() == "Active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+# --------------------------------------------------------------- problem
+class Layer:
+    """One segregated transpose conv (C1-C4) with host + device buffers."""
+
+    def __init__(self, cfg, rank, torch, sc, dev, world):
+        self.cfg = cfg
+        rng = np.random.default_rng(SEED + 7919 * rank)
+        b, n, cin, cout, k, p = (cfg[x] for x in ("batch", "n", "cin", "cout", "k", "p"))
+        self.x_host = gen((b, n, n, cin), cfg["xd"], rng)
+        krng = np.random.default_rng(SEED)
+        self.k_host = gen((k, k, cin, cout), cfg["wd"], krng, fan_in=cin * k * k)
+        self.tdt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
+        kd = torch.from_numpy(self.k_host).to(dev)
+        if world > 1:  # weights replicated from rank 0 (NCCL broadcast, untimed)
+            torch.distributed.broadcast(kd, src=0)
+        self.kd = kd.to(self.tdt)
+        self.xd = torch.from_numpy(self.x_host).to(dev, self.tdt)
+        self.g = sc.tconv_geometry(n, k, k, p)
+        self.sks = sc.segregate(self.kd, p, math="auto")
+        self.math = {v: k for k, v in sc.MATHS.items()}[self.sks.math]
+        self.y = torch.empty((b, self.g.out_h, self.g.out_w, cout), dtype=self.tdt, device=dev)
+        self.x_pinned = torch.from_numpy(self.x_host).to(self.tdt).pin_memory()
+        self.y_pinned = torch.empty(self.y.shape, dtype=self.tdt).pin_memory()
+        self.sc = sc
+        self.macs = sc.count_ops_fused(sc.LayerShape(n, cin, cout, k, k, p)).mults * b
+        e = self.xd.element_size()
+        self.alg_bytes = (self.xd.numel() + self.kd.numel() + self.y.numel()) * e
+        self.launches_per_step = 1
+        self.bound = "tensor" if self.math in ("bf16", "tf32") else "hbm"
+
+    def step(self):
+        self.sc.transpose_conv_fused(self.xd, self.sks, self.g, activation=self.cfg["act"],
+                                     out=self.y)
+
+    def step_e2e(self):
+        """Public API with host buffers: H2D of the step's input, compute, D2H of the result."""
+        self.xd.copy_(self.x_pinned, non_blocking=True)
+        self.step()
+        self.y_pinned.copy_(self.y, non_blocking=True)
+
+    def e2e_bytes(self):
+        return self.x_pinned.numel() * self.x_pinned.element_size(), \
+            self.y_pinned.numel() * self.y_pinned.element_size()
+
+    def conventional(self, torch, steps, flush):
+        """GPU upsample+conv (reference transpose_conv_naive) on the same data."""
+        cfg = self.cfg
+        ws_need = (cfg["batch"] * self.g.up_h ** 2 * cfg["cin"] * 4)
+        if ws_need > 24 * 2 ** 30 or self.tdt != torch.float32:
+            return None
+        xf = self.xd.float()
+        kf = torch.from_numpy(self.k_host).cuda()
+        ws = torch.empty(ws_need, dtype=torch.uint8, device="cuda")
+        ts = []
+        for i in range(steps + 1):
+            flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            self.sc.transpose_conv_naive(xf, kf, cfg["p"], activation=cfg["act"], workspace=ws)
+            b.record()
+            b.synchronize()
+            if i:
+                ts.append(a.elapsed_time(b))
+        ms = statistics.median(ts)
+        return {"value": round(self.macs / (ms * 1e-3) / 1e9, 2), "ms_per_step": round(ms, 4),
+                "what": "GPU upsample2x+pad then valid correlation (segconv_transpose_conv_naive)"}
+
+    def cudnn(self, torch, steps, flush):
+        """Library context: torch conv_transpose2d (cuDNN) on the same problem, NCHW."""
+        cfg = self.cfg
+        k = torch.from_numpy(self.k_host).cuda().to(self.tdt)
+        W = k.permute(2, 3, 0, 1).flip(2, 3).contiguous()
+        xn = self.xd.permute(0, 3, 1, 2).contiguous()
+        ts = []
+        for i in range(steps + 1):
+            flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            torch.nn.functional.conv_transpose2d(xn, W, stride=2, padding=cfg["k"] - 1 - cfg["p"])
+            b.record()
+            b.synchronize()
+            if i:
+                ts.append(a.elapsed_time(b))
+        ms = statistics.median(ts)
+        return {"value": round(self.macs / (ms * 1e-3) / 1e9, 2), "ms_per_step": round(ms, 4),
+                "what": "torch.nn.functional.conv_transpose2d (cuDNN), NCHW input, not ours"}
+
+    def cpu_sample(self, workers):
+        """Reference CPU path on a bounded sample of the batch: (out, secs, images)."""
+        import oracle
+        nimg = min(self.cfg["batch"], max(1, 2 * workers))
+        x = self.x_host[:nimg]
+        k = self.k_host
+        if self.cfg["dtype"] == "bf16":
+            x, k = oracle.bf16_round(x), oracle.bf16_round(k)
+        mode = 1  # images across threads, reference's sequential transpose_conv_fused each
+        if oracle.ref_available():
+            _, secs = oracle.ref_time_fused_batch(mode, x, k, self.cfg["p"], workers)
+            return secs, nimg, "reference"
+        t0 = time.perf_counter()
+        oracle.tconv_fused(x, k, self.cfg["p"])
+        return time.perf_counter() - t0, nimg, "port"
+
+
+class Stack:
+    """BASELINE C5: four-layer bf16 generator stack, batch 1024 sharded over ranks."""
+
+    def __init__(self, cfg, rank, world, torch, sc, dev):
+        from paper_2209_03704_b200 import stack as st
+        self.cfg = cfg
+        self.specs = st.c5_layers()
+        krng = np.random.default_rng(SEED)
+        self.k_host = [gen((s.k, s.k, s.cin, s.cout), "n02", krng) for s in self.specs]
+        ks = [torch.from_numpy(k).to(dev) for k in self.k_host]
+        if world > 1:
+            for k in ks:
+                torch.distributed.broadcast(k, src=0)
+        lo, hi = st.shard_range(cfg["batch"], rank, world)
+        self.lo, self.hi = lo, hi
+        s0 = self.specs[0]
+        rng = np.random.default_rng(SEED + 1)
+        xall = rng.standard_normal((cfg["batch"], s0.n_in, s0.n_in, s0.cin), dtype=np.float32)
+        self.x_host = xall[lo:hi]
+        self.stack = st.GeneratorStack(self.specs, ks, hi - lo, act_dtype=torch.bfloat16)
+        self.stack.x.copy_(torch.from_numpy(self.x_host))
+        self.math = "+".join({v: k for k, v in sc.MATHS.items()}[s.math] for s in self.stack.sks)
+        self.stack.capture()
+        self.macs = self.stack.useful_macs()
+        self.alg_bytes = self.stack.algorithmic_bytes()
+        self.launches_per_step = len(self.specs)
+        self.bound = "tensor"
+        self.x_pinned = torch.from_numpy(self.x_host).to(torch.bfloat16).pin_memory()
+        self.y_pinned = torch.empty(self.stack.out.shape, dtype=torch.bfloat16).pin_memory()
+
+    def step(self):
+        self.stack.forward()
+
+    def step_e2e(self):
+        self.stack.x.copy_(self.x_pinned, non_blocking=True)
+        self.stack.forward()
+        self.y_pinned.copy_(self.stack.out, non_blocking=True)
+
+    def e2e_bytes(self):
+        return self.x_pinned.numel() * 2, self.y_pinned.numel() * 2
+
+    def conventional(self, torch, steps, flush):
+        return None
+
+    def cudnn(self, torch, steps, flush):
+        return None
+
+    def cpu_sample(self, workers):
+        import oracle
+        nimg = min(self.hi - self.lo, max(1, 2 * workers))
+        x = oracle.bf16_round(self.x_host[:nimg])
+        t0 = time.perf_counter()
+        secs = 0.0
+        kind = "reference" if oracle.ref_available() else "port"
+        for s, k in zip(self.specs, self.k_host):
+            kb = oracle.bf16_round(k)
+            if kind == "reference":
+                y, dt = oracle.ref_time_fused_batch(1, x, kb, s.p, workers)
+                secs += dt
+            else:
+                y = oracle.tconv_fused(x, kb, s.p)
+            y = np.maximum(y, 0) if s.activation == "relu" else np.tanh(y)
+            x = oracle.bf16_round(y)
+        if kind == "port":
+            secs = time.perf_counter() - t0
+        return secs, nimg, kind
+
+
+def stack_macs_per_image():
+    from paper_2209_03704_b200 import segconv as sc
+    from paper_2209_03704_b200 import stack as st
+    return sum(sc.count_ops_fused(sc.LayerShape(s.n_in, s.cin, s.cout, s.k, s.k, s.p)).mults
+               for s in st.c5_layers())
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args, cfg):
+    """`--impl reference`: the reference's own CPU implementation (oracle/_ref, built
+    from the unmodified headers) on this box's host cores, same metric/config."""
+    import oracle
+    workers = os.cpu_count() or 1
+    kind = "reference" if oracle.ref_available() else "port"
+    name = args.config
+    rng = np.random.default_rng(SEED)
+    times, nimgs = [], 0
+    if cfg.get("stack"):
+        from paper_2209_03704_b200 import stack as st
+        specs = st.c5_layers()
+        krng = np.random.default_rng(SEED)
+        ks = [oracle.bf16_round(gen((s.k, s.k, s.cin, s.cout), "n02", krng)) for s in specs]
+        nimg = min(cfg["batch"], max(1, 2 * workers))
+        x0 = oracle.bf16_round(rng.standard_normal((nimg, 4, 4, 1024), dtype=np.float32))
+        macs_img = stack_macs_per_image()
+        for i in range(args.warmup + args.steps):
+            x, secs = x0, 0.0
+            for s, k in zip(specs, ks):
+                if kind == "reference":
+                    y, dt = oracle.ref_time_fused_batch(1, x, k, s.p, workers)
+                else:
+                    t0 = time.perf_counter()
+                    y = oracle.tconv_fused(x, k, s.p)
+                    dt = time.perf_counter() - t0
+                secs += dt
+                x = oracle.bf16_round(np.maximum(y, 0) if s.activation == "relu" else np.tanh(y))
+            if i >= args.warmup:
+                times.append(secs)
+        nimgs = nimg
+        macs = macs_img * nimg
+    else:
+        b, n, cin, cout, k, p = (cfg[x] for x in ("batch", "n", "cin", "cout", "k", "p"))
+        nimg = min(b, max(1, 2 * workers))
+        x = gen((nimg, n, n, cin), cfg["xd"], rng)
+        kk = gen((k, k, cin, cout), cfg["wd"], np.random.default_rng(SEED), fan_in=cin * k * k)
+        if cfg["dtype"] == "bf16":
+            x, kk = oracle.bf16_round(x), oracle.bf16_round(kk)
+        import ctypes  # noqa: F401
+        from oracle.oracle import count_ops
+        macs = count_ops(n, cin, cout, k, k, p)[2] * nimg
+        for i in range(args.warmup + args.steps):
+            if kind == "reference":
+                _, secs = oracle.ref_time_fused_batch(1, x, kk, p, workers)
+            else:
+                t0 = time.perf_counter()
+                oracle.tconv_fused(x, kk, p)
+                secs = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(secs)
+        nimgs = nimg
+    sec = statistics.median(times)
+    val = macs / sec / 1e9
+    sample = (f"{nimgs} of {cfg['batch']} images per step, harness batch-threading over the "
+              f"reference's sequential transpose_conv_fused (images across {workers} threads)"
+              if kind == "reference" else f"{nimgs} images per step, single-thread C port")
+    out = {"metric": METRIC, "value": round(val, 4), "unit": "useful GMAC/s", "impl": "reference",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
+           "scaling": "strong" if cfg.get("stack") else "weak", "vs_baseline": None,
+           "dtype": "f32", "data": "synthetic (seeded, BASELINE distributions)",
+           "config": {"workload": f"{name}: {cfg['desc']}", "sampled_images": nimgs},
+           "cpu_baseline": {"value": round(val, 4), "unit": "useful GMAC/s",
+                            "cores": workers if kind == "reference" else 1, "kind": kind,
+                            "sample": sample},
+           "e2e": {"value": round(val, 4), "unit": "useful GMAC/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------- main arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=os.environ.get("SEGCONV_BENCH_CONFIG", "C2"),
+                    choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="segconv", choices=["segconv", "reference"])
+    ap.add_argument("--no-baselines", action="store_true", help="skip conventional/cuDNN/CPU legs")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference(args, cfg)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2209_03704_b200 import segconv as sc
+
+    prob = Stack(cfg, rank, world, torch, sc, dev) if cfg.get("stack") else \
+        Layer(cfg, rank, torch, sc, dev, world)
+    flush_buf = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+
+    def flush():
+        flush_buf.fill_(1)
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        flush()
+        prob.step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, each bracketed by events; L2 flushed between steps
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = sc.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    with Clocks(local) as clk:
+        for a, b in evs:
+            flush()
+            a.record(stream)
+            prob.step()
+            b.record(stream)
+        torch.cuda.synchronize()
+    launches = sc.launch_count() - l0
+    if cfg.get("stack"):  # graph replays bypass the host counter: count the captured kernels
+        launches = args.steps * prob.launches_per_step
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    tot_ms = sum(step_ms)
+    t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    tot_ms = float(t.item())
+    ms = tot_ms / args.steps
+    macs_all = prob.macs * world if not cfg.get("stack") else prob.macs
+    if cfg.get("stack") and world > 1:
+        mt = torch.tensor([prob.macs], device=dev, dtype=torch.float64)
+        dist.all_reduce(mt)
+        macs_all = float(mt.item())
+    value = macs_all / (ms * 1e-3) / 1e9
+
+    # ---- e2e through the public API with host buffers (H2D + compute + D2H)
+    for _ in range(2):
+        prob.step_e2e()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record(stream)
+    for _ in range(args.steps):
+        prob.step_e2e()
+    eb.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([ea.elapsed_time(eb) / args.steps], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+    h2d, d2h = prob.e2e_bytes()
+
+    # ---- roofline of the dominant kernel (the whole step is that kernel, or the
+    # 4-kernel stack graph for C5)
+    pk = peaks()
+    kern_ms = statistics.mean(step_ms)
+    if prob.bound == "tensor":
+        ach = 2.0 * prob.macs / (kern_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": pk["bf16"],
+                "unit": "TFLOP/s", "frac": round(ach / pk["bf16"], 4),
+                "peak_src": pk["src"] + " bf16 burst"}
+    else:
+        ach = prob.alg_bytes / (kern_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm"], "unit": "GB/s",
+                "frac": round(ach / pk["hbm"], 4), "peak_src": pk["src"] + " copy"}
+    roof["traffic"] = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        tr = json.load(open(prof)).get(args.config)
+        if tr:
+            roof["traffic"] = tr.get("dram_bytes_per_launch")
+            roof["traffic_src"] = tr.get("source")
+    hbm_gbs = prob.alg_bytes / (kern_ms * 1e-3) / 1e9
+
+    out = None
+    if rank == 0:
+        extra = {}
+        if not args.no_baselines and world == 1:
+            try:
+                extra["conventional_gpu"] = prob.conventional(torch, 5, flush)
+            except Exception as e:  # report, do not hide
+                extra["conventional_gpu"] = {"error": str(e)[:200]}
+            try:
+                extra["cudnn_conv_transpose2d"] = prob.cudnn(torch, 5, flush)
+            except Exception as e:
+                extra["cudnn_conv_transpose2d"] = {"error": str(e)[:200]}
+            workers = os.cpu_count() or 1
+            try:
+                secs, nimg, kind = prob.cpu_sample(workers)
+                per_img = prob.macs / (cfg["batch"] if not cfg.get("stack") else prob.stack.batch)
+                cpu_val = per_img * nimg / secs / 1e9
+                extra["cpu_baseline"] = {
+                    "value": round(cpu_val, 4), "unit": "useful GMAC/s",
+                    "cores": workers if kind == "reference" else 1, "kind": kind,
+                    "sample": f"{nimg} images of the same workload, reference transpose_conv_fused "
+                              f"per image, images across {workers} host threads, one pass"}
+            except Exception as e:
+                extra["cpu_baseline"] = {"error": str(e)[:200]}
+        out = {"metric": METRIC, "value": round(value, 2), "unit": "useful GMAC/s",
+               "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": round(ms, 5), "higher_is_better": True,
+               "scaling": "strong" if cfg.get("stack") else "weak", "vs_baseline": None,
+               "dtype": "bf16" if cfg["dtype"] == "bf16" else "f32",
+               "data": "synthetic (seeded, BASELINE distributions; no dataset)",
+               "config": {"workload": f"{args.config}: {cfg['desc']}", "math": prob.math,
+                          "per_gpu_batch": (prob.hi - prob.lo) if cfg.get("stack") else cfg["batch"],
+                          "l2": "flushed between timed steps (256 MiB write, outside events)",
+                          "parallelism": f"batch-sharded x{world}, weights replicated"},
+               "hbm_gbs": round(hbm_gbs, 1),
+               "roofline": roof,
+               "e2e": {"value": round(macs_all / (e2e_ms * 1e-3) / 1e9, 2), "unit": "useful GMAC/s",
+                       "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                       "ms_per_step": round(e2e_ms, 4)},
+               "gpu_launches": int(launches),
+               "clocks": clk.summary()}
+        out.update(extra)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,173 @@
+/*
+ * segconv_b200.h -- C ABI of the B200-native segregated transpose convolution.
+ *
+ * This is the drop-in boundary.  The reference (`segconv`, header-only C++20,
+ * /root/reference/proj/include) has no FFI of its own; its operator API is the
+ * C++ template set in namespace segconv.  Each entry point below replaces one
+ * of those operators (cited as reference file:line) with a device-pointer,
+ * stream-ordered call; include/segconv_b200.hpp rebuilds the reference's C++
+ * signatures on top of it (value-semantics host tensors, same names, same
+ * ShapeError / ContractError behaviour).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  Device buffers are owned by the caller;
+ *    nothing is allocated on the hot path.  `stream` is a cudaStream_t passed
+ *    as void* (NULL = legacy default stream).  Launches are asynchronous.
+ *  - Layouts follow the reference: activations HWC per image with the channel
+ *    innermost (reference tensor.hpp:57-62,122-124); a batch is B contiguous
+ *    images (NHWC).  Kernels are (kh, kw, cin, cout), cout innermost
+ *    (tensor.hpp:148-151,198-200).
+ *  - All argument checks happen on the host before any launch and mirror the
+ *    reference's exceptions: SEGCONV_E_SHAPE <-> segconv::ShapeError,
+ *    SEGCONV_E_CONTRACT <-> segconv::ContractError (reference errors.hpp:14-23).
+ *    segconv_last_error() returns a thread-local message for the last failure.
+ *  - Entry points are stateless and reentrant (the plan object is the only
+ *    state, and it is immutable after creation).  No CPU fallback exists: if the
+ *    device code cannot run, calls return SEGCONV_E_CUDA.
+ */
+#ifndef SEGCONV_B200_H_
+#define SEGCONV_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SEGCONV_OK = 0,
+  SEGCONV_E_SHAPE = 1,       /* == segconv::ShapeError    (reference errors.hpp:16-18) */
+  SEGCONV_E_CONTRACT = 2,    /* == segconv::ContractError (reference errors.hpp:21-23) */
+  SEGCONV_E_CUDA = 3,        /* CUDA runtime / launch failure, no device, ...         */
+  SEGCONV_E_UNSUPPORTED = 4  /* valid request this build has no kernel for            */
+} segconv_status;
+
+/* Element types.  The reference supports float and double (tensor.hpp:65,154);
+ * bf16 is the BASELINE's tensor-core storage type (C3, C5). */
+typedef enum { SEGCONV_F32 = 0, SEGCONV_F64 = 1, SEGCONV_BF16 = 2 } segconv_dtype;
+
+/* Arithmetic used by transpose_conv_fused. */
+typedef enum {
+  SEGCONV_MATH_AUTO = 0,   /* pick from shape and dtypes                     */
+  SEGCONV_MATH_FFMA = 1,   /* SIMT, fp32 products + fp32 accumulate (fp64 for F64)           */
+  SEGCONV_MATH_EXACT = 2,  /* SIMT, reference accumulation order, no FMA contraction:         */
+                           /* bit-identical to the reference CPU path (slow; for parity)      */
+  SEGCONV_MATH_BF16 = 3,   /* tcgen05 kind::f16: bf16 operands, fp32 accumulate in TMEM       */
+  SEGCONV_MATH_TF32 = 4    /* tcgen05 kind::tf32: fp32 storage, tf32 operands, fp32 accumulate */
+} segconv_math;
+
+/* Epilogue flags, applied in this order: +bias[f], then ReLU or tanh. */
+enum {
+  SEGCONV_EPI_NONE = 0,
+  SEGCONV_EPI_BIAS = 1,
+  SEGCONV_EPI_RELU = 2,
+  SEGCONV_EPI_TANH = 4
+};
+
+/* Panel layouts produced by segconv_segregate. */
+typedef enum {
+  SEGCONV_PANEL_REF = 0,    /* per class (u, v, cin, cout): the reference sub-kernel layout  */
+                            /* (segregation.hpp:61-89); used by the SIMT kernels             */
+  SEGCONV_PANEL_KMAJOR = 1  /* per class (cout, u, v, cin): K-major MMA B operand, rows      */
+                            /* padded to cout_pad; used by the tcgen05 kernels               */
+} segconv_panel_layout;
+
+/* == segconv::TConvGeometry (reference geometry.hpp:18-27). */
+typedef struct {
+  int n_in, kh, kw, p_orig, p_fused, up_h, up_w, out_h, out_w;
+  int trim_extra_row, trim_extra_col;
+} segconv_geometry;
+
+/* Device-side counterpart of segconv::SubKernelSet<T> (reference
+ * segregation.hpp:43-55): describes the four parity panels, class q = r*2 + c,
+ * that segconv_segregate writes into one caller-owned buffer. */
+typedef struct {
+  int source_kh, source_kw, p_orig, p_orig_parity;
+  int cin, cout, cout_pad;
+  int sub_kh[4], sub_kw[4];      /* active_tap_count per axis (segregation.hpp:27-30) */
+  int off_r[4], off_c[4];        /* class_input_offset        (segregation.hpp:33-36) */
+  int u0[4], v0[4];              /* first_active_tap          (segregation.hpp:24)    */
+  int64_t sub_offset[4];         /* element offset of class q's panel                 */
+  int64_t total_elems;           /* elements in the whole panel buffer                */
+  int dtype;                     /* segconv_dtype of the panels                       */
+  int layout;                    /* segconv_panel_layout                              */
+} segconv_subkernels;
+
+/* ---------------------------------------------------------------- geometry */
+/* reference geometry.hpp:29-53 (tconv_geometry) */
+segconv_status segconv_tconv_geometry(int n_in, int kh, int kw, int p_orig, segconv_geometry* out);
+/* reference segregation.hpp:23-36 */
+int segconv_first_active_tap(int p, int r);
+int segconv_active_tap_count(int n, int p, int r);
+int segconv_class_input_offset(int p, int r);
+
+/* ------------------------------------------------------------- segregation */
+/* Shape half of reference segregation.hpp:61-89 (segregate): fills `out` for a
+ * (kh, kw, cin, cout) kernel at padding p_orig.  ContractError on kh/kw < 1,
+ * p_orig < 0 (segregation.hpp:63-64), ShapeError on cin/cout < 1. */
+segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_orig,
+                                       segconv_dtype panel_dtype, segconv_panel_layout layout,
+                                       segconv_subkernels* out);
+/* Data half of segregate: one kernel pass gathers taps k[u0+2u][v0+2v][ch][f]
+ * into the panels (with dtype conversion and re-layout).  d_kernel holds
+ * kh*kw*cin*cout elements of kernel_dtype; d_panels holds sks->total_elems. */
+segconv_status segconv_segregate(const void* d_kernel, segconv_dtype kernel_dtype,
+                                 const segconv_subkernels* sks, void* d_panels, void* stream);
+
+/* ------------------------------------------------------------ fused (hot) */
+/* reference fused_tconv.hpp:69-82 (transpose_conv_fused(input, sks, geom)),
+ * batched: d_x is (batch, n_in, n_in, cin) of x_dtype, d_y is
+ * (batch, out_h, out_w, cout) of y_dtype.  Checks of fused_tconv.hpp:17-35
+ * (check_fused_args) are applied.  d_bias (cout floats) is read only with
+ * SEGCONV_EPI_BIAS. */
+segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dtype, int batch,
+                                            int n_in, int cin, const segconv_subkernels* sks,
+                                            const void* d_panels, const segconv_geometry* geom,
+                                            const float* d_bias, unsigned epilogue,
+                                            segconv_math math, void* d_y, segconv_dtype y_dtype,
+                                            void* stream);
+
+/* Which math AUTO resolves to for this problem (no launch). */
+segconv_math segconv_select_math(segconv_dtype x_dtype, segconv_dtype panel_dtype, int cin,
+                                 int cout, int kh, int kw);
+
+/* ----------------------------------------------------- conventional path */
+/* reference tensor.hpp:224-259 (pad(upsample2x(x), p)): writes the
+ * (batch, up_h, up_w, cin) zero-inserted, padded map. */
+segconv_status segconv_upsample2x_pad(const void* d_x, segconv_dtype dtype, int batch, int n_in,
+                                      int cin, int p_orig, void* d_up, void* stream);
+/* reference reference_ops.hpp:86-108 (conv2d_valid), batched over `batch`
+ * (h, w, cin) maps; output (batch, h-kh+1, w-kw+1, cout). */
+segconv_status segconv_conv2d_valid(const void* d_src, segconv_dtype dtype, int batch, int h,
+                                    int w, int cin, const void* d_kernel, int kh, int kw,
+                                    int cout, const float* d_bias, unsigned epilogue, void* d_y,
+                                    void* stream);
+/* Bytes of workspace segconv_transpose_conv_naive needs (the upsampled map). */
+size_t segconv_naive_workspace_bytes(segconv_dtype dtype, int batch, int n_in, int cin,
+                                     int p_orig);
+/* reference reference_ops.hpp:116-133 (transpose_conv_naive): upsample, pad,
+ * valid-correlate -- the conventional baseline, materialising the map. */
+segconv_status segconv_transpose_conv_naive(const void* d_x, segconv_dtype dtype, int batch,
+                                            int n_in, int cin, const void* d_kernel, int kh,
+                                            int kw, int cout, int p_orig, void* d_workspace,
+                                            size_t workspace_bytes, const float* d_bias,
+                                            unsigned epilogue, void* d_y, void* stream);
+
+/* ------------------------------------------------------------ accounting */
+/* reference analysis.hpp:31-41,48-67: out = {naive mults, naive adds, fused
+ * mults, fused adds} for one image. */
+segconv_status segconv_count_ops(int n_in, int cin, int cout, int kh, int kw, int p_orig,
+                                 uint64_t out[4]);
+
+/* ------------------------------------------------------------ diagnostics */
+const char* segconv_last_error(void);
+const char* segconv_version(void);
+/* Number of kernels this library launched since load (all entry points). */
+uint64_t segconv_launch_count(void);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif /* SEGCONV_B200_H_ */

@@ -1,0 +1,94 @@
+"""ctypes binding of the C ABI in include/segconv_b200.h.
+
+Loads the in-tree ``libsegconv_b200.so`` (built by ``paper_2209_03704_b200.build``).
+There is no fallback: if the library is missing or cannot be loaded, importing
+the package's compute entry points raises ``SegconvLibraryError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libsegconv_b200.so")
+
+# segconv_status
+OK, E_SHAPE, E_CONTRACT, E_CUDA, E_UNSUPPORTED = range(5)
+# segconv_dtype
+F32, F64, BF16 = 0, 1, 2
+# segconv_math
+MATH_AUTO, MATH_FFMA, MATH_EXACT, MATH_BF16, MATH_TF32 = range(5)
+# epilogue flags
+EPI_NONE, EPI_BIAS, EPI_RELU, EPI_TANH = 0, 1, 2, 4
+# panel layouts
+PANEL_REF, PANEL_KMAJOR = 0, 1
+
+
+class SegconvLibraryError(RuntimeError):
+    pass
+
+
+class Geometry(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("n_in", "kh", "kw", "p_orig", "p_fused", "up_h", "up_w",
+                                       "out_h", "out_w", "trim_extra_row", "trim_extra_col")]
+
+
+class SubKernels(C.Structure):
+    _fields_ = [
+        ("source_kh", C.c_int), ("source_kw", C.c_int), ("p_orig", C.c_int),
+        ("p_orig_parity", C.c_int), ("cin", C.c_int), ("cout", C.c_int), ("cout_pad", C.c_int),
+        ("sub_kh", C.c_int * 4), ("sub_kw", C.c_int * 4), ("off_r", C.c_int * 4),
+        ("off_c", C.c_int * 4), ("u0", C.c_int * 4), ("v0", C.c_int * 4),
+        ("sub_offset", C.c_int64 * 4), ("total_elems", C.c_int64), ("dtype", C.c_int),
+        ("layout", C.c_int),
+    ]
+
+
+# (name, restype, argtypes) for every symbol include/segconv_b200.h declares.
+_vp, _i, _u, _sz = C.c_void_p, C.c_int, C.c_uint, C.c_size_t
+SIGNATURES = {
+    "segconv_tconv_geometry": (_i, [_i, _i, _i, _i, C.POINTER(Geometry)]),
+    "segconv_first_active_tap": (_i, [_i, _i]),
+    "segconv_active_tap_count": (_i, [_i, _i, _i]),
+    "segconv_class_input_offset": (_i, [_i, _i]),
+    "segconv_subkernels_init": (_i, [_i, _i, _i, _i, _i, _i, _i, C.POINTER(SubKernels)]),
+    "segconv_segregate": (_i, [_vp, _i, C.POINTER(SubKernels), _vp, _vp]),
+    "segconv_transpose_conv_fused": (_i, [_vp, _i, _i, _i, _i, C.POINTER(SubKernels), _vp,
+                                          C.POINTER(Geometry), _vp, _u, _i, _vp, _i, _vp]),
+    "segconv_select_math": (_i, [_i, _i, _i, _i, _i, _i]),
+    "segconv_upsample2x_pad": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _vp]),
+    "segconv_conv2d_valid": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _i, _vp, _u, _vp, _vp]),
+    "segconv_naive_workspace_bytes": (_sz, [_i, _i, _i, _i, _i]),
+    "segconv_transpose_conv_naive": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _vp, _sz,
+                                          _vp, _u, _vp, _vp]),
+    "segconv_count_ops": (_i, [_i, _i, _i, _i, _i, _i, C.POINTER(C.c_uint64)]),
+    "segconv_last_error": (C.c_char_p, []),
+    "segconv_version": (C.c_char_p, []),
+    "segconv_launch_count": (C.c_uint64, []),
+}
+
+_lib = None
+
+
+def lib():
+    """The loaded C library (raises SegconvLibraryError if it is not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise SegconvLibraryError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2209_03704_b200.build` "
+                "(there is no CPU fallback)")
+        try:
+            L = C.CDLL(LIB_PATH)
+        except OSError as e:  # pragma: no cover
+            raise SegconvLibraryError(f"cannot load {LIB_PATH}: {e}") from e
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return (lib().segconv_last_error() or b"").decode()

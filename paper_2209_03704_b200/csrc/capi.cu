@@ -1,0 +1,348 @@
+// capi.cu -- the extern "C" boundary (include/segconv_b200.h).
+//
+// Host-side validation mirrors the reference's exceptions before anything is
+// launched; dispatch picks the kernel family for the requested math.  There
+// is no CPU fallback: a missing device or a failed launch is SEGCONV_E_CUDA.
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "segconv_b200.h"
+
+namespace segconv_b200 {
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+static thread_local std::string g_err;
+
+static segconv_status fail(segconv_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+static segconv_status cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return SEGCONV_OK;
+  if (e == cudaErrorNotSupported)
+    return fail(SEGCONV_E_UNSUPPORTED, "%s: no kernel instantiation covers this problem", what);
+  cudaGetLastError();  // clear sticky-free errors so the next call is clean
+  return fail(SEGCONV_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+static bool valid_dtype(int d) { return d == SEGCONV_F32 || d == SEGCONV_F64 || d == SEGCONV_BF16; }
+static size_t dtype_size(int d) { return d == SEGCONV_F64 ? 8 : d == SEGCONV_BF16 ? 2 : 4; }
+
+static SegClasses classes_of(const segconv_subkernels& s, const segconv_geometry& g) {
+  SegClasses c{};
+  for (int q = 0; q < 4; ++q) {
+    const int r = q >> 1, cc = q & 1;
+    c.kh[q] = s.sub_kh[q];
+    c.kw[q] = s.sub_kw[q];
+    c.u0[q] = s.u0[q];
+    c.v0[q] = s.v0[q];
+    c.off_r[q] = s.off_r[q];
+    c.off_c[q] = s.off_c[q];
+    c.rows[q] = (g.out_h - r + 1) / 2;  // reference fused_tconv.hpp:51
+    c.cols[q] = (g.out_w - cc + 1) / 2;  // reference fused_tconv.hpp:52
+    c.sub_offset[q] = s.sub_offset[q];
+  }
+  return c;
+}
+
+}  // namespace segconv_b200
+
+using namespace segconv_b200;
+
+extern "C" {
+
+const char* segconv_last_error(void) { return g_err.c_str(); }
+const char* segconv_version(void) { return "segconv_b200 0.1 (sm_100a)"; }
+uint64_t segconv_launch_count(void) { return g_launches.load(); }
+
+// reference geometry.hpp:29-53
+segconv_status segconv_tconv_geometry(int n_in, int kh, int kw, int p_orig, segconv_geometry* g) {
+  if (!g) return fail(SEGCONV_E_CONTRACT, "geometry output pointer is null");
+  if (n_in < 1) return fail(SEGCONV_E_SHAPE, "input size must be >= 1, got %d", n_in);
+  if (kh < 1 || kw < 1) return fail(SEGCONV_E_SHAPE, "kernel dims must be >= 1, got %dx%d", kh, kw);
+  if (p_orig < 0) return fail(SEGCONV_E_SHAPE, "padding must be >= 0, got %d", p_orig);
+  segconv_geometry o;
+  o.n_in = n_in;
+  o.kh = kh;
+  o.kw = kw;
+  o.p_orig = p_orig;
+  o.p_fused = p_orig / 2;
+  o.up_h = o.up_w = 2 * n_in - 1 + 2 * p_orig;
+  o.out_h = o.up_h - kh + 1;
+  o.out_w = o.up_w - kw + 1;
+  if (o.out_h < 1 || o.out_w < 1)
+    return fail(SEGCONV_E_SHAPE, "kernel %dx%d does not fit the padded upsampled input (%dx%d)",
+                kh, kw, o.up_h, o.up_w);
+  o.trim_extra_row = o.out_h & 1;
+  o.trim_extra_col = o.out_w & 1;
+  *g = o;
+  return SEGCONV_OK;
+}
+
+// reference segregation.hpp:23-36
+int segconv_first_active_tap(int p, int r) { return (p + r) & 1; }
+int segconv_active_tap_count(int n, int p, int r) {
+  const int f = segconv_first_active_tap(p, r);
+  return f >= n ? 0 : (n - f + 1) / 2;
+}
+int segconv_class_input_offset(int p, int r) {
+  return (r + segconv_first_active_tap(p, r) - p) / 2 + p / 2;
+}
+
+// reference segregation.hpp:61-89 (shape half)
+segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_orig,
+                                       segconv_dtype panel_dtype, segconv_panel_layout layout,
+                                       segconv_subkernels* out) {
+  if (!out) return fail(SEGCONV_E_CONTRACT, "subkernel descriptor pointer is null");
+  if (kh < 1 || kw < 1) return fail(SEGCONV_E_CONTRACT, "cannot segregate a spatially empty kernel");
+  if (p_orig < 0) return fail(SEGCONV_E_CONTRACT, "padding must be non-negative");
+  if (cin < 1 || cout < 1)
+    return fail(SEGCONV_E_SHAPE, "bad kernel dims %dx%dx%dx%d", kh, kw, cin, cout);
+  if (!valid_dtype(panel_dtype)) return fail(SEGCONV_E_CONTRACT, "unknown panel dtype %d", (int)panel_dtype);
+  if (layout != SEGCONV_PANEL_REF && layout != SEGCONV_PANEL_KMAJOR)
+    return fail(SEGCONV_E_CONTRACT, "unknown panel layout %d", (int)layout);
+  segconv_subkernels s{};
+  s.source_kh = kh;
+  s.source_kw = kw;
+  s.p_orig = p_orig;
+  s.p_orig_parity = p_orig & 1;
+  s.cin = cin;
+  s.cout = cout;
+  // K-major panels pad the MMA N dimension to a multiple of 16 rows.
+  s.cout_pad = layout == SEGCONV_PANEL_KMAJOR ? (cout + 15) / 16 * 16 : cout;
+  int64_t off = 0;
+  for (int q = 0; q < 4; ++q) {
+    const int r = q >> 1, c = q & 1;
+    s.u0[q] = segconv_first_active_tap(p_orig, r);
+    s.v0[q] = segconv_first_active_tap(p_orig, c);
+    s.sub_kh[q] = segconv_active_tap_count(kh, p_orig, r);
+    s.sub_kw[q] = segconv_active_tap_count(kw, p_orig, c);
+    s.off_r[q] = segconv_class_input_offset(p_orig, r);
+    s.off_c[q] = segconv_class_input_offset(p_orig, c);
+    s.sub_offset[q] = off;
+    off += (int64_t)s.sub_kh[q] * s.sub_kw[q] * cin * s.cout_pad;
+  }
+  s.total_elems = off;
+  s.dtype = panel_dtype;
+  s.layout = layout;
+  *out = s;
+  return SEGCONV_OK;
+}
+
+segconv_status segconv_segregate(const void* d_kernel, segconv_dtype kernel_dtype,
+                                 const segconv_subkernels* sks, void* d_panels, void* stream) {
+  if (!sks || !d_kernel || !d_panels) return fail(SEGCONV_E_CONTRACT, "null argument to segregate");
+  if (!valid_dtype(kernel_dtype)) return fail(SEGCONV_E_CONTRACT, "unknown kernel dtype");
+  SegClasses cls{};
+  for (int q = 0; q < 4; ++q) {
+    cls.kh[q] = sks->sub_kh[q];
+    cls.kw[q] = sks->sub_kw[q];
+    cls.u0[q] = sks->u0[q];
+    cls.v0[q] = sks->v0[q];
+    cls.sub_offset[q] = sks->sub_offset[q];
+  }
+  if (sks->total_elems == 0) return SEGCONV_OK;
+  return cuda_status(launch_segregate(d_kernel, kernel_dtype, sks->source_kh, sks->source_kw,
+                                      sks->cin, sks->cout, sks->cout_pad, sks->layout, cls,
+                                      d_panels, sks->dtype, sks->total_elems,
+                                      (cudaStream_t)stream),
+                     "segregate");
+}
+
+segconv_math segconv_select_math(segconv_dtype x_dtype, segconv_dtype panel_dtype, int cin,
+                                 int cout, int kh, int kw) {
+  (void)kh;
+  (void)kw;
+  if (x_dtype == SEGCONV_BF16 && panel_dtype == SEGCONV_BF16 && cin >= 64 && cin % 64 == 0 &&
+      cout >= 16)
+    return SEGCONV_MATH_BF16;
+  return SEGCONV_MATH_FFMA;
+}
+
+// reference fused_tconv.hpp:17-35 (check_fused_args) + :69-82
+segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dtype, int batch,
+                                            int n_in, int cin, const segconv_subkernels* sks,
+                                            const void* d_panels, const segconv_geometry* geom,
+                                            const float* d_bias, unsigned epilogue,
+                                            segconv_math math, void* d_y, segconv_dtype y_dtype,
+                                            void* stream) {
+  if (!sks || !geom) return fail(SEGCONV_E_CONTRACT, "null descriptor");
+  if (batch < 0) return fail(SEGCONV_E_CONTRACT, "batch must be >= 0, got %d", batch);
+  if (n_in != geom->n_in)
+    return fail(SEGCONV_E_CONTRACT, "input is %dx%d but geometry was built for %dx%d", n_in, n_in,
+                geom->n_in, geom->n_in);
+  if (cin != sks->cin)
+    return fail(SEGCONV_E_CONTRACT, "channel mismatch: input has %d, sub-kernels expect %d", cin,
+                sks->cin);
+  if (sks->source_kh != geom->kh || sks->source_kw != geom->kw)
+    return fail(SEGCONV_E_CONTRACT,
+                "sub-kernel set was built from a %dx%d kernel, geometry expects %dx%d",
+                sks->source_kh, sks->source_kw, geom->kh, geom->kw);
+  if (sks->p_orig_parity != (geom->p_orig & 1))
+    return fail(SEGCONV_E_CONTRACT,
+                "sub-kernel set was segregated for padding parity %d, geometry has p_orig %d",
+                sks->p_orig_parity, geom->p_orig);
+  // The geometry must be one tconv_geometry would produce.
+  segconv_geometry chk;
+  if (segconv_tconv_geometry(geom->n_in, geom->kh, geom->kw, geom->p_orig, &chk) != SEGCONV_OK ||
+      chk.out_h != geom->out_h || chk.out_w != geom->out_w || chk.p_fused != geom->p_fused)
+    return fail(SEGCONV_E_CONTRACT, "inconsistent geometry descriptor");
+  if (!valid_dtype(x_dtype) || !valid_dtype(y_dtype))
+    return fail(SEGCONV_E_CONTRACT, "unknown activation dtype");
+  if ((epilogue & SEGCONV_EPI_RELU) && (epilogue & SEGCONV_EPI_TANH))
+    return fail(SEGCONV_E_CONTRACT, "ReLU and tanh epilogues are exclusive");
+  if ((epilogue & SEGCONV_EPI_BIAS) && !d_bias)
+    return fail(SEGCONV_E_CONTRACT, "bias epilogue requested without a bias pointer");
+  if (batch == 0) return SEGCONV_OK;
+  if (!d_x || !d_y || !d_panels) return fail(SEGCONV_E_CONTRACT, "null data pointer");
+
+  FusedProblem pr{};
+  pr.x = d_x;
+  pr.x_dtype = x_dtype;
+  pr.batch = batch;
+  pr.n = n_in;
+  pr.cin = cin;
+  pr.cout = sks->cout;
+  pr.cout_pad = sks->cout_pad;
+  pr.kh = geom->kh;
+  pr.kw = geom->kw;
+  pr.p = geom->p_orig;
+  pr.pf = geom->p_fused;
+  pr.out_h = geom->out_h;
+  pr.out_w = geom->out_w;
+  pr.cls = classes_of(*sks, *geom);
+  pr.panels = d_panels;
+  pr.panel_dtype = sks->dtype;
+  pr.panel_layout = sks->layout;
+  pr.bias = d_bias;
+  pr.epi = epilogue;
+  pr.y = d_y;
+  pr.y_dtype = y_dtype;
+  cudaStream_t s = (cudaStream_t)stream;
+
+  if (math == SEGCONV_MATH_AUTO)
+    math = segconv_select_math(x_dtype, (segconv_dtype)sks->dtype, cin, sks->cout, geom->kh,
+                               geom->kw);
+  switch (math) {
+    case SEGCONV_MATH_EXACT:
+      if (sks->layout != SEGCONV_PANEL_REF)
+        return fail(SEGCONV_E_CONTRACT, "EXACT math needs reference-layout panels");
+      return cuda_status(launch_direct_generic(pr, true, s), "transpose_conv_fused[exact]");
+    case SEGCONV_MATH_FFMA: {
+      if (sks->layout != SEGCONV_PANEL_REF)
+        return fail(SEGCONV_E_CONTRACT, "FFMA math needs reference-layout panels");
+      if (x_dtype != SEGCONV_F64 && sks->dtype != SEGCONV_F64) {
+        cudaError_t e = launch_direct_tiled(pr, s);
+        if (e != cudaErrorNotSupported) return cuda_status(e, "transpose_conv_fused[ffma]");
+      }
+      return cuda_status(launch_direct_generic(pr, false, s), "transpose_conv_fused[ffma]");
+    }
+    case SEGCONV_MATH_BF16:
+    case SEGCONV_MATH_TF32: {
+      if (sks->layout != SEGCONV_PANEL_KMAJOR)
+        return fail(SEGCONV_E_CONTRACT, "tensor-core math needs K-major panels");
+      if (!tc_igemm_supported(pr, math))
+        return fail(SEGCONV_E_UNSUPPORTED,
+                    "tensor-core path needs %s activations/panels and cin %% %d == 0",
+                    math == SEGCONV_MATH_BF16 ? "bf16" : "fp32", math == SEGCONV_MATH_BF16 ? 64 : 32);
+      return cuda_status(launch_tc_igemm(pr, math, s), "transpose_conv_fused[tcgen05]");
+    }
+    default:
+      return fail(SEGCONV_E_CONTRACT, "unknown math mode %d", (int)math);
+  }
+}
+
+size_t segconv_naive_workspace_bytes(segconv_dtype dtype, int batch, int n_in, int cin, int p_orig) {
+  if (batch < 0 || n_in < 1 || cin < 1 || p_orig < 0 || !valid_dtype(dtype)) return 0;
+  const size_t up = 2 * (size_t)n_in - 1 + 2 * (size_t)p_orig;
+  return (size_t)batch * up * up * cin * dtype_size(dtype);
+}
+
+segconv_status segconv_upsample2x_pad(const void* d_x, segconv_dtype dtype, int batch, int n_in,
+                                      int cin, int p_orig, void* d_up, void* stream) {
+  if (batch < 0 || n_in < 1 || cin < 1) return fail(SEGCONV_E_SHAPE, "tensor dims must be positive");
+  if (p_orig < 0) return fail(SEGCONV_E_CONTRACT, "pad factor must be non-negative");
+  if (!valid_dtype(dtype)) return fail(SEGCONV_E_CONTRACT, "unknown dtype");
+  if (batch == 0) return SEGCONV_OK;
+  return cuda_status(launch_upsample_pad(d_x, dtype, batch, n_in, cin, p_orig, d_up,
+                                         (cudaStream_t)stream),
+                     "upsample2x_pad");
+}
+
+// reference reference_ops.hpp:86-102
+segconv_status segconv_conv2d_valid(const void* d_src, segconv_dtype dtype, int batch, int h, int w,
+                                    int cin, const void* d_kernel, int kh, int kw, int cout,
+                                    const float* d_bias, unsigned epilogue, void* d_y,
+                                    void* stream) {
+  if (kh < 1 || kw < 1) return fail(SEGCONV_E_SHAPE, "conv2d_valid needs a non-empty kernel");
+  if (h < 1 || w < 1 || cin < 1 || cout < 1 || batch < 0)
+    return fail(SEGCONV_E_SHAPE, "tensor dims must be positive");
+  if (h - kh + 1 < 1 || w - kw + 1 < 1)
+    return fail(SEGCONV_E_SHAPE, "kernel %dx%d does not fit input %dx%d", kh, kw, h, w);
+  if (!valid_dtype(dtype)) return fail(SEGCONV_E_CONTRACT, "unknown dtype");
+  if ((epilogue & SEGCONV_EPI_BIAS) && !d_bias)
+    return fail(SEGCONV_E_CONTRACT, "bias epilogue requested without a bias pointer");
+  if (batch == 0) return SEGCONV_OK;
+  return cuda_status(launch_conv2d_valid(d_src, dtype, batch, h, w, cin, d_kernel, kh, kw, cout,
+                                         d_bias, epilogue, d_y, (cudaStream_t)stream),
+                     "conv2d_valid");
+}
+
+// reference reference_ops.hpp:116-133
+segconv_status segconv_transpose_conv_naive(const void* d_x, segconv_dtype dtype, int batch,
+                                            int n_in, int cin, const void* d_kernel, int kh,
+                                            int kw, int cout, int p_orig, void* d_workspace,
+                                            size_t workspace_bytes, const float* d_bias,
+                                            unsigned epilogue, void* d_y, void* stream) {
+  if (cin < 1 || cout < 1) return fail(SEGCONV_E_SHAPE, "bad kernel dims");
+  segconv_geometry g;
+  segconv_status st = segconv_tconv_geometry(n_in, kh, kw, p_orig, &g);
+  if (st != SEGCONV_OK) return st;
+  if (batch < 0) return fail(SEGCONV_E_CONTRACT, "batch must be >= 0");
+  const size_t need = segconv_naive_workspace_bytes(dtype, batch, n_in, cin, p_orig);
+  if (workspace_bytes < need)
+    return fail(SEGCONV_E_CONTRACT, "workspace too small: %zu < %zu bytes", workspace_bytes, need);
+  if (batch == 0) return SEGCONV_OK;
+  st = segconv_upsample2x_pad(d_x, dtype, batch, n_in, cin, p_orig, d_workspace, stream);
+  if (st != SEGCONV_OK) return st;
+  return segconv_conv2d_valid(d_workspace, dtype, batch, g.up_h, g.up_w, cin, d_kernel, kh, kw,
+                              cout, d_bias, epilogue, d_y, stream);
+}
+
+// reference analysis.hpp:31-67
+segconv_status segconv_count_ops(int n_in, int cin, int cout, int kh, int kw, int p_orig,
+                                 uint64_t out[4]) {
+  if (cin < 1 || cout < 1)
+    return fail(SEGCONV_E_SHAPE, "channel counts must be positive, got cin=%d cout=%d", cin, cout);
+  segconv_geometry g;
+  segconv_status st = segconv_tconv_geometry(n_in, kh, kw, p_orig, &g);
+  if (st != SEGCONV_OK) return st;
+  const uint64_t el = (uint64_t)g.out_h * g.out_w * cout, dl = (uint64_t)kh * kw * cin;
+  out[0] = el * dl;
+  out[1] = el * dl - el;
+  out[2] = out[3] = 0;
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 2; ++c) {
+      const uint64_t pos = (uint64_t)((g.out_h - r + 1) / 2) * ((g.out_w - c + 1) / 2);
+      const uint64_t len = (uint64_t)segconv_active_tap_count(kh, p_orig, r) *
+                           segconv_active_tap_count(kw, p_orig, c) * cin;
+      if (len == 0) continue;
+      out[2] += pos * cout * len;
+      out[3] += pos * cout * (len - 1);
+    }
+  return SEGCONV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+// common.cuh -- shared device helpers for the segconv B200 kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "segconv_b200.h"
+
+namespace segconv_b200 {
+
+// ----------------------------------------------------------------- dtypes
+template <typename T>
+struct DT;
+template <>
+struct DT<float> {
+  static constexpr int id = SEGCONV_F32;
+};
+template <>
+struct DT<double> {
+  static constexpr int id = SEGCONV_F64;
+};
+template <>
+struct DT<__nv_bfloat16> {
+  static constexpr int id = SEGCONV_BF16;
+};
+
+__device__ __forceinline__ float to_acc(float v) { return v; }
+__device__ __forceinline__ float to_acc(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ double to_acc(double v) { return v; }
+
+template <typename T>
+__device__ __forceinline__ T from_f(float v);
+template <>
+__device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) {
+  return __float2bfloat16_rn(v);
+}
+template <>
+__device__ __forceinline__ double from_f<double>(float v) { return (double)v; }
+
+template <typename T>
+__device__ __forceinline__ T from_d(double v);
+template <>
+__device__ __forceinline__ double from_d<double>(double v) { return v; }
+template <>
+__device__ __forceinline__ float from_d<float>(double v) { return (float)v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_d<__nv_bfloat16>(double v) {
+  return __float2bfloat16_rn((float)v);
+}
+
+// --------------------------------------------------------------- epilogue
+// Order: + bias[f], then ReLU or tanh (SEGCONV_EPI_* flags).
+__device__ __forceinline__ float epilogue_apply(float v, unsigned epi, const float* bias, int f) {
+  if (epi & SEGCONV_EPI_BIAS) v += __ldg(bias + f);
+  if (epi & SEGCONV_EPI_RELU) v = fmaxf(v, 0.0f);
+  if (epi & SEGCONV_EPI_TANH) v = tanhf(v);
+  return v;
+}
+__device__ __forceinline__ double epilogue_apply(double v, unsigned epi, const float* bias, int f) {
+  if (epi & SEGCONV_EPI_BIAS) v += (double)__ldg(bias + f);
+  if (epi & SEGCONV_EPI_RELU) v = v > 0.0 ? v : 0.0;
+  if (epi & SEGCONV_EPI_TANH) v = tanh(v);
+  return v;
+}
+
+// Store with the runtime output dtype (warp-uniform branch).
+__device__ __forceinline__ void store_out(void* y, long long idx, float v, int y_dtype) {
+  if (y_dtype == SEGCONV_BF16)
+    reinterpret_cast<__nv_bfloat16*>(y)[idx] = __float2bfloat16_rn(v);
+  else if (y_dtype == SEGCONV_F64)
+    reinterpret_cast<double*>(y)[idx] = (double)v;
+  else
+    reinterpret_cast<float*>(y)[idx] = v;
+}
+__device__ __forceinline__ void store_out(void* y, long long idx, double v, int y_dtype) {
+  if (y_dtype == SEGCONV_BF16)
+    reinterpret_cast<__nv_bfloat16*>(y)[idx] = __float2bfloat16_rn((float)v);
+  else if (y_dtype == SEGCONV_F64)
+    reinterpret_cast<double*>(y)[idx] = v;
+  else
+    reinterpret_cast<float*>(y)[idx] = (float)v;
+}
+
+}  // namespace segconv_b200

@@ -1,0 +1,57 @@
+// kernels.h -- internal launch interface between the C ABI (capi.cu) and the
+// kernel translation units.  Not part of the public boundary.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace segconv_b200 {
+
+// Per-class parity description, passed to kernels by value (class q = r*2 + c).
+struct SegClasses {
+  int kh[4], kw[4];        // active taps per axis (reference segregation.hpp:27-30)
+  int u0[4], v0[4];        // first active tap     (segregation.hpp:24)
+  int off_r[4], off_c[4];  // class input offset   (segregation.hpp:33-36)
+  int rows[4], cols[4];    // output block rows/cols of the class (fused_tconv.hpp:51-52)
+  long long sub_offset[4]; // element offset of the class panel
+};
+
+// Problem description for the fused (segregated) kernels.
+struct FusedProblem {
+  const void* x;
+  int x_dtype;
+  int batch, n, cin, cout, cout_pad;
+  int kh, kw, p, pf;  // source kernel dims, p_orig, p_fused
+  int out_h, out_w;
+  SegClasses cls;
+  const void* panels;
+  int panel_dtype, panel_layout;
+  const float* bias;
+  unsigned epi;
+  void* y;
+  int y_dtype;
+};
+
+cudaError_t launch_segregate(const void* k, int k_dtype, int kh, int kw, int cin, int cout,
+                             int cout_pad, int layout, const SegClasses& cls, void* panels,
+                             int p_dtype, long long total, cudaStream_t s);
+
+// SIMT kernels (direct.cu).  Return cudaErrorNotSupported when no
+// instantiation covers the problem.
+cudaError_t launch_direct_generic(const FusedProblem& pr, bool exact, cudaStream_t s);
+cudaError_t launch_direct_tiled(const FusedProblem& pr, cudaStream_t s);
+
+// Tensor-core implicit GEMM (tc_igemm.cu).
+cudaError_t launch_tc_igemm(const FusedProblem& pr, int math, cudaStream_t s);
+bool tc_igemm_supported(const FusedProblem& pr, int math);
+
+// Conventional path (conventional.cu).
+cudaError_t launch_upsample_pad(const void* x, int dtype, int batch, int n, int cin, int p,
+                                void* up, cudaStream_t s);
+cudaError_t launch_conv2d_valid(const void* src, int dtype, int batch, int h, int w, int cin,
+                                const void* k, int kh, int kw, int cout, const float* bias,
+                                unsigned epi, void* y, cudaStream_t s);
+
+void note_launch(int n = 1);
+
+}  // namespace segconv_b200

@@ -1,0 +1,459 @@
+"""Host-side mirror of the reference ``segconv`` operator API over the C ABI.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(/root/reference/proj/include/segconv, cited per function), operating on torch
+tensors in the reference's layouts:
+
+* activations: HWC per image (reference tensor.hpp:57-62), or a batch NHWC;
+* kernels: (kh, kw, cin, cout) (tensor.hpp:148-151).
+
+Device tensors are computed in place on the current CUDA stream.  Host (CPU)
+tensors are copied to the GPU, computed there and copied back, which is the
+value-semantics behaviour of the reference API -- the arithmetic always runs
+in the sm_100a kernels; there is no CPU implementation here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional, Sequence, Union
+
+import torch
+
+from . import _capi as A
+
+__all__ = [
+    "SegconvError", "ShapeError", "ContractError", "CudaError", "UnsupportedError",
+    "TConvGeometry", "tconv_geometry", "first_active_tap", "active_tap_count",
+    "class_input_offset", "sub_kernel_dims", "SubKernelSet", "segregate", "transpose_conv_fused",
+    "transpose_conv_fused_parallel", "transpose_conv_naive", "conv2d_valid", "upsample2x_pad",
+    "tensors_equal_exact", "tensors_equal_approx", "LayerShape", "OpCounts", "count_ops_naive",
+    "count_ops_fused", "select_math", "launch_count", "MATHS",
+]
+
+
+# ------------------------------------------------------------------ errors
+class SegconvError(RuntimeError):
+    """Base class (reference errors.hpp:10-12)."""
+
+
+class ShapeError(SegconvError):
+    """A dimension constraint was violated (reference errors.hpp:14-18)."""
+
+
+class ContractError(SegconvError):
+    """An API precondition was broken (reference errors.hpp:20-23)."""
+
+
+class CudaError(SegconvError):
+    """The device could not run the request (no CPU fallback exists)."""
+
+
+class UnsupportedError(SegconvError):
+    """Valid request with no kernel in this build."""
+
+
+_ERR = {A.E_SHAPE: ShapeError, A.E_CONTRACT: ContractError, A.E_CUDA: CudaError,
+        A.E_UNSUPPORTED: UnsupportedError}
+
+
+def _check(status: int) -> None:
+    if status != A.OK:
+        raise _ERR.get(status, SegconvError)(A.last_error())
+
+
+_DT = {torch.float32: A.F32, torch.float64: A.F64, torch.bfloat16: A.BF16}
+_DT_INV = {v: k for k, v in _DT.items()}
+MATHS = {"auto": A.MATH_AUTO, "ffma": A.MATH_FFMA, "exact": A.MATH_EXACT, "bf16": A.MATH_BF16,
+         "tf32": A.MATH_TF32}
+_MATH_INV = {v: k for k, v in MATHS.items()}
+_ACT = {None: A.EPI_NONE, "none": A.EPI_NONE, "relu": A.EPI_RELU, "tanh": A.EPI_TANH}
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _DT[t.dtype]
+    except KeyError:
+        raise ContractError(f"unsupported dtype {t.dtype} (float32, float64, bfloat16)") from None
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise CudaError("no CUDA device: the segregated transpose convolution runs only on the GPU")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def launch_count() -> int:
+    """Kernels launched by the C library since it was loaded."""
+    return int(A.lib().segconv_launch_count())
+
+
+# ---------------------------------------------------------------- geometry
+@dataclass(frozen=True)
+class TConvGeometry:
+    """== segconv::TConvGeometry (reference geometry.hpp:18-27)."""
+    n_in: int
+    kh: int
+    kw: int
+    p_orig: int
+    p_fused: int
+    up_h: int
+    up_w: int
+    out_h: int
+    out_w: int
+    trim_extra_row: bool
+    trim_extra_col: bool
+
+    def _c(self) -> A.Geometry:
+        return A.Geometry(self.n_in, self.kh, self.kw, self.p_orig, self.p_fused, self.up_h,
+                          self.up_w, self.out_h, self.out_w, int(self.trim_extra_row),
+                          int(self.trim_extra_col))
+
+
+def tconv_geometry(n_in: int, kh: int, kw: int, p_orig: int) -> TConvGeometry:
+    """reference geometry.hpp:29-53."""
+    g = A.Geometry()
+    _check(A.lib().segconv_tconv_geometry(int(n_in), int(kh), int(kw), int(p_orig), C.byref(g)))
+    return TConvGeometry(g.n_in, g.kh, g.kw, g.p_orig, g.p_fused, g.up_h, g.up_w, g.out_h,
+                         g.out_w, bool(g.trim_extra_row), bool(g.trim_extra_col))
+
+
+def first_active_tap(p: int, r: int) -> int:
+    """reference segregation.hpp:24."""
+    return A.lib().segconv_first_active_tap(p, r)
+
+
+def active_tap_count(n: int, p: int, r: int) -> int:
+    """reference segregation.hpp:27-30."""
+    return A.lib().segconv_active_tap_count(n, p, r)
+
+
+def class_input_offset(p: int, r: int) -> int:
+    """reference segregation.hpp:33-36."""
+    return A.lib().segconv_class_input_offset(p, r)
+
+
+def sub_kernel_dims(n: int):
+    """reference segregation.hpp:94-100: the four sub-kernel sizes of an odd n x n kernel."""
+    if n < 1:
+        raise ContractError("kernel size must be >= 1")
+    if n % 2 == 0:
+        raise ContractError("sub_kernel_dims is defined for odd sizes only")
+    hi, lo = (n + 1) // 2, n // 2
+    return [(hi, hi), (hi, lo), (lo, hi), (lo, lo)]
+
+
+# ------------------------------------------------------------- segregation
+class SubKernelSet:
+    """Device counterpart of segconv::SubKernelSet<T> (reference segregation.hpp:43-55).
+
+    ``panels`` is one device buffer holding the four parity sub-kernels (class
+    r*2+c).  Layout "ref" keeps the reference's (u, v, cin, cout) order (SIMT
+    kernels); layout "kmajor" stores (cout_pad, u, v, cin) rows for the
+    tcgen05 kernels.
+    """
+
+    def __init__(self, desc: A.SubKernels, panels: torch.Tensor, math: int):
+        self.desc = desc
+        self.panels = panels
+        self.math = math
+
+    source_kh = property(lambda s: s.desc.source_kh)
+    source_kw = property(lambda s: s.desc.source_kw)
+    p_orig_parity = property(lambda s: s.desc.p_orig_parity)
+    layout = property(lambda s: "ref" if s.desc.layout == A.PANEL_REF else "kmajor")
+    dtype = property(lambda s: s.panels.dtype)
+
+    def cin(self) -> int:
+        return self.desc.cin
+
+    def cout(self) -> int:
+        return self.desc.cout
+
+    def offset(self, r: int, c: int):
+        q = r * 2 + c
+        return (self.desc.off_r[q], self.desc.off_c[q])
+
+    @property
+    def class_input_offsets(self):
+        return [self.offset(q >> 1, q & 1) for q in range(4)]
+
+    def sub(self, r: int, c: int) -> torch.Tensor:
+        """View of class (r, c)'s panel in the reference (kh, kw, cin, cout) order."""
+        d, q = self.desc, r * 2 + c
+        kh, kw = d.sub_kh[q], d.sub_kw[q]
+        n = kh * kw * d.cin * d.cout_pad
+        flat = self.panels[d.sub_offset[q]: d.sub_offset[q] + n]
+        if d.layout == A.PANEL_REF:
+            return flat.view(kh, kw, d.cin, d.cout)
+        return flat.view(d.cout_pad, kh, kw, d.cin).permute(1, 2, 3, 0)[..., : d.cout]
+
+    @property
+    def subs(self):
+        return [self.sub(q >> 1, q & 1) for q in range(4)]
+
+
+def select_math(x_dtype: torch.dtype, panel_dtype: torch.dtype, cin: int, cout: int, kh: int,
+                kw: int) -> str:
+    """What math="auto" resolves to for a problem."""
+    m = A.lib().segconv_select_math(_DT[x_dtype], _DT[panel_dtype], cin, cout, kh, kw)
+    return _MATH_INV[m]
+
+
+def segregate(kernel: torch.Tensor, p_orig: int, *, math: str = "auto",
+              panel_dtype: Optional[torch.dtype] = None) -> SubKernelSet:
+    """reference segregation.hpp:61-89: split a (kh, kw, cin, cout) kernel into
+    the four parity panels, on the device.  ``math`` selects the consumer
+    ("ffma"/"exact" -> reference-layout panels; "bf16"/"tf32" -> K-major
+    panels for the tensor-core kernel; "auto" decides from dtype and shape)."""
+    if kernel.dim() != 4:
+        raise ShapeError(f"kernel must be (kh, kw, cin, cout), got {tuple(kernel.shape)}")
+    kh, kw, cin, cout = (int(v) for v in kernel.shape)
+    if kh < 1 or kw < 1:
+        raise ContractError("cannot segregate a spatially empty kernel")
+    if p_orig < 0:
+        raise ContractError("padding must be non-negative")
+    dev = _device()
+    k = kernel.to(dev).contiguous()
+    kd = _dtype_code(k)
+    if math not in MATHS:
+        raise ContractError(f"unknown math {math!r}")
+    m = MATHS[math]
+    if m == A.MATH_AUTO:
+        m = MATHS[select_math(k.dtype, panel_dtype or k.dtype, cin, cout, kh, kw)]
+    if panel_dtype is None:
+        panel_dtype = {A.MATH_BF16: torch.bfloat16, A.MATH_TF32: torch.float32}.get(m, k.dtype)
+    layout = A.PANEL_KMAJOR if m in (A.MATH_BF16, A.MATH_TF32) else A.PANEL_REF
+    desc = A.SubKernels()
+    _check(A.lib().segconv_subkernels_init(kh, kw, cin, cout, int(p_orig), _DT[panel_dtype],
+                                           layout, C.byref(desc)))
+    panels = torch.empty(max(1, desc.total_elems), dtype=panel_dtype, device=dev)
+    _check(A.lib().segconv_segregate(k.data_ptr(), kd, C.byref(desc), panels.data_ptr(),
+                                     _stream()))
+    return SubKernelSet(desc, panels, m)
+
+
+# ------------------------------------------------------------ fused (hot)
+def _as_batch(x: torch.Tensor):
+    if x.dim() == 3:
+        return x.unsqueeze(0), True
+    if x.dim() == 4:
+        return x, False
+    raise ShapeError(f"input must be HWC or NHWC, got {tuple(x.shape)}")
+
+
+def _epilogue(bias, activation):
+    if activation not in _ACT:
+        raise ContractError(f"unknown activation {activation!r} (relu, tanh, None)")
+    epi = _ACT[activation]
+    if bias is not None:
+        epi |= A.EPI_BIAS
+    return epi
+
+
+def transpose_conv_fused(x: torch.Tensor, k: Union[SubKernelSet, torch.Tensor],
+                         geom: Union[TConvGeometry, int, None] = None, *,
+                         bias: Optional[torch.Tensor] = None, activation: Optional[str] = None,
+                         math: Optional[str] = None, out_dtype: Optional[torch.dtype] = None,
+                         out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Segregated 2x transpose convolution.
+
+    ``transpose_conv_fused(x, sks, geom)``  -- reference fused_tconv.hpp:69-82
+    ``transpose_conv_fused(x, kernel, p)``  -- reference fused_tconv.hpp:85-92
+
+    ``x`` is (N, N, cin) or (B, N, N, cin); the result is (out_h, out_w, cout)
+    or (B, out_h, out_w, cout).  Optional fused epilogue: ``bias`` (cout,) then
+    ``activation`` "relu" | "tanh".
+    """
+    xb, squeeze = _as_batch(x)
+    if isinstance(k, torch.Tensor):
+        p = int(geom if geom is not None else 0)
+        if k.dim() != 4:
+            raise ShapeError("kernel must be (kh, kw, cin, cout)")
+        g = tconv_geometry(xb.shape[1], int(k.shape[0]), int(k.shape[1]), p)
+        if xb.shape[1] != xb.shape[2]:
+            raise ContractError(f"transpose conv expects a square input, got "
+                                f"{xb.shape[1]}x{xb.shape[2]}")
+        sks = segregate(k, p, math=math or "auto")
+    else:
+        if not isinstance(geom, TConvGeometry):
+            raise ContractError("transpose_conv_fused(x, sks, geom) needs a TConvGeometry")
+        sks, g = k, geom
+        if xb.shape[1] != g.n_in or xb.shape[2] != g.n_in:
+            raise ContractError(f"input is {xb.shape[1]}x{xb.shape[2]} but geometry was built "
+                                f"for {g.n_in}x{g.n_in}")
+    m = MATHS[math] if math is not None else sks.math
+    host = not xb.is_cuda
+    dev = _device()
+    xd = xb.to(dev).contiguous()
+    b, cin = int(xd.shape[0]), int(xd.shape[3])
+    odt = out_dtype or xd.dtype
+    if out is None:
+        y = torch.empty((b, g.out_h, g.out_w, sks.cout()), dtype=odt, device=dev)
+    else:
+        y = out if out.dim() == 4 else out.unsqueeze(0)
+        if tuple(y.shape) != (b, g.out_h, g.out_w, sks.cout()) or not y.is_contiguous():
+            raise ContractError("`out` has the wrong shape or is not contiguous")
+    epi = _epilogue(bias, activation)
+    bptr = None
+    if bias is not None:
+        bias = bias.to(dev, torch.float32).contiguous()
+        if bias.numel() != sks.cout():
+            raise ContractError(f"bias has {bias.numel()} elements, cout is {sks.cout()}")
+        bptr = bias.data_ptr()
+    gc = g._c()
+    _check(A.lib().segconv_transpose_conv_fused(
+        xd.data_ptr(), _dtype_code(xd), b, int(xd.shape[1]), cin, C.byref(sks.desc),
+        sks.panels.data_ptr(), C.byref(gc), bptr, epi, m, y.data_ptr(), _dtype_code(y),
+        _stream()))
+    if host:
+        y = y.cpu()
+    return y[0] if squeeze else y
+
+
+def transpose_conv_fused_parallel(x: torch.Tensor, sks: SubKernelSet, geom: TConvGeometry,
+                                  workers: int, **kw) -> torch.Tensor:
+    """reference fused_tconv.hpp:101-147.  The reference splits cout across CPU
+    threads; here the GPU grid is the parallelism, so ``workers`` is validated
+    (ContractError if < 1, fused_tconv.hpp:104) and otherwise has no effect --
+    the result equals transpose_conv_fused exactly, as in the reference."""
+    if workers < 1:
+        raise ContractError("worker count must be >= 1")
+    return transpose_conv_fused(x, sks, geom, **kw)
+
+
+# ------------------------------------------------------- conventional path
+def upsample2x_pad(x: torch.Tensor, p: int) -> torch.Tensor:
+    """reference tensor.hpp:224-259: pad(upsample2x(x), p) on the device."""
+    xb, squeeze = _as_batch(x)
+    dev = _device()
+    host = not xb.is_cuda
+    xd = xb.to(dev).contiguous()
+    b, h, w, c = (int(v) for v in xd.shape)
+    if h != w:
+        raise ContractError("upsample2x_pad expects square maps")
+    U = 2 * h - 1 + 2 * p
+    up = torch.empty((b, U, U, c), dtype=xd.dtype, device=dev)
+    _check(A.lib().segconv_upsample2x_pad(xd.data_ptr(), _dtype_code(xd), b, h, c, int(p),
+                                          up.data_ptr(), _stream()))
+    if host:
+        up = up.cpu()
+    return up[0] if squeeze else up
+
+
+def conv2d_valid(src: torch.Tensor, k: torch.Tensor, *, bias=None, activation=None) -> torch.Tensor:
+    """reference reference_ops.hpp:86-108."""
+    sb, squeeze = _as_batch(src)
+    dev = _device()
+    host = not sb.is_cuda
+    sd = sb.to(dev).contiguous()
+    kd = k.to(dev, sd.dtype).contiguous()
+    if kd.dim() != 4:
+        raise ShapeError("kernel must be (kh, kw, cin, cout)")
+    kh, kw, kc, cout = (int(v) for v in kd.shape)
+    b, h, w, cin = (int(v) for v in sd.shape)
+    if kh < 1 or kw < 1:
+        raise ShapeError("conv2d_valid needs a non-empty kernel")
+    if kc != cin:
+        raise ContractError(f"channel mismatch: input has {cin}, kernel expects {kc}")
+    oh, ow = h - kh + 1, w - kw + 1
+    if oh < 1 or ow < 1:
+        raise ShapeError(f"kernel {kh}x{kw} does not fit input {h}x{w}")
+    y = torch.empty((b, oh, ow, cout), dtype=sd.dtype, device=dev)
+    epi = _epilogue(bias, activation)
+    bptr = bias.to(dev, torch.float32).contiguous().data_ptr() if bias is not None else None
+    _check(A.lib().segconv_conv2d_valid(sd.data_ptr(), _dtype_code(sd), b, h, w, cin,
+                                        kd.data_ptr(), kh, kw, cout, bptr, epi, y.data_ptr(),
+                                        _stream()))
+    if host:
+        y = y.cpu()
+    return y[0] if squeeze else y
+
+
+def transpose_conv_naive(x: torch.Tensor, k: torch.Tensor, p: int, *, bias=None,
+                         activation=None, workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """reference reference_ops.hpp:116-133: upsample, pad, valid-correlate
+    (the conventional baseline; materialises the (2N-1+2p)^2 map)."""
+    xb, squeeze = _as_batch(x)
+    dev = _device()
+    host = not xb.is_cuda
+    xd = xb.to(dev).contiguous()
+    if k.dim() != 4:
+        raise ShapeError("kernel must be (kh, kw, cin, cout)")
+    kd = k.to(dev, xd.dtype).contiguous()
+    kh, kw, kc, cout = (int(v) for v in kd.shape)
+    b, h, w, cin = (int(v) for v in xd.shape)
+    if kc != cin:
+        raise ContractError(f"channel mismatch: input has {cin}, kernel expects {kc}")
+    g = tconv_geometry(h, kh, kw, p)
+    if h != w:
+        raise ContractError(f"transpose conv expects a square input, got {h}x{w}")
+    need = int(A.lib().segconv_naive_workspace_bytes(_dtype_code(xd), b, h, cin, int(p)))
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+    y = torch.empty((b, g.out_h, g.out_w, cout), dtype=xd.dtype, device=dev)
+    epi = _epilogue(bias, activation)
+    bptr = bias.to(dev, torch.float32).contiguous().data_ptr() if bias is not None else None
+    _check(A.lib().segconv_transpose_conv_naive(
+        xd.data_ptr(), _dtype_code(xd), b, h, cin, kd.data_ptr(), kh, kw, cout, int(p),
+        workspace.data_ptr(), workspace.numel() * workspace.element_size(), bptr, epi,
+        y.data_ptr(), _stream()))
+    if host:
+        y = y.cpu()
+    return y[0] if squeeze else y
+
+
+# ------------------------------------------------------------ comparators
+def tensors_equal_exact(a: torch.Tensor, b: torch.Tensor) -> bool:
+    """reference tensor.hpp:263-272: same shape and IEEE-equal (+0 == -0)."""
+    return tuple(a.shape) == tuple(b.shape) and bool(torch.equal(a.cpu(), b.cpu()) or
+                                                     bool((a.cpu() == b.cpu()).all()))
+
+
+def tensors_equal_approx(a: torch.Tensor, b: torch.Tensor, rel_tol: float) -> bool:
+    """reference tensor.hpp:275-286: |a-b| <= tol * max(|a|, |b|, 1)."""
+    if tuple(a.shape) != tuple(b.shape):
+        return False
+    a64, b64 = a.detach().double().cpu(), b.detach().double().cpu()
+    scale = torch.maximum(torch.maximum(a64.abs(), b64.abs()), torch.ones_like(a64))
+    return bool(((a64 - b64).abs() <= rel_tol * scale).all())
+
+
+# ---------------------------------------------------------------- counts
+@dataclass(frozen=True)
+class LayerShape:
+    """reference analysis.hpp:15-22."""
+    n_in: int
+    cin: int
+    cout: int
+    kh: int
+    kw: int
+    p_orig: int
+
+
+@dataclass(frozen=True)
+class OpCounts:
+    mults: int
+    adds: int
+
+
+def _counts(s: LayerShape):
+    o = (C.c_uint64 * 4)()
+    _check(A.lib().segconv_count_ops(s.n_in, s.cin, s.cout, s.kh, s.kw, s.p_orig, o))
+    return [int(v) for v in o]
+
+
+def count_ops_naive(s: LayerShape) -> OpCounts:
+    """reference analysis.hpp:31-41."""
+    v = _counts(s)
+    return OpCounts(v[0], v[1])
+
+
+def count_ops_fused(s: LayerShape) -> OpCounts:
+    """reference analysis.hpp:48-67 (useful MACs: the metric numerator)."""
+    v = _counts(s)
+    return OpCounts(v[2], v[3])

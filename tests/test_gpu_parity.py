@@ -1,0 +1,337 @@
+"""GPU parity of the sm_100a kernels against the oracle and the reference's own
+golden vectors, through the C ABI (via the ctypes mirror).
+
+Bars:
+  * integer-valued fuzz (run_verify ranges)  -> bit-exact in every math mode;
+  * EXACT math on real data                  -> bit-exact vs the reference;
+  * FFMA fp32 on real data                   -> |a-b| <= 1e-5 * max(|a|,|b|,1)
+    (the reference's tensors_equal_approx, tensor.hpp:275-286);
+  * bf16 / tf32 tensor-core paths            -> same form, tol 1e-2.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2209_03704_b200 import segconv as sc
+
+pytestmark = pytest.mark.gpu
+G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+TOL_F32 = 1e-5
+TOL_TC = 1e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    launches0 = sc.launch_count()
+    yield
+    assert sc.launch_count() > launches0  # the native kernels really ran
+
+
+def approx_ok(got, want, tol):
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    assert got.shape == want.shape
+    scale = np.maximum(np.maximum(np.abs(got), np.abs(want)), 1.0)
+    err = np.abs(got - want) / scale
+    i = int(np.argmax(err))
+    assert err.flat[i] <= tol, f"max scaled err {err.flat[i]:.3e} at flat index {i} " \
+                               f"(got {got.flat[i]}, want {want.flat[i]})"
+    return float(err.max())
+
+
+def cuda(a, dtype=torch.float32):
+    return torch.as_tensor(np.ascontiguousarray(a)).to("cuda", dtype)
+
+
+def run_fused(x, k, p, math="ffma", **kw):
+    xt, kt = cuda(x), cuda(k)
+    g = sc.tconv_geometry(xt.shape[-2], kt.shape[0], kt.shape[1], p)
+    sks = sc.segregate(kt, p, math=math)
+    y = sc.transpose_conv_fused(xt, sks, g, **kw)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+# ------------------------------------------------------------- segregation
+def test_segregate_panels_match_reference():
+    z = np.load(os.path.join(G, "segregation.npz"))
+    keys = sorted({k.rsplit("_", 1)[0] for k in z.files if k.endswith("_kernel")})
+    for key in keys:
+        k = z[key + "_kernel"]
+        p = int(key.split("_p")[1])
+        for math in ("ffma", "tf32"):
+            sks = sc.segregate(cuda(k), p, math=math)
+            for q in range(4):
+                got = sks.subs[q].float().cpu().numpy()
+                np.testing.assert_array_equal(got, z[f"{key}_sub{q}"], err_msg=f"{key} q{q} {math}")
+            assert [tuple(o) for o in z[key + "_offs"]] == sks.class_input_offsets
+
+
+# -------------------------------------------------------------- int fuzz
+@pytest.mark.parametrize("math", ["ffma", "exact"])
+def test_verify_fuzz_bit_exact(math):
+    """The reference's 200-case run_verify (seed 20240911): GPU == reference, exactly."""
+    z = np.load(os.path.join(G, "verify_cases.npz"))
+    for i in range(200):
+        n, k, p, cin, cout = z[f"c{i}_dims"].tolist()
+        got = run_fused(z[f"c{i}_x"].astype(np.float32), z[f"c{i}_k"].astype(np.float32), p, math)
+        np.testing.assert_array_equal(got, z[f"c{i}_y"], err_msg=f"case {i} (n={n} k={k} p={p})")
+
+
+def test_verify_fuzz_batched_bit_exact():
+    """Same cases, 3 images per launch (batch path, per-image geometry)."""
+    z = np.load(os.path.join(G, "verify_cases.npz"))
+    for i in range(0, 200, 7):
+        n, k, p, cin, cout = z[f"c{i}_dims"].tolist()
+        x = z[f"c{i}_x"].astype(np.float32)
+        kk = z[f"c{i}_k"].astype(np.float32)
+        xb = np.stack([x, -x, 2 * x])
+        got = run_fused(xb, kk, p)
+        want = z[f"c{i}_y"]
+        np.testing.assert_array_equal(got, np.stack([want, -want, 2 * want]))
+
+
+def test_injected_fault_is_localised():
+    """reference verify.hpp:26-28,95-102: corrupt one panel element of case 4 on
+    the device; the harness must report exactly case 4."""
+    z = np.load(os.path.join(G, "verify_cases.npz"))
+    bad = []
+    for i in range(10):
+        n, k, p, cin, cout = z[f"c{i}_dims"].tolist()
+        xt, kt = cuda(z[f"c{i}_x"]), cuda(z[f"c{i}_k"])
+        g = sc.tconv_geometry(n, k, k, p)
+        sks = sc.segregate(kt, p, math="ffma")
+        if i == 4:
+            for q in range(4):
+                d = sks.desc
+                if d.sub_kh[q] * d.sub_kw[q] > 0:
+                    sks.panels[d.sub_offset[q]] += 1.0
+                    break
+        y = sc.transpose_conv_fused(xt, sks, g).cpu().numpy()
+        if not np.array_equal(y, z[f"c{i}_y"]):
+            bad.append(i)
+    assert bad == [4]
+
+
+# ------------------------------------------------------------- real data
+def test_real_cases_exact_mode_bit_identical_to_reference():
+    z = np.load(os.path.join(G, "real_cases.npz"))
+    for i in range(int(z["count"])):
+        b, n, cin, cout, kh, kw, p = z[f"r{i}_dims"].tolist()
+        got = run_fused(z[f"r{i}_x"], z[f"r{i}_k"], p, "exact")
+        np.testing.assert_array_equal(got, z[f"r{i}_fused"], err_msg=f"real case {i}")
+
+
+def test_real_cases_ffma_within_tolerance():
+    z = np.load(os.path.join(G, "real_cases.npz"))
+    for i in range(int(z["count"])):
+        b, n, cin, cout, kh, kw, p = z[f"r{i}_dims"].tolist()
+        got = run_fused(z[f"r{i}_x"], z[f"r{i}_k"], p, "ffma")
+        approx_ok(got, z[f"r{i}_fused"], TOL_F32)
+
+
+def test_frozen_worked_example():
+    z = np.load(os.path.join(G, "frozen.npz"))
+    for math in ("ffma", "exact"):
+        np.testing.assert_array_equal(run_fused(z["x"], z["k"], 2, math), z["fused"])
+    y = sc.transpose_conv_naive(cuda(z["x"]), cuda(z["k"]), 2).cpu().numpy()
+    np.testing.assert_array_equal(y, z["naive"])
+
+
+def test_double_precision():
+    z = np.load(os.path.join(G, "f64_case.npz"))
+    xt, kt = cuda(z["x"], torch.float64), cuda(z["k"], torch.float64)
+    g = sc.tconv_geometry(6, 5, 5, 2)
+    for math in ("exact", "ffma"):
+        sks = sc.segregate(kt, 2, math=math)
+        y = sc.transpose_conv_fused(xt, sks, g).cpu().numpy()
+        if math == "exact":
+            np.testing.assert_array_equal(y, z["fused"])
+        else:
+            np.testing.assert_allclose(y, z["fused"], rtol=0, atol=1e-12)
+
+
+def test_degenerate_kernels():
+    # reference proj/tests/test_fused.cpp:94-115
+    rng = np.random.default_rng(31)
+    x = rng.uniform(-1, 1, (4, 4, 3)).astype(np.float32)
+    for (shape, p) in [((1, 1, 3, 2), 0), ((1, 4, 3, 2), 1)]:
+        k = rng.uniform(-1, 1, shape).astype(np.float32)
+        for math in ("ffma", "exact"):
+            got = run_fused(x, k, p, math)
+            want = oracle.tconv_fused(x, k, p)
+            if math == "exact":
+                np.testing.assert_array_equal(got, want)
+            else:
+                approx_ok(got, want, TOL_F32)
+    zero = np.zeros((3, 3, 3, 1), np.float32)
+    assert not run_fused(x, zero, 1).any()
+
+
+def test_contract_errors_on_device_tensors():
+    x = torch.zeros(6, 6, 2, device="cuda")
+    k = torch.zeros(4, 4, 2, 2, device="cuda")
+    with pytest.raises(sc.ContractError):
+        sc.transpose_conv_fused(x, sc.segregate(k, 1), sc.tconv_geometry(6, 4, 4, 2))
+    with pytest.raises(sc.ContractError):
+        sc.transpose_conv_fused(x, sc.segregate(k, 2), sc.tconv_geometry(5, 4, 4, 2))
+    with pytest.raises(sc.ContractError):
+        sc.transpose_conv_fused(torch.zeros(6, 6, 3, device="cuda"), sc.segregate(k, 2),
+                                sc.tconv_geometry(6, 4, 4, 2))
+    with pytest.raises(sc.ContractError):
+        sc.transpose_conv_fused(torch.zeros(5, 6, 2, device="cuda"), k, 2)
+    with pytest.raises(sc.ShapeError):
+        sc.transpose_conv_naive(torch.zeros(4, 4, 2, device="cuda"),
+                                torch.zeros(9, 9, 2, 1, device="cuda"), 0)
+
+
+def test_parallel_variant_equals_sequential():
+    rng = np.random.default_rng(1001)
+    x = cuda(rng.uniform(-1, 1, (9, 9, 2)))
+    k = cuda(rng.uniform(-1, 1, (3, 3, 2, 37)))
+    g = sc.tconv_geometry(9, 3, 3, 1)
+    sks = sc.segregate(k, 1)
+    seq = sc.transpose_conv_fused(x, sks, g)
+    for w in (1, 2, 3, 4, 9):
+        assert torch.equal(sc.transpose_conv_fused_parallel(x, sks, g, w), seq)
+    with pytest.raises(sc.ContractError):
+        sc.transpose_conv_fused_parallel(x, sks, g, 0)
+
+
+def test_host_tensors_round_trip():
+    """Value-semantics call with host tensors: H2D, compute on the GPU, D2H."""
+    rng = np.random.default_rng(4)
+    x = rng.uniform(-1, 1, (8, 8, 3)).astype(np.float32)
+    k = rng.uniform(-1, 1, (5, 5, 3, 4)).astype(np.float32)
+    y = sc.transpose_conv_fused(torch.from_numpy(x), torch.from_numpy(k), 2, math="exact")
+    assert y.device.type == "cpu"
+    np.testing.assert_array_equal(y.numpy(), oracle.ref_tconv_fused(x, k, 2)
+                                  if oracle.ref_available() else oracle.tconv_fused(x, k, 2))
+
+
+# --------------------------------------------------------- epilogue fusion
+@pytest.mark.parametrize("act", [None, "relu", "tanh"])
+def test_bias_activation_epilogue(act):
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-1, 1, (2, 10, 10, 8)).astype(np.float32)
+    for cout in (3, 40):
+        k = rng.normal(0, 0.2, (3, 3, 8, cout)).astype(np.float32)
+        bias = rng.normal(0, 0.5, cout).astype(np.float32)
+        got = run_fused(x, k, 0, "ffma", bias=cuda(bias), activation=act)
+        want = oracle.tconv_fused(x, k, 0).astype(np.float64) + bias
+        if act == "relu":
+            want = np.maximum(want, 0)
+        elif act == "tanh":
+            want = np.tanh(want)
+        approx_ok(got, want, TOL_F32)
+
+
+def test_bf16_storage_ffma():
+    """bf16 activations/weights, fp32 accumulate: vs the oracle on bf16-rounded inputs."""
+    rng = np.random.default_rng(5)
+    x = oracle.bf16_round(rng.normal(0, 1, (2, 7, 7, 128)))
+    k = oracle.bf16_round(rng.normal(0, 0.02, (3, 3, 128, 3)))
+    xt, kt = cuda(x, torch.bfloat16), cuda(k, torch.bfloat16)
+    g = sc.tconv_geometry(7, 3, 3, 0)
+    sks = sc.segregate(kt, 0, math="ffma")
+    y = sc.transpose_conv_fused(xt, sks, g, out_dtype=torch.float32).cpu().numpy()
+    approx_ok(y, oracle.tconv_fused(x, k, 0), TOL_F32)
+    yb = sc.transpose_conv_fused(xt, sks, g).float().cpu().numpy()
+    approx_ok(yb, oracle.tconv_fused(x, k, 0), TOL_TC)
+
+
+# ------------------------------------------------------- conventional path
+def test_conventional_path_matches_oracle_and_cudnn():
+    rng = np.random.default_rng(8)
+    for (n, cin, cout, kk, p) in [(9, 4, 5, 3, 0), (6, 3, 40, 4, 2), (12, 8, 3, 5, 1)]:
+        x = rng.uniform(-1, 1, (2, n, n, cin)).astype(np.float32)
+        k = rng.uniform(-1, 1, (kk, kk, cin, cout)).astype(np.float32)
+        got = sc.transpose_conv_naive(cuda(x), cuda(k), p).cpu().numpy()
+        approx_ok(got, oracle.tconv_naive(x, k, p), TOL_F32)
+        # independent library cross-check: conv_transpose2d with the
+        # kernel flipped and stride 2, padding n-1-p
+        W = torch.from_numpy(k).permute(2, 3, 0, 1).flip(2, 3).contiguous().cuda()
+        ref = torch.nn.functional.conv_transpose2d(cuda(x).permute(0, 3, 1, 2), W, stride=2,
+                                                   padding=kk - 1 - p)
+        approx_ok(got, ref.permute(0, 2, 3, 1).cpu().numpy(), 1e-4)
+
+
+def test_upsample_pad_matches_definition():
+    rng = np.random.default_rng(2)
+    x = rng.uniform(-1, 1, (2, 5, 5, 3)).astype(np.float32)
+    up = sc.upsample2x_pad(cuda(x), 2).cpu().numpy()
+    want = np.zeros((2, 13, 13, 3), np.float32)
+    want[:, 2:11:2, 2:11:2, :] = x
+    np.testing.assert_array_equal(up, want)
+
+
+# -------------------------------------------------- BASELINE-sized configs
+def _cfg_data(seed, b, n, cin, cout, kk, xdist, wdist):
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-1, 1, (b, n, n, cin)) if xdist == "u" else rng.normal(0, 1, (b, n, n, cin))
+    if wdist == "u":
+        k = rng.uniform(-1, 1, (kk, kk, cin, cout))
+    elif wdist == "he":
+        k = rng.normal(0, np.sqrt(2.0 / (cin * kk * kk)), (kk, kk, cin, cout))
+    else:
+        k = rng.normal(0, 0.02, (kk, kk, cin, cout))
+    return x.astype(np.float32), k.astype(np.float32)
+
+
+def test_config_c1_full():
+    x, k = _cfg_data(1, 1, 32, 1, 1, 3, "u", "u")
+    got = run_fused(x, k, 0)
+    assert got.shape == (1, 61, 61, 1)
+    approx_ok(got, oracle.tconv_fused(x, k, 0), TOL_F32)
+    np.testing.assert_array_equal(run_fused(x, k, 0, "exact"), oracle.tconv_fused(x, k, 0))
+
+
+def test_config_c2_full():
+    x, k = _cfg_data(2, 16, 64, 64, 32, 3, "u", "he")
+    got = run_fused(x, k, 0)
+    assert got.shape == (16, 125, 125, 32)
+    approx_ok(got, oracle.tconv_fused(x, k, 0), TOL_F32)
+
+
+def test_config_c4_full_tanh():
+    x, k = _cfg_data(4, 32, 256, 64, 3, 5, "u", "n")
+    got = run_fused(x, k, 0, activation="tanh")
+    assert got.shape == (32, 507, 507, 3)
+    idx = [0, 13, 31]  # oracle on a sample of images (each ~0.3 s on one core)
+    approx_ok(got[idx], np.tanh(oracle.tconv_fused(x[idx], k, 0)), TOL_F32)
+
+
+def test_linearity_full_size_int_exact():
+    """Size-independent property at the C2 size: T(a+b) == T(a) + T(b) exactly on ints."""
+    rng = np.random.default_rng(3)
+    a = rng.integers(-8, 9, (16, 64, 64, 64)).astype(np.float32)
+    b = rng.integers(-8, 9, (16, 64, 64, 64)).astype(np.float32)
+    k = rng.integers(-8, 9, (3, 3, 64, 32)).astype(np.float32)
+    ya, yb, ys = run_fused(a, k, 0), run_fused(b, k, 0), run_fused(a + b, k, 0)
+    np.testing.assert_array_equal(ys, ya + yb)
+
+
+def test_delta_kernel_routing():
+    """Single 1 at tap (a, b): input (i, j) lands at (2i+p-a, 2j+p-b) when in range
+    (reference SPEC / test_reference_ops.cpp:20-31)."""
+    rng = np.random.default_rng(6)
+    n, cin = 11, 2
+    x = rng.integers(-8, 9, (n, n, cin)).astype(np.float32)
+    for kk, p in [(3, 0), (4, 2), (5, 1)]:
+        for (a, b) in [(0, 0), (kk - 1, 0), (1, kk - 1)]:
+            k = np.zeros((kk, kk, cin, 1), np.float32)
+            k[a, b, 1, 0] = 1
+            y = run_fused(x, k, p)[..., 0]
+            g = oracle.geometry(n, kk, kk, p)
+            want = np.zeros((g.out_h, g.out_w), np.float32)
+            for i in range(n):
+                for j in range(n):
+                    yy, xx = 2 * i + p - a, 2 * j + p - b
+                    if 0 <= yy < g.out_h and 0 <= xx < g.out_w:
+                        want[yy, xx] = x[i, j, 1]
+            np.testing.assert_array_equal(y, want)
