@@ -165,8 +165,8 @@ segconv_math segconv_select_math(segconv_dtype x_dtype, segconv_dtype panel_dtyp
                                  int cout, int kh, int kw) {
   (void)kh;
   (void)kw;
-  if (x_dtype == SEGCONV_BF16 && panel_dtype == SEGCONV_BF16 && cin >= 64 && cin % 64 == 0 &&
-      cout >= 16)
+  if (x_dtype == SEGCONV_BF16 && panel_dtype == SEGCONV_BF16 &&
+      tc_igemm_available(SEGCONV_MATH_BF16, cin, cout))
     return SEGCONV_MATH_BF16;
   return SEGCONV_MATH_FFMA;
 }
