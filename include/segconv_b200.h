@@ -45,7 +45,12 @@ typedef enum {
 
 /* Element types.  The reference supports float and double (tensor.hpp:65,154);
  * bf16 is the BASELINE's tensor-core storage type (C3, C5). */
-typedef enum { SEGCONV_F32 = 0, SEGCONV_F64 = 1, SEGCONV_BF16 = 2 } segconv_dtype;
+typedef enum {
+  SEGCONV_F32 = 0,
+  SEGCONV_F64 = 1,
+  SEGCONV_BF16 = 2,
+  SEGCONV_F16_SPLIT = 3  /* panels only: fp32 weights stored as hi + lo fp16 planes */
+} segconv_dtype;
 
 /* Arithmetic used by transpose_conv_fused. */
 typedef enum {
@@ -54,7 +59,10 @@ typedef enum {
   SEGCONV_MATH_EXACT = 2,  /* SIMT, reference accumulation order, no FMA contraction:         */
                            /* bit-identical to the reference CPU path (slow; for parity)      */
   SEGCONV_MATH_BF16 = 3,   /* tcgen05 kind::f16: bf16 operands, fp32 accumulate in TMEM       */
-  SEGCONV_MATH_TF32 = 4    /* tcgen05 kind::tf32: fp32 storage, tf32 operands, fp32 accumulate */
+  SEGCONV_MATH_TF32 = 4,   /* reserved (kind::tf32); not built in this version                 */
+  SEGCONV_MATH_F16X3 = 5   /* tcgen05 kind::f16 on split operands: x = xh + xl, w = wh + wl     */
+                           /* (fp16 each), y = xh*wh + xl*wh + xh*wl accumulated in fp32 TMEM;  */
+                           /* ~22-bit operands, fp32-class accuracy for |x|,|w| < 2^15          */
 } segconv_math;
 
 /* Epilogue flags, applied in this order: +bias[f], then ReLU or tanh. */
@@ -69,8 +77,10 @@ enum {
 typedef enum {
   SEGCONV_PANEL_REF = 0,    /* per class (u, v, cin, cout): the reference sub-kernel layout  */
                             /* (segregation.hpp:61-89); used by the SIMT kernels             */
-  SEGCONV_PANEL_KMAJOR = 1  /* per class (cout, u, v, cin): K-major MMA B operand, rows      */
-                            /* padded to cout_pad; used by the tcgen05 kernels               */
+  SEGCONV_PANEL_KMAJOR = 1, /* per class (cout, u, v, cin): K-major, rows padded to cout_pad */
+  SEGCONV_PANEL_UMMA = 2    /* tcgen05 B-operand image: blocks (n_tile, k_block, class, tap),  */
+                            /* each [plane][k-chunk of 8][n_tile rows][8] -- the exact SMEM    */
+                            /* K-major no-swizzle layout, so one bulk copy stages one block     */
 } segconv_panel_layout;
 
 /* == segconv::TConvGeometry (reference geometry.hpp:18-27). */
@@ -92,6 +102,9 @@ typedef struct {
   int64_t total_elems;           /* elements in the whole panel buffer                */
   int dtype;                     /* segconv_dtype of the panels                       */
   int layout;                    /* segconv_panel_layout                              */
+  int n_tile;                    /* UMMA layout: output features per block            */
+  int k_block;                   /* UMMA layout: input channels per block             */
+  int math;                      /* segconv_math the panels were laid out for         */
 } segconv_subkernels;
 
 /* ---------------------------------------------------------------- geometry */
@@ -109,6 +122,10 @@ int segconv_class_input_offset(int p, int r);
 segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_orig,
                                        segconv_dtype panel_dtype, segconv_panel_layout layout,
                                        segconv_subkernels* out);
+/* Same, choosing dtype/layout for a math mode (AUTO resolves from x_dtype). */
+segconv_status segconv_subkernels_for_math(int kh, int kw, int cin, int cout, int p_orig,
+                                           segconv_dtype x_dtype, segconv_math math,
+                                           segconv_subkernels* out);
 /* Data half of segregate: one kernel pass gathers taps k[u0+2u][v0+2v][ch][f]
  * into the panels (with dtype conversion and re-layout).  d_kernel holds
  * kh*kw*cin*cout elements of kernel_dtype; d_panels holds sks->total_elems. */

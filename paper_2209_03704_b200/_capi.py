@@ -15,13 +15,13 @@ LIB_PATH = os.path.join(PKG, "libsegconv_b200.so")
 # segconv_status
 OK, E_SHAPE, E_CONTRACT, E_CUDA, E_UNSUPPORTED = range(5)
 # segconv_dtype
-F32, F64, BF16 = 0, 1, 2
+F32, F64, BF16, F16_SPLIT = 0, 1, 2, 3
 # segconv_math
-MATH_AUTO, MATH_FFMA, MATH_EXACT, MATH_BF16, MATH_TF32 = range(5)
+MATH_AUTO, MATH_FFMA, MATH_EXACT, MATH_BF16, MATH_TF32, MATH_F16X3 = range(6)
 # epilogue flags
 EPI_NONE, EPI_BIAS, EPI_RELU, EPI_TANH = 0, 1, 2, 4
 # panel layouts
-PANEL_REF, PANEL_KMAJOR = 0, 1
+PANEL_REF, PANEL_KMAJOR, PANEL_UMMA = 0, 1, 2
 
 
 class SegconvLibraryError(RuntimeError):
@@ -40,7 +40,7 @@ class SubKernels(C.Structure):
         ("sub_kh", C.c_int * 4), ("sub_kw", C.c_int * 4), ("off_r", C.c_int * 4),
         ("off_c", C.c_int * 4), ("u0", C.c_int * 4), ("v0", C.c_int * 4),
         ("sub_offset", C.c_int64 * 4), ("total_elems", C.c_int64), ("dtype", C.c_int),
-        ("layout", C.c_int),
+        ("layout", C.c_int), ("n_tile", C.c_int), ("k_block", C.c_int), ("math", C.c_int),
     ]
 
 
@@ -52,6 +52,7 @@ SIGNATURES = {
     "segconv_active_tap_count": (_i, [_i, _i, _i]),
     "segconv_class_input_offset": (_i, [_i, _i]),
     "segconv_subkernels_init": (_i, [_i, _i, _i, _i, _i, _i, _i, C.POINTER(SubKernels)]),
+    "segconv_subkernels_for_math": (_i, [_i, _i, _i, _i, _i, _i, _i, C.POINTER(SubKernels)]),
     "segconv_segregate": (_i, [_vp, _i, C.POINTER(SubKernels), _vp, _vp]),
     "segconv_transpose_conv_fused": (_i, [_vp, _i, _i, _i, _i, C.POINTER(SubKernels), _vp,
                                           C.POINTER(Geometry), _vp, _u, _i, _vp, _i, _vp]),

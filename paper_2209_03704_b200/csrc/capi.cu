@@ -110,9 +110,14 @@ segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_
   if (p_orig < 0) return fail(SEGCONV_E_CONTRACT, "padding must be non-negative");
   if (cin < 1 || cout < 1)
     return fail(SEGCONV_E_SHAPE, "bad kernel dims %dx%dx%dx%d", kh, kw, cin, cout);
-  if (!valid_dtype(panel_dtype)) return fail(SEGCONV_E_CONTRACT, "unknown panel dtype %d", (int)panel_dtype);
-  if (layout != SEGCONV_PANEL_REF && layout != SEGCONV_PANEL_KMAJOR)
+  if (!valid_dtype(panel_dtype) && panel_dtype != SEGCONV_F16_SPLIT)
+    return fail(SEGCONV_E_CONTRACT, "unknown panel dtype %d", (int)panel_dtype);
+  if (layout != SEGCONV_PANEL_REF && layout != SEGCONV_PANEL_KMAJOR && layout != SEGCONV_PANEL_UMMA)
     return fail(SEGCONV_E_CONTRACT, "unknown panel layout %d", (int)layout);
+  if (layout == SEGCONV_PANEL_UMMA && panel_dtype != SEGCONV_BF16 && panel_dtype != SEGCONV_F16_SPLIT)
+    return fail(SEGCONV_E_CONTRACT, "UMMA panels are bf16 or split-fp16");
+  if (layout != SEGCONV_PANEL_UMMA && panel_dtype == SEGCONV_F16_SPLIT)
+    return fail(SEGCONV_E_CONTRACT, "split-fp16 panels need the UMMA layout");
   segconv_subkernels s{};
   s.source_kh = kh;
   s.source_kw = kw;
@@ -120,9 +125,15 @@ segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_
   s.p_orig_parity = p_orig & 1;
   s.cin = cin;
   s.cout = cout;
+  s.dtype = panel_dtype;
+  s.layout = layout;
+  s.math = layout == SEGCONV_PANEL_UMMA
+               ? (panel_dtype == SEGCONV_F16_SPLIT ? SEGCONV_MATH_F16X3 : SEGCONV_MATH_BF16)
+               : SEGCONV_MATH_FFMA;
   // K-major panels pad the MMA N dimension to a multiple of 16 rows.
   s.cout_pad = layout == SEGCONV_PANEL_KMAJOR ? (cout + 15) / 16 * 16 : cout;
   int64_t off = 0;
+  int taps = 0;
   for (int q = 0; q < 4; ++q) {
     const int r = q >> 1, c = q & 1;
     s.u0[q] = segconv_first_active_tap(p_orig, r);
@@ -131,14 +142,57 @@ segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_
     s.sub_kw[q] = segconv_active_tap_count(kw, p_orig, c);
     s.off_r[q] = segconv_class_input_offset(p_orig, r);
     s.off_c[q] = segconv_class_input_offset(p_orig, c);
-    s.sub_offset[q] = off;
+    s.sub_offset[q] = layout == SEGCONV_PANEL_UMMA ? taps : off;  // UMMA: first tap block
     off += (int64_t)s.sub_kh[q] * s.sub_kw[q] * cin * s.cout_pad;
+    taps += s.sub_kh[q] * s.sub_kw[q];
   }
   s.total_elems = off;
-  s.dtype = panel_dtype;
-  s.layout = layout;
+  if (layout == SEGCONV_PANEL_UMMA) {
+    s.n_tile = tc_n_tile(s.math, cout);
+    s.k_block = tc_k_block(cin, cout);
+    const int n_tiles = (cout + s.n_tile - 1) / s.n_tile;
+    const int nkb = (cin + s.k_block - 1) / s.k_block;
+    const int planes = panel_dtype == SEGCONV_F16_SPLIT ? 2 : 1;
+    s.cout_pad = n_tiles * s.n_tile;
+    s.total_elems = (int64_t)n_tiles * nkb * taps * planes * s.k_block * s.n_tile;
+  }
   *out = s;
   return SEGCONV_OK;
+}
+
+static bool tc_shape_ok(int kh, int kw, int p_orig) {
+  // every parity class must own at least one tap (kh, kw >= 2 guarantees it)
+  for (int r = 0; r < 2; ++r)
+    if (segconv_active_tap_count(kh, p_orig, r) == 0 || segconv_active_tap_count(kw, p_orig, r) == 0)
+      return false;
+  return kh * kw <= 49;
+}
+
+segconv_status segconv_subkernels_for_math(int kh, int kw, int cin, int cout, int p_orig,
+                                           segconv_dtype x_dtype, segconv_math math,
+                                           segconv_subkernels* out) {
+  if (!valid_dtype(x_dtype)) return fail(SEGCONV_E_CONTRACT, "unknown activation dtype");
+  if (math == SEGCONV_MATH_AUTO) {
+    math = segconv_select_math(x_dtype, x_dtype, cin, cout, kh, kw);
+    if ((math == SEGCONV_MATH_BF16 || math == SEGCONV_MATH_F16X3) && !tc_shape_ok(kh, kw, p_orig))
+      math = SEGCONV_MATH_FFMA;
+  }
+  switch (math) {
+    case SEGCONV_MATH_FFMA:
+    case SEGCONV_MATH_EXACT: {
+      const segconv_status st =
+          segconv_subkernels_init(kh, kw, cin, cout, p_orig, x_dtype, SEGCONV_PANEL_REF, out);
+      if (st == SEGCONV_OK) out->math = math;
+      return st;
+    }
+    case SEGCONV_MATH_BF16:
+      return segconv_subkernels_init(kh, kw, cin, cout, p_orig, SEGCONV_BF16, SEGCONV_PANEL_UMMA, out);
+    case SEGCONV_MATH_F16X3:
+      return segconv_subkernels_init(kh, kw, cin, cout, p_orig, SEGCONV_F16_SPLIT,
+                                     SEGCONV_PANEL_UMMA, out);
+    default:
+      return fail(SEGCONV_E_UNSUPPORTED, "math mode %d has no kernels in this build", (int)math);
+  }
 }
 
 segconv_status segconv_segregate(const void* d_kernel, segconv_dtype kernel_dtype,
@@ -154,6 +208,17 @@ segconv_status segconv_segregate(const void* d_kernel, segconv_dtype kernel_dtyp
     cls.sub_offset[q] = sks->sub_offset[q];
   }
   if (sks->total_elems == 0) return SEGCONV_OK;
+  if (sks->layout == SEGCONV_PANEL_UMMA) {
+    int taps = 0;
+    for (int q = 0; q < 4; ++q) taps += sks->sub_kh[q] * sks->sub_kw[q];
+    const int n_tiles = sks->cout_pad / sks->n_tile;
+    const int nkb = (sks->cin + sks->k_block - 1) / sks->k_block;
+    return cuda_status(launch_segregate_umma(d_kernel, kernel_dtype, sks->source_kw, sks->cin,
+                                             sks->cout, cls, sks->n_tile, sks->k_block, nkb,
+                                             n_tiles, taps, sks->dtype == SEGCONV_F16_SPLIT,
+                                             d_panels, (cudaStream_t)stream),
+                       "segregate[umma]");
+  }
   return cuda_status(launch_segregate(d_kernel, kernel_dtype, sks->source_kh, sks->source_kw,
                                       sks->cin, sks->cout, sks->cout_pad, sks->layout, cls,
                                       d_panels, sks->dtype, sks->total_elems,
@@ -165,9 +230,13 @@ segconv_math segconv_select_math(segconv_dtype x_dtype, segconv_dtype panel_dtyp
                                  int cout, int kh, int kw) {
   (void)kh;
   (void)kw;
-  if (x_dtype == SEGCONV_BF16 && panel_dtype == SEGCONV_BF16 &&
+  const bool taps_ok = kh >= 2 && kw >= 2 && kh * kw <= 49;
+  if (x_dtype == SEGCONV_BF16 && (panel_dtype == SEGCONV_BF16) && taps_ok &&
       tc_igemm_available(SEGCONV_MATH_BF16, cin, cout))
     return SEGCONV_MATH_BF16;
+  if (x_dtype == SEGCONV_F32 && (panel_dtype == SEGCONV_F32 || panel_dtype == SEGCONV_F16_SPLIT) &&
+      taps_ok && tc_igemm_available(SEGCONV_MATH_F16X3, cin, cout))
+    return SEGCONV_MATH_F16X3;
   return SEGCONV_MATH_FFMA;
 }
 
@@ -232,9 +301,7 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
   pr.y_dtype = y_dtype;
   cudaStream_t s = (cudaStream_t)stream;
 
-  if (math == SEGCONV_MATH_AUTO)
-    math = segconv_select_math(x_dtype, (segconv_dtype)sks->dtype, cin, sks->cout, geom->kh,
-                               geom->kw);
+  if (math == SEGCONV_MATH_AUTO) math = (segconv_math)sks->math;  // what the panels were built for
   switch (math) {
     case SEGCONV_MATH_EXACT:
       if (sks->layout != SEGCONV_PANEL_REF)
@@ -250,13 +317,17 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
       return cuda_status(launch_direct_generic(pr, false, s), "transpose_conv_fused[ffma]");
     }
     case SEGCONV_MATH_BF16:
-    case SEGCONV_MATH_TF32: {
-      if (sks->layout != SEGCONV_PANEL_KMAJOR)
-        return fail(SEGCONV_E_CONTRACT, "tensor-core math needs K-major panels");
+    case SEGCONV_MATH_F16X3: {
+      if (sks->layout != SEGCONV_PANEL_UMMA)
+        return fail(SEGCONV_E_CONTRACT, "tensor-core math needs UMMA-layout panels");
+      if ((int)math != sks->math)
+        return fail(SEGCONV_E_CONTRACT, "panels were laid out for math %d, not %d", sks->math,
+                    (int)math);
       if (!tc_igemm_supported(pr, math))
         return fail(SEGCONV_E_UNSUPPORTED,
-                    "tensor-core path needs %s activations/panels and cin %% %d == 0",
-                    math == SEGCONV_MATH_BF16 ? "bf16" : "fp32", math == SEGCONV_MATH_BF16 ? 64 : 32);
+                    "tensor-core path needs %s activations, cin %% 8 == 0, taps in every parity "
+                    "class and a halo that fits shared memory",
+                    math == SEGCONV_MATH_BF16 ? "bf16" : "fp32");
       return cuda_status(launch_tc_igemm(pr, math, s), "transpose_conv_fused[tcgen05]");
     }
     default:

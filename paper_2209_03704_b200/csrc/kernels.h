@@ -36,6 +36,12 @@ cudaError_t launch_segregate(const void* k, int k_dtype, int kh, int kw, int cin
                              int cout_pad, int layout, const SegClasses& cls, void* panels,
                              int p_dtype, long long total, cudaStream_t s);
 
+cudaError_t launch_segregate_umma(const void* k, int k_dtype, int kw, int cin, int cout,
+                                  const SegClasses& cls, int NT, int KB, int nkb, int n_tiles,
+                                  int taps, bool split, void* panels, cudaStream_t s);
+int tc_n_tile(int math, int cout);
+int tc_k_block(int cin, int cout);
+
 // SIMT kernels (direct.cu).  Return cudaErrorNotSupported when no
 // instantiation covers the problem.
 cudaError_t launch_direct_generic(const FusedProblem& pr, bool exact, cudaStream_t s);

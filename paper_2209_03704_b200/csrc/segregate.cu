@@ -6,6 +6,10 @@
 // elements (gather; each source tap is read exactly once), with dtype
 // conversion and, for the tensor-core path, re-layout to K-major
 // (cout_pad, u, v, cin) rows so a panel row is one MMA B-operand row.
+#include <cuda_fp16.h>
+
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -86,6 +90,89 @@ cudaError_t launch_segregate(const void* k, int k_dtype, int kh, int kw, int cin
   SEG_CASE(__nv_bfloat16, SEGCONV_BF16)
 #undef SEG_CASE
   return cudaErrorInvalidValue;
+}
+
+// UMMA panel image for the tcgen05 kernel: blocks (n_tile, k_block, class,
+// tap), each [plane][k-chunk j][row n][8 elems] = the SMEM K-major no-swizzle
+// layout the MMA reads, so one cp.async.bulk stages one block.  SPLIT stores
+// w as fp16 hi + lo planes (w = hi + lo to ~22 bits); otherwise one bf16 plane.
+// One thread writes one 16-byte row chunk of every plane.
+template <typename TK, bool SPLIT>
+__global__ void segregate_umma_kernel(const TK* __restrict__ k, int kw, int cin, int cout,
+                                      SegClasses cls, int NT, int KB, int nkb, int taps,
+                                      uint16_t* __restrict__ out, long long rows_total) {
+  const int CH = KB / 8;
+  constexpr int PLANES = SPLIT ? 2 : 1;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < rows_total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int n = (int)(e % NT);
+    long long t1 = e / NT;
+    const int j = (int)(t1 % CH);
+    const long long blk = t1 / CH;
+    const int t = (int)(blk % taps);
+    const long long t2 = blk / taps;
+    const int kb = (int)(t2 % nkb);
+    const int nt = (int)(t2 / nkb);
+    int q = 0;
+#pragma unroll
+    for (int qq = 1; qq < 4; ++qq)
+      if (t >= cls.sub_offset[qq]) q = qq;
+    const int tl = t - (int)cls.sub_offset[q];
+    const int u = tl / cls.kw[q], v = tl % cls.kw[q];
+    const int f = nt * NT + n;
+    uint16_t hi[8], lo[8];
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      const int ci = kb * KB + j * 8 + x;
+      float w = 0.0f;
+      if (f < cout && ci < cin)
+        w = (float)to_acc(k[(((long long)(cls.u0[q] + 2 * u) * kw + (cls.v0[q] + 2 * v)) * cin + ci) *
+                                cout + f]);
+      if constexpr (SPLIT) {
+        const __half h = __float2half_rn(w);
+        hi[x] = __half_as_ushort(h);
+        lo[x] = __half_as_ushort(__float2half_rn(w - __half2float(h)));
+      } else {
+        hi[x] = __bfloat16_as_ushort(__float2bfloat16_rn(w));
+      }
+    }
+    const long long block_elems = (long long)PLANES * KB * NT;
+    uint16_t* dst = out + blk * block_elems + (long long)j * NT * 8 + (long long)n * 8;
+#pragma unroll
+    for (int x = 0; x < 8; ++x) dst[x] = hi[x];
+    if constexpr (SPLIT) {
+#pragma unroll
+      for (int x = 0; x < 8; ++x) dst[(long long)CH * NT * 8 + x] = lo[x];
+    }
+  }
+}
+
+cudaError_t launch_segregate_umma(const void* k, int k_dtype, int kw, int cin, int cout,
+                                  const SegClasses& cls, int NT, int KB, int nkb, int n_tiles,
+                                  int taps, bool split, void* panels, cudaStream_t s) {
+  const long long rows_total = (long long)n_tiles * nkb * taps * (KB / 8) * NT;
+  const int threads = 256;
+  const unsigned blocks = (unsigned)std::min<long long>((rows_total + threads - 1) / threads, 148LL * 32);
+#define SEGU(KT)                                                                               \
+  do {                                                                                         \
+    if (split)                                                                                 \
+      segregate_umma_kernel<KT, true><<<blocks, threads, 0, s>>>(                              \
+          (const KT*)k, kw, cin, cout, cls, NT, KB, nkb, taps, (uint16_t*)panels, rows_total); \
+    else                                                                                       \
+      segregate_umma_kernel<KT, false><<<blocks, threads, 0, s>>>(                             \
+          (const KT*)k, kw, cin, cout, cls, NT, KB, nkb, taps, (uint16_t*)panels, rows_total); \
+  } while (0)
+  if (k_dtype == SEGCONV_F32)
+    SEGU(float);
+  else if (k_dtype == SEGCONV_BF16)
+    SEGU(__nv_bfloat16);
+  else if (k_dtype == SEGCONV_F64)
+    SEGU(double);
+  else
+    return cudaErrorInvalidValue;
+#undef SEGU
+  note_launch();
+  return cudaGetLastError();
 }
 
 }  // namespace segconv_b200

@@ -65,7 +65,7 @@ def _check(status: int) -> None:
 _DT = {torch.float32: A.F32, torch.float64: A.F64, torch.bfloat16: A.BF16}
 _DT_INV = {v: k for k, v in _DT.items()}
 MATHS = {"auto": A.MATH_AUTO, "ffma": A.MATH_FFMA, "exact": A.MATH_EXACT, "bf16": A.MATH_BF16,
-         "tf32": A.MATH_TF32}
+         "tf32": A.MATH_TF32, "f16x3": A.MATH_F16X3}
 _MATH_INV = {v: k for k, v in MATHS.items()}
 _ACT = {None: A.EPI_NONE, "none": A.EPI_NONE, "relu": A.EPI_RELU, "tanh": A.EPI_TANH}
 
@@ -153,19 +153,20 @@ class SubKernelSet:
 
     ``panels`` is one device buffer holding the four parity sub-kernels (class
     r*2+c).  Layout "ref" keeps the reference's (u, v, cin, cout) order (SIMT
-    kernels); layout "kmajor" stores (cout_pad, u, v, cin) rows for the
-    tcgen05 kernels.
+    kernels); layout "umma" is the tcgen05 B-operand image (bf16, or fp32
+    weights split into fp16 hi + lo planes for math="f16x3").
     """
 
-    def __init__(self, desc: A.SubKernels, panels: torch.Tensor, math: int):
+    def __init__(self, desc: A.SubKernels, panels: torch.Tensor):
         self.desc = desc
         self.panels = panels
-        self.math = math
 
     source_kh = property(lambda s: s.desc.source_kh)
     source_kw = property(lambda s: s.desc.source_kw)
     p_orig_parity = property(lambda s: s.desc.p_orig_parity)
-    layout = property(lambda s: "ref" if s.desc.layout == A.PANEL_REF else "kmajor")
+    math = property(lambda s: s.desc.math)
+    layout = property(lambda s: {A.PANEL_REF: "ref", A.PANEL_KMAJOR: "kmajor",
+                                 A.PANEL_UMMA: "umma"}[s.desc.layout])
     dtype = property(lambda s: s.panels.dtype)
 
     def cin(self) -> int:
@@ -183,14 +184,29 @@ class SubKernelSet:
         return [self.offset(q >> 1, q & 1) for q in range(4)]
 
     def sub(self, r: int, c: int) -> torch.Tensor:
-        """View of class (r, c)'s panel in the reference (kh, kw, cin, cout) order."""
+        """Class (r, c)'s sub-kernel in the reference (kh, kw, cin, cout) order
+        (a view for "ref" panels; a decoded float32 copy for "umma" panels)."""
         d, q = self.desc, r * 2 + c
         kh, kw = d.sub_kh[q], d.sub_kw[q]
-        n = kh * kw * d.cin * d.cout_pad
-        flat = self.panels[d.sub_offset[q]: d.sub_offset[q] + n]
         if d.layout == A.PANEL_REF:
-            return flat.view(kh, kw, d.cin, d.cout)
-        return flat.view(d.cout_pad, kh, kw, d.cin).permute(1, 2, 3, 0)[..., : d.cout]
+            n = kh * kw * d.cin * d.cout_pad
+            return self.panels[d.sub_offset[q]: d.sub_offset[q] + n].view(kh, kw, d.cin, d.cout)
+        if d.layout == A.PANEL_KMAJOR:
+            n = kh * kw * d.cin * d.cout_pad
+            flat = self.panels[d.sub_offset[q]: d.sub_offset[q] + n]
+            return flat.view(d.cout_pad, kh, kw, d.cin).permute(1, 2, 3, 0)[..., : d.cout]
+        # UMMA image: blocks (n_tile, k_block, tap) x [plane][chunk][row][8]
+        NT, KB = d.n_tile, d.k_block
+        nkb = (d.cin + KB - 1) // KB
+        ntl = d.cout_pad // NT
+        taps = sum(d.sub_kh[i] * d.sub_kw[i] for i in range(4))
+        planes = 2 if d.dtype == A.F16_SPLIT else 1
+        blk = self.panels.view(ntl, nkb, taps, planes, KB // 8, NT, 8).float()
+        w = blk[:, :, :, 0] + (blk[:, :, :, 1] if planes == 2 else 0)
+        # -> (tap, kb, chunk, e, nt, n) -> (tap, cin_pad, cout_pad)
+        w = w.permute(2, 1, 3, 5, 0, 4).reshape(taps, nkb * KB, ntl * NT)
+        t0 = int(d.sub_offset[q])
+        return w[t0: t0 + kh * kw, : d.cin, : d.cout].reshape(kh, kw, d.cin, d.cout)
 
     @property
     def subs(self):
@@ -204,12 +220,17 @@ def select_math(x_dtype: torch.dtype, panel_dtype: torch.dtype, cin: int, cout: 
     return _MATH_INV[m]
 
 
+_PANEL_TORCH = {A.F32: torch.float32, A.F64: torch.float64, A.BF16: torch.bfloat16,
+                A.F16_SPLIT: torch.float16}
+
+
 def segregate(kernel: torch.Tensor, p_orig: int, *, math: str = "auto",
-              panel_dtype: Optional[torch.dtype] = None) -> SubKernelSet:
+              x_dtype: Optional[torch.dtype] = None) -> SubKernelSet:
     """reference segregation.hpp:61-89: split a (kh, kw, cin, cout) kernel into
     the four parity panels, on the device.  ``math`` selects the consumer
-    ("ffma"/"exact" -> reference-layout panels; "bf16"/"tf32" -> K-major
-    panels for the tensor-core kernel; "auto" decides from dtype and shape)."""
+    ("ffma"/"exact" -> reference-layout panels; "bf16"/"f16x3" -> tcgen05
+    panel image; "auto" decides from the activation dtype (default: the
+    kernel's dtype) and the shape)."""
     if kernel.dim() != 4:
         raise ShapeError(f"kernel must be (kh, kw, cin, cout), got {tuple(kernel.shape)}")
     kh, kw, cin, cout = (int(v) for v in kernel.shape)
@@ -217,24 +238,22 @@ def segregate(kernel: torch.Tensor, p_orig: int, *, math: str = "auto",
         raise ContractError("cannot segregate a spatially empty kernel")
     if p_orig < 0:
         raise ContractError("padding must be non-negative")
+    if math not in MATHS:
+        raise ContractError(f"unknown math {math!r}")
     dev = _device()
     k = kernel.to(dev).contiguous()
     kd = _dtype_code(k)
-    if math not in MATHS:
-        raise ContractError(f"unknown math {math!r}")
-    m = MATHS[math]
-    if m == A.MATH_AUTO:
-        m = MATHS[select_math(k.dtype, panel_dtype or k.dtype, cin, cout, kh, kw)]
-    if panel_dtype is None:
-        panel_dtype = {A.MATH_BF16: torch.bfloat16, A.MATH_TF32: torch.float32}.get(m, k.dtype)
-    layout = A.PANEL_KMAJOR if m in (A.MATH_BF16, A.MATH_TF32) else A.PANEL_REF
+    xd = _DT[x_dtype] if x_dtype is not None else kd
     desc = A.SubKernels()
-    _check(A.lib().segconv_subkernels_init(kh, kw, cin, cout, int(p_orig), _DT[panel_dtype],
-                                           layout, C.byref(desc)))
-    panels = torch.empty(max(1, desc.total_elems), dtype=panel_dtype, device=dev)
+    _check(A.lib().segconv_subkernels_for_math(kh, kw, cin, cout, int(p_orig), xd, MATHS[math],
+                                               C.byref(desc)))
+    if desc.layout == A.PANEL_REF and desc.dtype != kd:
+        k = k.to(_PANEL_TORCH[desc.dtype])
+        kd = desc.dtype
+    panels = torch.empty(max(1, desc.total_elems), dtype=_PANEL_TORCH[desc.dtype], device=dev)
     _check(A.lib().segconv_segregate(k.data_ptr(), kd, C.byref(desc), panels.data_ptr(),
                                      _stream()))
-    return SubKernelSet(desc, panels, m)
+    return SubKernelSet(desc, panels)
 
 
 # ------------------------------------------------------------ fused (hot)
@@ -278,7 +297,8 @@ def transpose_conv_fused(x: torch.Tensor, k: Union[SubKernelSet, torch.Tensor],
         if xb.shape[1] != xb.shape[2]:
             raise ContractError(f"transpose conv expects a square input, got "
                                 f"{xb.shape[1]}x{xb.shape[2]}")
-        sks = segregate(k, p, math=math or "auto")
+        sks = segregate(k, p, math=math or "auto", x_dtype=xb.dtype)
+        math = None
     else:
         if not isinstance(geom, TConvGeometry):
             raise ContractError("transpose_conv_fused(x, sks, geom) needs a TConvGeometry")
@@ -286,7 +306,7 @@ def transpose_conv_fused(x: torch.Tensor, k: Union[SubKernelSet, torch.Tensor],
         if xb.shape[1] != g.n_in or xb.shape[2] != g.n_in:
             raise ContractError(f"input is {xb.shape[1]}x{xb.shape[2]} but geometry was built "
                                 f"for {g.n_in}x{g.n_in}")
-    m = MATHS[math] if math is not None else sks.math
+    m = MATHS[math] if math is not None else A.MATH_AUTO
     host = not xb.is_cuda
     dev = _device()
     xd = xb.to(dev).contiguous()

@@ -64,7 +64,7 @@ def test_segregate_panels_match_reference():
     for key in keys:
         k = z[key + "_kernel"]
         p = int(key.split("_p")[1])
-        for math in ("ffma", "tf32"):
+        for math in ("ffma", "bf16", "f16x3"):
             sks = sc.segregate(cuda(k), p, math=math)
             for q in range(4):
                 got = sks.subs[q].float().cpu().numpy()
@@ -271,6 +271,7 @@ def test_conventional_path_matches_oracle_and_cudnn():
         # independent library cross-check: conv_transpose2d with the
         # kernel flipped and stride 2, padding n-1-p
         W = torch.from_numpy(k).permute(2, 3, 0, 1).flip(2, 3).contiguous().cuda()
+        torch.backends.cudnn.allow_tf32 = False  # fp32 reference, not TF32
         ref = torch.nn.functional.conv_transpose2d(cuda(x).permute(0, 3, 1, 2), W, stride=2,
                                                    padding=kk - 1 - p)
         approx_ok(got, ref.permute(0, 2, 3, 1).cpu().numpy(), 1e-4)

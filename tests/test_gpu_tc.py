@@ -1,0 +1,147 @@
+"""Parity of the tcgen05 implicit-GEMM path (math "bf16" and "f16x3") against the
+oracle, through the C ABI.
+
+* Integer-valued data in [-8, 8] is exact in bf16 and fp16 and every partial sum
+  stays below 2^24, so both tensor-core modes must be BIT-EXACT against the
+  reference on it -- this pins the halo-shift addressing, class offsets, the
+  interleaved epilogue and the trim, for every padding parity.
+* Real data: f16x3 <= 1e-5 scaled error vs the fp32 reference (north_star fp32
+  bar); bf16 <= 1e-2 (north_star tensor-core bar) vs the reference run on the
+  same bf16-rounded operands.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2209_03704_b200 import segconv as sc
+
+pytestmark = pytest.mark.gpu
+
+
+def cuda(a, dt=torch.float32):
+    return torch.as_tensor(np.ascontiguousarray(a)).to("cuda", dt)
+
+
+def scaled_err(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float((np.abs(a - b) / np.maximum(np.maximum(np.abs(a), np.abs(b)), 1.0)).max())
+
+
+def run_tc(x, k, p, math, act=None, bias=None, out_dtype=None):
+    dt = torch.bfloat16 if math == "bf16" else torch.float32
+    xt, kt = cuda(x, dt), cuda(k, dt)
+    g = sc.tconv_geometry(xt.shape[1], kt.shape[0], kt.shape[1], p)
+    sks = sc.segregate(kt, p, math=math)
+    assert sks.layout == "umma"
+    y = sc.transpose_conv_fused(xt, sks, g, activation=act,
+                                bias=None if bias is None else cuda(bias), out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    return y.float().cpu().numpy()
+
+
+INT_CASES = [  # (batch, n, cin, cout, k, p)
+    (2, 6, 16, 16, 3, 0), (1, 5, 16, 20, 4, 0), (3, 4, 32, 7, 3, 1), (1, 9, 16, 64, 5, 2),
+    (2, 7, 24, 33, 2, 3), (1, 3, 64, 48, 6, 4), (1, 12, 128, 16, 7, 0), (4, 2, 16, 3, 3, 0),
+    (1, 16, 72, 130, 4, 2), (2, 11, 8, 5, 3, 1), (1, 1, 16, 16, 2, 1), (5, 4, 1024, 32, 3, 0),
+    (3, 10, 64, 32, 3, 0), (2, 14, 32, 16, 5, 0), (1, 20, 16, 8, 3, 0),
+]
+
+
+@pytest.mark.parametrize("math", ["bf16", "f16x3"])
+@pytest.mark.parametrize("case", INT_CASES)
+def test_int_fuzz_bit_exact(math, case):
+    b, n, cin, cout, k, p = case
+    rng = np.random.default_rng(hash(case) % 2**32)
+    x = rng.integers(-8, 9, (b, n, n, cin)).astype(np.float32)
+    kk = rng.integers(-8, 9, (k, k, cin, cout)).astype(np.float32)
+    got = run_tc(x, kk, p, math, out_dtype=torch.float32)
+    want = oracle.tconv_fused(x, kk, p)
+    np.testing.assert_array_equal(got, want, err_msg=f"{math} {case}")
+
+
+@pytest.mark.parametrize("case", [(2, 9, 32, 40, 3, 0), (1, 13, 64, 17, 5, 2), (3, 8, 16, 64, 4, 1)])
+def test_f16x3_real_within_fp32_tolerance(case):
+    b, n, cin, cout, k, p = case
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-1, 1, (b, n, n, cin)).astype(np.float32)
+    kk = rng.normal(0, np.sqrt(2.0 / (cin * k * k)), (k, k, cin, cout)).astype(np.float32)
+    got = run_tc(x, kk, p, "f16x3")
+    assert scaled_err(got, oracle.tconv_fused(x, kk, p)) <= 1e-5
+
+
+@pytest.mark.parametrize("case", [(2, 9, 64, 40, 3, 0), (1, 16, 512, 64, 4, 0), (2, 5, 128, 3, 3, 2)])
+def test_bf16_real_within_tc_tolerance(case):
+    b, n, cin, cout, k, p = case
+    rng = np.random.default_rng(8)
+    x = oracle.bf16_round(rng.normal(0, 1, (b, n, n, cin)))
+    kk = oracle.bf16_round(rng.normal(0, 0.02, (k, k, cin, cout)))
+    want = oracle.tconv_fused(x, kk, p)
+    got32 = run_tc(x, kk, p, "bf16", out_dtype=torch.float32)
+    assert scaled_err(got32, want) <= 1e-5          # only summation order differs
+    got = run_tc(x, kk, p, "bf16")                  # bf16 output storage
+    assert scaled_err(got, want) <= 1e-2
+
+
+@pytest.mark.parametrize("act", ["relu", "tanh"])
+def test_tc_epilogue_bias_activation(act):
+    rng = np.random.default_rng(9)
+    x = rng.uniform(-1, 1, (2, 8, 8, 32)).astype(np.float32)
+    kk = rng.normal(0, 0.1, (3, 3, 32, 24)).astype(np.float32)
+    bias = rng.normal(0, 0.3, 24).astype(np.float32)
+    got = run_tc(x, kk, 0, "f16x3", act=act, bias=bias)
+    want = oracle.tconv_fused(x, kk, 0).astype(np.float64) + bias
+    want = np.maximum(want, 0) if act == "relu" else np.tanh(want)
+    assert scaled_err(got, want) <= 1e-5
+
+
+def test_auto_selects_tensor_path_for_wide_layers():
+    assert sc.select_math(torch.bfloat16, torch.bfloat16, 512, 256, 4, 4) == "bf16"
+    assert sc.select_math(torch.float32, torch.float32, 64, 32, 3, 3) == "f16x3"
+    assert sc.select_math(torch.float32, torch.float32, 1, 1, 3, 3) == "ffma"
+    k = torch.zeros(3, 3, 64, 32, device="cuda")
+    assert sc.segregate(k, 0).layout == "umma"
+
+
+# --------------------------------------------------------- BASELINE configs
+def test_config_c2_full_f16x3():
+    rng = np.random.default_rng(2)
+    x = rng.uniform(-1, 1, (16, 64, 64, 64)).astype(np.float32)
+    k = (rng.standard_normal((3, 3, 64, 32)) * np.sqrt(2.0 / 576)).astype(np.float32)
+    got = run_tc(x, k, 0, "f16x3")
+    assert got.shape == (16, 125, 125, 32)
+    assert scaled_err(got, oracle.tconv_fused(x, k, 0)) <= 1e-5
+
+
+def test_config_c3_bf16_sampled():
+    rng = np.random.default_rng(3)
+    x = oracle.bf16_round(rng.standard_normal((128, 16, 16, 512), dtype=np.float32))
+    k = oracle.bf16_round(rng.standard_normal((4, 4, 512, 256), dtype=np.float32) * 0.02)
+    got = run_tc(x, k, 0, "bf16")
+    assert got.shape == (128, 28, 28, 256)
+    idx = [0, 77, 127]
+    assert scaled_err(got[idx], oracle.tconv_fused(x[idx], k, 0)) <= 1e-2
+
+
+def test_config_c5_stack_bf16():
+    """Four-layer generator (BASELINE C5) on a batch slice vs the oracle chain with
+    bf16 rounding between layers, ReLU after a,b,c and tanh after d."""
+    from paper_2209_03704_b200 import stack as st
+    specs = st.c5_layers()
+    rng = np.random.default_rng(5)
+    ks = [oracle.bf16_round(rng.standard_normal((s.k, s.k, s.cin, s.cout), dtype=np.float32) * 0.02)
+          for s in specs]
+    b = 6
+    x = oracle.bf16_round(rng.standard_normal((b, 4, 4, 1024), dtype=np.float32))
+    stack = st.GeneratorStack(specs, [cuda(k) for k in ks], b)
+    y = stack.forward(cuda(x, torch.bfloat16)).float().cpu().numpy()
+    stack.capture()
+    y2 = stack.forward(cuda(x, torch.bfloat16)).float().cpu().numpy()
+    np.testing.assert_array_equal(y, y2)  # graph replay == eager
+    h = x
+    for s, k in zip(specs, ks):
+        h = oracle.tconv_fused(h, k, s.p)
+        h = oracle.bf16_round(np.maximum(h, 0) if s.activation == "relu" else np.tanh(h))
+    assert y.shape == (b, 19, 19, 3)
+    assert scaled_err(y, h) <= 1e-2
