@@ -66,6 +66,7 @@ SIGNATURES = {
     "segconv_last_error": (C.c_char_p, []),
     "segconv_version": (C.c_char_p, []),
     "segconv_launch_count": (C.c_uint64, []),
+    "segconv_debug_trace": (_sz, [_vp, _sz]),
 }
 
 _lib = None

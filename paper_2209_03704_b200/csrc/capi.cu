@@ -3,6 +3,7 @@
 // Host-side validation mirrors the reference's exceptions before anything is
 // launched; dispatch picks the kernel family for the requested math.  There
 // is no CPU fallback: a missing device or a failed launch is SEGCONV_E_CUDA.
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -66,6 +67,14 @@ extern "C" {
 const char* segconv_last_error(void) { return g_err.c_str(); }
 const char* segconv_version(void) { return "segconv_b200 0.1 (sm_100a)"; }
 uint64_t segconv_launch_count(void) { return g_launches.load(); }
+
+size_t segconv_debug_trace(void* host_out, size_t bytes) {
+  const unsigned long long* t = tc_trace_ptr();
+  if (!t || !host_out) return 0;
+  const size_t n = std::min(bytes, (size_t)4 * 8 * 64 * sizeof(unsigned long long));
+  if (cudaMemcpy(host_out, t, n, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  return n;
+}
 
 // reference geometry.hpp:29-53
 segconv_status segconv_tconv_geometry(int n_in, int kh, int kw, int p_orig, segconv_geometry* g) {

@@ -44,6 +44,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -84,6 +85,7 @@ struct Params {
   int tap_shift[MAX_TAPS];
   int first_tap[4];
   int rows[4], cols[4];
+  unsigned long long* trace;  // optional event trace (SEGCONV_TC_TRACE), CTAs 0..3
 };
 
 // ------------------------------------------------------------ PTX helpers
@@ -224,6 +226,15 @@ __device__ __forceinline__ void split8(const float4& a, const float4& b, uint32_
   }
 }
 
+// Debug trace: trace[(cta * 8 + event) * 64 + local_unit] = globaltimer (ns).
+// events: 0 A-TMA issued, 1 converted, 2 MMA start, 3 MMA issued, 4 epi start, 5 epi done
+__device__ __forceinline__ void trace_ev(const Params& p, int ev, int local) {
+  if (p.trace == nullptr || blockIdx.x >= 4 || local >= 64) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  p.trace[(blockIdx.x * 8 + ev) * 64 + local] = t;
+}
+
 // Work unit u -> (m-group, n-tile); n-tile major so a CTA's units share weights.
 __device__ __forceinline__ void unit_coords(const Params& p, long long u, long long& mg, int& nt) {
   nt = (int)(u / p.m_groups);
@@ -242,6 +253,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   extern __shared__ __align__(1024) uint8_t smem[];
   const int SA = p.stages_a, SB = p.stages_b;
+  const int NB = p.b_resident ? 1 : SB;  // B barriers: one for the resident set
   uint8_t* a_base = smem;
   uint8_t* b_base = smem + (size_t)SA * p.a_stage_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(b_base + (size_t)SB * p.b_stage_bytes);
@@ -249,8 +261,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* a_full = a_land + SA;   // stage ready for the MMA
   uint64_t* a_empty = a_full + SA;  // MMA done with the stage
   uint64_t* b_full = a_empty + SA;
-  uint64_t* b_empty = b_full + SB;
-  uint64_t* acc_full = b_empty + SB;
+  uint64_t* b_empty = b_full + NB;
+  uint64_t* acc_full = b_empty + NB;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
@@ -263,7 +275,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&a_full[s], a_full_count);
       mbar_init(&a_empty[s], 1);
     }
-    for (int s = 0; s < SB; ++s) {
+    for (int s = 0; s < NB; ++s) {
       mbar_init(&b_full[s], 1);
       mbar_init(&b_empty[s], 1);
     }
@@ -316,6 +328,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int pc = 0; pc < p.pieces; ++pc)
               tma_load_3d(sbase + (uint32_t)j * col_bytes + (uint32_t)(pc * p.piece_rows) * row_bytes,
                           &tmap, 0, m0 + pc * p.piece_rows, kb * CH + j, bar);
+          if (kb == 0) trace_ev(p, 0, (int)((u - blockIdx.x) / gridDim.x));
           if (++st == SA) {
             st = 0;
             ph ^= 1;
@@ -362,6 +375,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               named_bar(1, 128);
             }
             fence_proxy_async();  // generic-proxy SMEM writes -> visible to the tensor core
+            if (kb == 0 && pt == 0) trace_ev(p, 1, (int)((u - blockIdx.x) / gridDim.x));
             mbar_arrive(&a_full[st]);
             if (++st == SA) {
               st = 0;
@@ -469,6 +483,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (long long u = blockIdx.x; u < p.total_units; u += gridDim.x) {
         mbar_wait(&acc_empty[acc], pacc ^ 1);
         tc_fence_after();
+        trace_ev(p, 2, (int)((u - blockIdx.x) / gridDim.x));
         const uint32_t d_base = tmem_base + (uint32_t)(acc * ACC_COLS);
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(&a_full[sa], pa);
@@ -523,6 +538,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         mma_commit(&acc_full[acc]);
+        trace_ev(p, 3, (int)((u - blockIdx.x) / gridDim.x));
         if (++acc == ACC_BUFS) {
           acc = 0;
           pacc ^= 1;
@@ -541,6 +557,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       unit_coords(p, u, mg, nt);
       mbar_wait(&acc_full[acc], pacc);
       tc_fence_after();
+      if (threadIdx.x == 0) trace_ev(p, 4, (int)((u - blockIdx.x) / gridDim.x));
 #pragma unroll 1
       for (int g = 0; g < G; ++g) {
         const long long m = mg * MPG + g * BM + warp * 32 + lane;
@@ -594,6 +611,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       tc_fence_before();
+      if (threadIdx.x == 0) trace_ev(p, 5, (int)((u - blockIdx.x) / gridDim.x));
       mbar_arrive(&acc_empty[acc]);
       if (++acc == ACC_BUFS) {
         acc = 0;
@@ -616,10 +634,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 // ------------------------------------------------------------ host plan
 // Tile shape decisions shared by segregate (panel image) and the launcher.
+// An SS-mode MMA (M=128, K=16) reads 4 KB of A plus 32*N bytes of B from
+// SMEM at ~128 B/cycle, against N/2 cycles of tensor work, so N >= 128 is
+// needed to be compute-bound (measured: scripts/mma_bench.cu).  Wide layers
+// therefore use 128-feature tiles (4 classes x 128 = all 512 TMEM columns).
 int tc_n_tile(int math, int cout) {
   (void)math;
   const int c16 = (cout + 15) / 16 * 16;
-  return c16 >= 64 ? 64 : c16 >= 32 ? 32 : 16;
+  return c16 >= 128 ? 128 : c16 >= 64 ? 64 : c16 >= 32 ? 32 : 16;
 }
 // Narrow-output layers (cout <= 16) have wide images, hence tall halos: use
 // 32-channel blocks so two A stages fit.
@@ -741,7 +763,8 @@ static Plan make_plan_g(const FusedProblem& pr, int math, int G) {
   p.a_stage_bytes = planes * CH * p.S_pad * 16;  // == CH * S_pad * 32 for the fp32 landing
   p.a_stage_bytes = (p.a_stage_bytes + 1023) / 1024 * 1024;
   p.b_stage_bytes = planes * p.kb * NT * 2;
-  const int bar_bytes = 512;
+  // mbarriers: 3 per A stage, 2 per streamed B stage (<= 12), 4 accumulator, TMEM slot
+  const int bar_bytes = (3 * 4 + 2 * 12 + 4) * 8 + 16;
   const int budget = tc::SMEM_LIMIT - bar_bytes;
   const int b_all = p.nkb * p.taps * p.b_stage_bytes;
   // weights resident when there is one n-tile and they fit beside 2 A stages
@@ -804,6 +827,21 @@ bool tc_igemm_supported(const FusedProblem& pr, int math) {
   return make_plan(pr, math).ok;
 }
 
+// SEGCONV_TC_TRACE=1: a device buffer of 4 CTAs x 8 events x 64 units of
+// globaltimer stamps, readable through segconv_debug_trace() (diagnostics only).
+static unsigned long long* g_trace = nullptr;
+static unsigned long long* tc_trace_buffer() {
+  static bool init = false;
+  if (!init) {
+    init = true;
+    const char* e = getenv("SEGCONV_TC_TRACE");
+    if (e && e[0] == '1' && cudaMalloc(&g_trace, 4 * 8 * 64 * sizeof(unsigned long long)) == cudaSuccess)
+      cudaMemset(g_trace, 0, 4 * 8 * 64 * sizeof(unsigned long long));
+  }
+  return g_trace;
+}
+const unsigned long long* tc_trace_ptr() { return g_trace; }
+
 template <int MODE, int NT, int G>
 static cudaError_t launch_t(const Plan& pl, cudaStream_t s) {
   auto kern = tc::tc_halo_kernel<MODE, NT, G>;
@@ -822,7 +860,9 @@ static cudaError_t launch_t(const Plan& pl, cudaStream_t s) {
       sms = 148;
   }
   const long long grid = std::min<long long>(pl.p.total_units, sms);
-  kern<<<(unsigned)grid, tc::NUM_THREADS, pl.smem, s>>>(pl.p, pl.tmap);
+  tc::Params prm = pl.p;
+  prm.trace = tc_trace_buffer();
+  kern<<<(unsigned)grid, tc::NUM_THREADS, pl.smem, s>>>(prm, pl.tmap);
   note_launch();
   return cudaGetLastError();
 }
@@ -840,10 +880,12 @@ cudaError_t launch_tc_igemm(const FusedProblem& pr, int math, cudaStream_t s) {
   TCL_G(tc::MODE_BF16, 32)
   TCL(tc::MODE_BF16, 64, 1)
   TCL(tc::MODE_BF16, 64, 2)
+  TCL(tc::MODE_BF16, 128, 1)
   TCL_G(tc::MODE_F16X3, 16)
   TCL_G(tc::MODE_F16X3, 32)
   TCL(tc::MODE_F16X3, 64, 1)
   TCL(tc::MODE_F16X3, 64, 2)
+  TCL(tc::MODE_F16X3, 128, 1)
 #undef TCL_G
 #undef TCL
   return cudaErrorNotSupported;

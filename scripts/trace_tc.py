@@ -1,0 +1,38 @@
+"""Per-unit pipeline timeline of the tcgen05 kernel (diagnostics).
+Run with SEGCONV_TC_TRACE=1:  python scripts/trace_tc.py C2"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2209_03704_b200 import _capi as A  # noqa: E402
+from paper_2209_03704_b200 import segconv as sc  # noqa: E402
+
+cfg = bench.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C2"]
+prob = bench.Layer(cfg, 0, torch, sc, torch.device("cuda", 0), 1)
+for _ in range(3):
+    prob.step()
+torch.cuda.synchronize()
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+prob.step()
+b.record()
+torch.cuda.synchronize()
+print("kernel ms", a.elapsed_time(b))
+buf = np.zeros(4 * 8 * 64, dtype=np.uint64)
+n = A.lib().segconv_debug_trace(buf.ctypes.data_as(C.c_void_p), buf.nbytes)
+tr = buf.reshape(4, 8, 64).astype(np.int64)
+names = ["A-tma", "conv", "mma0", "mma1", "epi0", "epi1"]
+t0 = tr[tr > 0].min()
+for cta in range(2):
+    print(f"CTA {cta}")
+    for u in range(64):
+        row = tr[cta, :6, u]
+        if not row.any():
+            break
+        print(f"  unit {u}: " + "  ".join(f"{nm}={(v - t0) / 1000:7.2f}us" if v else f"{nm}=   -   "
+                                          for nm, v in zip(names, row)))
