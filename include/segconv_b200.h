@@ -78,9 +78,12 @@ typedef enum {
   SEGCONV_PANEL_REF = 0,    /* per class (u, v, cin, cout): the reference sub-kernel layout  */
                             /* (segregation.hpp:61-89); used by the SIMT kernels             */
   SEGCONV_PANEL_KMAJOR = 1, /* per class (cout, u, v, cin): K-major, rows padded to cout_pad */
-  SEGCONV_PANEL_UMMA = 2    /* tcgen05 B-operand image: blocks (n_tile, k_block, class, tap),  */
+  SEGCONV_PANEL_UMMA = 2,   /* tcgen05 B-operand image: blocks (n_tile, k_block, class, tap),  */
                             /* each [plane][k-chunk of 8][n_tile rows][8] -- the exact SMEM    */
                             /* K-major no-swizzle layout, so one bulk copy stages one block     */
+  SEGCONV_PANEL_UMMA_FOLD = 3 /* class-folded tcgen05 A-operand image for cout <= 32:         */
+                            /* [plane][k_block][k-chunk][shift * 4*cp + class*cp + f][8] over  */
+                            /* the union window of shifts (zero where a class has no tap)      */
 } segconv_panel_layout;
 
 /* == segconv::TConvGeometry (reference geometry.hpp:18-27). */

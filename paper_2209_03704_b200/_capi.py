@@ -21,7 +21,7 @@ MATH_AUTO, MATH_FFMA, MATH_EXACT, MATH_BF16, MATH_TF32, MATH_F16X3 = range(6)
 # epilogue flags
 EPI_NONE, EPI_BIAS, EPI_RELU, EPI_TANH = 0, 1, 2, 4
 # panel layouts
-PANEL_REF, PANEL_KMAJOR, PANEL_UMMA = 0, 1, 2
+PANEL_REF, PANEL_KMAJOR, PANEL_UMMA, PANEL_UMMA_FOLD = 0, 1, 2, 3
 
 
 class SegconvLibraryError(RuntimeError):

@@ -121,12 +121,16 @@ segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_
     return fail(SEGCONV_E_SHAPE, "bad kernel dims %dx%dx%dx%d", kh, kw, cin, cout);
   if (!valid_dtype(panel_dtype) && panel_dtype != SEGCONV_F16_SPLIT)
     return fail(SEGCONV_E_CONTRACT, "unknown panel dtype %d", (int)panel_dtype);
-  if (layout != SEGCONV_PANEL_REF && layout != SEGCONV_PANEL_KMAJOR && layout != SEGCONV_PANEL_UMMA)
+  if (layout != SEGCONV_PANEL_REF && layout != SEGCONV_PANEL_KMAJOR && layout != SEGCONV_PANEL_UMMA &&
+      layout != SEGCONV_PANEL_UMMA_FOLD)
     return fail(SEGCONV_E_CONTRACT, "unknown panel layout %d", (int)layout);
-  if (layout == SEGCONV_PANEL_UMMA && panel_dtype != SEGCONV_BF16 && panel_dtype != SEGCONV_F16_SPLIT)
+  const bool umma = layout == SEGCONV_PANEL_UMMA || layout == SEGCONV_PANEL_UMMA_FOLD;
+  if (umma && panel_dtype != SEGCONV_BF16 && panel_dtype != SEGCONV_F16_SPLIT)
     return fail(SEGCONV_E_CONTRACT, "UMMA panels are bf16 or split-fp16");
-  if (layout != SEGCONV_PANEL_UMMA && panel_dtype == SEGCONV_F16_SPLIT)
-    return fail(SEGCONV_E_CONTRACT, "split-fp16 panels need the UMMA layout");
+  if (!umma && panel_dtype == SEGCONV_F16_SPLIT)
+    return fail(SEGCONV_E_CONTRACT, "split-fp16 panels need a UMMA layout");
+  if (layout == SEGCONV_PANEL_UMMA_FOLD && cout > 32)
+    return fail(SEGCONV_E_CONTRACT, "class-folded panels need cout <= 32");
   segconv_subkernels s{};
   s.source_kh = kh;
   s.source_kw = kw;
@@ -136,9 +140,8 @@ segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_
   s.cout = cout;
   s.dtype = panel_dtype;
   s.layout = layout;
-  s.math = layout == SEGCONV_PANEL_UMMA
-               ? (panel_dtype == SEGCONV_F16_SPLIT ? SEGCONV_MATH_F16X3 : SEGCONV_MATH_BF16)
-               : SEGCONV_MATH_FFMA;
+  s.math = umma ? (panel_dtype == SEGCONV_F16_SPLIT ? SEGCONV_MATH_F16X3 : SEGCONV_MATH_BF16)
+                : SEGCONV_MATH_FFMA;
   // K-major panels pad the MMA N dimension to a multiple of 16 rows.
   s.cout_pad = layout == SEGCONV_PANEL_KMAJOR ? (cout + 15) / 16 * 16 : cout;
   int64_t off = 0;
@@ -156,6 +159,15 @@ segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_
     taps += s.sub_kh[q] * s.sub_kw[q];
   }
   s.total_elems = off;
+  if (layout == SEGCONV_PANEL_UMMA_FOLD) {
+    s.n_tile = fold_cp(cout);
+    s.k_block = fold_kb(s.math, cin);
+    const int nkb = (cin + s.k_block - 1) / s.k_block;
+    const int planes = panel_dtype == SEGCONV_F16_SPLIT ? 2 : 1;
+    s.cout_pad = s.n_tile;
+    for (int q = 0; q < 4; ++q) s.sub_offset[q] = 0;
+    s.total_elems = (int64_t)planes * nkb * (s.k_block / 8) * fold_rows(kh, kw, p_orig, cout) * 8;
+  }
   if (layout == SEGCONV_PANEL_UMMA) {
     s.n_tile = tc_n_tile(s.math, cout);
     s.k_block = tc_k_block(cin, cout);
@@ -195,10 +207,13 @@ segconv_status segconv_subkernels_for_math(int kh, int kw, int cin, int cout, in
       return st;
     }
     case SEGCONV_MATH_BF16:
-      return segconv_subkernels_init(kh, kw, cin, cout, p_orig, SEGCONV_BF16, SEGCONV_PANEL_UMMA, out);
-    case SEGCONV_MATH_F16X3:
-      return segconv_subkernels_init(kh, kw, cin, cout, p_orig, SEGCONV_F16_SPLIT,
-                                     SEGCONV_PANEL_UMMA, out);
+    case SEGCONV_MATH_F16X3: {
+      // narrow layers (cout <= 32, p_fused == 0): class-folded kernel
+      const bool fold = tc_fold_fits(math, kh, kw, p_orig, cin, cout);
+      return segconv_subkernels_init(
+          kh, kw, cin, cout, p_orig, math == SEGCONV_MATH_BF16 ? SEGCONV_BF16 : SEGCONV_F16_SPLIT,
+          fold ? SEGCONV_PANEL_UMMA_FOLD : SEGCONV_PANEL_UMMA, out);
+    }
     default:
       return fail(SEGCONV_E_UNSUPPORTED, "math mode %d has no kernels in this build", (int)math);
   }
@@ -217,6 +232,18 @@ segconv_status segconv_segregate(const void* d_kernel, segconv_dtype kernel_dtyp
     cls.sub_offset[q] = sks->sub_offset[q];
   }
   if (sks->total_elems == 0) return SEGCONV_OK;
+  if (sks->layout == SEGCONV_PANEL_UMMA_FOLD) {
+    cls.off_r[0] = cls.off_r[1] = 0;
+    for (int q = 0; q < 4; ++q) {
+      cls.off_r[q] = sks->off_r[q];
+      cls.off_c[q] = sks->off_c[q];
+    }
+    return cuda_status(launch_segregate_fold(d_kernel, kernel_dtype, sks->source_kh,
+                                             sks->source_kw, sks->cin, sks->cout, sks->p_orig, cls,
+                                             sks->dtype == SEGCONV_F16_SPLIT, d_panels,
+                                             (cudaStream_t)stream),
+                       "segregate[fold]");
+  }
   if (sks->layout == SEGCONV_PANEL_UMMA) {
     int taps = 0;
     for (int q = 0; q < 4; ++q) taps += sks->sub_kh[q] * sks->sub_kw[q];
@@ -327,11 +354,18 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
     }
     case SEGCONV_MATH_BF16:
     case SEGCONV_MATH_F16X3: {
-      if (sks->layout != SEGCONV_PANEL_UMMA)
+      if (sks->layout != SEGCONV_PANEL_UMMA && sks->layout != SEGCONV_PANEL_UMMA_FOLD)
         return fail(SEGCONV_E_CONTRACT, "tensor-core math needs UMMA-layout panels");
       if ((int)math != sks->math)
         return fail(SEGCONV_E_CONTRACT, "panels were laid out for math %d, not %d", sks->math,
                     (int)math);
+      if (sks->layout == SEGCONV_PANEL_UMMA_FOLD) {
+        if (!tc_fold_supported(pr, math))
+          return fail(SEGCONV_E_UNSUPPORTED,
+                      "class-folded tensor-core path: needs p_fused == 0, cin a multiple of the "
+                      "channel block and a halo that fits shared memory");
+        return cuda_status(launch_tc_fold(pr, math, s), "transpose_conv_fused[tcgen05 fold]");
+      }
       if (!tc_igemm_supported(pr, math))
         return fail(SEGCONV_E_UNSUPPORTED,
                     "tensor-core path needs %s activations, cin %% 8 == 0, taps in every parity "

@@ -40,6 +40,18 @@ cudaError_t launch_segregate_umma(const void* k, int k_dtype, int kw, int cin, i
                                   const SegClasses& cls, int NT, int KB, int nkb, int n_tiles,
                                   int taps, bool split, void* panels, cudaStream_t s);
 int tc_n_tile(int math, int cout);
+// class-folded tcgen05 kernel for narrow layers (tc_fold.cu)
+cudaError_t launch_tc_fold(const FusedProblem& pr, int math, cudaStream_t s);
+bool tc_fold_supported(const FusedProblem& pr, int math);
+bool tc_fold_available(int math, int cin, int cout);
+bool tc_fold_fits(int math, int kh, int kw, int p, int cin, int cout);
+void fold_window(int kh, int kw, int p, int* ur, int* uc);
+int fold_cp(int cout);
+int fold_kb(int math, int cin);
+int fold_rows(int kh, int kw, int p, int cout);
+cudaError_t launch_segregate_fold(const void* k, int k_dtype, int kh, int kw, int cin, int cout,
+                                  int p, const SegClasses& cls, bool split, void* panels,
+                                  cudaStream_t s);
 int tc_k_block(int cin, int cout);
 
 // SIMT kernels (direct.cu).  Return cudaErrorNotSupported when no

@@ -175,4 +175,88 @@ cudaError_t launch_segregate_umma(const void* k, int k_dtype, int kw, int cin, i
   return cudaGetLastError();
 }
 
+// Class-folded A-operand image (tc_fold.cu): for k-block kb, k-chunk j, row
+// = shift * 4*CP + q*CP + f: W = sub_q[dy - off_r][dx - off_c][ci][f] when
+// that is a tap of class q, else 0.  Trailing (128 - 4*CP) rows stay zero.
+template <typename TK, bool SPLIT>
+__global__ void segregate_fold_kernel(const TK* __restrict__ k, int kw, int cin, int cout,
+                                      SegClasses cls, int CP, int KB, int uc, int rows_per_col,
+                                      int nshift_rows, uint16_t* __restrict__ out,
+                                      long long chunks_total, long long plane_elems) {
+  const int CH = KB / 8;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < chunks_total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(e % rows_per_col);
+    const long long col = e / rows_per_col;  // kb * CH + j
+    const int j = (int)(col % CH), kb = (int)(col / CH);
+    uint16_t hi[8], lo[8];
+    const int R = 4 * CP;
+    const int s = row / R, q = (row % R) / CP, f = (row % R) % CP;
+    const int dy = s / uc, dx = s % uc;
+    const int u = dy - cls.off_r[q], v = dx - cls.off_c[q];
+    const bool tap = row < nshift_rows && f < cout && u >= 0 && u < cls.kh[q] && v >= 0 &&
+                     v < cls.kw[q];
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      const int ci = kb * KB + j * 8 + x;
+      float w = 0.0f;
+      if (tap && ci < cin)
+        w = (float)to_acc(
+            k[(((long long)(cls.u0[q] + 2 * u) * kw + (cls.v0[q] + 2 * v)) * cin + ci) * cout + f]);
+      if constexpr (SPLIT) {
+        const __half h = __float2half_rn(w);
+        hi[x] = __half_as_ushort(h);
+        lo[x] = __half_as_ushort(__float2half_rn(w - __half2float(h)));
+      } else {
+        hi[x] = __bfloat16_as_ushort(__float2bfloat16_rn(w));
+      }
+    }
+    uint16_t* dst = out + e * 8;
+#pragma unroll
+    for (int x = 0; x < 8; ++x) dst[x] = hi[x];
+    if constexpr (SPLIT) {
+#pragma unroll
+      for (int x = 0; x < 8; ++x) dst[plane_elems + x] = lo[x];
+    }
+  }
+}
+
+cudaError_t launch_segregate_fold(const void* k, int k_dtype, int kh, int kw, int cin, int cout,
+                                  int p, const SegClasses& cls, bool split, void* panels,
+                                  cudaStream_t s) {
+  int ur, uc;
+  fold_window(kh, kw, p, &ur, &uc);
+  const int CP = fold_cp(cout);
+  const int KB = fold_kb(split ? SEGCONV_MATH_F16X3 : SEGCONV_MATH_BF16, cin);
+  const int nkb = (cin + KB - 1) / KB;
+  const int rows = fold_rows(kh, kw, p, cout);
+  const long long chunks_total = (long long)nkb * (KB / 8) * rows;
+  const long long plane_elems = chunks_total * 8;
+  const unsigned blocks = (unsigned)std::min<long long>((chunks_total + 255) / 256, 148LL * 32);
+#define SEGF(KT)                                                                               \
+  do {                                                                                         \
+    if (split)                                                                                 \
+      segregate_fold_kernel<KT, true><<<blocks, 256, 0, s>>>((const KT*)k, kw, cin, cout, cls,  \
+                                                             CP, KB, uc, rows, ur * uc * 4 * CP, \
+                                                             (uint16_t*)panels, chunks_total,  \
+                                                             plane_elems);                     \
+    else                                                                                       \
+      segregate_fold_kernel<KT, false><<<blocks, 256, 0, s>>>((const KT*)k, kw, cin, cout, cls, \
+                                                              CP, KB, uc, rows, ur * uc * 4 * CP, \
+                                                              (uint16_t*)panels, chunks_total, \
+                                                              plane_elems);                    \
+  } while (0)
+  if (k_dtype == SEGCONV_F32)
+    SEGF(float);
+  else if (k_dtype == SEGCONV_BF16)
+    SEGF(__nv_bfloat16);
+  else if (k_dtype == SEGCONV_F64)
+    SEGF(double);
+  else
+    return cudaErrorInvalidValue;
+#undef SEGF
+  note_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace segconv_b200

@@ -166,7 +166,7 @@ class SubKernelSet:
     p_orig_parity = property(lambda s: s.desc.p_orig_parity)
     math = property(lambda s: s.desc.math)
     layout = property(lambda s: {A.PANEL_REF: "ref", A.PANEL_KMAJOR: "kmajor",
-                                 A.PANEL_UMMA: "umma"}[s.desc.layout])
+                                 A.PANEL_UMMA: "umma", A.PANEL_UMMA_FOLD: "fold"}[s.desc.layout])
     dtype = property(lambda s: s.panels.dtype)
 
     def cin(self) -> int:
@@ -195,12 +195,29 @@ class SubKernelSet:
             n = kh * kw * d.cin * d.cout_pad
             flat = self.panels[d.sub_offset[q]: d.sub_offset[q] + n]
             return flat.view(d.cout_pad, kh, kw, d.cin).permute(1, 2, 3, 0)[..., : d.cout]
+        planes = 2 if d.dtype == A.F16_SPLIT else 1
+        if d.layout == A.PANEL_UMMA_FOLD:
+            # [plane][k_block][chunk][shift*4*cp + q*cp + f][8] over the union window
+            CP, KB = d.n_tile, d.k_block
+            nkb = (d.cin + KB - 1) // KB
+            uc = max(d.off_c[i] + d.sub_kw[i] for i in range(4))
+            ur = max(d.off_r[i] + d.sub_kh[i] for i in range(4))
+            rows = ur * uc * 4 * CP + (128 - 4 * CP)
+            blk = self.panels.view(planes, nkb, KB // 8, rows, 8).float()
+            w = blk[0] + (blk[1] if planes == 2 else 0)          # (nkb, CH, rows, 8)
+            w = w.permute(2, 0, 1, 3).reshape(rows, nkb * KB)     # (rows, cin_pad)
+            out = torch.zeros(kh, kw, d.cin, d.cout, device=w.device)
+            for u in range(kh):
+                for v in range(kw):
+                    s_ = (d.off_r[q] + u) * uc + (d.off_c[q] + v)
+                    r0 = s_ * 4 * CP + q * CP
+                    out[u, v] = w[r0: r0 + d.cout, : d.cin].t()
+            return out
         # UMMA image: blocks (n_tile, k_block, tap) x [plane][chunk][row][8]
         NT, KB = d.n_tile, d.k_block
         nkb = (d.cin + KB - 1) // KB
         ntl = d.cout_pad // NT
         taps = sum(d.sub_kh[i] * d.sub_kw[i] for i in range(4))
-        planes = 2 if d.dtype == A.F16_SPLIT else 1
         blk = self.panels.view(ntl, nkb, taps, planes, KB // 8, NT, 8).float()
         w = blk[:, :, :, 0] + (blk[:, :, :, 1] if planes == 2 else 0)
         # -> (tap, kb, chunk, e, nt, n) -> (tap, cin_pad, cout_pad)

@@ -34,7 +34,7 @@ def run_tc(x, k, p, math, act=None, bias=None, out_dtype=None):
     xt, kt = cuda(x, dt), cuda(k, dt)
     g = sc.tconv_geometry(xt.shape[1], kt.shape[0], kt.shape[1], p)
     sks = sc.segregate(kt, p, math=math)
-    assert sks.layout == "umma"
+    assert sks.layout in ("umma", "fold")
     y = sc.transpose_conv_fused(xt, sks, g, activation=act,
                                 bias=None if bias is None else cuda(bias), out_dtype=out_dtype)
     torch.cuda.synchronize()
@@ -46,6 +46,9 @@ INT_CASES = [  # (batch, n, cin, cout, k, p)
     (2, 7, 24, 33, 2, 3), (1, 3, 64, 48, 6, 4), (1, 12, 128, 16, 7, 0), (4, 2, 16, 3, 3, 0),
     (1, 16, 72, 130, 4, 2), (2, 11, 8, 5, 3, 1), (1, 1, 16, 16, 2, 1), (5, 4, 1024, 32, 3, 0),
     (3, 10, 64, 32, 3, 0), (2, 14, 32, 16, 5, 0), (1, 20, 16, 8, 3, 0),
+    # wide images: the class-folded kernel's 2-D block staging (n >= 64)
+    (1, 70, 16, 3, 5, 0), (1, 100, 16, 12, 3, 0), (2, 66, 64, 3, 5, 0), (1, 80, 16, 4, 4, 1),
+    (1, 64, 48, 32, 3, 0), (2, 65, 32, 1, 7, 1),
 ]
 
 
@@ -101,7 +104,7 @@ def test_auto_selects_tensor_path_for_wide_layers():
     assert sc.select_math(torch.float32, torch.float32, 64, 32, 3, 3) == "f16x3"
     assert sc.select_math(torch.float32, torch.float32, 1, 1, 3, 3) == "ffma"
     k = torch.zeros(3, 3, 64, 32, device="cuda")
-    assert sc.segregate(k, 0).layout == "umma"
+    assert sc.segregate(k, 0).layout in ("umma", "fold")
 
 
 # --------------------------------------------------------- BASELINE configs
@@ -112,6 +115,16 @@ def test_config_c2_full_f16x3():
     got = run_tc(x, k, 0, "f16x3")
     assert got.shape == (16, 125, 125, 32)
     assert scaled_err(got, oracle.tconv_fused(x, k, 0)) <= 1e-5
+
+
+def test_config_c4_full_f16x3_tanh():
+    rng = np.random.default_rng(4)
+    x = rng.uniform(-1, 1, (32, 256, 256, 64)).astype(np.float32)
+    k = (rng.standard_normal((5, 5, 64, 3)) * 0.02).astype(np.float32)
+    got = run_tc(x, k, 0, "f16x3", act="tanh")
+    assert got.shape == (32, 507, 507, 3)
+    idx = [0, 31]
+    assert scaled_err(got[idx], np.tanh(oracle.tconv_fused(x[idx], k, 0))) <= 1e-5
 
 
 def test_config_c3_bf16_sampled():
