@@ -64,6 +64,7 @@ cudaError_t launch_tc_igemm(const FusedProblem& pr, int math, cudaStream_t s);
 bool tc_igemm_supported(const FusedProblem& pr, int math);
 bool tc_igemm_available(int math, int cin, int cout);
 const unsigned long long* tc_trace_ptr();
+unsigned long long* tc_trace_buffer();
 
 // Conventional path (conventional.cu).
 cudaError_t launch_upsample_pad(const void* x, int dtype, int batch, int n, int cin, int p,

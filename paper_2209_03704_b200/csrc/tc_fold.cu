@@ -30,8 +30,9 @@
 // epilogue maps lanes to (class, feature) so each store instruction writes
 // one output pixel's features contiguously, with bias / ReLU / tanh fused.
 //
-// Warp roles (352 threads): 0-3 epilogue, 4-7 fp16 hi/lo converters (split
-// math), 8 MMA issuer, 9 weight loader + TMEM owner, 10 halo TMA issuer.
+// Warp roles (480 threads): 0-7 epilogue (warps w and w+4 share TMEM lane
+// quadrant w % 4 and split its 32-column blocks), 8-11 fp16 hi/lo converters
+// (split math), 12 MMA issuer, 13 weight loader + TMEM owner, 14 halo TMA.
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
@@ -46,9 +47,10 @@ namespace tcf {
 using namespace tc;
 
 constexpr int MODE_BF16 = 0, MODE_F16X3 = 1;
-constexpr int NUM_THREADS = 352;
+constexpr int NUM_THREADS = 480;  // 15 warps
 constexpr int SMEM_LIMIT = 227 * 1024;
 constexpr int MAX_SHIFTS = 16;
+constexpr int EPI_TILE_BYTES = 8 * 32 * 36 * 4;  // one transpose tile per epilogue warp
 
 struct Params {
   const uint8_t* panels;
@@ -71,7 +73,18 @@ struct Params {
   int shifts;
   int shift_off[MAX_SHIFTS];       // dy * pitch + dx
   int rows[4], cols[4];
+  unsigned long long* trace;       // optional event trace (SEGCONV_TC_TRACE)
+  int debug_nostore;               // diagnostics (SEGCONV_TC_DEBUG bits): 1 skip global
+                                   // stores, 2 skip the fp16 split, 4 skip epilogue body
 };
+
+__device__ __forceinline__ void trace_ev(const Params& p, int ev, long long u) {
+  const int local = (int)((u - blockIdx.x) / gridDim.x);
+  if (p.trace == nullptr || blockIdx.x >= 160 || local >= 64) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  p.trace[(blockIdx.x * 8 + ev) * 64 + local] = t;
+}
 
 __device__ __forceinline__ void unit_origin(const Params& p, long long u, long long& m0, int& b,
                                             int& i0, int& j0) {
@@ -88,6 +101,122 @@ __device__ __forceinline__ void unit_origin(const Params& p, long long u, long l
   }
 }
 
+// Position of the current D column (anchor) while walking a 32-column chunk.
+struct Walk {
+  int b, i, j, jj, rowlen, tc, imax;
+};
+
+template <typename YT>
+__device__ __forceinline__ YT cvt_out(float v) {
+  return from_f<YT>(v);
+}
+
+// Epilogue of one 32 x 32 block of D (32 rows = (class, feature) pairs of
+// this warp's TMEM lane quadrant, 32 consecutive anchor columns).  The block
+// is transposed through a padded SMEM tile (row stride 36 floats: scalar
+// writes and 16-byte reads are both conflict-free) so each thread then owns
+// ONE anchor and writes every class pixel it touches with 16-byte stores.
+template <typename YT, int ACT>
+__device__ __forceinline__ void fold_epilogue_block(const Params& p, const float (&v)[32],
+                                                    float* tile, const Walk& w, int warp,
+                                                    int lane) {
+  // write: thread = row, column k -> tile[k][row]
+#pragma unroll
+  for (int k = 0; k < 32; ++k) tile[k * 36 + lane] = v[k];
+  __syncwarp();
+  // this thread's anchor: column lane of the block
+  int jj = w.jj + lane, i = w.i, b = w.b;
+  if (jj >= w.rowlen) {  // rows shorter than the block: divide once
+    const int di = jj / w.rowlen;
+    jj -= di * w.rowlen;
+    i += di;
+    if (i >= w.imax) {
+      b += i / w.imax;
+      i -= (i / w.imax) * w.imax;
+    }
+  }
+  const int j = w.j - w.jj + jj;
+  const bool anchor_ok = jj < w.tc && b < p.batch;
+  YT* __restrict__ y = reinterpret_cast<YT*>(p.y);
+  const int CP = p.CP;
+  const int q0 = (warp * 32) / CP;                 // first class in this quadrant
+  const int nq = min(4 - q0, max(1, 32 / CP));     // classes held by these 32 rows
+  auto fin = [&](float x, int f) {
+    if (p.epi & SEGCONV_EPI_BIAS) x += __ldg(p.bias + f);
+    if (ACT == 1) x = fmaxf(x, 0.0f);
+    if (ACT == 2) x = tanhf(x);
+    return x;
+  };
+  constexpr int LPP = 32 * (int)sizeof(YT) / 16;  // lanes per 32-feature pixel row
+  if (CP == 32 && p.cout == 32) {
+    // warp-cooperative stores: LPP lanes write one anchor's 32 features as
+    // consecutive 16-byte pieces, so every instruction writes whole lines
+    const int q = q0, r = q >> 1, c = q & 1;
+    const bool ok = anchor_ok && i < p.rows[q] && j < p.cols[q];
+    const long long base =
+        ok ? (((long long)b * p.out_h + (2 * i + r)) * p.out_w + (2 * j + c)) * 32 : -1;
+    constexpr int PPR = 32 / LPP;  // anchors per round
+    const int sub = lane % LPP, slot = lane / LPP;
+    float4 a[32 / PPR][LPP == 8 ? 1 : 2];
+#pragma unroll
+    for (int t = 0; t < 32 / PPR; ++t) {  // all tile reads first (ILP)
+      const float* src = tile + (t * PPR + slot) * 36;
+      if (LPP == 8) {
+        a[t][0] = *reinterpret_cast<const float4*>(src + sub * 4);
+      } else {
+        a[t][0] = *reinterpret_cast<const float4*>(src + sub * 8);
+        a[t][LPP == 8 ? 0 : 1] = *reinterpret_cast<const float4*>(src + sub * 8 + 4);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 32 / PPR; ++t) {
+      const long long bb = __shfl_sync(0xffffffffu, base, t * PPR + slot);
+      if (bb < 0 || (p.debug_nostore & 1)) continue;
+      if (LPP == 8) {
+        const int f = sub * 4;
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(y) + bb + f) =
+            make_float4(fin(a[t][0].x, f), fin(a[t][0].y, f + 1), fin(a[t][0].z, f + 2),
+                        fin(a[t][0].w, f + 3));
+      } else {
+        const int f = sub * 8;
+        const float4 x0 = a[t][0], x1 = a[t][LPP == 8 ? 0 : 1];
+        __nv_bfloat162 h[4] = {__floats2bfloat162_rn(fin(x0.x, f), fin(x0.y, f + 1)),
+                               __floats2bfloat162_rn(fin(x0.z, f + 2), fin(x0.w, f + 3)),
+                               __floats2bfloat162_rn(fin(x1.x, f + 4), fin(x1.y, f + 5)),
+                               __floats2bfloat162_rn(fin(x1.z, f + 6), fin(x1.w, f + 7))};
+        *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(y) + bb + f) =
+            *reinterpret_cast<const uint4*>(h);
+      }
+    }
+    __syncwarp();
+    return;
+  }
+  const float* row = tile + lane * 36;  // this anchor's 32 (class, feature) values
+  for (int qq = 0; qq < nq; ++qq) {
+    const int q = q0 + qq, r = q >> 1, c = q & 1;
+    if (!(anchor_ok && i < p.rows[q] && j < p.cols[q])) continue;
+    const float* src = row + (q * CP - warp * 32);
+    YT* dst = y + (((long long)b * p.out_h + (2 * i + r)) * p.out_w + (2 * j + c)) * p.cout;
+    if (!(p.debug_nostore & 1))
+      for (int f = 0; f < p.cout; ++f) dst[f] = from_f<YT>(fin(src[f], f));
+  }
+  __syncwarp();
+}
+
+// Advance a walk by d staged columns (d >= 0).
+__device__ __forceinline__ void walk_advance(Walk& w, int d) {
+  w.jj += d;
+  w.j += d;
+  while (w.jj >= w.rowlen) {
+    w.jj -= w.rowlen;
+    w.j -= w.rowlen;
+    if (++w.i == w.imax) {
+      w.i = 0;
+      ++w.b;
+    }
+  }
+}
+
 template <int MODE, int N>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_fold_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmap) {
@@ -98,7 +227,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int SA = p.stages_a;
   uint8_t* w_base = smem;                         // resident weights
   uint8_t* a_base = smem + p.w_bytes;             // halo stages
-  uint64_t* bars = reinterpret_cast<uint64_t*>(a_base + (size_t)SA * p.a_stage_bytes);
+  uint8_t* epi_base = a_base + (size_t)SA * p.a_stage_bytes;  // 4 x 32 x 36 floats
+  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_base + EPI_TILE_BYTES);
   uint64_t* a_land = bars;
   uint64_t* a_full = a_land + SA;
   uint64_t* a_empty = a_full + SA;
@@ -108,7 +238,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + ACC_BUFS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 8 && lane == 0) {
+  if (warp == 12 && lane == 0) {
     for (int s = 0; s < SA; ++s) {
       mbar_init(&a_land[s], 1);
       mbar_init(&a_full[s], MODE == MODE_F16X3 ? 128u : 1u);
@@ -117,13 +247,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     mbar_init(w_full, 1);
     for (int s = 0; s < ACC_BUFS; ++s) {
       mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], 128);
+      mbar_init(&acc_empty[s], 256);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 10 && lane == 0)
+  if (warp == 14 && lane == 0)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-  if (warp == 9) {
+  if (warp == 13) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
                      smem_u32(tmem_slot))
                  : "memory");
@@ -140,7 +270,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t WCOL = (uint32_t)p.w_rows * 16;             // weight k-chunk column
   const uint32_t W_PLANE = (uint32_t)p.nkb * CH * WCOL;
 
-  if (warp == 10) {
+  if (warp == 14) {
     // ================= halo TMA issuer
     if (lane == 0) {
       int st = 0;
@@ -169,6 +299,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             &tmap, 0, (int)m0 + pc * p.piece_rows, kb * CH + j, bar);
             }
           }
+          if (kb == 0) trace_ev(p, 0, u);
           if (++st == SA) {
             st = 0;
             ph ^= 1;
@@ -176,46 +307,55 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 8 && warp < 12) {
     // ================= fp16 hi/lo split in place (f16x3)
+    // All reads of a stage's fp32 rows happen before the single barrier,
+    // then every thread writes its rows' hi / lo halves (in-place hazard).
     if constexpr (MODE == MODE_F16X3) {
-      const int pt = threadIdx.x - 128;
+      const int pt = threadIdx.x - 256;
       int st = 0;
       uint32_t ph = 0;
       const int rows_staged = p.block_mode ? p.P * p.TRH : p.pieces * p.piece_rows;
-      constexpr int RPT = 8;  // rows per thread: one pass covers all <= 1024 staged rows
+      // RPC row slots of 128 per chunk column; RPT_MAX = 4 chunks x RPC slots
+      constexpr int RPC = 3, RPT_MAX = 4 * RPC;  // <= 384 rows x 4 chunks per stage
       for (long long u = blockIdx.x; u < p.units; u += gridDim.x) {
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(&a_land[st], ph);
           const uint32_t sbase = smem_u32(a_base + (size_t)st * p.a_stage_bytes);
-          for (int j = 0; j < CH; ++j) {
-            const uint32_t cbase = sbase + (uint32_t)j * 2 * COL;
-            // all reads of the column precede all writes (in-place hazard)
-            for (int r0 = 0; r0 < rows_staged; r0 += 128 * RPT) {
-              float4 v[RPT][2];
+          if (p.debug_nostore & 2) {
+            mbar_arrive(&a_full[st]);
+            if (++st == SA) {
+              st = 0;
+              ph ^= 1;
+            }
+            continue;
+          }
+          // RPT rows of each k-chunk column per thread: reads of the whole
+          // stage first, one barrier, then the in-place hi/lo writes
+          float4 v[RPT_MAX][2];
 #pragma unroll
-              for (int k = 0; k < RPT; ++k) {
-                const int s = r0 + pt + k * 128;
-                if (s < rows_staged) {
-                  ld_shared_v4f(cbase + (uint32_t)s * 32, v[k][0]);
-                  ld_shared_v4f(cbase + (uint32_t)s * 32 + 16, v[k][1]);
-                }
-              }
-              named_bar(1, 128);
+          for (int k = 0; k < RPT_MAX; ++k) {
+            const int j = k / RPC, s = pt + (k % RPC) * 128;
+            if (j < CH && s < rows_staged) {
+              const uint32_t src = sbase + (uint32_t)j * 2 * COL + (uint32_t)s * 32;
+              ld_shared_v4f(src, v[k][0]);
+              ld_shared_v4f(src + 16, v[k][1]);
+            }
+          }
+          named_bar(1, 128);
 #pragma unroll
-              for (int k = 0; k < RPT; ++k) {
-                const int s = r0 + pt + k * 128;
-                if (s < rows_staged) {
-                  uint32_t hi[4], lo[4];
-                  split8(v[k][0], v[k][1], hi, lo);
-                  st_shared_v4(cbase + (uint32_t)s * 16, hi[0], hi[1], hi[2], hi[3]);
-                  st_shared_v4(cbase + COL + (uint32_t)s * 16, lo[0], lo[1], lo[2], lo[3]);
-                }
-              }
-              named_bar(1, 128);
+          for (int k = 0; k < RPT_MAX; ++k) {
+            const int j = k / RPC, s = pt + (k % RPC) * 128;
+            if (j < CH && s < rows_staged) {
+              uint32_t hi[4], lo[4];
+              split8x2(v[k][0], v[k][1], hi, lo);
+              const uint32_t dst = sbase + (uint32_t)j * 2 * COL + (uint32_t)s * 16;
+              st_shared_v4(dst, hi[0], hi[1], hi[2], hi[3]);
+              st_shared_v4(dst + COL, lo[0], lo[1], lo[2], lo[3]);
             }
           }
           fence_proxy_async();
+          if (kb == 0 && threadIdx.x == 256) trace_ev(p, 1, u);
           mbar_arrive(&a_full[st]);
           if (++st == SA) {
             st = 0;
@@ -224,7 +364,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == 13) {
     // ================= resident weights: one bulk-copy pass
     if (lane == 0) {
       mbar_arrive_expect_tx(w_full, (uint32_t)p.w_bytes);
@@ -232,7 +372,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (uint32_t off = 0; off < (uint32_t)p.w_bytes; off += CHUNK)
         bulk_g2s(w_base + off, p.panels + off, min(CHUNK, (uint32_t)p.w_bytes - off), w_full);
     }
-  } else if (warp == 8) {
+  } else if (warp == 12) {
     // ================= MMA issuer
     if (lane == 0) {
       mbar_wait(w_full, 0);
@@ -243,6 +383,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (long long u = blockIdx.x; u < p.units; u += gridDim.x) {
         mbar_wait(&acc_empty[acc], pacc ^ 1);
         tc_fence_after();
+        trace_ev(p, 2, u);
         const uint32_t d = tmem_base + (uint32_t)(acc * N);
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(&a_full[sa], pa);
@@ -276,6 +417,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         mma_commit(&acc_full[acc]);
+        trace_ev(p, 3, u);
         if (++acc == ACC_BUFS) {
           acc = 0;
           pacc ^= 1;
@@ -286,12 +428,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ================= epilogue: lanes = (class, feature), columns = anchors
     int acc = 0;
     uint32_t pacc = 0;
-    const int row = warp * 32 + lane;
+    const int quad = warp & 3, half = warp >> 2;  // TMEM lane quadrant, column-block parity
+    const int row = quad * 32 + lane;
     const int q = row / p.CP, f = row - (row / p.CP) * p.CP;
     const bool row_ok = row < p.R && f < p.cout;
-    const bool warp_live = warp * 32 < p.R;
+    const bool warp_live = quad * 32 < p.R;
     const int r = q >> 1, c = q & 1;
     const int qrows = row_ok ? p.rows[q] : 0, qcols = row_ok ? p.cols[q] : 0;
+    const float bias_f = (row_ok && (p.epi & SEGCONV_EPI_BIAS)) ? __ldg(p.bias + f) : 0.0f;
     const long long img = (long long)p.n * p.n;
     for (long long u = blockIdx.x; u < p.units; u += gridDim.x) {
       long long m0;
@@ -299,51 +443,52 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       unit_origin(p, u, m0, b0, i0, j0);
       mbar_wait(&acc_full[acc], pacc);
       tc_fence_after();
-      if (warp_live) {
-        const uint32_t tbase = tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(acc * N);
+      if (threadIdx.x == 0) trace_ev(p, 4, u);
+      if (warp_live) {  // quadrant holds (class, feature) rows
+        const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * N);
+        const int act = (p.epi & SEGCONV_EPI_RELU) ? 1 : (p.epi & SEGCONV_EPI_TANH) ? 2 : 0;
+        const int sel = (p.y_dtype == SEGCONV_BF16 ? 3 : 0) + act;
+        float* tile = reinterpret_cast<float*>(epi_base) + warp * 32 * 36;
+        // anchor of the unit's first column, decoded once; blocks walk from it
+        Walk w;
+        if (!p.block_mode) {
+          w.b = (int)(m0 / img);
+          const int rem = (int)(m0 - (long long)w.b * img);
+          w.i = rem / p.n;
+          w.j = rem - w.i * p.n;
+          w.jj = w.j;
+          w.rowlen = p.n;
+          w.tc = 1 << 30;
+          w.imax = p.n;
+        } else {
+          w.b = b0;
+          w.i = i0;
+          w.j = j0;
+          w.jj = 0;
+          w.rowlen = p.P;
+          w.tc = p.TC;
+          w.imax = 1 << 30;
+        }
+        walk_advance(w, 32 * half);
 #pragma unroll 1
-        for (int c0 = 0; c0 < N; c0 += 32) {
+        for (int c0 = 32 * half; c0 < N; c0 += 64) {
           float v[32];
           tmem_ld32(tbase + (uint32_t)c0, v);
-          if (!row_ok) continue;
-          // anchor of column c0, then step along the row
-          int b, i, j, rowlen;
-          if (!p.block_mode) {
-            const long long m = m0 + c0;
-            b = (int)(m / img);
-            const int rem = (int)(m - (long long)b * img);
-            i = rem / p.n;
-            j = rem - i * p.n;
-            rowlen = p.n;
-          } else {
-            b = b0;
-            i = i0 + c0 / p.P;
-            j = j0 + c0 % p.P;
-            rowlen = p.P;
-          }
-          int jj = p.block_mode ? c0 % p.P : j;  // position within the staged row
-#pragma unroll
-          for (int k = 0; k < 32; ++k) {
-            const bool in_tile = !p.block_mode || jj < p.TC;
-            if (in_tile && b < p.batch && i < qrows && j < qcols) {
-              const long long pix =
-                  ((long long)b * p.out_h + (2 * i + r)) * p.out_w + (2 * j + c);
-              store_out(p.y, pix * p.cout + f, epilogue_apply(v[k], p.epi, p.bias, f), p.y_dtype);
-            }
-            ++j;
-            ++jj;
-            if (jj == rowlen) {  // wrap to the next staged row
-              jj = 0;
-              j -= rowlen;
-              if (++i == (p.block_mode ? 1 << 30 : p.n)) {
-                i = 0;
-                ++b;
-              }
+          if (!(p.debug_nostore & 4)) {
+            switch (sel) {
+              case 0: fold_epilogue_block<float, 0>(p, v, tile, w, quad, lane); break;
+              case 1: fold_epilogue_block<float, 1>(p, v, tile, w, quad, lane); break;
+              case 2: fold_epilogue_block<float, 2>(p, v, tile, w, quad, lane); break;
+              case 3: fold_epilogue_block<__nv_bfloat16, 0>(p, v, tile, w, quad, lane); break;
+              case 4: fold_epilogue_block<__nv_bfloat16, 1>(p, v, tile, w, quad, lane); break;
+              default: fold_epilogue_block<__nv_bfloat16, 2>(p, v, tile, w, quad, lane); break;
             }
           }
+          walk_advance(w, 64);
         }
       }
       tc_fence_before();
+      if (threadIdx.x == 0) trace_ev(p, 5, u);
       mbar_arrive(&acc_empty[acc]);
       if (++acc == ACC_BUFS) {
         acc = 0;
@@ -354,7 +499,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == 13) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
                  : "memory");
@@ -493,7 +638,9 @@ static FoldPlan make_fold_plan_n(const FusedProblem& pr, int math, int block_n) 
   }
   p.shifts = ur * uc;
   if (p.shifts > tcf::MAX_SHIFTS) return pl;
-  if (split && (p.block_mode ? p.P * p.TRH : p.S_pad) > 1024) return pl;  // converter: one pass
+  if (pr.y_dtype != SEGCONV_F32 && pr.y_dtype != SEGCONV_BF16) return pl;
+  if (split && ((p.block_mode ? p.P * p.TRH : p.pieces * p.piece_rows) > 3 * 128 || p.kb > 32))
+    return pl;  // converter: <= 3 rows of 128 per k-chunk column, <= 4 chunks
   for (int dy = 0; dy < ur; ++dy)
     for (int dx = 0; dx < uc; ++dx) p.shift_off[dy * uc + dx] = dy * pitch + dx;
   p.w_rows = p.shifts * p.R + (128 - p.R);
@@ -501,10 +648,11 @@ static FoldPlan make_fold_plan_n(const FusedProblem& pr, int math, int block_n) 
   p.w_bytes = (p.w_bytes + 1023) / 1024 * 1024;
   p.a_stage_bytes = (planes * CH * p.S_pad * 16 + 1023) / 1024 * 1024;
   const int bar_bytes = (3 * 4 + 1 + 8) * 8 + 16;
-  const int left = tcf::SMEM_LIMIT - bar_bytes - p.w_bytes;
+  const int left = tcf::SMEM_LIMIT - bar_bytes - p.w_bytes - tcf::EPI_TILE_BYTES;
   p.stages_a = std::min(4, left / p.a_stage_bytes);
   if (p.stages_a < 2) return pl;
-  pl.smem = (size_t)p.w_bytes + (size_t)p.stages_a * p.a_stage_bytes + bar_bytes;
+  pl.smem = (size_t)p.w_bytes + (size_t)p.stages_a * p.a_stage_bytes + tcf::EPI_TILE_BYTES +
+            bar_bytes;
   // halo tensor map
   EncodeTiledFn2 fn = encode_fn2();
   if (!fn) return pl;
@@ -567,7 +715,11 @@ static cudaError_t launch_fold_t(const FoldPlan& pl, cudaStream_t s) {
       sms = 148;
   }
   const long long grid = std::min<long long>(pl.p.units, sms);
-  kern<<<(unsigned)grid, tcf::NUM_THREADS, pl.smem, s>>>(pl.p, pl.tmap);
+  tcf::Params prm = pl.p;
+  prm.trace = tc_trace_buffer();
+  static const int dbg = getenv("SEGCONV_TC_DEBUG") ? atoi(getenv("SEGCONV_TC_DEBUG")) : 0;
+  prm.debug_nostore = dbg;
+  kern<<<(unsigned)grid, tcf::NUM_THREADS, pl.smem, s>>>(prm, pl.tmap);
   note_launch();
   return cudaGetLastError();
 }

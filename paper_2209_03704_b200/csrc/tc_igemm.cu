@@ -91,7 +91,7 @@ struct Params {
 // Debug trace: trace[(cta * 8 + event) * 64 + local_unit] = globaltimer (ns).
 // events: 0 A-TMA issued, 1 converted, 2 MMA start, 3 MMA issued, 4 epi start, 5 epi done
 __device__ __forceinline__ void trace_ev(const Params& p, int ev, int local) {
-  if (p.trace == nullptr || blockIdx.x >= 4 || local >= 64) return;
+  if (p.trace == nullptr || blockIdx.x >= 160 || local >= 64) return;
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   p.trace[(blockIdx.x * 8 + ev) * 64 + local] = t;
@@ -689,16 +689,16 @@ bool tc_igemm_supported(const FusedProblem& pr, int math) {
   return make_plan(pr, math).ok;
 }
 
-// SEGCONV_TC_TRACE=1: a device buffer of 4 CTAs x 8 events x 64 units of
+// SEGCONV_TC_TRACE=1: a device buffer of 160 CTAs x 8 events x 64 units of
 // globaltimer stamps, readable through segconv_debug_trace() (diagnostics only).
 static unsigned long long* g_trace = nullptr;
-static unsigned long long* tc_trace_buffer() {
+unsigned long long* tc_trace_buffer() {
   static bool init = false;
   if (!init) {
     init = true;
     const char* e = getenv("SEGCONV_TC_TRACE");
-    if (e && e[0] == '1' && cudaMalloc(&g_trace, 4 * 8 * 64 * sizeof(unsigned long long)) == cudaSuccess)
-      cudaMemset(g_trace, 0, 4 * 8 * 64 * sizeof(unsigned long long));
+    if (e && e[0] == '1' && cudaMalloc(&g_trace, 160 * 8 * 64 * sizeof(unsigned long long)) == cudaSuccess)
+      cudaMemset(g_trace, 0, 160 * 8 * 64 * sizeof(unsigned long long));
   }
   return g_trace;
 }

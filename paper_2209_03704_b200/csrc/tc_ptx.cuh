@@ -114,6 +114,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[32]) {
   uint32_t r[16];
   asm volatile(
@@ -141,6 +151,25 @@ __device__ __forceinline__ void ld_shared_v4f(uint32_t addr, float4& v) {
 
 __host__ __device__ constexpr int pow2_cols(int c) {
   return c <= 32 ? 32 : c <= 64 ? 64 : c <= 128 ? 128 : c <= 256 ? 256 : 512;
+}
+
+// Packed split: cvt.rn.f16x2.f32 for hi, residual in fp32, cvt again for lo.
+__device__ __forceinline__ uint32_t cvt_f16x2(float lo_elem, float hi_elem) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi_elem), "f"(lo_elem));
+  return r;
+}
+__device__ __forceinline__ void split8x2(const float4& a, const float4& b, uint32_t (&hi)[4],
+                                         uint32_t (&lo)[4]) {
+  const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t h = cvt_f16x2(v[2 * k], v[2 * k + 1]);
+    const __half2 hh = *reinterpret_cast<const __half2*>(&h);
+    const float2 hf = __half22float2(hh);
+    hi[k] = h;
+    lo[k] = cvt_f16x2(v[2 * k] - hf.x, v[2 * k + 1] - hf.y);
+  }
 }
 
 // Split 8 fp32 values into fp16 hi / lo halves packed as 4 x b32 each.

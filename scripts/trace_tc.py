@@ -23,9 +23,9 @@ prob.step()
 b.record()
 torch.cuda.synchronize()
 print("kernel ms", a.elapsed_time(b))
-buf = np.zeros(4 * 8 * 64, dtype=np.uint64)
+buf = np.zeros(160 * 8 * 64, dtype=np.uint64)
 n = A.lib().segconv_debug_trace(buf.ctypes.data_as(C.c_void_p), buf.nbytes)
-tr = buf.reshape(4, 8, 64).astype(np.int64)
+tr = buf.reshape(160, 8, 64).astype(np.int64)
 names = ["A-tma", "conv", "mma0", "mma1", "epi0", "epi1"]
 t0 = tr[tr > 0].min()
 for cta in range(2):
@@ -36,3 +36,19 @@ for cta in range(2):
             break
         print(f"  unit {u}: " + "  ".join(f"{nm}={(v - t0) / 1000:7.2f}us" if v else f"{nm}=   -   "
                                           for nm, v in zip(names, row)))
+
+# all-CTA summary: first A-TMA and last epilogue-done per CTA
+starts, ends, nunits = [], [], []
+for cta in range(160):
+    row = tr[cta]
+    if not row.any():
+        continue
+    starts.append(row[row > 0].min())
+    ends.append(row[5][row[5] > 0].max() if (row[5] > 0).any() else 0)
+    nunits.append(int((row[5] > 0).sum()))
+starts, ends = np.array(starts), np.array(ends)
+print(f"CTAs {len(starts)}: start spread {(starts.max()-starts.min())/1000:.2f}us, "
+      f"end min {(ends.min()-t0)/1000:.2f}us max {(ends.max()-t0)/1000:.2f}us, units/CTA {min(nunits)}-{max(nunits)}")
+slow = np.argsort(ends)[-3:]
+for c in slow:
+    print("  slowest CTA", c, f"end {(ends[c]-t0)/1000:.2f}us start {(starts[c]-t0)/1000:.2f}us units {nunits[c]}")
