@@ -1,0 +1,103 @@
+"""Batch-sharded multi-GPU driver logic on CPU with gloo (world size 2).
+
+`ShardedStack` (paper_2209_03704_b200/stack.py) owns: the batch partition,
+the one-time weight broadcast from rank 0 and the output all-gather.  The
+per-rank compute (`GeneratorStack`, sm_100a kernels) is replaced here by a
+CPU stand-in built on the oracle -- test infrastructure only -- so the
+collective logic is exercised without a GPU.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+from paper_2209_03704_b200 import stack as st
+
+
+def test_shard_range_partitions_batch():
+    for batch in (1, 2, 7, 16, 1024, 1000):
+        for world in (1, 2, 3, 4, 8):
+            spans = [st.shard_range(batch, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == batch
+            for (a, b), (c, d) in zip(spans, spans[1:]):
+                assert b == c and a <= b
+            sizes = [b - a for a, b in spans]
+            assert max(sizes) - min(sizes) <= 1
+
+
+class _CpuStack:
+    """Stand-in for GeneratorStack: the same chain on the oracle, fp32."""
+
+    def __init__(self, specs, kernels, batch, **kw):
+        self.specs = list(specs)
+        self.kernels = [k.detach().cpu().numpy().astype(np.float32) for k in kernels]
+        self.batch = batch
+        self.out = None
+
+    def forward(self, x):
+        h = x.numpy()
+        for s, k in zip(self.specs, self.kernels):
+            h = oracle.tconv_fused(h, k, s.p)
+            h = np.maximum(h, 0) if s.activation == "relu" else np.tanh(h)
+        self.out = torch.from_numpy(np.ascontiguousarray(h))
+        return self.out
+
+
+SPECS = [st.LayerSpec(8, 6, 4, 3, 0, "relu"), st.LayerSpec(6, 3, 5, 3, 0, "tanh")]
+
+
+def _worker(rank, world, port, batch, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        st.GeneratorStack = _CpuStack
+        rng = np.random.default_rng(100 + rank)  # ranks start with DIFFERENT weights
+        ks = [torch.from_numpy(rng.normal(0, 0.2, (s.k, s.k, s.cin, s.cout)).astype(np.float32))
+              for s in SPECS]
+        sh = st.ShardedStack(SPECS, ks, batch)
+        xr = np.random.default_rng(7).normal(0, 1, (batch, 4, 4, 8)).astype(np.float32)
+        sh.forward(torch.from_numpy(xr[sh.lo:sh.hi]))
+        full = sh.gather()
+        w0 = [k.numpy() for k in sh.kernels]
+        q.put((rank, sh.lo, sh.hi, full.numpy(), w0))
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+@pytest.mark.parametrize("batch", [5, 8])
+def test_sharded_stack_gloo_world2(batch):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, batch, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, lo0, hi0, full0, w0), (r1, lo1, hi1, full1, w1) = res
+    assert (lo0, hi1) == (0, batch) and hi0 == lo1
+    for a, b in zip(w0, w1):  # weights replicated from rank 0
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(full0, full1)  # every rank holds the full batch
+    # equals the single-process chain on rank 0's weights
+    xr = np.random.default_rng(7).normal(0, 1, (batch, 4, 4, 8)).astype(np.float32)
+    h = xr
+    for s, k in zip(SPECS, w0):
+        h = oracle.tconv_fused(h, k, s.p)
+        h = np.maximum(h, 0) if s.activation == "relu" else np.tanh(h)
+    np.testing.assert_allclose(full0, h, rtol=0, atol=1e-6)
