@@ -71,7 +71,7 @@ uint64_t segconv_launch_count(void) { return g_launches.load(); }
 size_t segconv_debug_trace(void* host_out, size_t bytes) {
   const unsigned long long* t = tc_trace_ptr();
   if (!t || !host_out) return 0;
-  const size_t n = std::min(bytes, (size_t)160 * 8 * 64 * sizeof(unsigned long long));
+  const size_t n = std::min(bytes, (size_t)160 * 16 * 64 * sizeof(unsigned long long));
   if (cudaMemcpy(host_out, t, n, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
   return n;
 }
@@ -364,6 +364,8 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
           return fail(SEGCONV_E_UNSUPPORTED,
                       "class-folded tensor-core path: needs p_fused == 0, cin a multiple of the "
                       "channel block and a halo that fits shared memory");
+        if (tc_fold_ts_supported(pr, math))
+          return cuda_status(launch_tc_fold_ts(pr, s), "transpose_conv_fused[tcgen05 fold-ts]");
         return cuda_status(launch_tc_fold(pr, math, s), "transpose_conv_fused[tcgen05 fold]");
       }
       if (!tc_igemm_supported(pr, math))

@@ -43,6 +43,9 @@ int tc_n_tile(int math, int cout);
 // class-folded tcgen05 kernel for narrow layers (tc_fold.cu)
 cudaError_t launch_tc_fold(const FusedProblem& pr, int math, cudaStream_t s);
 bool tc_fold_supported(const FusedProblem& pr, int math);
+// TMEM-weights variant for split-fp16 layers with cout in (16, 32] (tc_fold_ts.cu)
+cudaError_t launch_tc_fold_ts(const FusedProblem& pr, cudaStream_t s);
+bool tc_fold_ts_supported(const FusedProblem& pr, int math);
 bool tc_fold_available(int math, int cin, int cout);
 bool tc_fold_fits(int math, int kh, int kw, int p, int cin, int cout);
 void fold_window(int kh, int kw, int p, int* ur, int* uc);

@@ -70,35 +70,51 @@ struct Params {
   int S, S_pad, pieces, piece_rows;
   int a_stage_bytes, w_bytes, w_rows;
   int stages_a;
+  int land, stages_l, l_stage_bytes;  // LAND: fp32 halo lands by TMA in [row][kb] boxes
+                                      // (128-byte rows), converters write the operand stages
   int shifts;
   int shift_off[MAX_SHIFTS];       // dy * pitch + dx
   int rows[4], cols[4];
+  int a_tmem_col;                  // TMEM-A variant: first weight column (D below it)
+  int w_img_bytes;                 // TMEM-A variant: bytes of the staged weight image
   unsigned long long* trace;       // optional event trace (SEGCONV_TC_TRACE)
   int debug_nostore;               // diagnostics (SEGCONV_TC_DEBUG bits): 1 skip global
-                                   // stores, 2 skip the fp16 split, 4 skip epilogue body
+                                   // stores, 2 skip the fp16 split, 4 skip epilogue body,
+                                   // 8 skip the MMAs
 };
 
-__device__ __forceinline__ void trace_ev(const Params& p, int ev, long long u) {
-  const int local = (int)((u - blockIdx.x) / gridDim.x);
+__device__ __forceinline__ void trace_ev(const Params& p, int ev, int local) {
   if (p.trace == nullptr || blockIdx.x >= 160 || local >= 64) return;
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  p.trace[(blockIdx.x * 8 + ev) * 64 + local] = t;
+  p.trace[(blockIdx.x * 16 + ev) * 64 + local] = t;
 }
 
-__device__ __forceinline__ void unit_origin(const Params& p, long long u, long long& m0, int& b,
-                                            int& i0, int& j0) {
+// Work unit k (0, 1, ...) of this CTA.  BLOCK: round-robin tiles.  LINEAR:
+// each CTA owns one contiguous range of virtual positions (the grid split in
+// 16-position granules, so the busiest CTA has at most one granule more than
+// the average) cut into units of <= N anchors; a unit's MMA N is its length.
+__device__ __forceinline__ bool next_unit(const Params& p, int k, long long& m0, int& nu, int& b,
+                                          int& i0, int& j0) {
   if (!p.block_mode) {
-    m0 = u * p.N;
+    const long long g16 = (p.Mv + 15) / 16;
+    const long long s16 = g16 * blockIdx.x / gridDim.x, e16 = g16 * (blockIdx.x + 1) / gridDim.x;
+    m0 = (s16 + (long long)k * (p.N / 16)) * 16;
+    if (m0 >= e16 * 16) return false;
+    nu = (int)min((long long)p.N, e16 * 16 - m0);
     b = i0 = j0 = 0;
-  } else {
-    const long long per = (long long)p.tiles_r * p.tiles_c;
-    b = (int)(u / per);
-    const int t = (int)(u - (long long)b * per);
-    i0 = (t / p.tiles_c) * p.TR;
-    j0 = (t % p.tiles_c) * p.TC;
-    m0 = 0;
+    return true;
   }
+  const long long u = blockIdx.x + (long long)k * gridDim.x;
+  if (u >= p.units) return false;
+  const long long per = (long long)p.tiles_r * p.tiles_c;
+  b = (int)(u / per);
+  const int t = (int)(u - (long long)b * per);
+  i0 = (t / p.tiles_c) * p.TR;
+  j0 = (t % p.tiles_c) * p.TC;
+  m0 = 0;
+  nu = p.N;
+  return true;
 }
 
 // Position of the current D column (anchor) while walking a 32-column chunk.
@@ -119,7 +135,7 @@ __device__ __forceinline__ YT cvt_out(float v) {
 template <typename YT, int ACT>
 __device__ __forceinline__ void fold_epilogue_block(const Params& p, const float (&v)[32],
                                                     float* tile, const Walk& w, int warp,
-                                                    int lane) {
+                                                    int lane, int ncols) {
   // write: thread = row, column k -> tile[k][row]
 #pragma unroll
   for (int k = 0; k < 32; ++k) tile[k * 36 + lane] = v[k];
@@ -136,7 +152,7 @@ __device__ __forceinline__ void fold_epilogue_block(const Params& p, const float
     }
   }
   const int j = w.j - w.jj + jj;
-  const bool anchor_ok = jj < w.tc && b < p.batch;
+  const bool anchor_ok = jj < w.tc && b < p.batch && lane < ncols;  // ncols: unit's live columns
   YT* __restrict__ y = reinterpret_cast<YT*>(p.y);
   const int CP = p.CP;
   const int q0 = (warp * 32) / CP;                 // first class in this quadrant
@@ -217,25 +233,39 @@ __device__ __forceinline__ void walk_advance(Walk& w, int d) {
   }
 }
 
-template <int MODE, int N>
+template <int MODE, int N, bool TMEM_A>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_fold_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmap) {
-  constexpr int ACC_BUFS = 512 / N;  // N = 128 -> 4, 256 -> 2
-  constexpr uint32_t IDESC = idesc_f16(MODE == MODE_BF16 ? 1 : 0, N);
+  // TMEM: D tiles of N fp32 columns.  TMEM_A: D double-buffered in columns
+  // [0, 256) and the resident weights (the MMA A operand) in [256, 512);
+  // otherwise D fills all 512 columns and the weights live in SMEM.
+  constexpr int ACC_BUFS = TMEM_A ? 256 / N : 512 / N;
+  constexpr int PLANES = MODE == MODE_F16X3 ? 2 : 1;
 
   extern __shared__ __align__(1024) uint8_t smem[];
   const int SA = p.stages_a;
-  uint8_t* w_base = smem;                         // resident weights
-  uint8_t* a_base = smem + p.w_bytes;             // halo stages
-  uint8_t* epi_base = a_base + (size_t)SA * p.a_stage_bytes;  // 4 x 32 x 36 floats
-  uint64_t* bars = reinterpret_cast<uint64_t*>(epi_base + EPI_TILE_BYTES);
+  // SMEM-A: [resident weights][operand stages][landing stages][epilogue tiles]
+  // TMEM-A: [operand stages][epilogue tiles][landing stages]; the weight image
+  //         is staged once over the first two regions and copied into TMEM
+  //         (tcgen05.cp) before any operand stage or tile is written.
+  const int SL = p.land ? p.stages_l : 0;
+  uint8_t* w_base = smem;
+  uint8_t* a_base = TMEM_A ? smem : smem + p.w_bytes;
+  uint8_t* epi_base = TMEM_A ? a_base + (size_t)SA * p.a_stage_bytes
+                             : a_base + (size_t)SA * p.a_stage_bytes + (size_t)SL * p.l_stage_bytes;
+  uint8_t* l_base = TMEM_A ? epi_base + EPI_TILE_BYTES : a_base + (size_t)SA * p.a_stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(
+      TMEM_A ? l_base + (size_t)SL * p.l_stage_bytes : epi_base + EPI_TILE_BYTES);
   uint64_t* a_land = bars;
   uint64_t* a_full = a_land + SA;
   uint64_t* a_empty = a_full + SA;
   uint64_t* w_full = a_empty + SA;
   uint64_t* acc_full = w_full + 1;
   uint64_t* acc_empty = acc_full + ACC_BUFS;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + ACC_BUFS);
+  uint64_t* l_full = acc_empty + ACC_BUFS;
+  uint64_t* l_empty = l_full + SL;
+  uint64_t* w_free = l_empty + SL;  // TMEM-A: weight image copied out of SMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_free + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 12 && lane == 0) {
@@ -244,7 +274,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_init(&a_full[s], MODE == MODE_F16X3 ? 128u : 1u);
       mbar_init(&a_empty[s], 1);
     }
+    for (int s = 0; s < SL; ++s) {
+      mbar_init(&l_full[s], 1);
+      mbar_init(&l_empty[s], 128);
+    }
     mbar_init(w_full, 1);
+    mbar_init(w_free, 1);
     for (int s = 0; s < ACC_BUFS; ++s) {
       mbar_init(&acc_full[s], 1);
       mbar_init(&acc_empty[s], 256);
@@ -269,10 +304,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const uint32_t LBO_X = MODE == MODE_F16X3 ? 2 * COL : COL;  // hi/lo interleaved columns
   const uint32_t WCOL = (uint32_t)p.w_rows * 16;             // weight k-chunk column
   const uint32_t W_PLANE = (uint32_t)p.nkb * CH * WCOL;
+  const int KS_ALL = p.cin / 16;                             // K=16 steps over cin
 
   if (warp == 14) {
     // ================= halo TMA issuer
-    if (lane == 0) {
+    if (lane == 0 && p.land) {
+      // LAND: one 2-D box {kb channels, rows} per piece -> 4*kb-byte rows
+      int sl = 0;
+      uint32_t ph = 0;
+      const uint32_t row_bytes = (uint32_t)p.kb * 4;
+      const uint32_t stage_tx = (uint32_t)(p.pieces * p.piece_rows) * row_bytes;
+      long long m0;
+      int nu, b, i0, j0;
+      for (int k = 0; next_unit(p, k, m0, nu, b, i0, j0); ++k) {
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          mbar_wait(&l_empty[sl], ph ^ 1);
+          mbar_arrive_expect_tx(&l_full[sl], stage_tx);
+          const uint32_t lbase = smem_u32(l_base + (size_t)sl * p.l_stage_bytes);
+          for (int pc = 0; pc < p.pieces; ++pc)
+            tma_load_2d(lbase + (uint32_t)(pc * p.piece_rows) * row_bytes, &tmap, kb * p.kb,
+                        (int)m0 + pc * p.piece_rows, &l_full[sl]);
+          if (kb == 0) trace_ev(p, 0, k);
+          if (++sl == SL) {
+            sl = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    } else if (lane == 0) {
+      if (TMEM_A) mbar_wait(w_free, 0);  // operand stages hold the staged weights until then
       int st = 0;
       uint32_t ph = 0;
       const uint32_t row_bytes = MODE == MODE_F16X3 ? 32 : 16;
@@ -280,10 +340,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t box_rows = p.block_mode ? (uint32_t)(p.P * p.TRH) : (uint32_t)p.piece_rows;
       const uint32_t stage_tx =
           (uint32_t)CH * (p.block_mode ? box_rows : (uint32_t)(p.pieces * p.piece_rows)) * row_bytes;
-      for (long long u = blockIdx.x; u < p.units; u += gridDim.x) {
-        long long m0;
-        int b, i0, j0;
-        unit_origin(p, u, m0, b, i0, j0);
+      long long m0;
+      int nu, b, i0, j0;
+      for (int k = 0; next_unit(p, k, m0, nu, b, i0, j0); ++k) {
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(&a_empty[st], ph ^ 1);
           uint64_t* bar = MODE == MODE_F16X3 ? &a_land[st] : &a_full[st];
@@ -299,7 +358,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                             &tmap, 0, (int)m0 + pc * p.piece_rows, kb * CH + j, bar);
             }
           }
-          if (kb == 0) trace_ev(p, 0, u);
+          if (kb == 0) trace_ev(p, 0, k);
           if (++st == SA) {
             st = 0;
             ph ^= 1;
@@ -311,14 +370,77 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     // ================= fp16 hi/lo split in place (f16x3)
     // All reads of a stage's fp32 rows happen before the single barrier,
     // then every thread writes its rows' hi / lo halves (in-place hazard).
-    if constexpr (MODE == MODE_F16X3) {
+    if (MODE == MODE_F16X3 && p.land) {
+      // LAND: item = (row, 16-byte k-chunk); a warp reads 8 whole 128-byte
+      // landing rows and writes 8 consecutive rows of each chunk column
+      const int pt = threadIdx.x - 256;
+      int sa = 0, sl = 0;
+      uint32_t pa = 0, pl = 0;
+      const uint32_t lrow = (uint32_t)p.kb * 4;
+      if (TMEM_A) mbar_wait(w_free, 0);  // operand stages hold the staged weights until then
+      long long m0;
+      int nu, b, i0, j0;
+      for (int k = 0; next_unit(p, k, m0, nu, b, i0, j0); ++k) {
+        const int rows_live = min(p.pieces * p.piece_rows, nu + p.shift_off[p.shifts - 1]);
+        const int items = rows_live * CH;
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          mbar_wait(&l_full[sl], pl);
+          mbar_wait(&a_empty[sa], pa ^ 1);
+          const uint32_t lbase = smem_u32(l_base + (size_t)sl * p.l_stage_bytes);
+          const uint32_t abase = smem_u32(a_base + (size_t)sa * p.a_stage_bytes);
+          for (int it0 = pt; it0 < ((p.debug_nostore & 2) ? 0 : items); it0 += 4 * 128) {
+            float4 v[4][2];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int it = it0 + u * 128;
+              if (it < items) {
+                const int r = it / CH, j = it - (it / CH) * CH;
+                const uint32_t src = lbase + (uint32_t)r * lrow + (uint32_t)j * 32;
+                ld_shared_v4f(src, v[u][0]);
+                ld_shared_v4f(src + 16, v[u][1]);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int it = it0 + u * 128;
+              if (it < items) {
+                const int r = it / CH, j = it - (it / CH) * CH;
+                uint32_t hi[4], lo[4];
+                split8x2(v[u][0], v[u][1], hi, lo);
+                const uint32_t dst = abase + (uint32_t)j * 2 * COL + (uint32_t)r * 16;
+                st_shared_v4(dst, hi[0], hi[1], hi[2], hi[3]);
+                st_shared_v4(dst + COL, lo[0], lo[1], lo[2], lo[3]);
+              }
+            }
+          }
+          fence_proxy_async();
+          if (kb == 0 && threadIdx.x == 256) trace_ev(p, 1, k);
+          if (kb == p.nkb - 1 && threadIdx.x == 256) trace_ev(p, 7, k);
+          mbar_arrive(&a_full[sa]);
+          mbar_arrive(&l_empty[sl]);
+          if (++sa == SA) {
+            sa = 0;
+            pa ^= 1;
+          }
+          if (++sl == SL) {
+            sl = 0;
+            pl ^= 1;
+          }
+        }
+      }
+    } else if constexpr (MODE == MODE_F16X3) {
       const int pt = threadIdx.x - 256;
       int st = 0;
       uint32_t ph = 0;
       const int rows_staged = p.block_mode ? p.P * p.TRH : p.pieces * p.piece_rows;
       // RPC row slots of 128 per chunk column; RPT_MAX = 4 chunks x RPC slots
       constexpr int RPC = 3, RPT_MAX = 4 * RPC;  // <= 384 rows x 4 chunks per stage
-      for (long long u = blockIdx.x; u < p.units; u += gridDim.x) {
+      long long m0;
+      int nu, b, i0, j0;
+      for (int k = 0; next_unit(p, k, m0, nu, b, i0, j0); ++k) {
+        // rows a unit actually reads: its anchors plus the largest shift
+        const int rows_live = p.block_mode ? rows_staged
+                                           : min(rows_staged, nu + p.shift_off[p.shifts - 1] + 1);
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(&a_land[st], ph);
           const uint32_t sbase = smem_u32(a_base + (size_t)st * p.a_stage_bytes);
@@ -330,32 +452,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             }
             continue;
           }
-          // RPT rows of each k-chunk column per thread: reads of the whole
-          // stage first, one barrier, then the in-place hi/lo writes
           float4 v[RPT_MAX][2];
 #pragma unroll
-          for (int k = 0; k < RPT_MAX; ++k) {
-            const int j = k / RPC, s = pt + (k % RPC) * 128;
-            if (j < CH && s < rows_staged) {
+          for (int q = 0; q < RPT_MAX; ++q) {
+            const int j = q / RPC, s = pt + (q % RPC) * 128;
+            if (j < CH && s < rows_live) {
               const uint32_t src = sbase + (uint32_t)j * 2 * COL + (uint32_t)s * 32;
-              ld_shared_v4f(src, v[k][0]);
-              ld_shared_v4f(src + 16, v[k][1]);
+              ld_shared_v4f(src, v[q][0]);
+              ld_shared_v4f(src + 16, v[q][1]);
             }
           }
           named_bar(1, 128);
 #pragma unroll
-          for (int k = 0; k < RPT_MAX; ++k) {
-            const int j = k / RPC, s = pt + (k % RPC) * 128;
-            if (j < CH && s < rows_staged) {
+          for (int q = 0; q < RPT_MAX; ++q) {
+            const int j = q / RPC, s = pt + (q % RPC) * 128;
+            if (j < CH && s < rows_live) {
               uint32_t hi[4], lo[4];
-              split8x2(v[k][0], v[k][1], hi, lo);
+              split8x2(v[q][0], v[q][1], hi, lo);
               const uint32_t dst = sbase + (uint32_t)j * 2 * COL + (uint32_t)s * 16;
               st_shared_v4(dst, hi[0], hi[1], hi[2], hi[3]);
               st_shared_v4(dst + COL, lo[0], lo[1], lo[2], lo[3]);
             }
           }
           fence_proxy_async();
-          if (kb == 0 && threadIdx.x == 256) trace_ev(p, 1, u);
+          if (kb == 0 && threadIdx.x == 256) trace_ev(p, 1, k);
           mbar_arrive(&a_full[st]);
           if (++st == SA) {
             st = 0;
@@ -365,48 +485,86 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 13) {
-    // ================= resident weights: one bulk-copy pass
+    // ================= resident weights in SMEM: one bulk-copy pass
     if (lane == 0) {
-      mbar_arrive_expect_tx(w_full, (uint32_t)p.w_bytes);
+      const uint32_t wb = TMEM_A ? (uint32_t)p.w_img_bytes : (uint32_t)p.w_bytes;
+      mbar_arrive_expect_tx(w_full, wb);
       constexpr uint32_t CHUNK = 32768;
-      for (uint32_t off = 0; off < (uint32_t)p.w_bytes; off += CHUNK)
-        bulk_g2s(w_base + off, p.panels + off, min(CHUNK, (uint32_t)p.w_bytes - off), w_full);
+      for (uint32_t off = 0; off < wb; off += CHUNK)
+        bulk_g2s(w_base + off, p.panels + off, min(CHUNK, wb - off), w_full);
     }
   } else if (warp == 12) {
     // ================= MMA issuer
     if (lane == 0) {
       mbar_wait(w_full, 0);
       tc_fence_after();
+      trace_ev(p, 6, 0);
       const uint32_t w_addr = smem_u32(w_base);
+      const uint32_t a_tm = tmem_base + (uint32_t)p.a_tmem_col;
+      if constexpr (TMEM_A) {
+        // staged image [plane][k_block][k-chunk][shift*128 + row][16 B]: each
+        // (shift, plane, k-chunk) is one 128-row block -> 4 TMEM columns at
+        // ((shift * PLANES + plane) * KS_ALL + chunk / 2) * 8 + (chunk % 2) * 4
+        for (int s = 0; s < p.shifts; ++s)
+          for (int pl = 0; pl < PLANES; ++pl)
+            for (int J = 0; J < p.cin / 8; ++J) {
+              const int kbi = J / CH, j = J - (J / CH) * CH;
+              const uint32_t src = w_addr + ((uint32_t)(pl * p.nkb + kbi) * CH + j) * WCOL +
+                                   (uint32_t)(s * p.R) * 16;
+              tmem_cp_128x128b(a_tm + (uint32_t)(((s * PLANES + pl) * KS_ALL + J / 2) * 8 + (J & 1) * 4),
+                               sdesc(src, 2048, 128));
+            }
+        mma_commit(w_free);
+      }
       int sa = 0, acc = 0;
       uint32_t pa = 0, pacc = 0;
-      for (long long u = blockIdx.x; u < p.units; u += gridDim.x) {
+      long long m0;
+      int nu, b, i0, j0;
+      for (int k = 0; next_unit(p, k, m0, nu, b, i0, j0); ++k) {
+        const uint32_t idesc = idesc_f16(MODE == MODE_BF16 ? 1 : 0, nu);
         mbar_wait(&acc_empty[acc], pacc ^ 1);
         tc_fence_after();
-        trace_ev(p, 2, u);
+        trace_ev(p, 2, k);
         const uint32_t d = tmem_base + (uint32_t)(acc * N);
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(&a_full[sa], pa);
           tc_fence_after();
           const uint32_t x_addr = smem_u32(a_base + (size_t)sa * p.a_stage_bytes);
           const uint32_t w_kb = w_addr + (uint32_t)(kb * CH) * WCOL;
-          for (int s = 0; s < p.shifts; ++s) {
+          for (int s = 0; s < ((p.debug_nostore & 8) ? 0 : p.shifts); ++s) {
             const uint32_t xs = x_addr + (uint32_t)p.shift_off[s] * 16;
             const uint32_t ws = w_kb + (uint32_t)(s * p.R) * 16;
             for (int ks = 0; ks < CH / 2; ++ks) {
               const uint32_t acc_flag = (kb == 0 && s == 0 && ks == 0) ? 0u : 1u;
-              const uint64_t wh = sdesc(ws + (uint32_t)ks * 2 * WCOL, WCOL, 128);
-              if constexpr (MODE == MODE_F16X3) {
-                const uint32_t xk = xs + (uint32_t)ks * 4 * COL;  // hi chunks 2ks, 2ks+1
-                const uint64_t xh = sdesc(xk, LBO_X, 128);
-                const uint64_t xl = sdesc(xk + COL, LBO_X, 128);
-                const uint64_t wl = sdesc(ws + W_PLANE + (uint32_t)ks * 2 * WCOL, WCOL, 128);
-                mma_f16(d, wh, xh, IDESC, acc_flag);
-                mma_f16(d, wl, xh, IDESC, 1u);
-                mma_f16(d, wh, xl, IDESC, 1u);
+              if constexpr (TMEM_A) {
+                // weight columns: ((shift * PLANES + plane) * KS_ALL + k-step) * 8
+                const int ksg = kb * (CH / 2) + ks;
+                const uint32_t wh = a_tm + (uint32_t)((s * PLANES * KS_ALL + ksg) * 8);
+                if constexpr (MODE == MODE_F16X3) {
+                  const uint32_t xk = xs + (uint32_t)ks * 4 * COL;
+                  const uint64_t xh = sdesc(xk, LBO_X, 128);
+                  const uint64_t xl = sdesc(xk + COL, LBO_X, 128);
+                  const uint32_t wl = wh + (uint32_t)(KS_ALL * 8);
+                  mma_f16_ts(d, wh, xh, idesc, acc_flag);
+                  mma_f16_ts(d, wl, xh, idesc, 1u);
+                  mma_f16_ts(d, wh, xl, idesc, 1u);
+                } else {
+                  mma_f16_ts(d, wh, sdesc(xs + (uint32_t)ks * 2 * COL, LBO_X, 128), idesc, acc_flag);
+                }
               } else {
-                const uint64_t xh = sdesc(xs + (uint32_t)ks * 2 * COL, LBO_X, 128);
-                mma_f16(d, wh, xh, IDESC, acc_flag);
+                const uint64_t wh = sdesc(ws + (uint32_t)ks * 2 * WCOL, WCOL, 128);
+                if constexpr (MODE == MODE_F16X3) {
+                  const uint32_t xk = xs + (uint32_t)ks * 4 * COL;  // hi chunks 2ks, 2ks+1
+                  const uint64_t xh = sdesc(xk, LBO_X, 128);
+                  const uint64_t xl = sdesc(xk + COL, LBO_X, 128);
+                  const uint64_t wl = sdesc(ws + W_PLANE + (uint32_t)ks * 2 * WCOL, WCOL, 128);
+                  mma_f16(d, wh, xh, idesc, acc_flag);
+                  mma_f16(d, wl, xh, idesc, 1u);
+                  mma_f16(d, wh, xl, idesc, 1u);
+                } else {
+                  const uint64_t xh = sdesc(xs + (uint32_t)ks * 2 * COL, LBO_X, 128);
+                  mma_f16(d, wh, xh, idesc, acc_flag);
+                }
               }
             }
           }
@@ -417,7 +575,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
         mma_commit(&acc_full[acc]);
-        trace_ev(p, 3, u);
+        trace_ev(p, 3, k);
         if (++acc == ACC_BUFS) {
           acc = 0;
           pacc ^= 1;
@@ -426,24 +584,22 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else {
     // ================= epilogue: lanes = (class, feature), columns = anchors
-    int acc = 0;
-    uint32_t pacc = 0;
     const int quad = warp & 3, half = warp >> 2;  // TMEM lane quadrant, column-block parity
     const int row = quad * 32 + lane;
+    int acc = 0;
+    uint32_t pacc = 0;
     const int q = row / p.CP, f = row - (row / p.CP) * p.CP;
     const bool row_ok = row < p.R && f < p.cout;
     const bool warp_live = quad * 32 < p.R;
-    const int r = q >> 1, c = q & 1;
-    const int qrows = row_ok ? p.rows[q] : 0, qcols = row_ok ? p.cols[q] : 0;
-    const float bias_f = (row_ok && (p.epi & SEGCONV_EPI_BIAS)) ? __ldg(p.bias + f) : 0.0f;
+    (void)q;
+    (void)row_ok;
     const long long img = (long long)p.n * p.n;
-    for (long long u = blockIdx.x; u < p.units; u += gridDim.x) {
-      long long m0;
-      int b0, i0, j0;
-      unit_origin(p, u, m0, b0, i0, j0);
+    long long m0;
+    int nu, b0, i0, j0;
+    for (int k = 0; next_unit(p, k, m0, nu, b0, i0, j0); ++k) {
       mbar_wait(&acc_full[acc], pacc);
       tc_fence_after();
-      if (threadIdx.x == 0) trace_ev(p, 4, u);
+      if (threadIdx.x == 0) trace_ev(p, 4, k);
       if (warp_live) {  // quadrant holds (class, feature) rows
         const uint32_t tbase = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * N);
         const int act = (p.epi & SEGCONV_EPI_RELU) ? 1 : (p.epi & SEGCONV_EPI_TANH) ? 2 : 0;
@@ -471,24 +627,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         walk_advance(w, 32 * half);
 #pragma unroll 1
-        for (int c0 = 32 * half; c0 < N; c0 += 64) {
+        for (int c0 = 32 * half; c0 < nu; c0 += 64) {
           float v[32];
           tmem_ld32(tbase + (uint32_t)c0, v);
           if (!(p.debug_nostore & 4)) {
             switch (sel) {
-              case 0: fold_epilogue_block<float, 0>(p, v, tile, w, quad, lane); break;
-              case 1: fold_epilogue_block<float, 1>(p, v, tile, w, quad, lane); break;
-              case 2: fold_epilogue_block<float, 2>(p, v, tile, w, quad, lane); break;
-              case 3: fold_epilogue_block<__nv_bfloat16, 0>(p, v, tile, w, quad, lane); break;
-              case 4: fold_epilogue_block<__nv_bfloat16, 1>(p, v, tile, w, quad, lane); break;
-              default: fold_epilogue_block<__nv_bfloat16, 2>(p, v, tile, w, quad, lane); break;
+              case 0: fold_epilogue_block<float, 0>(p, v, tile, w, quad, lane, nu - c0); break;
+              case 1: fold_epilogue_block<float, 1>(p, v, tile, w, quad, lane, nu - c0); break;
+              case 2: fold_epilogue_block<float, 2>(p, v, tile, w, quad, lane, nu - c0); break;
+              case 3: fold_epilogue_block<__nv_bfloat16, 0>(p, v, tile, w, quad, lane, nu - c0); break;
+              case 4: fold_epilogue_block<__nv_bfloat16, 1>(p, v, tile, w, quad, lane, nu - c0); break;
+              default: fold_epilogue_block<__nv_bfloat16, 2>(p, v, tile, w, quad, lane, nu - c0); break;
             }
           }
           walk_advance(w, 64);
+          if (c0 == 32 * half && threadIdx.x == 0) trace_ev(p, 8, k);
         }
       }
       tc_fence_before();
-      if (threadIdx.x == 0) trace_ev(p, 5, u);
+      if (threadIdx.x == 0) trace_ev(p, 5, k);
       mbar_arrive(&acc_empty[acc]);
       if (++acc == ACC_BUFS) {
         acc = 0;
@@ -558,6 +715,7 @@ struct FoldPlan {
   tcf::Params p;
   CUtensorMap tmap;
   size_t smem;
+  bool tmem_a;
   bool ok;
 };
 
@@ -644,15 +802,40 @@ static FoldPlan make_fold_plan_n(const FusedProblem& pr, int math, int block_n) 
   for (int dy = 0; dy < ur; ++dy)
     for (int dx = 0; dx < uc; ++dx) p.shift_off[dy * uc + dx] = dy * pitch + dx;
   p.w_rows = p.shifts * p.R + (128 - p.R);
-  p.w_bytes = planes * p.nkb * CH * p.w_rows * 16;
+  // TMEM-A variant: when the four classes fill all 128 MMA rows and the weights
+  // fit 256 TMEM columns (shifts * planes * cin / 2), the weights become the
+  // MMA A operand in TMEM and all of shared memory goes to halo stages.
+  pl.tmem_a = p.R == 128 && p.N <= 128 && p.shifts * planes * pr.cin / 2 <= 256 &&
+              getenv("SEGCONV_FOLD_NO_TMEM_A") == nullptr;
+  p.a_tmem_col = 256;
+  p.w_img_bytes = planes * p.nkb * CH * p.w_rows * 16;
+  p.w_bytes = pl.tmem_a ? 0 : p.w_img_bytes;
   p.w_bytes = (p.w_bytes + 1023) / 1024 * 1024;
   p.a_stage_bytes = (planes * CH * p.S_pad * 16 + 1023) / 1024 * 1024;
-  const int bar_bytes = (3 * 4 + 1 + 8) * 8 + 16;
+  const int max_stages = 8;
+  const int bar_bytes = (5 * max_stages + 2 + 8) * 8 + 16;
   const int left = tcf::SMEM_LIMIT - bar_bytes - p.w_bytes - tcf::EPI_TILE_BYTES;
-  p.stages_a = std::min(4, left / p.a_stage_bytes);
+  // LAND (split math, LINEAR staging): the fp32 halo lands as {kb, rows} TMA
+  // boxes (4*kb-byte rows: 128-byte requests at kb = 32, against 32-byte ones
+  // for per-chunk boxes) and the converters write the operand stages.
+  p.land = split && !p.block_mode && getenv("SEGCONV_FOLD_NO_LAND") == nullptr ? 1 : 0;
+  if (p.land) {
+    p.l_stage_bytes = (p.pieces * p.piece_rows * p.kb * 4 + 1023) / 1024 * 1024;
+    const int pair = p.a_stage_bytes + p.l_stage_bytes;
+    const int n = std::min(left / pair, max_stages - 1);
+    p.stages_l = std::max(2, (n * 3) / 7);
+    p.stages_a = std::min(max_stages, (left - p.stages_l * p.l_stage_bytes) / p.a_stage_bytes);
+    if (p.stages_a < 2) p.land = 0;
+  }
+  if (!p.land) {
+    p.stages_l = p.l_stage_bytes = 0;
+    p.stages_a = std::min(pl.tmem_a ? max_stages : 4, left / p.a_stage_bytes);
+  }
   if (p.stages_a < 2) return pl;
-  pl.smem = (size_t)p.w_bytes + (size_t)p.stages_a * p.a_stage_bytes + tcf::EPI_TILE_BYTES +
-            bar_bytes;
+  // TMEM-A stages the weight image over the operand stages + epilogue tiles
+  if (pl.tmem_a && p.w_img_bytes > p.stages_a * p.a_stage_bytes + tcf::EPI_TILE_BYTES) return pl;
+  pl.smem = (size_t)p.w_bytes + (size_t)p.stages_a * p.a_stage_bytes +
+            (size_t)p.stages_l * p.l_stage_bytes + tcf::EPI_TILE_BYTES + bar_bytes;
   // halo tensor map
   EncodeTiledFn2 fn = encode_fn2();
   if (!fn) return pl;
@@ -666,6 +849,13 @@ static FoldPlan make_fold_plan_n(const FusedProblem& pr, int math, int block_n) 
                                    (cuuint64_t)8 * es};
     const cuuint32_t box[4] = {8, (cuuint32_t)p.P, (cuuint32_t)p.TRH, 1};
     rc = fn(&pl.tmap, dt, 4, const_cast<void*>(pr.x), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (p.land) {
+    const cuuint64_t dims[2] = {(cuuint64_t)pr.cin, (cuuint64_t)p.Mv};
+    const cuuint64_t strides[1] = {(cuuint64_t)pr.cin * es};
+    const cuuint32_t box[2] = {(cuuint32_t)p.kb, (cuuint32_t)p.piece_rows};
+    rc = fn(&pl.tmap, dt, 2, const_cast<void*>(pr.x), dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
@@ -697,9 +887,9 @@ bool tc_fold_supported(const FusedProblem& pr, int math) {
   return make_fold_plan(pr, math).ok;
 }
 
-template <int MODE, int N>
+template <int MODE, int N, bool TMEM_A>
 static cudaError_t launch_fold_t(const FoldPlan& pl, cudaStream_t s) {
-  auto kern = tcf::tc_fold_kernel<MODE, N>;
+  auto kern = tcf::tc_fold_kernel<MODE, N, TMEM_A>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -729,11 +919,14 @@ cudaError_t launch_tc_fold(const FusedProblem& pr, int math, cudaStream_t s) {
   if (!pl.ok) return cudaErrorNotSupported;
   if (pl.p.units == 0) return cudaSuccess;
   const int mode = math == SEGCONV_MATH_F16X3 ? tcf::MODE_F16X3 : tcf::MODE_BF16;
+  if (pl.tmem_a)
+    return mode == tcf::MODE_F16X3 ? launch_fold_t<tcf::MODE_F16X3, 128, true>(pl, s)
+                                   : launch_fold_t<tcf::MODE_BF16, 128, true>(pl, s);
   if (mode == tcf::MODE_F16X3)
-    return pl.p.N == 256 ? launch_fold_t<tcf::MODE_F16X3, 256>(pl, s)
-                         : launch_fold_t<tcf::MODE_F16X3, 128>(pl, s);
-  return pl.p.N == 256 ? launch_fold_t<tcf::MODE_BF16, 256>(pl, s)
-                       : launch_fold_t<tcf::MODE_BF16, 128>(pl, s);
+    return pl.p.N == 256 ? launch_fold_t<tcf::MODE_F16X3, 256, false>(pl, s)
+                         : launch_fold_t<tcf::MODE_F16X3, 128, false>(pl, s);
+  return pl.p.N == 256 ? launch_fold_t<tcf::MODE_BF16, 256, false>(pl, s)
+                       : launch_fold_t<tcf::MODE_BF16, 128, false>(pl, s);
 }
 
 }  // namespace segconv_b200

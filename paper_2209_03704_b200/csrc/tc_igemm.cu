@@ -94,7 +94,7 @@ __device__ __forceinline__ void trace_ev(const Params& p, int ev, int local) {
   if (p.trace == nullptr || blockIdx.x >= 160 || local >= 64) return;
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  p.trace[(blockIdx.x * 8 + ev) * 64 + local] = t;
+  p.trace[(blockIdx.x * 16 + ev) * 64 + local] = t;
 }
 
 // Work unit u -> (m-group, n-tile); n-tile major so a CTA's units share weights.
@@ -697,8 +697,8 @@ unsigned long long* tc_trace_buffer() {
   if (!init) {
     init = true;
     const char* e = getenv("SEGCONV_TC_TRACE");
-    if (e && e[0] == '1' && cudaMalloc(&g_trace, 160 * 8 * 64 * sizeof(unsigned long long)) == cudaSuccess)
-      cudaMemset(g_trace, 0, 160 * 8 * 64 * sizeof(unsigned long long));
+    if (e && e[0] == '1' && cudaMalloc(&g_trace, 160 * 16 * 64 * sizeof(unsigned long long)) == cudaSuccess)
+      cudaMemset(g_trace, 0, 160 * 16 * 64 * sizeof(unsigned long long));
   }
   return g_trace;
 }

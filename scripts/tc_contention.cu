@@ -1,0 +1,170 @@
+// tc_contention.cu -- diagnostics: does the C2 fold kernel's MMA stream hold
+// its rate on all 148 SMs, and what do concurrent TMEM reads (the epilogue)
+// and tcgen05.cp (weight staging) cost?
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tc_contention scripts/tc_contention.cu
+// Per CTA: one thread issues U units of 48 MMAs (N=128, K=16, A in TMEM,
+// B in SMEM), D double-buffered; with epi=1 four warps drain each finished D
+// (4 x tcgen05.ld 32x32b.x32 per warp) before it is reused.
+#include <cstdint>
+#include <cstdio>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+__device__ __forceinline__ void wait(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{\n.reg .pred P1;\nW:\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n@!P1 bra W;\n}\n" ::"r"(
+          smem_u32(b)),
+      "r"(ph)
+      : "memory");
+}
+__device__ __forceinline__ void commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(b))
+               : "memory");
+}
+
+__global__ void __launch_bounds__(256, 1) run(int units, int epi, int cps, int ntile,
+                                             unsigned long long* out, int rnd) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[2], empty[2], cpbar;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u + blockIdx.x * 97u;
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    h ^= h >> 15;
+    // random fp16 pairs in [-2, 2) (exponent bits limited) or the constant 1.0
+    ((uint32_t*)smem)[i] = rnd ? (h & 0xbfffbfffu) & 0xbbffbbffu : 0x3c003c00u;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 128;" ::"r"(smem_u32(&empty[s])));
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&cpbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(&tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tslot;
+  unsigned long long t0 = clock64();
+  if (threadIdx.x == 0) {
+    // weight staging: `cps` tcgen05.cp 128x128b blocks (2 KB each) into columns 256..
+    for (int i = 0; i < cps; ++i)
+      asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(tmem + 256 + (uint32_t)(i % 64) * 4),
+                   "l"(desc(smem_u32(smem) + (uint32_t)(i % 64) * 2048, 2048, 128))
+                   : "memory");
+    commit(&cpbar);
+    wait(&cpbar, 0);
+    unsigned long long t1 = clock64();
+    out[blockIdx.x * 4 + 1] = t1 - t0;
+    const uint32_t COL = 200 * 16, LBO = 2 * COL;
+    const int shift_off[4] = {0, 1, 64, 65};
+    const uint32_t x0 = smem_u32(smem);
+    const uint32_t id = (1u << 4) | ((uint32_t)(ntile >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    for (int u = 0; u < units; ++u) {
+      const int b = u & 1;
+      if (u >= 2) wait(&empty[b], ((u >> 1) - 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t d = tmem + (uint32_t)b * 128;
+      for (int kb = 0; kb < 2; ++kb)
+        for (int s = 0; s < 4; ++s)
+          for (int ks = 0; ks < 2; ++ks) {
+            const uint32_t acc = (kb == 0 && s == 0 && ks == 0) ? 0u : 1u;
+            const uint32_t xk = x0 + (uint32_t)kb * 4 * LBO + (uint32_t)shift_off[s] * 16 +
+                                (uint32_t)ks * 2 * LBO;
+            const uint64_t xh = desc(xk, LBO, 128), xl = desc(xk + COL, LBO, 128);
+            const uint32_t wh = tmem + 256 + (uint32_t)((s * 2 * 4 + kb * 2 + ks) * 8);
+            const uint32_t wl = wh + 32;
+#define MMA(A_, B_, ACC_)                                                                     \
+  asm volatile(                                                                              \
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], [%1], " \
+      "%2, %3, p;\n}\n" ::"r"(d),                                                             \
+      "r"(A_), "l"(B_), "r"(id), "r"(ACC_))
+            MMA(wh, xh, acc);
+            MMA(wl, xh, 1u);
+            MMA(wh, xl, 1u);
+          }
+      commit(&full[b]);
+    }
+    // drain
+    for (int u = (units > 2 ? units - 2 : 0); u < units; ++u) wait(&full[u & 1], (u >> 1) & 1);
+    out[blockIdx.x * 4 + 0] = clock64() - t1;
+  } else if (warp >= 4) {
+    // epilogue: drain each D (128 columns) with tcgen05.ld, then release it
+    float acc = 0.f;
+    for (int u = 0; u < units; ++u) {
+      const int b = u & 1;
+      wait(&full[b], (u >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (epi) {
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t r[32];
+          const uint32_t ta = tmem + ((uint32_t)((warp - 4) * 32) << 16) + (uint32_t)(b * 128 + c);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+              "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+              : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+                "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+                "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+                "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+                "=r"(r[31])
+              : "r"(ta));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          for (int i = 0; i < 32; ++i) acc += __uint_as_float(r[i]);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[b])) : "memory");
+    }
+    if (acc == 12345.f) out[0] = 1;  // keep the loads
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+int main() {
+  unsigned long long* d;
+  cudaMalloc(&d, 148 * 4 * 8);
+  unsigned long long h[148 * 4];
+  cudaFuncSetAttribute(run, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  struct V {
+    int grid, units, epi, cps, n;
+  } vs[] = {{1, 32, 0, 0, 128},  {148, 32, 0, 0, 128}, {1, 32, 1, 0, 128}, {148, 32, 1, 0, 128},
+            {148, 32, 1, 0, 64}};
+  for (int rnd = 0; rnd < 2; ++rnd)
+  for (const V& v : vs) {
+    for (int rep = 0; rep < 2; ++rep) {
+      run<<<v.grid, 256, 160 * 1024>>>(v.units, v.epi, v.cps, v.n, d, rnd);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) {
+        printf("error %s\n", cudaGetErrorString(e));
+        return 1;
+      }
+    }
+    cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    double mx = 0, cpmx = 0;
+    for (int c = 0; c < v.grid; ++c) {
+      mx = h[c * 4] > mx ? h[c * 4] : mx;
+      cpmx = h[c * 4 + 1] > cpmx ? h[c * 4 + 1] : cpmx;
+    }
+    printf("%s grid %3d units %2d epi %d cps %2d N %3d: %.1f cycles/MMA (max CTA), cp phase %.0f cycles (%.1f/cp)\n",
+           rnd ? "random" : "const ", v.grid, v.units, v.epi, v.cps, v.n, mx / (v.units * 48.0), cpmx, v.cps ? cpmx / v.cps : 0.0);
+  }
+  return 0;
+}
