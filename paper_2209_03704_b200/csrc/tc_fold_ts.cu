@@ -72,6 +72,7 @@ struct Params {
   const uint8_t* panels;  // UMMA_FOLD image, split planes
   unsigned long long* trace;
   int debug;
+  int cluster;  // CTAs per cluster sharing the weight image load (1, 2 or 4)
 };
 
 __device__ __forceinline__ void trace_ev(const Params& p, int ev, int local) {
@@ -89,6 +90,26 @@ __device__ __forceinline__ bool next_unit(const Params& p, int k, long long& m0,
   if (m0 >= e16 * 16) return false;
   nu = (int)min(128LL, e16 * 16 - m0);
   return true;
+}
+
+// The weight image lands at the top stages of every CTA.  With clusters, CTA
+// r of the cluster fetches slice r of the image and multicasts it to all, so
+// L2 serves each weight byte once per cluster rather than once per SM.
+__device__ __forceinline__ void issue_weights(const Params& p, uint8_t* smem, uint64_t* w_full) {
+  mbar_arrive_expect_tx(w_full, (uint32_t)p.w_img_bytes);
+  uint8_t* dst = smem + (size_t)p.w_stage0 * p.stage_bytes;
+  if (p.cluster > 1) {
+    const uint32_t r = cluster_ctarank();
+    const uint32_t slice = (uint32_t)p.w_img_bytes / (uint32_t)p.cluster;  // 16-byte multiple
+    const uint16_t mask = (uint16_t)((1u << p.cluster) - 1);
+    constexpr uint32_t CHUNK = 16384;
+    for (uint32_t off = r * slice; off < (r + 1) * slice; off += CHUNK)
+      bulk_g2s_multicast(dst + off, p.panels + off, min(CHUNK, (r + 1) * slice - off), w_full, mask);
+    return;
+  }
+  constexpr uint32_t CHUNK = 32768;
+  for (uint32_t off = 0; off < (uint32_t)p.w_img_bytes; off += CHUNK)
+    bulk_g2s(dst + off, p.panels + off, min(CHUNK, (uint32_t)p.w_img_bytes - off), w_full);
 }
 
 template <int ACT>
@@ -156,6 +177,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (p.cluster > 1) cluster_sync();  // peers' mbarriers exist before any multicast lands
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) trace_ev(p, 10, 0);  // prologue done
 
@@ -180,11 +202,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (!weights_issued && st == p.w_stage0) {
             // the first unit's halo is queued ahead of the weight image
             weights_issued = true;
-            mbar_arrive_expect_tx(w_full, (uint32_t)p.w_img_bytes);
-            constexpr uint32_t CHUNK = 32768;
-            for (uint32_t off = 0; off < (uint32_t)p.w_img_bytes; off += CHUNK)
-              bulk_g2s(smem + (size_t)p.w_stage0 * p.stage_bytes + off, p.panels + off,
-                       min(CHUNK, (uint32_t)p.w_img_bytes - off), w_full);
+            issue_weights(p, smem, w_full);
           }
           if (!freed && st >= p.w_stage0) {
             mbar_wait(w_free, 0);
@@ -202,11 +220,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
       if (!weights_issued) {  // fewer stages of work than w_stage0
-        mbar_arrive_expect_tx(w_full, (uint32_t)p.w_img_bytes);
-        constexpr uint32_t CHUNK = 32768;
-        for (uint32_t off = 0; off < (uint32_t)p.w_img_bytes; off += CHUNK)
-          bulk_g2s(smem + (size_t)p.w_stage0 * p.stage_bytes + off, p.panels + off,
-                   min(CHUNK, (uint32_t)p.w_img_bytes - off), w_full);
+        issue_weights(p, smem, w_full);
       }
     }
   } else if (warp >= 8 && warp < 12) {
@@ -407,6 +421,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (p.cluster > 1) cluster_sync();  // no CTA leaves while a peer's multicast may target it
   if (threadIdx.x == 0) {
     trace_ev(p, 11, 0);  // all roles done
     if (p.trace && blockIdx.x < 160) p.trace[(blockIdx.x * 16 + 13) * 64] = clock64();
@@ -515,9 +530,39 @@ static cudaError_t launch_fold_ts_t(const tcfs::Params& prm, const CUtensorMap& 
       sms = 148;
   }
   const long long units = (prm.Mv + 127) / 128;
-  const long long grid = std::min<long long>(units, sms);
+  long long grid = std::min<long long>(units, sms);
   const size_t smem = (size_t)tcfs::STAGES * prm.stage_bytes + (3 * tcfs::STAGES + 6) * 8 + 16;
-  kern<<<(unsigned)grid, tcfs::NUM_THREADS, smem, s>>>(prm, tmap);
+  tcfs::Params pc = prm;
+  static const char* cl_env = getenv("SEGCONV_FOLD_TS_CLUSTER");
+  pc.cluster = cl_env ? atoi(cl_env) : 1;  // measured: 2- and 4-CTA clusters of this
+                                            // 205 KB-SMEM kernel do not all fit at once
+  if (pc.cluster != 1 && pc.cluster != 2 && pc.cluster != 4) pc.cluster = 1;
+  while (pc.cluster > 1 && ((uint32_t)prm.w_img_bytes % (16u * pc.cluster) != 0 || grid < pc.cluster))
+    pc.cluster /= 2;
+  if (pc.cluster > 1) {
+    grid = grid / pc.cluster * pc.cluster;  // whole clusters; ranges re-split over the grid
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(tcfs::NUM_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)pc.cluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, pc, tmap);
+    if (e == cudaSuccess) {
+      note_launch();
+      return cudaSuccess;
+    }
+    cudaGetLastError();  // cluster launch refused: plain launch below
+    pc.cluster = 1;
+    grid = std::min<long long>(units, sms);
+  }
+  kern<<<(unsigned)grid, tcfs::NUM_THREADS, smem, s>>>(pc, tmap);
   note_launch();
   return cudaGetLastError();
 }
