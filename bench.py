@@ -154,10 +154,10 @@ class Layer:
                                      out=self.y)
 
     def step_e2e(self):
-        """Public API with host buffers: H2D of the step's input, compute, D2H of the result."""
-        self.xd.copy_(self.x_pinned, non_blocking=True)
-        self.step()
-        self.y_pinned.copy_(self.y, non_blocking=True)
+        """Public API with host buffers (C ABI segconv_transpose_conv_fused_host): the
+        step's input H2D, compute and result D2H, pipelined over batch slices."""
+        self.sc.transpose_conv_fused(self.x_pinned, self.sks, self.g, activation=self.cfg["act"],
+                                     out=self.y_pinned, staging=(self.xd, self.y), sync=False)
 
     def e2e_bytes(self):
         return self.x_pinned.numel() * self.x_pinned.element_size(), \

@@ -148,6 +148,23 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
                                             segconv_math math, void* d_y, segconv_dtype y_dtype,
                                             void* stream);
 
+/* Host-buffer form of the same operator -- the reference's value-semantics
+ * call (fused_tconv.hpp:69-82 takes and returns host tensors).  h_x is
+ * (batch, n_in, n_in, cin) of x_dtype and h_y (batch, out_h, out_w, cout) of
+ * y_dtype in host memory (page-locked for the copies to overlap); d_x / d_y are
+ * caller-owned device staging buffers of the same sizes.  The batch is cut into
+ * `chunks` slices (<= 0: library default); slice i's host->device copy, fused
+ * kernel and device->host copy run on `stream` plus two library-owned copy
+ * streams, so the transfers overlap the kernels and each other.  Asynchronous:
+ * everything is ordered before later work on `stream`. */
+segconv_status segconv_transpose_conv_fused_host(const void* h_x, void* d_x, segconv_dtype x_dtype,
+                                                 int batch, int n_in, int cin,
+                                                 const segconv_subkernels* sks,
+                                                 const void* d_panels, const segconv_geometry* geom,
+                                                 const float* d_bias, unsigned epilogue,
+                                                 segconv_math math, void* d_y, void* h_y,
+                                                 segconv_dtype y_dtype, int chunks, void* stream);
+
 /* Which math AUTO resolves to for this problem (no launch). */
 segconv_math segconv_select_math(segconv_dtype x_dtype, segconv_dtype panel_dtype, int cin,
                                  int cout, int kh, int kw);

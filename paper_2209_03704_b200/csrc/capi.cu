@@ -380,6 +380,80 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
   }
 }
 
+// Host-buffer pipeline over batch slices (see the header).  Copy streams and
+// events are created once per thread and device.
+namespace {
+struct HostPipe {
+  int dev = -1;
+  cudaStream_t in = nullptr, out = nullptr;
+  cudaEvent_t fork = nullptr, loaded = nullptr, computed = nullptr, drained = nullptr;
+};
+thread_local HostPipe g_pipe;
+}  // namespace
+
+segconv_status segconv_transpose_conv_fused_host(const void* h_x, void* d_x, segconv_dtype x_dtype,
+                                                 int batch, int n_in, int cin,
+                                                 const segconv_subkernels* sks,
+                                                 const void* d_panels, const segconv_geometry* geom,
+                                                 const float* d_bias, unsigned epilogue,
+                                                 segconv_math math, void* d_y, void* h_y,
+                                                 segconv_dtype y_dtype, int chunks, void* stream) {
+  if (!sks || !geom) return fail(SEGCONV_E_CONTRACT, "null descriptor");
+  if (batch < 0) return fail(SEGCONV_E_CONTRACT, "batch must be >= 0, got %d", batch);
+  if (!valid_dtype(x_dtype) || !valid_dtype(y_dtype))
+    return fail(SEGCONV_E_CONTRACT, "unknown activation dtype");
+  if (batch == 0) return SEGCONV_OK;
+  if (!h_x || !h_y || !d_x || !d_y) return fail(SEGCONV_E_CONTRACT, "null data pointer");
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "transpose_conv_fused_host");
+  HostPipe& hp = g_pipe;
+  if (hp.dev != dev) {
+    hp = HostPipe{};
+    if ((e = cudaStreamCreateWithFlags(&hp.in, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaStreamCreateWithFlags(&hp.out, cudaStreamNonBlocking)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&hp.fork, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&hp.loaded, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&hp.computed, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventCreateWithFlags(&hp.drained, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_status(e, "transpose_conv_fused_host: stream setup");
+    hp.dev = dev;
+  }
+  const size_t xs = (size_t)n_in * n_in * cin * dtype_size(x_dtype);
+  const size_t ys = (size_t)geom->out_h * geom->out_w * sks->cout * dtype_size(y_dtype);
+  if (chunks <= 0) chunks = 8;
+  chunks = std::max(1, std::min(chunks, batch));
+  cudaStream_t s = (cudaStream_t)stream;
+  // the copy streams start after everything already queued on `stream`
+  if ((e = cudaEventRecord(hp.fork, s)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(hp.in, hp.fork, 0)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(hp.out, hp.fork, 0)) != cudaSuccess)
+    return cuda_status(e, "transpose_conv_fused_host: fork");
+  for (int c = 0; c < chunks; ++c) {
+    const int b0 = (int)((long long)batch * c / chunks), b1 = (int)((long long)batch * (c + 1) / chunks);
+    if (b1 == b0) continue;
+    const size_t xo = (size_t)b0 * xs, yo = (size_t)b0 * ys;
+    if ((e = cudaMemcpyAsync((char*)d_x + xo, (const char*)h_x + xo, (size_t)(b1 - b0) * xs,
+                             cudaMemcpyHostToDevice, hp.in)) != cudaSuccess ||
+        (e = cudaEventRecord(hp.loaded, hp.in)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(s, hp.loaded, 0)) != cudaSuccess)
+      return cuda_status(e, "transpose_conv_fused_host: upload");
+    const segconv_status st = segconv_transpose_conv_fused(
+        (const char*)d_x + xo, x_dtype, b1 - b0, n_in, cin, sks, d_panels, geom, d_bias, epilogue,
+        math, (char*)d_y + yo, y_dtype, stream);
+    if (st != SEGCONV_OK) return st;
+    if ((e = cudaEventRecord(hp.computed, s)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(hp.out, hp.computed, 0)) != cudaSuccess ||
+        (e = cudaMemcpyAsync((char*)h_y + yo, (const char*)d_y + yo, (size_t)(b1 - b0) * ys,
+                             cudaMemcpyDeviceToHost, hp.out)) != cudaSuccess)
+      return cuda_status(e, "transpose_conv_fused_host: download");
+  }
+  if ((e = cudaEventRecord(hp.drained, hp.out)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(s, hp.drained, 0)) != cudaSuccess)
+    return cuda_status(e, "transpose_conv_fused_host: join");
+  return SEGCONV_OK;
+}
+
 size_t segconv_naive_workspace_bytes(segconv_dtype dtype, int batch, int n_in, int cin, int p_orig) {
   if (batch < 0 || n_in < 1 || cin < 1 || p_orig < 0 || !valid_dtype(dtype)) return 0;
   const size_t up = 2 * (size_t)n_in - 1 + 2 * (size_t)p_orig;

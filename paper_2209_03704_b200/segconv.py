@@ -295,7 +295,8 @@ def transpose_conv_fused(x: torch.Tensor, k: Union[SubKernelSet, torch.Tensor],
                          geom: Union[TConvGeometry, int, None] = None, *,
                          bias: Optional[torch.Tensor] = None, activation: Optional[str] = None,
                          math: Optional[str] = None, out_dtype: Optional[torch.dtype] = None,
-                         out: Optional[torch.Tensor] = None) -> torch.Tensor:
+                         out: Optional[torch.Tensor] = None, staging=None,
+                         chunks: Optional[int] = None, sync: bool = True) -> torch.Tensor:
     """Segregated 2x transpose convolution.
 
     ``transpose_conv_fused(x, sks, geom)``  -- reference fused_tconv.hpp:69-82
@@ -304,6 +305,13 @@ def transpose_conv_fused(x: torch.Tensor, k: Union[SubKernelSet, torch.Tensor],
     ``x`` is (N, N, cin) or (B, N, N, cin); the result is (out_h, out_w, cout)
     or (B, out_h, out_w, cout).  Optional fused epilogue: ``bias`` (cout,) then
     ``activation`` "relu" | "tanh".
+
+    A host (CPU) ``x`` gives a host result, as the reference's value-semantics
+    call does, through segconv_transpose_conv_fused_host: batch slices are
+    uploaded, computed and downloaded in a pipeline (``chunks`` slices; use
+    page-locked ``x`` / ``out`` for overlap).  ``staging`` = (device x, device y)
+    buffers to reuse; ``sync=False`` leaves the result pending on the current
+    stream.
     """
     xb, squeeze = _as_batch(x)
     if isinstance(k, torch.Tensor):
@@ -325,6 +333,9 @@ def transpose_conv_fused(x: torch.Tensor, k: Union[SubKernelSet, torch.Tensor],
                                 f"for {g.n_in}x{g.n_in}")
     m = MATHS[math] if math is not None else A.MATH_AUTO
     host = not xb.is_cuda
+    if host:
+        y = _fused_host(xb, sks, g, m, bias, activation, out_dtype, out, staging, chunks, sync)
+        return y[0] if squeeze else y
     dev = _device()
     xd = xb.to(dev).contiguous()
     b, cin = int(xd.shape[0]), int(xd.shape[3])
@@ -350,6 +361,44 @@ def transpose_conv_fused(x: torch.Tensor, k: Union[SubKernelSet, torch.Tensor],
     if host:
         y = y.cpu()
     return y[0] if squeeze else y
+
+
+def _fused_host(xb, sks, g, m, bias, activation, out_dtype, out, staging, chunks, sync):
+    """Host-buffer call: C ABI segconv_transpose_conv_fused_host (pipelined copies)."""
+    dev = _device()
+    xh = xb.contiguous()
+    b, cin = int(xh.shape[0]), int(xh.shape[3])
+    odt = out_dtype or xh.dtype
+    shape = (b, g.out_h, g.out_w, sks.cout())
+    if out is None:
+        yh = torch.empty(shape, dtype=odt, pin_memory=torch.cuda.is_available())
+    else:
+        yh = out if out.dim() == 4 else out.unsqueeze(0)
+        if tuple(yh.shape) != shape or not yh.is_contiguous() or yh.is_cuda:
+            raise ContractError("`out` must be a contiguous host tensor of the output shape")
+    if staging is None:
+        xd = torch.empty(xh.shape, dtype=xh.dtype, device=dev)
+        yd = torch.empty(shape, dtype=yh.dtype, device=dev)
+    else:
+        xd, yd = staging
+        if tuple(xd.shape) != tuple(xh.shape) or tuple(yd.shape) != shape or \
+                xd.dtype != xh.dtype or yd.dtype != yh.dtype:
+            raise ContractError("staging buffers do not match the input / output")
+    epi = _epilogue(bias, activation)
+    bptr = None
+    if bias is not None:
+        bias = bias.to(dev, torch.float32).contiguous()
+        if bias.numel() != sks.cout():
+            raise ContractError(f"bias has {bias.numel()} elements, cout is {sks.cout()}")
+        bptr = bias.data_ptr()
+    gc = g._c()
+    _check(A.lib().segconv_transpose_conv_fused_host(
+        xh.data_ptr(), xd.data_ptr(), _dtype_code(xh), b, int(xh.shape[1]), cin,
+        C.byref(sks.desc), sks.panels.data_ptr(), C.byref(gc), bptr, epi, m, yd.data_ptr(),
+        yh.data_ptr(), _dtype_code(yh), int(chunks or 0), _stream()))
+    if sync:
+        torch.cuda.current_stream().synchronize()
+    return yh
 
 
 def transpose_conv_fused_parallel(x: torch.Tensor, sks: SubKernelSet, geom: TConvGeometry,

@@ -351,3 +351,24 @@ def test_delta_kernel_routing():
                     if 0 <= yy < g.out_h and 0 <= xx < g.out_w:
                         want[yy, xx] = x[i, j, 1]
             np.testing.assert_array_equal(y, want)
+
+
+# ------------------------------------------------ host-buffer pipeline (e2e)
+@pytest.mark.parametrize("batch,chunks", [(16, 0), (5, 3), (3, 8), (1, 1)])
+def test_host_buffer_pipeline_matches_device_call(batch, chunks):
+    """segconv_transpose_conv_fused_host (host x in, host y out, batch slices
+    pipelined over copy streams) equals the device-pointer call bit for bit,
+    for uneven slicing and more slices than images."""
+    rng = np.random.default_rng(batch * 31 + chunks)
+    x = rng.uniform(-1, 1, (batch, 64, 64, 64)).astype(np.float32)
+    k = (rng.standard_normal((3, 3, 64, 32)) * 0.059).astype(np.float32)
+    kt = cuda(k)
+    g = sc.tconv_geometry(64, 3, 3, 0)
+    sks = sc.segregate(kt, 0, math="auto")
+    want = sc.transpose_conv_fused(cuda(x), sks, g).cpu().numpy()
+    xh = torch.from_numpy(x).pin_memory()
+    got = sc.transpose_conv_fused(xh, sks, g, chunks=chunks)
+    assert not got.is_cuda
+    assert np.array_equal(got.numpy(), want)
+    # and against the oracle at the fp32 tolerance (first image)
+    approx_ok(got.numpy()[0], oracle.tconv_fused(x[:1], k, 0)[0], TOL_F32)
