@@ -421,7 +421,7 @@ segconv_status segconv_transpose_conv_fused_host(const void* h_x, void* d_x, seg
   }
   const size_t xs = (size_t)n_in * n_in * cin * dtype_size(x_dtype);
   const size_t ys = (size_t)geom->out_h * geom->out_w * sks->cout * dtype_size(y_dtype);
-  if (chunks <= 0) chunks = 8;
+  if (chunks <= 0) chunks = 16;  // measured on C2: 1 -> 0.99 ms, 4 -> 0.75, 16 -> 0.73 (copies alone 0.62)
   chunks = std::max(1, std::min(chunks, batch));
   cudaStream_t s = (cudaStream_t)stream;
   // the copy streams start after everything already queued on `stream`
