@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -210,6 +211,14 @@ segconv_status segconv_subkernels_for_math(int kh, int kw, int cin, int cout, in
     case SEGCONV_MATH_F16X3: {
       // narrow layers (cout <= 32, p_fused == 0): class-folded kernel
       const bool fold = tc_fold_fits(math, kh, kw, p_orig, cin, cout);
+      // wide bf16 layers: CTA-pair kernel on K-major (class, f, u, v, ch) panels
+      if (!fold && math == SEGCONV_MATH_BF16 && tc_wide_fits(kh, kw, p_orig, cin, cout) &&
+          getenv("SEGCONV_NO_WIDE") == nullptr) {
+        const segconv_status st = segconv_subkernels_init(kh, kw, cin, cout, p_orig, SEGCONV_BF16,
+                                                          SEGCONV_PANEL_KMAJOR, out);
+        if (st == SEGCONV_OK) out->math = SEGCONV_MATH_BF16;
+        return st;
+      }
       return segconv_subkernels_init(
           kh, kw, cin, cout, p_orig, math == SEGCONV_MATH_BF16 ? SEGCONV_BF16 : SEGCONV_F16_SPLIT,
           fold ? SEGCONV_PANEL_UMMA_FOLD : SEGCONV_PANEL_UMMA, out);
@@ -354,6 +363,16 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
     }
     case SEGCONV_MATH_BF16:
     case SEGCONV_MATH_F16X3: {
+      if (sks->layout == SEGCONV_PANEL_KMAJOR && math == SEGCONV_MATH_BF16) {
+        if ((int)math != sks->math)
+          return fail(SEGCONV_E_CONTRACT, "panels were laid out for math %d, not %d", sks->math,
+                      (int)math);
+        if (!tc_wide_supported(pr, math))
+          return fail(SEGCONV_E_UNSUPPORTED,
+                      "CTA-pair tensor-core path needs bf16 activations, cin %% 64 == 0, cout >= 64, "
+                      "p_fused == 0 and a halo of <= 256 rows");
+        return cuda_status(launch_tc_wide(pr, s), "transpose_conv_fused[tcgen05 pair]");
+      }
       if (sks->layout != SEGCONV_PANEL_UMMA && sks->layout != SEGCONV_PANEL_UMMA_FOLD)
         return fail(SEGCONV_E_CONTRACT, "tensor-core math needs UMMA-layout panels");
       if ((int)math != sks->math)

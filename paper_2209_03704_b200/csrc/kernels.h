@@ -43,6 +43,11 @@ int tc_n_tile(int math, int cout);
 // class-folded tcgen05 kernel for narrow layers (tc_fold.cu)
 cudaError_t launch_tc_fold(const FusedProblem& pr, int math, cudaStream_t s);
 bool tc_fold_supported(const FusedProblem& pr, int math);
+// CTA-pair (cta_group::2) implicit GEMM for wide bf16 layers (tc_wide.cu)
+cudaError_t launch_tc_wide(const FusedProblem& pr, cudaStream_t s);
+bool tc_wide_supported(const FusedProblem& pr, int math);
+bool tc_wide_fits(int kh, int kw, int p, int cin, int cout);
+int tc_wide_ntile(int cout);
 // TMEM-weights variant for split-fp16 layers with cout in (16, 32] (tc_fold_ts.cu)
 cudaError_t launch_tc_fold_ts(const FusedProblem& pr, cudaStream_t s);
 bool tc_fold_ts_supported(const FusedProblem& pr, int math);

@@ -1,0 +1,585 @@
+// tc_wide.cu -- K3 for wide bf16 layers (BASELINE C3, C5 a-c): the segregated
+// transpose convolution as a CTA-pair (cta_group::2) tcgen05 implicit GEMM.
+//
+// Replaces reference proj/include/segconv/fused_tconv.hpp:42-60 and the dot
+// loop of reference_ops.hpp:31-79 for layers with cin % 64 == 0 and cout >= 64.
+//
+// Formulation (halo shift, as tc_igemm.cu).  Anchors m = (b, i, j) of the
+// NHWC input are GEMM rows; class q's tap (u, v) reads pixel m + shift,
+// shift = (off_r + u) * n + (off_c + v), so every tap of every class is the
+// same staged halo read from a different row.  A work unit is (pair tile of
+// 256 anchors, feature tile of NT <= 256 outputs, class q):
+//   D[m, f] = sum_{taps t of q} sum_ch X[m + shift_t, ch] * W_t[f, ch]
+// with K = taps(q) * cin.
+//
+// B200 mapping.
+//   * Two CTAs of a cluster (one TPC) run one M = 256 MMA (cta_group::2): CTA
+//     r stages anchors [m0 + 128 r, +128) and features [NT/2 r, +NT/2) of the
+//     tile, so each SM reads 4 KB of A and NT/2 * 32 B of B per K=16 step --
+//     half the shared-memory and L2 traffic of a 1-SM tile -- while its TMEM
+//     holds the full 128 x NT accumulator of its anchors.
+//   * Halo and weights arrive by TMA as 128-byte rows (64 bf16 channels) with
+//     the 128-byte swizzle; the MMA reads them through SW128 K-major
+//     descriptors.  A row shift of the halo is a descriptor start offset with
+//     base_offset 0 (known-answer test: scripts/sw128_test.cu).
+//   * Weights come from the KMAJOR panels (class, f, u, v, ch): one 3-D
+//     tensor map per class, box {64 ch, 1 tap, NT/2 features}.
+//   * Both CTAs' TMA loads complete on the leader's mbarriers; the leader's
+//     single MMA thread issues every MMA and multicasts its commits to both
+//     CTAs' "empty" / "accumulator full" barriers; both epilogues release the
+//     accumulator on the leader's barrier.
+//   * D is double-buffered in TMEM (2 x NT columns), so the epilogue of one
+//     unit overlaps the MMAs of the next.
+//
+// Warp roles (224 threads per CTA): 0-3 epilogue (lane = anchor: each thread
+// stores its anchor's features contiguously, bias / ReLU / tanh fused),
+// 4 TMA producer, 5 MMA issuer (leader CTA), 6 TMEM allocator.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_ptx.cuh"
+
+namespace segconv_b200 {
+namespace tcw {
+
+using namespace tc;
+
+constexpr int NUM_THREADS = 224;
+constexpr int SMEM_LIMIT = 227 * 1024;
+constexpr int KB = 64;  // channels per stage: one 128-byte row
+constexpr int MAX_TAPS_Q = 16;
+constexpr int MAX_STAGES_A = 4, MAX_STAGES_B = 12;
+
+struct Params {
+  void* y;
+  const float* bias;
+  unsigned epi;
+  int y_dtype;
+  int batch, n, cin, cout, out_h, out_w;
+  long long Mv;  // batch * n * n anchors (virtual positions, p_fused == 0)
+  int NT, n_tiles, nkb;
+  int S_rows;
+  int a_stage_bytes, b_stage_bytes, stages_a, stages_b;
+  int taps[4];
+  int shift[4][MAX_TAPS_Q];
+  int rows[4], cols[4];
+  long long pair_tiles, units;
+  unsigned long long* trace;
+  int debug;
+};
+
+struct Maps {
+  CUtensorMap x;     // (cin, Mv) bf16, box {64, S_rows}, 128B swizzle
+  CUtensorMap w[4];  // class q: (cin, taps_q, cout_pad) bf16, box {64, 1, NT/2}, 128B swizzle
+};
+
+// ---------------------------------------------------------------- PTX (pair)
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// arrive (+ expect tx) on an mbarrier given by its shared::cluster address
+__device__ __forceinline__ void mbar_arrive_expect_tx_cl(uint32_t bar_cl, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(
+                   bar_cl),
+               "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cl(uint32_t bar_cl) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cl)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cl(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+// TMA loads into this CTA's SMEM, completing on a (possibly peer) mbarrier
+__device__ __forceinline__ void tma2_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                             uint32_t bar_cl) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cl), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma2_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                             int c2, uint32_t bar_cl) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cl), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+// commit prior MMAs to the mbarrier at this offset in both CTAs of the pair
+__device__ __forceinline__ void commit2(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// SW128 K-major descriptor: SBO = 1024 (8-row atoms), layout type 2, base offset 0
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+__host__ __device__ constexpr uint32_t idesc_bf16_m256(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
+__device__ __forceinline__ void trace_ev(const Params& p, int ev, int local) {
+  if (p.trace == nullptr || blockIdx.x >= 160 || local >= 64) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  p.trace[(blockIdx.x * 16 + ev) * 64 + local] = t;
+}
+
+// unit k of this pair -> (pair tile, feature tile, class)
+__device__ __forceinline__ bool unit_of(const Params& p, int k, long long& pt, int& nt, int& q) {
+  const long long pairs = gridDim.x / 2;
+  const long long u = (long long)(blockIdx.x / 2) + (long long)k * pairs;
+  if (u >= p.units) return false;
+  q = (int)(u & 3);
+  const long long t = u >> 2;
+  nt = (int)(t % p.n_tiles);
+  pt = t / p.n_tiles;
+  return true;
+}
+
+template <int ACT>
+__device__ __forceinline__ float finish(float v, const float* bias, unsigned epi, int f) {
+  if (epi & SEGCONV_EPI_BIAS) v += __ldg(bias + f);
+  if (ACT == 1) v = fmaxf(v, 0.0f);
+  if (ACT == 2) v = tanhf(v);
+  return v;
+}
+
+template <typename YT, int ACT>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    wide_kernel(const __grid_constant__ Params p, const __grid_constant__ Maps maps) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int SA = p.stages_a, SB = p.stages_b;
+  uint8_t* a_base = smem;
+  uint8_t* b_base = smem + (size_t)SA * p.a_stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b_base + (size_t)SB * p.b_stage_bytes);
+  uint64_t* a_full = bars;          // leader: both CTAs' halo bytes
+  uint64_t* a_empty = a_full + SA;  // each CTA: MMAs done with the stage
+  uint64_t* b_full = a_empty + SA;
+  uint64_t* b_empty = b_full + SB;
+  uint64_t* acc_full = b_empty + SB;  // each CTA: accumulator ready
+  uint64_t* acc_empty = acc_full + 2;  // leader: both epilogues drained it
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  if (warp == 5 && lane == 0) {
+    for (int s = 0; s < SA; ++s) {
+      mbar_init(&a_full[s], 1);
+      mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], 8);  // one arrive per epilogue warp of both CTAs
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.x)) : "memory");
+    for (int q = 0; q < 4; ++q)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.w[q])) : "memory");
+  }
+  if (warp == 6) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // both CTAs' barriers initialised before any remote arrive
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int NT2 = p.NT / 2;
+  const uint32_t a_tx = (uint32_t)p.S_rows * 128, b_tx = (uint32_t)NT2 * 128;
+
+  if (warp == 4) {
+    // ===== TMA producer (both CTAs): own halo rows and own half of the features
+    if (lane == 0) {
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
+      long long pt;
+      int nt, q;
+      for (int k = 0; unit_of(p, k, pt, nt, q); ++k) {
+        const long long m0 = pt * 256 + (long long)rank * 128;
+        const int f0 = nt * p.NT + (int)rank * NT2;
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          mbar_wait(&a_empty[sa], pa ^ 1);
+          // the leader expects both CTAs' bytes on its barrier; the peer only
+          // issues its loads (they complete on the leader's barrier)
+          const uint32_t af = mapa(smem_u32(&a_full[sa]), 0);
+          if (rank == 0) mbar_arrive_expect_tx(&a_full[sa], (p.debug & 32) ? 0u : 2 * a_tx);
+          if (!(p.debug & 32))  // diagnostics: no halo loads
+            tma2_load_2d(smem_u32(a_base + (size_t)sa * p.a_stage_bytes), &maps.x, kb * KB, (int)m0, af);
+          if (++sa == SA) {
+            sa = 0;
+            pa ^= 1;
+          }
+          for (int t = 0; t < p.taps[q]; ++t) {
+            mbar_wait(&b_empty[sb], pb ^ 1);
+            const uint32_t bf = mapa(smem_u32(&b_full[sb]), 0);
+            if (rank == 0) mbar_arrive_expect_tx(&b_full[sb], (p.debug & 16) ? 0u : 2 * b_tx);
+            if (!(p.debug & 16))  // diagnostics: no weight loads
+              tma2_load_3d(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), &maps.w[q], kb * KB, t,
+                           f0, bf);
+            if (++sb == SB) {
+              sb = 0;
+              pb ^= 1;
+            }
+          }
+        }
+        if (rank == 0) trace_ev(p, 0, k);
+      }
+    }
+  } else if (warp == 5) {
+    // ===== MMA issuer (leader CTA; the whole warp runs the loop, one lane issues)
+    if (rank == 0) {
+      const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base, 0);
+      int sa = 0, sb = 0, acc = 0;
+      uint32_t pa = 0, pb = 0, pacc = 0;
+      long long pt;
+      int nt, q;
+      const uint32_t idesc = idesc_bf16_m256(p.NT);
+      for (int k = 0; unit_of(p, k, pt, nt, q); ++k) {
+        mbar_wait(&acc_empty[acc], pacc ^ 1);
+        tc_fence_after();
+        if (lane == 0) trace_ev(p, 2, k);
+        const uint32_t d = tb + (uint32_t)(acc * p.NT);
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          mbar_wait(&a_full[sa], pa);
+          tc_fence_after();
+          const uint32_t xa = smem_u32(a_base + (size_t)sa * p.a_stage_bytes);
+          for (int t = 0; t < p.taps[q]; ++t) {
+            mbar_wait(&b_full[sb], pb);
+            tc_fence_after();
+            const uint32_t wa = smem_u32(b_base + (size_t)sb * p.b_stage_bytes);
+            const uint64_t ad = sw128_desc(xa + (uint32_t)p.shift[q][t] * 128);
+            const uint64_t bd = sw128_desc(wa);
+            if (!(p.debug & 8) && elect_one()) {
+#pragma unroll
+              for (int ks = 0; ks < KB / 16; ++ks)  // +32 bytes per K=16 step: +2 in the start field
+                mma2_bf16(d, ad + 2u * ks, bd + 2u * ks, idesc,
+                          (kb == 0 && t == 0 && ks == 0) ? 0u : 1u);
+            }
+            __syncwarp();
+            if (elect_one()) commit2(&b_empty[sb]);
+            __syncwarp();
+            if (++sb == SB) {
+              sb = 0;
+              pb ^= 1;
+            }
+          }
+          if (elect_one()) commit2(&a_empty[sa]);
+          __syncwarp();
+          if (++sa == SA) {
+            sa = 0;
+            pa ^= 1;
+          }
+        }
+        if (elect_one()) commit2(&acc_full[acc]);
+        __syncwarp();
+        if (lane == 0) trace_ev(p, 3, k);
+        if (++acc == 2) {
+          acc = 0;
+          pacc ^= 1;
+        }
+      }
+    }
+  } else if (warp < 4) {
+    // ===== epilogue: lane = anchor; each thread writes its anchor's features
+    const uint32_t lane_base = tmem_base + ((uint32_t)(warp * 32) << 16);
+    const uint32_t acc_empty_leader0 = mapa(smem_u32(&acc_empty[0]), 0);
+    const int img = p.n * p.n;
+    int acc = 0;
+    uint32_t pacc = 0;
+    long long pt;
+    int nt, q;
+    for (int k = 0; unit_of(p, k, pt, nt, q); ++k) {
+      mbar_wait(&acc_full[acc], pacc);
+      tc_fence_after();
+      if (threadIdx.x == 0 && rank == 0) trace_ev(p, 4, k);
+      const long long m = pt * 256 + (long long)rank * 128 + warp * 32 + lane;
+      const int b = (int)(m / img);
+      const int rem = (int)(m - (long long)b * img);
+      const int i = rem / p.n, j = rem - (rem / p.n) * p.n;
+      const int r = q >> 1, c = q & 1;
+      const bool ok = m < p.Mv && i < p.rows[q] && j < p.cols[q] && !(p.debug & 1);
+      YT* dst = reinterpret_cast<YT*>(p.y) +
+                ((long long)((long long)b * p.out_h + 2 * i + r) * p.out_w + 2 * j + c) * p.cout +
+                nt * p.NT;
+      const int fmax = p.cout - nt * p.NT;  // features of this tile that exist
+#pragma unroll 1
+      for (int c0 = 0; c0 < p.NT; c0 += 32) {
+        float v[32];
+        tmem_ld32(lane_base + (uint32_t)(acc * p.NT + c0), v);
+        if (!ok || c0 >= fmax) continue;
+        if (c0 + 32 <= fmax) {
+          if constexpr (sizeof(YT) == 2) {
+            uint32_t w[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int f = nt * p.NT + c0 + 2 * e;
+              const __nv_bfloat162 h = __floats2bfloat162_rn(finish<ACT>(v[2 * e], p.bias, p.epi, f),
+                                                             finish<ACT>(v[2 * e + 1], p.bias, p.epi, f + 1));
+              w[e] = *reinterpret_cast<const uint32_t*>(&h);
+            }
+            uint4* o = reinterpret_cast<uint4*>(dst + c0);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+          } else {
+            float4* o = reinterpret_cast<float4*>(dst + c0);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int f = nt * p.NT + c0 + 4 * e;
+              o[e] = make_float4(finish<ACT>(v[4 * e], p.bias, p.epi, f),
+                                 finish<ACT>(v[4 * e + 1], p.bias, p.epi, f + 1),
+                                 finish<ACT>(v[4 * e + 2], p.bias, p.epi, f + 2),
+                                 finish<ACT>(v[4 * e + 3], p.bias, p.epi, f + 3));
+            }
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (c0 + e < fmax) dst[c0 + e] = from_f<YT>(finish<ACT>(v[e], p.bias, p.epi, nt * p.NT + c0 + e));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cl(acc_empty_leader0 + (uint32_t)acc * 8);
+      if (++acc == 2) {
+        acc = 0;
+        pacc ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // the pair's MMAs and remote arrivals are over before TMEM is freed
+  if (warp == 6) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
+                 : "memory");
+  }
+}
+
+}  // namespace tcw
+
+// ------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFnW)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFnW encode_fn_w() {
+  static EncodeTiledFnW fn = nullptr;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFnW)f;
+  }
+  return fn;
+}
+
+// features per pair tile: the whole (32-padded) cout up to 256
+int tc_wide_ntile(int cout) {
+  const int c32 = (cout + 31) / 32 * 32;
+  return std::min(256, c32);
+}
+
+bool tc_wide_fits(int kh, int kw, int p, int cin, int cout) {
+  if (p / 2 != 0 || cin % tcw::KB != 0 || cout < 64) return false;
+  for (int r = 0; r < 2; ++r) {
+    const int u0 = (p + r) & 1;
+    const int ah = u0 >= kh ? 0 : (kh - u0 + 1) / 2, aw = u0 >= kw ? 0 : (kw - u0 + 1) / 2;
+    if (ah == 0 || aw == 0) return false;
+  }
+  return kh * kw <= 4 * tcw::MAX_TAPS_Q;
+}
+
+static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
+  p = tcw::Params{};
+  if (pr.pf != 0 || pr.x_dtype != SEGCONV_BF16 || pr.panel_dtype != SEGCONV_BF16) return false;
+  if (pr.panel_layout != SEGCONV_PANEL_KMAJOR) return false;
+  if (pr.y_dtype != SEGCONV_BF16 && pr.y_dtype != SEGCONV_F32) return false;
+  if (!tc_wide_fits(pr.kh, pr.kw, pr.p, pr.cin, pr.cout)) return false;
+  p.y = pr.y;
+  p.bias = pr.bias;
+  p.epi = pr.epi;
+  p.y_dtype = pr.y_dtype;
+  p.batch = pr.batch;
+  p.n = pr.n;
+  p.cin = pr.cin;
+  p.cout = pr.cout;
+  p.out_h = pr.out_h;
+  p.out_w = pr.out_w;
+  p.Mv = (long long)pr.batch * pr.n * pr.n;
+  p.NT = tc_wide_ntile(pr.cout);
+  p.n_tiles = (pr.cout + p.NT - 1) / p.NT;
+  if (p.n_tiles * p.NT > pr.cout_pad && p.n_tiles > 1) {
+    // the last tile may run past cout_pad: the TMA box is zero-filled out of bounds
+  }
+  p.nkb = pr.cin / tcw::KB;
+  int max_shift = 0;
+  for (int q = 0; q < 4; ++q) {
+    p.taps[q] = pr.cls.kh[q] * pr.cls.kw[q];
+    if (p.taps[q] > tcw::MAX_TAPS_Q) return false;
+    for (int u = 0; u < pr.cls.kh[q]; ++u)
+      for (int v = 0; v < pr.cls.kw[q]; ++v) {
+        const int s = (pr.cls.off_r[q] + u) * pr.n + (pr.cls.off_c[q] + v);
+        p.shift[q][u * pr.cls.kw[q] + v] = s;
+        max_shift = std::max(max_shift, s);
+      }
+    p.rows[q] = pr.cls.rows[q];
+    p.cols[q] = pr.cls.cols[q];
+  }
+  p.S_rows = (128 + max_shift + 7) / 8 * 8;
+  if (p.S_rows > 256) return false;  // one TMA box
+  p.a_stage_bytes = (p.S_rows * 128 + 1023) / 1024 * 1024;
+  p.b_stage_bytes = (p.NT / 2) * 128;
+  if (p.b_stage_bytes % 1024) return false;
+  const int bar_bytes = (2 * tcw::MAX_STAGES_A + 2 * tcw::MAX_STAGES_B + 4) * 8 + 16;
+  const int budget = tcw::SMEM_LIMIT - bar_bytes;
+  p.stages_a = 3;
+  p.stages_b = std::min(tcw::MAX_STAGES_B, (budget - p.stages_a * p.a_stage_bytes) / p.b_stage_bytes);
+  if (p.stages_b < 4) {
+    p.stages_a = 2;
+    p.stages_b = std::min(tcw::MAX_STAGES_B, (budget - p.stages_a * p.a_stage_bytes) / p.b_stage_bytes);
+  }
+  if (p.stages_b < 2) return false;
+  p.pair_tiles = (p.Mv + 255) / 256;
+  p.units = p.pair_tiles * p.n_tiles * 4;
+  if ((long long)pr.batch * pr.out_h * pr.out_w * pr.cout >= (1LL << 40)) return false;
+  // tensor maps
+  EncodeTiledFnW fn = encode_fn_w();
+  if (!fn) return false;
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)pr.cin, (cuuint64_t)p.Mv};
+    const cuuint64_t strides[1] = {(cuuint64_t)pr.cin * 2};
+    const cuuint32_t box[2] = {(cuuint32_t)tcw::KB, (cuuint32_t)p.S_rows};
+    const cuuint32_t es[2] = {1, 1};
+    if (fn(&maps.x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pr.x), dims, strides,
+           box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  for (int q = 0; q < 4; ++q) {
+    const cuuint64_t dims[3] = {(cuuint64_t)pr.cin, (cuuint64_t)p.taps[q], (cuuint64_t)pr.cout_pad};
+    const cuuint64_t strides[2] = {(cuuint64_t)pr.cin * 2, (cuuint64_t)p.taps[q] * pr.cin * 2};
+    const cuuint32_t box[3] = {(cuuint32_t)tcw::KB, 1, (cuuint32_t)(p.NT / 2)};
+    const cuuint32_t es[3] = {1, 1, 1};
+    void* base = (char*)const_cast<void*>(pr.panels) + pr.cls.sub_offset[q] * 2;
+    if (fn(&maps.w[q], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  return true;
+}
+
+bool tc_wide_supported(const FusedProblem& pr, int math) {
+  if (math != SEGCONV_MATH_BF16) return false;
+  tcw::Params p;
+  tcw::Maps m;
+  return make_wide(pr, p, m);
+}
+
+template <typename YT, int ACT>
+static cudaError_t launch_wide_t(const tcw::Params& prm, const tcw::Maps& maps, cudaStream_t s) {
+  auto kern = tcw::wide_kernel<YT, ACT>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tcw::SMEM_LIMIT);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
+    (void)e;
+    configured = true;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+  }
+  const long long pairs = std::min<long long>(prm.units, sms / 2);
+  const size_t smem = (size_t)prm.stages_a * prm.a_stage_bytes + (size_t)prm.stages_b * prm.b_stage_bytes +
+                      (2 * tcw::MAX_STAGES_A + 2 * tcw::MAX_STAGES_B + 4) * 8 + 16;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * pairs));
+  cfg.blockDim = dim3(tcw::NUM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm, maps);
+  if (e == cudaSuccess) note_launch();
+  return e;
+}
+
+cudaError_t launch_tc_wide(const FusedProblem& pr, cudaStream_t s) {
+  tcw::Params p;
+  tcw::Maps maps;
+  if (!make_wide(pr, p, maps)) return cudaErrorNotSupported;
+  if (p.units == 0) return cudaSuccess;
+  p.trace = tc_trace_buffer();
+  static const int dbg = getenv("SEGCONV_TC_DEBUG") ? atoi(getenv("SEGCONV_TC_DEBUG")) : 0;
+  p.debug = dbg;
+  const int act = (pr.epi & SEGCONV_EPI_RELU) ? 1 : (pr.epi & SEGCONV_EPI_TANH) ? 2 : 0;
+  if (pr.y_dtype == SEGCONV_BF16) {
+    if (act == 1) return launch_wide_t<__nv_bfloat16, 1>(p, maps, s);
+    if (act == 2) return launch_wide_t<__nv_bfloat16, 2>(p, maps, s);
+    return launch_wide_t<__nv_bfloat16, 0>(p, maps, s);
+  }
+  if (act == 1) return launch_wide_t<float, 1>(p, maps, s);
+  if (act == 2) return launch_wide_t<float, 2>(p, maps, s);
+  return launch_wide_t<float, 0>(p, maps, s);
+}
+
+}  // namespace segconv_b200

@@ -34,7 +34,7 @@ def run_tc(x, k, p, math, act=None, bias=None, out_dtype=None):
     xt, kt = cuda(x, dt), cuda(k, dt)
     g = sc.tconv_geometry(xt.shape[1], kt.shape[0], kt.shape[1], p)
     sks = sc.segregate(kt, p, math=math)
-    assert sks.layout in ("umma", "fold")
+    assert sks.layout in ("umma", "fold", "kmajor")
     y = sc.transpose_conv_fused(xt, sks, g, activation=act,
                                 bias=None if bias is None else cuda(bias), out_dtype=out_dtype)
     torch.cuda.synchronize()
