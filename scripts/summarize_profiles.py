@@ -20,7 +20,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G = os.path.join(ROOT, "gpurun_out")
 P = os.path.join(ROOT, "profiles")
-HOT = {"C1": "tconv_pixlanes", "C2": "tc_fold", "C3": "tc_halo", "C4": "tc_fold", "C5": "tc_"}
+HOT = {"C1": "tconv_pixlanes", "C2": "fold_ts", "C3": "wide_kernel", "C4": "tc_fold", "C5": "wide_kernel"}
 
 
 def short(name):
@@ -51,12 +51,16 @@ def launches(rnd, cfg):
     ours = [r for r in out if not r[1].startswith("vectorized") and "elementwise" not in r[1]
             and "fill" not in r[1].lower()]
     hot = [r for r in ours if HOT[cfg] in r[1]]
+    if hot:  # full-batch step launches only (the e2e leg launches per batch slice)
+        big = max(r[2] for r in hot)
+        hot = [r for r in hot if r[2] >= 0.5 * big]
     step = [r for r in ours if "segregate" not in r[1]]
     summary = {}
     if hot:
         avg = sum(r[2] for r in hot) / len(hot)
         summary = {"hot_kernel": hot[0][1], "launches": len(hot), "avg_duration_us": avg / 1e3,
                    "dram_bytes_per_launch": (hot[-1][3] + hot[-1][4]),
+                   "avg_dram_bytes_per_launch": sum(r[3] + r[4] for r in hot) / len(hot),
                    "share_of_step_kernels": sum(r[2] for r in hot) / max(1e-9, sum(r[2] for r in step))}
     return summary
 
