@@ -42,6 +42,18 @@ static segconv_status cuda_status(cudaError_t e, const char* what) {
 static bool valid_dtype(int d) { return d == SEGCONV_F32 || d == SEGCONV_F64 || d == SEGCONV_BF16; }
 static size_t dtype_size(int d) { return d == SEGCONV_F64 ? 8 : d == SEGCONV_BF16 ? 2 : 4; }
 
+static bool ring_panels_apply(int kh, int kw, int cin, int cout, int p_orig, int panel_dtype) {
+  return kh == 5 && kw == 5 && cout == 3 && p_orig == 0 && cin % 32 == 0 && cin <= 256 &&
+         panel_dtype == SEGCONV_F16_SPLIT;
+}
+// elements of the folded image that precede an appended ring image
+static int64_t fold_image_elems(const segconv_subkernels& s) {
+  const int nkb = (s.cin + s.k_block - 1) / s.k_block;
+  const int planes = s.dtype == SEGCONV_F16_SPLIT ? 2 : 1;
+  return (int64_t)planes * nkb * (s.k_block / 8) *
+         fold_rows(s.source_kh, s.source_kw, s.p_orig, s.cout) * 8;
+}
+
 static SegClasses classes_of(const segconv_subkernels& s, const segconv_geometry& g) {
   SegClasses c{};
   for (int q = 0; q < 4; ++q) {
@@ -168,6 +180,10 @@ segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_
     s.cout_pad = s.n_tile;
     for (int q = 0; q < 4; ++q) s.sub_offset[q] = 0;
     s.total_elems = (int64_t)planes * nkb * (s.k_block / 8) * fold_rows(kh, kw, p_orig, cout) * 8;
+    // split-fp16 5x5 -> 3-channel layers also carry the pixel-scatter image
+    // (tc_ring.cu) after the folded one; the kernel is picked per call by image size
+    if (ring_panels_apply(kh, kw, cin, cout, p_orig, panel_dtype))
+      s.total_elems += (int64_t)(ring_image_bytes(cin) / 2);
   }
   if (layout == SEGCONV_PANEL_UMMA) {
     s.n_tile = tc_n_tile(s.math, cout);
@@ -247,11 +263,17 @@ segconv_status segconv_segregate(const void* d_kernel, segconv_dtype kernel_dtyp
       cls.off_r[q] = sks->off_r[q];
       cls.off_c[q] = sks->off_c[q];
     }
-    return cuda_status(launch_segregate_fold(d_kernel, kernel_dtype, sks->source_kh,
-                                             sks->source_kw, sks->cin, sks->cout, sks->p_orig, cls,
-                                             sks->dtype == SEGCONV_F16_SPLIT, d_panels,
-                                             (cudaStream_t)stream),
-                       "segregate[fold]");
+    segconv_status st = cuda_status(
+        launch_segregate_fold(d_kernel, kernel_dtype, sks->source_kh, sks->source_kw, sks->cin,
+                              sks->cout, sks->p_orig, cls, sks->dtype == SEGCONV_F16_SPLIT,
+                              d_panels, (cudaStream_t)stream),
+        "segregate[fold]");
+    if (st == SEGCONV_OK && sks->total_elems > fold_image_elems(*sks))
+      st = cuda_status(launch_ring_image(d_kernel, kernel_dtype, sks->cin, cls,
+                                         (uint16_t*)d_panels + fold_image_elems(*sks),
+                                         (cudaStream_t)stream),
+                       "segregate[ring]");
+    return st;
   }
   if (sks->layout == SEGCONV_PANEL_UMMA) {
     int taps = 0;
@@ -383,6 +405,9 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
           return fail(SEGCONV_E_UNSUPPORTED,
                       "class-folded tensor-core path: needs p_fused == 0, cin a multiple of the "
                       "channel block and a halo that fits shared memory");
+        if (sks->total_elems > fold_image_elems(*sks) && tc_ring_supported(pr, math))
+          return cuda_status(launch_tc_ring(pr, (const uint16_t*)d_panels + fold_image_elems(*sks), s),
+                             "transpose_conv_fused[tcgen05 ring]");
         if (tc_fold_ts_supported(pr, math))
           return cuda_status(launch_tc_fold_ts(pr, s), "transpose_conv_fused[tcgen05 fold-ts]");
         return cuda_status(launch_tc_fold(pr, math, s), "transpose_conv_fused[tcgen05 fold]");

@@ -48,6 +48,12 @@ cudaError_t launch_tc_wide(const FusedProblem& pr, cudaStream_t s);
 bool tc_wide_supported(const FusedProblem& pr, int math);
 bool tc_wide_fits(int kh, int kw, int p, int cin, int cout);
 int tc_wide_ntile(int cout);
+// pixel-scatter kernel with a register row ring for n=5, cout=3 layers (tc_ring.cu)
+bool tc_ring_supported(const FusedProblem& pr, int math);
+cudaError_t launch_tc_ring(const FusedProblem& pr, const void* ring_img, cudaStream_t s);
+cudaError_t launch_ring_image(const void* k, int k_dtype, int cin, const SegClasses& cls, void* out,
+                              cudaStream_t s);
+size_t ring_image_bytes(int cin);
 // TMEM-weights variant for split-fp16 layers with cout in (16, 32] (tc_fold_ts.cu)
 cudaError_t launch_tc_fold_ts(const FusedProblem& pr, cudaStream_t s);
 bool tc_fold_ts_supported(const FusedProblem& pr, int math);
