@@ -46,6 +46,10 @@ static bool ring_panels_apply(int kh, int kw, int cin, int cout, int p_orig, int
   return kh == 5 && kw == 5 && cout == 3 && p_orig == 0 && cin % 32 == 0 && cin <= 256 &&
          panel_dtype == SEGCONV_F16_SPLIT;
 }
+static bool tile_panels_apply(int kh, int kw, int cin, int cout, int p_orig, int panel_dtype) {
+  return kh == 3 && kw == 3 && cout == 3 && p_orig == 0 && cin % 64 == 0 && cin <= 512 &&
+         panel_dtype == SEGCONV_BF16;
+}
 // elements of the folded image that precede an appended ring image
 static int64_t fold_image_elems(const segconv_subkernels& s) {
   const int nkb = (s.cin + s.k_block - 1) / s.k_block;
@@ -184,6 +188,9 @@ segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_
     // (tc_ring.cu) after the folded one; the kernel is picked per call by image size
     if (ring_panels_apply(kh, kw, cin, cout, p_orig, panel_dtype))
       s.total_elems += (int64_t)(ring_image_bytes(cin) / 2);
+    // bf16 3x3 -> 3-channel layers carry the small-image pixel-scatter image (tc_tile.cu)
+    if (tile_panels_apply(kh, kw, cin, cout, p_orig, panel_dtype))
+      s.total_elems += (int64_t)(tile_image_bytes(cin) / 2);
   }
   if (layout == SEGCONV_PANEL_UMMA) {
     s.n_tile = tc_n_tile(s.math, cout);
@@ -268,11 +275,16 @@ segconv_status segconv_segregate(const void* d_kernel, segconv_dtype kernel_dtyp
                               sks->cout, sks->p_orig, cls, sks->dtype == SEGCONV_F16_SPLIT,
                               d_panels, (cudaStream_t)stream),
         "segregate[fold]");
-    if (st == SEGCONV_OK && sks->total_elems > fold_image_elems(*sks))
-      st = cuda_status(launch_ring_image(d_kernel, kernel_dtype, sks->cin, cls,
-                                         (uint16_t*)d_panels + fold_image_elems(*sks),
-                                         (cudaStream_t)stream),
-                       "segregate[ring]");
+    if (st == SEGCONV_OK && sks->total_elems > fold_image_elems(*sks)) {
+      uint16_t* tail = (uint16_t*)d_panels + fold_image_elems(*sks);
+      st = sks->dtype == SEGCONV_F16_SPLIT
+               ? cuda_status(launch_ring_image(d_kernel, kernel_dtype, sks->cin, cls, tail,
+                                               (cudaStream_t)stream),
+                             "segregate[ring]")
+               : cuda_status(launch_tile_image(d_kernel, kernel_dtype, sks->cin, cls, tail,
+                                               (cudaStream_t)stream),
+                             "segregate[tile]");
+    }
     return st;
   }
   if (sks->layout == SEGCONV_PANEL_UMMA) {
@@ -405,6 +417,9 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
           return fail(SEGCONV_E_UNSUPPORTED,
                       "class-folded tensor-core path: needs p_fused == 0, cin a multiple of the "
                       "channel block and a halo that fits shared memory");
+        if (sks->total_elems > fold_image_elems(*sks) && tc_tile_supported(pr, math))
+          return cuda_status(launch_tc_tile(pr, (const uint16_t*)d_panels + fold_image_elems(*sks), s),
+                             "transpose_conv_fused[tcgen05 tile]");
         if (sks->total_elems > fold_image_elems(*sks) && tc_ring_supported(pr, math))
           return cuda_status(launch_tc_ring(pr, (const uint16_t*)d_panels + fold_image_elems(*sks), s),
                              "transpose_conv_fused[tcgen05 ring]");

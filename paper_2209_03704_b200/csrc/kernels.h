@@ -54,6 +54,12 @@ cudaError_t launch_tc_ring(const FusedProblem& pr, const void* ring_img, cudaStr
 cudaError_t launch_ring_image(const void* k, int k_dtype, int cin, const SegClasses& cls, void* out,
                               cudaStream_t s);
 size_t ring_image_bytes(int cin);
+// pixel-scatter kernel for 3x3 -> 3-channel bf16 layers on small images (tc_tile.cu)
+bool tc_tile_supported(const FusedProblem& pr, int math);
+cudaError_t launch_tc_tile(const FusedProblem& pr, const void* img, cudaStream_t s);
+cudaError_t launch_tile_image(const void* k, int k_dtype, int cin, const SegClasses& cls, void* out,
+                              cudaStream_t s);
+size_t tile_image_bytes(int cin);
 // TMEM-weights variant for split-fp16 layers with cout in (16, 32] (tc_fold_ts.cu)
 cudaError_t launch_tc_fold_ts(const FusedProblem& pr, cudaStream_t s);
 bool tc_fold_ts_supported(const FusedProblem& pr, int math);

@@ -1,0 +1,50 @@
+// tc_scatter.cuh -- column layout shared by the pixel-scatter kernels
+// (tc_ring.cu, tc_tile.cu) and their weight images.
+#pragma once
+
+namespace segconv_b200 {
+
+// Column layout of D (= rows of the weight image), p_orig = 0: per-axis
+// parity r has act(r) = (KH - r + 1) / 2 taps starting at offset r, so the
+// union window is U = act(0) rows / cols.  Columns: for dy, a group padded
+// to a multiple of 16; inside it (q, dx, f) with f fastest.
+template <int KH, int COUT>
+struct ScatterLayout {
+  static constexpr int act(int r) { return (KH - r + 1) / 2; }
+  static constexpr int U = (KH + 1) / 2;
+  static constexpr bool has(int q, int dy, int dx) {
+    return dy >= (q >> 1) && dy < (q >> 1) + act(q >> 1) && dx >= (q & 1) &&
+           dx < (q & 1) + act(q & 1);
+  }
+  static constexpr bool has_dy(int q, int dy) {
+    return dy >= (q >> 1) && dy < (q >> 1) + act(q >> 1);
+  }
+  static constexpr int group_len(int dy) {
+    int n = 0;
+    for (int q = 0; q < 4; ++q)
+      for (int dx = 0; dx < U; ++dx)
+        if (has(q, dy, dx)) n += COUT;
+    return n;
+  }
+  static constexpr int group_pad(int dy) { return (group_len(dy) + 15) / 16 * 16; }
+  static constexpr int group_off(int dy) {
+    int o = 0;
+    for (int d = 0; d < dy; ++d) o += group_pad(d);
+    return o;
+  }
+  static constexpr int N = group_off(U);
+  // column of (dy, q, dx, f) inside its group, -1 if absent
+  static constexpr int col_in_group(int dy, int q, int dx, int f) {
+    if (!has(q, dy, dx)) return -1;
+    int c = 0;
+    for (int qq = 0; qq < 4; ++qq)
+      for (int xx = 0; xx < U; ++xx)
+        if (has(qq, dy, xx)) {
+          if (qq == q && xx == dx) return c + f;
+          c += COUT;
+        }
+    return -1;
+  }
+};
+
+}  // namespace segconv_b200

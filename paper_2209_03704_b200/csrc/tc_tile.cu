@@ -1,0 +1,402 @@
+// tc_tile.cu -- K3 for few-output-channel bf16 layers on small images
+// (BASELINE C5 layer d: 1024 x 11^2 x 128 -> 19^2 x 3, n = 3, tanh).
+//
+// Replaces reference proj/include/segconv/fused_tconv.hpp:42-60 and the dot
+// loop of reference_ops.hpp:31-79 for these layers.
+//
+// Pixel scatter, as tc_ring.cu: one MMA per K step computes, for 128
+// consecutive input pixels p (the NHWC order runs across rows and images),
+//   D[p, (dy, q, dx, f)] = sum_ch X[p, ch] * W_q[dy - off_r][dx - off_c][ch][f]
+// (27 useful columns of N = 48 for n = 3, cout = 3), and the epilogue sums
+// the shifts: anchor m of the tile takes D[m + dy * n + dx, (dy, q, dx, f)].
+// Images here are small (the largest shift, n + 1, is < 64 pixels), so one
+// 128-pixel tile yields 128 - (n + 1) anchors; tiles overlap by n + 1 pixels.
+// The D tile goes TMEM -> registers -> a padded SMEM tile, and each epilogue
+// thread gathers its anchor's 4 x cout sums from it.  bf16 activations land by
+// TMA (box {64 channels, 128 pixels}, 128-byte swizzle) and are the MMA A
+// operand directly; the weight image (rows = D columns) is resident in SMEM.
+//
+// Warp roles (192 threads): 0-3 epilogue, 4 TMA producer / TMEM owner,
+// 5 MMA issuer.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_ptx.cuh"
+#include "tc_scatter.cuh"
+
+namespace segconv_b200 {
+namespace tct {
+
+using namespace tc;
+
+constexpr int NUM_THREADS = 192;
+constexpr int SMEM_LIMIT = 227 * 1024;
+constexpr int KB = 64;  // bf16 channels per stage: one 128-byte row
+constexpr int MAX_STAGES = 8;
+constexpr int TILE = 128;
+
+struct Params {
+  const uint8_t* panels;  // tile weight image: [k-chunk][N rows][8 bf16]
+  void* y;
+  const float* bias;
+  unsigned epi;
+  int batch, n, cin, cout, out_h, out_w;
+  long long Mv, tiles;
+  int step;  // anchors per tile = TILE - (n + 1)
+  int rows[4], cols[4];
+  int stage_bytes, stages, w_bytes;
+  unsigned long long* trace;
+  int debug;
+};
+
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+
+template <int KH, int COUT, int ACT, typename YT>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    tile_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmap) {
+  using L = ScatterLayout<KH, COUT>;
+  constexpr int U = L::U, N = L::N, TP = N + 1;  // SMEM tile pitch (floats)
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int SA = p.stages;
+  uint8_t* a_base = smem;
+  uint8_t* w_base = smem + (size_t)SA * p.stage_bytes;
+  float* dtile = reinterpret_cast<float*>(w_base + p.w_bytes);  // [TILE][TP]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dtile + TILE * TP + (TILE * TP) % 2);
+  uint64_t* a_full = bars;
+  uint64_t* a_empty = a_full + SA;
+  uint64_t* acc_full = a_empty + SA;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* w_full = acc_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 5 && lane == 0) {
+    for (int s = 0; s < SA; ++s) {
+      mbar_init(&a_full[s], 1);
+      mbar_init(&a_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&acc_full[s], 1);
+      mbar_init(&acc_empty[s], 128);
+    }
+    mbar_init(w_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    if (lane == 0)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int NKB = p.cin / KB;
+  const uint32_t WCOL = (uint32_t)N * 16;
+
+  if (warp == 4) {
+    // ===== TMA producer: weights once, then {64 ch, 128 pixels} boxes per tile
+    if (lane == 0) {
+      mbar_arrive_expect_tx(w_full, (uint32_t)p.w_bytes);
+      for (uint32_t off = 0; off < (uint32_t)p.w_bytes; off += 32768)
+        bulk_g2s(w_base + off, p.panels + off, min(32768u, (uint32_t)p.w_bytes - off), w_full);
+      int st = 0;
+      uint32_t ph = 0;
+      for (long long t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+        const int p0 = (int)(t * p.step);
+        for (int kb = 0; kb < NKB; ++kb) {
+          mbar_wait(&a_empty[st], ph ^ 1);
+          mbar_arrive_expect_tx(&a_full[st], (uint32_t)p.stage_bytes);
+          tma_load_2d(smem_u32(a_base + (size_t)st * p.stage_bytes), &tmap, kb * KB, p0, &a_full[st]);
+          if (++st == SA) {
+            st = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 5) {
+    // ===== MMA issuer (whole warp in the loop; one elected lane issues)
+    const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base, 0);
+    const uint32_t wb = smem_u32(w_base);
+    constexpr uint32_t IDESC = idesc_f16(1, N);
+    int st = 0, acc = 0;
+    uint32_t ph = 0, pacc = 0;
+    mbar_wait(w_full, 0);
+    tc_fence_after();
+    for (long long t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+      mbar_wait(&acc_empty[acc], pacc ^ 1);
+      tc_fence_after();
+      const uint32_t d = tb + (uint32_t)(acc * N);
+      for (int kb = 0; kb < NKB; ++kb) {
+        mbar_wait(&a_full[st], ph);
+        tc_fence_after();
+        const uint64_t ad = sw128_desc(smem_u32(a_base + (size_t)st * p.stage_bytes));
+        if (!(p.debug & 8) && elect_one()) {
+#pragma unroll
+          for (int ks = 0; ks < KB / 16; ++ks) {
+            const uint64_t bd = sdesc(wb + (uint32_t)(kb * (KB / 8) + 2 * ks) * WCOL, WCOL, 128);
+            mma_f16(d, ad + 2u * ks, bd, IDESC, (kb == 0 && ks == 0) ? 0u : 1u);
+          }
+        }
+        __syncwarp();
+        if (elect_one()) mma_commit(&a_empty[st]);
+        __syncwarp();
+        if (++st == SA) {
+          st = 0;
+          ph ^= 1;
+        }
+      }
+      if (elect_one()) mma_commit(&acc_full[acc]);
+      __syncwarp();
+      if (++acc == 2) {
+        acc = 0;
+        pacc ^= 1;
+      }
+    }
+  } else {
+    // ===== epilogue (warps 0-3): TMEM row (pixel) -> SMEM tile -> per-anchor sums
+    const int m = warp * 32 + lane;  // pixel row of the tile this thread drains / anchor it sums
+    const uint32_t lane_base = tmem_base + ((uint32_t)(warp * 32) << 16);
+    float bias[COUT];
+#pragma unroll
+    for (int f = 0; f < COUT; ++f) bias[f] = (p.epi & SEGCONV_EPI_BIAS) ? __ldg(p.bias + f) : 0.0f;
+    YT* y = reinterpret_cast<YT*>(p.y);
+    const int img = p.n * p.n;
+    int acc = 0;
+    uint32_t pacc = 0;
+    for (long long t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+      mbar_wait(&acc_full[acc], pacc);
+      tc_fence_after();
+      {
+        float v[32];
+        tmem_ld32(lane_base + (uint32_t)(acc * N), v);
+#pragma unroll
+        for (int c = 0; c < 32; ++c) dtile[m * TP + c] = v[c];
+        if constexpr (N > 32) {
+          tmem_ld16(lane_base + (uint32_t)(acc * N + 32), v);
+#pragma unroll
+          for (int c = 0; c < N - 32 && c < 16; ++c) dtile[m * TP + 32 + c] = v[c];
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&acc_empty[acc]);  // D is in SMEM now; the MMA may reuse the buffer
+      if (++acc == 2) {
+        acc = 0;
+        pacc ^= 1;
+      }
+      named_bar(1, 128);
+      const long long g = t * p.step + m;  // this thread's anchor
+      if (m < p.step && g < p.Mv && !(p.debug & 1)) {
+        const int b = (int)(g / img);
+        const int rem = (int)(g - (long long)b * img);
+        const int i = rem / p.n, j = rem - (rem / p.n) * p.n;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = q >> 1, c = q & 1;
+          if (i >= p.rows[q] || j >= p.cols[q]) continue;
+          YT* o = y + (((long long)b * p.out_h + 2 * i + r) * p.out_w + 2 * j + c) * COUT;
+#pragma unroll
+          for (int f = 0; f < COUT; ++f) {
+            float s = 0.0f;
+#pragma unroll
+            for (int dy = 0; dy < U; ++dy)
+#pragma unroll
+              for (int dx = 0; dx < U; ++dx) {
+                const int col = L::col_in_group(dy, q, dx, f);
+                if (col < 0) continue;
+                s += dtile[(m + dy * p.n + dx) * TP + L::group_off(dy) + col];
+              }
+            s += bias[f];
+            if (ACT == 1) s = fmaxf(s, 0.0f);
+            if (ACT == 2) s = tanhf(s);
+            o[f] = from_f<YT>(s);
+          }
+        }
+      }
+      named_bar(1, 128);  // the tile is rewritten by the next unit
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem_base)
+                 : "memory");
+  }
+}
+
+// Weight image: rows = D columns (dy, q, dx, f), [k-chunk][N rows][8 bf16].
+template <int KH, int COUT, typename TK>
+__global__ void tile_image_kernel(const TK* __restrict__ k, int cin, SegClasses cls,
+                                  __nv_bfloat16* __restrict__ out) {
+  using L = ScatterLayout<KH, COUT>;
+  const long long total = (long long)(cin / 8) * L::N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int row = (int)(e % L::N), chunk = (int)(e / L::N);
+    int dy = 0;
+    while (dy + 1 < L::U && row >= L::group_off(dy + 1)) ++dy;
+    const int cg = row - L::group_off(dy);
+    int qq = -1, dxx = -1, ff = -1;
+    for (int q = 0; q < 4 && qq < 0; ++q)
+      for (int dx = 0; dx < L::U && qq < 0; ++dx)
+        for (int f = 0; f < COUT; ++f)
+          if (L::col_in_group(dy, q, dx, f) == cg) {
+            qq = q;
+            dxx = dx;
+            ff = f;
+            break;
+          }
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      float w = 0.0f;
+      if (qq >= 0) {
+        const int u = dy - cls.off_r[qq], v = dxx - cls.off_c[qq];
+        const int ci = chunk * 8 + x;
+        w = to_acc(k[(((long long)(cls.u0[qq] + 2 * u) * KH + (cls.v0[qq] + 2 * v)) * cin + ci) * COUT + ff]);
+      }
+      out[e * 8 + x] = __float2bfloat16_rn(w);
+    }
+  }
+}
+
+}  // namespace tct
+
+// ------------------------------------------------------------ host side
+size_t tile_image_bytes(int cin) { return (size_t)(cin / 8) * ScatterLayout<3, 3>::N * 16; }
+
+static bool tile_shape(const FusedProblem& pr) {
+  return pr.kh == 3 && pr.kw == 3 && pr.cout == 3 && pr.p == 0 && pr.pf == 0 &&
+         pr.cin % tct::KB == 0 && pr.cin <= 512 && pr.n + 1 <= 64 && pr.x_dtype == SEGCONV_BF16 &&
+         (pr.y_dtype == SEGCONV_BF16 || pr.y_dtype == SEGCONV_F32);
+}
+
+bool tc_tile_supported(const FusedProblem& pr, int math) {
+  if (math != SEGCONV_MATH_BF16 || getenv("SEGCONV_NO_TILE")) return false;
+  return tile_shape(pr);
+}
+
+cudaError_t launch_tile_image(const void* k, int k_dtype, int cin, const SegClasses& cls, void* out,
+                              cudaStream_t s) {
+  const long long total = (long long)(cin / 8) * ScatterLayout<3, 3>::N;
+  const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 1024);
+  if (k_dtype == SEGCONV_BF16)
+    tct::tile_image_kernel<3, 3, __nv_bfloat16><<<blocks, 256, 0, s>>>(
+        (const __nv_bfloat16*)k, cin, cls, (__nv_bfloat16*)out);
+  else if (k_dtype == SEGCONV_F32)
+    tct::tile_image_kernel<3, 3, float><<<blocks, 256, 0, s>>>((const float*)k, cin, cls,
+                                                               (__nv_bfloat16*)out);
+  else
+    return cudaErrorNotSupported;
+  note_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tc_tile(const FusedProblem& pr, const void* img, cudaStream_t s) {
+  if (!tile_shape(pr)) return cudaErrorNotSupported;
+  using L = ScatterLayout<3, 3>;
+  tct::Params p{};
+  p.panels = (const uint8_t*)img;
+  p.y = pr.y;
+  p.bias = pr.bias;
+  p.epi = pr.epi;
+  p.batch = pr.batch;
+  p.n = pr.n;
+  p.cin = pr.cin;
+  p.cout = pr.cout;
+  p.out_h = pr.out_h;
+  p.out_w = pr.out_w;
+  for (int q = 0; q < 4; ++q) {
+    p.rows[q] = pr.cls.rows[q];
+    p.cols[q] = pr.cls.cols[q];
+  }
+  p.Mv = (long long)pr.batch * pr.n * pr.n;
+  p.step = tct::TILE - (pr.n + 1);
+  p.tiles = (p.Mv + p.step - 1) / p.step;
+  if (p.tiles == 0) return cudaSuccess;
+  p.stage_bytes = tct::TILE * 128;
+  p.w_bytes = (int)tile_image_bytes(pr.cin);
+  const int fixed = p.w_bytes + (tct::TILE * (L::N + 1) + 2) * 4 + (2 * tct::MAX_STAGES + 5) * 8 + 16;
+  p.stages = std::min(tct::MAX_STAGES, (tct::SMEM_LIMIT - fixed) / p.stage_bytes);
+  if (p.stages < 2) return cudaErrorNotSupported;
+  static const int dbg = getenv("SEGCONV_TC_DEBUG") ? atoi(getenv("SEGCONV_TC_DEBUG")) : 0;
+  p.debug = dbg;
+  p.trace = nullptr;
+  typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                          const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                          CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                          CUtensorMapFloatOOBfill);
+  static Enc enc = nullptr;
+  if (!enc) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return cudaErrorNotSupported;
+    enc = (Enc)f;
+  }
+  CUtensorMap tmap;
+  const cuuint64_t dims[2] = {(cuuint64_t)pr.cin, (cuuint64_t)p.Mv};
+  const cuuint64_t strides[1] = {(cuuint64_t)pr.cin * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)tct::KB, (cuuint32_t)tct::TILE};
+  const cuuint32_t es[2] = {1, 1};
+  if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pr.x), dims, strides, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorNotSupported;
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+  }
+  const long long grid = std::min<long long>(p.tiles, sms);
+  const size_t smem = (size_t)p.stages * p.stage_bytes + fixed;
+  const int act = (pr.epi & SEGCONV_EPI_RELU) ? 1 : (pr.epi & SEGCONV_EPI_TANH) ? 2 : 0;
+  cudaError_t e = cudaSuccess;
+#define TILE_LAUNCH(A, YT)                                                                       \
+  {                                                                                              \
+    auto kern = tct::tile_kernel<3, 3, A, YT>;                                                   \
+    static bool cfg = false;                                                                     \
+    if (!cfg) {                                                                                  \
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tct::SMEM_LIMIT); \
+      if (e != cudaSuccess) return e;                                                            \
+      cfg = true;                                                                                \
+    }                                                                                            \
+    kern<<<(unsigned)grid, tct::NUM_THREADS, smem, s>>>(p, tmap);                                \
+  }
+  if (pr.y_dtype == SEGCONV_BF16) {
+    if (act == 1)
+      TILE_LAUNCH(1, __nv_bfloat16)
+    else if (act == 2)
+      TILE_LAUNCH(2, __nv_bfloat16)
+    else
+      TILE_LAUNCH(0, __nv_bfloat16)
+  } else {
+    if (act == 1)
+      TILE_LAUNCH(1, float)
+    else if (act == 2)
+      TILE_LAUNCH(2, float)
+    else
+      TILE_LAUNCH(0, float)
+  }
+#undef TILE_LAUNCH
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace segconv_b200
