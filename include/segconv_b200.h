@@ -199,6 +199,10 @@ segconv_status segconv_count_ops(int n_in, int cin, int cout, int kh, int kw, in
 
 /* ------------------------------------------------------------ diagnostics */
 const char* segconv_last_error(void);
+/* Kernel family the last segconv_transpose_conv_fused call on this thread ran
+ * ("tc-fold-ts", "tc-pair", "tc-ring", "tc-tile", "tc-fold", "tc-halo",
+ * "simt-tiled", "simt-generic", "simt-exact"). */
+const char* segconv_last_path(void);
 const char* segconv_version(void);
 /* Number of kernels this library launched since load (all entry points). */
 uint64_t segconv_launch_count(void);

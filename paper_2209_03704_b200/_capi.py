@@ -67,6 +67,7 @@ SIGNATURES = {
                                           _vp, _u, _vp, _vp]),
     "segconv_count_ops": (_i, [_i, _i, _i, _i, _i, _i, C.POINTER(C.c_uint64)]),
     "segconv_last_error": (C.c_char_p, []),
+    "segconv_last_path": (C.c_char_p, []),
     "segconv_version": (C.c_char_p, []),
     "segconv_launch_count": (C.c_uint64, []),
     "segconv_debug_trace": (_sz, [_vp, _sz]),

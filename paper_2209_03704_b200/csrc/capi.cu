@@ -20,6 +20,7 @@ static std::atomic<uint64_t> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
 static thread_local std::string g_err;
+static thread_local const char* g_path = "";  // kernel family of the last fused call
 
 static segconv_status fail(segconv_status st, const char* fmt, ...) {
   char buf[512];
@@ -82,6 +83,7 @@ using namespace segconv_b200;
 extern "C" {
 
 const char* segconv_last_error(void) { return g_err.c_str(); }
+const char* segconv_last_path(void) { return g_path; }
 const char* segconv_version(void) { return "segconv_b200 0.1 (sm_100a)"; }
 uint64_t segconv_launch_count(void) { return g_launches.load(); }
 
@@ -385,14 +387,17 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
     case SEGCONV_MATH_EXACT:
       if (sks->layout != SEGCONV_PANEL_REF)
         return fail(SEGCONV_E_CONTRACT, "EXACT math needs reference-layout panels");
+      g_path = "simt-exact";
       return cuda_status(launch_direct_generic(pr, true, s), "transpose_conv_fused[exact]");
     case SEGCONV_MATH_FFMA: {
       if (sks->layout != SEGCONV_PANEL_REF)
         return fail(SEGCONV_E_CONTRACT, "FFMA math needs reference-layout panels");
       if (x_dtype != SEGCONV_F64 && sks->dtype != SEGCONV_F64) {
+        g_path = "simt-tiled";
         cudaError_t e = launch_direct_tiled(pr, s);
         if (e != cudaErrorNotSupported) return cuda_status(e, "transpose_conv_fused[ffma]");
       }
+      g_path = "simt-generic";
       return cuda_status(launch_direct_generic(pr, false, s), "transpose_conv_fused[ffma]");
     }
     case SEGCONV_MATH_BF16:
@@ -405,6 +410,7 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
           return fail(SEGCONV_E_UNSUPPORTED,
                       "CTA-pair tensor-core path needs bf16 activations, cin %% 64 == 0, cout >= 64, "
                       "p_fused == 0 and a halo of <= 256 rows");
+        g_path = "tc-pair";
         return cuda_status(launch_tc_wide(pr, s), "transpose_conv_fused[tcgen05 pair]");
       }
       if (sks->layout != SEGCONV_PANEL_UMMA && sks->layout != SEGCONV_PANEL_UMMA_FOLD)
@@ -417,14 +423,15 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
           return fail(SEGCONV_E_UNSUPPORTED,
                       "class-folded tensor-core path: needs p_fused == 0, cin a multiple of the "
                       "channel block and a halo that fits shared memory");
-        if (sks->total_elems > fold_image_elems(*sks) && tc_tile_supported(pr, math))
+        if (sks->total_elems > fold_image_elems(*sks) && tc_tile_supported(pr, math) && (g_path = "tc-tile"))
           return cuda_status(launch_tc_tile(pr, (const uint16_t*)d_panels + fold_image_elems(*sks), s),
                              "transpose_conv_fused[tcgen05 tile]");
-        if (sks->total_elems > fold_image_elems(*sks) && tc_ring_supported(pr, math))
+        if (sks->total_elems > fold_image_elems(*sks) && tc_ring_supported(pr, math) && (g_path = "tc-ring"))
           return cuda_status(launch_tc_ring(pr, (const uint16_t*)d_panels + fold_image_elems(*sks), s),
                              "transpose_conv_fused[tcgen05 ring]");
-        if (tc_fold_ts_supported(pr, math))
+        if (tc_fold_ts_supported(pr, math) && (g_path = "tc-fold-ts"))
           return cuda_status(launch_tc_fold_ts(pr, s), "transpose_conv_fused[tcgen05 fold-ts]");
+        g_path = "tc-fold";
         return cuda_status(launch_tc_fold(pr, math, s), "transpose_conv_fused[tcgen05 fold]");
       }
       if (!tc_igemm_supported(pr, math))
@@ -432,6 +439,7 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
                     "tensor-core path needs %s activations, cin %% 8 == 0, taps in every parity "
                     "class and a halo that fits shared memory",
                     math == SEGCONV_MATH_BF16 ? "bf16" : "fp32");
+      g_path = "tc-halo";
       return cuda_status(launch_tc_igemm(pr, math, s), "transpose_conv_fused[tcgen05]");
     }
     default:

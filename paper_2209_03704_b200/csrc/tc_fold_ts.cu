@@ -492,7 +492,7 @@ static bool make_fold_ts_params(const FusedProblem& pr, tcfs::Params& p) {
   if (p.w_img_bytes > stage_area) return false;
   p.w_stage0 = (stage_area - p.w_img_bytes) / p.stage_bytes;  // first stage the staging covers
   // the staging starts inside stage w_stage0; keep it 16-byte aligned at its start
-  if (p.w_stage0 < 2) return false;
+  if (p.w_stage0 < 1) return false;
   for (int q = 0; q < 4; ++q) {
     p.rows[q] = pr.cls.rows[q];
     p.cols[q] = pr.cls.cols[q];

@@ -28,7 +28,7 @@ __all__ = [
     "class_input_offset", "sub_kernel_dims", "SubKernelSet", "segregate", "transpose_conv_fused",
     "transpose_conv_fused_parallel", "transpose_conv_naive", "conv2d_valid", "upsample2x_pad",
     "tensors_equal_exact", "tensors_equal_approx", "LayerShape", "OpCounts", "count_ops_naive",
-    "count_ops_fused", "select_math", "launch_count", "MATHS",
+    "count_ops_fused", "select_math", "launch_count", "last_path", "MATHS",
 ]
 
 
@@ -228,6 +228,11 @@ class SubKernelSet:
     @property
     def subs(self):
         return [self.sub(q >> 1, q & 1) for q in range(4)]
+
+
+def last_path() -> str:
+    """Kernel family the last transpose_conv_fused call on this thread ran."""
+    return (A.lib().segconv_last_path() or b"").decode()
 
 
 def select_math(x_dtype: torch.dtype, panel_dtype: torch.dtype, cin: int, cout: int, kh: int,

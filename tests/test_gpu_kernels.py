@@ -1,0 +1,132 @@
+"""Per-kernel-family GPU parity: each tcgen05 kernel the dispatcher picks is
+exercised at small sizes (ragged batches, partial tiles, tile/segment edges,
+fused epilogues) against the C oracle, and the test asserts which kernel ran
+(segconv_last_path).
+
+Bars: split-fp16 math on fp32 data -> the reference's
+tensors_equal_approx at 1e-5; bf16 operand paths -> 1e-2 (the oracle sees the
+same bf16-rounded inputs, so the remaining difference is fp32 summation order,
+<= 1e-4 here, plus bf16 output rounding where the output is bf16).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2209_03704_b200 import segconv as sc
+
+pytestmark = pytest.mark.gpu
+TOL_F32 = 1e-5
+TOL_TC = 1e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+
+
+def scaled_err(got, want):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    assert got.shape == want.shape
+    return float((np.abs(got - want) / np.maximum(np.maximum(np.abs(got), np.abs(want)), 1.0)).max())
+
+
+def run(x, k, p, math, act=None, bias=None, out_dtype=None):
+    dt = torch.bfloat16 if math == "bf16" else torch.float32
+    g = sc.tconv_geometry(x.shape[1], k.shape[0], k.shape[1], p)
+    sks = sc.segregate(torch.from_numpy(k).cuda().to(dt), p, math=math)
+    bt = torch.from_numpy(bias).cuda() if bias is not None else None
+    y = sc.transpose_conv_fused(torch.from_numpy(x).cuda().to(dt), sks, g, activation=act, bias=bt,
+                                out_dtype=out_dtype)
+    torch.cuda.synchronize()
+    return y.float().cpu().numpy(), sc.last_path()
+
+
+def want_of(x, k, p, act=None, bias=None):
+    w = oracle.tconv_fused(x, k, p)
+    if bias is not None:
+        w = w + bias
+    if act == "relu":
+        w = np.maximum(w, 0)
+    if act == "tanh":
+        w = np.tanh(w)
+    return w
+
+
+# ---- fp32 64 -> 32, 3x3 (BASELINE C2 family): TMEM-weight fold kernel
+@pytest.mark.parametrize("batch,n,act", [(1, 64, None), (3, 64, "relu"), (2, 40, "tanh"), (5, 17, None)])
+def test_fold_ts_split_fp16(batch, n, act):
+    rng = np.random.default_rng(batch * 100 + n)
+    x = rng.uniform(-1, 1, (batch, n, n, 64)).astype(np.float32)
+    k = (rng.standard_normal((3, 3, 64, 32)) * 0.059).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, 32).astype(np.float32) if act else None
+    got, path = run(x, k, 0, "f16x3", act, b)
+    assert path == "tc-fold-ts"
+    assert scaled_err(got, want_of(x, k, 0, act, b)) <= TOL_F32
+
+
+# ---- wide bf16 layers (C3, C5 a-c): CTA-pair kernel
+@pytest.mark.parametrize("batch,n,cin,cout,ks,act", [
+    (4, 16, 512, 256, 4, None),   # C3 shape (reduced batch)
+    (3, 4, 1024, 512, 3, "relu"),  # C5 layer a: two feature tiles, tiny images
+    (2, 7, 256, 128, 3, "relu"),   # C5 layer c
+    (5, 5, 512, 256, 3, None),     # odd image, partial pair tile
+    (2, 9, 64, 96, 4, "tanh"),     # cout not a multiple of 64, single k-block
+])
+def test_pair_kernel_bf16(batch, n, cin, cout, ks, act):
+    rng = np.random.default_rng(batch * 7 + n + cin)
+    x = oracle.bf16_round(rng.standard_normal((batch, n, n, cin)).astype(np.float32))
+    k = oracle.bf16_round((rng.standard_normal((ks, ks, cin, cout)) * 0.02).astype(np.float32))
+    got, path = run(x, k, 0, "bf16", act, out_dtype=torch.float32)
+    assert path == "tc-pair"
+    assert scaled_err(got, want_of(x, k, 0, act)) <= 1e-4  # fp32 accumulate; bar is 1e-2
+
+
+def test_pair_kernel_bf16_output():
+    rng = np.random.default_rng(5)
+    x = oracle.bf16_round(rng.standard_normal((2, 16, 16, 128)).astype(np.float32))
+    k = oracle.bf16_round((rng.standard_normal((4, 4, 128, 64)) * 0.02).astype(np.float32))
+    got, path = run(x, k, 0, "bf16")
+    assert path == "tc-pair"
+    assert scaled_err(got, want_of(x, k, 0)) <= TOL_TC
+
+
+# ---- high-resolution 5x5 -> 3 fp32 (C4 family): pixel-scatter row-ring kernel
+@pytest.mark.parametrize("batch,n,cin,act,bias", [(1, 128, 64, None, False), (2, 128, 64, "tanh", True),
+                                                  (3, 256, 32, None, False), (1, 256, 64, "tanh", False)])
+def test_ring_kernel(batch, n, cin, act, bias):
+    rng = np.random.default_rng(batch * 13 + n + cin)
+    x = rng.uniform(-1, 1, (batch, n, n, cin)).astype(np.float32)
+    k = (rng.standard_normal((5, 5, cin, 3)) * 0.02).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, 3).astype(np.float32) if bias else None
+    got, path = run(x, k, 0, "f16x3", act, b)
+    assert path == "tc-ring"
+    assert scaled_err(got, want_of(x, k, 0, act, b)) <= TOL_F32
+
+
+def test_ring_falls_back_for_other_sizes():
+    """The row ring needs 128- or 256-pixel rows; other sizes take the folded kernel."""
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, (2, 40, 40, 64)).astype(np.float32)
+    k = (rng.standard_normal((5, 5, 64, 3)) * 0.02).astype(np.float32)
+    got, path = run(x, k, 0, "f16x3")
+    assert path == "tc-fold"
+    assert scaled_err(got, want_of(x, k, 0)) <= TOL_F32
+
+
+# ---- small-image 3x3 -> 3 bf16 (C5 layer d family): pixel-scatter tile kernel
+@pytest.mark.parametrize("batch,n,cin,act,odt", [(4, 11, 128, "tanh", torch.float32),
+                                                 (3, 7, 64, None, torch.float32),
+                                                 (7, 11, 128, "tanh", torch.bfloat16),
+                                                 (2, 30, 192, None, torch.float32),
+                                                 (1, 3, 64, "relu", torch.float32)])
+def test_tile_kernel(batch, n, cin, act, odt):
+    rng = np.random.default_rng(batch * 17 + n + cin)
+    x = oracle.bf16_round(rng.standard_normal((batch, n, n, cin)).astype(np.float32))
+    k = oracle.bf16_round((rng.standard_normal((3, 3, cin, 3)) * 0.02).astype(np.float32))
+    got, path = run(x, k, 0, "bf16", act, out_dtype=odt)
+    assert path == "tc-tile"
+    tol = 1e-4 if odt == torch.float32 else TOL_TC
+    assert scaled_err(got, want_of(x, k, 0, act)) <= tol
