@@ -418,7 +418,7 @@ def main():
     # overhead (ctypes, argument checks) is not on the device clock; the e2e
     # leg below goes through the public Python API eagerly.
     graph = None
-    if not cfg.get("stack"):
+    if not cfg.get("stack") and not os.environ.get("SEGCONV_BENCH_EAGER"):
         side = torch.cuda.Stream()
         side.wait_stream(stream)
         with torch.cuda.stream(side):

@@ -136,9 +136,11 @@ __device__ __forceinline__ void load_halo(float* xs, const TX* __restrict__ x, i
                                           int cin, int gr0, int gc0, int ci0, int tid,
                                           int nthr) {
   constexpr int PIX = TH * TW;
-  for (int idx = tid; idx < PIX * CI; idx += nthr) {
-    const int ch = idx % CI;
-    const int pix = idx / CI;
+  // only the channels that exist (a 1-channel layer loads 1/CI of the tile)
+  const int nch = min(CI, cin - ci0);
+  for (int idx = tid; idx < PIX * nch; idx += nthr) {
+    const int ch = idx % nch;
+    const int pix = idx / nch;
     const int row = pix / TW, col = pix - (pix / TW) * TW;
     const int gr = gr0 + row, gc = gc0 + col, gch = ci0 + ch;
     float v = 0.0f;
@@ -156,7 +158,8 @@ __device__ __forceinline__ void load_weights(float* ws, const TW* __restrict__ p
                                              int f0, int tid, int nthr) {
   using P = Par<K, PODD>;
   constexpr int TAPS = P::TAPS;
-  for (int idx = tid; idx < CI * TAPS * FW; idx += nthr) {
+  const int nch = min(CI, cin - ci0);
+  for (int idx = tid; idx < nch * TAPS * FW; idx += nthr) {
     const int fl = idx % FW;
     const int t = (idx / FW) % TAPS;
     const int ch = idx / (FW * TAPS);
@@ -432,9 +435,60 @@ static cudaError_t run_tiled_t(const FusedProblem& pr, cudaStream_t s) {
 #undef KC
 }
 
+// ------------------------------------------------------------ tiny layers
+// One thread per output element (b, oy, ox, f): class (oy & 1, ox & 1),
+// anchor (oy >> 1, ox >> 1), dot over the class's taps and channels in the
+// reference order (u, v, ch).  For layers whose whole work is a few thousand
+// MACs (BASELINE C1: 1 x 32^2 x 1 -> 61^2 x 1) the tiled kernels' staging
+// is pure latency; this is one global read per tap.
+template <typename TX, typename TW>
+__global__ void __launch_bounds__(256) tconv_outputs(const FusedProblem pr, long long total) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= total) return;
+  const int f = (int)(e % pr.cout);
+  long long t = e / pr.cout;
+  const int ox = (int)(t % pr.out_w);
+  t /= pr.out_w;
+  const int oy = (int)(t % pr.out_h);
+  const int b = (int)(t / pr.out_h);
+  const int r = oy & 1, c = ox & 1, q = r * 2 + c, i = oy >> 1, j = ox >> 1;
+  const TX* __restrict__ x = (const TX*)pr.x;
+  const TW* __restrict__ w = (const TW*)pr.panels + pr.cls.sub_offset[q];
+  const int kw = pr.cls.kw[q];
+  float acc = 0.0f;
+  for (int u = 0; u < pr.cls.kh[q]; ++u) {
+    const int gr = i + pr.cls.off_r[q] + u - pr.pf;
+    for (int v = 0; v < kw; ++v) {
+      const int gc = j + pr.cls.off_c[q] + v - pr.pf;
+      if (gr < 0 || gr >= pr.n || gc < 0 || gc >= pr.n) continue;  // zero padding
+      const TX* xp = x + (((long long)b * pr.n + gr) * pr.n + gc) * pr.cin;
+      const TW* wp = w + ((long long)(u * kw + v) * pr.cin) * pr.cout + f;
+      for (int ch = 0; ch < pr.cin; ++ch) acc = fmaf(to_acc(xp[ch]), to_acc(wp[(long long)ch * pr.cout]), acc);
+    }
+  }
+  store_out(pr.y, e, epilogue_apply(acc, pr.epi, pr.bias, f), pr.y_dtype);
+}
+
+static bool tiny_layer(const FusedProblem& pr) {
+  const long long outs = (long long)pr.batch * pr.out_h * pr.out_w * pr.cout;
+  return outs <= (1 << 16) && (long long)pr.kh * pr.kw * pr.cin <= 64;
+}
+
 cudaError_t launch_direct_tiled(const FusedProblem& pr, cudaStream_t s) {
   if (pr.kh != pr.kw || pr.kh < 1 || pr.kh > 7) return cudaErrorNotSupported;
   if (pr.panel_layout != SEGCONV_PANEL_REF) return cudaErrorNotSupported;
+  if (tiny_layer(pr) && ((pr.x_dtype == SEGCONV_F32 && pr.panel_dtype == SEGCONV_F32) ||
+                         (pr.x_dtype == SEGCONV_BF16 && pr.panel_dtype == SEGCONV_BF16))) {
+    const long long total = (long long)pr.batch * pr.out_h * pr.out_w * pr.cout;
+    if (total == 0) return cudaSuccess;
+    const unsigned blocks = (unsigned)((total + 255) / 256);
+    if (pr.x_dtype == SEGCONV_F32)
+      tconv_outputs<float, float><<<blocks, 256, 0, s>>>(pr, total);
+    else
+      tconv_outputs<__nv_bfloat16, __nv_bfloat16><<<blocks, 256, 0, s>>>(pr, total);
+    note_launch();
+    return cudaGetLastError();
+  }
   if (pr.x_dtype == SEGCONV_F32 && pr.panel_dtype == SEGCONV_F32)
     return run_tiled_t<float, float>(pr, s);
   if (pr.x_dtype == SEGCONV_BF16 && pr.panel_dtype == SEGCONV_BF16)
