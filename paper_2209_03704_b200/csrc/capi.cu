@@ -193,6 +193,10 @@ segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_
     // bf16 3x3 -> 3-channel layers carry the small-image pixel-scatter image (tc_tile.cu)
     if (tile_panels_apply(kh, kw, cin, cout, p_orig, panel_dtype))
       s.total_elems += (int64_t)(tile_image_bytes(cin) / 2);
+    // split-fp16 layers with 4 classes x 32 features: compact weight image of
+    // the TMEM-weight kernel (tc_fold_ts.cu), only the blocks that hold taps
+    if (fold_ts_panels_apply(kh, kw, cin, cout, p_orig, panel_dtype))
+      s.total_elems += (int64_t)(fold_ts_image_bytes_for(kh, kw, cin, p_orig) / 2);
   }
   if (layout == SEGCONV_PANEL_UMMA) {
     s.n_tile = tc_n_tile(s.math, cout);
@@ -279,13 +283,20 @@ segconv_status segconv_segregate(const void* d_kernel, segconv_dtype kernel_dtyp
         "segregate[fold]");
     if (st == SEGCONV_OK && sks->total_elems > fold_image_elems(*sks)) {
       uint16_t* tail = (uint16_t*)d_panels + fold_image_elems(*sks);
-      st = sks->dtype == SEGCONV_F16_SPLIT
-               ? cuda_status(launch_ring_image(d_kernel, kernel_dtype, sks->cin, cls, tail,
-                                               (cudaStream_t)stream),
-                             "segregate[ring]")
-               : cuda_status(launch_tile_image(d_kernel, kernel_dtype, sks->cin, cls, tail,
-                                               (cudaStream_t)stream),
-                             "segregate[tile]");
+      if (fold_ts_panels_apply(sks->source_kh, sks->source_kw, sks->cin, sks->cout, sks->p_orig,
+                               sks->dtype))
+        st = cuda_status(launch_fold_ts_image(d_kernel, kernel_dtype, sks->source_kh,
+                                              sks->source_kw, sks->cin, sks->cout, sks->p_orig,
+                                              cls, tail, (cudaStream_t)stream),
+                         "segregate[fold-ts]");
+      else if (sks->dtype == SEGCONV_F16_SPLIT)
+        st = cuda_status(launch_ring_image(d_kernel, kernel_dtype, sks->cin, cls, tail,
+                                           (cudaStream_t)stream),
+                         "segregate[ring]");
+      else
+        st = cuda_status(launch_tile_image(d_kernel, kernel_dtype, sks->cin, cls, tail,
+                                           (cudaStream_t)stream),
+                         "segregate[tile]");
     }
     return st;
   }
@@ -429,8 +440,13 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
         if (sks->total_elems > fold_image_elems(*sks) && tc_ring_supported(pr, math) && (g_path = "tc-ring"))
           return cuda_status(launch_tc_ring(pr, (const uint16_t*)d_panels + fold_image_elems(*sks), s),
                              "transpose_conv_fused[tcgen05 ring]");
-        if (tc_fold_ts_supported(pr, math) && (g_path = "tc-fold-ts"))
-          return cuda_status(launch_tc_fold_ts(pr, s), "transpose_conv_fused[tcgen05 fold-ts]");
+        if (sks->total_elems > fold_image_elems(*sks) &&
+            fold_ts_panels_apply(sks->source_kh, sks->source_kw, sks->cin, sks->cout, sks->p_orig,
+                                 sks->dtype) &&
+            tc_fold_ts_supported(pr, math) && (g_path = "tc-fold-ts"))
+          return cuda_status(
+              launch_tc_fold_ts(pr, (const uint16_t*)d_panels + fold_image_elems(*sks), s),
+              "transpose_conv_fused[tcgen05 fold-ts]");
         g_path = "tc-fold";
         return cuda_status(launch_tc_fold(pr, math, s), "transpose_conv_fused[tcgen05 fold]");
       }

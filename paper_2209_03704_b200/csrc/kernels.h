@@ -61,7 +61,11 @@ cudaError_t launch_tile_image(const void* k, int k_dtype, int cin, const SegClas
                               cudaStream_t s);
 size_t tile_image_bytes(int cin);
 // TMEM-weights variant for split-fp16 layers with cout in (16, 32] (tc_fold_ts.cu)
-cudaError_t launch_tc_fold_ts(const FusedProblem& pr, cudaStream_t s);
+cudaError_t launch_tc_fold_ts(const FusedProblem& pr, const void* img, cudaStream_t s);
+bool fold_ts_panels_apply(int kh, int kw, int cin, int cout, int p_orig, int panel_dtype);
+size_t fold_ts_image_bytes_for(int kh, int kw, int cin, int p_orig);
+cudaError_t launch_fold_ts_image(const void* k, int k_dtype, int kh, int kw, int cin, int cout,
+                                 int p_orig, const SegClasses& cls, void* out, cudaStream_t s);
 bool tc_fold_ts_supported(const FusedProblem& pr, int math);
 bool tc_fold_available(int math, int cin, int cout);
 bool tc_fold_fits(int math, int kh, int kw, int p, int cin, int cout);

@@ -65,7 +65,9 @@ struct Params {
   int nkb_img, kb_img;  // channel blocking of the panel image
   long long Mv;         // batch * n * n virtual positions
   int S_pad;            // rows per k-chunk column of a stage (= TMA box rows)
-  int stage_bytes, w_img_bytes, w_rows, w_stage0;
+  int stage_bytes, w_img_bytes, w_stage0;
+  int nblk;              // non-zero (shift, class) blocks of the compact weight image
+  int blk_of[MAX_SHIFTS][4];  // block index of (shift, class), -1: no tap (zeros)
   int shifts, max_shift;
   int shift_off[MAX_SHIFTS];
   int rows[4], cols[4];
@@ -184,7 +186,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int NKB = p.cin / KB;                   // stages per unit
   const int KS = p.cin / 16;                    // K=16 steps over cin
   const uint32_t COL = (uint32_t)p.S_pad * 16;  // one k-chunk column (one plane)
-  const uint32_t WCOL = (uint32_t)p.w_rows * 16;
   const uint32_t w_stage_addr = smem_u32(smem) + (uint32_t)p.w_stage0 * p.stage_bytes;
 
   if (warp == 13) {
@@ -199,8 +200,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int nu;
       for (int k = 0; next_unit(p, k, m0, nu); ++k) {
         for (int h = 0; h < NKB; ++h) {
-          if (!weights_issued && st == p.w_stage0) {
-            // the first unit's halo is queued ahead of the weight image
+          if (!weights_issued) {
+            // the (compact) weight image is queued first: no MMA can start before it
             weights_issued = true;
             issue_weights(p, smem, w_full);
           }
@@ -346,28 +347,35 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = warp & 3, half = warp >> 2, r = q >> 1, c = q & 1, f = lane;
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
     {
-      // weights: staged image [plane][k-block][k-chunk][shift * 128 + row][16 B]
-      // -> TMEM columns ((shift * 2 + plane) * KS + ks) * 8 of this thread's
-      // row; the quadrant's two warps take one plane each
+      // weights: staged compact image [plane][k-chunk][block][32 rows][16 B]
+      // (only the (shift, class) blocks that hold taps) -> TMEM columns
+      // ((shift * 2 + plane) * KS + ks) * 8 of this thread's row, zeros for
+      // the classes a shift does not touch; the quadrant's two warps take one
+      // plane each
       mbar_wait(w_full, 0);
       if (threadIdx.x == 0) trace_ev(p, 6, 0);
-      const int row = q * 32 + lane, pl = half;
-      const int cpk = p.kb_img / 8;
-      for (int s = 0; s < p.shifts; ++s)
+      const int pl = half, CHT = p.cin / 8;
+      for (int s = 0; s < p.shifts; ++s) {
+        const int blk = p.blk_of[s][q];
         for (int ks = 0; ks < KS; ++ks) {
           uint32_t rr[8];
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            const int J = 2 * ks + hh, kbi = J / cpk, j = J - kbi * cpk;
-            const uint32_t src = w_stage_addr + ((uint32_t)(pl * p.nkb_img + kbi) * cpk + j) * WCOL +
-                                 (uint32_t)(s * 128 + row) * 16;
-            asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(rr[4 * hh]), "=r"(rr[4 * hh + 1]), "=r"(rr[4 * hh + 2]),
-                           "=r"(rr[4 * hh + 3])
-                         : "r"(src));
+            const int J = 2 * ks + hh;
+            if (blk >= 0) {
+              const uint32_t src = w_stage_addr +
+                                   (((uint32_t)(pl * CHT + J) * p.nblk + blk) * 32 + lane) * 16;
+              asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(rr[4 * hh]), "=r"(rr[4 * hh + 1]), "=r"(rr[4 * hh + 2]),
+                             "=r"(rr[4 * hh + 3])
+                           : "r"(src));
+            } else {
+              rr[4 * hh] = rr[4 * hh + 1] = rr[4 * hh + 2] = rr[4 * hh + 3] = 0u;
+            }
           }
           tmem_st8(lane_base + A_COL + (uint32_t)(((s * 2 + pl) * KS + ks) * 8), rr);
         }
+      }
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(w_free);
@@ -455,6 +463,110 @@ static EncodeTiledFnTS encode_fn_ts() {
   return fn;
 }
 
+// (shift, class) blocks of the compact weight image, shift-major.
+static int fold_ts_blocks(const SegClasses& cls, int ur, int uc, int (*blk_of)[4]) {
+  int nb = 0;
+  for (int dy = 0; dy < ur; ++dy)
+    for (int dx = 0; dx < uc; ++dx)
+      for (int q = 0; q < 4; ++q) {
+        const int u = dy - cls.off_r[q], v = dx - cls.off_c[q];
+        const bool tap = u >= 0 && u < cls.kh[q] && v >= 0 && v < cls.kw[q];
+        if (blk_of) blk_of[dy * uc + dx][q] = tap ? nb : -1;
+        nb += tap ? 1 : 0;
+      }
+  return nb;
+}
+size_t fold_ts_image_bytes(int cin, int nblk) { return (size_t)2 * (cin / 8) * nblk * 32 * 16; }
+
+// Compact image: [plane hi/lo][k-chunk][block (shift, class)][32 rows f][8 fp16].
+__global__ void fold_ts_image_kernel(const float* __restrict__ k, int kw, int cin, int cout,
+                                     SegClasses cls, int ur, int uc, uint16_t* __restrict__ out,
+                                     long long total) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int f = (int)(e % 32);
+    const long long t = e / 32;
+    // decode (chunk, block): total = CHT * nblk * 32, blocks enumerated on the fly
+    int nb = 0;
+    for (int dy = 0; dy < ur; ++dy)
+      for (int dx = 0; dx < uc; ++dx)
+        for (int q = 0; q < 4; ++q) {
+          const int u = dy - cls.off_r[q], v = dx - cls.off_c[q];
+          if (u >= 0 && u < cls.kh[q] && v >= 0 && v < cls.kw[q]) ++nb;
+        }
+    const int blk = (int)(t % nb);
+    const int J = (int)(t / nb);
+    int b = 0, qq = 0, uu = 0, vv = 0;
+    for (int dy = 0; dy < ur; ++dy)
+      for (int dx = 0; dx < uc; ++dx)
+        for (int q = 0; q < 4; ++q) {
+          const int u = dy - cls.off_r[q], v = dx - cls.off_c[q];
+          if (u >= 0 && u < cls.kh[q] && v >= 0 && v < cls.kw[q]) {
+            if (b == blk) {
+              qq = q;
+              uu = u;
+              vv = v;
+            }
+            ++b;
+          }
+        }
+    uint16_t hi[8], lo[8];
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      const int ci = J * 8 + x;
+      float w = 0.0f;
+      if (f < cout)
+        w = k[(((long long)(cls.u0[qq] + 2 * uu) * kw + (cls.v0[qq] + 2 * vv)) * cin + ci) * cout + f];
+      const __half h = __float2half_rn(w);
+      hi[x] = __half_as_ushort(h);
+      lo[x] = __half_as_ushort(__float2half_rn(w - __half2float(h)));
+    }
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      out[e * 8 + x] = hi[x];
+      out[total * 8 + e * 8 + x] = lo[x];
+    }
+  }
+}
+
+cudaError_t launch_fold_ts_image(const void* k, int k_dtype, int kh, int kw, int cin, int cout,
+                                 int p_orig, const SegClasses& cls, void* out, cudaStream_t s) {
+  if (k_dtype != SEGCONV_F32) return cudaErrorNotSupported;
+  int ur, uc;
+  fold_window(kh, kw, p_orig, &ur, &uc);
+  const int nb = fold_ts_blocks(cls, ur, uc, nullptr);
+  const long long total = (long long)(cin / 8) * nb * 32;
+  const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 1024);
+  fold_ts_image_kernel<<<blocks, 256, 0, s>>>((const float*)k, kw, cin, cout, cls, ur, uc,
+                                               (uint16_t*)out, total);
+  note_launch();
+  return cudaGetLastError();
+}
+
+// Whether split-fp16 folded panels of this shape carry the compact image.
+bool fold_ts_panels_apply(int kh, int kw, int cin, int cout, int p_orig, int panel_dtype) {
+  if (panel_dtype != SEGCONV_F16_SPLIT || fold_cp(cout) != 32 || p_orig / 2 != 0) return false;
+  if (cin % 32 != 0) return false;
+  int ur, uc;
+  fold_window(kh, kw, p_orig, &ur, &uc);
+  return ur * uc == 4 && ur * uc * cin <= 256;
+}
+size_t fold_ts_image_bytes_for(int kh, int kw, int cin, int p_orig) {
+  // block count from the parity geometry alone (mirrors segconv_subkernels_init)
+  SegClasses c{};
+  for (int q = 0; q < 4; ++q) {
+    const int r = q >> 1, cc = q & 1;
+    const int u0 = (p_orig + r) & 1, v0 = (p_orig + cc) & 1;
+    c.kh[q] = u0 >= kh ? 0 : (kh - u0 + 1) / 2;
+    c.kw[q] = v0 >= kw ? 0 : (kw - v0 + 1) / 2;
+    c.off_r[q] = (r + u0 - p_orig) / 2 + p_orig / 2;
+    c.off_c[q] = (cc + v0 - p_orig) / 2 + p_orig / 2;
+  }
+  int ur, uc;
+  fold_window(kh, kw, p_orig, &ur, &uc);
+  return fold_ts_image_bytes(cin, fold_ts_blocks(c, ur, uc, nullptr));
+}
+
 static bool make_fold_ts_params(const FusedProblem& pr, tcfs::Params& p) {
   p = tcfs::Params{};
   if (pr.pf != 0 || pr.x_dtype != SEGCONV_F32 || pr.panel_dtype != SEGCONV_F16_SPLIT) return false;
@@ -486,8 +598,8 @@ static bool make_fold_ts_params(const FusedProblem& pr, tcfs::Params& p) {
   if (p.S_pad > 256 || p.S_pad > tcfs::RPT * 128) return false;  // one TMA box, converter rows
   p.stage_bytes = tcfs::KB * 4 * p.S_pad;  // == CH * 2 planes * S_pad * 16 after the split
   p.stage_bytes = (p.stage_bytes + 1023) / 1024 * 1024;
-  p.w_rows = fold_rows(pr.kh, pr.kw, pr.p, pr.cout);
-  p.w_img_bytes = 2 * (pr.cin / 8) * p.w_rows * 16;
+  p.nblk = fold_ts_blocks(pr.cls, ur, uc, p.blk_of);
+  p.w_img_bytes = (int)fold_ts_image_bytes(pr.cin, p.nblk);
   const int stage_area = tcfs::STAGES * p.stage_bytes;
   if (p.w_img_bytes > stage_area) return false;
   p.w_stage0 = (stage_area - p.w_img_bytes) / p.stage_bytes;  // first stage the staging covers
@@ -567,9 +679,10 @@ static cudaError_t launch_fold_ts_t(const tcfs::Params& prm, const CUtensorMap& 
   return cudaGetLastError();
 }
 
-cudaError_t launch_tc_fold_ts(const FusedProblem& pr, cudaStream_t s) {
+cudaError_t launch_tc_fold_ts(const FusedProblem& pr, const void* img, cudaStream_t s) {
   tcfs::Params p;
   if (!make_fold_ts_params(pr, p)) return cudaErrorNotSupported;
+  p.panels = (const uint8_t*)img;  // the compact image appended to the folded panels
   if (p.Mv == 0) return cudaSuccess;
   EncodeTiledFnTS fn = encode_fn_ts();
   if (!fn) return cudaErrorNotSupported;
