@@ -68,12 +68,16 @@ struct Params {
   int shift[4][MAX_TAPS_Q];
   int rows[4], cols[4];
   long long pair_tiles, units;
+  // TILE2D (p_fused > 0): each CTA stages TR rows of the padded (virtual) grid,
+  // VW = n + 2 p_fused wide, as one 4-D TMA box whose out-of-image part is
+  // zero-filled -- the padding is never materialised
+  int tile2d, pf, VW, TR, TRH, tiles_per_img;
   unsigned long long* trace;
   int debug;
 };
 
 struct Maps {
-  CUtensorMap x;     // (cin, Mv) bf16, box {64, S_rows}, 128B swizzle
+  CUtensorMap x;     // (cin, Mv) bf16, box {64, S_rows}; TILE2D: (cin, n, n, batch), box {64, VW, TRH, 1}
   CUtensorMap w[4];  // class q: (cin, taps_q, cout_pad) bf16, box {64, 1, NT/2}, 128B swizzle
 };
 
@@ -120,6 +124,14 @@ __device__ __forceinline__ void tma2_load_3d(uint32_t dst, const CUtensorMap* ma
       "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cl), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma2_load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
+                                             int c2, int c3, uint32_t bar_cl) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cl), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
 __device__ __forceinline__ void mma2_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
@@ -238,6 +250,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int nt, q;
       for (int k = 0; unit_of(p, k, pt, nt, q); ++k) {
         const long long m0 = pt * 256 + (long long)rank * 128;
+        const long long g = pt * 2 + rank;  // TILE2D: this CTA's row tile
+        const int tb = p.tile2d ? (int)(g / p.tiles_per_img) : 0;
+        const int tvi0 = p.tile2d ? (int)(g - (long long)tb * p.tiles_per_img) * p.TR : 0;
         const int f0 = nt * p.NT + (int)rank * NT2;
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(&a_empty[sa], pa ^ 1);
@@ -245,8 +260,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           // issues its loads (they complete on the leader's barrier)
           const uint32_t af = mapa(smem_u32(&a_full[sa]), 0);
           if (rank == 0) mbar_arrive_expect_tx(&a_full[sa], (p.debug & 32) ? 0u : 2 * a_tx);
-          if (!(p.debug & 32))  // diagnostics: no halo loads
-            tma2_load_2d(smem_u32(a_base + (size_t)sa * p.a_stage_bytes), &maps.x, kb * KB, (int)m0, af);
+          if (!(p.debug & 32)) {  // diagnostics: no halo loads
+            if (p.tile2d)
+              tma2_load_4d(smem_u32(a_base + (size_t)sa * p.a_stage_bytes), &maps.x, kb * KB, -p.pf,
+                           tvi0 - p.pf, tb, af);
+            else
+              tma2_load_2d(smem_u32(a_base + (size_t)sa * p.a_stage_bytes), &maps.x, kb * KB,
+                           (int)m0, af);
+          }
           if (++sa == SA) {
             sa = 0;
             pa ^= 1;
@@ -334,12 +355,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&acc_full[acc], pacc);
       tc_fence_after();
       if (threadIdx.x == 0 && rank == 0) trace_ev(p, 4, k);
-      const long long m = pt * 256 + (long long)rank * 128 + warp * 32 + lane;
-      const int b = (int)(m / img);
-      const int rem = (int)(m - (long long)b * img);
-      const int i = rem / p.n, j = rem - (rem / p.n) * p.n;
+      int b, i, j;
+      bool in_range;
+      if (p.tile2d) {
+        const long long g = pt * 2 + rank;
+        b = (int)(g / p.tiles_per_img);
+        const int t = warp * 32 + lane;
+        i = (int)(g - (long long)b * p.tiles_per_img) * p.TR + t / p.VW;
+        j = t - (t / p.VW) * p.VW;
+        in_range = b < p.batch && t < p.TR * p.VW;
+      } else {
+        const long long m = pt * 256 + (long long)rank * 128 + warp * 32 + lane;
+        b = (int)(m / img);
+        const int rem = (int)(m - (long long)b * img);
+        i = rem / p.n;
+        j = rem - (rem / p.n) * p.n;
+        in_range = m < p.Mv;
+      }
       const int r = q >> 1, c = q & 1;
-      const bool ok = m < p.Mv && i < p.rows[q] && j < p.cols[q] && !(p.debug & 1);
+      const bool ok = in_range && i < p.rows[q] && j < p.cols[q] && !(p.debug & 1);
       YT* dst = reinterpret_cast<YT*>(p.y) +
                 ((long long)((long long)b * p.out_h + 2 * i + r) * p.out_w + 2 * j + c) * p.cout +
                 nt * p.NT;
@@ -428,7 +462,7 @@ int tc_wide_ntile(int cout) {
 }
 
 bool tc_wide_fits(int kh, int kw, int p, int cin, int cout) {
-  if (p / 2 != 0 || cin % tcw::KB != 0 || cout < 64) return false;
+  if (cin % tcw::KB != 0 || cout < 64) return false;
   for (int r = 0; r < 2; ++r) {
     const int u0 = (p + r) & 1;
     const int ah = u0 >= kh ? 0 : (kh - u0 + 1) / 2, aw = u0 >= kw ? 0 : (kw - u0 + 1) / 2;
@@ -439,7 +473,7 @@ bool tc_wide_fits(int kh, int kw, int p, int cin, int cout) {
 
 static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
   p = tcw::Params{};
-  if (pr.pf != 0 || pr.x_dtype != SEGCONV_BF16 || pr.panel_dtype != SEGCONV_BF16) return false;
+  if (pr.x_dtype != SEGCONV_BF16 || pr.panel_dtype != SEGCONV_BF16) return false;
   if (pr.panel_layout != SEGCONV_PANEL_KMAJOR) return false;
   if (pr.y_dtype != SEGCONV_BF16 && pr.y_dtype != SEGCONV_F32) return false;
   if (!tc_wide_fits(pr.kh, pr.kw, pr.p, pr.cin, pr.cout)) return false;
@@ -460,21 +494,36 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
     // the last tile may run past cout_pad: the TMA box is zero-filled out of bounds
   }
   p.nkb = pr.cin / tcw::KB;
-  int max_shift = 0;
+  p.pf = pr.pf;
+  p.tile2d = pr.pf > 0 ? 1 : 0;
+  p.VW = pr.n + 2 * pr.pf;  // pitch of the staged rows (the padded grid in TILE2D)
+  int max_shift = 0, max_dy = 0;
   for (int q = 0; q < 4; ++q) {
     p.taps[q] = pr.cls.kh[q] * pr.cls.kw[q];
     if (p.taps[q] > tcw::MAX_TAPS_Q) return false;
     for (int u = 0; u < pr.cls.kh[q]; ++u)
       for (int v = 0; v < pr.cls.kw[q]; ++v) {
-        const int s = (pr.cls.off_r[q] + u) * pr.n + (pr.cls.off_c[q] + v);
+        const int pitch = p.tile2d ? p.VW : pr.n;
+        const int s = (pr.cls.off_r[q] + u) * pitch + (pr.cls.off_c[q] + v);
         p.shift[q][u * pr.cls.kw[q] + v] = s;
         max_shift = std::max(max_shift, s);
+        max_dy = std::max(max_dy, pr.cls.off_r[q] + u);
       }
     p.rows[q] = pr.cls.rows[q];
     p.cols[q] = pr.cls.cols[q];
   }
-  p.S_rows = (128 + max_shift + 7) / 8 * 8;
-  if (p.S_rows > 256) return false;  // one TMA box
+  if (p.tile2d) {
+    if (p.VW > 128) return false;
+    p.TR = 128 / p.VW;
+    p.TRH = p.TR + max_dy + 1;  // + one row: shifted reads of the last anchors wrap a row
+    const int vh = std::max(pr.cls.rows[0], pr.cls.rows[2]);
+    p.tiles_per_img = (vh + p.TR - 1) / p.TR;
+    p.S_rows = p.VW * p.TRH;
+    if (p.TRH > 256 || p.S_rows > 384) return false;
+  } else {
+    p.S_rows = (128 + max_shift + 7) / 8 * 8;
+    if (p.S_rows > 256) return false;  // one TMA box
+  }
   p.a_stage_bytes = (p.S_rows * 128 + 1023) / 1024 * 1024;
   p.b_stage_bytes = (p.NT / 2) * 128;
   if (p.b_stage_bytes % 1024) return false;
@@ -487,13 +536,24 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
     p.stages_b = std::min(tcw::MAX_STAGES_B, (budget - p.stages_a * p.a_stage_bytes) / p.b_stage_bytes);
   }
   if (p.stages_b < 2) return false;
-  p.pair_tiles = (p.Mv + 255) / 256;
+  p.pair_tiles = p.tile2d ? ((long long)pr.batch * p.tiles_per_img + 1) / 2 : (p.Mv + 255) / 256;
   p.units = p.pair_tiles * p.n_tiles * 4;
   if ((long long)pr.batch * pr.out_h * pr.out_w * pr.cout >= (1LL << 40)) return false;
   // tensor maps
   EncodeTiledFnW fn = encode_fn_w();
   if (!fn) return false;
-  {
+  if (p.tile2d) {
+    const cuuint64_t dims[4] = {(cuuint64_t)pr.cin, (cuuint64_t)pr.n, (cuuint64_t)pr.n,
+                                (cuuint64_t)pr.batch};
+    const cuuint64_t strides[3] = {(cuuint64_t)pr.cin * 2, (cuuint64_t)pr.n * pr.cin * 2,
+                                   (cuuint64_t)pr.n * pr.n * pr.cin * 2};
+    const cuuint32_t box[4] = {(cuuint32_t)tcw::KB, (cuuint32_t)p.VW, (cuuint32_t)p.TRH, 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    if (fn(&maps.x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pr.x), dims, strides,
+           box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  } else {
     const cuuint64_t dims[2] = {(cuuint64_t)pr.cin, (cuuint64_t)p.Mv};
     const cuuint64_t strides[1] = {(cuuint64_t)pr.cin * 2};
     const cuuint32_t box[2] = {(cuuint32_t)tcw::KB, (cuuint32_t)p.S_rows};

@@ -74,7 +74,8 @@ __global__ void __launch_bounds__(256, 1) run(int units, int epi, int cps, int n
     const uint32_t COL = 200 * 16, LBO = 2 * COL;
     const int shift_off[4] = {0, 1, 64, 65};
     const uint32_t x0 = smem_u32(smem);
-    const uint32_t id = (1u << 4) | ((uint32_t)(ntile >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const int mm = ntile >= 1000 ? 64 : 128, nn = ntile >= 1000 ? ntile - 1000 : ntile;
+    const uint32_t id = (1u << 4) | ((uint32_t)(nn >> 3) << 17) | ((uint32_t)(mm >> 4) << 24);
     for (int u = 0; u < units; ++u) {
       const int b = u & 1;
       if (u >= 2) wait(&empty[b], ((u >> 1) - 1) & 1);
@@ -146,7 +147,7 @@ int main() {
   struct V {
     int grid, units, epi, cps, n;
   } vs[] = {{1, 32, 0, 0, 128},  {148, 32, 0, 0, 128}, {1, 32, 1, 0, 128}, {148, 32, 1, 0, 128},
-            {148, 32, 1, 0, 64}};
+            {148, 32, 1, 0, 64}, {148, 32, 0, 0, 1128}, {148, 32, 0, 0, 1064}, {148, 32, 0, 0, 256}};
   for (int rnd = 0; rnd < 2; ++rnd)
   for (const V& v : vs) {
     for (int rep = 0; rep < 2; ++rep) {
@@ -164,7 +165,7 @@ int main() {
       cpmx = h[c * 4 + 1] > cpmx ? h[c * 4 + 1] : cpmx;
     }
     printf("%s grid %3d units %2d epi %d cps %2d N %3d: %.1f cycles/MMA (max CTA), cp phase %.0f cycles (%.1f/cp)\n",
-           rnd ? "random" : "const ", v.grid, v.units, v.epi, v.cps, v.n, mx / (v.units * 48.0), cpmx, v.cps ? cpmx / v.cps : 0.0);
+           rnd ? "random" : "const ", v.grid, v.units, v.epi, v.cps, v.n >= 1000 ? -(v.n - 1000) : v.n, mx / (v.units * 48.0), cpmx, v.cps ? cpmx / v.cps : 0.0);
   }
   return 0;
 }

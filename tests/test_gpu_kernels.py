@@ -84,6 +84,24 @@ def test_pair_kernel_bf16(batch, n, cin, cout, ks, act):
     assert scaled_err(got, want_of(x, k, 0, act)) <= 1e-4  # fp32 accumulate; bar is 1e-2
 
 
+@pytest.mark.parametrize("batch,n,cin,cout,ks,p,act", [
+    (2, 16, 128, 64, 4, 2, "relu"),  # DCGAN-standard layer: 4x4, out = 2N (p = 2, p_fused = 1)
+    (3, 5, 256, 128, 3, 1, None),    # p = 1: odd-padding class swap, p_fused = 0
+    (2, 8, 64, 64, 4, 3, None),      # p = 3: p_fused = 1, odd parity
+    (1, 7, 128, 96, 5, 2, "tanh"),   # 5x5, p = 2
+    (4, 4, 512, 256, 4, 2, "relu"),  # GAN first layer 4 -> 8
+])
+def test_pair_kernel_padded(batch, n, cin, cout, ks, p, act):
+    """p_orig > 0: the padded grid is staged by 4-D TMA boxes whose
+    out-of-image part is zero-filled."""
+    rng = np.random.default_rng(batch * 31 + n + cin + p)
+    x = oracle.bf16_round(rng.standard_normal((batch, n, n, cin)).astype(np.float32))
+    k = oracle.bf16_round((rng.standard_normal((ks, ks, cin, cout)) * 0.02).astype(np.float32))
+    got, path = run(x, k, p, "bf16", act, out_dtype=torch.float32)
+    assert path == "tc-pair"
+    assert scaled_err(got, want_of(x, k, p, act)) <= 1e-4
+
+
 def test_pair_kernel_bf16_output():
     rng = np.random.default_rng(5)
     x = oracle.bf16_round(rng.standard_normal((2, 16, 16, 128)).astype(np.float32))
