@@ -52,7 +52,7 @@ constexpr int NUM_THREADS = 224;
 constexpr int SMEM_LIMIT = 227 * 1024;
 constexpr int KB = 64;  // channels per stage: one 128-byte row
 constexpr int MAX_TAPS_Q = 16;
-constexpr int MAX_STAGES_A = 4, MAX_STAGES_B = 12;
+constexpr int MAX_STAGES_A = 8, MAX_STAGES_B = 12;
 
 struct Params {
   void* y;
@@ -72,6 +72,12 @@ struct Params {
   // VW = n + 2 p_fused wide, as one 4-D TMA box whose out-of-image part is
   // zero-filled -- the padding is never materialised
   int tile2d, pf, VW, TR, TRH, tiles_per_img;
+  // IM2COL (small images, where the halo-shift grid wastes rows): GEMM rows are
+  // only class q's output anchors; each tap's A tile is gathered by an im2col
+  // TMA (walk over the anchors, tap offset added per load)
+  int im2col;
+  long long unit_base[5];  // first unit of class q (units are class-major)
+  int tap_off_r[4][MAX_TAPS_Q], tap_off_c[4][MAX_TAPS_Q];
   unsigned long long* trace;
   int debug;
 };
@@ -79,6 +85,7 @@ struct Params {
 struct Maps {
   CUtensorMap x;     // (cin, Mv) bf16, box {64, S_rows}; TILE2D: (cin, n, n, batch), box {64, VW, TRH, 1}
   CUtensorMap w[4];  // class q: (cin, taps_q, cout_pad) bf16, box {64, 1, NT/2}, 128B swizzle
+  CUtensorMap xi[4]; // IM2COL class q: (cin, n, n, batch), walk over its anchors, 64 ch x 128 px
 };
 
 // ---------------------------------------------------------------- PTX (pair)
@@ -134,6 +141,16 @@ __device__ __forceinline__ void tma2_load_4d(uint32_t dst, const CUtensorMap* ma
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cl), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+__device__ __forceinline__ void tma2_load_im2col(uint32_t dst, const CUtensorMap* map, int c, int w,
+                                                 int h, int n, uint16_t ow, uint16_t oh,
+                                                 uint32_t bar_cl) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.im2col.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %8};" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cl), "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow),
+      "h"(oh)
+      : "memory");
+}
 __device__ __forceinline__ void mma2_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
                                           uint32_t accumulate) {
   asm volatile(
@@ -173,6 +190,14 @@ __device__ __forceinline__ bool unit_of(const Params& p, int k, long long& pt, i
   const long long pairs = gridDim.x / 2;
   const long long u = (long long)(blockIdx.x / 2) + (long long)k * pairs;
   if (u >= p.units) return false;
+  if (p.im2col) {  // class-major: [class q][pair tile][feature tile]
+    q = 0;
+    while (u >= p.unit_base[q + 1]) ++q;
+    const long long v = u - p.unit_base[q];
+    nt = (int)(v % p.n_tiles);
+    pt = v / p.n_tiles;
+    return true;
+  }
   q = (int)(u & 3);
   const long long t = u >> 2;
   nt = (int)(t % p.n_tiles);
@@ -223,8 +248,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
   if (warp == 4 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.x)) : "memory");
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < 4; ++q) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.w[q])) : "memory");
+      if (p.im2col)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.xi[q])) : "memory");
+    }
   }
   if (warp == 6) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
@@ -254,6 +282,38 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int tb = p.tile2d ? (int)(g / p.tiles_per_img) : 0;
         const int tvi0 = p.tile2d ? (int)(g - (long long)tb * p.tiles_per_img) * p.TR : 0;
         const int f0 = nt * p.NT + (int)rank * NT2;
+        if (p.im2col) {
+          // this CTA's first anchor of class q: (b, i, j) on the class's rows x cols grid
+          const int R = p.rows[q], C = p.cols[q];
+          const long long a0 = pt * 256 + (long long)rank * 128;
+          const int ib = (int)(a0 / ((long long)R * C));
+          const int rem = (int)(a0 - (long long)ib * R * C);
+          const int i0 = rem / C, j0 = rem - (rem / C) * C;
+          for (int kb = 0; kb < p.nkb; ++kb)
+            for (int t = 0; t < p.taps[q]; ++t) {
+              mbar_wait(&a_empty[sa], pa ^ 1);
+              const uint32_t af = mapa(smem_u32(&a_full[sa]), 0);
+              if (rank == 0) mbar_arrive_expect_tx(&a_full[sa], 2 * 128 * 128);
+              tma2_load_im2col(smem_u32(a_base + (size_t)sa * p.a_stage_bytes), &maps.xi[q],
+                               kb * KB, j0 - p.pf, i0 - p.pf, ib, (uint16_t)p.tap_off_c[q][t],
+                               (uint16_t)p.tap_off_r[q][t], af);
+              if (++sa == SA) {
+                sa = 0;
+                pa ^= 1;
+              }
+              mbar_wait(&b_empty[sb], pb ^ 1);
+              const uint32_t bf = mapa(smem_u32(&b_full[sb]), 0);
+              if (rank == 0) mbar_arrive_expect_tx(&b_full[sb], 2 * b_tx);
+              tma2_load_3d(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), &maps.w[q], kb * KB, t,
+                           f0, bf);
+              if (++sb == SB) {
+                sb = 0;
+                pb ^= 1;
+              }
+            }
+          if (rank == 0) trace_ev(p, 0, k);
+          continue;
+        }
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(&a_empty[sa], pa ^ 1);
           // the leader expects both CTAs' bytes on its barrier; the peer only
@@ -302,6 +362,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
         if (lane == 0) trace_ev(p, 2, k);
         const uint32_t d = tb + (uint32_t)(acc * p.NT);
+        if (p.im2col) {
+          for (int kb = 0; kb < p.nkb; ++kb)
+            for (int t = 0; t < p.taps[q]; ++t) {
+              mbar_wait(&a_full[sa], pa);
+              mbar_wait(&b_full[sb], pb);
+              tc_fence_after();
+              const uint64_t ad = sw128_desc(smem_u32(a_base + (size_t)sa * p.a_stage_bytes));
+              const uint64_t bd = sw128_desc(smem_u32(b_base + (size_t)sb * p.b_stage_bytes));
+              if (elect_one()) {
+#pragma unroll
+                for (int ks = 0; ks < KB / 16; ++ks)
+                  mma2_bf16(d, ad + 2u * ks, bd + 2u * ks, idesc,
+                            (kb == 0 && t == 0 && ks == 0) ? 0u : 1u);
+              }
+              __syncwarp();
+              if (elect_one()) {
+                commit2(&a_empty[sa]);
+                commit2(&b_empty[sb]);
+              }
+              __syncwarp();
+              if (++sa == SA) {
+                sa = 0;
+                pa ^= 1;
+              }
+              if (++sb == SB) {
+                sb = 0;
+                pb ^= 1;
+              }
+            }
+        } else
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(&a_full[sa], pa);
           tc_fence_after();
@@ -357,7 +447,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (threadIdx.x == 0 && rank == 0) trace_ev(p, 4, k);
       int b, i, j;
       bool in_range;
-      if (p.tile2d) {
+      if (p.im2col) {
+        const int R = p.rows[q], C = p.cols[q];
+        const long long a = pt * 256 + (long long)rank * 128 + warp * 32 + lane;
+        b = (int)(a / ((long long)R * C));
+        const int rem = (int)(a - (long long)b * R * C);
+        i = rem / C;
+        j = rem - (rem / C) * C;
+        in_range = b < p.batch;
+      } else if (p.tile2d) {
         const long long g = pt * 2 + rank;
         b = (int)(g / p.tiles_per_img);
         const int t = warp * 32 + lane;
@@ -524,20 +622,59 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
     p.S_rows = (128 + max_shift + 7) / 8 * 8;
     if (p.S_rows > 256) return false;  // one TMA box
   }
+  // IM2COL when the halo-shift grid would compute mostly non-output anchors
+  // (tiny images: C5 a 44 %, b 54 % useful rows) and the feature tile is wide
+  // enough that re-gathering A per tap stays within L2 bandwidth
+  {
+    long long useful = 0, taps = 0;
+    for (int q = 0; q < 4; ++q) {
+      useful += (long long)pr.cls.rows[q] * pr.cls.cols[q] * p.taps[q];
+      taps += p.taps[q];
+    }
+    const double eff = (double)useful / ((double)p.VW * p.VW * taps);
+    p.im2col = (eff < 0.6 && p.NT == 256) ? 1 : 0;
+    const char* e = getenv("SEGCONV_WIDE_IM2COL");
+    if (e) p.im2col = atoi(e) ? 1 : 0;
+  }
+  if (p.im2col) {
+    p.tile2d = 0;
+    p.S_rows = 128;
+    for (int q = 0; q < 4; ++q)
+      for (int u = 0; u < pr.cls.kh[q]; ++u)
+        for (int v = 0; v < pr.cls.kw[q]; ++v) {
+          p.tap_off_r[q][u * pr.cls.kw[q] + v] = pr.cls.off_r[q] + u;
+          p.tap_off_c[q][u * pr.cls.kw[q] + v] = pr.cls.off_c[q] + v;
+        }
+  }
   p.a_stage_bytes = (p.S_rows * 128 + 1023) / 1024 * 1024;
   p.b_stage_bytes = (p.NT / 2) * 128;
   if (p.b_stage_bytes % 1024) return false;
   const int bar_bytes = (2 * tcw::MAX_STAGES_A + 2 * tcw::MAX_STAGES_B + 4) * 8 + 16;
   const int budget = tcw::SMEM_LIMIT - bar_bytes;
-  p.stages_a = 3;
-  p.stages_b = std::min(tcw::MAX_STAGES_B, (budget - p.stages_a * p.a_stage_bytes) / p.b_stage_bytes);
-  if (p.stages_b < 4) {
-    p.stages_a = 2;
+  if (p.im2col) {  // A and B both per (k-block, tap): paired rings
+    p.stages_a = p.stages_b = std::min(tcw::MAX_STAGES_A, budget / (p.a_stage_bytes + p.b_stage_bytes));
+    if (p.stages_a < 2) return false;
+  } else {
+    p.stages_a = 3;
     p.stages_b = std::min(tcw::MAX_STAGES_B, (budget - p.stages_a * p.a_stage_bytes) / p.b_stage_bytes);
+    if (p.stages_b < 4) {
+      p.stages_a = 2;
+      p.stages_b = std::min(tcw::MAX_STAGES_B, (budget - p.stages_a * p.a_stage_bytes) / p.b_stage_bytes);
+    }
+    if (p.stages_b < 2) return false;
   }
-  if (p.stages_b < 2) return false;
-  p.pair_tiles = p.tile2d ? ((long long)pr.batch * p.tiles_per_img + 1) / 2 : (p.Mv + 255) / 256;
-  p.units = p.pair_tiles * p.n_tiles * 4;
+  if (p.im2col) {
+    p.unit_base[0] = 0;
+    for (int q = 0; q < 4; ++q) {
+      const long long aq = (long long)pr.batch * pr.cls.rows[q] * pr.cls.cols[q];
+      p.unit_base[q + 1] = p.unit_base[q] + (aq + 255) / 256 * p.n_tiles;
+    }
+    p.units = p.unit_base[4];
+    p.pair_tiles = 0;
+  } else {
+    p.pair_tiles = p.tile2d ? ((long long)pr.batch * p.tiles_per_img + 1) / 2 : (p.Mv + 255) / 256;
+    p.units = p.pair_tiles * p.n_tiles * 4;
+  }
   if ((long long)pr.batch * pr.out_h * pr.out_w * pr.cout >= (1LL << 40)) return false;
   // tensor maps
   EncodeTiledFnW fn = encode_fn_w();
@@ -562,6 +699,37 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
+  }
+  if (p.im2col) {
+    typedef CUresult (*EncIm2col)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const int*, const int*,
+                                  cuuint32_t, cuuint32_t, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncIm2col enc2 = nullptr;
+    if (!enc2) {
+      void* f = nullptr;
+      cudaDriverEntryPointQueryResult qr;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f, cudaEnableDefault, &qr) !=
+              cudaSuccess ||
+          qr != cudaDriverEntryPointSuccess)
+        return false;
+      enc2 = (EncIm2col)f;
+    }
+    const cuuint64_t dims[4] = {(cuuint64_t)pr.cin, (cuuint64_t)pr.n, (cuuint64_t)pr.n,
+                                (cuuint64_t)pr.batch};
+    const cuuint64_t strides[3] = {(cuuint64_t)pr.cin * 2, (cuuint64_t)pr.n * pr.cin * 2,
+                                   (cuuint64_t)pr.n * pr.n * pr.cin * 2};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    for (int q = 0; q < 4; ++q) {
+      // walk origins (anchor - p_fused) over [-pf, C-1-pf] x [-pf, R-1-pf] of every image
+      const int lower[2] = {-pr.pf, -pr.pf};
+      const int upper[2] = {pr.cls.cols[q] - pr.pf - pr.n, pr.cls.rows[q] - pr.pf - pr.n};
+      if (enc2(&maps.xi[q], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pr.x), dims,
+               strides, lower, upper, (cuuint32_t)tcw::KB, 128, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    }
   }
   for (int q = 0; q < 4; ++q) {
     const cuuint64_t dims[3] = {(cuuint64_t)pr.cin, (cuuint64_t)p.taps[q], (cuuint64_t)pr.cout_pad};
