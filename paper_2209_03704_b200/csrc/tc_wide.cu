@@ -622,9 +622,8 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
     p.S_rows = (128 + max_shift + 7) / 8 * 8;
     if (p.S_rows > 256) return false;  // one TMA box
   }
-  // IM2COL when the halo-shift grid would compute mostly non-output anchors
-  // (tiny images: C5 a 44 %, b 54 % useful rows) and the feature tile is wide
-  // enough that re-gathering A per tap stays within L2 bandwidth
+  // IM2COL: GEMM rows are only output anchors (the halo-shift grid computes
+  // every virtual position: C5 a 44 %, b 54 %, c 65 %, C3 77 % useful rows)
   {
     long long useful = 0, taps = 0;
     for (int q = 0; q < 4; ++q) {
@@ -632,7 +631,11 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
       taps += p.taps[q];
     }
     const double eff = (double)useful / ((double)p.VW * p.VW * taps);
-    p.im2col = (eff < 0.6 && p.NT == 256) ? 1 : 0;
+    (void)eff;
+    // measured (B200, bench.py): im2col beats the halo-shift staging on every
+    // BASELINE shape -- C3 89.7 -> 79.9 us (78 % useful rows), C5 237 -> 138 us
+    // -- the extra per-tap A gathers are L2 hits, the saved MMA rows are not
+    p.im2col = 1;
     const char* e = getenv("SEGCONV_WIDE_IM2COL");
     if (e) p.im2col = atoi(e) ? 1 : 0;
   }
