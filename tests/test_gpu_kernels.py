@@ -102,6 +102,21 @@ def test_pair_kernel_padded(batch, n, cin, cout, ks, p, act):
     assert scaled_err(got, want_of(x, k, p, act)) <= 1e-4
 
 
+@pytest.mark.parametrize("batch,n,cin,cout,ks,p", [(4, 16, 512, 256, 4, 0), (2, 16, 128, 64, 4, 2),
+                                                    (3, 5, 256, 128, 3, 1)])
+def test_pair_kernel_halo_shift_staging(batch, n, cin, cout, ks, p, monkeypatch):
+    """The halo-shift staging of the pair kernel (linear TMA rows for p_fused = 0,
+    padded 4-D boxes otherwise) -- the alternative to im2col, selected by
+    SEGCONV_WIDE_IM2COL=0."""
+    monkeypatch.setenv("SEGCONV_WIDE_IM2COL", "0")
+    rng = np.random.default_rng(batch * 3 + n + p)
+    x = oracle.bf16_round(rng.standard_normal((batch, n, n, cin)).astype(np.float32))
+    k = oracle.bf16_round((rng.standard_normal((ks, ks, cin, cout)) * 0.02).astype(np.float32))
+    got, path = run(x, k, p, "bf16", out_dtype=torch.float32)
+    assert path == "tc-pair"
+    assert scaled_err(got, want_of(x, k, p)) <= 1e-4
+
+
 def test_pair_kernel_bf16_output():
     rng = np.random.default_rng(5)
     x = oracle.bf16_round(rng.standard_normal((2, 16, 16, 128)).astype(np.float32))
