@@ -380,6 +380,8 @@ def main():
                     choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="segconv", choices=["segconv", "reference"])
     ap.add_argument("--no-baselines", action="store_true", help="skip conventional/cuDNN/CPU legs")
+    ap.add_argument("--no-e2e", action="store_true",
+                    help="diagnostics (ncu launch lists): skip the host-buffer e2e leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
@@ -469,18 +471,19 @@ def main():
     value = macs_all / (ms * 1e-3) / 1e9
 
     # ---- e2e through the public API with host buffers (H2D + compute + D2H)
-    for _ in range(2):
+    e2e_steps = 0 if args.no_e2e else args.steps
+    for _ in range(2 if e2e_steps else 0):
         prob.step_e2e()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ea.record(stream)
-    for _ in range(args.steps):
+    for _ in range(e2e_steps):
         prob.step_e2e()
     eb.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = torch.tensor([ea.elapsed_time(eb) / args.steps], device=dev, dtype=torch.float64)
+    e2e_ms = torch.tensor([ea.elapsed_time(eb) / max(1, e2e_steps)], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())

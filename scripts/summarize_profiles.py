@@ -20,7 +20,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 G = os.path.join(ROOT, "gpurun_out")
 P = os.path.join(ROOT, "profiles")
-HOT = {"C1": "tconv_pixlanes", "C2": "fold_ts", "C3": "wide_kernel", "C4": "tc_fold", "C5": "wide_kernel"}
+HOT = {"C1": "tconv_outputs", "C2": "fold_ts_kernel", "C3": "wide_kernel", "C4": "ring_kernel", "C5": "wide_kernel"}
 
 
 def short(name):
