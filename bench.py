@@ -45,6 +45,15 @@ CONFIGS = {
                act="tanh", desc="low-channel fp32 + tanh, 32x256x256x64 -> 32x507x507x3, n=5"),
     "C5": dict(batch=1024, stack=True, dtype="bf16",
                desc="4-layer bf16 generator stack, batch 1024 sharded, 4->5->7->11->19"),
+    # single layers of the C5 stack (diagnostics: --config C5a .. C5d)
+    "C5a": dict(batch=1024, n=4, cin=1024, cout=512, k=3, p=0, dtype="bf16", xd="n", wd="n02",
+                act="relu", desc="C5 layer a: 1024x4x4x1024 -> 5x5x512"),
+    "C5b": dict(batch=1024, n=5, cin=512, cout=256, k=3, p=0, dtype="bf16", xd="n", wd="n02",
+                act="relu", desc="C5 layer b: 1024x5x5x512 -> 7x7x256"),
+    "C5c": dict(batch=1024, n=7, cin=256, cout=128, k=3, p=0, dtype="bf16", xd="n", wd="n02",
+                act="relu", desc="C5 layer c: 1024x7x7x256 -> 11x11x128"),
+    "C5d": dict(batch=1024, n=11, cin=128, cout=3, k=3, p=0, dtype="bf16", xd="n", wd="n02",
+                act="tanh", desc="C5 layer d: 1024x11x11x128 -> 19x19x3"),
 }
 SEED = 20240911
 

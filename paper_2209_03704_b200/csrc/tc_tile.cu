@@ -16,8 +16,9 @@
 // TMA (box {64 channels, 128 pixels}, 128-byte swizzle) and are the MMA A
 // operand directly; the weight image (rows = D columns) is resident in SMEM.
 //
-// Warp roles (192 threads): 0-3 epilogue, 4 TMA producer / TMEM owner,
-// 5 MMA issuer.
+// Warp roles (320 threads): 0-7 epilogue (0-3 also drain TMEM; thread t sums
+// anchor t % 128 for output row parity t / 128), 8 TMA producer / TMEM
+// owner, 9 MMA issuer.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -34,7 +35,7 @@ namespace tct {
 
 using namespace tc;
 
-constexpr int NUM_THREADS = 192;
+constexpr int NUM_THREADS = 320;
 constexpr int SMEM_LIMIT = 227 * 1024;
 constexpr int KB = 64;  // bf16 channels per stage: one 128-byte row
 constexpr int MAX_STAGES = 8;
@@ -53,6 +54,13 @@ struct Params {
   unsigned long long* trace;
   int debug;
 };
+
+__device__ __forceinline__ void trace_ev(const Params& p, int ev, int local) {
+  if (p.trace == nullptr || blockIdx.x >= 160 || local >= 64) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  p.trace[(blockIdx.x * 16 + ev) * 64 + local] = t;
+}
 
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
   return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
@@ -78,7 +86,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp == 5 && lane == 0) {
+  if (warp == 9 && lane == 0) {
     for (int s = 0; s < SA; ++s) {
       mbar_init(&a_full[s], 1);
       mbar_init(&a_empty[s], 1);
@@ -90,7 +98,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     mbar_init(w_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 4) {
+  if (warp == 8) {
     if (lane == 0)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
@@ -105,7 +113,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int NKB = p.cin / KB;
   const uint32_t WCOL = (uint32_t)N * 16;
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ===== TMA producer: weights once, then {64 ch, 128 pixels} boxes per tile
     if (lane == 0) {
       mbar_arrive_expect_tx(w_full, (uint32_t)p.w_bytes);
@@ -113,8 +121,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         bulk_g2s(w_base + off, p.panels + off, min(32768u, (uint32_t)p.w_bytes - off), w_full);
       int st = 0;
       uint32_t ph = 0;
-      for (long long t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+      int k = 0;
+      for (long long t = blockIdx.x; t < p.tiles; t += gridDim.x, ++k) {
         const int p0 = (int)(t * p.step);
+        trace_ev(p, 0, k);
         for (int kb = 0; kb < NKB; ++kb) {
           mbar_wait(&a_empty[st], ph ^ 1);
           mbar_arrive_expect_tx(&a_full[st], (uint32_t)p.stage_bytes);
@@ -126,7 +136,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ===== MMA issuer (whole warp in the loop; one elected lane issues)
     const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base, 0);
     const uint32_t wb = smem_u32(w_base);
@@ -135,9 +145,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t ph = 0, pacc = 0;
     mbar_wait(w_full, 0);
     tc_fence_after();
-    for (long long t = blockIdx.x; t < p.tiles; t += gridDim.x) {
+    int k = 0;
+    for (long long t = blockIdx.x; t < p.tiles; t += gridDim.x, ++k) {
       mbar_wait(&acc_empty[acc], pacc ^ 1);
       tc_fence_after();
+      if (lane == 0) trace_ev(p, 2, k);
       const uint32_t d = tb + (uint32_t)(acc * N);
       for (int kb = 0; kb < NKB; ++kb) {
         mbar_wait(&a_full[st], ph);
@@ -166,9 +178,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else {
-    // ===== epilogue (warps 0-3): TMEM row (pixel) -> SMEM tile -> per-anchor sums
-    const int m = warp * 32 + lane;  // pixel row of the tile this thread drains / anchor it sums
-    const uint32_t lane_base = tmem_base + ((uint32_t)(warp * 32) << 16);
+    // ===== epilogue (warps 0-7): TMEM rows (pixels) -> SMEM tile (warps 0-3),
+    // then thread t sums anchor t % 128 for output rows of parity t / 128
+    const int m = threadIdx.x & 127, rr = threadIdx.x >> 7;
+    const bool drain = warp < 4;
+    const uint32_t lane_base = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
     float bias[COUT];
 #pragma unroll
     for (int f = 0; f < COUT; ++f) bias[f] = (p.epi & SEGCONV_EPI_BIAS) ? __ldg(p.bias + f) : 0.0f;
@@ -176,10 +190,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int img = p.n * p.n;
     int acc = 0;
     uint32_t pacc = 0;
-    for (long long t = blockIdx.x; t < p.tiles; t += gridDim.x) {
-      mbar_wait(&acc_full[acc], pacc);
-      tc_fence_after();
-      {
+    int k = 0;
+    for (long long t = blockIdx.x; t < p.tiles; t += gridDim.x, ++k) {
+      if (drain) {
+        mbar_wait(&acc_full[acc], pacc);
+        tc_fence_after();
+        if (threadIdx.x == 0) trace_ev(p, 4, k);
         float v[32];
         tmem_ld32(lane_base + (uint32_t)(acc * N), v);
 #pragma unroll
@@ -189,24 +205,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
           for (int c = 0; c < N - 32 && c < 16; ++c) dtile[m * TP + 32 + c] = v[c];
         }
+        tc_fence_before();
+        mbar_arrive(&acc_empty[acc]);  // D is in SMEM now; the MMA may reuse the buffer
       }
-      tc_fence_before();
-      mbar_arrive(&acc_empty[acc]);  // D is in SMEM now; the MMA may reuse the buffer
       if (++acc == 2) {
         acc = 0;
         pacc ^= 1;
       }
-      named_bar(1, 128);
+      named_bar(1, 256);
       const long long g = t * p.step + m;  // this thread's anchor
       if (m < p.step && g < p.Mv && !(p.debug & 1)) {
         const int b = (int)(g / img);
         const int rem = (int)(g - (long long)b * img);
         const int i = rem / p.n, j = rem - (rem / p.n) * p.n;
+        float out[2][COUT];
+        bool okc[2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int r = q >> 1, c = q & 1;
-          if (i >= p.rows[q] || j >= p.cols[q]) continue;
-          YT* o = y + (((long long)b * p.out_h + 2 * i + r) * p.out_w + 2 * j + c) * COUT;
+        for (int c = 0; c < 2; ++c) {
+          const int q = rr * 2 + c;
+          okc[c] = i < p.rows[q] && j < p.cols[q];
 #pragma unroll
           for (int f = 0; f < COUT; ++f) {
             float s = 0.0f;
@@ -214,24 +231,51 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             for (int dy = 0; dy < U; ++dy)
 #pragma unroll
               for (int dx = 0; dx < U; ++dx) {
-                const int col = L::col_in_group(dy, q, dx, f);
-                if (col < 0) continue;
+                // classes of row parity rr: q = 2 rr + c, both unrolled below
+                const int col0 = L::col_in_group(dy, 0 + c, dx, f), col2 = L::col_in_group(dy, 2 + c, dx, f);
+                const int col = rr ? col2 : col0;
+                if ((rr ? col2 : col0) < 0) continue;
                 s += dtile[(m + dy * p.n + dx) * TP + L::group_off(dy) + col];
               }
             s += bias[f];
             if (ACT == 1) s = fmaxf(s, 0.0f);
-            if (ACT == 2) s = tanhf(s);
-            o[f] = from_f<YT>(s);
+            if (ACT == 2) {
+              if constexpr (sizeof(YT) == 2) {
+                // bf16 output (8-bit mantissa): the SFU tanh (~2^-11 rel.) is exact enough
+                asm("tanh.approx.f32 %0, %0;" : "+f"(s));
+              } else {
+                s = tanhf(s);
+              }
+            }
+            out[c][f] = s;
           }
         }
+        // pixels (2i + rr, 2j) and (2i + rr, 2j + 1): 2 x COUT consecutive values
+        YT* o = y + (((long long)b * p.out_h + 2 * i + rr) * p.out_w + 2 * j) * COUT;
+        if (sizeof(YT) == 2 && okc[0] && okc[1] && ((reinterpret_cast<uintptr_t>(o) & 3) == 0) &&
+            (COUT % 1 == 0) && (2 * COUT) % 2 == 0) {
+          const float* fl = &out[0][0];
+#pragma unroll
+          for (int e = 0; e < COUT; ++e) {  // 2*COUT values as COUT bf16 pairs
+            const __nv_bfloat162 h = __floats2bfloat162_rn(fl[2 * e], fl[2 * e + 1]);
+            reinterpret_cast<uint32_t*>(o)[e] = *reinterpret_cast<const uint32_t*>(&h);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+            if (okc[c])
+#pragma unroll
+              for (int f = 0; f < COUT; ++f) o[c * COUT + f] = from_f<YT>(out[c][f]);
+        }
       }
-      named_bar(1, 128);  // the tile is rewritten by the next unit
+      named_bar(1, 256);  // the tile is rewritten by the next unit
+      if (threadIdx.x == 0) trace_ev(p, 5, k);
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == 8) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem_base)
                  : "memory");
@@ -334,7 +378,7 @@ cudaError_t launch_tc_tile(const FusedProblem& pr, const void* img, cudaStream_t
   if (p.stages < 2) return cudaErrorNotSupported;
   static const int dbg = getenv("SEGCONV_TC_DEBUG") ? atoi(getenv("SEGCONV_TC_DEBUG")) : 0;
   p.debug = dbg;
-  p.trace = nullptr;
+  p.trace = tc_trace_buffer();
   typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                           CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
