@@ -163,3 +163,40 @@ def test_tile_kernel(batch, n, cin, act, odt):
     assert path == "tc-tile"
     tol = 1e-4 if odt == torch.float32 else TOL_TC
     assert scaled_err(got, want_of(x, k, 0, act)) <= tol
+
+
+# ---- integer-valued data: every kernel family is bit-exact
+def _ints(rng, shape, lo, hi):
+    return rng.integers(lo, hi + 1, shape).astype(np.float32)
+
+
+@pytest.mark.parametrize("case", [
+    # (math, batch, n, cin, cout, k, p, expected path)
+    ("f16x3", 3, 64, 64, 32, 3, 0, "tc-fold-ts"),
+    ("f16x3", 2, 128, 64, 3, 5, 0, "tc-ring"),
+    ("bf16", 5, 11, 128, 3, 3, 0, "tc-tile"),
+    ("bf16", 4, 8, 128, 128, 4, 0, "tc-pair"),
+    ("bf16", 3, 6, 64, 64, 4, 2, "tc-pair"),
+    ("bf16", 2, 5, 256, 96, 3, 1, "tc-pair"),
+])
+def test_kernel_families_int_exact(case):
+    math, batch, n, cin, cout, ks, p, path = case
+    rng = np.random.default_rng(batch * 1000 + n * 10 + ks)
+    x = _ints(rng, (batch, n, n, cin), -3, 3)
+    k = _ints(rng, (ks, ks, cin, cout), -2, 2)
+    got, ran = run(x, k, p, math, out_dtype=torch.float32)
+    assert ran == path
+    want = oracle.tconv_fused(x, k, p)
+    assert np.array_equal(got, want), f"max abs diff {np.abs(got - want).max()}"
+
+
+@pytest.mark.parametrize("math,shape", [("f16x3", (64, 64, 32, 3)), ("bf16", (11, 128, 3, 3)),
+                                        ("bf16", (16, 512, 256, 4))])
+def test_empty_batch_is_a_no_op(math, shape):
+    """batch == 0 (the reference's empty-tensor edge): no launch, empty result."""
+    n, cin, cout, ks = shape
+    dt = torch.bfloat16 if math == "bf16" else torch.float32
+    g = sc.tconv_geometry(n, ks, ks, 0)
+    sks = sc.segregate(torch.zeros((ks, ks, cin, cout), device="cuda", dtype=dt), 0, math=math)
+    y = sc.transpose_conv_fused(torch.zeros((0, n, n, cin), device="cuda", dtype=dt), sks, g)
+    assert tuple(y.shape) == (0, g.out_h, g.out_w, cout)
