@@ -25,6 +25,13 @@ __device__ __forceinline__ uint32_t elect_one() {
       : "+r"(pred));
   return pred;
 }
+// Programmatic dependent launch: let the next kernel in the stream start its
+// prologue on SMs this grid frees (it must griddep_wait() before reading what
+// this grid writes); wait for the previous grid's results before reading them.
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
 }

@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) griddep_launch_dependents();
   const int NKB = p.cin / KB;
   const uint32_t WCOL = (uint32_t)N * 16;
 
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_arrive_expect_tx(w_full, (uint32_t)p.w_bytes);
       for (uint32_t off = 0; off < (uint32_t)p.w_bytes; off += 32768)
         bulk_g2s(w_base + off, p.panels + off, min(32768u, (uint32_t)p.w_bytes - off), w_full);
+      griddep_wait();  // activations come from the previous kernel (stack layer)
       int st = 0;
       uint32_t ph = 0;
       int k = 0;
@@ -421,7 +423,18 @@ cudaError_t launch_tc_tile(const FusedProblem& pr, const void* img, cudaStream_t
       if (e != cudaSuccess) return e;                                                            \
       cfg = true;                                                                                \
     }                                                                                            \
-    kern<<<(unsigned)grid, tct::NUM_THREADS, smem, s>>>(p, tmap);                                \
+    cudaLaunchConfig_t lc = {};                                                                 \
+    lc.gridDim = dim3((unsigned)grid);                                                           \
+    lc.blockDim = dim3(tct::NUM_THREADS);                                                        \
+    lc.dynamicSmemBytes = smem;                                                                  \
+    lc.stream = s;                                                                               \
+    cudaLaunchAttribute at[1];                                                                   \
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                               \
+    at[0].val.programmaticStreamSerializationAllowed = 1;                                        \
+    lc.attrs = at;                                                                               \
+    lc.numAttrs = getenv("SEGCONV_NO_PDL") ? 0 : 1;                                              \
+    e = cudaLaunchKernelEx(&lc, kern, p, tmap);                                                  \
+    if (e != cudaSuccess) return e;                                                              \
   }
   if (pr.y_dtype == SEGCONV_BF16) {
     if (act == 1)

@@ -265,6 +265,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   cluster_sync();  // both CTAs' barriers initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) griddep_launch_dependents();  // next layer may start its prologue
 
   const int NT2 = p.NT / 2;
   const uint32_t a_tx = (uint32_t)p.S_rows * 128, b_tx = (uint32_t)NT2 * 128;
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 4) {
     // ===== TMA producer (both CTAs): own halo rows and own half of the features
     if (lane == 0) {
+      griddep_wait();  // activations come from the previous kernel (stack layer)
       int sa = 0, sb = 0;
       uint32_t pa = 0, pb = 0;
       long long pt;
@@ -782,13 +784,16 @@ static cudaError_t launch_wide_t(const tcw::Params& prm, const tcw::Maps& maps, 
   cfg.blockDim = dim3(tcw::NUM_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the previous
+  at[1].val.programmaticStreamSerializationAllowed = 1;              // kernel's tail
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  static const bool pdl = getenv("SEGCONV_NO_PDL") == nullptr;
+  cfg.numAttrs = pdl ? 2 : 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm, maps);
   if (e == cudaSuccess) note_launch();
   return e;
