@@ -17,6 +17,7 @@ __all__ = [
     "tconv_naive", "scatter_f64", "count_ops", "ref_geometry", "ref_segregate", "ref_tconv_fused",
     "ref_tconv_naive", "ref_tconv_fused_parallel", "ref_run_verify", "ref_verify_case",
     "ref_count_ops", "ref_time_fused_batch", "OracleError", "bf16_round", "tf32_round",
+    "tconv_backward", "scatter_backward_f64", "ref_tconv_backward", "ref_time_backward",
 ]
 
 
@@ -57,6 +58,11 @@ def load_oracle():
             seg.argtypes = [pt, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, pt]
             seg.restype = C.c_size_t
         lib.orc_scatter_f64.argtypes = lib.orc_tconv_fused_f64.argtypes
+        for name, T in (("f32", C.c_float), ("f64", C.c_double)):
+            pt = C.POINTER(T)
+            getattr(lib, f"orc_tconv_backward_{name}").argtypes = [
+                pt, C.c_int, C.c_int, C.c_int, pt, C.c_int, C.c_int, C.c_int, C.c_int, pt, pt, pt]
+        lib.orc_scatter_backward_f64.argtypes = lib.orc_tconv_backward_f64.argtypes
         lib.orc_subkernel_dims.argtypes = [C.c_int, C.c_int, C.c_int, ip, ip]
         lib.orc_count_ops.argtypes = [C.c_int] * 6 + [C.POINTER(C.c_uint64)]
         _lib = lib
@@ -82,6 +88,12 @@ def load_ref():
             for op in ("fused", "naive"):
                 getattr(lib, f"ref_tconv_{op}_{nm}").argtypes = [
                     T, C.c_int, C.c_int, C.c_int, T, C.c_int, C.c_int, C.c_int, C.c_int, T]
+        for nm, T in (("f32", fp), ("f64", dp)):
+            getattr(lib, f"ref_tconv_backward_{nm}").argtypes = [
+                T, C.c_int, C.c_int, C.c_int, T, C.c_int, C.c_int, C.c_int, C.c_int, T, T, T]
+        lib.ref_time_backward_f32.argtypes = [
+            fp, C.c_int, C.c_int, C.c_int, fp, C.c_int, C.c_int, C.c_int, C.c_int, fp, C.c_int,
+            fp, fp, dp]
         lib.ref_tconv_fused_parallel_f32.argtypes = [
             fp, C.c_int, C.c_int, C.c_int, fp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, fp]
         lib.ref_count_ops.argtypes = [C.c_int] * 6 + [C.POINTER(C.c_uint64)]
@@ -205,6 +217,38 @@ def scatter_f64(x, k, p):
     return out[0] if squeeze else out
 
 
+def _backward(fn_name, x, k, p, gy, lib, force_f64=False):
+    x = np.asarray(x)
+    f64 = force_f64 or x.dtype == np.float64
+    cast = _f64 if f64 else _f32
+    x, k, gy = cast(x), cast(k), cast(gy)
+    squeeze = x.ndim == 3
+    if squeeze:
+        x, gy = x[None], gy[None]
+    b, n, _, cin = x.shape
+    kh, kw, _, cout = k.shape
+    g = geometry(n, kh, kw, p)
+    if gy.shape != (b, g.out_h, g.out_w, cout):
+        raise OracleError(2, f"output gradient shape {gy.shape} != {(b, g.out_h, g.out_w, cout)}")
+    gx = np.empty_like(x)
+    gk = np.empty_like(k)
+    T = C.c_double if f64 else C.c_float
+    fn = getattr(lib, fn_name if force_f64 else f"{fn_name}_{'f64' if f64 else 'f32'}")
+    _check(fn(_ptr(x, T), b, n, cin, _ptr(k, T), kh, kw, cout, p, _ptr(gy, T), _ptr(gx, T),
+              _ptr(gk, T)), lib)
+    return (gx[0] if squeeze else gx), gk
+
+
+def tconv_backward(x, k, p, gy):
+    """(input grad, kernel grad) of the fused layer, reference order (layers.hpp:171-211);
+    the kernel grad is summed over the batch."""
+    return _backward("orc_tconv_backward", x, k, p, gy, load_oracle())
+
+
+def scatter_backward_f64(x, k, p, gy):
+    return _backward("orc_scatter_backward_f64", x, k, p, gy, load_oracle(), force_f64=True)
+
+
 def count_ops(n, cin, cout, kh, kw, p):
     """(naive_mults, naive_adds, fused_mults, fused_adds)."""
     o = (C.c_uint64 * 4)()
@@ -259,6 +303,26 @@ def ref_tconv_fused_parallel(x, k, p, workers):
     _check(lib.ref_tconv_fused_parallel_f32(_ptr(x, C.c_float), b, n, cin, _ptr(k, C.c_float), kh,
                                             kw, cout, p, workers, _ptr(out, C.c_float)), lib)
     return out[0] if squeeze else out
+
+
+def ref_tconv_backward(x, k, p, gy):
+    """The reference's own net::FusedTConv forward + backward per image."""
+    return _backward("ref_tconv_backward", x, k, p, gy, load_ref())
+
+
+def ref_time_backward(x, k, p, gy, workers):
+    """Times the reference backward (threads over the batch); returns (gx, gk, seconds)."""
+    x, k, gy = _f32(x), _f32(k), _f32(gy)
+    b, n, _, cin = x.shape
+    kh, kw, _, cout = k.shape
+    gx, gk = np.empty_like(x), np.empty_like(k)
+    secs = C.c_double()
+    lib = load_ref()
+    fp = C.c_float
+    _check(lib.ref_time_backward_f32(_ptr(x, fp), b, n, cin, _ptr(k, fp), kh, kw, cout, p,
+                                     _ptr(gy, fp), workers, _ptr(gx, fp), _ptr(gk, fp),
+                                     C.byref(secs)), lib)
+    return gx, gk, secs.value
 
 
 def ref_count_ops(n, cin, cout, kh, kw, p):

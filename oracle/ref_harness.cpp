@@ -12,6 +12,7 @@
 #include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <memory>
 #include <random>
 #include <string>
 #include <thread>
@@ -20,6 +21,7 @@
 #include "segconv/analysis.hpp"
 #include "segconv/fused_tconv.hpp"
 #include "segconv/geometry.hpp"
+#include "segconv/netdemo/layers.hpp"
 #include "segconv/reference_ops.hpp"
 #include "segconv/segregation.hpp"
 #include "segconv/tensor.hpp"
@@ -78,6 +80,31 @@ int run_batch(int variant, const T* x, int batch, int n, int cin, const T* k, in
         y = segconv::transpose_conv_fused_parallel(in, sks, geom, workers);
       std::memcpy(out + b * osz, y.data(), osz * sizeof(T));
     }
+  });
+}
+
+
+// Backward of the reference's trainable fused layer (netdemo/layers.hpp:171-211)
+// over a batch: one FusedTConv, grads zeroed once (model.hpp:192), then per
+// image forward + backward; gx per image, gk = the accumulated tap gradient.
+template <typename T>
+int run_backward(const T* x, int batch, int n, int cin, const T* k, int kh, int kw, int cout,
+                 int p, const T* gy, T* gx, T* gk) {
+  return guarded([&] {
+    segconv::net::FusedTConv<T> layer(kernel(k, kh, kw, cin, cout), p);
+    for (auto& blk : layer.params()) std::fill(blk.grads, blk.grads + blk.size, T(0));
+    const auto geom = segconv::tconv_geometry(n, kh, kw, p);
+    const size_t isz = (size_t)n * n * cin;
+    const size_t osz = (size_t)geom.out_h * geom.out_w * cout;
+    for (int b = 0; b < batch; ++b) {
+      layer.forward(image(x + b * isz, n, cin));
+      const auto g = segconv::Tensor<T>::from_data(geom.out_h, geom.out_w, cout,
+                                                   std::vector<T>(gy + b * osz, gy + (b + 1) * osz));
+      const auto gi = layer.backward(g);
+      std::memcpy(gx + b * isz, gi.data(), isz * sizeof(T));
+    }
+    const auto blk = layer.params()[0];
+    std::memcpy(gk, blk.grads, blk.size * sizeof(T));
   });
 }
 
@@ -243,6 +270,61 @@ int ref_time_fused_batch_f32(int mode, const float* x, int batch, int n, int cin
       const int nt = std::max(1, std::min(workers, batch));
       for (int t = 0; t < nt; ++t) pool.emplace_back(work);
       for (auto& th : pool) th.join();
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    *seconds = std::chrono::duration<double>(t1 - t0).count();
+  });
+}
+
+int ref_tconv_backward_f32(const float* x, int batch, int n, int cin, const float* k, int kh,
+                           int kw, int cout, int p, const float* gy, float* gx, float* gk) {
+  return run_backward<float>(x, batch, n, cin, k, kh, kw, cout, p, gy, gx, gk);
+}
+int ref_tconv_backward_f64(const double* x, int batch, int n, int cin, const double* k, int kh,
+                           int kw, int cout, int p, const double* gy, double* gx, double* gk) {
+  return run_backward<double>(x, batch, n, cin, k, kh, kw, cout, p, gy, gx, gk);
+}
+
+// CPU baseline timing of the reference backward: `workers` threads each own a
+// FusedTConv and run forward + backward over a contiguous slice of the batch
+// (the layer caches its input, so one layer cannot be shared across threads);
+// the per-thread tap gradients are summed inside the timed region.
+int ref_time_backward_f32(const float* x, int batch, int n, int cin, const float* k, int kh, int kw,
+                          int cout, int p, const float* gy, int workers, float* gx, float* gk,
+                          double* seconds) {
+  return guarded([&] {
+    const auto geom = segconv::tconv_geometry(n, kh, kw, p);
+    const size_t isz = (size_t)n * n * cin;
+    const size_t osz = (size_t)geom.out_h * geom.out_w * cout;
+    const size_t ksz = (size_t)kh * kw * cin * cout;
+    const int nt = std::max(1, std::min(workers, batch));
+    std::vector<std::unique_ptr<segconv::net::FusedTConv<float>>> layers;
+    for (int t = 0; t < nt; ++t) {
+      layers.emplace_back(new segconv::net::FusedTConv<float>(kernel(k, kh, kw, cin, cout), p));
+      for (auto& blk : layers.back()->params()) std::fill(blk.grads, blk.grads + blk.size, 0.0f);
+    }
+    std::vector<segconv::Tensor<float>> ins, gs;
+    for (int b = 0; b < batch; ++b) {
+      ins.push_back(image(x + b * isz, n, cin));
+      gs.push_back(segconv::Tensor<float>::from_data(
+          geom.out_h, geom.out_w, cout, std::vector<float>(gy + b * osz, gy + (b + 1) * osz)));
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t)
+      pool.emplace_back([&, t] {
+        const int b0 = (int)((long long)batch * t / nt), b1 = (int)((long long)batch * (t + 1) / nt);
+        for (int b = b0; b < b1; ++b) {
+          layers[t]->forward(ins[b]);
+          const auto gi = layers[t]->backward(gs[b]);
+          std::memcpy(gx + b * isz, gi.data(), isz * sizeof(float));
+        }
+      });
+    for (auto& th : pool) th.join();
+    std::memset(gk, 0, ksz * sizeof(float));
+    for (int t = 0; t < nt; ++t) {
+      const float* g = layers[t]->params()[0].grads;
+      for (size_t e = 0; e < ksz; ++e) gk[e] += g[e];
     }
     const auto t1 = std::chrono::steady_clock::now();
     *seconds = std::chrono::duration<double>(t1 - t0).count();

@@ -16,6 +16,13 @@ Fixtures (all small):
   real_cases.npz     U[-1,1] float cases incl. BASELINE-shaped reductions, with
                      the reference's fused and naive outputs
   f64_case.npz       a double-precision case (proj/tests/test_fused.cpp:61-70)
+  backward.npz       input and kernel gradients of net::FusedTConv (forward +
+                     backward per image, grads zeroed once per batch;
+                     proj/include/segconv/netdemo/layers.hpp:171-211) on the
+                     FD-test shape family (proj/tests/test_netdemo.cpp:137-152),
+                     rectangular kernels, batches, integer and double cases
+                     (`python tests/golden/make_golden.py backward` rewrites
+                     only this file)
 """
 from __future__ import annotations
 
@@ -140,8 +147,42 @@ def main():
     k = r64.uniform(-1, 1, (5, 5, 2, 3))
     np.savez_compressed(os.path.join(OUT, "f64_case.npz"), x=x, k=k, p=np.int32(2),
                         fused=oracle.ref_tconv_fused(x, k, 2), naive=oracle.ref_tconv_naive(x, k, 2))
+    backward()
     print("golden fixtures written to", OUT)
 
 
+def backward():
+    rng = np.random.default_rng(137152)
+    specs = []  # (batch, n, cin, cout, kh, kw, p, kind)
+    while len(specs) < 20:  # the FD-test family: n 3-6, p 0-3, k 1-5, cin 1-2, cout 1-3
+        n, p, k = int(rng.integers(3, 7)), int(rng.integers(0, 4)), int(rng.integers(1, 6))
+        if 2 * n + 2 * p - k < 1 or k > 2 * n - 1 + 2 * p:
+            continue
+        specs.append((1, n, int(rng.integers(1, 3)), int(rng.integers(1, 4)), k, k, p, "real"))
+    specs += [(3, 5, 3, 2, 3, 4, 2, "real"), (2, 4, 2, 3, 4, 3, 1, "real"), (4, 6, 4, 5, 4, 4, 2, "real"),
+              (2, 8, 16, 8, 3, 3, 0, "real"), (3, 4, 32, 16, 4, 4, 0, "real"), (2, 5, 8, 8, 5, 5, 3, "real"),
+              (3, 6, 8, 4, 4, 4, 2, "int"), (2, 5, 6, 3, 3, 3, 1, "int"), (2, 5, 2, 3, 5, 5, 2, "f64")]
+    out = {"count": np.int32(len(specs))}
+    for i, (b, n, cin, cout, kh, kw, p, kind) in enumerate(specs):
+        g = oracle.ref_geometry(n, kh, kw, p)
+        if kind == "int":
+            x = rng.integers(-3, 4, (b, n, n, cin)).astype(np.float32)
+            k = rng.integers(-2, 3, (kh, kw, cin, cout)).astype(np.float32)
+            gy = rng.integers(-2, 3, (b, g.out_h, g.out_w, cout)).astype(np.float32)
+        else:
+            dt = np.float64 if kind == "f64" else np.float32
+            x = rng.uniform(-1, 1, (b, n, n, cin)).astype(dt)
+            k = rng.uniform(-1, 1, (kh, kw, cin, cout)).astype(dt)
+            gy = rng.uniform(-1, 1, (b, g.out_h, g.out_w, cout)).astype(dt)
+        gx, gk = oracle.ref_tconv_backward(x, k, p, gy)
+        out[f"b{i}_dims"] = np.array([b, n, cin, cout, kh, kw, p], dtype=np.int32)
+        out[f"b{i}_x"], out[f"b{i}_k"], out[f"b{i}_gy"] = x, k, gy
+        out[f"b{i}_gx"], out[f"b{i}_gk"] = gx, gk
+    np.savez_compressed(os.path.join(OUT, "backward.npz"), **out)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["backward"]:
+        backward()
+    else:
+        main()

@@ -160,3 +160,81 @@ def test_reference_shim_live():
         np.testing.assert_array_equal(oracle.tconv_fused(x, kk, p), oracle.ref_tconv_fused(x, kk, p))
         np.testing.assert_array_equal(oracle.ref_tconv_fused_parallel(x, kk, p, 3),
                                       oracle.ref_tconv_fused(x, kk, p))
+
+
+# ---------------------------------------------------------------- backward
+def _bwd_cases():
+    z = _npz("backward.npz")
+    for i in range(int(z["count"])):
+        yield i, [int(v) for v in z[f"b{i}_dims"]], z[f"b{i}_x"], z[f"b{i}_k"], z[f"b{i}_gy"], \
+            z[f"b{i}_gx"], z[f"b{i}_gk"]
+
+
+def test_backward_bit_exact_vs_reference_goldens():
+    """oracle.tconv_backward == net::FusedTConv::backward (layers.hpp:171-211), bit for bit,
+    float and double, batches with the kernel gradient summed over images."""
+    n_cases = 0
+    for i, dims, x, k, gy, gx, gk in _bwd_cases():
+        p = dims[6]
+        got_x, got_k = oracle.tconv_backward(x, k, p, gy)
+        assert got_x.dtype == gx.dtype
+        np.testing.assert_array_equal(got_x, gx, err_msg=f"case {i} dims {dims}")
+        np.testing.assert_array_equal(got_k, gk, err_msg=f"case {i} dims {dims}")
+        n_cases += 1
+    assert n_cases >= 25
+
+
+def test_backward_matches_independent_scatter_form():
+    """The scatter-form gradients (sharing no code with the restatement) agree in double."""
+    for i, dims, x, k, gy, gx, gk in _bwd_cases():
+        sx, sk = oracle.scatter_backward_f64(x, k, dims[6], gy)
+        tol = 1e-12 if x.dtype == np.float64 else 1e-4
+        np.testing.assert_allclose(sx, gx, rtol=0, atol=tol * max(1.0, np.abs(sx).max()))
+        np.testing.assert_allclose(sk, gk, rtol=0, atol=tol * max(1.0, np.abs(sk).max()))
+
+
+@pytest.mark.parametrize("n,cin,cout,k,p", [(3, 1, 2, 3, 0), (4, 2, 1, 4, 2), (3, 2, 3, 5, 3),
+                                             (4, 1, 1, 1, 1)])
+def test_backward_finite_differences(n, cin, cout, k, p):
+    """Central differences of L = sum(G * fused(x, k)) confirm both gradients
+    (the reference's own check, tests/test_netdemo.cpp:55-101,137-152)."""
+    rng = np.random.default_rng(n * 100 + k * 10 + p)
+    x = rng.uniform(-1, 1, (1, n, n, cin))
+    kk = rng.uniform(-1, 1, (k, k, cin, cout))
+    g = oracle.geometry(n, k, k, p)
+    G = rng.uniform(-1, 1, (1, g.out_h, g.out_w, cout))
+    gx, gk = oracle.tconv_backward(x, kk, p, G)
+    eps = 1e-6
+
+    def loss(xx, kk2):
+        return float((oracle.tconv_fused(xx, kk2, p) * G).sum())
+
+    for arr, grad, is_x in ((x, gx, True), (kk, gk, False)):
+        flat = arr.reshape(-1)
+        for e in range(flat.size):
+            s = flat[e]
+            flat[e] = s + eps
+            lp = loss(x, kk)
+            flat[e] = s - eps
+            lm = loss(x, kk)
+            flat[e] = s
+            fd = (lp - lm) / (2 * eps)
+            assert abs(fd - grad.reshape(-1)[e]) <= 1e-6 * max(1.0, abs(fd)), (is_x, e)
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference shim not built")
+def test_backward_reference_live():
+    rng = np.random.default_rng(11)
+    for (b, n, cin, cout, k, p) in [(2, 5, 3, 4, 3, 0), (3, 6, 2, 5, 4, 2), (1, 3, 1, 1, 5, 3)]:
+        x = rng.uniform(-1, 1, (b, n, n, cin)).astype(np.float32)
+        kk = rng.uniform(-1, 1, (k, k, cin, cout)).astype(np.float32)
+        g = oracle.geometry(n, k, k, p)
+        gy = rng.uniform(-1, 1, (b, g.out_h, g.out_w, cout)).astype(np.float32)
+        a = oracle.tconv_backward(x, kk, p, gy)
+        r = oracle.ref_tconv_backward(x, kk, p, gy)
+        np.testing.assert_array_equal(a[0], r[0])
+        np.testing.assert_array_equal(a[1], r[1])
+        gx, gk, secs = oracle.ref_time_backward(x, kk, p, gy, 2)
+        np.testing.assert_array_equal(gx, r[0])
+        np.testing.assert_allclose(gk, r[1], rtol=0, atol=1e-5)
+        assert secs >= 0
