@@ -165,6 +165,33 @@ segconv_status segconv_transpose_conv_fused_host(const void* h_x, void* d_x, seg
                                                  segconv_math math, void* d_y, void* h_y,
                                                  segconv_dtype y_dtype, int chunks, void* stream);
 
+/* ------------------------------------------------------------- backward */
+/* reference netdemo/layers.hpp:171-211 (net::FusedTConv<T>::backward), batched:
+ * the gradients of the fused layer with respect to its input and its kernel.
+ * d_x is the forward input (batch, n_in, n_in, cin), d_gy the output gradient
+ * (batch, out_h, out_w, cout), d_kernel the ORIGINAL (kh, kw, cin, cout) kernel,
+ * all of `dtype`.  Outputs (either may be NULL to skip it, not both):
+ *   d_gx  (batch, n_in, n_in, cin) of `dtype`: the output gradient scattered
+ *         back through the sub-kernels, cropped by p_fused (layers.hpp:178-210);
+ *   d_gk  (kh, kw, cin, cout), F32 (F64 for F64 data): tap gradients at the
+ *         original tap positions, summed over the batch.  accumulate != 0 adds
+ *         to the existing contents, as the reference's grad_ accumulates over
+ *         backward calls between zero_grads (netdemo/model.hpp:192-201).
+ * math: EXACT (float/double: the reference's accumulation order, no FMA --
+ * bit-identical to the reference), FFMA (SIMT tiles), BF16 (bf16 data: the
+ * input gradient on the tcgen05 CTA-pair kernel, a stride-2 im2col walk over
+ * gy, when cout % 64 == 0 and cin >= 64; the kernel gradient on SIMT tiles
+ * with fp32 accumulation), AUTO (BF16 for bf16 data, FFMA otherwise).
+ * Errors: geometry ShapeError/ContractError as segconv_tconv_geometry; the
+ * reference's "backward before forward" StateError has no counterpart (the
+ * forward input is an argument). */
+segconv_status segconv_transpose_conv_fused_backward(const void* d_x, const void* d_gy,
+                                                     segconv_dtype dtype, int batch, int n_in,
+                                                     int cin, const void* d_kernel, int kh, int kw,
+                                                     int cout, int p_orig, segconv_math math,
+                                                     void* d_gx, void* d_gk, int accumulate,
+                                                     void* stream);
+
 /* Which math AUTO resolves to for this problem (no launch). */
 segconv_math segconv_select_math(segconv_dtype x_dtype, segconv_dtype panel_dtype, int cin,
                                  int cout, int kh, int kw);

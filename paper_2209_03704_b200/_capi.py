@@ -59,6 +59,8 @@ SIGNATURES = {
     "segconv_transpose_conv_fused_host": (_i, [_vp, _vp, _i, _i, _i, _i, C.POINTER(SubKernels),
                                                _vp, C.POINTER(Geometry), _vp, _u, _i, _vp, _vp,
                                                _i, _i, _vp]),
+    "segconv_transpose_conv_fused_backward": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _i, _i, _i,
+                                                   _i, _i, _vp, _vp, _i, _vp]),
     "segconv_select_math": (_i, [_i, _i, _i, _i, _i, _i]),
     "segconv_upsample2x_pad": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _vp]),
     "segconv_conv2d_valid": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _i, _vp, _u, _vp, _vp]),

@@ -463,6 +463,80 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
   }
 }
 
+// ------------------------------------------------------------ backward
+segconv_status segconv_transpose_conv_fused_backward(const void* d_x, const void* d_gy, segconv_dtype dtype,
+                                                     int batch, int n_in, int cin, const void* d_kernel,
+                                                     int kh, int kw, int cout, int p_orig, segconv_math math,
+                                                     void* d_gx, void* d_gk, int accumulate, void* stream) {
+  segconv_geometry g;
+  segconv_status st = segconv_tconv_geometry(n_in, kh, kw, p_orig, &g);
+  if (st != SEGCONV_OK) return st;
+  if (batch < 0) return fail(SEGCONV_E_CONTRACT, "batch must be >= 0, got %d", batch);
+  if (cin < 1 || cout < 1) return fail(SEGCONV_E_SHAPE, "channel counts must be >= 1, got %d, %d", cin, cout);
+  if (!valid_dtype(dtype)) return fail(SEGCONV_E_CONTRACT, "unknown dtype %d", (int)dtype);
+  if (!d_gx && !d_gk) return fail(SEGCONV_E_CONTRACT, "neither an input nor a kernel gradient was requested");
+  if (batch > 0) {  // an empty batch may come with null activation pointers
+    if (!d_gy) return fail(SEGCONV_E_CONTRACT, "null output gradient");
+    if (d_gx && !d_kernel) return fail(SEGCONV_E_CONTRACT, "the input gradient needs the kernel");
+    if (d_gk && !d_x) return fail(SEGCONV_E_CONTRACT, "the kernel gradient needs the forward input");
+  }
+  if (math == SEGCONV_MATH_AUTO)
+    math = dtype == SEGCONV_BF16 ? SEGCONV_MATH_BF16 : SEGCONV_MATH_FFMA;
+  if (math == SEGCONV_MATH_EXACT && dtype == SEGCONV_BF16)
+    return fail(SEGCONV_E_CONTRACT, "EXACT math is defined for float and double (the reference's types)");
+  if (math == SEGCONV_MATH_BF16 && dtype != SEGCONV_BF16)
+    return fail(SEGCONV_E_CONTRACT, "BF16 math needs bf16 tensors");
+  if (math != SEGCONV_MATH_EXACT && math != SEGCONV_MATH_FFMA && math != SEGCONV_MATH_BF16)
+    return fail(SEGCONV_E_UNSUPPORTED, "math mode %d has no backward kernels in this build", (int)math);
+
+  BackwardProblem pr{};
+  pr.x = d_x;
+  pr.gy = d_gy;
+  pr.k = d_kernel;
+  pr.dtype = dtype;
+  pr.batch = batch;
+  pr.n = n_in;
+  pr.cin = cin;
+  pr.cout = cout;
+  pr.kh = kh;
+  pr.kw = kw;
+  pr.p = p_orig;
+  pr.pf = g.p_fused;
+  pr.out_h = g.out_h;
+  pr.out_w = g.out_w;
+  pr.gx = d_gx;
+  pr.gk = d_gk;
+  pr.accumulate = accumulate ? 1 : 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool exact = math == SEGCONV_MATH_EXACT;
+  const char* dpath = "";
+  if (d_gx) {
+    if (math == SEGCONV_MATH_BF16 && tc_bwd_data_supported(pr)) {
+      dpath = "tc-pair";
+      st = cuda_status(launch_tc_bwd_data(pr, s), "transpose_conv_fused_backward[input, tcgen05 pair]");
+    } else {
+      dpath = exact ? "simt-exact" : "simt-ffma";
+      st = cuda_status(launch_bwd_data_simt(pr, exact, s), "transpose_conv_fused_backward[input]");
+    }
+    if (st != SEGCONV_OK) return st;
+  }
+  const char* wpath = "-";
+  if (d_gk) {
+    if (math == SEGCONV_MATH_BF16 && tc_bwd_weight_supported(pr)) {
+      wpath = "tc-pair";
+      st = cuda_status(launch_tc_bwd_weight(pr, s), "transpose_conv_fused_backward[kernel, tcgen05 pair]");
+    } else {
+      wpath = exact ? "simt-exact" : "simt-ffma";
+      st = cuda_status(launch_bwd_weight_simt(pr, exact, s), "transpose_conv_fused_backward[kernel]");
+    }
+    if (st != SEGCONV_OK) return st;
+  }
+  static thread_local char path[48];
+  snprintf(path, sizeof path, "bwd:%s+%s", d_gx ? dpath : "-", wpath);
+  g_path = path;
+  return SEGCONV_OK;
+}
+
 // Host-buffer pipeline over batch slices (see the header).  Copy streams and
 // events are created once per thread and device.
 namespace {

@@ -32,6 +32,27 @@ struct FusedProblem {
   int y_dtype;
 };
 
+// Backward pass of the fused layer (reference netdemo/layers.hpp:171-211).
+// x, gy, k share `dtype`; gx has dtype; gk is F32 (F64 for F64 data).
+struct BackwardProblem {
+  const void* x;
+  const void* gy;
+  const void* k;  // original (kh, kw, cin, cout) kernel
+  int dtype;
+  int batch, n, cin, cout, kh, kw, p, pf, out_h, out_w;
+  void* gx;
+  void* gk;
+  int accumulate;  // gk += (the reference accumulates tap gradients across calls)
+};
+cudaError_t launch_bwd_data_simt(const BackwardProblem& pr, bool exact, cudaStream_t s);
+cudaError_t launch_bwd_weight_simt(const BackwardProblem& pr, bool exact, cudaStream_t s);
+bool tc_bwd_data_supported(const BackwardProblem& pr);
+cudaError_t launch_tc_bwd_data(const BackwardProblem& pr, cudaStream_t s);
+bool tc_bwd_weight_supported(const BackwardProblem& pr);
+cudaError_t launch_tc_bwd_weight(const BackwardProblem& pr, cudaStream_t s);
+cudaError_t launch_wgrad_reduce(const float* ws, float* gk, long long ksz, int splits, int accumulate,
+                                cudaStream_t s);
+
 cudaError_t launch_segregate(const void* k, int k_dtype, int kh, int kw, int cin, int cout,
                              int cout_pad, int layout, const SegClasses& cls, void* panels,
                              int p_dtype, long long total, cudaStream_t s);

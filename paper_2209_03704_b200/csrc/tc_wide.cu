@@ -51,7 +51,7 @@ using namespace tc;
 constexpr int NUM_THREADS = 224;
 constexpr int SMEM_LIMIT = 227 * 1024;
 constexpr int KB = 64;  // channels per stage: one 128-byte row
-constexpr int MAX_TAPS_Q = 16;
+constexpr int MAX_TAPS_Q = 25;  // 5x5: the input-gradient walk uses every tap as one class
 constexpr int MAX_STAGES_A = 8, MAX_STAGES_B = 12;
 
 struct Params {
@@ -78,6 +78,21 @@ struct Params {
   int im2col;
   long long unit_base[5];  // first unit of class q (units are class-major)
   int tap_off_r[4][MAX_TAPS_Q], tap_off_c[4][MAX_TAPS_Q];
+  // walk origin of anchor (i, j): (wscale * i + wbase_r, wscale * j + wbase_c);
+  // output pixel of anchor (i, j) of class (r, c): (ostride * i + r, ostride * j + c).
+  // Forward: wscale 1, wbase -p_fused, ostride 2.  Input gradient (launch_tc_bwd_data):
+  // wscale 2 (stride-2 im2col walk over gy), ostride 1, one class holding every tap.
+  int wscale, wbase_r, wbase_c, ostride;
+  int b_tap_last;  // B map coordinates (k, n, tap) instead of (k, tap, n)
+  // WGRAD (mode 1, launch_tc_bwd_weight): per unit (split s, tap t, 256-channel pair
+  // tile ct, feature tile nt), D[ch, f] = sum over the split's 64-pixel chunks of
+  // x[m, ch] * gy[b, 2i+p-U, 2j+p-V, f].  Both operands are MN-major (channels /
+  // features contiguous, pixels = K): A from a 2-D map over x, B from the
+  // stride-2 im2col walk over gy.  Results go to wout (+ s * ksz when split).
+  int mode;
+  int w_kw, w_taps, w_ch_pairs, w_splits, w_cin, w_cout, w_direct, w_accumulate;
+  long long w_chunks, w_cps, w_ksz;
+  float* wout;
   unsigned long long* trace;
   int debug;
 };
@@ -177,6 +192,29 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
 __host__ __device__ constexpr uint32_t idesc_bf16_m256(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
+// both operands MN-major (a_major bit 15, b_major bit 16)
+__host__ __device__ constexpr uint32_t idesc_bf16_m256_mn(int n) {
+  return idesc_bf16_m256(n) | (1u << 15) | (1u << 16);
+}
+// SW128 MN-major descriptor: 64-element (128-byte) rows along MN, one row per K;
+// LBO = bytes between 64-element MN blocks, SBO = 1024 (8 K rows per atom)
+__device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t addr, uint32_t lbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+// WGRAD unit k of this pair -> (split, tap, channel pair tile, feature tile)
+__device__ __forceinline__ bool wunit_of(const Params& p, int k, int& s, int& t, int& ct, int& nt) {
+  const long long pairs = gridDim.x / 2;
+  long long u = (long long)(blockIdx.x / 2) + (long long)k * pairs;
+  if (u >= p.units) return false;
+  nt = (int)(u % p.n_tiles);
+  u /= p.n_tiles;
+  ct = (int)(u % p.w_ch_pairs);
+  u /= p.w_ch_pairs;
+  t = (int)(u % p.w_taps);
+  s = (int)(u / p.w_taps);
+  return true;
+}
 
 __device__ __forceinline__ void trace_ev(const Params& p, int ev, int local) {
   if (p.trace == nullptr || blockIdx.x >= 160 || local >= 64) return;
@@ -272,7 +310,43 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (warp == 4) {
     // ===== TMA producer (both CTAs): own halo rows and own half of the features
-    if (lane == 0) {
+    if (lane == 0 && p.mode == 1) {
+      griddep_wait();
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
+      int s, t, ct, nt;
+      const int img = p.n * p.n;
+      for (int k = 0; wunit_of(p, k, s, t, ct, nt); ++k) {
+        const int ch0 = ct * 256 + (int)rank * 128, f0 = nt * p.NT + (int)rank * NT2;
+        const long long c1 = min(p.w_chunks, (long long)(s + 1) * p.w_cps);
+        for (long long c = (long long)s * p.w_cps; c < c1; ++c) {
+          const long long m = c * 64;
+          const int b0 = (int)(m / img), rem = (int)(m - (long long)b0 * img);
+          const int i0 = rem / p.n, j0 = rem - (rem / p.n) * p.n;
+          mbar_wait(&a_empty[sa], pa ^ 1);
+          const uint32_t af = mapa(smem_u32(&a_full[sa]), 0);
+          if (rank == 0) mbar_arrive_expect_tx(&a_full[sa], 2 * 2 * 64 * 128);
+          const uint32_t ad = smem_u32(a_base + (size_t)sa * p.a_stage_bytes);
+          tma2_load_2d(ad, &maps.x, ch0, (int)m, af);
+          tma2_load_2d(ad + 8192, &maps.x, ch0 + 64, (int)m, af);
+          if (++sa == SA) {
+            sa = 0;
+            pa ^= 1;
+          }
+          mbar_wait(&b_empty[sb], pb ^ 1);
+          const uint32_t bf = mapa(smem_u32(&b_full[sb]), 0);
+          if (rank == 0) mbar_arrive_expect_tx(&b_full[sb], 2 * (uint32_t)NT2 * 128);
+          const uint32_t bd = smem_u32(b_base + (size_t)sb * p.b_stage_bytes);
+          for (int h = 0; h < NT2 / 64; ++h)
+            tma2_load_im2col(bd + h * 8192, &maps.xi[0], f0 + 64 * h, 2 * j0 + p.wbase_c, 2 * i0 + p.wbase_r,
+                             b0, (uint16_t)p.tap_off_c[0][t], (uint16_t)p.tap_off_r[0][t], bf);
+          if (++sb == SB) {
+            sb = 0;
+            pb ^= 1;
+          }
+        }
+      }
+    } else if (lane == 0) {
       griddep_wait();  // activations come from the previous kernel (stack layer)
       int sa = 0, sb = 0;
       uint32_t pa = 0, pb = 0;
@@ -297,8 +371,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint32_t af = mapa(smem_u32(&a_full[sa]), 0);
               if (rank == 0) mbar_arrive_expect_tx(&a_full[sa], 2 * 128 * 128);
               tma2_load_im2col(smem_u32(a_base + (size_t)sa * p.a_stage_bytes), &maps.xi[q],
-                               kb * KB, j0 - p.pf, i0 - p.pf, ib, (uint16_t)p.tap_off_c[q][t],
-                               (uint16_t)p.tap_off_r[q][t], af);
+                               kb * KB, p.wscale * j0 + p.wbase_c, p.wscale * i0 + p.wbase_r, ib,
+                               (uint16_t)p.tap_off_c[q][t], (uint16_t)p.tap_off_r[q][t], af);
               if (++sa == SA) {
                 sa = 0;
                 pa ^= 1;
@@ -306,8 +380,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               mbar_wait(&b_empty[sb], pb ^ 1);
               const uint32_t bf = mapa(smem_u32(&b_full[sb]), 0);
               if (rank == 0) mbar_arrive_expect_tx(&b_full[sb], 2 * b_tx);
-              tma2_load_3d(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), &maps.w[q], kb * KB, t,
-                           f0, bf);
+              if (p.b_tap_last)
+                tma2_load_3d(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), &maps.w[q], kb * KB, f0,
+                             t, bf);
+              else
+                tma2_load_3d(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), &maps.w[q], kb * KB, t,
+                             f0, bf);
               if (++sb == SB) {
                 sb = 0;
                 pb ^= 1;
@@ -352,7 +430,51 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   } else if (warp == 5) {
     // ===== MMA issuer (leader CTA; the whole warp runs the loop, one lane issues)
-    if (rank == 0) {
+    if (rank == 0 && p.mode == 1) {
+      const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base, 0);
+      int sa = 0, sb = 0, acc = 0;
+      uint32_t pa = 0, pb = 0, pacc = 0;
+      int s, t, ct, nt;
+      const uint32_t idesc = idesc_bf16_m256_mn(p.NT);
+      for (int k = 0; wunit_of(p, k, s, t, ct, nt); ++k) {
+        mbar_wait(&acc_empty[acc], pacc ^ 1);
+        tc_fence_after();
+        const uint32_t d = tb + (uint32_t)(acc * p.NT);
+        const long long c0 = (long long)s * p.w_cps, c1 = min(p.w_chunks, c0 + p.w_cps);
+        for (long long c = c0; c < c1; ++c) {
+          mbar_wait(&a_full[sa], pa);
+          mbar_wait(&b_full[sb], pb);
+          tc_fence_after();
+          const uint64_t ad = sw128_mn_desc(smem_u32(a_base + (size_t)sa * p.a_stage_bytes), 8192);
+          const uint64_t bd = sw128_mn_desc(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), 8192);
+          if (elect_one()) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)  // K = 16 pixels = 2 atoms of 8 rows: +2048 bytes
+              mma2_bf16(d, ad + 128u * ks, bd + 128u * ks, idesc, (c == c0 && ks == 0) ? 0u : 1u);
+          }
+          __syncwarp();
+          if (elect_one()) {
+            commit2(&a_empty[sa]);
+            commit2(&b_empty[sb]);
+          }
+          __syncwarp();
+          if (++sa == SA) {
+            sa = 0;
+            pa ^= 1;
+          }
+          if (++sb == SB) {
+            sb = 0;
+            pb ^= 1;
+          }
+        }
+        if (elect_one()) commit2(&acc_full[acc]);
+        __syncwarp();
+        if (++acc == 2) {
+          acc = 0;
+          pacc ^= 1;
+        }
+      }
+    } else if (rank == 0) {
       const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base, 0);
       int sa = 0, sb = 0, acc = 0;
       uint32_t pa = 0, pb = 0, pacc = 0;
@@ -434,6 +556,45 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
+  } else if (warp < 4 && p.mode == 1) {
+    // ===== WGRAD epilogue: lane = input channel; 32 features per TMEM load
+    const uint32_t lane_base = tmem_base + ((uint32_t)(warp * 32) << 16);
+    const uint32_t acc_empty_leader0 = mapa(smem_u32(&acc_empty[0]), 0);
+    int acc = 0;
+    uint32_t pacc = 0;
+    int s, t, ct, nt;
+    for (int k = 0; wunit_of(p, k, s, t, ct, nt); ++k) {
+      mbar_wait(&acc_full[acc], pacc);
+      tc_fence_after();
+      const int ch = ct * 256 + (int)rank * 128 + warp * 32 + lane;
+      const bool ok = ch < p.w_cin;
+      float* dst = p.wout + (p.w_direct ? 0LL : (long long)s * p.w_ksz) +
+                   ((long long)t * p.w_cin + (ok ? ch : 0)) * p.w_cout + nt * p.NT;
+#pragma unroll 1
+      for (int c0 = 0; c0 < p.NT; c0 += 32) {
+        float v[32];
+        tmem_ld32(lane_base + (uint32_t)(acc * p.NT + c0), v);
+        if (!ok) continue;
+        float4* o = reinterpret_cast<float4*>(dst + c0);
+        if (p.w_direct && p.w_accumulate) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float4 a = o[e];
+            o[e] = make_float4(a.x + v[4 * e], a.y + v[4 * e + 1], a.z + v[4 * e + 2], a.w + v[4 * e + 3]);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cl(acc_empty_leader0 + (uint32_t)acc * 8);
+      if (++acc == 2) {
+        acc = 0;
+        pacc ^= 1;
+      }
+    }
   } else if (warp < 4) {
     // ===== epilogue: lane = anchor; each thread writes its anchor's features
     const uint32_t lane_base = tmem_base + ((uint32_t)(warp * 32) << 16);
@@ -475,7 +636,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int r = q >> 1, c = q & 1;
       const bool ok = in_range && i < p.rows[q] && j < p.cols[q] && !(p.debug & 1);
       YT* dst = reinterpret_cast<YT*>(p.y) +
-                ((long long)((long long)b * p.out_h + 2 * i + r) * p.out_w + 2 * j + c) * p.cout +
+                ((long long)((long long)b * p.out_h + p.ostride * i + r) * p.out_w + p.ostride * j + c) *
+                    p.cout +
                 nt * p.NT;
       const int fmax = p.cout - nt * p.NT;  // features of this tile that exist
 #pragma unroll 1
@@ -555,6 +717,24 @@ static EncodeTiledFnW encode_fn_w() {
   return fn;
 }
 
+typedef CUresult (*EncIm2colW)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncIm2colW encode_im2col_w() {
+  static EncIm2colW fn = nullptr;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncIm2colW)f;
+  }
+  return fn;
+}
+
 // features per pair tile: the whole (32-padded) cout up to 256
 int tc_wide_ntile(int cout) {
   const int c32 = (cout + 31) / 32 * 32;
@@ -577,6 +757,9 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
   if (pr.panel_layout != SEGCONV_PANEL_KMAJOR) return false;
   if (pr.y_dtype != SEGCONV_BF16 && pr.y_dtype != SEGCONV_F32) return false;
   if (!tc_wide_fits(pr.kh, pr.kw, pr.p, pr.cin, pr.cout)) return false;
+  p.wscale = 1;
+  p.wbase_r = p.wbase_c = -pr.pf;
+  p.ostride = 2;
   p.y = pr.y;
   p.bias = pr.bias;
   p.epi = pr.epi;
@@ -750,6 +933,222 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
   return true;
 }
 
+// Input gradient of the fused layer (reference netdemo/layers.hpp:171-211) on
+// the same pair kernel: gx[m, ch] = sum_{U,V,f} gy[b, 2i+p-U, 2j+p-V, f] k[U,V,ch,f]
+// is one "class" whose K loop runs over every tap (U, V) and cout in 64-feature
+// blocks.  A = a stride-2 im2col walk over gy (origin (2i + p-kh+1, 2j + p-kw+1),
+// tap offset (kh-1-U, kw-1-V); positions outside gy are zero-filled by the TMA),
+// B = the original kernel, whose (U, V, ch, f) layout is already K-major for
+// N = ch -- no flipped or re-laid-out copy is made.
+static bool make_wide_dgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps& maps) {
+  p = tcw::Params{};
+  if (pr.dtype != SEGCONV_BF16) return false;
+  if (pr.cout % tcw::KB != 0 || pr.cin < 64 || pr.cin % 8 != 0) return false;
+  const int taps = pr.kh * pr.kw;
+  if (taps > tcw::MAX_TAPS_Q) return false;
+  const int lo_r = pr.p - pr.kh + 1, lo_c = pr.p - pr.kw + 1;
+  if (lo_r < -128 || lo_c < -128 || pr.p > 128) return false;  // rank-4 im2col corner range
+  if ((long long)pr.batch * pr.n * pr.n * pr.cin >= (1LL << 40)) return false;
+  p.y = pr.gx;
+  p.y_dtype = SEGCONV_BF16;
+  p.batch = pr.batch;
+  p.n = pr.n;
+  p.cin = pr.cout;  // GEMM K channels
+  p.cout = pr.cin;  // GEMM N: input-gradient channels
+  p.out_h = p.out_w = pr.n;
+  p.Mv = (long long)pr.batch * pr.n * pr.n;
+  p.NT = tc_wide_ntile(pr.cin);
+  p.n_tiles = (pr.cin + p.NT - 1) / p.NT;
+  p.nkb = pr.cout / tcw::KB;
+  p.im2col = 1;
+  p.S_rows = 128;
+  p.taps[0] = taps;
+  for (int U = 0; U < pr.kh; ++U)
+    for (int V = 0; V < pr.kw; ++V) {
+      p.tap_off_r[0][U * pr.kw + V] = pr.kh - 1 - U;
+      p.tap_off_c[0][U * pr.kw + V] = pr.kw - 1 - V;
+    }
+  p.rows[0] = p.cols[0] = pr.n;
+  p.wscale = 2;
+  p.wbase_r = lo_r;
+  p.wbase_c = lo_c;
+  p.ostride = 1;
+  p.b_tap_last = 1;
+  p.a_stage_bytes = 128 * 128;
+  p.b_stage_bytes = (p.NT / 2) * 128;
+  if (p.b_stage_bytes % 1024) return false;
+  const int bar_bytes = (2 * tcw::MAX_STAGES_A + 2 * tcw::MAX_STAGES_B + 4) * 8 + 16;
+  p.stages_a = p.stages_b =
+      std::min(tcw::MAX_STAGES_A, (tcw::SMEM_LIMIT - bar_bytes) / (p.a_stage_bytes + p.b_stage_bytes));
+  if (p.stages_a < 2) return false;
+  p.unit_base[0] = 0;
+  const long long u1 = (p.Mv + 255) / 256 * p.n_tiles;
+  for (int q = 1; q <= 4; ++q) p.unit_base[q] = u1;
+  p.units = u1;
+  EncodeTiledFnW fn = encode_fn_w();
+  if (!fn) return false;
+  typedef CUresult (*EncIm2col)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncIm2col enc2 = nullptr;
+  if (!enc2) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess)
+      return false;
+    enc2 = (EncIm2col)f;
+  }
+  {
+    const cuuint64_t dims[4] = {(cuuint64_t)pr.cout, (cuuint64_t)pr.out_w, (cuuint64_t)pr.out_h,
+                                (cuuint64_t)pr.batch};
+    const cuuint64_t strides[3] = {(cuuint64_t)pr.cout * 2, (cuuint64_t)pr.out_w * pr.cout * 2,
+                                   (cuuint64_t)pr.out_h * pr.out_w * pr.cout * 2};
+    // walk: origins lo, lo + 2, ..., out - 1 - p (n per axis); corners {W, H}
+    const int lower[2] = {lo_c, lo_r};
+    const int upper[2] = {-pr.p, -pr.p};
+    const cuuint32_t es[4] = {1, 2, 2, 1};
+    if (enc2(&maps.xi[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pr.gy), dims, strides, lower,
+             upper, (cuuint32_t)tcw::KB, 128, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)pr.cout, (cuuint64_t)pr.cin, (cuuint64_t)taps};
+    const cuuint64_t strides[2] = {(cuuint64_t)pr.cout * 2, (cuuint64_t)pr.cin * pr.cout * 2};
+    const cuuint32_t box[3] = {(cuuint32_t)tcw::KB, (cuuint32_t)(p.NT / 2), 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (fn(&maps.w[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(pr.k), dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  // every map the kernel prefetches must be valid
+  maps.x = maps.xi[0];
+  for (int q = 1; q < 4; ++q) {
+    maps.w[q] = maps.w[0];
+    maps.xi[q] = maps.xi[0];
+  }
+  return true;
+}
+
+// Kernel gradient (reference layers.hpp:196-199: gw[f] += ip[ch] * gp[f]) on the
+// pair kernel, mode 1: gk[t, ch, f] = sum_m x[m, ch] gy[b, 2i+p-U, 2j+p-V, f],
+// M = 256 channels per pair x N = 128/256 features, K = pixels in 64-pixel
+// chunks, both operands MN-major SW128.  The pixel reduction is split so the
+// units fill the pairs evenly; splits > 1 write fp32 partials that
+// launch_wgrad_reduce sums in split order (deterministic).
+static bool make_wide_wgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps& maps, int pairs) {
+  p = tcw::Params{};
+  if (pr.dtype != SEGCONV_BF16 || pr.batch < 1) return false;
+  if (pr.cin % 128 != 0 || pr.cout % 128 != 0) return false;
+  const int taps = pr.kh * pr.kw;
+  if (taps > tcw::MAX_TAPS_Q) return false;
+  const int lo_r = pr.p - pr.kh + 1, lo_c = pr.p - pr.kw + 1;
+  if (lo_r < -128 || lo_c < -128 || pr.p > 128) return false;
+  const long long M = (long long)pr.batch * pr.n * pr.n;
+  if (M + 64 >= (1LL << 31)) return false;
+  p.mode = 1;
+  p.n = pr.n;
+  p.batch = pr.batch;
+  p.NT = pr.cout % 256 == 0 ? 256 : 128;
+  p.n_tiles = pr.cout / p.NT;
+  p.w_kw = pr.kw;
+  p.w_taps = taps;
+  p.w_ch_pairs = (pr.cin + 255) / 256;
+  p.w_cin = pr.cin;
+  p.w_cout = pr.cout;
+  p.w_ksz = (long long)taps * pr.cin * pr.cout;
+  p.w_accumulate = pr.accumulate;
+  p.wbase_r = lo_r;
+  p.wbase_c = lo_c;
+  for (int U = 0; U < pr.kh; ++U)
+    for (int V = 0; V < pr.kw; ++V) {
+      p.tap_off_r[0][U * pr.kw + V] = pr.kh - 1 - U;
+      p.tap_off_c[0][U * pr.kw + V] = pr.kw - 1 - V;
+    }
+  p.w_chunks = (M + 63) / 64;
+  // splits: best wave balance over the pairs, >= 8 chunks per unit (epilogue overlap)
+  const long long base = (long long)taps * p.w_ch_pairs * p.n_tiles;
+  int best = 1;
+  double best_eff = 0;
+  for (int sp = 1; sp <= 64; ++sp) {
+    if (sp > 1 && p.w_chunks / sp < 8) break;
+    const long long units = base * sp;
+    const long long waves = (units + pairs - 1) / pairs;
+    const double eff = (double)units / (double)(waves * pairs);
+    if (eff > best_eff + 0.02) {
+      best_eff = eff;
+      best = sp;
+    }
+  }
+  p.w_cps = (p.w_chunks + best - 1) / best;
+  p.w_splits = (int)((p.w_chunks + p.w_cps - 1) / p.w_cps);
+  p.w_direct = p.w_splits == 1;
+  p.units = base * p.w_splits;
+  p.a_stage_bytes = 2 * 64 * 128;
+  p.b_stage_bytes = (p.NT / 2) * 128;
+  const int bar_bytes = (2 * tcw::MAX_STAGES_A + 2 * tcw::MAX_STAGES_B + 4) * 8 + 16;
+  p.stages_a = p.stages_b =
+      std::min(tcw::MAX_STAGES_A, (tcw::SMEM_LIMIT - bar_bytes) / (p.a_stage_bytes + p.b_stage_bytes));
+  EncodeTiledFnW fn = encode_fn_w();
+  if (!fn) return false;
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)pr.cin, (cuuint64_t)M};
+    const cuuint64_t strides[1] = {(cuuint64_t)pr.cin * 2};
+    const cuuint32_t box[2] = {64, 64};
+    const cuuint32_t es[2] = {1, 1};
+    if (fn(&maps.x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pr.x), dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  EncIm2colW enc2 = encode_im2col_w();
+  if (!enc2) return false;
+  {
+    const cuuint64_t dims[4] = {(cuuint64_t)pr.cout, (cuuint64_t)pr.out_w, (cuuint64_t)pr.out_h,
+                                (cuuint64_t)pr.batch};
+    const cuuint64_t strides[3] = {(cuuint64_t)pr.cout * 2, (cuuint64_t)pr.out_w * pr.cout * 2,
+                                   (cuuint64_t)pr.out_h * pr.out_w * pr.cout * 2};
+    const int lower[2] = {lo_c, lo_r};
+    const int upper[2] = {-pr.p, -pr.p};
+    const cuuint32_t es[4] = {1, 2, 2, 1};
+    if (enc2(&maps.xi[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pr.gy), dims, strides, lower,
+             upper, 64, 64, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  for (int q = 0; q < 4; ++q) {
+    maps.w[q] = maps.x;
+    if (q) maps.xi[q] = maps.xi[0];
+  }
+  return true;
+}
+
+static int wide_pairs() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      sms = 148;
+  }
+  return sms / 2;
+}
+
+bool tc_bwd_weight_supported(const BackwardProblem& pr) {
+  tcw::Params p;
+  tcw::Maps m;
+  return make_wide_wgrad(pr, p, m, wide_pairs());
+}
+
+bool tc_bwd_data_supported(const BackwardProblem& pr) {
+  tcw::Params p;
+  tcw::Maps m;
+  return make_wide_dgrad(pr, p, m);
+}
+
 bool tc_wide_supported(const FusedProblem& pr, int math) {
   if (math != SEGCONV_MATH_BF16) return false;
   tcw::Params p;
@@ -816,6 +1215,34 @@ cudaError_t launch_tc_wide(const FusedProblem& pr, cudaStream_t s) {
   if (act == 1) return launch_wide_t<float, 1>(p, maps, s);
   if (act == 2) return launch_wide_t<float, 2>(p, maps, s);
   return launch_wide_t<float, 0>(p, maps, s);
+}
+
+cudaError_t launch_tc_bwd_weight(const BackwardProblem& pr, cudaStream_t s) {
+  tcw::Params p;
+  tcw::Maps maps;
+  if (!make_wide_wgrad(pr, p, maps, wide_pairs())) return cudaErrorNotSupported;
+  p.trace = nullptr;
+  if (p.w_direct) {
+    p.wout = (float*)pr.gk;
+    return launch_wide_t<float, 0>(p, maps, s);
+  }
+  float* ws = nullptr;
+  cudaError_t e = cudaMallocAsync((void**)&ws, (size_t)p.w_splits * p.w_ksz * sizeof(float), s);
+  if (e != cudaSuccess) return e;
+  p.wout = ws;
+  e = launch_wide_t<float, 0>(p, maps, s);
+  if (e == cudaSuccess) e = launch_wgrad_reduce(ws, (float*)pr.gk, p.w_ksz, p.w_splits, pr.accumulate, s);
+  cudaError_t e2 = cudaFreeAsync(ws, s);
+  return e != cudaSuccess ? e : e2;
+}
+
+cudaError_t launch_tc_bwd_data(const BackwardProblem& pr, cudaStream_t s) {
+  tcw::Params p;
+  tcw::Maps maps;
+  if (!make_wide_dgrad(pr, p, maps)) return cudaErrorNotSupported;
+  if (p.units == 0) return cudaSuccess;
+  p.trace = nullptr;
+  return launch_wide_t<__nv_bfloat16, 0>(p, maps, s);
 }
 
 }  // namespace segconv_b200

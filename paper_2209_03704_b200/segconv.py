@@ -23,12 +23,13 @@ import torch
 from . import _capi as A
 
 __all__ = [
-    "SegconvError", "ShapeError", "ContractError", "CudaError", "UnsupportedError",
+    "SegconvError", "ShapeError", "ContractError", "StateError", "CudaError", "UnsupportedError",
     "TConvGeometry", "tconv_geometry", "first_active_tap", "active_tap_count",
     "class_input_offset", "sub_kernel_dims", "SubKernelSet", "segregate", "transpose_conv_fused",
     "transpose_conv_fused_parallel", "transpose_conv_naive", "conv2d_valid", "upsample2x_pad",
     "tensors_equal_exact", "tensors_equal_approx", "LayerShape", "OpCounts", "count_ops_naive",
     "count_ops_fused", "select_math", "launch_count", "last_path", "MATHS",
+    "transpose_conv_fused_backward", "FusedTConv", "TransposeConvFused",
 ]
 
 
@@ -43,6 +44,11 @@ class ShapeError(SegconvError):
 
 class ContractError(SegconvError):
     """An API precondition was broken (reference errors.hpp:20-23)."""
+
+
+class StateError(SegconvError):
+    """An operation was called out of order, e.g. backward before forward
+    (reference errors.hpp:39, netdemo/layers.hpp:46-48)."""
 
 
 class CudaError(SegconvError):
@@ -366,6 +372,146 @@ def transpose_conv_fused(x: torch.Tensor, k: Union[SubKernelSet, torch.Tensor],
     if host:
         y = y.cpu()
     return y[0] if squeeze else y
+
+
+def transpose_conv_fused_backward(x: torch.Tensor, kernel: torch.Tensor, p_orig: int,
+                                  grad_out: torch.Tensor, *, math: Optional[str] = None,
+                                  input_grad: bool = True, kernel_grad: bool = True,
+                                  grad_kernel: Optional[torch.Tensor] = None):
+    """Gradients of the fused layer -- reference netdemo/layers.hpp:171-211
+    (net::FusedTConv::backward), batched.
+
+    ``x`` (B, N, N, cin) or (N, N, cin) is the forward input, ``kernel`` the
+    original (kh, kw, cin, cout) kernel, ``grad_out`` the output gradient.
+    Returns ``(grad_input, grad_kernel)`` (either None when not requested);
+    grad_input has x's dtype, grad_kernel is float32 (float64 for double data)
+    and summed over the batch.  Passing ``grad_kernel`` accumulates into it, as
+    the reference's grad_ does across backward calls.  ``math``: "exact"
+    (bit-identical to the reference, float/double), "ffma", "bf16", None (auto).
+    """
+    xb, squeeze = _as_batch(x)
+    gb, _ = _as_batch(grad_out)
+    if kernel.dim() != 4:
+        raise ShapeError(f"kernel must be (kh, kw, cin, cout), got {tuple(kernel.shape)}")
+    kh, kw, kcin, cout = (int(v) for v in kernel.shape)
+    b, n, n2, cin = (int(v) for v in xb.shape)
+    if n != n2:
+        raise ContractError(f"fused_tconv expects a square input, got {n}x{n2}")
+    if kcin != cin:
+        raise ContractError(f"channel mismatch: input has {cin}, kernel expects {kcin}")
+    g = tconv_geometry(n, kh, kw, int(p_orig))
+    if tuple(gb.shape) != (b, g.out_h, g.out_w, cout):
+        raise ContractError("fused_tconv: output gradient shape mismatch")
+    if math is not None and math not in MATHS:
+        raise ContractError(f"unknown math {math!r}")
+    dev = _device()
+    dt = xb.dtype
+    xd = xb.to(dev).contiguous()
+    gd = gb.to(dev, dt).contiguous()
+    kd = kernel.to(dev, dt).contiguous()
+    gx = torch.empty_like(xd) if input_grad else None
+    acc_dt = torch.float64 if dt == torch.float64 else torch.float32
+    acc = 0
+    if kernel_grad:
+        if grad_kernel is not None:
+            if tuple(grad_kernel.shape) != (kh, kw, cin, cout) or grad_kernel.dtype != acc_dt or \
+                    not grad_kernel.is_cuda or not grad_kernel.is_contiguous():
+                raise ContractError(f"grad_kernel must be a contiguous {acc_dt} CUDA tensor of the "
+                                    "kernel's shape")
+            gk, acc = grad_kernel, 1
+        else:
+            gk = torch.empty((kh, kw, cin, cout), dtype=acc_dt, device=dev)
+    else:
+        gk = None
+    m = MATHS[math] if math is not None else A.MATH_AUTO
+    _check(A.lib().segconv_transpose_conv_fused_backward(
+        xd.data_ptr(), gd.data_ptr(), _dtype_code(xd), b, n, cin, kd.data_ptr(), kh, kw, cout,
+        int(p_orig), m, gx.data_ptr() if gx is not None else None,
+        gk.data_ptr() if gk is not None else None, acc, _stream()))
+    if gx is not None and squeeze:
+        gx = gx[0]
+    return gx, gk
+
+
+class FusedTConv:
+    """Trainable fused 2x transpose convolution -- the reference's
+    net::FusedTConv<T> (netdemo/layers.hpp:150-230) on the GPU, batched.
+
+    forward(x) caches the input and runs the segregated kernels; backward(g)
+    returns the input gradient and adds the kernel gradient into ``grad``;
+    params() exposes (values, grads); on_params_updated() re-segregates."""
+
+    def __init__(self, kernel: torch.Tensor, p: int, *, math: Optional[str] = None):
+        self.kernel_ = kernel.to(_device()).contiguous()
+        self.p_ = int(p)
+        self.math = math
+        acc_dt = torch.float64 if self.kernel_.dtype == torch.float64 else torch.float32
+        self.grad = torch.zeros(self.kernel_.shape, dtype=acc_dt, device=self.kernel_.device)
+        self._input = None
+        self.on_params_updated()
+
+    def name(self) -> str:
+        return "fused_tconv"
+
+    def kernel(self) -> torch.Tensor:
+        return self.kernel_
+
+    def padding(self) -> int:
+        return self.p_
+
+    def on_params_updated(self) -> None:
+        self.sks_ = segregate(self.kernel_, self.p_, math=self.math or "auto")
+
+    def params(self):
+        return [(self.kernel_, self.grad)]
+
+    def zero_grads(self) -> None:
+        self.grad.zero_()
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        xb, _ = _as_batch(x)
+        if xb.shape[1] != xb.shape[2]:
+            raise ContractError(f"fused_tconv expects a square input, got "
+                                f"{xb.shape[1]}x{xb.shape[2]}")
+        self.geom_ = tconv_geometry(int(xb.shape[1]), int(self.kernel_.shape[0]),
+                                    int(self.kernel_.shape[1]), self.p_)
+        self._input = x.to(_device()).contiguous()
+        return transpose_conv_fused(self._input, self.sks_, self.geom_,
+                                    math=self.math if self.math != "auto" else None)
+
+    def backward(self, g: torch.Tensor) -> torch.Tensor:
+        if self._input is None:
+            raise StateError("fused_tconv: backward called before forward")
+        gx, _ = transpose_conv_fused_backward(self._input, self.kernel_, self.p_, g,
+                                              math=self._bwd_math(), grad_kernel=self.grad)
+        return gx
+
+    def _bwd_math(self):
+        if self.math in (None, "auto"):
+            return None
+        return "bf16" if self.math in ("bf16",) else ("exact" if self.math == "exact" else "ffma")
+
+
+class TransposeConvFused(torch.autograd.Function):
+    """torch.autograd wrapper: y = transpose_conv_fused(x, kernel, p) with the
+    backward of transpose_conv_fused_backward (NHWC tensors, kernel (kh, kw,
+    cin, cout))."""
+
+    @staticmethod
+    def forward(ctx, x, kernel, p):
+        ctx.save_for_backward(x, kernel)
+        ctx.p = int(p)
+        return transpose_conv_fused(x, kernel, int(p))
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        x, kernel = ctx.saved_tensors
+        gx, gk = transpose_conv_fused_backward(
+            x, kernel, ctx.p, grad_out.contiguous(), input_grad=ctx.needs_input_grad[0],
+            kernel_grad=ctx.needs_input_grad[1])
+        if gk is not None:
+            gk = gk.to(kernel.dtype)
+        return gx, gk, None
 
 
 def _fused_host(xb, sks, g, m, bias, activation, out_dtype, out, staging, chunks, sync):

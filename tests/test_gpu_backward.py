@@ -1,0 +1,240 @@
+"""GPU parity of the backward pass of the fused layer (reference
+netdemo/layers.hpp:171-211, net::FusedTConv::backward) against the C oracle,
+which tests/test_oracle.py pins bit-exactly to the reference.
+
+Bars: EXACT math is bit-identical to the reference (golden vectors, float and
+double); FFMA is within 1e-5 of the oracle (scaled error, fp32 summation-order
+differences only) and bit-exact on integer data; the bf16 tensor-core input
+gradient equals the oracle's fp32 result rounded to bf16 on integer data and is
+within 1e-2 (the bf16 output rounding) on real data.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2209_03704_b200 import segconv as sc
+
+pytestmark = pytest.mark.gpu
+G = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+
+
+def scaled_err(got, want):
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    assert got.shape == want.shape
+    if got.size == 0:
+        return 0.0
+    return float((np.abs(got - want) / np.maximum(np.maximum(np.abs(got), np.abs(want)), 1.0)).max())
+
+
+def gpu_bwd(x, k, p, gy, math=None, dtype=None, **kw):
+    dt = dtype or {np.float32: torch.float32, np.float64: torch.float64}[x.dtype.type]
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda().to(dt)  # noqa: E731
+    gx, gk = sc.transpose_conv_fused_backward(t(x), t(k), p, t(gy), math=math, **kw)
+    torch.cuda.synchronize()
+    return (None if gx is None else gx.double().cpu().numpy(),
+            None if gk is None else gk.double().cpu().numpy(), sc.last_path())
+
+
+def test_exact_matches_reference_goldens_bit_for_bit():
+    z = np.load(os.path.join(G, "backward.npz"))
+    for i in range(int(z["count"])):
+        dims = [int(v) for v in z[f"b{i}_dims"]]
+        x, k, gy = z[f"b{i}_x"], z[f"b{i}_k"], z[f"b{i}_gy"]
+        gx, gk, path = gpu_bwd(x, k, dims[6], gy, math="exact")
+        assert path == "bwd:simt-exact+simt-exact"
+        np.testing.assert_array_equal(gx.astype(x.dtype), z[f"b{i}_gx"], err_msg=f"case {i} {dims}")
+        np.testing.assert_array_equal(gk.astype(x.dtype), z[f"b{i}_gk"], err_msg=f"case {i} {dims}")
+
+
+@pytest.mark.parametrize("b,n,cin,cout,k,p", [
+    (2, 16, 64, 32, 3, 0),    # C2 layer shape (reduced batch)
+    (3, 8, 48, 20, 4, 2),     # partial channel tiles, p_fused = 1
+    (1, 5, 3, 7, 5, 3),       # tiny channels, odd p
+    (2, 9, 130, 70, 3, 1),    # channel tiles past 128
+    (4, 6, 16, 8, 1, 0),      # 1x1 kernel: classes without taps
+    (2, 11, 128, 3, 3, 0),    # C5 layer d shape (fp32)
+])
+def test_ffma_f32(b, n, cin, cout, k, p):
+    rng = np.random.default_rng(b * 1000 + n * 10 + k)
+    x = rng.uniform(-1, 1, (b, n, n, cin)).astype(np.float32)
+    kk = (rng.standard_normal((k, k, cin, cout)) * 0.05).astype(np.float32)
+    g = oracle.geometry(n, k, k, p)
+    gy = rng.uniform(-1, 1, (b, g.out_h, g.out_w, cout)).astype(np.float32)
+    wx, wk = oracle.tconv_backward(x, kk, p, gy)
+    gx, gk, path = gpu_bwd(x, kk, p, gy, math="ffma")
+    assert path == "bwd:simt-ffma+simt-ffma"
+    assert scaled_err(gx, wx) <= 1e-5
+    assert scaled_err(gk, wk) <= 1e-5
+
+
+@pytest.mark.parametrize("b,n,cin,cout,k,p", [(3, 6, 8, 5, 4, 2), (2, 12, 64, 32, 3, 0), (64, 4, 16, 16, 3, 1)])
+def test_ffma_int_exact(b, n, cin, cout, k, p):
+    """Integer data: every partial sum is exact, so any summation order is bit-exact."""
+    rng = np.random.default_rng(n * 7 + cin)
+    x = rng.integers(-3, 4, (b, n, n, cin)).astype(np.float32)
+    kk = rng.integers(-2, 3, (k, k, cin, cout)).astype(np.float32)
+    g = oracle.geometry(n, k, k, p)
+    gy = rng.integers(-2, 3, (b, g.out_h, g.out_w, cout)).astype(np.float32)
+    wx, wk = oracle.tconv_backward(x, kk, p, gy)
+    gx, gk, _ = gpu_bwd(x, kk, p, gy, math="ffma")
+    np.testing.assert_array_equal(gx, wx)
+    np.testing.assert_array_equal(gk, wk)
+
+
+def test_f64_ffma_and_exact():
+    rng = np.random.default_rng(3)
+    x = rng.uniform(-1, 1, (2, 7, 7, 5))
+    kk = rng.uniform(-1, 1, (4, 3, 5, 6))
+    g = oracle.geometry(7, 4, 3, 2)
+    gy = rng.uniform(-1, 1, (2, g.out_h, g.out_w, 6))
+    wx, wk = oracle.tconv_backward(x, kk, 2, gy)
+    gx, gk, _ = gpu_bwd(x, kk, 2, gy, math="exact")
+    np.testing.assert_array_equal(gx, wx)
+    np.testing.assert_array_equal(gk, wk)
+    gx, gk, _ = gpu_bwd(x, kk, 2, gy, math="ffma")
+    assert scaled_err(gx, wx) <= 1e-13 and scaled_err(gk, wk) <= 1e-13
+
+
+@pytest.mark.parametrize("b,n,cin,cout,k,p", [
+    (4, 16, 512, 256, 4, 0),  # BASELINE C3 layer (reduced batch)
+    (2, 8, 128, 64, 4, 2),    # DCGAN-standard 4x4, p = 2
+    (3, 5, 64, 128, 3, 1),
+    (2, 7, 96, 64, 5, 2),     # 25 taps, cin not a multiple of 64
+    (2, 4, 256, 512, 3, 0),   # C5 layer b-like: two feature blocks of K
+    (1, 3, 320, 64, 2, 1),    # gx channels over one 256 tile
+    (2, 8, 128, 128, 4, 2),   # kernel grad on the pair kernel: N = 128 features
+    (3, 5, 256, 256, 3, 1),
+    (1, 3, 384, 128, 2, 1),   # kernel grad: second channel pair half empty
+    (64, 8, 128, 128, 3, 0),  # kernel grad: pixel reduction split over units
+])
+def test_bf16_tensor_core_input_grad(b, n, cin, cout, k, p):
+    rng = np.random.default_rng(b * 100 + n + cin)
+    x = rng.integers(-3, 4, (b, n, n, cin)).astype(np.float32)
+    kk = rng.integers(-2, 3, (k, k, cin, cout)).astype(np.float32)
+    g = oracle.geometry(n, k, k, p)
+    gy = rng.integers(-2, 3, (b, g.out_h, g.out_w, cout)).astype(np.float32)
+    wx, wk = oracle.tconv_backward(x, kk, p, gy)
+    gx, gk, path = gpu_bwd(x, kk, p, gy, math="bf16", dtype=torch.bfloat16)
+    wpath = "tc-pair" if cin % 128 == 0 and cout % 128 == 0 else "simt-ffma"
+    assert path == "bwd:tc-pair+" + wpath
+    # exact fp32 sums, then one bf16 rounding of the input gradient
+    np.testing.assert_array_equal(gx, oracle.bf16_round(wx.astype(np.float32)))
+    np.testing.assert_array_equal(gk, wk)
+
+
+@pytest.mark.parametrize("b,n,cin,cout,k,p", [(4, 16, 512, 256, 4, 0), (3, 7, 128, 64, 3, 1)])
+def test_bf16_real_data(b, n, cin, cout, k, p):
+    rng = np.random.default_rng(b + n + cin)
+    x = oracle.bf16_round(rng.standard_normal((b, n, n, cin)).astype(np.float32))
+    kk = oracle.bf16_round((rng.standard_normal((k, k, cin, cout)) * 0.02).astype(np.float32))
+    g = oracle.geometry(n, k, k, p)
+    gy = oracle.bf16_round(rng.standard_normal((b, g.out_h, g.out_w, cout)).astype(np.float32))
+    wx, wk = oracle.tconv_backward(x, kk, p, gy)
+    gx, gk, path = gpu_bwd(x, kk, p, gy, dtype=torch.bfloat16)  # auto -> bf16
+    assert path.startswith("bwd:tc-pair")
+    assert scaled_err(gx, wx) <= 1e-2
+    assert scaled_err(gk, wk) <= 1e-4
+
+
+def test_bf16_falls_back_to_simt_when_cout_is_not_a_k_block():
+    rng = np.random.default_rng(9)
+    x = oracle.bf16_round(rng.standard_normal((2, 6, 6, 64)).astype(np.float32))
+    kk = oracle.bf16_round((rng.standard_normal((3, 3, 64, 40)) * 0.05).astype(np.float32))
+    g = oracle.geometry(6, 3, 3, 0)
+    gy = oracle.bf16_round(rng.standard_normal((2, g.out_h, g.out_w, 40)).astype(np.float32))
+    wx, wk = oracle.tconv_backward(x, kk, 0, gy)
+    gx, gk, path = gpu_bwd(x, kk, 0, gy, math="bf16", dtype=torch.bfloat16)
+    assert path == "bwd:simt-ffma+simt-ffma"
+    assert scaled_err(gx, wx) <= 1e-2 and scaled_err(gk, wk) <= 1e-4
+
+
+def test_kernel_grad_accumulates_like_the_reference():
+    """grad_kernel= accumulates (the reference's grad_ across backward calls):
+    two half-batch calls == one full-batch call, bit-exact under EXACT math."""
+    rng = np.random.default_rng(4)
+    x = rng.uniform(-1, 1, (4, 5, 5, 3)).astype(np.float32)
+    kk = rng.uniform(-1, 1, (3, 3, 3, 2)).astype(np.float32)
+    g = oracle.geometry(5, 3, 3, 1)
+    gy = rng.uniform(-1, 1, (4, g.out_h, g.out_w, 2)).astype(np.float32)
+    t = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+    acc = torch.zeros((3, 3, 3, 2), dtype=torch.float32, device="cuda")
+    for s in (slice(0, 2), slice(2, 4)):
+        sc.transpose_conv_fused_backward(t(x[s]), t(kk), 1, t(gy[s]), math="exact", input_grad=False,
+                                         grad_kernel=acc)
+    _, wk = oracle.tconv_backward(x, kk, 1, gy)
+    np.testing.assert_array_equal(acc.cpu().numpy(), wk)
+
+
+def test_empty_batch_zeroes_the_kernel_grad():
+    t = torch.zeros((0, 4, 4, 8), device="cuda")
+    gy = torch.zeros((0, 7, 7, 4), device="cuda")
+    gx, gk = sc.transpose_conv_fused_backward(t, torch.ones((3, 3, 8, 4), device="cuda"), 1, gy)
+    assert tuple(gx.shape) == (0, 4, 4, 8)
+    assert torch.count_nonzero(gk).item() == 0
+
+
+def test_errors():
+    x = torch.zeros((1, 4, 4, 2), device="cuda")
+    k = torch.zeros((3, 3, 2, 2), device="cuda")
+    gy = torch.zeros((1, 5, 5, 2), device="cuda")  # out = 2n + 2p - k = 5
+    with pytest.raises(sc.ContractError):
+        sc.transpose_conv_fused_backward(x, k, 0, torch.zeros((1, 6, 6, 2), device="cuda"))
+    with pytest.raises(sc.ContractError):
+        sc.transpose_conv_fused_backward(x, torch.zeros((3, 3, 3, 2), device="cuda"), 0, gy)
+    with pytest.raises(sc.ContractError):
+        sc.transpose_conv_fused_backward(x.bfloat16(), k.bfloat16(), 0, gy, math="exact")
+    with pytest.raises(sc.ShapeError):
+        sc.transpose_conv_fused_backward(torch.zeros((1, 1, 1, 2), device="cuda"),
+                                         torch.zeros((7, 7, 2, 2), device="cuda"), 0,
+                                         torch.zeros((1, 1, 1, 2), device="cuda"))
+
+
+def test_layer_class_mirrors_the_reference_layer():
+    """FusedTConv: forward caches the input, backward returns gx and accumulates
+    into grad, state error before forward (reference test_netdemo.cpp:222-238)."""
+    rng = np.random.default_rng(5)
+    kk = rng.uniform(-1, 1, (4, 4, 3, 2))
+    layer = sc.FusedTConv(torch.from_numpy(kk), 2, math="exact")
+    with pytest.raises(sc.StateError):
+        layer.backward(torch.zeros((1, 8, 8, 2), dtype=torch.float64, device="cuda"))
+    x = rng.uniform(-1, 1, (2, 4, 4, 3))
+    y = layer.forward(torch.from_numpy(x))
+    np.testing.assert_array_equal(y.cpu().numpy(), oracle.tconv_fused(x, kk, 2))
+    g = oracle.geometry(4, 4, 4, 2)
+    gy = rng.uniform(-1, 1, (2, g.out_h, g.out_w, 2))
+    gx = layer.backward(torch.from_numpy(gy).cuda())
+    wx, wk = oracle.tconv_backward(x, kk, 2, gy)
+    np.testing.assert_array_equal(gx.cpu().numpy(), wx)
+    (vals, grads), = layer.params()
+    np.testing.assert_array_equal(grads.cpu().numpy(), wk)
+    layer.zero_grads()
+    assert torch.count_nonzero(layer.grad).item() == 0
+
+
+@pytest.mark.parametrize("n,cin,cout,k,p", [(5, 3, 4, 3, 1), (4, 2, 3, 4, 2), (6, 4, 2, 5, 3)])
+def test_autograd_matches_torch_conv_transpose(n, cin, cout, k, p):
+    """The autograd wrapper's gradients equal torch's conv_transpose2d gradients
+    (stride 2, padding k-1-p, flipped kernel) in double."""
+    rng = np.random.default_rng(n + k)
+    x = torch.tensor(rng.uniform(-1, 1, (2, n, n, cin)), device="cuda", requires_grad=True)
+    kk = torch.tensor(rng.uniform(-1, 1, (k, k, cin, cout)), device="cuda", requires_grad=True)
+    y = sc.TransposeConvFused.apply(x, kk, p)
+    gy = torch.tensor(rng.uniform(-1, 1, tuple(y.shape)), device="cuda")
+    (y * gy).sum().backward()
+    x2 = x.detach().clone().permute(0, 3, 1, 2).requires_grad_(True)
+    w2 = kk.detach().clone().flip(0, 1).permute(2, 3, 0, 1).contiguous().requires_grad_(True)
+    y2 = torch.nn.functional.conv_transpose2d(x2, w2, stride=2, padding=k - 1 - p)
+    torch.testing.assert_close(y2.permute(0, 2, 3, 1), y.detach(), rtol=1e-12, atol=1e-12)
+    (y2 * gy.permute(0, 3, 1, 2)).sum().backward()
+    torch.testing.assert_close(x2.grad.permute(0, 2, 3, 1), x.grad, rtol=1e-12, atol=1e-12)
+    torch.testing.assert_close(w2.grad.permute(2, 3, 0, 1).flip(0, 1), kk.grad, rtol=1e-12, atol=1e-12)
