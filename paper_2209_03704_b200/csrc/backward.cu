@@ -266,6 +266,21 @@ __global__ void wgrad_reduce(const ACC* __restrict__ ws, ACC* __restrict__ gk, l
   for (int i = 0; i < splits; ++i) s += ws[(long long)i * ksz + e];
   gk[e] = s;
 }
+// float4 version (ksz % 4 == 0, 16-byte aligned buffers), same per-element order
+__global__ void wgrad_reduce4(const float4* __restrict__ ws, float4* __restrict__ gk, long long n4, int splits,
+                              int accumulate) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n4) return;
+  float4 s = accumulate ? gk[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = 0; i < splits; ++i) {
+    const float4 v = __ldcs(ws + (long long)i * n4 + e);  // read once: streaming
+    s.x += v.x;
+    s.y += v.y;
+    s.z += v.z;
+    s.w += v.w;
+  }
+  gk[e] = s;
+}
 
 }  // namespace bwd
 
@@ -341,7 +356,7 @@ static cudaError_t bwd_weight_t(const BackwardProblem& pr, bool exact, cudaStrea
     return e;
   }
   ACC* ws = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&ws, (size_t)splits * ksz * sizeof(ACC), s);
+  cudaError_t e = workspace_alloc((void**)&ws, (size_t)splits * ksz * sizeof(ACC), s);
   if (e != cudaSuccess) return e;
   bwd::wgrad_ffma<T, ACC><<<grid, bwd::NT, 0, s>>>((const T*)pr.x, (const T*)pr.gy, ws, pr, (int)splits,
                                                    chunk, 0);
@@ -357,9 +372,39 @@ static cudaError_t bwd_weight_t(const BackwardProblem& pr, bool exact, cudaStrea
   return e != cudaSuccess ? e : e2;
 }
 
+// Split-K partial sums live in a library-owned stream-ordered pool whose
+// release threshold keeps freed blocks mapped (the default pool returns them to
+// the OS at every synchronisation, making each call pay a fresh mapping).
+cudaError_t workspace_alloc(void** p, size_t bytes, cudaStream_t s) {
+  static cudaMemPool_t pools[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, s);
+  if (!pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool;
+    e = cudaMemPoolCreate(&pool, &props);
+    if (e != cudaSuccess) return e;
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    pools[dev] = pool;
+  }
+  return cudaMallocFromPoolAsync(p, bytes, pools[dev], s);
+}
+
 cudaError_t launch_wgrad_reduce(const float* ws, float* gk, long long ksz, int splits, int accumulate,
                                 cudaStream_t s) {
-  bwd::wgrad_reduce<float><<<(unsigned)((ksz + 255) / 256), 256, 0, s>>>(ws, gk, ksz, splits, accumulate);
+  if (ksz % 4 == 0 && ((uintptr_t)ws & 15) == 0 && ((uintptr_t)gk & 15) == 0) {
+    const long long n4 = ksz / 4;
+    bwd::wgrad_reduce4<<<(unsigned)((n4 + 255) / 256), 256, 0, s>>>((const float4*)ws, (float4*)gk, n4, splits,
+                                                                     accumulate);
+  } else {
+    bwd::wgrad_reduce<float><<<(unsigned)((ksz + 255) / 256), 256, 0, s>>>(ws, gk, ksz, splits, accumulate);
+  }
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) note_launch();
   return e;

@@ -50,6 +50,7 @@ bool tc_bwd_data_supported(const BackwardProblem& pr);
 cudaError_t launch_tc_bwd_data(const BackwardProblem& pr, cudaStream_t s);
 bool tc_bwd_weight_supported(const BackwardProblem& pr);
 cudaError_t launch_tc_bwd_weight(const BackwardProblem& pr, cudaStream_t s);
+cudaError_t workspace_alloc(void** p, size_t bytes, cudaStream_t s);
 cudaError_t launch_wgrad_reduce(const float* ws, float* gk, long long ksz, int splits, int accumulate,
                                 cudaStream_t s);
 

@@ -1227,7 +1227,7 @@ cudaError_t launch_tc_bwd_weight(const BackwardProblem& pr, cudaStream_t s) {
     return launch_wide_t<float, 0>(p, maps, s);
   }
   float* ws = nullptr;
-  cudaError_t e = cudaMallocAsync((void**)&ws, (size_t)p.w_splits * p.w_ksz * sizeof(float), s);
+  cudaError_t e = workspace_alloc((void**)&ws, (size_t)p.w_splits * p.w_ksz * sizeof(float), s);
   if (e != cudaSuccess) return e;
   p.wout = ws;
   e = launch_wide_t<float, 0>(p, maps, s);

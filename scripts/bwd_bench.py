@@ -21,8 +21,8 @@ def main():
         kk = (torch.randn((k, k, cin, cout), device="cuda") * 0.02).to(dt)
         gy = torch.randn((b, g.out_h, g.out_w, cout), device="cuda").to(dt)
         macs = b * n * n * cin * cout * k * k  # dense (every tap reaches every pixel, minus borders)
-        for part in ("input", "kernel"):
-            kw = dict(input_grad=part == "input", kernel_grad=part == "kernel")
+        for part in ("input", "kernel", "both"):
+            kw = dict(input_grad=part != "kernel", kernel_grad=part != "input")
             for _ in range(3):
                 sc.transpose_conv_fused_backward(x, kk, p, gy, **kw)
             torch.cuda.synchronize()
@@ -35,8 +35,9 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             us = e0.elapsed_time(e1) * 1000 / reps
+            m = macs * (2 if part == "both" else 1)
             print(json.dumps({"config": name, "part": part, "path": path, "us": round(us, 2),
-                              "tflops": round(2 * macs / us / 1e6, 1)}), flush=True)
+                              "tflops": round(2 * m / us / 1e6, 1)}), flush=True)
 
 
 if __name__ == "__main__":
