@@ -40,7 +40,10 @@ typedef enum {
   SEGCONV_E_SHAPE = 1,       /* == segconv::ShapeError    (reference errors.hpp:16-18) */
   SEGCONV_E_CONTRACT = 2,    /* == segconv::ContractError (reference errors.hpp:21-23) */
   SEGCONV_E_CUDA = 3,        /* CUDA runtime / launch failure, no device, ...         */
-  SEGCONV_E_UNSUPPORTED = 4  /* valid request this build has no kernel for            */
+  SEGCONV_E_UNSUPPORTED = 4, /* valid request this build has no kernel for            */
+  SEGCONV_E_IO = 5,          /* == segconv::IoError       (reference errors.hpp:34-37) */
+  SEGCONV_E_PARSE = 6        /* == segconv::ParseError    (reference errors.hpp:25-31); */
+                             /*    segconv_last_error_offset() = its byte_offset        */
 } segconv_status;
 
 /* Element types.  The reference supports float and double (tensor.hpp:65,154);
@@ -164,6 +167,37 @@ segconv_status segconv_transpose_conv_fused_host(const void* h_x, void* d_x, seg
                                                  const float* d_bias, unsigned epilogue,
                                                  segconv_math math, void* d_y, void* h_y,
                                                  segconv_dtype y_dtype, int chunks, void* stream);
+
+/* ---------------------------------------------------- SGC1 tensor files */
+/* reference tensor_io.hpp:12-103: "SGC1" magic, u32 LE height, width,
+ * channels, precision (0 f32 / 1 f64), then the HWC data little-endian.
+ * Host-side; no device needed except for segconv_load_tensor_batch's upload. */
+typedef struct {
+  int height, width, channels;
+  int precision; /* 0 = f32, 1 = f64 (reference Precision) */
+} segconv_tensor_file_info;
+
+/* reference tensor_io.hpp:53-74 (peek_tensor_file): IoError if the file cannot
+ * be opened; ParseError at offset = bytes read for a short header, 0 for a bad
+ * magic, 16 for an unknown precision tag, 4 for a non-positive dimension. */
+segconv_status segconv_peek_tensor_file(const char* path, segconv_tensor_file_info* info);
+/* reference tensor_io.hpp:76-91 (load_tensor<T>): dtype F32/F64 must match the
+ * stored precision (ContractError); ParseError at min(size, expected) when the
+ * payload size is wrong.  host_dst holds dst_bytes (>= h*w*c*elem). */
+segconv_status segconv_load_tensor(const char* path, segconv_dtype dtype, void* host_dst,
+                                   size_t dst_bytes);
+/* reference tensor_io.hpp:93-103 (save_tensor<T>). */
+segconv_status segconv_save_tensor(const char* path, const void* host_src, int height, int width,
+                                   int channels, segconv_dtype dtype);
+/* Batch loader: `count` files of one shape and precision into a (count, h, w,
+ * c) NHWC batch.  Each image is read into its slot of host_staging (page-locked
+ * for overlap, count*h*w*c elements) and its upload to d_dst is queued on
+ * `stream` right away, so file reads overlap the host->device copies.  Errors
+ * as segconv_load_tensor; a shape mismatch between files is a ContractError. */
+segconv_status segconv_load_tensor_batch(const char* const* paths, int count, segconv_dtype dtype,
+                                         void* host_staging, void* d_dst, void* stream);
+/* Byte offset of the last SEGCONV_E_PARSE on this thread. */
+size_t segconv_last_error_offset(void);
 
 /* ------------------------------------------------------------- backward */
 /* reference netdemo/layers.hpp:171-211 (net::FusedTConv<T>::backward), batched:

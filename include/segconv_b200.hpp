@@ -40,12 +40,24 @@ struct ContractError : Error {
 struct CudaError : Error {
   using Error::Error;
 };
+struct ParseError : Error {
+  ParseError(const std::string& msg, std::size_t offset) : Error(msg), byte_offset(offset) {}
+  std::size_t byte_offset;
+};
+struct IoError : Error {
+  using Error::Error;
+};
+struct StateError : Error {
+  using Error::Error;
+};
 
 inline void throw_on(segconv_status st) {
   if (st == SEGCONV_OK) return;
   const std::string msg = segconv_last_error();
   if (st == SEGCONV_E_SHAPE) throw ShapeError(msg);
   if (st == SEGCONV_E_CONTRACT) throw ContractError(msg);
+  if (st == SEGCONV_E_PARSE) throw ParseError(msg, segconv_last_error_offset());
+  if (st == SEGCONV_E_IO) throw IoError(msg);
   throw CudaError(msg);
 }
 
@@ -296,6 +308,109 @@ Tensor<T> transpose_conv_naive(const Tensor<T>& input, const Kernel<T>& k, int p
   dy.to_host(out.data(), out.size() * sizeof(T));
   return out;
 }
+
+// ------------------------------------------------------------- SGC1 files
+// reference tensor_io.hpp:46-103
+enum class Precision { f32 = 0, f64 = 1 };
+template <typename T>
+inline constexpr Precision precision_of = std::is_same_v<T, double> ? Precision::f64 : Precision::f32;
+
+struct TensorFileInfo {
+  int height = 0, width = 0, channels = 0;
+  Precision precision = Precision::f32;
+};
+
+inline TensorFileInfo peek_tensor_file(const std::string& path) {
+  segconv_tensor_file_info i;
+  throw_on(segconv_peek_tensor_file(path.c_str(), &i));
+  return TensorFileInfo{i.height, i.width, i.channels, (Precision)i.precision};
+}
+
+template <typename T>
+Tensor<T> load_tensor(const std::string& path) {
+  const TensorFileInfo info = peek_tensor_file(path);
+  Tensor<T> t(info.height, info.width, info.channels);
+  throw_on(segconv_load_tensor(path.c_str(), dtype_of<T>::value, t.data(), t.size() * sizeof(T)));
+  return t;
+}
+
+template <typename T>
+void save_tensor(const Tensor<T>& t, const std::string& path) {
+  throw_on(segconv_save_tensor(path.c_str(), t.data(), t.height(), t.width(), t.channels(),
+                               dtype_of<T>::value));
+}
+
+// ------------------------------------------------------------- training layer
+namespace net {
+
+// reference netdemo/layers.hpp:23-29
+template <typename T>
+struct ParamBlock {
+  T* values = nullptr;
+  T* grads = nullptr;
+  std::size_t size = 0;
+};
+
+// reference netdemo/layers.hpp:150-230 (net::FusedTConv<T>): forward runs the
+// segregated GPU kernels, backward the GPU backward pass
+// (segconv_transpose_conv_fused_backward); values and gradients live on the
+// host as in the reference, so an optimizer written against params() works
+// unchanged.  Default math EXACT: bit-identical to the reference layer.
+template <typename T>
+class FusedTConv {
+ public:
+  FusedTConv(Kernel<T> k, int p, segconv_math math = SEGCONV_MATH_EXACT)
+      : kernel_(std::move(k)), grad_(kernel_.kh(), kernel_.kw(), kernel_.cin(), kernel_.cout()), p_(p),
+        math_(math), sks_(segregate(kernel_, p, fwd_math(math))) {}
+
+  const char* name() const { return "fused_tconv"; }
+
+  Tensor<T> forward(const Tensor<T>& in) {
+    if (in.height() != in.width())
+      throw ContractError("fused_tconv expects a square input, got " + std::to_string(in.height()) + "x" +
+                          std::to_string(in.width()));
+    geom_ = tconv_geometry(in.height(), kernel_.kh(), kernel_.kw(), p_);
+    input_ = in;
+    has_input_ = true;
+    return transpose_conv_fused(in, sks_, geom_);
+  }
+
+  Tensor<T> backward(const Tensor<T>& g) {
+    if (!has_input_) throw StateError(std::string(name()) + ": backward called before forward");
+    if (g.height() != geom_.out_h || g.width() != geom_.out_w || g.channels() != kernel_.cout())
+      throw ContractError("fused_tconv: output gradient shape mismatch");
+    Tensor<T> gin(input_.height(), input_.width(), input_.channels());
+    DeviceBuffer dx(input_.data(), input_.size() * sizeof(T)), dg(g.data(), g.size() * sizeof(T));
+    DeviceBuffer dk(kernel_.data(), kernel_.size() * sizeof(T));
+    DeviceBuffer dgk(grad_.data(), grad_.size() * sizeof(T)), dgx(gin.size() * sizeof(T));
+    throw_on(segconv_transpose_conv_fused_backward(
+        dx.get(), dg.get(), dtype_of<T>::value, 1, input_.height(), input_.channels(), dk.get(), kernel_.kh(),
+        kernel_.kw(), kernel_.cout(), p_, math_, dgx.get(), dgk.get(), /*accumulate=*/1, nullptr));
+    dgx.to_host(gin.data(), gin.size() * sizeof(T));
+    dgk.to_host(grad_.data(), grad_.size() * sizeof(T));
+    return gin;
+  }
+
+  std::vector<ParamBlock<T>> params() { return {{kernel_.data(), grad_.data(), kernel_.size()}}; }
+  void on_params_updated() { sks_ = segregate(kernel_, p_, fwd_math(math_)); }
+  const Kernel<T>& kernel() const { return kernel_; }
+  int padding() const { return p_; }
+
+ private:
+  static segconv_math fwd_math(segconv_math m) {
+    return m == SEGCONV_MATH_EXACT ? SEGCONV_MATH_EXACT : SEGCONV_MATH_AUTO;
+  }
+  Kernel<T> kernel_;
+  Kernel<T> grad_;
+  int p_;
+  segconv_math math_;
+  SubKernelSet<T> sks_;
+  TConvGeometry geom_{};
+  Tensor<T> input_;
+  bool has_input_ = false;
+};
+
+}  // namespace net
 
 // reference tensor.hpp:263-286
 template <typename T>

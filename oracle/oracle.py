@@ -18,6 +18,7 @@ __all__ = [
     "ref_tconv_naive", "ref_tconv_fused_parallel", "ref_run_verify", "ref_verify_case",
     "ref_count_ops", "ref_time_fused_batch", "OracleError", "bf16_round", "tf32_round",
     "tconv_backward", "scatter_backward_f64", "ref_tconv_backward", "ref_time_backward",
+    "ref_save_tensor", "ref_load_tensor",
 ]
 
 
@@ -94,6 +95,9 @@ def load_ref():
         lib.ref_time_backward_f32.argtypes = [
             fp, C.c_int, C.c_int, C.c_int, fp, C.c_int, C.c_int, C.c_int, C.c_int, fp, C.c_int,
             fp, fp, dp]
+        lib.ref_save_tensor.argtypes = [C.c_char_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
+        lib.ref_load_tensor.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_size_t, ip]
+        lib.ref_last_error_offset.restype = C.c_size_t
         lib.ref_tconv_fused_parallel_f32.argtypes = [
             fp, C.c_int, C.c_int, C.c_int, fp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, fp]
         lib.ref_count_ops.argtypes = [C.c_int] * 6 + [C.POINTER(C.c_uint64)]
@@ -323,6 +327,30 @@ def ref_time_backward(x, k, p, gy, workers):
                                      _ptr(gy, fp), workers, _ptr(gx, fp), _ptr(gk, fp),
                                      C.byref(secs)), lib)
     return gx, gk, secs.value
+
+
+def ref_save_tensor(path, t):
+    """The reference's save_tensor (tensor_io.hpp:93-103) on an (h, w, c) f32/f64 array."""
+    t = np.ascontiguousarray(t)
+    f64 = t.dtype == np.float64
+    t = _f64(t) if f64 else _f32(t)
+    lib = load_ref()
+    _check(lib.ref_save_tensor(os.fsencode(path), t.ctypes.data, *t.shape, int(f64)), lib)
+
+
+def ref_load_tensor(path, f64=False):
+    """The reference's load_tensor<T>; returns the array, or raises OracleError
+    with .code (5 IoError, 6 ParseError, 2 ContractError) and .offset."""
+    lib = load_ref()
+    d = (C.c_int * 4)()
+    cap = 1 << 22
+    buf = np.empty(cap, dtype=np.float64 if f64 else np.float32)
+    code = lib.ref_load_tensor(os.fsencode(path), int(f64), buf.ctypes.data, cap, d)
+    if code:
+        e = OracleError(code, (lib.ref_last_error() or b"").decode())
+        e.offset = int(lib.ref_last_error_offset())
+        raise e
+    return buf[: d[0] * d[1] * d[2]].reshape(d[0], d[1], d[2]).copy()
 
 
 def ref_count_ops(n, cin, cout, kh, kw, p):

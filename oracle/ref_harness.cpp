@@ -25,17 +25,26 @@
 #include "segconv/reference_ops.hpp"
 #include "segconv/segregation.hpp"
 #include "segconv/tensor.hpp"
+#include "segconv/tensor_io.hpp"
 #include "segconv/verify.hpp"
 
 namespace {
 
 thread_local std::string g_err;
+thread_local size_t g_offset = 0;
 
 template <typename F>
 int guarded(F&& fn) {
   try {
     fn();
     return 0;
+  } catch (const segconv::ParseError& e) {
+    g_err = e.what();
+    g_offset = e.byte_offset;
+    return 6;
+  } catch (const segconv::IoError& e) {
+    g_err = e.what();
+    return 5;
   } catch (const segconv::ShapeError& e) {
     g_err = e.what();
     return 1;
@@ -113,6 +122,38 @@ int run_backward(const T* x, int batch, int n, int cin, const T* k, int kh, int 
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+size_t ref_last_error_offset() { return g_offset; }
+
+// SGC1 container through the reference's own tensor_io.hpp
+int ref_save_tensor(const char* path, const void* data, int h, int w, int c, int f64) {
+  return guarded([&] {
+    if (f64)
+      segconv::save_tensor(segconv::Tensor<double>::from_data(
+                               h, w, c, std::vector<double>((const double*)data, (const double*)data + (size_t)h * w * c)),
+                           path);
+    else
+      segconv::save_tensor(segconv::Tensor<float>::from_data(
+                               h, w, c, std::vector<float>((const float*)data, (const float*)data + (size_t)h * w * c)),
+                           path);
+  });
+}
+// dims_out: h, w, c, precision; data copied into out (capacity in elements)
+int ref_load_tensor(const char* path, int f64, void* out, size_t cap, int dims_out[4]) {
+  return guarded([&] {
+    const auto info = segconv::peek_tensor_file(path);
+    dims_out[0] = info.height;
+    dims_out[1] = info.width;
+    dims_out[2] = info.channels;
+    dims_out[3] = (int)info.precision;
+    if (f64) {
+      const auto t = segconv::load_tensor<double>(path);
+      if (t.size() <= cap) std::memcpy(out, t.data(), t.size() * sizeof(double));
+    } else {
+      const auto t = segconv::load_tensor<float>(path);
+      if (t.size() <= cap) std::memcpy(out, t.data(), t.size() * sizeof(float));
+    }
+  });
+}
 
 int ref_tconv_geometry(int n_in, int kh, int kw, int p, int out[11]) {
   return guarded([&] {

@@ -13,7 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libsegconv_b200.so")
 
 # segconv_status
-OK, E_SHAPE, E_CONTRACT, E_CUDA, E_UNSUPPORTED = range(5)
+OK, E_SHAPE, E_CONTRACT, E_CUDA, E_UNSUPPORTED, E_IO, E_PARSE = range(7)
 # segconv_dtype
 F32, F64, BF16, F16_SPLIT = 0, 1, 2, 3
 # segconv_math
@@ -44,6 +44,11 @@ class SubKernels(C.Structure):
     ]
 
 
+class TensorFileInfo(C.Structure):
+    _fields_ = [("height", C.c_int), ("width", C.c_int), ("channels", C.c_int),
+                ("precision", C.c_int)]
+
+
 # (name, restype, argtypes) for every symbol include/segconv_b200.h declares.
 _vp, _i, _u, _sz = C.c_void_p, C.c_int, C.c_uint, C.c_size_t
 SIGNATURES = {
@@ -62,6 +67,11 @@ SIGNATURES = {
     "segconv_transpose_conv_fused_backward": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _i, _i, _i,
                                                    _i, _i, _vp, _vp, _i, _vp]),
     "segconv_select_math": (_i, [_i, _i, _i, _i, _i, _i]),
+    "segconv_peek_tensor_file": (_i, [C.c_char_p, C.POINTER(TensorFileInfo)]),
+    "segconv_load_tensor": (_i, [C.c_char_p, _i, _vp, _sz]),
+    "segconv_save_tensor": (_i, [C.c_char_p, _vp, _i, _i, _i, _i]),
+    "segconv_load_tensor_batch": (_i, [C.POINTER(C.c_char_p), _i, _i, _vp, _vp, _vp]),
+    "segconv_last_error_offset": (_sz, []),
     "segconv_upsample2x_pad": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _vp]),
     "segconv_conv2d_valid": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _i, _vp, _u, _vp, _vp]),
     "segconv_naive_workspace_bytes": (_sz, [_i, _i, _i, _i, _i]),

@@ -32,6 +32,11 @@ static segconv_status fail(segconv_status st, const char* fmt, ...) {
   return st;
 }
 
+segconv_status set_error(segconv_status st, const char* msg) {
+  g_err = msg ? msg : "";
+  return st;
+}
+
 static segconv_status cuda_status(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return SEGCONV_OK;
   if (e == cudaErrorNotSupported)

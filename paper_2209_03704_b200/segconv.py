@@ -15,6 +15,7 @@ in the sm_100a kernels; there is no CPU implementation here.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 from typing import Optional, Sequence, Union
 
@@ -29,7 +30,8 @@ __all__ = [
     "transpose_conv_fused_parallel", "transpose_conv_naive", "conv2d_valid", "upsample2x_pad",
     "tensors_equal_exact", "tensors_equal_approx", "LayerShape", "OpCounts", "count_ops_naive",
     "count_ops_fused", "select_math", "launch_count", "last_path", "MATHS",
-    "transpose_conv_fused_backward", "FusedTConv", "TransposeConvFused",
+    "transpose_conv_fused_backward", "FusedTConv", "TransposeConvFused", "IoError", "ParseError",
+    "TensorFileInfo", "peek_tensor_file", "load_tensor", "save_tensor", "load_tensor_batch",
 ]
 
 
@@ -51,6 +53,19 @@ class StateError(SegconvError):
     (reference errors.hpp:39, netdemo/layers.hpp:46-48)."""
 
 
+class IoError(SegconvError):
+    """A file could not be opened, read or written (reference errors.hpp:34-37)."""
+
+
+class ParseError(SegconvError):
+    """Malformed file contents; ``byte_offset`` is where parsing stopped
+    (reference errors.hpp:25-31)."""
+
+    def __init__(self, msg: str, byte_offset: int = 0):
+        super().__init__(msg)
+        self.byte_offset = byte_offset
+
+
 class CudaError(SegconvError):
     """The device could not run the request (no CPU fallback exists)."""
 
@@ -60,10 +75,12 @@ class UnsupportedError(SegconvError):
 
 
 _ERR = {A.E_SHAPE: ShapeError, A.E_CONTRACT: ContractError, A.E_CUDA: CudaError,
-        A.E_UNSUPPORTED: UnsupportedError}
+        A.E_UNSUPPORTED: UnsupportedError, A.E_IO: IoError}
 
 
 def _check(status: int) -> None:
+    if status == A.E_PARSE:
+        raise ParseError(A.last_error(), int(A.lib().segconv_last_error_offset()))
     if status != A.OK:
         raise _ERR.get(status, SegconvError)(A.last_error())
 
@@ -512,6 +529,77 @@ class TransposeConvFused(torch.autograd.Function):
         if gk is not None:
             gk = gk.to(kernel.dtype)
         return gx, gk, None
+
+
+# ------------------------------------------------------------ SGC1 files
+@dataclass(frozen=True)
+class TensorFileInfo:
+    """== segconv::TensorFileInfo (reference tensor_io.hpp:48-51)."""
+    height: int
+    width: int
+    channels: int
+    precision: str  # "f32" | "f64"
+
+
+_PREC = {0: "f32", 1: "f64"}
+_PREC_T = {"f32": torch.float32, "f64": torch.float64}
+
+
+def peek_tensor_file(path: str) -> TensorFileInfo:
+    """reference tensor_io.hpp:53-74: parse the 20-byte SGC1 header."""
+    info = A.TensorFileInfo()
+    _check(A.lib().segconv_peek_tensor_file(os.fsencode(path), C.byref(info)))
+    return TensorFileInfo(info.height, info.width, info.channels, _PREC[info.precision])
+
+
+def load_tensor(path: str, dtype: Optional[torch.dtype] = None, *, device=None) -> torch.Tensor:
+    """reference tensor_io.hpp:76-91 (load_tensor<T>): an (h, w, c) tensor.
+    ``dtype`` (float32/float64) must match the stored precision
+    (ContractError); default: the stored one.  ``device`` moves the result."""
+    info = peek_tensor_file(path)
+    dt = dtype or _PREC_T[info.precision]
+    if dt not in (torch.float32, torch.float64):
+        raise ContractError("SGC1 stores float32 or float64 tensors")
+    pin = device is not None and torch.device(device).type == "cuda" and torch.cuda.is_available()
+    t = torch.empty((info.height, info.width, info.channels), dtype=dt, pin_memory=pin)
+    _check(A.lib().segconv_load_tensor(os.fsencode(path), _DT[dt], t.data_ptr(),
+                                       t.numel() * t.element_size()))
+    return t.to(device, non_blocking=True) if device is not None else t
+
+
+def save_tensor(t: torch.Tensor, path: str) -> None:
+    """reference tensor_io.hpp:93-103 (save_tensor<T>): t is (h, w, c) float32/float64."""
+    if t.dim() != 3:
+        raise ShapeError(f"SGC1 holds (h, w, c) tensors, got {tuple(t.shape)}")
+    if t.dtype not in (torch.float32, torch.float64):
+        raise ContractError("SGC1 stores float32 or float64 tensors")
+    h = t.detach().cpu().contiguous()
+    _check(A.lib().segconv_save_tensor(os.fsencode(path), h.data_ptr() if h.numel() else None,
+                                       int(h.shape[0]), int(h.shape[1]), int(h.shape[2]),
+                                       _DT[h.dtype]))
+
+
+def load_tensor_batch(paths, dtype: Optional[torch.dtype] = None, *, device=None) -> torch.Tensor:
+    """Many SGC1 files of one shape -> a (B, h, w, c) batch.  With a CUDA
+    ``device`` the files are read into a page-locked staging buffer and each
+    image's upload is queued as soon as it is read (reads overlap copies)."""
+    paths = list(paths)
+    if not paths:
+        raise ContractError("empty batch")
+    info = peek_tensor_file(paths[0])
+    dt = dtype or _PREC_T[info.precision]
+    shape = (len(paths), info.height, info.width, info.channels)
+    cuda = device is not None and torch.device(device).type == "cuda"
+    host = torch.empty(shape, dtype=dt, pin_memory=cuda)
+    dev = torch.empty(shape, dtype=dt, device=device) if cuda else None
+    arr = (C.c_char_p * len(paths))(*[os.fsencode(p) for p in paths])
+    _check(A.lib().segconv_load_tensor_batch(arr, len(paths), _DT[dt], host.data_ptr(),
+                                             dev.data_ptr() if dev is not None else None,
+                                             _stream() if cuda else None))
+    if cuda:
+        torch.cuda.current_stream().synchronize()  # the staging buffer is released on return
+        return dev
+    return host if device is None else host.to(device)
 
 
 def _fused_host(xb, sks, g, m, bias, activation, out_dtype, out, staging, chunks, sync):

@@ -130,6 +130,88 @@ int main() {
     }
     CHECK(c1 && c2 && c3 && c4, "rect / channel / extent / parity errors");
   }
+  // SGC1 container (reference tests/test_io.cpp:44-127)
+  {
+    const std::string path = "/tmp/segconv_b200_test_host_api.sgc";
+    std::mt19937 rng(44);
+    std::uniform_real_distribution<double> d(-1, 1);
+    Tensor<double> t(5, 4, 3);
+    for (size_t i = 0; i < t.size(); ++i) t.data()[i] = d(rng);
+    segconv::save_tensor(t, path);
+    const auto info = segconv::peek_tensor_file(path);
+    CHECK(info.height == 5 && info.width == 4 && info.channels == 3 &&
+              info.precision == segconv::Precision::f64,
+          "SGC1 header round trip");
+    CHECK(segconv::tensors_equal_exact(segconv::load_tensor<double>(path), t), "SGC1 data round trip");
+    bool c1 = false, c2 = false;
+    try {
+      segconv::load_tensor<float>(path);
+    } catch (const segconv::ContractError&) {
+      c1 = true;
+    }
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    std::fwrite("SGC1xxxx", 1, 8, f);
+    std::fclose(f);
+    try {
+      segconv::peek_tensor_file(path);
+    } catch (const segconv::ParseError& e) {
+      c2 = e.byte_offset == 8;
+    }
+    CHECK(c1 && c2, "SGC1 precision mismatch / short header errors");
+    std::remove(path.c_str());
+  }
+  // trainable layer: forward + backward == scatter-form gradients on integer data
+  {
+    std::mt19937 rng(137);
+    std::uniform_int_distribution<int> d(-3, 3);
+    const int n = 5, cin = 3, cout = 2, kk = 4, p = 2;
+    Tensor<double> in(n, n, cin);
+    for (size_t i = 0; i < in.size(); ++i) in.data()[i] = d(rng);
+    Kernel<double> k(kk, kk, cin, cout);
+    for (size_t i = 0; i < k.size(); ++i) k.data()[i] = d(rng);
+    segconv::net::FusedTConv<double> layer(k, p);
+    bool state = false;
+    try {
+      layer.backward(Tensor<double>(8, 8, cout));
+    } catch (const segconv::StateError&) {
+      state = true;
+    }
+    CHECK(state, "layer backward before forward -> StateError");
+    const auto y = layer.forward(in);
+    Tensor<double> g(y.height(), y.width(), cout);
+    for (size_t i = 0; i < g.size(); ++i) g.data()[i] = d(rng);
+    const auto gin = layer.backward(g);
+    const auto gin2 = layer.backward(g);  // tap gradients accumulate across calls
+    bool ok = segconv::tensors_equal_exact(gin, gin2);
+    const int oh = y.height(), ow = y.width();
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j)
+        for (int ch = 0; ch < cin; ++ch) {
+          double want = 0;
+          for (int u = 0; u < kk; ++u)
+            for (int v = 0; v < kk; ++v) {
+              const int yy = 2 * i + p - u, xx = 2 * j + p - v;
+              if (yy < 0 || yy >= oh || xx < 0 || xx >= ow) continue;
+              for (int f = 0; f < cout; ++f) want += k(u, v, ch, f) * g(yy, xx, f);
+            }
+          ok = ok && gin(i, j, ch) == want;
+        }
+    auto blocks = layer.params();
+    for (int u = 0; u < kk; ++u)
+      for (int v = 0; v < kk; ++v)
+        for (int ch = 0; ch < cin; ++ch)
+          for (int f = 0; f < cout; ++f) {
+            double want = 0;
+            for (int i = 0; i < n; ++i)
+              for (int j = 0; j < n; ++j) {
+                const int yy = 2 * i + p - u, xx = 2 * j + p - v;
+                if (yy < 0 || yy >= oh || xx < 0 || xx >= ow) continue;
+                want += in(i, j, ch) * g(yy, xx, f);
+              }
+            ok = ok && blocks[0].grads[(((size_t)u * kk + v) * cin + ch) * cout + f] == 2 * want;
+          }
+    CHECK(ok && blocks.size() == 1 && blocks[0].size == k.size(), "layer gradients == scatter form, exact");
+  }
   std::printf("%d failure(s)\n", failures);
   return failures;
 }

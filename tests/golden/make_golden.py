@@ -23,6 +23,9 @@ Fixtures (all small):
                      rectangular kernels, batches, integer and double cases
                      (`python tests/golden/make_golden.py backward` rewrites
                      only this file)
+  sgc/*.sgc          SGC1 tensor files written by the reference's save_tensor
+                     (tensor_io.hpp:93-103) + sgc/values.npz with their contents
+                     (`python tests/golden/make_golden.py sgc`)
 """
 from __future__ import annotations
 
@@ -148,6 +151,7 @@ def main():
     np.savez_compressed(os.path.join(OUT, "f64_case.npz"), x=x, k=k, p=np.int32(2),
                         fused=oracle.ref_tconv_fused(x, k, 2), naive=oracle.ref_tconv_naive(x, k, 2))
     backward()
+    sgc()
     print("golden fixtures written to", OUT)
 
 
@@ -181,8 +185,25 @@ def backward():
     np.savez_compressed(os.path.join(OUT, "backward.npz"), **out)
 
 
+def sgc():
+    d = os.path.join(OUT, "sgc")
+    os.makedirs(d, exist_ok=True)
+    rng = np.random.default_rng(4490)
+    vals = {
+        "f32_5x4x3": rng.uniform(-2, 2, (5, 4, 3)).astype(np.float32),
+        "f64_2x3x2": rng.uniform(-2, 2, (2, 3, 2)),
+        "f32_1x1x1": np.array([[[3.5]]], dtype=np.float32),
+        "f32_6x6x8": rng.standard_normal((6, 6, 8)).astype(np.float32),
+    }
+    for name, v in vals.items():
+        oracle.ref_save_tensor(os.path.join(d, name + ".sgc"), v)
+    np.savez_compressed(os.path.join(d, "values.npz"), **vals)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["backward"]:
         backward()
+    elif sys.argv[1:] == ["sgc"]:
+        sgc()
     else:
         main()
