@@ -232,6 +232,81 @@ class Layer:
         return time.perf_counter() - t0, nimg, "port"
 
 
+class LayerBackward(Layer):
+    """`--pass backward`: the layer's backward pass (reference netdemo/layers.hpp:171-211,
+    input + kernel gradients) on the same synthetic layer, output gradient ~ N(0, 1).
+    Useful MACs = 2 x the forward's (every forward product has one input-gradient
+    and one kernel-gradient product)."""
+
+    def __init__(self, cfg, rank, torch, sc, dev, world):
+        super().__init__(cfg, rank, torch, sc, dev, world)
+        rng = np.random.default_rng(SEED + 31 + rank)
+        self.gy_host = rng.standard_normal(tuple(self.y.shape), dtype=np.float32)
+        self.gyd = torch.from_numpy(self.gy_host).to(dev, self.tdt)
+        self.gy_pinned = torch.from_numpy(self.gy_host).to(self.tdt).pin_memory()
+        self.macs *= 2
+        e = self.xd.element_size()
+        self.alg_bytes = (2 * self.xd.numel() + self.kd.numel() + self.gyd.numel()) * e + \
+            self.kd.numel() * 4
+        self.torch = torch
+        self.launches_per_step = 2
+        self.gx_pinned = torch.empty(self.xd.shape, dtype=self.tdt).pin_memory()
+        self.gk_pinned = torch.empty(self.kd.shape, dtype=torch.float32).pin_memory()
+
+    def step(self):
+        self.sc.transpose_conv_fused_backward(self.xd, self.kd, self.cfg["p"], self.gyd)
+
+    def step_e2e(self):
+        """Public API from host buffers: x and gy uploaded, both gradients read back."""
+        xd = self.x_pinned.to(self.xd.device, non_blocking=True)
+        gyd = self.gy_pinned.to(self.xd.device, non_blocking=True)
+        gx, gk = self.sc.transpose_conv_fused_backward(xd, self.kd, self.cfg["p"], gyd)
+        self.gx_pinned.copy_(gx, non_blocking=True)
+        self.gk_pinned.copy_(gk, non_blocking=True)
+
+    def e2e_bytes(self):
+        return (self.x_pinned.numel() + self.gy_pinned.numel()) * self.x_pinned.element_size(), \
+            self.gx_pinned.numel() * self.gx_pinned.element_size() + self.gk_pinned.numel() * 4
+
+    def conventional(self, torch, steps, flush):
+        return None
+
+    def cudnn(self, torch, steps, flush):
+        """Library context: torch's conv_transpose2d backward (cuDNN dgrad + wgrad), NCHW."""
+        cfg = self.cfg
+        k = torch.from_numpy(self.k_host).cuda().to(self.tdt)
+        W = k.permute(2, 3, 0, 1).flip(2, 3).contiguous().requires_grad_(True)
+        xn = self.xd.permute(0, 3, 1, 2).contiguous().requires_grad_(True)
+        y = torch.nn.functional.conv_transpose2d(xn, W, stride=2, padding=cfg["k"] - 1 - cfg["p"])
+        g = self.gyd.permute(0, 3, 1, 2).contiguous()
+        ts = []
+        for i in range(steps + 1):
+            flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            torch.autograd.grad(y, (xn, W), g, retain_graph=True)
+            b.record()
+            b.synchronize()
+            if i:
+                ts.append(a.elapsed_time(b))
+        ms = statistics.median(ts)
+        return {"value": round(self.macs / (ms * 1e-3) / 1e9, 2), "ms_per_step": round(ms, 4),
+                "what": "torch conv_transpose2d backward (cuDNN dgrad + wgrad), NCHW, not ours"}
+
+    def cpu_sample(self, workers):
+        import oracle
+        nimg = min(self.cfg["batch"], max(1, workers))
+        x, k, gy = self.x_host[:nimg], self.k_host, self.gy_host[:nimg]
+        if self.cfg["dtype"] == "bf16":
+            x, k, gy = oracle.bf16_round(x), oracle.bf16_round(k), oracle.bf16_round(gy)
+        if oracle.ref_available():
+            _, _, secs = oracle.ref_time_backward(x, k, self.cfg["p"], gy, workers)
+            return secs, nimg, "reference"
+        t0 = time.perf_counter()
+        oracle.tconv_backward(x, k, self.cfg["p"], gy)
+        return time.perf_counter() - t0, nimg, "port"
+
+
 class Stack:
     """BASELINE C5: four-layer bf16 generator stack, batch 1024 sharded over ranks."""
 
@@ -350,12 +425,25 @@ def run_reference(args, cfg):
         import ctypes  # noqa: F401
         from oracle.oracle import count_ops
         macs = count_ops(n, cin, cout, k, k, p)[2] * nimg
+        bwd = args.pass_ == "backward"
+        if bwd:  # backward: 2x the forward's useful MACs; output gradient ~ N(0, 1)
+            macs *= 2
+            g = oracle.geometry(n, k, k, p)
+            gy = rng.standard_normal((nimg, g.out_h, g.out_w, cout), dtype=np.float32)
+            if cfg["dtype"] == "bf16":
+                gy = oracle.bf16_round(gy)
         for i in range(args.warmup + args.steps):
             if kind == "reference":
-                _, secs = oracle.ref_time_fused_batch(1, x, kk, p, workers)
+                if bwd:
+                    _, _, secs = oracle.ref_time_backward(x, kk, p, gy, workers)
+                else:
+                    _, secs = oracle.ref_time_fused_batch(1, x, kk, p, workers)
             else:
                 t0 = time.perf_counter()
-                oracle.tconv_fused(x, kk, p)
+                if bwd:
+                    oracle.tconv_backward(x, kk, p, gy)
+                else:
+                    oracle.tconv_fused(x, kk, p)
                 secs = time.perf_counter() - t0
             if i >= args.warmup:
                 times.append(secs)
@@ -365,7 +453,11 @@ def run_reference(args, cfg):
     sample = (f"{nimgs} of {cfg['batch']} images per step, harness batch-threading over the "
               f"reference's sequential transpose_conv_fused (images across {workers} threads)"
               if kind == "reference" else f"{nimgs} images per step, single-thread C port")
-    out = {"metric": METRIC, "value": round(val, 4), "unit": "useful GMAC/s", "impl": "reference",
+    if args.pass_ == "backward":
+        sample = sample.replace("transpose_conv_fused",
+                                "net::FusedTConv::backward (timed; its forward untimed)")
+    out = {"metric": METRIC + (" [backward pass]" if args.pass_ == "backward" else ""),
+           "value": round(val, 4), "unit": "useful GMAC/s", "impl": "reference",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
            "scaling": "strong" if cfg.get("stack") else "weak", "vs_baseline": None,
@@ -389,6 +481,8 @@ def main():
                     choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="segconv", choices=["segconv", "reference"])
     ap.add_argument("--no-baselines", action="store_true", help="skip conventional/cuDNN/CPU legs")
+    ap.add_argument("--pass", dest="pass_", default="forward", choices=["forward", "backward"],
+                    help="backward: the layer's input + kernel gradients (not for the C5 stack)")
     ap.add_argument("--no-e2e", action="store_true",
                     help="diagnostics (ncu launch lists): skip the host-buffer e2e leg")
     args = ap.parse_args()
@@ -413,8 +507,11 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     from paper_2209_03704_b200 import segconv as sc
 
+    bwd = args.pass_ == "backward"
+    if bwd and cfg.get("stack"):
+        raise SystemExit("--pass backward runs on single-layer configs (C1-C4, C5a-d)")
     prob = Stack(cfg, rank, world, torch, sc, dev) if cfg.get("stack") else \
-        Layer(cfg, rank, torch, sc, dev, world)
+        (LayerBackward if bwd else Layer)(cfg, rank, torch, sc, dev, world)
     flush_buf = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
 
     def flush():
@@ -429,7 +526,8 @@ def main():
     # overhead (ctypes, argument checks) is not on the device clock; the e2e
     # leg below goes through the public Python API eagerly.
     graph = None
-    if not cfg.get("stack") and not os.environ.get("SEGCONV_BENCH_EAGER"):
+    # (the backward pass allocates its split-K workspace per call: eager)
+    if not cfg.get("stack") and not bwd and not os.environ.get("SEGCONV_BENCH_EAGER"):
         side = torch.cuda.Stream()
         side.wait_stream(stream)
         with torch.cuda.stream(side):
@@ -532,6 +630,8 @@ def main():
                 extra["cudnn_conv_transpose2d"] = prob.cudnn(torch, 5, flush)
             except Exception as e:
                 extra["cudnn_conv_transpose2d"] = {"error": str(e)[:200]}
+            if bwd:
+                extra["cudnn_conv_transpose2d_backward"] = extra.pop("cudnn_conv_transpose2d")
             workers = os.cpu_count() or 1
             try:
                 secs, nimg, kind = prob.cpu_sample(workers)
@@ -540,17 +640,22 @@ def main():
                 extra["cpu_baseline"] = {
                     "value": round(cpu_val, 4), "unit": "useful GMAC/s",
                     "cores": workers if kind == "reference" else 1, "kind": kind,
-                    "sample": f"{nimg} images of the same workload, reference transpose_conv_fused "
-                              f"per image, images across {workers} host threads, one pass"}
+                    "sample": (f"{nimg} images of the same workload, reference "
+                               + ("net::FusedTConv::backward (timed; its forward untimed)" if bwd
+                                  else "transpose_conv_fused")
+                               + f" per image, images across {workers} host threads, one pass")}
             except Exception as e:
                 extra["cpu_baseline"] = {"error": str(e)[:200]}
-        out = {"metric": METRIC, "value": round(value, 2), "unit": "useful GMAC/s",
+        out = {"metric": METRIC + (" [backward pass]" if bwd else ""), "value": round(value, 2),
+               "unit": "useful GMAC/s",
                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": round(ms, 5), "higher_is_better": True,
                "scaling": "strong" if cfg.get("stack") else "weak", "vs_baseline": None,
                "dtype": "bf16" if cfg["dtype"] == "bf16" else "f32",
                "data": "synthetic (seeded, BASELINE distributions; no dataset)",
-               "config": {"workload": f"{args.config}: {cfg['desc']}", "math": prob.math,
+               "config": {"workload": f"{args.config}: {cfg['desc']}"
+                          + (" -- backward (input + kernel gradients)" if bwd else ""),
+                          "math": prob.math,
                           "per_gpu_batch": (prob.hi - prob.lo) if cfg.get("stack") else cfg["batch"],
                           "l2": "flushed between timed steps (256 MiB write, outside events)",
                           "parallelism": f"batch-sharded x{world}, weights replicated"},

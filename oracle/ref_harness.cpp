@@ -328,8 +328,7 @@ int ref_tconv_backward_f64(const double* x, int batch, int n, int cin, const dou
 
 // CPU baseline timing of the reference backward: `workers` threads each own a
 // FusedTConv and run forward + backward over a contiguous slice of the batch
-// (the layer caches its input, so one layer cannot be shared across threads);
-// the per-thread tap gradients are summed inside the timed region.
+// (the layer caches its input, so one layer cannot be shared across threads).
 int ref_time_backward_f32(const float* x, int batch, int n, int cin, const float* k, int kh, int kw,
                           int cout, int p, const float* gy, int workers, float* gx, float* gk,
                           double* seconds) {
@@ -350,25 +349,31 @@ int ref_time_backward_f32(const float* x, int batch, int n, int cin, const float
       gs.push_back(segconv::Tensor<float>::from_data(
           geom.out_h, geom.out_w, cout, std::vector<float>(gy + b * osz, gy + (b + 1) * osz)));
     }
-    const auto t0 = std::chrono::steady_clock::now();
+    // the forward each backward needs (the layer caches its input) is run but not
+    // timed: seconds = max over threads of that thread's backward time + the
+    // final sum of the per-thread tap gradients
+    std::vector<double> busy(nt, 0.0);
     std::vector<std::thread> pool;
     for (int t = 0; t < nt; ++t)
       pool.emplace_back([&, t] {
         const int b0 = (int)((long long)batch * t / nt), b1 = (int)((long long)batch * (t + 1) / nt);
         for (int b = b0; b < b1; ++b) {
           layers[t]->forward(ins[b]);
+          const auto a = std::chrono::steady_clock::now();
           const auto gi = layers[t]->backward(gs[b]);
+          busy[t] += std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
           std::memcpy(gx + b * isz, gi.data(), isz * sizeof(float));
         }
       });
     for (auto& th : pool) th.join();
+    const auto t0 = std::chrono::steady_clock::now();
     std::memset(gk, 0, ksz * sizeof(float));
     for (int t = 0; t < nt; ++t) {
       const float* g = layers[t]->params()[0].grads;
       for (size_t e = 0; e < ksz; ++e) gk[e] += g[e];
     }
     const auto t1 = std::chrono::steady_clock::now();
-    *seconds = std::chrono::duration<double>(t1 - t0).count();
+    *seconds = *std::max_element(busy.begin(), busy.end()) + std::chrono::duration<double>(t1 - t0).count();
   });
 }
 

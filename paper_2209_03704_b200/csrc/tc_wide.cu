@@ -316,13 +316,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t pa = 0, pb = 0;
       int s, t, ct, nt;
       const int img = p.n * p.n;
+      const int di = 64 / p.n, dj = 64 - (64 / p.n) * p.n;  // a chunk = di rows + dj pixels
       for (int k = 0; wunit_of(p, k, s, t, ct, nt); ++k) {
         const int ch0 = ct * 256 + (int)rank * 128, f0 = nt * p.NT + (int)rank * NT2;
         const long long c1 = min(p.w_chunks, (long long)(s + 1) * p.w_cps);
+        // first anchor of the unit's first chunk; then advanced by 64 pixels per
+        // chunk without divisions (the single producer lane is on the critical path)
+        const long long mfirst = (long long)s * p.w_cps * 64;
+        int b0 = (int)(mfirst / img);
+        int i0 = (int)(mfirst - (long long)b0 * img);
+        int j0 = i0 % p.n;
+        i0 /= p.n;
         for (long long c = (long long)s * p.w_cps; c < c1; ++c) {
           const long long m = c * 64;
-          const int b0 = (int)(m / img), rem = (int)(m - (long long)b0 * img);
-          const int i0 = rem / p.n, j0 = rem - (rem / p.n) * p.n;
           mbar_wait(&a_empty[sa], pa ^ 1);
           const uint32_t af = mapa(smem_u32(&a_full[sa]), 0);
           if (rank == 0) mbar_arrive_expect_tx(&a_full[sa], 2 * 2 * 64 * 128);
@@ -343,6 +349,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (++sb == SB) {
             sb = 0;
             pb ^= 1;
+          }
+          j0 += dj;
+          i0 += di;
+          if (j0 >= p.n) {
+            j0 -= p.n;
+            ++i0;
+          }
+          if (i0 >= p.n) {
+            const int q = i0 / p.n;
+            b0 += q;
+            i0 -= q * p.n;
           }
         }
       }
@@ -1069,20 +1086,27 @@ static bool make_wide_wgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
       p.tap_off_c[0][U * pr.kw + V] = pr.kw - 1 - V;
     }
   p.w_chunks = (M + 63) / 64;
-  // splits: best wave balance over the pairs, >= 8 chunks per unit (epilogue overlap)
+  // splits: minimise modelled time = waves x chunks per unit x t_chunk + the
+  // split-K round trip of the partials (write + reduce read, ~5 TB/s, + launch);
+  // t_chunk ~ 0.6 us for a 256 x 256 x 64 pair chunk (measured, B200)
   const long long base = (long long)taps * p.w_ch_pairs * p.n_tiles;
+  const double t_chunk = 0.6 * p.NT / 256.0;
+  const double t_split = (double)taps * pr.cin * pr.cout * 8.0 / 5e6;  // us per split
   int best = 1;
-  double best_eff = 0;
+  double best_t = 1e300;
   for (int sp = 1; sp <= 64; ++sp) {
     if (sp > 1 && p.w_chunks / sp < 8) break;
     const long long units = base * sp;
     const long long waves = (units + pairs - 1) / pairs;
-    const double eff = (double)units / (double)(waves * pairs);
-    if (eff > best_eff + 0.02) {
-      best_eff = eff;
+    const double t = (double)waves * (double)((p.w_chunks + sp - 1) / sp) * t_chunk +
+                     (sp > 1 ? sp * t_split + 3.0 : 0.0);
+    if (t < best_t * 0.98) {
+      best_t = t;
       best = sp;
     }
   }
+  if (const char* e = getenv("SEGCONV_WGRAD_SPLITS"))  // diagnostics
+    if (*e) best = std::max(1, atoi(e));
   p.w_cps = (p.w_chunks + best - 1) / best;
   p.w_splits = (int)((p.w_chunks + p.w_cps - 1) / p.w_cps);
   p.w_direct = p.w_splits == 1;
