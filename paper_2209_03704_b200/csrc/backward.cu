@@ -51,6 +51,27 @@ __device__ __forceinline__ ACC ld(const T* p) {
   return (ACC)to_acc(p[0]);
 }
 
+// 4 consecutive elements p[0..3] (entries at or past `lim` read as 0); one
+// vector load when all 4 exist and p is aligned for it
+template <typename ACC, typename T>
+__device__ __forceinline__ void ld4(const T* p, int lim, bool ok, ACC (&v)[4]) {
+  if (ok && lim >= 4 && (reinterpret_cast<uintptr_t>(p) & (4 * sizeof(T) - 1)) == 0) {
+    if constexpr (sizeof(T) == 4) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+      v[0] = q.x, v[1] = q.y, v[2] = q.z, v[3] = q.w;
+      return;
+    } else if constexpr (sizeof(T) == 2) {
+      const uint2 q = __ldg(reinterpret_cast<const uint2*>(p));
+      const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&q.x);
+      const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&q.y);
+      v[0] = __low2float(a), v[1] = __high2float(a), v[2] = __low2float(b), v[3] = __high2float(b);
+      return;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) v[e] = (ok && e < lim) ? ld<ACC>(p + e) : ACC(0);
+}
+
 // reference segregation.hpp:23-36
 __device__ __forceinline__ int first_tap(int p, int r) { return (p + r) & 1; }
 __device__ __forceinline__ int tap_count(int n, int p, int r) {
@@ -157,11 +178,13 @@ __global__ void __launch_bounds__(NT) dgrad_ffma(const T* __restrict__ gy, const
     const T* gp = gy + (((long long)b * pr.out_h + (av ? y : 0)) * pr.out_w + (av ? xx : 0)) * pr.cout;
     const T* kp = k + ((long long)t * pr.cin + (kv ? ch0 + lp : 0)) * pr.cout;
     for (int f0 = 0; f0 < pr.cout; f0 += BK) {
+      ACC va[4], vb[4];
+      ld4<ACC>(gp + f0 + lf, pr.cout - f0 - lf, av, va);
+      ld4<ACC>(kp + f0 + lf, pr.cout - f0 - lf, kv, vb);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const int f = f0 + lf + e;
-        As[lf + e][lp] = (av && f < pr.cout) ? ld<ACC>(gp + f) : ACC(0);
-        Bs[lf + e][lp] = (kv && f < pr.cout) ? ld<ACC>(kp + f) : ACC(0);
+        As[lf + e][lp] = va[e];
+        Bs[lf + e][lp] = vb[e];
       }
       __syncthreads();
 #pragma unroll
@@ -192,6 +215,165 @@ __global__ void __launch_bounds__(NT) dgrad_ffma(const T* __restrict__ gy, const
   }
 }
 
+// Narrow layers (cout % 16 != 0, e.g. the 3-channel output layers C4, C5 d):
+// K packed as (tap, f) pairs, f fastest, so a 16-deep step never idles on
+// missing features (cout = 3 would use 3 of every 16).
+template <typename T, typename ACC>
+__global__ void __launch_bounds__(NT) dgrad_ffma_packed(const T* __restrict__ gy, const T* __restrict__ k,
+                                                        T* __restrict__ gx, BackwardProblem pr) {
+  __shared__ ACC As[BK][BM + 4];
+  __shared__ ACC Bs[BK][BN + 4];
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const long long M = (long long)pr.batch * pr.n * pr.n;
+  const long long m0 = (long long)blockIdx.x * BM;
+  const int ch0 = blockIdx.y * BN;
+  const int lp = tid >> 2, lf = (tid & 3) * 4;
+  const long long m = m0 + lp;
+  const bool mv = m < M;
+  const int j = mv ? (int)(m % pr.n) : 0, i = mv ? (int)((m / pr.n) % pr.n) : 0;
+  const int b = mv ? (int)(m / ((long long)pr.n * pr.n)) : 0;
+  const bool kv = ch0 + lp < pr.cin;
+  const int K = pr.kh * pr.kw * pr.cout;
+  const T* gb = gy + (long long)b * pr.out_h * pr.out_w * pr.cout;
+  ACC acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    int t = (k0 + lf) / pr.cout, f = (k0 + lf) - ((k0 + lf) / pr.cout) * pr.cout;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      ACC va = 0, vb = 0;
+      if (k0 + lf + e < K) {
+        const int U = t / pr.kw, V = t - (t / pr.kw) * pr.kw;
+        const int y = 2 * i + pr.p - U, xx = 2 * j + pr.p - V;
+        if (mv && y >= 0 && y < pr.out_h && xx >= 0 && xx < pr.out_w)
+          va = ld<ACC>(gb + ((long long)y * pr.out_w + xx) * pr.cout + f);
+        if (kv) vb = ld<ACC>(k + ((long long)t * pr.cin + ch0 + lp) * pr.cout + f);
+      }
+      As[lf + e][lp] = va;
+      Bs[lf + e][lp] = vb;
+      if (++f == pr.cout) {
+        f = 0;
+        ++t;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      ACC a[4], w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        a[e] = As[kk][ty * 4 + e];
+        w[e] = Bs[kk][tx * 4 + e];
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] += a[r] * w[c];
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const long long mm = m0 + ty * 4 + r;
+    if (mm >= M) continue;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int ch = ch0 + tx * 4 + c;
+      if (ch < pr.cin) gx[mm * pr.cin + ch] = from_acc<T>(acc[r][c]);
+    }
+  }
+}
+
+// gk with N packed as (tap, f) pairs (cout % 64 != 0): one CTA covers 64
+// channels x 64 packed columns over a pixel range, every tap of the tile at once.
+template <typename T, typename ACC>
+__global__ void __launch_bounds__(NT) wgrad_ffma_packed(const T* __restrict__ x, const T* __restrict__ gy,
+                                                        ACC* __restrict__ out, BackwardProblem pr, int splits,
+                                                        long long chunk, int direct) {
+  __shared__ ACC As[BK][BM + 4];
+  __shared__ ACC Bs[BK][BN + 4];
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const long long M = (long long)pr.batch * pr.n * pr.n;
+  const int NP = pr.kh * pr.kw * pr.cout;
+  const int ch0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int s = blockIdx.z;
+  const long long mb = (long long)s * chunk, me = (mb + chunk < M) ? mb + chunk : M;
+  const int lp = tid >> 4, lc = (tid & 15) * 4;
+  // this thread's 4 packed columns: tap offsets (U, V) and feature f
+  int cu[4], cv[4], cf[4];
+  bool cok[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int n = n0 + lc + e;
+    cok[e] = n < NP;
+    const int t = cok[e] ? n / pr.cout : 0;
+    cf[e] = cok[e] ? n - t * pr.cout : 0;
+    cu[e] = t / pr.kw;
+    cv[e] = t - (t / pr.kw) * pr.kw;
+  }
+  ACC acc[4][4] = {};
+  const int img = pr.n * pr.n, di = BK / pr.n, dj = BK - (BK / pr.n) * pr.n;
+  const long long mf = mb + lp;
+  int b = (int)(mf / img), i = (int)(mf - (long long)b * img), j = i % pr.n;
+  i /= pr.n;
+  for (long long mk = mb; mk < me; mk += BK) {
+    const long long m = mk + lp;
+    const bool mv = m < me;
+    ACC va[4];
+    ld4<ACC>(x + (mv ? m : 0) * pr.cin + ch0 + lc, pr.cin - ch0 - lc, mv, va);
+    const T* gb = gy + (long long)b * pr.out_h * pr.out_w * pr.cout;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int y = 2 * i + pr.p - cu[e], xx = 2 * j + pr.p - cv[e];
+      const bool ok = mv && cok[e] && y >= 0 && y < pr.out_h && xx >= 0 && xx < pr.out_w;
+      As[lp][lc + e] = va[e];
+      Bs[lp][lc + e] = ok ? ld<ACC>(gb + ((long long)y * pr.out_w + xx) * pr.cout + cf[e]) : ACC(0);
+    }
+    j += dj;
+    i += di;
+    if (j >= pr.n) {
+      j -= pr.n;
+      ++i;
+    }
+    if (i >= pr.n) {
+      const int q = i / pr.n;
+      b += q;
+      i -= q * pr.n;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      ACC a[4], w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        a[e] = As[kk][ty * 4 + e];
+        w[e] = Bs[kk][tx * 4 + e];
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] += a[r] * w[c];
+    }
+    __syncthreads();
+  }
+  const long long ksz = (long long)pr.kh * pr.kw * pr.cin * pr.cout;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int n = n0 + tx * 4 + c;
+    if (n >= NP) continue;
+    const int t = n / pr.cout, f = n - (n / pr.cout) * pr.cout;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int ch = ch0 + ty * 4 + r;
+      if (ch >= pr.cin) continue;
+      const long long idx = ((long long)t * pr.cin + ch) * pr.cout + f;
+      if (direct)
+        out[idx] = (pr.accumulate ? out[idx] : ACC(0)) + acc[r][c];
+      else
+        out[(long long)s * ksz + idx] = acc[r][c];
+    }
+  }
+}
+
 // gk tile: 64 input channels x 64 features of one tap over a pixel range.
 template <typename T, typename ACC>
 __global__ void __launch_bounds__(NT) wgrad_ffma(const T* __restrict__ x, const T* __restrict__ gy,
@@ -207,20 +389,36 @@ __global__ void __launch_bounds__(NT) wgrad_ffma(const T* __restrict__ x, const 
   const long long mb = (long long)s * chunk, me = (mb + chunk < M) ? mb + chunk : M;
   const int lp = tid >> 4, lc = (tid & 15) * 4;  // loader: pixel lp, 4 consecutive channels
   ACC acc[4][4] = {};
+  // this thread's pixel (b, i, j), advanced by BK pixels per step without divisions
+  const int img = pr.n * pr.n, di = BK / pr.n, dj = BK - (BK / pr.n) * pr.n;
+  const long long m0 = mb + lp;
+  int b = (int)(m0 / img), i = (int)(m0 - (long long)b * img), j = i % pr.n;
+  i /= pr.n;
   for (long long mk = mb; mk < me; mk += BK) {
     const long long m = mk + lp;
     const bool mv = m < me;
-    const int j = mv ? (int)(m % pr.n) : 0, i = mv ? (int)((m / pr.n) % pr.n) : 0;
-    const int b = mv ? (int)(m / ((long long)pr.n * pr.n)) : 0;
     const int y = 2 * i + pr.p - U, xx = 2 * j + pr.p - V;
     const bool gv = mv && y >= 0 && y < pr.out_h && xx >= 0 && xx < pr.out_w;
     const T* xp = x + (mv ? m : 0) * pr.cin;
     const T* gp = gy + (((long long)b * pr.out_h + (gv ? y : 0)) * pr.out_w + (gv ? xx : 0)) * pr.cout;
+    ACC va[4], vb[4];
+    ld4<ACC>(xp + ch0 + lc, pr.cin - ch0 - lc, gv, va);
+    ld4<ACC>(gp + f0 + lc, pr.cout - f0 - lc, gv, vb);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int ch = ch0 + lc + e, f = f0 + lc + e;
-      As[lp][lc + e] = (gv && ch < pr.cin) ? ld<ACC>(xp + ch) : ACC(0);
-      Bs[lp][lc + e] = (gv && f < pr.cout) ? ld<ACC>(gp + f) : ACC(0);
+      As[lp][lc + e] = va[e];
+      Bs[lp][lc + e] = vb[e];
+    }
+    j += dj;
+    i += di;
+    if (j >= pr.n) {
+      j -= pr.n;
+      ++i;
+    }
+    if (i >= pr.n) {
+      const int q = i / pr.n;
+      b += q;
+      i -= q * pr.n;
     }
     __syncthreads();
 #pragma unroll
@@ -309,7 +507,10 @@ static cudaError_t bwd_data_t(const BackwardProblem& pr, bool exact, cudaStream_
   } else {
     using ACC = typename std::conditional<sizeof(T) == 8, double, float>::type;
     dim3 grid((unsigned)((M + bwd::BM - 1) / bwd::BM), (unsigned)((pr.cin + bwd::BN - 1) / bwd::BN));
-    bwd::dgrad_ffma<T, ACC><<<grid, bwd::NT, 0, s>>>((const T*)pr.gy, (const T*)pr.k, (T*)pr.gx, pr);
+    if (pr.cout % bwd::BK != 0)
+      bwd::dgrad_ffma_packed<T, ACC><<<grid, bwd::NT, 0, s>>>((const T*)pr.gy, (const T*)pr.k, (T*)pr.gx, pr);
+    else
+      bwd::dgrad_ffma<T, ACC><<<grid, bwd::NT, 0, s>>>((const T*)pr.gy, (const T*)pr.k, (T*)pr.gx, pr);
   }
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) note_launch();
@@ -338,7 +539,11 @@ static cudaError_t bwd_weight_t(const BackwardProblem& pr, bool exact, cudaStrea
       return e;
     }
   }
-  const int tiles = ((pr.cin + bwd::BM - 1) / bwd::BM) * ((pr.cout + bwd::BN - 1) / bwd::BN) * pr.kh * pr.kw;
+  // cout % 64 != 0: (tap, f) packed columns, all taps of a tile in one CTA
+  const bool packed = pr.cout % bwd::BN != 0;
+  const int taps = pr.kh * pr.kw;
+  const int ntile = packed ? (taps * pr.cout + bwd::BN - 1) / bwd::BN : (pr.cout + bwd::BN - 1) / bwd::BN;
+  const int tiles = ((pr.cin + bwd::BM - 1) / bwd::BM) * ntile * (packed ? 1 : taps);
   // split the pixel reduction until ~2 CTAs per SM, keeping >= 512 pixels per split
   long long splits = std::max(1LL, (2LL * sm_count() + tiles - 1) / tiles);
   splits = std::min(splits, std::max(1LL, M / 512));
@@ -346,23 +551,25 @@ static cudaError_t bwd_weight_t(const BackwardProblem& pr, bool exact, cudaStrea
   long long chunk = (M + splits - 1) / splits;
   chunk = std::max<long long>(bwd::BK, (chunk + bwd::BK - 1) / bwd::BK * bwd::BK);
   splits = std::max(1LL, (M + chunk - 1) / chunk);
-  dim3 grid((unsigned)((pr.cin + bwd::BM - 1) / bwd::BM), (unsigned)((pr.cout + bwd::BN - 1) / bwd::BN),
-            (unsigned)(pr.kh * pr.kw * splits));
-  if (splits == 1) {
-    bwd::wgrad_ffma<T, ACC><<<grid, bwd::NT, 0, s>>>((const T*)pr.x, (const T*)pr.gy, (ACC*)pr.gk, pr, 1,
-                                                     std::max(chunk, 1LL), 1);
+  dim3 grid((unsigned)((pr.cin + bwd::BM - 1) / bwd::BM), (unsigned)ntile,
+            (unsigned)((packed ? 1 : taps) * splits));
+  auto launch = [&](ACC* out, int direct) {
+    if (packed)
+      bwd::wgrad_ffma_packed<T, ACC><<<grid, bwd::NT, 0, s>>>((const T*)pr.x, (const T*)pr.gy, out, pr,
+                                                              (int)splits, chunk, direct);
+    else
+      bwd::wgrad_ffma<T, ACC><<<grid, bwd::NT, 0, s>>>((const T*)pr.x, (const T*)pr.gy, out, pr, (int)splits,
+                                                       chunk, direct);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) note_launch();
     return e;
-  }
+  };
+  if (splits == 1) return launch((ACC*)pr.gk, 1);
   ACC* ws = nullptr;
   cudaError_t e = workspace_alloc((void**)&ws, (size_t)splits * ksz * sizeof(ACC), s);
   if (e != cudaSuccess) return e;
-  bwd::wgrad_ffma<T, ACC><<<grid, bwd::NT, 0, s>>>((const T*)pr.x, (const T*)pr.gy, ws, pr, (int)splits,
-                                                   chunk, 0);
-  e = cudaGetLastError();
+  e = launch(ws, 0);
   if (e == cudaSuccess) {
-    note_launch();
     bwd::wgrad_reduce<ACC><<<(unsigned)((ksz + 255) / 256), 256, 0, s>>>(ws, (ACC*)pr.gk, ksz, (int)splits,
                                                                         pr.accumulate);
     e = cudaGetLastError();
