@@ -175,11 +175,11 @@ class Layer:
     def conventional(self, torch, steps, flush):
         """GPU upsample+conv (reference transpose_conv_naive) on the same data."""
         cfg = self.cfg
-        ws_need = (cfg["batch"] * self.g.up_h ** 2 * cfg["cin"] * 4)
-        if ws_need > 24 * 2 ** 30 or self.tdt != torch.float32:
+        ws_need = (cfg["batch"] * self.g.up_h ** 2 * cfg["cin"] * self.xd.element_size())
+        if ws_need > 24 * 2 ** 30:
             return None
-        xf = self.xd.float()
-        kf = torch.from_numpy(self.k_host).cuda()
+        xf = self.xd  # same dtype as the fused path (bf16 -> tensor-core conv2d_valid)
+        kf = self.kd
         ws = torch.empty(ws_need, dtype=torch.uint8, device="cuda")
         ts = []
         for i in range(steps + 1):
@@ -193,7 +193,8 @@ class Layer:
                 ts.append(a.elapsed_time(b))
         ms = statistics.median(ts)
         return {"value": round(self.macs / (ms * 1e-3) / 1e9, 2), "ms_per_step": round(ms, 4),
-                "what": "GPU upsample2x+pad then valid correlation (segconv_transpose_conv_naive)"}
+                "what": "GPU upsample2x+pad then valid correlation (segconv_transpose_conv_naive; "
+                        + self.sc.last_path() + " correlation)"}
 
     def cudnn(self, torch, steps, flush):
         """Library context: torch conv_transpose2d (cuDNN) on the same problem, NCHW."""

@@ -18,7 +18,7 @@ __all__ = [
     "ref_tconv_naive", "ref_tconv_fused_parallel", "ref_run_verify", "ref_verify_case",
     "ref_count_ops", "ref_time_fused_batch", "OracleError", "bf16_round", "tf32_round",
     "tconv_backward", "scatter_backward_f64", "ref_tconv_backward", "ref_time_backward",
-    "ref_save_tensor", "ref_load_tensor",
+    "ref_save_tensor", "ref_load_tensor", "conv2d_valid", "ref_conv2d_valid",
 ]
 
 
@@ -64,6 +64,10 @@ def load_oracle():
             getattr(lib, f"orc_tconv_backward_{name}").argtypes = [
                 pt, C.c_int, C.c_int, C.c_int, pt, C.c_int, C.c_int, C.c_int, C.c_int, pt, pt, pt]
         lib.orc_scatter_backward_f64.argtypes = lib.orc_tconv_backward_f64.argtypes
+        for name, T in (("f32", C.c_float), ("f64", C.c_double)):
+            pt = C.POINTER(T)
+            getattr(lib, f"orc_conv2d_valid_{name}").argtypes = [pt] + [C.c_int] * 4 + [pt] + \
+                [C.c_int] * 3 + [pt]
         lib.orc_subkernel_dims.argtypes = [C.c_int, C.c_int, C.c_int, ip, ip]
         lib.orc_count_ops.argtypes = [C.c_int] * 6 + [C.POINTER(C.c_uint64)]
         _lib = lib
@@ -95,6 +99,7 @@ def load_ref():
         lib.ref_time_backward_f32.argtypes = [
             fp, C.c_int, C.c_int, C.c_int, fp, C.c_int, C.c_int, C.c_int, C.c_int, fp, C.c_int,
             fp, fp, dp]
+        lib.ref_conv2d_valid_f32.argtypes = [fp] + [C.c_int] * 4 + [fp] + [C.c_int] * 3 + [fp]
         lib.ref_save_tensor.argtypes = [C.c_char_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
         lib.ref_load_tensor.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_size_t, ip]
         lib.ref_last_error_offset.restype = C.c_size_t
@@ -251,6 +256,32 @@ def tconv_backward(x, k, p, gy):
 
 def scatter_backward_f64(x, k, p, gy):
     return _backward("orc_scatter_backward_f64", x, k, p, gy, load_oracle(), force_f64=True)
+
+
+def _conv_valid(lib, prefix, src, k):
+    src = np.asarray(src)
+    f64 = src.dtype == np.float64 and prefix == "orc"
+    cast = _f64 if f64 else _f32
+    src, k = cast(src), cast(k)
+    squeeze = src.ndim == 3
+    if squeeze:
+        src = src[None]
+    b, h, w, cin = src.shape
+    kh, kw, _, cout = k.shape
+    out = np.empty((b, h - kh + 1, w - kw + 1, cout), dtype=src.dtype)
+    T = C.c_double if f64 else C.c_float
+    fn = getattr(lib, f"{prefix}_conv2d_valid_{'f64' if f64 else 'f32'}")
+    _check(fn(_ptr(src, T), b, h, w, cin, _ptr(k, T), kh, kw, cout, _ptr(out, T)), lib)
+    return out[0] if squeeze else out
+
+
+def conv2d_valid(src, k):
+    """Valid correlation, reference order (reference_ops.hpp:86-102), batch or single map."""
+    return _conv_valid(load_oracle(), "orc", src, k)
+
+
+def ref_conv2d_valid(src, k):
+    return _conv_valid(load_ref(), "ref", src, k)
 
 
 def count_ops(n, cin, cout, kh, kw, p):

@@ -317,6 +317,21 @@ int ref_time_fused_batch_f32(int mode, const float* x, int batch, int n, int cin
   });
 }
 
+// reference_ops.hpp:86-108 (conv2d_valid) over a batch of (h, w, cin) maps
+int ref_conv2d_valid_f32(const float* src, int batch, int h, int w, int cin, const float* k, int kh, int kw,
+                         int cout, float* out) {
+  return guarded([&] {
+    const auto kk = kernel(k, kh, kw, cin, cout);
+    const size_t isz = (size_t)h * w * cin, osz = (size_t)(h - kh + 1) * (w - kw + 1) * cout;
+    for (int b = 0; b < batch; ++b) {
+      const auto in = segconv::Tensor<float>::from_data(h, w, cin,
+                                                        std::vector<float>(src + b * isz, src + (b + 1) * isz));
+      const auto y = segconv::conv2d_valid(in, kk);
+      std::memcpy(out + b * osz, y.data(), osz * sizeof(float));
+    }
+  });
+}
+
 int ref_tconv_backward_f32(const float* x, int batch, int n, int cin, const float* k, int kh,
                            int kw, int cout, int p, const float* gy, float* gx, float* gk) {
   return run_backward<float>(x, batch, n, cin, k, kh, kw, cout, p, gy, gx, gk);

@@ -647,6 +647,13 @@ segconv_status segconv_conv2d_valid(const void* d_src, segconv_dtype dtype, int 
   if ((epilogue & SEGCONV_EPI_BIAS) && !d_bias)
     return fail(SEGCONV_E_CONTRACT, "bias epilogue requested without a bias pointer");
   if (batch == 0) return SEGCONV_OK;
+  if (dtype == SEGCONV_BF16 && tc_conv_valid_supported(batch, h, w, cin, kh, kw, cout) &&
+      !getenv("SEGCONV_NO_TC_CONV"))
+    g_path = "tc-pair";
+  else if (dtype == SEGCONV_F32 && kh == kw && cout > 4 && kh >= 3 && kh <= 5)
+    g_path = "simt-tiled";
+  else
+    g_path = "simt-generic";
   return cuda_status(launch_conv2d_valid(d_src, dtype, batch, h, w, cin, d_kernel, kh, kw, cout,
                                          d_bias, epilogue, d_y, (cudaStream_t)stream),
                      "conv2d_valid");

@@ -9,6 +9,8 @@
 // SIMT kernel.
 #include <algorithm>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -180,11 +182,41 @@ static cudaError_t run_conv_tiled(const float* src, int batch, int h, int w, int
   return cudaGetLastError();
 }
 
+// (taps, cin, cout) -> (cout, taps, cin): the K-major B operand of the
+// tensor-core valid correlation
+__global__ void kmajor_transpose(const __nv_bfloat16* __restrict__ k, int taps, int cin, int cout,
+                                 __nv_bfloat16* __restrict__ kt) {
+  const long long total = (long long)taps * cin * cout;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int ch = (int)(e % cin);
+    const long long r = e / cin;
+    const int t = (int)(r % taps), f = (int)(r / taps);
+    kt[e] = k[((long long)t * cin + ch) * cout + f];
+  }
+}
+
 cudaError_t launch_conv2d_valid(const void* src, int dtype, int batch, int h, int w, int cin,
                                 const void* k, int kh, int kw, int cout, const float* bias,
                                 unsigned epi, void* y, cudaStream_t s) {
   const long long total = (long long)batch * (h - kh + 1) * (w - kw + 1) * cout;
   if (total <= 0) return cudaSuccess;
+  if (dtype == SEGCONV_BF16 && tc_conv_valid_supported(batch, h, w, cin, kh, kw, cout) &&
+      getenv("SEGCONV_NO_TC_CONV") == nullptr) {
+    const long long kn = (long long)kh * kw * cin * cout;
+    void* kt = nullptr;
+    cudaError_t e = workspace_alloc(&kt, (size_t)kn * 2, s);
+    if (e != cudaSuccess) return e;
+    kmajor_transpose<<<(unsigned)std::min<long long>((kn + 255) / 256, 148LL * 16), 256, 0, s>>>(
+        (const __nv_bfloat16*)k, kh * kw, cin, cout, (__nv_bfloat16*)kt);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) {
+      note_launch();
+      e = launch_tc_conv_valid(src, batch, h, w, cin, kt, kh, kw, cout, bias, epi, y, s);
+    }
+    const cudaError_t e2 = cudaFreeAsync(kt, s);
+    return e != cudaSuccess ? e : e2;
+  }
   if (dtype == SEGCONV_F32 && kh == kw && cout > 4) {
     const float* sp = (const float*)src;
     const float* kp = (const float*)k;

@@ -49,6 +49,9 @@ cudaError_t launch_bwd_weight_simt(const BackwardProblem& pr, bool exact, cudaSt
 bool tc_bwd_data_supported(const BackwardProblem& pr);
 cudaError_t launch_tc_bwd_data(const BackwardProblem& pr, cudaStream_t s);
 bool tc_bwd_weight_supported(const BackwardProblem& pr);
+bool tc_conv_valid_supported(int batch, int h, int w, int cin, int kh, int kw, int cout);
+cudaError_t launch_tc_conv_valid(const void* src, int batch, int h, int w, int cin, const void* kt, int kh,
+                                 int kw, int cout, const float* bias, unsigned epi, void* y, cudaStream_t s);
 cudaError_t launch_tc_bwd_weight(const BackwardProblem& pr, cudaStream_t s);
 cudaError_t workspace_alloc(void** p, size_t bytes, cudaStream_t s);
 cudaError_t launch_wgrad_reduce(const float* ws, float* gk, long long ksz, int splits, int accumulate,

@@ -1167,6 +1167,93 @@ bool tc_bwd_weight_supported(const BackwardProblem& pr) {
   return make_wide_wgrad(pr, p, m, wide_pairs());
 }
 
+// Valid correlation (reference reference_ops.hpp:86-102, conv2d_valid) on the
+// pair kernel: one class, every tap (u, v) an im2col offset of the stride-1 walk
+// over the output pixels; B = the kernel transposed to (cout, tap, cin) K-major
+// (launch_kmajor_transpose); bias / ReLU / tanh epilogue as the fused op.
+static bool make_wide_conv(const void* src, int batch, int h, int w, int cin, const void* kt, int kh, int kw,
+                           int cout, const float* bias, unsigned epi, void* y, tcw::Params& p, tcw::Maps& maps) {
+  p = tcw::Params{};
+  const int taps = kh * kw;
+  if (cin % tcw::KB != 0 || cout < 64 || taps > tcw::MAX_TAPS_Q || kh > 128 || kw > 128) return false;
+  const int oh = h - kh + 1, ow = w - kw + 1;
+  if (oh < 1 || ow < 1 || batch < 1) return false;
+  if ((long long)batch * oh * ow * cout >= (1LL << 40)) return false;
+  p.y = y;
+  p.bias = bias;
+  p.epi = epi;
+  p.y_dtype = SEGCONV_BF16;
+  p.batch = batch;
+  p.n = h;
+  p.cin = cin;
+  p.cout = cout;
+  p.out_h = oh;
+  p.out_w = ow;
+  p.NT = tc_wide_ntile(cout);
+  p.n_tiles = (cout + p.NT - 1) / p.NT;
+  p.nkb = cin / tcw::KB;
+  p.im2col = 1;
+  p.S_rows = 128;
+  p.taps[0] = taps;
+  for (int u = 0; u < kh; ++u)
+    for (int v = 0; v < kw; ++v) {
+      p.tap_off_r[0][u * kw + v] = u;
+      p.tap_off_c[0][u * kw + v] = v;
+    }
+  p.rows[0] = oh;
+  p.cols[0] = ow;
+  p.wscale = 1;
+  p.wbase_r = p.wbase_c = 0;
+  p.ostride = 1;
+  p.a_stage_bytes = 128 * 128;
+  p.b_stage_bytes = (p.NT / 2) * 128;
+  if (p.b_stage_bytes % 1024) return false;
+  const int bar_bytes = (2 * tcw::MAX_STAGES_A + 2 * tcw::MAX_STAGES_B + 4) * 8 + 16;
+  p.stages_a = p.stages_b =
+      std::min(tcw::MAX_STAGES_A, (tcw::SMEM_LIMIT - bar_bytes) / (p.a_stage_bytes + p.b_stage_bytes));
+  if (p.stages_a < 2) return false;
+  const long long u1 = ((long long)batch * oh * ow + 255) / 256 * p.n_tiles;
+  p.unit_base[0] = 0;
+  for (int q = 1; q <= 4; ++q) p.unit_base[q] = u1;
+  p.units = u1;
+  EncodeTiledFnW fn = encode_fn_w();
+  EncIm2colW enc2 = encode_im2col_w();
+  if (!fn || !enc2) return false;
+  {
+    const cuuint64_t dims[4] = {(cuuint64_t)cin, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)batch};
+    const cuuint64_t strides[3] = {(cuuint64_t)cin * 2, (cuuint64_t)w * cin * 2, (cuuint64_t)h * w * cin * 2};
+    const int lower[2] = {0, 0};
+    const int upper[2] = {-(kw - 1), -(kh - 1)};  // walk origins: the output pixels
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    if (enc2(&maps.xi[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(src), dims, strides, lower,
+             upper, (cuuint32_t)tcw::KB, 128, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)cin, (cuuint64_t)taps, (cuuint64_t)cout};
+    const cuuint64_t strides[2] = {(cuuint64_t)cin * 2, (cuuint64_t)taps * cin * 2};
+    const cuuint32_t box[3] = {(cuuint32_t)tcw::KB, 1, (cuuint32_t)(p.NT / 2)};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (fn(&maps.w[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(kt), dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+  }
+  maps.x = maps.xi[0];
+  for (int q = 1; q < 4; ++q) {
+    maps.w[q] = maps.w[0];
+    maps.xi[q] = maps.xi[0];
+  }
+  return true;
+}
+
+bool tc_conv_valid_supported(int batch, int h, int w, int cin, int kh, int kw, int cout) {
+  const int taps = kh * kw;
+  return cin % tcw::KB == 0 && cout >= 64 && cout % 8 == 0 && taps <= tcw::MAX_TAPS_Q && h - kh + 1 >= 1 &&
+         w - kw + 1 >= 1 && batch >= 1 && kh <= 128 && kw <= 128;
+}
+
 bool tc_bwd_data_supported(const BackwardProblem& pr) {
   tcw::Params p;
   tcw::Maps m;
@@ -1266,6 +1353,19 @@ cudaError_t launch_tc_bwd_data(const BackwardProblem& pr, cudaStream_t s) {
   if (!make_wide_dgrad(pr, p, maps)) return cudaErrorNotSupported;
   if (p.units == 0) return cudaSuccess;
   p.trace = nullptr;
+  return launch_wide_t<__nv_bfloat16, 0>(p, maps, s);
+}
+
+cudaError_t launch_tc_conv_valid(const void* src, int batch, int h, int w, int cin, const void* kt, int kh,
+                                 int kw, int cout, const float* bias, unsigned epi, void* y, cudaStream_t s) {
+  tcw::Params p;
+  tcw::Maps maps;
+  if (!make_wide_conv(src, batch, h, w, cin, kt, kh, kw, cout, bias, epi, y, p, maps))
+    return cudaErrorNotSupported;
+  p.trace = nullptr;
+  const int act = (epi & SEGCONV_EPI_RELU) ? 1 : (epi & SEGCONV_EPI_TANH) ? 2 : 0;
+  if (act == 1) return launch_wide_t<__nv_bfloat16, 1>(p, maps, s);
+  if (act == 2) return launch_wide_t<__nv_bfloat16, 2>(p, maps, s);
   return launch_wide_t<__nv_bfloat16, 0>(p, maps, s);
 }
 

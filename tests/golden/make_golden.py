@@ -23,6 +23,8 @@ Fixtures (all small):
                      rectangular kernels, batches, integer and double cases
                      (`python tests/golden/make_golden.py backward` rewrites
                      only this file)
+  conv_valid.npz     conv2d_valid (reference_ops.hpp:86-102) on rectangular
+                     maps and kernels (`python tests/golden/make_golden.py conv`)
   sgc/*.sgc          SGC1 tensor files written by the reference's save_tensor
                      (tensor_io.hpp:93-103) + sgc/values.npz with their contents
                      (`python tests/golden/make_golden.py sgc`)
@@ -152,6 +154,7 @@ def main():
                         fused=oracle.ref_tconv_fused(x, k, 2), naive=oracle.ref_tconv_naive(x, k, 2))
     backward()
     sgc()
+    conv()
     print("golden fixtures written to", OUT)
 
 
@@ -185,6 +188,20 @@ def backward():
     np.savez_compressed(os.path.join(OUT, "backward.npz"), **out)
 
 
+def conv():
+    rng = np.random.default_rng(86102)
+    out = {}
+    specs = [(1, 5, 5, 1, 3, 3, 1), (2, 7, 9, 3, 3, 2, 4), (3, 6, 4, 8, 2, 3, 5), (1, 9, 9, 16, 5, 5, 7),
+             (2, 4, 6, 2, 4, 1, 3), (1, 12, 10, 64, 3, 3, 32)]
+    for i, (b, h, w, cin, kh, kw, cout) in enumerate(specs):
+        s = rng.uniform(-1, 1, (b, h, w, cin)).astype(np.float32)
+        k = rng.uniform(-1, 1, (kh, kw, cin, cout)).astype(np.float32)
+        out[f"c{i}_src"], out[f"c{i}_k"] = s, k
+        out[f"c{i}_y"] = oracle.ref_conv2d_valid(s, k)
+    out["count"] = np.int32(len(specs))
+    np.savez_compressed(os.path.join(OUT, "conv_valid.npz"), **out)
+
+
 def sgc():
     d = os.path.join(OUT, "sgc")
     os.makedirs(d, exist_ok=True)
@@ -205,5 +222,7 @@ if __name__ == "__main__":
         backward()
     elif sys.argv[1:] == ["sgc"]:
         sgc()
+    elif sys.argv[1:] == ["conv"]:
+        conv()
     else:
         main()

@@ -238,3 +238,10 @@ def test_backward_reference_live():
         np.testing.assert_array_equal(gx, r[0])
         np.testing.assert_allclose(gk, r[1], rtol=0, atol=1e-5)
         assert secs >= 0
+
+
+def test_conv2d_valid_bit_exact_vs_reference_goldens():
+    """oracle.conv2d_valid == reference conv2d_valid (reference_ops.hpp:86-102)."""
+    z = _npz("conv_valid.npz")
+    for i in range(int(z["count"])):
+        np.testing.assert_array_equal(oracle.conv2d_valid(z[f"c{i}_src"], z[f"c{i}_k"]), z[f"c{i}_y"])
