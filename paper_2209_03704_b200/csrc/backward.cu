@@ -23,6 +23,7 @@
 // The tensor-core input gradient (bf16) is tc_wide.cu's CTA-pair kernel run on
 // a stride-2 im2col walk over gy (launch_tc_bwd_data there).
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -544,9 +545,11 @@ static cudaError_t bwd_weight_t(const BackwardProblem& pr, bool exact, cudaStrea
   const int taps = pr.kh * pr.kw;
   const int ntile = packed ? (taps * pr.cout + bwd::BN - 1) / bwd::BN : (pr.cout + bwd::BN - 1) / bwd::BN;
   const int tiles = ((pr.cin + bwd::BM - 1) / bwd::BM) * ntile * (packed ? 1 : taps);
-  // split the pixel reduction until ~2 CTAs per SM, keeping >= 512 pixels per split
-  long long splits = std::max(1LL, (2LL * sm_count() + tiles - 1) / tiles);
-  splits = std::min(splits, std::max(1LL, M / 512));
+  // split the pixel reduction until ~CPS CTAs per SM (latency hiding for the
+  // gathers), keeping >= 256 pixels per split
+  static const int cps = getenv("SEGCONV_WGRAD_CPS") ? std::max(1, atoi(getenv("SEGCONV_WGRAD_CPS"))) : 4;
+  long long splits = std::max(1LL, ((long long)cps * sm_count() + tiles - 1) / tiles);
+  splits = std::min(splits, std::max(1LL, M / 256));
   if (M == 0) splits = 1;
   long long chunk = (M + splits - 1) / splits;
   chunk = std::max<long long>(bwd::BK, (chunk + bwd::BK - 1) / bwd::BK * bwd::BK);
