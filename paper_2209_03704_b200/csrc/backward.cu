@@ -481,7 +481,37 @@ __global__ void wgrad_reduce4(const float4* __restrict__ ws, float4* __restrict_
   gk[e] = s;
 }
 
+// stream-K pieces: element idx of gk belongs to tile T = ((t * ch_pairs + ch / 256)
+// * n_tiles + f / NT); its pieces are the pairs overlapping [T*chunks, (T+1)*chunks)
+// in slot order 0, 1, ... (deterministic)
+__global__ void wgrad_reduce_streamk(const float* __restrict__ ws, float* __restrict__ gk, int cin, int cout,
+                                     int taps, int nt_feat, long long chunks, long long share, int accumulate) {
+  const long long ksz = (long long)taps * cin * cout;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ksz) return;
+  const int f = (int)(e % cout);
+  const int ch = (int)((e / cout) % cin);
+  const int t = (int)(e / ((long long)cout * cin));
+  const int ch_pairs = (cin + 255) / 256, n_tiles = cout / nt_feat;
+  const long long T = ((long long)t * ch_pairs + ch / 256) * n_tiles + f / nt_feat;
+  const long long ts = T * chunks;
+  const int pieces = (int)((ts + chunks - 1) / share - ts / share) + 1;
+  float s = accumulate ? gk[e] : 0.f;
+  for (int i = 0; i < pieces; ++i) s += __ldcs(ws + (long long)i * ksz + e);
+  gk[e] = s;
+}
+
 }  // namespace bwd
+
+cudaError_t launch_wgrad_reduce_streamk(const float* ws, float* gk, int cin, int cout, int taps, int nt_feat,
+                                        long long chunks, long long share, int accumulate, cudaStream_t s) {
+  const long long ksz = (long long)taps * cin * cout;
+  bwd::wgrad_reduce_streamk<<<(unsigned)((ksz + 255) / 256), 256, 0, s>>>(ws, gk, cin, cout, taps, nt_feat, chunks,
+                                                                          share, accumulate);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) note_launch();
+  return e;
+}
 
 static int sm_count() {
   static int sms = 0;

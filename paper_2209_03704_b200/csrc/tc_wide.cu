@@ -92,6 +92,10 @@ struct Params {
   int mode;
   int w_kw, w_taps, w_ch_pairs, w_splits, w_cin, w_cout, w_direct, w_accumulate;
   long long w_chunks, w_cps, w_ksz;
+  // stream-K schedule (w_share > 0): pair P takes chunk-units [P * share, (P+1) * share)
+  // of the (tile, chunk) space, cutting tiles into pieces; piece i of a tile goes
+  // to slot i of the workspace (launch_wgrad_reduce_streamk sums them in order)
+  long long w_share;
   float* wout;
   unsigned long long* trace;
   int debug;
@@ -216,6 +220,36 @@ __device__ __forceinline__ bool wunit_of(const Params& p, int k, int& s, int& t,
   return true;
 }
 
+// WGRAD segment k of this pair: tile (t, ct, nt), chunk range [c0, c1), output slot
+__device__ __forceinline__ bool wseg_of(const Params& p, int k, int& t, int& ct, int& nt, long long& c0,
+                                        long long& c1, int& slot) {
+  long long tile;
+  if (p.w_share > 0) {
+    const long long pair = blockIdx.x / 2;
+    const long long total = p.units * p.w_chunks;
+    const long long g0 = pair * p.w_share, g1 = min(total, g0 + p.w_share);
+    tile = g0 / p.w_chunks + k;
+    const long long ts = tile * p.w_chunks;
+    const long long s0 = max(g0, ts), s1 = min(g1, ts + p.w_chunks);
+    if (s0 >= s1) return false;
+    c0 = s0 - ts;
+    c1 = s1 - ts;
+    slot = (int)(pair - ts / p.w_share);
+  } else {
+    int s;
+    if (!wunit_of(p, k, s, t, ct, nt)) return false;
+    c0 = (long long)s * p.w_cps;
+    c1 = min(p.w_chunks, c0 + p.w_cps);
+    slot = p.w_direct ? 0 : s;
+    return true;
+  }
+  nt = (int)(tile % p.n_tiles);
+  tile /= p.n_tiles;
+  ct = (int)(tile % p.w_ch_pairs);
+  t = (int)(tile / p.w_ch_pairs);
+  return true;
+}
+
 __device__ __forceinline__ void trace_ev(const Params& p, int ev, int local) {
   if (p.trace == nullptr || blockIdx.x >= 160 || local >= 64) return;
   unsigned long long t;
@@ -314,20 +348,20 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       griddep_wait();
       int sa = 0, sb = 0;
       uint32_t pa = 0, pb = 0;
-      int s, t, ct, nt;
+      int t, ct, nt, slot;
+      long long cb, ce;
       const int img = p.n * p.n;
       const int di = 64 / p.n, dj = 64 - (64 / p.n) * p.n;  // a chunk = di rows + dj pixels
-      for (int k = 0; wunit_of(p, k, s, t, ct, nt); ++k) {
+      for (int k = 0; wseg_of(p, k, t, ct, nt, cb, ce, slot); ++k) {
         const int ch0 = ct * 256 + (int)rank * 128, f0 = nt * p.NT + (int)rank * NT2;
-        const long long c1 = min(p.w_chunks, (long long)(s + 1) * p.w_cps);
-        // first anchor of the unit's first chunk; then advanced by 64 pixels per
+        // first anchor of the segment's first chunk; then advanced by 64 pixels per
         // chunk without divisions (the single producer lane is on the critical path)
-        const long long mfirst = (long long)s * p.w_cps * 64;
+        const long long mfirst = cb * 64;
         int b0 = (int)(mfirst / img);
         int i0 = (int)(mfirst - (long long)b0 * img);
         int j0 = i0 % p.n;
         i0 /= p.n;
-        for (long long c = (long long)s * p.w_cps; c < c1; ++c) {
+        for (long long c = cb; c < ce; ++c) {
           const long long m = c * 64;
           mbar_wait(&a_empty[sa], pa ^ 1);
           const uint32_t af = mapa(smem_u32(&a_full[sa]), 0);
@@ -451,13 +485,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base, 0);
       int sa = 0, sb = 0, acc = 0;
       uint32_t pa = 0, pb = 0, pacc = 0;
-      int s, t, ct, nt;
+      int t, ct, nt, slot;
+      long long c0, c1;
       const uint32_t idesc = idesc_bf16_m256_mn(p.NT);
-      for (int k = 0; wunit_of(p, k, s, t, ct, nt); ++k) {
+      for (int k = 0; wseg_of(p, k, t, ct, nt, c0, c1, slot); ++k) {
         mbar_wait(&acc_empty[acc], pacc ^ 1);
         tc_fence_after();
         const uint32_t d = tb + (uint32_t)(acc * p.NT);
-        const long long c0 = (long long)s * p.w_cps, c1 = min(p.w_chunks, c0 + p.w_cps);
         for (long long c = c0; c < c1; ++c) {
           mbar_wait(&a_full[sa], pa);
           mbar_wait(&b_full[sb], pb);
@@ -579,13 +613,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t acc_empty_leader0 = mapa(smem_u32(&acc_empty[0]), 0);
     int acc = 0;
     uint32_t pacc = 0;
-    int s, t, ct, nt;
-    for (int k = 0; wunit_of(p, k, s, t, ct, nt); ++k) {
+    int t, ct, nt, slot;
+    long long c0, c1;
+    for (int k = 0; wseg_of(p, k, t, ct, nt, c0, c1, slot); ++k) {
       mbar_wait(&acc_full[acc], pacc);
       tc_fence_after();
       const int ch = ct * 256 + (int)rank * 128 + warp * 32 + lane;
       const bool ok = ch < p.w_cin;
-      float* dst = p.wout + (p.w_direct ? 0LL : (long long)s * p.w_ksz) +
+      float* dst = p.wout + (long long)slot * p.w_ksz +
                    ((long long)t * p.w_cin + (ok ? ch : 0)) * p.w_cout + nt * p.NT;
 #pragma unroll 1
       for (int c0 = 0; c0 < p.NT; c0 += 32) {
@@ -1111,6 +1146,25 @@ static bool make_wide_wgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
   p.w_splits = (int)((p.w_chunks + p.w_cps - 1) / p.w_cps);
   p.w_direct = p.w_splits == 1;
   p.units = base * p.w_splits;
+  // stream-K alternative: every pair the same number of chunk-units; a tile is
+  // cut into at most ceil(chunks / share) + 1 pieces
+  {
+    const long long share = (base * p.w_chunks + pairs - 1) / pairs;
+    const int maxp = (int)((p.w_chunks + share - 1) / share) + 1;
+    const double t_sk = (double)share * t_chunk + maxp * t_split + 3.0;
+    const char* e = getenv("SEGCONV_WGRAD_STREAMK");
+    // measured (B200): the pieces' extra reduction and the busier L2 with every
+    // pair active make it slower than the pixel splits on C3 / C5 (152 vs 144 us
+    // on C3), so it is opt-in (SEGCONV_WGRAD_STREAMK=1)
+    (void)t_sk;
+    const bool want = e && *e && atoi(e) != 0;
+    if (want && share >= 8) {
+      p.w_share = share;
+      p.w_splits = maxp;  // workspace slots
+      p.w_direct = 0;
+      p.units = base;  // tiles
+    }
+  }
   p.a_stage_bytes = 2 * 64 * 128;
   p.b_stage_bytes = (p.NT / 2) * 128;
   const int bar_bytes = (2 * tcw::MAX_STAGES_A + 2 * tcw::MAX_STAGES_B + 4) * 8 + 16;
@@ -1286,7 +1340,9 @@ static cudaError_t launch_wide_t(const tcw::Params& prm, const tcw::Maps& maps, 
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
       sms = 148;
   }
-  const long long pairs = std::min<long long>(prm.units, sms / 2);
+  long long pairs = std::min<long long>(prm.units, sms / 2);
+  if (prm.mode == 1 && prm.w_share > 0)  // stream-K: every pair with a share of chunk-units
+    pairs = (prm.units * prm.w_chunks + prm.w_share - 1) / prm.w_share;
   const size_t smem = (size_t)prm.stages_a * prm.a_stage_bytes + (size_t)prm.stages_b * prm.b_stage_bytes +
                       (2 * tcw::MAX_STAGES_A + 2 * tcw::MAX_STAGES_B + 4) * 8 + 16;
   cudaLaunchConfig_t cfg = {};
@@ -1342,7 +1398,13 @@ cudaError_t launch_tc_bwd_weight(const BackwardProblem& pr, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   p.wout = ws;
   e = launch_wide_t<float, 0>(p, maps, s);
-  if (e == cudaSuccess) e = launch_wgrad_reduce(ws, (float*)pr.gk, p.w_ksz, p.w_splits, pr.accumulate, s);
+  if (e == cudaSuccess) {
+    if (p.w_share > 0)
+      e = launch_wgrad_reduce_streamk(ws, (float*)pr.gk, pr.cin, pr.cout, p.w_taps, p.NT, p.w_chunks,
+                                      p.w_share, pr.accumulate, s);
+    else
+      e = launch_wgrad_reduce(ws, (float*)pr.gk, p.w_ksz, p.w_splits, pr.accumulate, s);
+  }
   cudaError_t e2 = cudaFreeAsync(ws, s);
   return e != cudaSuccess ? e : e2;
 }
