@@ -241,6 +241,17 @@ segconv_status segconv_conv2d_valid(const void* d_src, segconv_dtype dtype, int 
                                     int w, int cin, const void* d_kernel, int kh, int kw,
                                     int cout, const float* d_bias, unsigned epilogue, void* d_y,
                                     void* stream);
+/* reference netdemo/layers.hpp:98-122 (net::ConvValid<T>::backward), batched:
+ * gradients of conv2d_valid.  d_src (batch, h, w, cin) is the forward input,
+ * d_gy (batch, h-kh+1, w-kw+1, cout) the output gradient, d_kernel (kh, kw,
+ * cin, cout); d_gx (batch, h, w, cin) of dtype, d_gk (kh, kw, cin, cout) F32 (F64
+ * for F64 data) summed over the batch, `accumulate` as in
+ * segconv_transpose_conv_fused_backward.  math: EXACT (bit-identical to the
+ * reference layer), FFMA, BF16 (tcgen05 pair kernel, stride-1 walks), AUTO. */
+segconv_status segconv_conv2d_valid_backward(const void* d_src, const void* d_gy, segconv_dtype dtype,
+                                             int batch, int h, int w, int cin, const void* d_kernel,
+                                             int kh, int kw, int cout, segconv_math math, void* d_gx,
+                                             void* d_gk, int accumulate, void* stream);
 /* Bytes of workspace segconv_transpose_conv_naive needs (the upsampled map). */
 size_t segconv_naive_workspace_bytes(segconv_dtype dtype, int batch, int n_in, int cin,
                                      int p_orig);

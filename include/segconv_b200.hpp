@@ -351,6 +351,43 @@ struct ParamBlock {
   std::size_t size = 0;
 };
 
+// reference netdemo/layers.hpp:84-137 (net::ConvValid<T>): conv2d_valid forward,
+// backward on the GPU (segconv_conv2d_valid_backward), host-side values/grads.
+template <typename T>
+class ConvValid {
+ public:
+  explicit ConvValid(Kernel<T> k, segconv_math math = SEGCONV_MATH_EXACT)
+      : kernel_(std::move(k)), grad_(kernel_.kh(), kernel_.kw(), kernel_.cin(), kernel_.cout()), math_(math) {}
+  const char* name() const { return "conv_valid"; }
+  Tensor<T> forward(const Tensor<T>& in) {
+    input_ = in;
+    has_input_ = true;
+    return conv2d_valid(in, kernel_);
+  }
+  Tensor<T> backward(const Tensor<T>& g) {
+    if (!has_input_) throw StateError(std::string(name()) + ": backward called before forward");
+    Tensor<T> gin(input_.height(), input_.width(), input_.channels());
+    DeviceBuffer dx(input_.data(), input_.size() * sizeof(T)), dg(g.data(), g.size() * sizeof(T));
+    DeviceBuffer dk(kernel_.data(), kernel_.size() * sizeof(T));
+    DeviceBuffer dgk(grad_.data(), grad_.size() * sizeof(T)), dgx(gin.size() * sizeof(T));
+    throw_on(segconv_conv2d_valid_backward(dx.get(), dg.get(), dtype_of<T>::value, 1, input_.height(),
+                                           input_.width(), input_.channels(), dk.get(), kernel_.kh(),
+                                           kernel_.kw(), kernel_.cout(), math_, dgx.get(), dgk.get(), 1, nullptr));
+    dgx.to_host(gin.data(), gin.size() * sizeof(T));
+    dgk.to_host(grad_.data(), grad_.size() * sizeof(T));
+    return gin;
+  }
+  std::vector<ParamBlock<T>> params() { return {{kernel_.data(), grad_.data(), kernel_.size()}}; }
+  const Kernel<T>& kernel() const { return kernel_; }
+
+ private:
+  Kernel<T> kernel_;
+  Kernel<T> grad_;
+  segconv_math math_;
+  Tensor<T> input_;
+  bool has_input_ = false;
+};
+
 // reference netdemo/layers.hpp:150-230 (net::FusedTConv<T>): forward runs the
 // segregated GPU kernels, backward the GPU backward pass
 // (segconv_transpose_conv_fused_backward); values and gradients live on the

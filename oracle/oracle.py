@@ -19,6 +19,7 @@ __all__ = [
     "ref_count_ops", "ref_time_fused_batch", "OracleError", "bf16_round", "tf32_round",
     "tconv_backward", "scatter_backward_f64", "ref_tconv_backward", "ref_time_backward",
     "ref_save_tensor", "ref_load_tensor", "conv2d_valid", "ref_conv2d_valid",
+    "conv2d_valid_backward", "ref_conv2d_valid_backward",
 ]
 
 
@@ -66,6 +67,8 @@ def load_oracle():
         lib.orc_scatter_backward_f64.argtypes = lib.orc_tconv_backward_f64.argtypes
         for name, T in (("f32", C.c_float), ("f64", C.c_double)):
             pt = C.POINTER(T)
+            getattr(lib, f"orc_conv2d_valid_backward_{name}").argtypes = [pt] + [C.c_int] * 4 + \
+                [pt] + [C.c_int] * 3 + [pt, pt, pt]
             getattr(lib, f"orc_conv2d_valid_{name}").argtypes = [pt] + [C.c_int] * 4 + [pt] + \
                 [C.c_int] * 3 + [pt]
         lib.orc_subkernel_dims.argtypes = [C.c_int, C.c_int, C.c_int, ip, ip]
@@ -100,6 +103,9 @@ def load_ref():
             fp, C.c_int, C.c_int, C.c_int, fp, C.c_int, C.c_int, C.c_int, C.c_int, fp, C.c_int,
             fp, fp, dp]
         lib.ref_conv2d_valid_f32.argtypes = [fp] + [C.c_int] * 4 + [fp] + [C.c_int] * 3 + [fp]
+        for nm, T in (("f32", fp), ("f64", dp)):
+            getattr(lib, f"ref_conv2d_valid_backward_{nm}").argtypes = [T] + [C.c_int] * 4 + [T] + \
+                [C.c_int] * 3 + [T, T, T]
         lib.ref_save_tensor.argtypes = [C.c_char_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
         lib.ref_load_tensor.argtypes = [C.c_char_p, C.c_int, C.c_void_p, C.c_size_t, ip]
         lib.ref_last_error_offset.restype = C.c_size_t
@@ -273,6 +279,34 @@ def _conv_valid(lib, prefix, src, k):
     fn = getattr(lib, f"{prefix}_conv2d_valid_{'f64' if f64 else 'f32'}")
     _check(fn(_ptr(src, T), b, h, w, cin, _ptr(k, T), kh, kw, cout, _ptr(out, T)), lib)
     return out[0] if squeeze else out
+
+
+def _conv_backward(lib, prefix, src, k, gy):
+    src = np.asarray(src)
+    f64 = src.dtype == np.float64
+    cast = _f64 if f64 else _f32
+    src, k, gy = cast(src), cast(k), cast(gy)
+    squeeze = src.ndim == 3
+    if squeeze:
+        src, gy = src[None], gy[None]
+    b, h, w, cin = src.shape
+    kh, kw, _, cout = k.shape
+    if gy.shape != (b, h - kh + 1, w - kw + 1, cout):
+        raise OracleError(2, f"output gradient shape {gy.shape}")
+    gx, gk = np.empty_like(src), np.empty_like(k)
+    T = C.c_double if f64 else C.c_float
+    fn = getattr(lib, f"{prefix}_conv2d_valid_backward_{'f64' if f64 else 'f32'}")
+    _check(fn(_ptr(src, T), b, h, w, cin, _ptr(k, T), kh, kw, cout, _ptr(gy, T), _ptr(gx, T), _ptr(gk, T)), lib)
+    return (gx[0] if squeeze else gx), gk
+
+
+def conv2d_valid_backward(src, k, gy):
+    """(input grad, kernel grad) of conv2d_valid, reference order (layers.hpp:98-122)."""
+    return _conv_backward(load_oracle(), "orc", src, k, gy)
+
+
+def ref_conv2d_valid_backward(src, k, gy):
+    return _conv_backward(load_ref(), "ref", src, k, gy)
 
 
 def conv2d_valid(src, k):

@@ -117,6 +117,25 @@ int run_backward(const T* x, int batch, int n, int cin, const T* k, int kh, int 
   });
 }
 
+// net::ConvValid forward + backward per image (layers.hpp:84-122), grads zeroed once
+template <typename T>
+int run_conv_backward(const T* src, int batch, int h, int w, int cin, const T* k, int kh, int kw, int cout,
+                      const T* gy, T* gx, T* gk) {
+  return guarded([&] {
+    segconv::net::ConvValid<T> layer(kernel(k, kh, kw, cin, cout));
+    for (auto& blk : layer.params()) std::fill(blk.grads, blk.grads + blk.size, T(0));
+    const int oh = h - kh + 1, ow = w - kw + 1;
+    const size_t isz = (size_t)h * w * cin, osz = (size_t)oh * ow * cout;
+    for (int b = 0; b < batch; ++b) {
+      layer.forward(segconv::Tensor<T>::from_data(h, w, cin, std::vector<T>(src + b * isz, src + (b + 1) * isz)));
+      const auto gi = layer.backward(
+          segconv::Tensor<T>::from_data(oh, ow, cout, std::vector<T>(gy + b * osz, gy + (b + 1) * osz)));
+      std::memcpy(gx + b * isz, gi.data(), isz * sizeof(T));
+    }
+    const auto blk = layer.params()[0];
+    std::memcpy(gk, blk.grads, blk.size * sizeof(T));
+  });
+}
 }  // namespace
 
 extern "C" {
@@ -330,6 +349,15 @@ int ref_conv2d_valid_f32(const float* src, int batch, int h, int w, int cin, con
       std::memcpy(out + b * osz, y.data(), osz * sizeof(float));
     }
   });
+}
+
+int ref_conv2d_valid_backward_f32(const float* src, int batch, int h, int w, int cin, const float* k, int kh,
+                                  int kw, int cout, const float* gy, float* gx, float* gk) {
+  return run_conv_backward<float>(src, batch, h, w, cin, k, kh, kw, cout, gy, gx, gk);
+}
+int ref_conv2d_valid_backward_f64(const double* src, int batch, int h, int w, int cin, const double* k, int kh,
+                                  int kw, int cout, const double* gy, double* gx, double* gk) {
+  return run_conv_backward<double>(src, batch, h, w, cin, k, kh, kw, cout, gy, gx, gk);
 }
 
 int ref_tconv_backward_f32(const float* x, int batch, int n, int cin, const float* k, int kh,

@@ -74,6 +74,8 @@ SIGNATURES = {
     "segconv_last_error_offset": (_sz, []),
     "segconv_upsample2x_pad": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _vp]),
     "segconv_conv2d_valid": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _i, _vp, _u, _vp, _vp]),
+    "segconv_conv2d_valid_backward": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _vp,
+                                           _vp, _i, _vp]),
     "segconv_naive_workspace_bytes": (_sz, [_i, _i, _i, _i, _i]),
     "segconv_transpose_conv_naive": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _vp, _sz,
                                           _vp, _u, _vp, _vp]),

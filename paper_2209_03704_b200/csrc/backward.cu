@@ -152,6 +152,58 @@ __global__ void __launch_bounds__(256) wgrad_exact(const T* __restrict__ x, cons
   gk[e] = s;
 }
 
+// ------------------------------------------------- EXACT: conv2d_valid
+// reference netdemo/layers.hpp:98-122 (ConvValid::backward): contributions to
+// gin(a, c) arrive for output pixels (y, x) = (a - u, c - v) in ascending
+// order, i.e. u and v descending; acc over f ascending, no FMA.
+template <typename T>
+__global__ void __launch_bounds__(256) conv_dgrad_exact(const T* __restrict__ gy, const T* __restrict__ k,
+                                                        T* __restrict__ gx, BackwardProblem pr) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)pr.batch * pr.in_h * pr.in_w * pr.cin;
+  if (e >= total) return;
+  const int ch = (int)(e % pr.cin);
+  const long long m = e / pr.cin;
+  const int c = (int)(m % pr.in_w), a = (int)((m / pr.in_w) % pr.in_h);
+  const int b = (int)(m / ((long long)pr.in_h * pr.in_w));
+  T sum = 0;
+  for (int u = pr.kh - 1; u >= 0; --u) {
+    const int y = a - u;
+    if (y < 0 || y >= pr.out_h) continue;
+    for (int v = pr.kw - 1; v >= 0; --v) {
+      const int x = c - v;
+      if (x < 0 || x >= pr.out_w) continue;
+      const T* gp = gy + (((long long)b * pr.out_h + y) * pr.out_w + x) * pr.cout;
+      const T* w = k + (((long long)u * pr.kw + v) * pr.cin + ch) * pr.cout;
+      T acc = 0;
+      for (int f = 0; f < pr.cout; ++f) acc = add_rn(acc, mul_rn(w[f], gp[f]));
+      sum = add_rn(sum, acc);
+    }
+  }
+  gx[e] = sum;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) conv_wgrad_exact(const T* __restrict__ x, const T* __restrict__ gy,
+                                                        T* __restrict__ gk, BackwardProblem pr) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)pr.kh * pr.kw * pr.cin * pr.cout;
+  if (e >= total) return;
+  const int f = (int)(e % pr.cout);
+  const int ch = (int)((e / pr.cout) % pr.cin);
+  const int t = (int)(e / ((long long)pr.cout * pr.cin));
+  const int u = t / pr.kw, v = t - (t / pr.kw) * pr.kw;
+  T s = pr.accumulate ? gk[e] : T(0);
+  for (int b = 0; b < pr.batch; ++b)
+    for (int y = 0; y < pr.out_h; ++y)
+      for (int xx = 0; xx < pr.out_w; ++xx) {
+        const T xv = x[(((long long)b * pr.in_h + y + u) * pr.in_w + xx + v) * pr.cin + ch];
+        const T gv = gy[(((long long)b * pr.out_h + y) * pr.out_w + xx) * pr.cout + f];
+        s = add_rn(s, mul_rn(xv, gv));
+      }
+  gk[e] = s;
+}
+
 // ------------------------------------------------------------- FFMA tiles
 constexpr int BM = 64, BN = 64, BK = 16, NT = 256;
 
@@ -162,19 +214,19 @@ __global__ void __launch_bounds__(NT) dgrad_ffma(const T* __restrict__ gy, const
   __shared__ ACC As[BK][BM + 4];
   __shared__ ACC Bs[BK][BN + 4];
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const long long M = (long long)pr.batch * pr.n * pr.n;
+  const long long M = (long long)pr.batch * pr.in_h * pr.in_w;
   const long long m0 = (long long)blockIdx.x * BM;
   const int ch0 = blockIdx.y * BN;
   const int lp = tid >> 2, lf = (tid & 3) * 4;  // loader: row lp, 4 consecutive features
   const long long m = m0 + lp;
   const bool mv = m < M;
-  const int j = mv ? (int)(m % pr.n) : 0, i = mv ? (int)((m / pr.n) % pr.n) : 0;
-  const int b = mv ? (int)(m / ((long long)pr.n * pr.n)) : 0;
+  const int j = mv ? (int)(m % pr.in_w) : 0, i = mv ? (int)((m / pr.in_w) % pr.in_h) : 0;
+  const int b = mv ? (int)(m / ((long long)pr.in_h * pr.in_w)) : 0;
   const bool kv = ch0 + lp < pr.cin;
   ACC acc[4][4] = {};
   for (int t = 0; t < pr.kh * pr.kw; ++t) {
     const int U = t / pr.kw, V = t - (t / pr.kw) * pr.kw;
-    const int y = 2 * i + pr.p - U, xx = 2 * j + pr.p - V;
+    const int y = pr.stride * i + pr.p - U, xx = pr.stride * j + pr.p - V;
     const bool av = mv && y >= 0 && y < pr.out_h && xx >= 0 && xx < pr.out_w;
     const T* gp = gy + (((long long)b * pr.out_h + (av ? y : 0)) * pr.out_w + (av ? xx : 0)) * pr.cout;
     const T* kp = k + ((long long)t * pr.cin + (kv ? ch0 + lp : 0)) * pr.cout;
@@ -225,14 +277,14 @@ __global__ void __launch_bounds__(NT) dgrad_ffma_packed(const T* __restrict__ gy
   __shared__ ACC As[BK][BM + 4];
   __shared__ ACC Bs[BK][BN + 4];
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const long long M = (long long)pr.batch * pr.n * pr.n;
+  const long long M = (long long)pr.batch * pr.in_h * pr.in_w;
   const long long m0 = (long long)blockIdx.x * BM;
   const int ch0 = blockIdx.y * BN;
   const int lp = tid >> 2, lf = (tid & 3) * 4;
   const long long m = m0 + lp;
   const bool mv = m < M;
-  const int j = mv ? (int)(m % pr.n) : 0, i = mv ? (int)((m / pr.n) % pr.n) : 0;
-  const int b = mv ? (int)(m / ((long long)pr.n * pr.n)) : 0;
+  const int j = mv ? (int)(m % pr.in_w) : 0, i = mv ? (int)((m / pr.in_w) % pr.in_h) : 0;
+  const int b = mv ? (int)(m / ((long long)pr.in_h * pr.in_w)) : 0;
   const bool kv = ch0 + lp < pr.cin;
   const int K = pr.kh * pr.kw * pr.cout;
   const T* gb = gy + (long long)b * pr.out_h * pr.out_w * pr.cout;
@@ -244,7 +296,7 @@ __global__ void __launch_bounds__(NT) dgrad_ffma_packed(const T* __restrict__ gy
       ACC va = 0, vb = 0;
       if (k0 + lf + e < K) {
         const int U = t / pr.kw, V = t - (t / pr.kw) * pr.kw;
-        const int y = 2 * i + pr.p - U, xx = 2 * j + pr.p - V;
+        const int y = pr.stride * i + pr.p - U, xx = pr.stride * j + pr.p - V;
         if (mv && y >= 0 && y < pr.out_h && xx >= 0 && xx < pr.out_w)
           va = ld<ACC>(gb + ((long long)y * pr.out_w + xx) * pr.cout + f);
         if (kv) vb = ld<ACC>(k + ((long long)t * pr.cin + ch0 + lp) * pr.cout + f);
@@ -293,7 +345,7 @@ __global__ void __launch_bounds__(NT) wgrad_ffma_packed(const T* __restrict__ x,
   __shared__ ACC As[BK][BM + 4];
   __shared__ ACC Bs[BK][BN + 4];
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const long long M = (long long)pr.batch * pr.n * pr.n;
+  const long long M = (long long)pr.batch * pr.in_h * pr.in_w;
   const int NP = pr.kh * pr.kw * pr.cout;
   const int ch0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
   const int s = blockIdx.z;
@@ -312,10 +364,10 @@ __global__ void __launch_bounds__(NT) wgrad_ffma_packed(const T* __restrict__ x,
     cv[e] = t - (t / pr.kw) * pr.kw;
   }
   ACC acc[4][4] = {};
-  const int img = pr.n * pr.n, di = BK / pr.n, dj = BK - (BK / pr.n) * pr.n;
+  const int img = pr.in_h * pr.in_w, di = BK / pr.in_w, dj = BK - (BK / pr.in_w) * pr.in_w;
   const long long mf = mb + lp;
-  int b = (int)(mf / img), i = (int)(mf - (long long)b * img), j = i % pr.n;
-  i /= pr.n;
+  int b = (int)(mf / img), i = (int)(mf - (long long)b * img), j = i % pr.in_w;
+  i /= pr.in_w;
   for (long long mk = mb; mk < me; mk += BK) {
     const long long m = mk + lp;
     const bool mv = m < me;
@@ -324,21 +376,21 @@ __global__ void __launch_bounds__(NT) wgrad_ffma_packed(const T* __restrict__ x,
     const T* gb = gy + (long long)b * pr.out_h * pr.out_w * pr.cout;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int y = 2 * i + pr.p - cu[e], xx = 2 * j + pr.p - cv[e];
+      const int y = pr.stride * i + pr.p - cu[e], xx = pr.stride * j + pr.p - cv[e];
       const bool ok = mv && cok[e] && y >= 0 && y < pr.out_h && xx >= 0 && xx < pr.out_w;
       As[lp][lc + e] = va[e];
       Bs[lp][lc + e] = ok ? ld<ACC>(gb + ((long long)y * pr.out_w + xx) * pr.cout + cf[e]) : ACC(0);
     }
     j += dj;
     i += di;
-    if (j >= pr.n) {
-      j -= pr.n;
+    if (j >= pr.in_w) {
+      j -= pr.in_w;
       ++i;
     }
-    if (i >= pr.n) {
-      const int q = i / pr.n;
+    if (i >= pr.in_h) {
+      const int q = i / pr.in_h;
       b += q;
-      i -= q * pr.n;
+      i -= q * pr.in_h;
     }
     __syncthreads();
 #pragma unroll
@@ -383,7 +435,7 @@ __global__ void __launch_bounds__(NT) wgrad_ffma(const T* __restrict__ x, const 
   __shared__ ACC As[BK][BM + 4];
   __shared__ ACC Bs[BK][BN + 4];
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-  const long long M = (long long)pr.batch * pr.n * pr.n;
+  const long long M = (long long)pr.batch * pr.in_h * pr.in_w;
   const int ch0 = blockIdx.x * BM, f0 = blockIdx.y * BN;
   const int t = blockIdx.z / splits, s = blockIdx.z - (blockIdx.z / splits) * splits;
   const int U = t / pr.kw, V = t - (t / pr.kw) * pr.kw;
@@ -391,14 +443,14 @@ __global__ void __launch_bounds__(NT) wgrad_ffma(const T* __restrict__ x, const 
   const int lp = tid >> 4, lc = (tid & 15) * 4;  // loader: pixel lp, 4 consecutive channels
   ACC acc[4][4] = {};
   // this thread's pixel (b, i, j), advanced by BK pixels per step without divisions
-  const int img = pr.n * pr.n, di = BK / pr.n, dj = BK - (BK / pr.n) * pr.n;
+  const int img = pr.in_h * pr.in_w, di = BK / pr.in_w, dj = BK - (BK / pr.in_w) * pr.in_w;
   const long long m0 = mb + lp;
-  int b = (int)(m0 / img), i = (int)(m0 - (long long)b * img), j = i % pr.n;
-  i /= pr.n;
+  int b = (int)(m0 / img), i = (int)(m0 - (long long)b * img), j = i % pr.in_w;
+  i /= pr.in_w;
   for (long long mk = mb; mk < me; mk += BK) {
     const long long m = mk + lp;
     const bool mv = m < me;
-    const int y = 2 * i + pr.p - U, xx = 2 * j + pr.p - V;
+    const int y = pr.stride * i + pr.p - U, xx = pr.stride * j + pr.p - V;
     const bool gv = mv && y >= 0 && y < pr.out_h && xx >= 0 && xx < pr.out_w;
     const T* xp = x + (mv ? m : 0) * pr.cin;
     const T* gp = gy + (((long long)b * pr.out_h + (gv ? y : 0)) * pr.out_w + (gv ? xx : 0)) * pr.cout;
@@ -412,14 +464,14 @@ __global__ void __launch_bounds__(NT) wgrad_ffma(const T* __restrict__ x, const 
     }
     j += dj;
     i += di;
-    if (j >= pr.n) {
-      j -= pr.n;
+    if (j >= pr.in_w) {
+      j -= pr.in_w;
       ++i;
     }
-    if (i >= pr.n) {
-      const int q = i / pr.n;
+    if (i >= pr.in_h) {
+      const int q = i / pr.in_h;
       b += q;
-      i -= q * pr.n;
+      i -= q * pr.in_h;
     }
     __syncthreads();
 #pragma unroll
@@ -526,14 +578,18 @@ static int sm_count() {
 
 template <typename T>
 static cudaError_t bwd_data_t(const BackwardProblem& pr, bool exact, cudaStream_t s) {
-  const long long M = (long long)pr.batch * pr.n * pr.n;
+  const long long M = (long long)pr.batch * pr.in_h * pr.in_w;
   if (M == 0) return cudaSuccess;
   if (exact) {
     if constexpr (sizeof(T) == 2) return cudaErrorNotSupported;
     else {
       const long long total = M * pr.cin;
-      bwd::dgrad_exact<T><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(
-          (const T*)pr.gy, (const T*)pr.k, (T*)pr.gx, pr);
+      if (pr.conv)
+        bwd::conv_dgrad_exact<T><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(
+            (const T*)pr.gy, (const T*)pr.k, (T*)pr.gx, pr);
+      else
+        bwd::dgrad_exact<T><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(
+            (const T*)pr.gy, (const T*)pr.k, (T*)pr.gx, pr);
     }
   } else {
     using ACC = typename std::conditional<sizeof(T) == 8, double, float>::type;
@@ -559,12 +615,16 @@ template <typename T>
 static cudaError_t bwd_weight_t(const BackwardProblem& pr, bool exact, cudaStream_t s) {
   using ACC = typename std::conditional<sizeof(T) == 8, double, float>::type;
   const long long ksz = (long long)pr.kh * pr.kw * pr.cin * pr.cout;
-  const long long M = (long long)pr.batch * pr.n * pr.n;
+  const long long M = (long long)pr.batch * pr.in_h * pr.in_w;
   if (exact) {
     if constexpr (sizeof(T) == 2) return cudaErrorNotSupported;
     else {
-      bwd::wgrad_exact<T><<<(unsigned)((ksz + 255) / 256), 256, 0, s>>>((const T*)pr.x, (const T*)pr.gy,
-                                                                        (T*)pr.gk, pr);
+      if (pr.conv)
+        bwd::conv_wgrad_exact<T><<<(unsigned)((ksz + 255) / 256), 256, 0, s>>>((const T*)pr.x, (const T*)pr.gy,
+                                                                                 (T*)pr.gk, pr);
+      else
+        bwd::wgrad_exact<T><<<(unsigned)((ksz + 255) / 256), 256, 0, s>>>((const T*)pr.x, (const T*)pr.gy,
+                                                                          (T*)pr.gk, pr);
       cudaError_t e = cudaGetLastError();
       if (e == cudaSuccess) note_launch();
       return e;

@@ -469,6 +469,46 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
 }
 
 // ------------------------------------------------------------ backward
+// Shared dispatch of the two backward entry points: tensor-core pair kernel for
+// bf16 where it applies, SIMT (EXACT / FFMA) otherwise.
+static segconv_status run_backward(const BackwardProblem& pr, segconv_math math, cudaStream_t s,
+                                   const char* what) {
+  const bool exact = math == SEGCONV_MATH_EXACT;
+  segconv_status st = SEGCONV_OK;
+  const char* dpath = "";
+  char msg[160];
+  if (pr.gx) {
+    if (math == SEGCONV_MATH_BF16 && tc_bwd_data_supported(pr)) {
+      dpath = "tc-pair";
+      snprintf(msg, sizeof msg, "%s[input, tcgen05 pair]", what);
+      st = cuda_status(launch_tc_bwd_data(pr, s), msg);
+    } else {
+      dpath = exact ? "simt-exact" : "simt-ffma";
+      snprintf(msg, sizeof msg, "%s[input]", what);
+      st = cuda_status(launch_bwd_data_simt(pr, exact, s), msg);
+    }
+    if (st != SEGCONV_OK) return st;
+  }
+  const char* wpath = "-";
+  if (pr.gk) {
+    if (math == SEGCONV_MATH_BF16 && tc_bwd_weight_supported(pr)) {
+      wpath = "tc-pair";
+      snprintf(msg, sizeof msg, "%s[kernel, tcgen05 pair]", what);
+      st = cuda_status(launch_tc_bwd_weight(pr, s), msg);
+    } else {
+      wpath = exact ? "simt-exact" : "simt-ffma";
+      snprintf(msg, sizeof msg, "%s[kernel]", what);
+      st = cuda_status(launch_bwd_weight_simt(pr, exact, s), msg);
+    }
+    if (st != SEGCONV_OK) return st;
+  }
+  static thread_local char path[48];
+  snprintf(path, sizeof path, "bwd:%s+%s", pr.gx ? dpath : "-", wpath);
+  g_path = path;
+  return SEGCONV_OK;
+}
+
+
 segconv_status segconv_transpose_conv_fused_backward(const void* d_x, const void* d_gy, segconv_dtype dtype,
                                                      int batch, int n_in, int cin, const void* d_kernel,
                                                      int kh, int kw, int cout, int p_orig, segconv_math math,
@@ -509,37 +549,13 @@ segconv_status segconv_transpose_conv_fused_backward(const void* d_x, const void
   pr.pf = g.p_fused;
   pr.out_h = g.out_h;
   pr.out_w = g.out_w;
+  pr.stride = 2;
+  pr.in_h = pr.in_w = n_in;
+  pr.conv = 0;
   pr.gx = d_gx;
   pr.gk = d_gk;
   pr.accumulate = accumulate ? 1 : 0;
-  cudaStream_t s = (cudaStream_t)stream;
-  const bool exact = math == SEGCONV_MATH_EXACT;
-  const char* dpath = "";
-  if (d_gx) {
-    if (math == SEGCONV_MATH_BF16 && tc_bwd_data_supported(pr)) {
-      dpath = "tc-pair";
-      st = cuda_status(launch_tc_bwd_data(pr, s), "transpose_conv_fused_backward[input, tcgen05 pair]");
-    } else {
-      dpath = exact ? "simt-exact" : "simt-ffma";
-      st = cuda_status(launch_bwd_data_simt(pr, exact, s), "transpose_conv_fused_backward[input]");
-    }
-    if (st != SEGCONV_OK) return st;
-  }
-  const char* wpath = "-";
-  if (d_gk) {
-    if (math == SEGCONV_MATH_BF16 && tc_bwd_weight_supported(pr)) {
-      wpath = "tc-pair";
-      st = cuda_status(launch_tc_bwd_weight(pr, s), "transpose_conv_fused_backward[kernel, tcgen05 pair]");
-    } else {
-      wpath = exact ? "simt-exact" : "simt-ffma";
-      st = cuda_status(launch_bwd_weight_simt(pr, exact, s), "transpose_conv_fused_backward[kernel]");
-    }
-    if (st != SEGCONV_OK) return st;
-  }
-  static thread_local char path[48];
-  snprintf(path, sizeof path, "bwd:%s+%s", d_gx ? dpath : "-", wpath);
-  g_path = path;
-  return SEGCONV_OK;
+  return run_backward(pr, math, (cudaStream_t)stream, "transpose_conv_fused_backward");
 }
 
 // Host-buffer pipeline over batch slices (see the header).  Copy streams and
@@ -657,6 +673,55 @@ segconv_status segconv_conv2d_valid(const void* d_src, segconv_dtype dtype, int 
   return cuda_status(launch_conv2d_valid(d_src, dtype, batch, h, w, cin, d_kernel, kh, kw, cout,
                                          d_bias, epilogue, d_y, (cudaStream_t)stream),
                      "conv2d_valid");
+}
+
+// reference netdemo/layers.hpp:98-122 (net::ConvValid<T>::backward), batched
+segconv_status segconv_conv2d_valid_backward(const void* d_src, const void* d_gy, segconv_dtype dtype, int batch,
+                                             int h, int w, int cin, const void* d_kernel, int kh, int kw,
+                                             int cout, segconv_math math, void* d_gx, void* d_gk, int accumulate,
+                                             void* stream) {
+  if (kh < 1 || kw < 1) return fail(SEGCONV_E_SHAPE, "conv2d_valid needs a non-empty kernel");
+  if (h < 1 || w < 1 || cin < 1 || cout < 1) return fail(SEGCONV_E_SHAPE, "tensor dims must be positive");
+  if (h - kh + 1 < 1 || w - kw + 1 < 1)
+    return fail(SEGCONV_E_SHAPE, "kernel %dx%d does not fit input %dx%d", kh, kw, h, w);
+  if (batch < 0) return fail(SEGCONV_E_CONTRACT, "batch must be >= 0, got %d", batch);
+  if (!valid_dtype(dtype)) return fail(SEGCONV_E_CONTRACT, "unknown dtype %d", (int)dtype);
+  if (!d_gx && !d_gk) return fail(SEGCONV_E_CONTRACT, "neither an input nor a kernel gradient was requested");
+  if (batch > 0) {
+    if (!d_gy) return fail(SEGCONV_E_CONTRACT, "null output gradient");
+    if (d_gx && !d_kernel) return fail(SEGCONV_E_CONTRACT, "the input gradient needs the kernel");
+    if (d_gk && !d_src) return fail(SEGCONV_E_CONTRACT, "the kernel gradient needs the forward input");
+  }
+  if (math == SEGCONV_MATH_AUTO) math = dtype == SEGCONV_BF16 ? SEGCONV_MATH_BF16 : SEGCONV_MATH_FFMA;
+  if (math == SEGCONV_MATH_EXACT && dtype == SEGCONV_BF16)
+    return fail(SEGCONV_E_CONTRACT, "EXACT math is defined for float and double (the reference's types)");
+  if (math == SEGCONV_MATH_BF16 && dtype != SEGCONV_BF16)
+    return fail(SEGCONV_E_CONTRACT, "BF16 math needs bf16 tensors");
+  if (math != SEGCONV_MATH_EXACT && math != SEGCONV_MATH_FFMA && math != SEGCONV_MATH_BF16)
+    return fail(SEGCONV_E_UNSUPPORTED, "math mode %d has no backward kernels in this build", (int)math);
+  BackwardProblem pr{};
+  pr.x = d_src;
+  pr.gy = d_gy;
+  pr.k = d_kernel;
+  pr.dtype = dtype;
+  pr.batch = batch;
+  pr.n = h;
+  pr.cin = cin;
+  pr.cout = cout;
+  pr.kh = kh;
+  pr.kw = kw;
+  pr.p = 0;
+  pr.pf = 0;
+  pr.out_h = h - kh + 1;
+  pr.out_w = w - kw + 1;
+  pr.stride = 1;
+  pr.in_h = h;
+  pr.in_w = w;
+  pr.conv = 1;
+  pr.gx = d_gx;
+  pr.gk = d_gk;
+  pr.accumulate = accumulate ? 1 : 0;
+  return run_backward(pr, math, (cudaStream_t)stream, "conv2d_valid_backward");
 }
 
 // reference reference_ops.hpp:116-133

@@ -40,6 +40,10 @@ struct BackwardProblem {
   const void* k;  // original (kh, kw, cin, cout) kernel
   int dtype;
   int batch, n, cin, cout, kh, kw, p, pf, out_h, out_w;
+  // gy position of input pixel (i, j) under tap (U, V): (stride*i + p - U, stride*j + p - V).
+  // Transpose conv: stride 2, in_h = in_w = n.  conv2d_valid (conv = 1): stride 1,
+  // p = 0, input in_h x in_w, gy (in_h - kh + 1) x (in_w - kw + 1).
+  int stride, in_h, in_w, conv;
   void* gx;
   void* gk;
   int accumulate;  // gk += (the reference accumulates tap gradients across calls)

@@ -91,6 +91,7 @@ struct Params {
   // stride-2 im2col walk over gy.  Results go to wout (+ s * ksz when split).
   int mode;
   int w_kw, w_taps, w_ch_pairs, w_splits, w_cin, w_cout, w_direct, w_accumulate;
+  int w_in_h, w_in_w;  // input map (anchor grid) of the kernel-gradient walk
   long long w_chunks, w_cps, w_ksz;
   // stream-K schedule (w_share > 0): pair P takes chunk-units [P * share, (P+1) * share)
   // of the (tile, chunk) space, cutting tiles into pieces; piece i of a tile goes
@@ -350,8 +351,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t pa = 0, pb = 0;
       int t, ct, nt, slot;
       long long cb, ce;
-      const int img = p.n * p.n;
-      const int di = 64 / p.n, dj = 64 - (64 / p.n) * p.n;  // a chunk = di rows + dj pixels
+      const int img = p.w_in_h * p.w_in_w;
+      const int di = 64 / p.w_in_w, dj = 64 - (64 / p.w_in_w) * p.w_in_w;  // a chunk = di rows + dj pixels
       for (int k = 0; wseg_of(p, k, t, ct, nt, cb, ce, slot); ++k) {
         const int ch0 = ct * 256 + (int)rank * 128, f0 = nt * p.NT + (int)rank * NT2;
         // first anchor of the segment's first chunk; then advanced by 64 pixels per
@@ -359,8 +360,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const long long mfirst = cb * 64;
         int b0 = (int)(mfirst / img);
         int i0 = (int)(mfirst - (long long)b0 * img);
-        int j0 = i0 % p.n;
-        i0 /= p.n;
+        int j0 = i0 % p.w_in_w;
+        i0 /= p.w_in_w;
         for (long long c = cb; c < ce; ++c) {
           const long long m = c * 64;
           mbar_wait(&a_empty[sa], pa ^ 1);
@@ -378,7 +379,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (rank == 0) mbar_arrive_expect_tx(&b_full[sb], 2 * (uint32_t)NT2 * 128);
           const uint32_t bd = smem_u32(b_base + (size_t)sb * p.b_stage_bytes);
           for (int h = 0; h < NT2 / 64; ++h)
-            tma2_load_im2col(bd + h * 8192, &maps.xi[0], f0 + 64 * h, 2 * j0 + p.wbase_c, 2 * i0 + p.wbase_r,
+            tma2_load_im2col(bd + h * 8192, &maps.xi[0], f0 + 64 * h, p.wscale * j0 + p.wbase_c,
+                             p.wscale * i0 + p.wbase_r,
                              b0, (uint16_t)p.tap_off_c[0][t], (uint16_t)p.tap_off_r[0][t], bf);
           if (++sb == SB) {
             sb = 0;
@@ -386,14 +388,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
           j0 += dj;
           i0 += di;
-          if (j0 >= p.n) {
-            j0 -= p.n;
+          if (j0 >= p.w_in_w) {
+            j0 -= p.w_in_w;
             ++i0;
           }
-          if (i0 >= p.n) {
-            const int q = i0 / p.n;
+          if (i0 >= p.w_in_h) {
+            const int q = i0 / p.w_in_h;
             b0 += q;
-            i0 -= q * p.n;
+            i0 -= q * p.w_in_h;
           }
         }
       }
@@ -998,17 +1000,24 @@ static bool make_wide_dgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
   if (pr.cout % tcw::KB != 0 || pr.cin < 64 || pr.cin % 8 != 0) return false;
   const int taps = pr.kh * pr.kw;
   if (taps > tcw::MAX_TAPS_Q) return false;
+  // walk origin of input pixel (i, j): (stride*i + lo_r, stride*j + lo_c); the
+  // corners bound the walk: [lo, stride*(in-1) + lo] in gy coordinates
   const int lo_r = pr.p - pr.kh + 1, lo_c = pr.p - pr.kw + 1;
-  if (lo_r < -128 || lo_c < -128 || pr.p > 128) return false;  // rank-4 im2col corner range
-  if ((long long)pr.batch * pr.n * pr.n * pr.cin >= (1LL << 40)) return false;
+  const int up_r = pr.stride * (pr.in_h - 1) + lo_r - (pr.out_h - 1);
+  const int up_c = pr.stride * (pr.in_w - 1) + lo_c - (pr.out_w - 1);
+  if (lo_r < -128 || lo_c < -128 || up_r < -128 || up_c < -128 || up_r > 127 || up_c > 127 || lo_r > 127 ||
+      lo_c > 127)
+    return false;  // rank-4 im2col corner range
+  if ((long long)pr.batch * pr.in_h * pr.in_w * pr.cin >= (1LL << 40)) return false;
   p.y = pr.gx;
   p.y_dtype = SEGCONV_BF16;
   p.batch = pr.batch;
-  p.n = pr.n;
+  p.n = pr.in_h;
   p.cin = pr.cout;  // GEMM K channels
   p.cout = pr.cin;  // GEMM N: input-gradient channels
-  p.out_h = p.out_w = pr.n;
-  p.Mv = (long long)pr.batch * pr.n * pr.n;
+  p.out_h = pr.in_h;
+  p.out_w = pr.in_w;
+  p.Mv = (long long)pr.batch * pr.in_h * pr.in_w;
   p.NT = tc_wide_ntile(pr.cin);
   p.n_tiles = (pr.cin + p.NT - 1) / p.NT;
   p.nkb = pr.cout / tcw::KB;
@@ -1020,8 +1029,9 @@ static bool make_wide_dgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
       p.tap_off_r[0][U * pr.kw + V] = pr.kh - 1 - U;
       p.tap_off_c[0][U * pr.kw + V] = pr.kw - 1 - V;
     }
-  p.rows[0] = p.cols[0] = pr.n;
-  p.wscale = 2;
+  p.rows[0] = pr.in_h;
+  p.cols[0] = pr.in_w;
+  p.wscale = pr.stride;
   p.wbase_r = lo_r;
   p.wbase_c = lo_c;
   p.ostride = 1;
@@ -1057,10 +1067,10 @@ static bool make_wide_dgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
                                 (cuuint64_t)pr.batch};
     const cuuint64_t strides[3] = {(cuuint64_t)pr.cout * 2, (cuuint64_t)pr.out_w * pr.cout * 2,
                                    (cuuint64_t)pr.out_h * pr.out_w * pr.cout * 2};
-    // walk: origins lo, lo + 2, ..., out - 1 - p (n per axis); corners {W, H}
+    // walk: origins lo, lo + stride, ... (in_h x in_w per image); corners {W, H}
     const int lower[2] = {lo_c, lo_r};
-    const int upper[2] = {-pr.p, -pr.p};
-    const cuuint32_t es[4] = {1, 2, 2, 1};
+    const int upper[2] = {up_c, up_r};
+    const cuuint32_t es[4] = {1, (cuuint32_t)pr.stride, (cuuint32_t)pr.stride, 1};
     if (enc2(&maps.xi[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pr.gy), dims, strides, lower,
              upper, (cuuint32_t)tcw::KB, 128, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -1098,11 +1108,18 @@ static bool make_wide_wgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
   const int taps = pr.kh * pr.kw;
   if (taps > tcw::MAX_TAPS_Q) return false;
   const int lo_r = pr.p - pr.kh + 1, lo_c = pr.p - pr.kw + 1;
-  if (lo_r < -128 || lo_c < -128 || pr.p > 128) return false;
-  const long long M = (long long)pr.batch * pr.n * pr.n;
+  const int up_r = pr.stride * (pr.in_h - 1) + lo_r - (pr.out_h - 1);
+  const int up_c = pr.stride * (pr.in_w - 1) + lo_c - (pr.out_w - 1);
+  if (lo_r < -128 || lo_c < -128 || up_r < -128 || up_c < -128 || up_r > 127 || up_c > 127 || lo_r > 127 ||
+      lo_c > 127)
+    return false;
+  const long long M = (long long)pr.batch * pr.in_h * pr.in_w;
   if (M + 64 >= (1LL << 31)) return false;
   p.mode = 1;
-  p.n = pr.n;
+  p.n = pr.in_h;
+  p.w_in_h = pr.in_h;
+  p.w_in_w = pr.in_w;
+  p.wscale = pr.stride;
   p.batch = pr.batch;
   p.NT = pr.cout % 256 == 0 ? 256 : 128;
   p.n_tiles = pr.cout / p.NT;
@@ -1190,8 +1207,8 @@ static bool make_wide_wgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
     const cuuint64_t strides[3] = {(cuuint64_t)pr.cout * 2, (cuuint64_t)pr.out_w * pr.cout * 2,
                                    (cuuint64_t)pr.out_h * pr.out_w * pr.cout * 2};
     const int lower[2] = {lo_c, lo_r};
-    const int upper[2] = {-pr.p, -pr.p};
-    const cuuint32_t es[4] = {1, 2, 2, 1};
+    const int upper[2] = {up_c, up_r};
+    const cuuint32_t es[4] = {1, (cuuint32_t)pr.stride, (cuuint32_t)pr.stride, 1};
     if (enc2(&maps.xi[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pr.gy), dims, strides, lower,
              upper, 64, 64, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)

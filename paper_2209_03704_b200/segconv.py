@@ -32,6 +32,7 @@ __all__ = [
     "count_ops_fused", "select_math", "launch_count", "last_path", "MATHS",
     "transpose_conv_fused_backward", "FusedTConv", "TransposeConvFused", "IoError", "ParseError",
     "TensorFileInfo", "peek_tensor_file", "load_tensor", "save_tensor", "load_tensor_batch",
+    "conv2d_valid_backward",
 ]
 
 
@@ -697,6 +698,53 @@ def conv2d_valid(src: torch.Tensor, k: torch.Tensor, *, bias=None, activation=No
     if host:
         y = y.cpu()
     return y[0] if squeeze else y
+
+
+def conv2d_valid_backward(src: torch.Tensor, kernel: torch.Tensor, grad_out: torch.Tensor, *,
+                          math: Optional[str] = None, input_grad: bool = True,
+                          kernel_grad: bool = True, grad_kernel: Optional[torch.Tensor] = None):
+    """Gradients of conv2d_valid -- reference netdemo/layers.hpp:98-122
+    (net::ConvValid::backward), batched; same conventions as
+    transpose_conv_fused_backward."""
+    sb, squeeze = _as_batch(src)
+    gb, _ = _as_batch(grad_out)
+    if kernel.dim() != 4:
+        raise ShapeError(f"kernel must be (kh, kw, cin, cout), got {tuple(kernel.shape)}")
+    kh, kw, kcin, cout = (int(v) for v in kernel.shape)
+    b, h, w, cin = (int(v) for v in sb.shape)
+    if kcin != cin:
+        raise ContractError(f"channel mismatch: input has {cin}, kernel expects {kcin}")
+    oh, ow = h - kh + 1, w - kw + 1
+    if oh < 1 or ow < 1:
+        raise ShapeError(f"kernel {kh}x{kw} does not fit input {h}x{w}")
+    if tuple(gb.shape) != (b, oh, ow, cout):
+        raise ContractError("conv_valid: output gradient shape mismatch")
+    if math is not None and math not in MATHS:
+        raise ContractError(f"unknown math {math!r}")
+    dev = _device()
+    dt = sb.dtype
+    sd, gd, kd = sb.to(dev).contiguous(), gb.to(dev, dt).contiguous(), kernel.to(dev, dt).contiguous()
+    gx = torch.empty_like(sd) if input_grad else None
+    acc_dt = torch.float64 if dt == torch.float64 else torch.float32
+    acc = 0
+    gk = None
+    if kernel_grad:
+        if grad_kernel is not None:
+            if tuple(grad_kernel.shape) != (kh, kw, cin, cout) or grad_kernel.dtype != acc_dt or \
+                    not grad_kernel.is_cuda or not grad_kernel.is_contiguous():
+                raise ContractError(f"grad_kernel must be a contiguous {acc_dt} CUDA tensor of the "
+                                    "kernel's shape")
+            gk, acc = grad_kernel, 1
+        else:
+            gk = torch.empty((kh, kw, cin, cout), dtype=acc_dt, device=dev)
+    m = MATHS[math] if math is not None else A.MATH_AUTO
+    _check(A.lib().segconv_conv2d_valid_backward(
+        sd.data_ptr(), gd.data_ptr(), _dtype_code(sd), b, h, w, cin, kd.data_ptr(), kh, kw, cout, m,
+        gx.data_ptr() if gx is not None else None, gk.data_ptr() if gk is not None else None, acc,
+        _stream()))
+    if gx is not None and squeeze:
+        gx = gx[0]
+    return gx, gk
 
 
 def transpose_conv_naive(x: torch.Tensor, k: torch.Tensor, p: int, *, bias=None,

@@ -212,6 +212,45 @@ int main() {
           }
     CHECK(ok && blocks.size() == 1 && blocks[0].size == k.size(), "layer gradients == scatter form, exact");
   }
+  // ConvValid layer (reference layers.hpp:84-137): gradients on integer data, exact
+  {
+    std::mt19937 rng(98);
+    std::uniform_int_distribution<int> d(-3, 3);
+    const int h = 7, w = 6, cin = 2, cout = 3, kh = 3, kw = 2;
+    Tensor<double> in(h, w, cin);
+    for (size_t i = 0; i < in.size(); ++i) in.data()[i] = d(rng);
+    Kernel<double> k(kh, kw, cin, cout);
+    for (size_t i = 0; i < k.size(); ++i) k.data()[i] = d(rng);
+    segconv::net::ConvValid<double> layer(k);
+    const auto y = layer.forward(in);
+    Tensor<double> g(y.height(), y.width(), cout);
+    for (size_t i = 0; i < g.size(); ++i) g.data()[i] = d(rng);
+    const auto gin = layer.backward(g);
+    bool ok = true;
+    for (int a = 0; a < h; ++a)
+      for (int c = 0; c < w; ++c)
+        for (int ch = 0; ch < cin; ++ch) {
+          double want = 0;
+          for (int u = 0; u < kh; ++u)
+            for (int v = 0; v < kw; ++v) {
+              const int yy = a - u, xx = c - v;
+              if (yy < 0 || yy >= y.height() || xx < 0 || xx >= y.width()) continue;
+              for (int f = 0; f < cout; ++f) want += k(u, v, ch, f) * g(yy, xx, f);
+            }
+          ok = ok && gin(a, c, ch) == want;
+        }
+    auto blocks = layer.params();
+    for (int u = 0; u < kh; ++u)
+      for (int v = 0; v < kw; ++v)
+        for (int ch = 0; ch < cin; ++ch)
+          for (int f = 0; f < cout; ++f) {
+            double want = 0;
+            for (int yy = 0; yy < y.height(); ++yy)
+              for (int xx = 0; xx < y.width(); ++xx) want += in(yy + u, xx + v, ch) * g(yy, xx, f);
+            ok = ok && blocks[0].grads[(((size_t)u * kw + v) * cin + ch) * cout + f] == want;
+          }
+    CHECK(ok, "ConvValid layer gradients == direct sums, exact");
+  }
   std::printf("%d failure(s)\n", failures);
   return failures;
 }

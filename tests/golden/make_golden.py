@@ -24,7 +24,8 @@ Fixtures (all small):
                      (`python tests/golden/make_golden.py backward` rewrites
                      only this file)
   conv_valid.npz     conv2d_valid (reference_ops.hpp:86-102) on rectangular
-                     maps and kernels (`python tests/golden/make_golden.py conv`)
+                     maps and kernels, and net::ConvValid's gradients
+                     (netdemo/layers.hpp:98-122) (`python tests/golden/make_golden.py conv`)
   sgc/*.sgc          SGC1 tensor files written by the reference's save_tensor
                      (tensor_io.hpp:93-103) + sgc/values.npz with their contents
                      (`python tests/golden/make_golden.py sgc`)
@@ -198,6 +199,9 @@ def conv():
         k = rng.uniform(-1, 1, (kh, kw, cin, cout)).astype(np.float32)
         out[f"c{i}_src"], out[f"c{i}_k"] = s, k
         out[f"c{i}_y"] = oracle.ref_conv2d_valid(s, k)
+        gy = rng.uniform(-1, 1, out[f"c{i}_y"].shape).astype(np.float32)
+        out[f"c{i}_gy"] = gy
+        out[f"c{i}_gx"], out[f"c{i}_gk"] = oracle.ref_conv2d_valid_backward(s, k, gy)
     out["count"] = np.int32(len(specs))
     np.savez_compressed(os.path.join(OUT, "conv_valid.npz"), **out)
 

@@ -80,3 +80,46 @@ def test_bf16_conventional_transpose_conv_uses_the_tensor_core_conv():
     yn = sc.transpose_conv_naive(xb, kb, 2)
     assert sc.last_path() == "tc-pair"
     np.testing.assert_array_equal(yn.float().cpu().numpy(), oracle.bf16_round(oracle.tconv_fused(x, k, 2)))
+
+
+# ---- backward (reference netdemo/layers.hpp:98-122, net::ConvValid::backward)
+def test_backward_exact_matches_reference_goldens():
+    z = np.load(os.path.join(G, "conv_valid.npz"))
+    for i in range(int(z["count"])):
+        t = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+        gx, gk = sc.conv2d_valid_backward(t(z[f"c{i}_src"]), t(z[f"c{i}_k"]), t(z[f"c{i}_gy"]), math="exact")
+        assert sc.last_path() == "bwd:simt-exact+simt-exact"
+        np.testing.assert_array_equal(gx.cpu().numpy(), z[f"c{i}_gx"])
+        np.testing.assert_array_equal(gk.cpu().numpy(), z[f"c{i}_gk"])
+
+
+@pytest.mark.parametrize("b,h,w,cin,kh,kw,cout", [(2, 9, 7, 5, 3, 2, 4), (3, 12, 12, 64, 3, 3, 32),
+                                                  (1, 6, 8, 16, 5, 5, 3), (2, 20, 20, 130, 4, 4, 70)])
+def test_backward_ffma(b, h, w, cin, kh, kw, cout):
+    rng = np.random.default_rng(b + h + cin)
+    s = rng.uniform(-1, 1, (b, h, w, cin)).astype(np.float32)
+    k = (rng.standard_normal((kh, kw, cin, cout)) * 0.05).astype(np.float32)
+    gy = rng.uniform(-1, 1, (b, h - kh + 1, w - kw + 1, cout)).astype(np.float32)
+    wx, wk = oracle.conv2d_valid_backward(s, k, gy)
+    t = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+    gx, gk = sc.conv2d_valid_backward(t(s), t(k), t(gy), math="ffma")
+    assert sc.last_path() == "bwd:simt-ffma+simt-ffma"
+    ax, ak = oracle.conv2d_valid_backward(np.abs(s), np.abs(k), np.abs(gy))
+    assert (np.abs(gx.cpu().numpy() - wx) <= 1e-5 * ax + 1e-7).all()
+    assert (np.abs(gk.cpu().numpy() - wk) <= 1e-5 * ak + 1e-7).all()
+
+
+@pytest.mark.parametrize("b,h,w,cin,kh,kw,cout", [(2, 9, 9, 128, 3, 3, 128), (3, 12, 7, 256, 4, 2, 128),
+                                                  (1, 33, 33, 256, 4, 4, 256), (4, 6, 5, 128, 5, 5, 64)])
+def test_backward_bf16_tensor_core_int_exact(b, h, w, cin, kh, kw, cout):
+    rng = np.random.default_rng(b * 10 + h + cin)
+    s = rng.integers(-3, 4, (b, h, w, cin)).astype(np.float32)
+    k = rng.integers(-2, 3, (kh, kw, cin, cout)).astype(np.float32)
+    gy = rng.integers(-2, 3, (b, h - kh + 1, w - kw + 1, cout)).astype(np.float32)
+    wx, wk = oracle.conv2d_valid_backward(s, k, gy)
+    t = lambda a: torch.from_numpy(a).cuda().bfloat16()  # noqa: E731
+    gx, gk = sc.conv2d_valid_backward(t(s), t(k), t(gy))
+    wpath = "tc-pair" if cin % 128 == 0 and cout % 128 == 0 else "simt-ffma"
+    assert sc.last_path() == "bwd:tc-pair+" + wpath
+    np.testing.assert_array_equal(gx.float().cpu().numpy(), oracle.bf16_round(wx))
+    np.testing.assert_array_equal(gk.cpu().numpy(), wk)

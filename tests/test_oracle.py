@@ -245,3 +245,12 @@ def test_conv2d_valid_bit_exact_vs_reference_goldens():
     z = _npz("conv_valid.npz")
     for i in range(int(z["count"])):
         np.testing.assert_array_equal(oracle.conv2d_valid(z[f"c{i}_src"], z[f"c{i}_k"]), z[f"c{i}_y"])
+
+
+def test_conv2d_valid_backward_bit_exact_vs_reference_goldens():
+    """oracle.conv2d_valid_backward == net::ConvValid::backward (layers.hpp:98-122)."""
+    z = _npz("conv_valid.npz")
+    for i in range(int(z["count"])):
+        gx, gk = oracle.conv2d_valid_backward(z[f"c{i}_src"], z[f"c{i}_k"], z[f"c{i}_gy"])
+        np.testing.assert_array_equal(gx, z[f"c{i}_gx"])
+        np.testing.assert_array_equal(gk, z[f"c{i}_gk"])
