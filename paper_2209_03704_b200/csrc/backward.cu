@@ -24,6 +24,7 @@
 // a stride-2 im2col walk over gy (launch_tc_bwd_data there).
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <type_traits>
 
 #include "common.cuh"
@@ -677,23 +678,30 @@ static cudaError_t bwd_weight_t(const BackwardProblem& pr, bool exact, cudaStrea
 // the OS at every synchronisation, making each call pay a fresh mapping).
 cudaError_t workspace_alloc(void** p, size_t bytes, cudaStream_t s) {
   static cudaMemPool_t pools[64] = {};
+  static std::mutex mu;  // pool creation only; allocation itself is stream-ordered
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev < 0 || dev >= 64) return cudaMallocAsync(p, bytes, s);
-  if (!pools[dev]) {
-    cudaMemPoolProps props = {};
-    props.allocType = cudaMemAllocationTypePinned;
-    props.location.type = cudaMemLocationTypeDevice;
-    props.location.id = dev;
-    cudaMemPool_t pool;
-    e = cudaMemPoolCreate(&pool, &props);
-    if (e != cudaSuccess) return e;
-    uint64_t keep = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    pools[dev] = pool;
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!pools[dev]) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      e = cudaMemPoolCreate(&pools[dev], &props);
+      if (e != cudaSuccess) {
+        pools[dev] = nullptr;
+        return e;
+      }
+      uint64_t keep = ~0ull;
+      cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    pool = pools[dev];
   }
-  return cudaMallocFromPoolAsync(p, bytes, pools[dev], s);
+  return cudaMallocFromPoolAsync(p, bytes, pool, s);
 }
 
 cudaError_t launch_wgrad_reduce(const float* ws, float* gk, long long ksz, int splits, int accumulate,
