@@ -250,11 +250,22 @@ class LayerBackward(Layer):
         self.alg_bytes = (2 * self.xd.numel() + self.kd.numel() + self.gyd.numel()) * e + \
             self.kd.numel() * 4
         self.torch = torch
+        self.world = world
         self.launches_per_step = 2
         self.gx_pinned = torch.empty(self.xd.shape, dtype=self.tdt).pin_memory()
         self.gk_pinned = torch.empty(self.kd.shape, dtype=torch.float32).pin_memory()
 
     def step(self):
+        if self.world > 1:
+            # data-parallel step: the kernel gradient's all-reduce (NCCL) runs while
+            # the input-gradient kernel computes (paper_2209_03704_b200/dp.py)
+            _, gk = self.sc.transpose_conv_fused_backward(self.xd, self.kd, self.cfg["p"], self.gyd,
+                                                          input_grad=False)
+            work = self.torch.distributed.all_reduce(gk, async_op=True)
+            self.sc.transpose_conv_fused_backward(self.xd, self.kd, self.cfg["p"], self.gyd,
+                                                  kernel_grad=False)
+            work.wait()
+            return
         self.sc.transpose_conv_fused_backward(self.xd, self.kd, self.cfg["p"], self.gyd)
 
     def step_e2e(self):
@@ -659,7 +670,9 @@ def main():
                           "math": prob.math,
                           "per_gpu_batch": (prob.hi - prob.lo) if cfg.get("stack") else cfg["batch"],
                           "l2": "flushed between timed steps (256 MiB write, outside events)",
-                          "parallelism": f"batch-sharded x{world}, weights replicated"},
+                          "parallelism": f"batch-sharded x{world}, weights replicated"
+                          + (", kernel-gradient all-reduce (NCCL) overlapped with the input "
+                             "gradient" if bwd and world > 1 else "")},
                "hbm_gbs": round(hbm_gbs, 1),
                "roofline": roof,
                "e2e": {"value": round(macs_all / (e2e_ms * 1e-3) / 1e9, 2), "unit": "useful GMAC/s",

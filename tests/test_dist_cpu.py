@@ -101,3 +101,55 @@ def test_sharded_stack_gloo_world2(batch):
         h = oracle.tconv_fused(h, k, s.p)
         h = np.maximum(h, 0) if s.activation == "relu" else np.tanh(h)
     np.testing.assert_allclose(full0, h, rtol=0, atol=1e-6)
+
+
+# ---- data-parallel backward: the kernel gradient is all-reduced over ranks
+def _bwd_worker(rank, world, port, batch, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2209_03704_b200 import dp
+        # CPU stand-ins for the per-rank sm_100a kernels (oracle: test infrastructure)
+        dp._segregate = lambda k, p, m: None
+        dp._local_forward = lambda x, sks, g, m: torch.from_numpy(
+            oracle.tconv_fused(x.numpy(), KB, PB))
+        dp._local_kernel_grad = lambda x, k, p, g, m: torch.from_numpy(
+            oracle.tconv_backward(x.numpy(), k.numpy(), p, g.numpy())[1])
+        dp._local_input_grad = lambda x, k, p, g, m: torch.from_numpy(
+            oracle.tconv_backward(x.numpy(), k.numpy(), p, g.numpy())[0])
+        rng = np.random.default_rng(300 + rank)  # different on each rank: rank 0's wins
+        k = torch.from_numpy(rng.uniform(-1, 1, KB.shape).astype(np.float32))
+        layer = dp.ShardedFusedTConv(k, PB, batch)
+        x = np.random.default_rng(5).uniform(-1, 1, (batch, 5, 5, 3)).astype(np.float32)
+        g = np.random.default_rng(6).uniform(-1, 1, (batch, 10, 10, 2)).astype(np.float32)
+        layer.forward(torch.from_numpy(x[layer.lo:layer.hi]))
+        gx = layer.backward(torch.from_numpy(g[layer.lo:layer.hi]))
+        q.put((rank, layer.lo, layer.hi, gx.numpy(), layer.grad.numpy(), layer.kernel_.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+KB = np.random.default_rng(4).uniform(-1, 1, (4, 4, 3, 2)).astype(np.float32)
+PB = 2
+
+
+@pytest.mark.parametrize("batch", [3, 6])
+def test_sharded_backward_gloo_world2(batch):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bwd_worker, args=(r, 2, port, batch, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(2)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, lo0, hi0, gx0, gk0, k0), (_, lo1, hi1, gx1, gk1, k1) = res
+    np.testing.assert_array_equal(k0, k1)  # kernel replicated from rank 0
+    x = np.random.default_rng(5).uniform(-1, 1, (batch, 5, 5, 3)).astype(np.float32)
+    g = np.random.default_rng(6).uniform(-1, 1, (batch, 10, 10, 2)).astype(np.float32)
+    wx, wk = oracle.tconv_backward(x, k0, PB, g)
+    np.testing.assert_array_equal(np.concatenate([gx0, gx1]), wx)  # input grads: per shard
+    np.testing.assert_array_equal(gk0, gk1)  # every rank holds the all-reduced sum
+    np.testing.assert_allclose(gk0, wk, rtol=0, atol=1e-5)  # == the full-batch kernel grad
