@@ -267,6 +267,7 @@ class LayerBackward(Layer):
             work.wait()
             return
         self.sc.transpose_conv_fused_backward(self.xd, self.kd, self.cfg["p"], self.gyd)
+        self.math = self.sc.last_path()  # e.g. "bwd:tc-pair+tc-pair"
 
     def step_e2e(self):
         """Public API from host buffers: x and gy uploaded, both gradients read back."""
@@ -624,7 +625,7 @@ def main():
     roof["traffic"] = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
-        tr = json.load(open(prof)).get(args.config)
+        tr = json.load(open(prof)).get(args.config + (":backward" if bwd else ""))
         if tr:
             roof["traffic"] = tr.get("dram_bytes_per_launch")
             roof["traffic_src"] = tr.get("source")
