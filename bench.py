@@ -265,6 +265,7 @@ class LayerBackward(Layer):
             self.sc.transpose_conv_fused_backward(self.xd, self.kd, self.cfg["p"], self.gyd,
                                                   kernel_grad=False)
             work.wait()
+            self.math = "bwd:dp (" + self.sc.last_path() + ", kernel grad all-reduced)"
             return
         self.sc.transpose_conv_fused_backward(self.xd, self.kd, self.cfg["p"], self.gyd)
         self.math = self.sc.last_path()  # e.g. "bwd:tc-pair+tc-pair"
