@@ -179,6 +179,41 @@ class DeviceBuffer {
   size_t n_ = 0;
 };
 
+namespace detail {
+// Value-semantics calls stage their host tensors through thread-local,
+// grow-only device buffers (one per role), so a loop of per-image calls does
+// not pay a cudaMalloc / cudaFree per tensor.
+class Staged {
+ public:
+  Staged(int slot, size_t bytes) : p_(buffer(slot, bytes)) {}
+  Staged(int slot, const void* host, size_t bytes) : Staged(slot, bytes) {
+    if (bytes && cudaMemcpy(p_, host, bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+      throw CudaError("cudaMemcpy H2D failed");
+  }
+  void* get() const { return p_; }
+  void to_host(void* dst, size_t bytes) const {
+    if (bytes && cudaMemcpy(dst, p_, bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+      throw CudaError("cudaMemcpy D2H failed");
+  }
+
+ private:
+  static void* buffer(int slot, size_t bytes) {
+    struct Slot {
+      DeviceBuffer buf;
+      size_t cap = 0;
+    };
+    thread_local Slot slots[8];
+    Slot& s = slots[slot];
+    if (s.cap < bytes) {
+      s.buf = DeviceBuffer(bytes);
+      s.cap = bytes;
+    }
+    return s.buf.get();
+  }
+  void* p_;
+};
+}  // namespace detail
+
 // ------------------------------------------------------------- geometry
 // reference geometry.hpp:18-53
 struct TConvGeometry {
@@ -225,7 +260,7 @@ SubKernelSet<T> segregate(const Kernel<T>& k, int p_orig, segconv_math math = SE
                                        dtype_of<T>::value, math, &s.desc));
   const size_t esz = s.desc.dtype == SEGCONV_F64 ? 8 : s.desc.dtype == SEGCONV_F32 ? 4 : 2;
   s.panels = std::make_shared<DeviceBuffer>(std::max<size_t>(1, s.desc.total_elems * esz));
-  DeviceBuffer dk(k.data(), k.size() * sizeof(T));
+  detail::Staged dk(0, k.data(), k.size() * sizeof(T));
   throw_on(segconv_segregate(dk.get(), dtype_of<T>::value, &s.desc, s.panels->get(), nullptr));
   if (cudaDeviceSynchronize() != cudaSuccess) throw CudaError("segregate failed");
   s.source_kh = k.kh();
@@ -242,8 +277,8 @@ Tensor<T> transpose_conv_fused(const Tensor<T>& input, const SubKernelSet<T>& sk
   if (input.height() != geom.n_in || input.width() != geom.n_in)
     throw ContractError("input size does not match the geometry");
   Tensor<T> out(geom.out_h, geom.out_w, sks.cout());
-  DeviceBuffer dx(input.data(), input.size() * sizeof(T));
-  DeviceBuffer dy(out.size() * sizeof(T));
+  detail::Staged dx(0, input.data(), input.size() * sizeof(T));
+  detail::Staged dy(1, out.size() * sizeof(T));
   const segconv_geometry g = geom.c();
   throw_on(segconv_transpose_conv_fused(dx.get(), dtype_of<T>::value, 1, input.height(),
                                         input.channels(), &sks.desc, sks.panels->get(), &g,
@@ -280,8 +315,8 @@ Tensor<T> conv2d_valid(const Tensor<T>& src, const Kernel<T>& k) {
   const int oh = src.height() - k.kh() + 1, ow = src.width() - k.kw() + 1;
   if (oh < 1 || ow < 1) throw ShapeError("kernel does not fit input");
   Tensor<T> out(oh, ow, k.cout());
-  DeviceBuffer ds(src.data(), src.size() * sizeof(T)), dk(k.data(), k.size() * sizeof(T));
-  DeviceBuffer dy(out.size() * sizeof(T));
+  detail::Staged ds(0, src.data(), src.size() * sizeof(T)), dk(2, k.data(), k.size() * sizeof(T));
+  detail::Staged dy(1, out.size() * sizeof(T));
   throw_on(segconv_conv2d_valid(ds.get(), dtype_of<T>::value, 1, src.height(), src.width(),
                                 src.channels(), dk.get(), k.kh(), k.kw(), k.cout(), nullptr,
                                 SEGCONV_EPI_NONE, dy.get(), nullptr));
@@ -299,8 +334,8 @@ Tensor<T> transpose_conv_naive(const Tensor<T>& input, const Kernel<T>& k, int p
   Tensor<T> out(geom.out_h, geom.out_w, k.cout());
   const size_t ws = segconv_naive_workspace_bytes(dtype_of<T>::value, 1, input.height(),
                                                   input.channels(), p);
-  DeviceBuffer dx(input.data(), input.size() * sizeof(T)), dk(k.data(), k.size() * sizeof(T));
-  DeviceBuffer dw(ws), dy(out.size() * sizeof(T));
+  detail::Staged dx(0, input.data(), input.size() * sizeof(T)), dk(2, k.data(), k.size() * sizeof(T));
+  detail::Staged dw(3, ws), dy(1, out.size() * sizeof(T));
   throw_on(segconv_transpose_conv_naive(dx.get(), dtype_of<T>::value, 1, input.height(),
                                         input.channels(), dk.get(), k.kh(), k.kw(), k.cout(), p,
                                         dw.get(), ws, nullptr, SEGCONV_EPI_NONE, dy.get(),
@@ -367,9 +402,9 @@ class ConvValid {
   Tensor<T> backward(const Tensor<T>& g) {
     if (!has_input_) throw StateError(std::string(name()) + ": backward called before forward");
     Tensor<T> gin(input_.height(), input_.width(), input_.channels());
-    DeviceBuffer dx(input_.data(), input_.size() * sizeof(T)), dg(g.data(), g.size() * sizeof(T));
-    DeviceBuffer dk(kernel_.data(), kernel_.size() * sizeof(T));
-    DeviceBuffer dgk(grad_.data(), grad_.size() * sizeof(T)), dgx(gin.size() * sizeof(T));
+    detail::Staged dx(0, input_.data(), input_.size() * sizeof(T)), dg(4, g.data(), g.size() * sizeof(T));
+    detail::Staged dk(2, kernel_.data(), kernel_.size() * sizeof(T));
+    detail::Staged dgk(5, grad_.data(), grad_.size() * sizeof(T)), dgx(1, gin.size() * sizeof(T));
     throw_on(segconv_conv2d_valid_backward(dx.get(), dg.get(), dtype_of<T>::value, 1, input_.height(),
                                            input_.width(), input_.channels(), dk.get(), kernel_.kh(),
                                            kernel_.kw(), kernel_.cout(), math_, dgx.get(), dgk.get(), 1, nullptr));
@@ -417,9 +452,9 @@ class FusedTConv {
     if (g.height() != geom_.out_h || g.width() != geom_.out_w || g.channels() != kernel_.cout())
       throw ContractError("fused_tconv: output gradient shape mismatch");
     Tensor<T> gin(input_.height(), input_.width(), input_.channels());
-    DeviceBuffer dx(input_.data(), input_.size() * sizeof(T)), dg(g.data(), g.size() * sizeof(T));
-    DeviceBuffer dk(kernel_.data(), kernel_.size() * sizeof(T));
-    DeviceBuffer dgk(grad_.data(), grad_.size() * sizeof(T)), dgx(gin.size() * sizeof(T));
+    detail::Staged dx(0, input_.data(), input_.size() * sizeof(T)), dg(4, g.data(), g.size() * sizeof(T));
+    detail::Staged dk(2, kernel_.data(), kernel_.size() * sizeof(T));
+    detail::Staged dgk(5, grad_.data(), grad_.size() * sizeof(T)), dgx(1, gin.size() * sizeof(T));
     throw_on(segconv_transpose_conv_fused_backward(
         dx.get(), dg.get(), dtype_of<T>::value, 1, input_.height(), input_.channels(), dk.get(), kernel_.kh(),
         kernel_.kw(), kernel_.cout(), p_, math_, dgx.get(), dgk.get(), /*accumulate=*/1, nullptr));
