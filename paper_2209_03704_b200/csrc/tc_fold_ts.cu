@@ -652,9 +652,7 @@ static cudaError_t launch_fold_ts_t(const tcfs::Params& prm, const CUtensorMap& 
   while (pc.cluster > 1 && ((uint32_t)prm.w_img_bytes % (16u * pc.cluster) != 0 || grid < pc.cluster))
     pc.cluster /= 2;
   if (pc.cluster > 1) {
-    grid = grid / pc.cluster * pc.cluster;  // whole clusters; ranges re-split over the grid
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(tcfs::NUM_THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -665,6 +663,16 @@ static cudaError_t launch_fold_ts_t(const tcfs::Params& prm, const CUtensorMap& 
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
+    // whole clusters, and no more than can be co-resident (GPCs with an odd
+    // number of free SMs would otherwise push a cluster into a second wave);
+    // the anchor ranges are re-split over the grid
+    cfg.gridDim = dim3((unsigned)(grid / pc.cluster * pc.cluster));
+    int max_clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&max_clusters, (void*)kern, &cfg) == cudaSuccess && max_clusters > 0)
+      grid = std::min<long long>(grid / pc.cluster, max_clusters) * pc.cluster;
+    else
+      grid = grid / pc.cluster * pc.cluster;
+    cfg.gridDim = dim3((unsigned)grid);
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, pc, tmap);
     if (e == cudaSuccess) {
       note_launch();
