@@ -46,6 +46,16 @@ CONFIGS = {
     "C5": dict(batch=1024, stack=True, dtype="bf16",
                desc="4-layer bf16 generator stack, batch 1024 sharded, 4->5->7->11->19"),
     # single layers of the C5 stack (diagnostics: --config C5a .. C5d)
+    # GAN generator presets (reference analysis.hpp:96-114, bench.hpp:118-124 `gan:<model>`):
+    # every layer 4x4 at p = 2 (out = 2N), bf16 chain, batch 64; not BASELINE configs
+    "gan:dcgan": dict(batch=64, stack=True, gan="dcgan", dtype="bf16",
+                      desc="DCGAN generator 4->64, 1024->3 channels, batch 64"),
+    "gan:artgan": dict(batch=64, stack=True, gan="artgan", dtype="bf16",
+                       desc="Art-GAN generator 4->64, 512->3 channels, batch 64"),
+    "gan:gpgan": dict(batch=64, stack=True, gan="gpgan", dtype="bf16",
+                      desc="GP-GAN generator 4->64, 512->3 channels, batch 64"),
+    "gan:ebgan": dict(batch=64, stack=True, gan="ebgan", dtype="bf16",
+                      desc="EB-GAN generator 4->256, 2048->64 channels, batch 64"),
     "C5a": dict(batch=1024, n=4, cin=1024, cout=512, k=3, p=0, dtype="bf16", xd="n", wd="n02",
                 act="relu", desc="C5 layer a: 1024x4x4x1024 -> 5x5x512"),
     "C5b": dict(batch=1024, n=5, cin=512, cout=256, k=3, p=0, dtype="bf16", xd="n", wd="n02",
@@ -327,7 +337,7 @@ class Stack:
     def __init__(self, cfg, rank, world, torch, sc, dev):
         from paper_2209_03704_b200 import stack as st
         self.cfg = cfg
-        self.specs = st.c5_layers()
+        self.specs = stack_specs(cfg)
         krng = np.random.default_rng(SEED)
         self.k_host = [gen((s.k, s.k, s.cin, s.cout), "n02", krng) for s in self.specs]
         ks = [torch.from_numpy(k).to(dev) for k in self.k_host]
@@ -389,11 +399,15 @@ class Stack:
         return secs, nimg, kind
 
 
-def stack_macs_per_image():
-    from paper_2209_03704_b200 import segconv as sc
+def stack_specs(cfg):
+    """Layer chain of a stack config: BASELINE C5, or a GAN generator preset."""
     from paper_2209_03704_b200 import stack as st
-    return sum(sc.count_ops_fused(sc.LayerShape(s.n_in, s.cin, s.cout, s.k, s.k, s.p)).mults
-               for s in st.c5_layers())
+    return st.gan_layers(cfg["gan"]) if cfg.get("gan") else st.c5_layers()
+
+
+def stack_macs_per_image(cfg):
+    from oracle.oracle import count_ops
+    return sum(count_ops(s.n_in, s.cin, s.cout, s.k, s.k, s.p)[2] for s in stack_specs(cfg))
 
 
 # ------------------------------------------------------------ reference arm
@@ -408,12 +422,13 @@ def run_reference(args, cfg):
     times, nimgs = [], 0
     if cfg.get("stack"):
         from paper_2209_03704_b200 import stack as st
-        specs = st.c5_layers()
+        specs = stack_specs(cfg)
         krng = np.random.default_rng(SEED)
         ks = [oracle.bf16_round(gen((s.k, s.k, s.cin, s.cout), "n02", krng)) for s in specs]
         nimg = min(cfg["batch"], max(1, 2 * workers))
-        x0 = oracle.bf16_round(rng.standard_normal((nimg, 4, 4, 1024), dtype=np.float32))
-        macs_img = stack_macs_per_image()
+        s0 = specs[0]
+        x0 = oracle.bf16_round(rng.standard_normal((nimg, s0.n_in, s0.n_in, s0.cin), dtype=np.float32))
+        macs_img = stack_macs_per_image(cfg)
         for i in range(args.warmup + args.steps):
             x, secs = x0, 0.0
             for s, k in zip(specs, ks):

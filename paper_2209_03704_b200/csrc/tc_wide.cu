@@ -795,14 +795,22 @@ int tc_wide_ntile(int cout) {
   return std::min(256, c32);
 }
 
+// Must agree with make_wide (the KMAJOR panels it implies have no other consumer):
+// every class has taps, at most MAX_TAPS_Q of them, and the im2col walk's
+// corner offsets (-p_fused .. ) fit the rank-4 range [-128, 127].
 bool tc_wide_fits(int kh, int kw, int p, int cin, int cout) {
-  if (cin % tcw::KB != 0 || cout < 64) return false;
+  if (cin % tcw::KB != 0 || cout < 64 || p < 0 || p / 2 > 120) return false;
+  int ah[2], aw[2];
   for (int r = 0; r < 2; ++r) {
     const int u0 = (p + r) & 1;
-    const int ah = u0 >= kh ? 0 : (kh - u0 + 1) / 2, aw = u0 >= kw ? 0 : (kw - u0 + 1) / 2;
-    if (ah == 0 || aw == 0) return false;
+    ah[r] = u0 >= kh ? 0 : (kh - u0 + 1) / 2;
+    aw[r] = u0 >= kw ? 0 : (kw - u0 + 1) / 2;
+    if (ah[r] == 0 || aw[r] == 0) return false;
   }
-  return kh * kw <= 4 * tcw::MAX_TAPS_Q;
+  for (int r = 0; r < 2; ++r)
+    for (int c = 0; c < 2; ++c)
+      if (ah[r] * aw[c] > tcw::MAX_TAPS_Q) return false;
+  return true;
 }
 
 static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
@@ -849,18 +857,6 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
     p.rows[q] = pr.cls.rows[q];
     p.cols[q] = pr.cls.cols[q];
   }
-  if (p.tile2d) {
-    if (p.VW > 128) return false;
-    p.TR = 128 / p.VW;
-    p.TRH = p.TR + max_dy + 1;  // + one row: shifted reads of the last anchors wrap a row
-    const int vh = std::max(pr.cls.rows[0], pr.cls.rows[2]);
-    p.tiles_per_img = (vh + p.TR - 1) / p.TR;
-    p.S_rows = p.VW * p.TRH;
-    if (p.TRH > 256 || p.S_rows > 384) return false;
-  } else {
-    p.S_rows = (128 + max_shift + 7) / 8 * 8;
-    if (p.S_rows > 256) return false;  // one TMA box
-  }
   // IM2COL: GEMM rows are only output anchors (the halo-shift grid computes
   // every virtual position: C5 a 44 %, b 54 %, c 65 %, C3 77 % useful rows)
   {
@@ -877,6 +873,22 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
     p.im2col = 1;
     const char* e = getenv("SEGCONV_WIDE_IM2COL");
     if (e) p.im2col = atoi(e) ? 1 : 0;
+  }
+  // halo-shift staging (SEGCONV_WIDE_IM2COL=0) limits: the staged rows must fit
+  // one TMA box; they do not constrain the im2col path (e.g. 128 x 128 maps)
+  if (!p.im2col) {
+    if (p.tile2d) {
+      if (p.VW > 128) return false;
+      p.TR = 128 / p.VW;
+      p.TRH = p.TR + max_dy + 1;  // + one row: shifted reads of the last anchors wrap a row
+      const int vh = std::max(pr.cls.rows[0], pr.cls.rows[2]);
+      p.tiles_per_img = (vh + p.TR - 1) / p.TR;
+      p.S_rows = p.VW * p.TRH;
+      if (p.TRH > 256 || p.S_rows > 384) return false;
+    } else {
+      p.S_rows = (128 + max_shift + 7) / 8 * 8;
+      if (p.S_rows > 256) return false;  // one TMA box
+    }
   }
   if (p.im2col) {
     p.tile2d = 0;

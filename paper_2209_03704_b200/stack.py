@@ -41,6 +41,27 @@ def c5_layers() -> List[LayerSpec]:
             LayerSpec(256, 128, 7, 3, 0, "relu"), LayerSpec(128, 3, 11, 3, 0, "tanh")]
 
 
+# reference proj/include/segconv/analysis.hpp:96-114 (gan_models): every
+# transpose-conv layer of the named generator, 4x4 kernels at p = 2 (out = 2N);
+# (layer index, N, cin, cout).  ReLU between layers, tanh on the last.
+GAN_MODELS = {
+    "dcgan": [(2, 4, 1024, 512), (3, 8, 512, 256), (4, 16, 256, 128), (5, 32, 128, 3)],
+    "artgan": [(2, 4, 512, 256), (3, 8, 256, 128), (4, 16, 128, 128), (6, 32, 128, 3)],
+    "gpgan": [(2, 4, 512, 256), (3, 8, 256, 128), (4, 16, 128, 64), (5, 32, 64, 3)],
+    "ebgan": [(2, 4, 2048, 1024), (3, 8, 1024, 512), (4, 16, 512, 256), (5, 32, 256, 128),
+              (6, 64, 128, 64), (7, 128, 64, 64)],
+}
+
+
+def gan_layers(model: str) -> List[LayerSpec]:
+    """The generator's layers as a chain (reference analysis.hpp:96-121, gan_model)."""
+    if model not in GAN_MODELS:
+        raise sc.ContractError(f"unknown GAN model '{model}' (known: {', '.join(GAN_MODELS)})")
+    rows = GAN_MODELS[model]
+    return [LayerSpec(cin, cout, n, 4, 2, "tanh" if i == len(rows) - 1 else "relu")
+            for i, (_, n, cin, cout) in enumerate(rows)]
+
+
 def shard_range(batch: int, rank: int, world: int):
     """Contiguous batch slice [lo, hi) owned by `rank` (balanced, remainder first)."""
     base, rem = divmod(batch, world)

@@ -200,3 +200,16 @@ def test_empty_batch_is_a_no_op(math, shape):
     sks = sc.segregate(torch.zeros((ks, ks, cin, cout), device="cuda", dtype=dt), 0, math=math)
     y = sc.transpose_conv_fused(torch.zeros((0, n, n, cin), device="cuda", dtype=dt), sks, g)
     assert tuple(y.shape) == (0, g.out_h, g.out_w, cout)
+
+
+@pytest.mark.parametrize("n,p", [(128, 2), (130, 0)])
+def test_pair_kernel_large_maps(n, p):
+    """Maps wider than the halo-shift staging's TMA box (EB-GAN's last layer,
+    128 x 128 x 64 -> 256 x 256 x 64, 4x4, p = 2): the im2col path has no such
+    limit, so AUTO must not refuse them."""
+    rng = np.random.default_rng(n + p)
+    x = rng.integers(-2, 3, (1, n, n, 64)).astype(np.float32)
+    k = rng.integers(-1, 2, (4, 4, 64, 64)).astype(np.float32)
+    got, path = run(x, k, p, "bf16", out_dtype=torch.float32)
+    assert path == "tc-pair"
+    assert np.array_equal(got, oracle.tconv_fused(x, k, p))
