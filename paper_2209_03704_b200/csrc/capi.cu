@@ -424,8 +424,8 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
                       (int)math);
         if (!tc_wide_supported(pr, math))
           return fail(SEGCONV_E_UNSUPPORTED,
-                      "CTA-pair tensor-core path needs bf16 activations, cin %% 64 == 0, cout >= 64, "
-                      "p_fused == 0 and a halo of <= 256 rows");
+                      "CTA-pair tensor-core path needs bf16 activations, cin %% 64 == 0 and at most 25 "
+                      "taps per parity class");
         g_path = "tc-pair";
         return cuda_status(launch_tc_wide(pr, s), "transpose_conv_fused[tcgen05 pair]");
       }

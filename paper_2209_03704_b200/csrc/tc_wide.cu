@@ -2,7 +2,7 @@
 // transpose convolution as a CTA-pair (cta_group::2) tcgen05 implicit GEMM.
 //
 // Replaces reference proj/include/segconv/fused_tconv.hpp:42-60 and the dot
-// loop of reference_ops.hpp:31-79 for layers with cin % 64 == 0 and cout >= 64.
+// loop of reference_ops.hpp:31-79 for bf16 layers with cin % 64 == 0.
 //
 // Formulation (halo shift, as tc_igemm.cu).  Anchors m = (b, i, j) of the
 // NHWC input are GEMM rows; class q's tap (u, v) reads pixel m + shift,
@@ -799,7 +799,11 @@ int tc_wide_ntile(int cout) {
 // every class has taps, at most MAX_TAPS_Q of them, and the im2col walk's
 // corner offsets (-p_fused .. ) fit the rank-4 range [-128, 127].
 bool tc_wide_fits(int kh, int kw, int p, int cin, int cout) {
-  if (cin % tcw::KB != 0 || cout < 64 || p < 0 || p / 2 > 120) return false;
+  // narrow outputs (e.g. the 3-channel last layer of a GAN generator at p = 2,
+  // which the folded / scatter kernels do not take) run with a 32-wide
+  // feature tile: the MMA idles on the padding, the layer is bound by its
+  // activation reads anyway
+  if (cin % tcw::KB != 0 || cout < 1 || p < 0 || p / 2 > 120) return false;
   int ah[2], aw[2];
   for (int r = 0; r < 2; ++r) {
     const int u0 = (p + r) & 1;

@@ -213,3 +213,24 @@ def test_pair_kernel_large_maps(n, p):
     got, path = run(x, k, p, "bf16", out_dtype=torch.float32)
     assert path == "tc-pair"
     assert np.array_equal(got, oracle.tconv_fused(x, k, p))
+
+
+@pytest.mark.parametrize("batch,n,cin,cout,p,act", [
+    (4, 32, 128, 3, 2, "tanh"),   # DCGAN / Art-GAN last layer (4x4, out = 2N)
+    (3, 32, 64, 3, 2, "tanh"),    # GP-GAN last layer
+    (2, 9, 128, 40, 1, None),     # 33..63 features: one 64-wide tile
+    (2, 6, 64, 17, 3, "relu"),
+])
+def test_pair_kernel_narrow_outputs(batch, n, cin, cout, p, act):
+    """cout < 64 with p_fused > 0 (no folded / scatter kernel): the pair kernel
+    with a 32- or 64-wide feature tile; integer data, exact."""
+    rng = np.random.default_rng(batch + n + cout)
+    x = rng.integers(-2, 3, (batch, n, n, cin)).astype(np.float32)
+    k = rng.integers(-1, 2, (4, 4, cin, cout)).astype(np.float32)
+    got, path = run(x, k, p, "bf16", act, out_dtype=torch.float32)
+    assert path == "tc-pair"
+    want = want_of(x, k, p, act)
+    if act == "tanh":
+        assert np.abs(got - want).max() <= 1e-6
+    else:
+        assert np.array_equal(got, want)
