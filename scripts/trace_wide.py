@@ -1,0 +1,34 @@
+"""Per-unit timeline of the CTA-pair kernel (SEGCONV_TC_TRACE=1): producer
+done (ev 0), MMA start/end (2/3), epilogue start (4), for CTA 0.
+python scripts/trace_wide.py B N CIN COUT K P"""
+import ctypes as C
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2209_03704_b200 import _capi as A  # noqa: E402
+from paper_2209_03704_b200 import segconv as sc  # noqa: E402
+
+b, n, cin, cout, k, p = (int(v) for v in sys.argv[1:7])
+x = torch.randn((b, n, n, cin), device="cuda").bfloat16()
+w = (torch.randn((k, k, cin, cout), device="cuda") * 0.02).bfloat16()
+g = sc.tconv_geometry(n, k, k, p)
+sks = sc.segregate(w, p)
+for _ in range(3):
+    sc.transpose_conv_fused(x, sks, g)
+torch.cuda.synchronize()
+sc.transpose_conv_fused(x, sks, g)
+torch.cuda.synchronize()
+buf = np.zeros(160 * 16 * 64, dtype=np.uint64)
+A.lib().segconv_debug_trace(buf.ctypes.data_as(C.c_void_p), buf.nbytes)
+tr = buf.reshape(160, 16, 64).astype(np.int64)
+t0 = tr[tr > 0].min()
+for cta in (0, 2):
+    print("CTA", cta, sc.last_path())
+    for u in range(20):
+        row = tr[cta, :6, u]
+        if not row.any():
+            break
+        print(f"  unit {u}: " + " ".join(f"ev{e}={(v - t0) / 1000:7.2f}" for e, v in enumerate(row) if v))
