@@ -52,9 +52,21 @@ static bool ring_panels_apply(int kh, int kw, int cin, int cout, int p_orig, int
   return kh == 5 && kw == 5 && cout == 3 && p_orig == 0 && cin % 32 == 0 && cin <= 256 &&
          panel_dtype == SEGCONV_F16_SPLIT;
 }
+// the pixel-scatter tile kernel's weight image rides on the folded panels (p = 0)
 static bool tile_panels_apply(int kh, int kw, int cin, int cout, int p_orig, int panel_dtype) {
-  return kh == 3 && kw == 3 && cout == 3 && p_orig == 0 && cin % 64 == 0 && cin <= 512 &&
+  return (kh == 3 || kh == 4) && kw == kh && cout == 3 && p_orig == 0 && cin % 64 == 0 && cin <= 512 &&
          panel_dtype == SEGCONV_BF16;
+}
+// ... and on the K-major panels of the 4x4, even-p (out = 2N) 3-channel layers
+static bool tile_kmajor_tail(int kh, int kw, int cin, int cout, int p_orig, int panel_dtype) {
+  return kh == 4 && kw == 4 && cout == 3 && p_orig == 2 && cin % 64 == 0 &&
+         cin <= 512 && panel_dtype == SEGCONV_BF16;
+}
+// elements of the K-major panels that precede an appended tile image
+static int64_t kmajor_elems(const segconv_subkernels& s) {
+  int64_t e = 0;
+  for (int q = 0; q < 4; ++q) e += (int64_t)s.sub_kh[q] * s.sub_kw[q] * s.cin * s.cout_pad;
+  return e;
 }
 // elements of the folded image that precede an appended ring image
 static int64_t fold_image_elems(const segconv_subkernels& s) {
@@ -183,6 +195,8 @@ segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_
     taps += s.sub_kh[q] * s.sub_kw[q];
   }
   s.total_elems = off;
+  if (layout == SEGCONV_PANEL_KMAJOR && tile_kmajor_tail(kh, kw, cin, cout, p_orig, panel_dtype))
+    s.total_elems += (int64_t)(tile_image_bytes(kh, cin) / 2);
   if (layout == SEGCONV_PANEL_UMMA_FOLD) {
     s.n_tile = fold_cp(cout);
     s.k_block = fold_kb(s.math, cin);
@@ -197,7 +211,7 @@ segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_
       s.total_elems += (int64_t)(ring_image_bytes(cin) / 2);
     // bf16 3x3 -> 3-channel layers carry the small-image pixel-scatter image (tc_tile.cu)
     if (tile_panels_apply(kh, kw, cin, cout, p_orig, panel_dtype))
-      s.total_elems += (int64_t)(tile_image_bytes(cin) / 2);
+      s.total_elems += (int64_t)(tile_image_bytes(kh, cin) / 2);
     // split-fp16 layers with 4 classes x 32 features: compact weight image of
     // the TMEM-weight kernel (tc_fold_ts.cu), only the blocks that hold taps
     if (fold_ts_panels_apply(kh, kw, cin, cout, p_orig, panel_dtype))
@@ -299,7 +313,7 @@ segconv_status segconv_segregate(const void* d_kernel, segconv_dtype kernel_dtyp
                                            (cudaStream_t)stream),
                          "segregate[ring]");
       else
-        st = cuda_status(launch_tile_image(d_kernel, kernel_dtype, sks->cin, cls, tail,
+        st = cuda_status(launch_tile_image(d_kernel, kernel_dtype, sks->source_kh, sks->cin, cls, tail,
                                            (cudaStream_t)stream),
                          "segregate[tile]");
     }
@@ -316,11 +330,21 @@ segconv_status segconv_segregate(const void* d_kernel, segconv_dtype kernel_dtyp
                                              d_panels, (cudaStream_t)stream),
                        "segregate[umma]");
   }
-  return cuda_status(launch_segregate(d_kernel, kernel_dtype, sks->source_kh, sks->source_kw,
-                                      sks->cin, sks->cout, sks->cout_pad, sks->layout, cls,
-                                      d_panels, sks->dtype, sks->total_elems,
-                                      (cudaStream_t)stream),
-                     "segregate");
+  const int64_t main_elems = sks->layout == SEGCONV_PANEL_KMAJOR ? kmajor_elems(*sks) : sks->total_elems;
+  segconv_status st = cuda_status(launch_segregate(d_kernel, kernel_dtype, sks->source_kh, sks->source_kw,
+                                                   sks->cin, sks->cout, sks->cout_pad, sks->layout, cls,
+                                                   d_panels, sks->dtype, main_elems, (cudaStream_t)stream),
+                                  "segregate");
+  if (st == SEGCONV_OK && sks->layout == SEGCONV_PANEL_KMAJOR && sks->total_elems > main_elems) {
+    for (int q = 0; q < 4; ++q) {  // the tile image reads the class input offsets
+      cls.off_r[q] = sks->off_r[q];
+      cls.off_c[q] = sks->off_c[q];
+    }
+    st = cuda_status(launch_tile_image(d_kernel, kernel_dtype, sks->source_kh, sks->cin, cls,
+                                       (uint16_t*)d_panels + main_elems, (cudaStream_t)stream),
+                     "segregate[tile]");
+  }
+  return st;
 }
 
 segconv_math segconv_select_math(segconv_dtype x_dtype, segconv_dtype panel_dtype, int cin,
@@ -422,6 +446,11 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
         if ((int)math != sks->math)
           return fail(SEGCONV_E_CONTRACT, "panels were laid out for math %d, not %d", sks->math,
                       (int)math);
+        if (sks->total_elems > kmajor_elems(*sks) && tc_tile_supported(pr, math)) {
+          g_path = "tc-tile";  // 3-channel 4x4 / even-p layer: pixel scatter reads x once
+          return cuda_status(launch_tc_tile(pr, (const uint16_t*)d_panels + kmajor_elems(*sks), s),
+                             "transpose_conv_fused[tcgen05 tile]");
+        }
         if (!tc_wide_supported(pr, math))
           return fail(SEGCONV_E_UNSUPPORTED,
                       "CTA-pair tensor-core path needs bf16 activations, cin %% 64 == 0 and at most 25 "

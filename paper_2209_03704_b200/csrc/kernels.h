@@ -88,9 +88,10 @@ size_t ring_image_bytes(int cin);
 // pixel-scatter kernel for 3x3 -> 3-channel bf16 layers on small images (tc_tile.cu)
 bool tc_tile_supported(const FusedProblem& pr, int math);
 cudaError_t launch_tc_tile(const FusedProblem& pr, const void* img, cudaStream_t s);
-cudaError_t launch_tile_image(const void* k, int k_dtype, int cin, const SegClasses& cls, void* out,
+bool tile_applies(int kh, int kw, int p, int n, int cin, int cout);
+cudaError_t launch_tile_image(const void* k, int k_dtype, int kh, int cin, const SegClasses& cls, void* out,
                               cudaStream_t s);
-size_t tile_image_bytes(int cin);
+size_t tile_image_bytes(int kh, int cin);
 // TMEM-weights variant for split-fp16 layers with cout in (16, 32] (tc_fold_ts.cu)
 cudaError_t launch_tc_fold_ts(const FusedProblem& pr, const void* img, cudaStream_t s);
 bool fold_ts_panels_apply(int kh, int kw, int cin, int cout, int p_orig, int panel_dtype);

@@ -4,14 +4,16 @@
 
 namespace segconv_b200 {
 
-// Column layout of D (= rows of the weight image), p_orig = 0: per-axis
-// parity r has act(r) = (KH - r + 1) / 2 taps starting at offset r, so the
-// union window is U = act(0) rows / cols.  Columns: for dy, a group padded
-// to a multiple of 16; inside it (q, dx, f) with f fastest.
+// Column layout of D (= rows of the weight image) for even p_orig (p = 0 as
+// written; an even p shifts every input offset by -p/2, which the kernels
+// apply): per-axis parity r has act(r) = (KH - r + 1) / 2 taps starting at
+// offset r, so the union window is U = max_r (r + act(r)) rows / cols (KH + 1)
+// / 2 for odd KH, KH / 2 + 1 for even KH).  Columns: for dy, a group padded to
+// a multiple of 16; inside it (q, dx, f) with f fastest.
 template <int KH, int COUT>
 struct ScatterLayout {
   static constexpr int act(int r) { return (KH - r + 1) / 2; }
-  static constexpr int U = (KH + 1) / 2;
+  static constexpr int U = act(0) > 1 + act(1) ? act(0) : 1 + act(1);
   static constexpr bool has(int q, int dy, int dx) {
     return dy >= (q >> 1) && dy < (q >> 1) + act(q >> 1) && dx >= (q & 1) &&
            dx < (q & 1) + act(q & 1);

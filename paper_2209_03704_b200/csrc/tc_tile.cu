@@ -2,15 +2,20 @@
 // (BASELINE C5 layer d: 1024 x 11^2 x 128 -> 19^2 x 3, n = 3, tanh).
 //
 // Replaces reference proj/include/segconv/fused_tconv.hpp:42-60 and the dot
-// loop of reference_ops.hpp:31-79 for these layers.
+// loop of reference_ops.hpp:31-79 for these layers; also the 4x4, p = 2
+// (out = 2N) 3-channel last layers of GAN generators (reference
+// analysis.hpp:96-114).
 //
 // Pixel scatter, as tc_ring.cu: one MMA per K step computes, for 128
 // consecutive input pixels p (the NHWC order runs across rows and images),
 //   D[p, (dy, q, dx, f)] = sum_ch X[p, ch] * W_q[dy - off_r][dx - off_c][ch][f]
 // (27 useful columns of N = 48 for n = 3, cout = 3), and the epilogue sums
 // the shifts: anchor m of the tile takes D[m + dy * n + dx, (dy, q, dx, f)].
-// Images here are small (the largest shift, n + 1, is < 64 pixels), so one
-// 128-pixel tile yields 128 - (n + 1) anchors; tiles overlap by n + 1 pixels.
+// Images here are small, so one 128-pixel tile yields 128 - (U - 1)(n + 1)
+// anchors; tiles overlap by (U - 1)(n + 1) pixels.  With an even p > 0 every
+// input offset moves by -p/2 (padding): the tile starts p/2 (n + 1) pixels
+// before its first anchor (a TMA box starting before pixel 0 is zero-filled)
+// and contributions from outside the image are masked.
 // The D tile goes TMEM -> registers -> a padded SMEM tile, and each epilogue
 // thread gathers its anchor's 4 x cout sums from it.  bf16 activations land by
 // TMA (box {64 channels, 128 pixels}, 128-byte swizzle) and are the MMA A
@@ -48,7 +53,9 @@ struct Params {
   unsigned epi;
   int batch, n, cin, cout, out_h, out_w;
   long long Mv, tiles;
-  int step;  // anchors per tile = TILE - (n + 1)
+  int step;  // anchors per tile = TILE - (U - 1) * (n + 1)
+  int pf;    // p_orig / 2: input offsets shift by -pf
+  int back;  // pf * (n + 1): pixels of the tile before its first anchor
   int rows[4], cols[4];
   int stage_bytes, stages, w_bytes;
   unsigned long long* trace;
@@ -125,7 +132,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t ph = 0;
       int k = 0;
       for (long long t = blockIdx.x; t < p.tiles; t += gridDim.x, ++k) {
-        const int p0 = (int)(t * p.step);
+        const int p0 = (int)(t * p.step) - p.back;  // may start before pixel 0: zero fill
         trace_ev(p, 0, k);
         for (int kb = 0; kb < NKB; ++kb) {
           mbar_wait(&a_empty[st], ph ^ 1);
@@ -199,13 +206,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         tc_fence_after();
         if (threadIdx.x == 0) trace_ev(p, 4, k);
         float v[32];
-        tmem_ld32(lane_base + (uint32_t)(acc * N), v);
 #pragma unroll
-        for (int c = 0; c < 32; ++c) dtile[m * TP + c] = v[c];
-        if constexpr (N > 32) {
-          tmem_ld16(lane_base + (uint32_t)(acc * N + 32), v);
+        for (int c0 = 0; c0 + 32 <= N; c0 += 32) {
+          tmem_ld32(lane_base + (uint32_t)(acc * N + c0), v);
 #pragma unroll
-          for (int c = 0; c < N - 32 && c < 16; ++c) dtile[m * TP + 32 + c] = v[c];
+          for (int c = 0; c < 32; ++c) dtile[m * TP + c0 + c] = v[c];
+        }
+        if constexpr (N % 32 != 0) {  // N is a multiple of 16
+          tmem_ld16(lane_base + (uint32_t)(acc * N + N / 32 * 32), v);
+#pragma unroll
+          for (int c = 0; c < 16; ++c) dtile[m * TP + N / 32 * 32 + c] = v[c];
         }
         tc_fence_before();
         mbar_arrive(&acc_empty[acc]);  // D is in SMEM now; the MMA may reuse the buffer
@@ -215,7 +225,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         pacc ^= 1;
       }
       named_bar(1, 256);
-      const long long g = t * p.step + m;  // this thread's anchor
+      const long long g = t * p.step + m;  // this thread's anchor, tile pixel p.back + m
       if (m < p.step && g < p.Mv && !(p.debug & 1)) {
         const int b = (int)(g / img);
         const int rem = (int)(g - (long long)b * img);
@@ -237,7 +247,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const int col0 = L::col_in_group(dy, 0 + c, dx, f), col2 = L::col_in_group(dy, 2 + c, dx, f);
                 const int col = rr ? col2 : col0;
                 if ((rr ? col2 : col0) < 0) continue;
-                s += dtile[(m + dy * p.n + dx) * TP + L::group_off(dy) + col];
+                const int ii = i + dy - p.pf, jj = j + dx - p.pf;  // input pixel (padding: zero)
+                if (ii < 0 || ii >= p.n || jj < 0 || jj >= p.n) continue;
+                s += dtile[(p.back + m + (dy - p.pf) * p.n + (dx - p.pf)) * TP + L::group_off(dy) + col];
               }
             s += bias[f];
             if (ACT == 1) s = fmaxf(s, 0.0f);
@@ -322,11 +334,28 @@ __global__ void tile_image_kernel(const TK* __restrict__ k, int cin, SegClasses 
 }  // namespace tct
 
 // ------------------------------------------------------------ host side
-size_t tile_image_bytes(int cin) { return (size_t)(cin / 8) * ScatterLayout<3, 3>::N * 16; }
+template <int KH>
+static constexpr int tile_n() {
+  return ScatterLayout<KH, 3>::N;
+}
+size_t tile_image_bytes(int kh, int cin) {
+  return (size_t)(cin / 8) * (kh == 4 ? tile_n<4>() : tile_n<3>()) * 16;
+}
+
+// 3x3 at p = 0 (C5 d) or 4x4 at an even p (GAN last layers, p = 2): cout = 3,
+// bf16, a tile of 128 pixels that still leaves >= 32 anchors
+bool tile_applies(int kh, int kw, int p, int n, int cin, int cout) {
+  if (kh != kw || cout != 3 || cin % tct::KB != 0 || cin > 512 || n < 1) return false;
+  if (!((kh == 3 && p == 0) || (kh == 4 && (p == 0 || p == 2)))) return false;
+  // anchors are the n x n input positions: every class grid must fit in them
+  // (out = 2n + 2p - kh, rows of class 0 = (out + 1) / 2)
+  if ((2 * n + 2 * p - kh + 1) / 2 > n) return false;
+  const int U = kh == 4 ? ScatterLayout<4, 3>::U : ScatterLayout<3, 3>::U;
+  return tct::TILE - (U - 1) * (n + 1) >= 32;
+}
 
 static bool tile_shape(const FusedProblem& pr) {
-  return pr.kh == 3 && pr.kw == 3 && pr.cout == 3 && pr.p == 0 && pr.pf == 0 &&
-         pr.cin % tct::KB == 0 && pr.cin <= 512 && pr.n + 1 <= 64 && pr.x_dtype == SEGCONV_BF16 &&
+  return tile_applies(pr.kh, pr.kw, pr.p, pr.n, pr.cin, pr.cout) && pr.x_dtype == SEGCONV_BF16 &&
          (pr.y_dtype == SEGCONV_BF16 || pr.y_dtype == SEGCONV_F32);
 }
 
@@ -335,25 +364,31 @@ bool tc_tile_supported(const FusedProblem& pr, int math) {
   return tile_shape(pr);
 }
 
-cudaError_t launch_tile_image(const void* k, int k_dtype, int cin, const SegClasses& cls, void* out,
-                              cudaStream_t s) {
-  const long long total = (long long)(cin / 8) * ScatterLayout<3, 3>::N;
+template <int KH>
+static cudaError_t tile_image_t(const void* k, int k_dtype, int cin, const SegClasses& cls, void* out,
+                                cudaStream_t s) {
+  const long long total = (long long)(cin / 8) * ScatterLayout<KH, 3>::N;
   const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 1024);
   if (k_dtype == SEGCONV_BF16)
-    tct::tile_image_kernel<3, 3, __nv_bfloat16><<<blocks, 256, 0, s>>>(
+    tct::tile_image_kernel<KH, 3, __nv_bfloat16><<<blocks, 256, 0, s>>>(
         (const __nv_bfloat16*)k, cin, cls, (__nv_bfloat16*)out);
   else if (k_dtype == SEGCONV_F32)
-    tct::tile_image_kernel<3, 3, float><<<blocks, 256, 0, s>>>((const float*)k, cin, cls,
-                                                               (__nv_bfloat16*)out);
+    tct::tile_image_kernel<KH, 3, float><<<blocks, 256, 0, s>>>((const float*)k, cin, cls,
+                                                                (__nv_bfloat16*)out);
   else
     return cudaErrorNotSupported;
   note_launch();
   return cudaGetLastError();
 }
 
-cudaError_t launch_tc_tile(const FusedProblem& pr, const void* img, cudaStream_t s) {
-  if (!tile_shape(pr)) return cudaErrorNotSupported;
-  using L = ScatterLayout<3, 3>;
+cudaError_t launch_tile_image(const void* k, int k_dtype, int kh, int cin, const SegClasses& cls, void* out,
+                              cudaStream_t s) {
+  return kh == 4 ? tile_image_t<4>(k, k_dtype, cin, cls, out, s) : tile_image_t<3>(k, k_dtype, cin, cls, out, s);
+}
+
+template <int KH>
+static cudaError_t launch_tile_t(const FusedProblem& pr, const void* img, cudaStream_t s) {
+  using L = ScatterLayout<KH, 3>;
   tct::Params p{};
   p.panels = (const uint8_t*)img;
   p.y = pr.y;
@@ -370,11 +405,13 @@ cudaError_t launch_tc_tile(const FusedProblem& pr, const void* img, cudaStream_t
     p.cols[q] = pr.cls.cols[q];
   }
   p.Mv = (long long)pr.batch * pr.n * pr.n;
-  p.step = tct::TILE - (pr.n + 1);
+  p.pf = pr.p / 2;
+  p.back = p.pf * (pr.n + 1);
+  p.step = tct::TILE - (L::U - 1) * (pr.n + 1);
   p.tiles = (p.Mv + p.step - 1) / p.step;
   if (p.tiles == 0) return cudaSuccess;
   p.stage_bytes = tct::TILE * 128;
-  p.w_bytes = (int)tile_image_bytes(pr.cin);
+  p.w_bytes = (int)tile_image_bytes(KH, pr.cin);
   const int fixed = p.w_bytes + (tct::TILE * (L::N + 1) + 2) * 4 + (2 * tct::MAX_STAGES + 5) * 8 + 16;
   p.stages = std::min(tct::MAX_STAGES, (tct::SMEM_LIMIT - fixed) / p.stage_bytes);
   if (p.stages < 2) return cudaErrorNotSupported;
@@ -416,7 +453,7 @@ cudaError_t launch_tc_tile(const FusedProblem& pr, const void* img, cudaStream_t
   cudaError_t e = cudaSuccess;
 #define TILE_LAUNCH(A, YT)                                                                       \
   {                                                                                              \
-    auto kern = tct::tile_kernel<3, 3, A, YT>;                                                   \
+    auto kern = tct::tile_kernel<KH, 3, A, YT>;                                                  \
     static bool cfg = false;                                                                     \
     if (!cfg) {                                                                                  \
       e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tct::SMEM_LIMIT); \
@@ -454,6 +491,11 @@ cudaError_t launch_tc_tile(const FusedProblem& pr, const void* img, cudaStream_t
 #undef TILE_LAUNCH
   note_launch();
   return cudaGetLastError();
+}
+
+cudaError_t launch_tc_tile(const FusedProblem& pr, const void* img, cudaStream_t s) {
+  if (!tile_shape(pr)) return cudaErrorNotSupported;
+  return pr.kh == 4 ? launch_tile_t<4>(pr, img, s) : launch_tile_t<3>(pr, img, s);
 }
 
 }  // namespace segconv_b200

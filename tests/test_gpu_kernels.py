@@ -215,22 +215,48 @@ def test_pair_kernel_large_maps(n, p):
     assert np.array_equal(got, oracle.tconv_fused(x, k, p))
 
 
-@pytest.mark.parametrize("batch,n,cin,cout,p,act", [
-    (4, 32, 128, 3, 2, "tanh"),   # DCGAN / Art-GAN last layer (4x4, out = 2N)
-    (3, 32, 64, 3, 2, "tanh"),    # GP-GAN last layer
-    (2, 9, 128, 40, 1, None),     # 33..63 features: one 64-wide tile
-    (2, 6, 64, 17, 3, "relu"),
+@pytest.mark.parametrize("batch,n,cin,cout,p,act,path", [
+    (4, 32, 128, 3, 2, "tanh", "tc-tile"),   # DCGAN / Art-GAN last layer (4x4, out = 2N)
+    (3, 32, 64, 3, 2, "tanh", "tc-tile"),    # GP-GAN last layer
+    (2, 50, 64, 3, 2, None, "tc-pair"),      # too wide for a 128-pixel scatter tile
+    (2, 9, 128, 40, 1, None, "tc-pair"),     # 33..63 features: one 64-wide tile
+    (2, 6, 64, 17, 3, "relu", "tc-pair"),
 ])
-def test_pair_kernel_narrow_outputs(batch, n, cin, cout, p, act):
-    """cout < 64 with p_fused > 0 (no folded / scatter kernel): the pair kernel
-    with a 32- or 64-wide feature tile; integer data, exact."""
+def test_narrow_outputs_at_padding(batch, n, cin, cout, p, act, path):
+    """cout < 64 with p_fused > 0: the 3-channel 4x4 layers take the pixel-scatter
+    tile kernel (input offsets shifted by -p/2, out-of-image taps masked), others
+    the pair kernel with a 32- or 64-wide feature tile; integer data, exact."""
     rng = np.random.default_rng(batch + n + cout)
     x = rng.integers(-2, 3, (batch, n, n, cin)).astype(np.float32)
     k = rng.integers(-1, 2, (4, 4, cin, cout)).astype(np.float32)
-    got, path = run(x, k, p, "bf16", act, out_dtype=torch.float32)
-    assert path == "tc-pair"
+    got, ran = run(x, k, p, "bf16", act, out_dtype=torch.float32)
+    assert ran == path
     want = want_of(x, k, p, act)
     if act == "tanh":
         assert np.abs(got - want).max() <= 1e-6
     else:
         assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("batch,n,cin,p,odt", [(5, 8, 64, 0, torch.float32), (3, 16, 128, 2, torch.bfloat16),
+                                               (2, 21, 192, 2, torch.float32), (7, 5, 64, 2, torch.float32)])
+def test_tile_kernel_4x4(batch, n, cin, p, odt):
+    """4x4 -> 3 on the tile kernel: p = 0 (folded panels) and even p > 0 (K-major
+    panels with the tile image appended); bf16 real data, tolerance as C5 d."""
+    rng = np.random.default_rng(batch * 3 + n + p)
+    x = oracle.bf16_round(rng.standard_normal((batch, n, n, cin)).astype(np.float32))
+    k = oracle.bf16_round((rng.standard_normal((4, 4, cin, 3)) * 0.02).astype(np.float32))
+    got, path = run(x, k, p, "bf16", "tanh", out_dtype=odt)
+    assert path == "tc-tile"
+    tol = 1e-4 if odt == torch.float32 else TOL_TC
+    assert scaled_err(got, want_of(x, k, p, "tanh")) <= tol
+
+
+def test_tile_kernel_not_used_where_class_grids_exceed_the_input():
+    """4x4 at p = 4: out = 2n + 4, class grids of n + 2 rows -- not n x n anchors."""
+    rng = np.random.default_rng(44)
+    x = rng.integers(-2, 3, (2, 10, 10, 64)).astype(np.float32)
+    k = rng.integers(-1, 2, (4, 4, 64, 3)).astype(np.float32)
+    got, path = run(x, k, 4, "bf16", out_dtype=torch.float32)
+    assert path != "tc-tile"
+    assert np.array_equal(got, oracle.tconv_fused(x, k, 4))
