@@ -235,6 +235,12 @@ segconv_math segconv_select_math(segconv_dtype x_dtype, segconv_dtype panel_dtyp
  * (batch, up_h, up_w, cin) zero-inserted, padded map. */
 segconv_status segconv_upsample2x_pad(const void* d_x, segconv_dtype dtype, int batch, int n_in,
                                       int cin, int p_orig, void* d_up, void* stream);
+/* reference netdemo/layers.hpp:66-73 (Upsample2x::backward) composed with the
+ * crop of the padding: d_gx (batch, n_in, n_in, cin) = d_gy (batch, up, up,
+ * cin) at (2i + p_orig, 2j + p_orig), up = 2 n_in - 1 + 2 p_orig. */
+segconv_status segconv_upsample2x_pad_backward(const void* d_gy, segconv_dtype dtype, int batch,
+                                               int n_in, int cin, int p_orig, void* d_gx,
+                                               void* stream);
 /* reference reference_ops.hpp:86-108 (conv2d_valid), batched over `batch`
  * (h, w, cin) maps; output (batch, h-kh+1, w-kw+1, cout). */
 segconv_status segconv_conv2d_valid(const void* d_src, segconv_dtype dtype, int batch, int h,

@@ -73,6 +73,7 @@ SIGNATURES = {
     "segconv_load_tensor_batch": (_i, [C.POINTER(C.c_char_p), _i, _i, _vp, _vp, _vp]),
     "segconv_last_error_offset": (_sz, []),
     "segconv_upsample2x_pad": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _vp]),
+    "segconv_upsample2x_pad_backward": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _vp]),
     "segconv_conv2d_valid": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _i, _vp, _u, _vp, _vp]),
     "segconv_conv2d_valid_backward": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _vp,
                                            _vp, _i, _vp]),

@@ -678,6 +678,20 @@ segconv_status segconv_upsample2x_pad(const void* d_x, segconv_dtype dtype, int 
                      "upsample2x_pad");
 }
 
+// reference netdemo/layers.hpp:66-73 (Upsample2x::backward) after the pad crop
+segconv_status segconv_upsample2x_pad_backward(const void* d_gy, segconv_dtype dtype, int batch, int n_in,
+                                               int cin, int p_orig, void* d_gx, void* stream) {
+  if (batch < 0 || n_in < 1 || cin < 1) return fail(SEGCONV_E_SHAPE, "tensor dims must be positive");
+  if (p_orig < 0) return fail(SEGCONV_E_CONTRACT, "pad factor must be non-negative");
+  if (!valid_dtype(dtype)) return fail(SEGCONV_E_CONTRACT, "unknown dtype");
+  if (batch == 0) return SEGCONV_OK;
+  if (!d_gy || !d_gx) return fail(SEGCONV_E_CONTRACT, "null data pointer");
+  g_path = "simt-gather";
+  return cuda_status(launch_upsample_pad_backward(d_gy, dtype, batch, n_in, cin, p_orig, d_gx,
+                                                  (cudaStream_t)stream),
+                     "upsample2x_pad_backward");
+}
+
 // reference reference_ops.hpp:86-102
 segconv_status segconv_conv2d_valid(const void* d_src, segconv_dtype dtype, int batch, int h, int w,
                                     int cin, const void* d_kernel, int kh, int kw, int cout,

@@ -57,6 +57,45 @@ cudaError_t launch_upsample_pad(const void* x, int dtype, int batch, int n, int 
   return cudaGetLastError();
 }
 
+// Backward of pad(upsample2x(x), p): gx(i, j) = g(2i + p, 2j + p) -- the
+// reference Upsample2x::backward (netdemo/layers.hpp:66-73) after the crop of
+// the padding (tensor.hpp:224-232).
+template <typename T>
+__global__ void upsample_pad_backward_kernel(const T* __restrict__ g, int batch, int n, int cin, int p,
+                                             T* __restrict__ gx) {
+  const long long U = 2LL * n - 1 + 2LL * p;
+  const long long total = (long long)batch * n * n * cin;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int ch = (int)(e % cin);
+    long long t = e / cin;
+    const int j = (int)(t % n);
+    t /= n;
+    const int i = (int)(t % n);
+    const long long b = t / n;
+    gx[e] = g[((b * U + 2 * i + p) * U + 2 * j + p) * cin + ch];
+  }
+}
+
+cudaError_t launch_upsample_pad_backward(const void* g, int dtype, int batch, int n, int cin, int p, void* gx,
+                                         cudaStream_t s) {
+  const long long total = (long long)batch * n * n * cin;
+  if (total == 0) return cudaSuccess;
+  const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 148LL * 64);
+  if (dtype == SEGCONV_F32)
+    upsample_pad_backward_kernel<float><<<blocks, 256, 0, s>>>((const float*)g, batch, n, cin, p, (float*)gx);
+  else if (dtype == SEGCONV_F64)
+    upsample_pad_backward_kernel<double><<<blocks, 256, 0, s>>>((const double*)g, batch, n, cin, p,
+                                                                (double*)gx);
+  else if (dtype == SEGCONV_BF16)
+    upsample_pad_backward_kernel<__nv_bfloat16><<<blocks, 256, 0, s>>>(
+        (const __nv_bfloat16*)g, batch, n, cin, p, (__nv_bfloat16*)gx);
+  else
+    return cudaErrorInvalidValue;
+  note_launch();
+  return cudaGetLastError();
+}
+
 // Generic valid correlation: one thread per output element (any shape/dtype).
 template <typename T, typename ACC>
 __global__ void __launch_bounds__(256)

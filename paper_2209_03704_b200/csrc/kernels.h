@@ -123,6 +123,8 @@ const unsigned long long* tc_trace_ptr();
 unsigned long long* tc_trace_buffer();
 
 // Conventional path (conventional.cu).
+cudaError_t launch_upsample_pad_backward(const void* g, int dtype, int batch, int n, int cin, int p, void* gx,
+                                         cudaStream_t s);
 cudaError_t launch_upsample_pad(const void* x, int dtype, int batch, int n, int cin, int p,
                                 void* up, cudaStream_t s);
 cudaError_t launch_conv2d_valid(const void* src, int dtype, int batch, int h, int w, int cin,

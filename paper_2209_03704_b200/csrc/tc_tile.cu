@@ -227,8 +227,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       named_bar(1, 256);
       const long long g = t * p.step + m;  // this thread's anchor, tile pixel p.back + m
       if (m < p.step && g < p.Mv && !(p.debug & 1)) {
-        const int b = (int)(g / img);
-        const int rem = (int)(g - (long long)b * img);
+        // 32-bit index math (Mv < 2^31 is checked on the host)
+        const unsigned gu = (unsigned)g;
+        const int b = (int)(gu / (unsigned)img);
+        const int rem = (int)(gu - (unsigned)b * (unsigned)img);
         const int i = rem / p.n, j = rem - (rem / p.n) * p.n;
         float out[2][COUT];
         bool okc[2];
@@ -405,6 +407,7 @@ static cudaError_t launch_tile_t(const FusedProblem& pr, const void* img, cudaSt
     p.cols[q] = pr.cls.cols[q];
   }
   p.Mv = (long long)pr.batch * pr.n * pr.n;
+  if (p.Mv >= (1LL << 31)) return cudaErrorNotSupported;
   p.pf = pr.p / 2;
   p.back = p.pf * (pr.n + 1);
   p.step = tct::TILE - (L::U - 1) * (pr.n + 1);

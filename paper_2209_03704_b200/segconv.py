@@ -32,7 +32,7 @@ __all__ = [
     "count_ops_fused", "select_math", "launch_count", "last_path", "MATHS",
     "transpose_conv_fused_backward", "FusedTConv", "TransposeConvFused", "IoError", "ParseError",
     "TensorFileInfo", "peek_tensor_file", "load_tensor", "save_tensor", "load_tensor_batch",
-    "conv2d_valid_backward",
+    "conv2d_valid_backward", "upsample2x_pad_backward",
 ]
 
 
@@ -669,6 +669,21 @@ def upsample2x_pad(x: torch.Tensor, p: int) -> torch.Tensor:
     if host:
         up = up.cpu()
     return up[0] if squeeze else up
+
+
+def upsample2x_pad_backward(grad_up: torch.Tensor, n_in: int, p: int) -> torch.Tensor:
+    """Gradient of upsample2x_pad (reference netdemo/layers.hpp:66-73 after the pad
+    crop): the (B, up, up, c) gradient sampled at (2i + p, 2j + p)."""
+    gb, squeeze = _as_batch(grad_up)
+    dev = _device()
+    gd = gb.to(dev).contiguous()
+    b, U, U2, c = (int(v) for v in gd.shape)
+    if U != U2 or U != 2 * int(n_in) - 1 + 2 * int(p):
+        raise ContractError(f"upsampled gradient is {U}x{U2}, expected {2 * n_in - 1 + 2 * p}")
+    gx = torch.empty((b, int(n_in), int(n_in), c), dtype=gd.dtype, device=dev)
+    _check(A.lib().segconv_upsample2x_pad_backward(gd.data_ptr(), _dtype_code(gd), b, int(n_in), c,
+                                                   int(p), gx.data_ptr(), _stream()))
+    return gx[0] if squeeze else gx
 
 
 def conv2d_valid(src: torch.Tensor, k: torch.Tensor, *, bias=None, activation=None) -> torch.Tensor:

@@ -123,3 +123,23 @@ def test_backward_bf16_tensor_core_int_exact(b, h, w, cin, kh, kw, cout):
     assert sc.last_path() == "bwd:tc-pair+" + wpath
     np.testing.assert_array_equal(gx.float().cpu().numpy(), oracle.bf16_round(wx))
     np.testing.assert_array_equal(gk.cpu().numpy(), wk)
+
+
+def test_conventional_training_path_matches_the_fused_backward():
+    """The reference's conventional model (Upsample2x -> pad -> ConvValid) trained on
+    the GPU: upsample2x_pad_backward(conv2d_valid_backward(...)) gives the same input
+    and kernel gradients as the fused layer's backward (exact, integer data)."""
+    rng = np.random.default_rng(21)
+    for (n, cin, cout, k, p) in [(6, 8, 5, 4, 2), (5, 3, 2, 3, 1), (7, 4, 4, 5, 0)]:
+        x = rng.integers(-3, 4, (2, n, n, cin)).astype(np.float32)
+        kk = rng.integers(-2, 3, (k, k, cin, cout)).astype(np.float32)
+        g = oracle.geometry(n, k, k, p)
+        gy = rng.integers(-2, 3, (2, g.out_h, g.out_w, cout)).astype(np.float32)
+        t = lambda a: torch.from_numpy(a).cuda()  # noqa: E731
+        up = sc.upsample2x_pad(t(x), p)
+        gup, gk = sc.conv2d_valid_backward(up, t(kk), t(gy), math="exact")
+        gx = sc.upsample2x_pad_backward(gup, n, p)
+        assert sc.last_path() == "simt-gather"
+        wx, wk = oracle.tconv_backward(x, kk, p, gy)
+        np.testing.assert_array_equal(gx.cpu().numpy(), wx)
+        np.testing.assert_array_equal(gk.cpu().numpy(), wk)
