@@ -32,7 +32,7 @@ __all__ = [
     "count_ops_fused", "select_math", "launch_count", "last_path", "MATHS",
     "transpose_conv_fused_backward", "FusedTConv", "TransposeConvFused", "IoError", "ParseError",
     "TensorFileInfo", "peek_tensor_file", "load_tensor", "save_tensor", "load_tensor_batch",
-    "conv2d_valid_backward", "upsample2x_pad_backward",
+    "conv2d_valid_backward", "upsample2x_pad_backward", "ConvValid", "Upsample2x",
 ]
 
 
@@ -508,6 +508,63 @@ class FusedTConv:
         if self.math in (None, "auto"):
             return None
         return "bf16" if self.math in ("bf16",) else ("exact" if self.math == "exact" else "ffma")
+
+
+class ConvValid:
+    """Trainable valid correlation -- the reference's net::ConvValid<T>
+    (netdemo/layers.hpp:84-137) on the GPU, batched; same conventions as
+    FusedTConv."""
+
+    def __init__(self, kernel: torch.Tensor, *, math: Optional[str] = None):
+        self.kernel_ = kernel.to(_device()).contiguous()
+        self.math = math
+        acc_dt = torch.float64 if self.kernel_.dtype == torch.float64 else torch.float32
+        self.grad = torch.zeros(self.kernel_.shape, dtype=acc_dt, device=self.kernel_.device)
+        self._input = None
+
+    def name(self) -> str:
+        return "conv_valid"
+
+    def kernel(self) -> torch.Tensor:
+        return self.kernel_
+
+    def params(self):
+        return [(self.kernel_, self.grad)]
+
+    def zero_grads(self) -> None:
+        self.grad.zero_()
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        self._input = x.to(_device()).contiguous()
+        return conv2d_valid(self._input, self.kernel_)
+
+    def backward(self, g: torch.Tensor) -> torch.Tensor:
+        if self._input is None:
+            raise StateError("conv_valid: backward called before forward")
+        gx, _ = conv2d_valid_backward(self._input, self.kernel_, g, math=self.math,
+                                      grad_kernel=self.grad)
+        return gx
+
+
+class Upsample2x:
+    """The reference's net::Upsample2x<T> (netdemo/layers.hpp:54-79) with the
+    conventional path's padding p folded in (pad(upsample2x(x), p))."""
+
+    def __init__(self, p: int = 0):
+        self.p = int(p)
+        self._n = None
+
+    def name(self) -> str:
+        return "upsample2x"
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        self._n = int(x.shape[-2])
+        return upsample2x_pad(x, self.p)
+
+    def backward(self, g: torch.Tensor) -> torch.Tensor:
+        if self._n is None:
+            raise StateError("upsample2x: backward called before forward")
+        return upsample2x_pad_backward(g, self._n, self.p)
 
 
 class TransposeConvFused(torch.autograd.Function):

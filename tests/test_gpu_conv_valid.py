@@ -143,3 +143,25 @@ def test_conventional_training_path_matches_the_fused_backward():
         wx, wk = oracle.tconv_backward(x, kk, p, gy)
         np.testing.assert_array_equal(gx.cpu().numpy(), wx)
         np.testing.assert_array_equal(gk.cpu().numpy(), wk)
+
+
+def test_conventional_model_layers_train_like_the_fused_layer():
+    """Python mirrors of the reference netdemo layers: Upsample2x -> ConvValid
+    (the conventional model) and FusedTConv give identical outputs and gradients
+    on integer data (reference test_netdemo.cpp compares the two models)."""
+    rng = np.random.default_rng(33)
+    n, cin, cout, k, p = 6, 4, 3, 4, 2
+    x = torch.from_numpy(rng.integers(-3, 4, (2, n, n, cin)).astype(np.float64))
+    kk = torch.from_numpy(rng.integers(-2, 3, (k, k, cin, cout)).astype(np.float64))
+    up, conv = sc.Upsample2x(p), sc.ConvValid(kk, math="exact")
+    fused = sc.FusedTConv(kk, p, math="exact")
+    y1 = conv.forward(up.forward(x))
+    y2 = fused.forward(x)
+    assert torch.equal(y1, y2)
+    g = torch.from_numpy(rng.integers(-2, 3, tuple(y1.shape)).astype(np.float64)).cuda()
+    gx1 = up.backward(conv.backward(g))
+    gx2 = fused.backward(g)
+    assert torch.equal(gx1, gx2)
+    assert torch.equal(conv.grad, fused.grad)
+    with pytest.raises(sc.StateError):
+        sc.ConvValid(kk).backward(g)
