@@ -264,3 +264,30 @@ def test_kernel_grad_schedules(b, n, cin, cout, k, p, streamk, monkeypatch):
     acc = torch.ones_like(gk)
     sc.transpose_conv_fused_backward(t(x), t(kk), p, t(gy), input_grad=False, grad_kernel=acc)
     np.testing.assert_array_equal(acc.cpu().numpy(), wk + 1)
+
+
+@pytest.mark.parametrize("b,n,cin,cout,k", [(128, 16, 512, 256, 4),   # BASELINE C3, full size
+                                            (1024, 5, 512, 256, 3),   # C5 layer b, full batch
+                                            (1024, 7, 256, 128, 3)])  # C5 layer c, full batch
+def test_full_size_tensor_core_backward_equals_simt(b, n, cin, cout, k):
+    """At the BASELINE sizes (too large for the CPU oracle): on integer data every
+    partial sum is exact, so the tcgen05 input/kernel gradients must equal the
+    independent SIMT kernels' bit for bit (both round the same exact sums to bf16
+    for the input gradient); plus linearity in the output gradient."""
+    gen = torch.Generator(device="cuda").manual_seed(b + n)
+    ri = lambda shape, lo, hi: torch.randint(lo, hi + 1, shape, device="cuda", generator=gen).bfloat16()  # noqa: E731
+    g = sc.tconv_geometry(n, k, k, 0)
+    x = ri((b, n, n, cin), -3, 3)
+    kk = ri((k, k, cin, cout), -2, 2)
+    gy1 = ri((b, g.out_h, g.out_w, cout), -1, 1)
+    gy2 = ri((b, g.out_h, g.out_w, cout), -1, 1)
+    gx_tc, gk_tc = sc.transpose_conv_fused_backward(x, kk, 0, gy1, math="bf16")
+    assert sc.last_path() == "bwd:tc-pair+tc-pair"
+    gx_s, gk_s = sc.transpose_conv_fused_backward(x, kk, 0, gy1, math="ffma")
+    assert sc.last_path() == "bwd:simt-ffma+simt-ffma"
+    assert torch.equal(gx_tc, gx_s)
+    assert torch.equal(gk_tc, gk_s)
+    _, gk2 = sc.transpose_conv_fused_backward(x, kk, 0, gy2, math="bf16", input_grad=False)
+    _, gk12 = sc.transpose_conv_fused_backward(x, kk, 0, (gy1.float() + gy2.float()).bfloat16(), math="bf16",
+                                               input_grad=False)
+    assert torch.equal(gk12, gk_tc + gk2)  # linear in the output gradient, exact
