@@ -64,8 +64,9 @@ static bool tile_kmajor_tail(int kh, int kw, int cin, int cout, int p_orig, int 
 }
 // elements of the K-major panels that precede an appended tile image
 static int64_t kmajor_elems(const segconv_subkernels& s) {
+  const int kcin = s.dtype == SEGCONV_F16_SPLIT ? 2 * s.cin : s.cin;
   int64_t e = 0;
-  for (int q = 0; q < 4; ++q) e += (int64_t)s.sub_kh[q] * s.sub_kw[q] * s.cin * s.cout_pad;
+  for (int q = 0; q < 4; ++q) e += (int64_t)s.sub_kh[q] * s.sub_kw[q] * kcin * s.cout_pad;
   return e;
 }
 // elements of the folded image that precede an appended ring image
@@ -163,8 +164,8 @@ segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_
   const bool umma = layout == SEGCONV_PANEL_UMMA || layout == SEGCONV_PANEL_UMMA_FOLD;
   if (umma && panel_dtype != SEGCONV_BF16 && panel_dtype != SEGCONV_F16_SPLIT)
     return fail(SEGCONV_E_CONTRACT, "UMMA panels are bf16 or split-fp16");
-  if (!umma && panel_dtype == SEGCONV_F16_SPLIT)
-    return fail(SEGCONV_E_CONTRACT, "split-fp16 panels need a UMMA layout");
+  if (!umma && panel_dtype == SEGCONV_F16_SPLIT && layout != SEGCONV_PANEL_KMAJOR)
+    return fail(SEGCONV_E_CONTRACT, "split-fp16 panels need a UMMA or K-major layout");
   if (layout == SEGCONV_PANEL_UMMA_FOLD && cout > 32)
     return fail(SEGCONV_E_CONTRACT, "class-folded panels need cout <= 32");
   segconv_subkernels s{};
@@ -178,6 +179,9 @@ segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_
   s.layout = layout;
   s.math = umma ? (panel_dtype == SEGCONV_F16_SPLIT ? SEGCONV_MATH_F16X3 : SEGCONV_MATH_BF16)
                 : SEGCONV_MATH_FFMA;
+  // K-major split panels: rows (f, u, v) of [hi(cin) | lo(cin)] fp16
+  const int kcin = (layout == SEGCONV_PANEL_KMAJOR && panel_dtype == SEGCONV_F16_SPLIT) ? 2 * cin : cin;
+  if (kcin != cin) s.math = SEGCONV_MATH_F16X3;
   // K-major panels pad the MMA N dimension to a multiple of 16 rows.
   s.cout_pad = layout == SEGCONV_PANEL_KMAJOR ? (cout + 15) / 16 * 16 : cout;
   int64_t off = 0;
@@ -191,10 +195,11 @@ segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_
     s.off_r[q] = segconv_class_input_offset(p_orig, r);
     s.off_c[q] = segconv_class_input_offset(p_orig, c);
     s.sub_offset[q] = layout == SEGCONV_PANEL_UMMA ? taps : off;  // UMMA: first tap block
-    off += (int64_t)s.sub_kh[q] * s.sub_kw[q] * cin * s.cout_pad;
+    off += (int64_t)s.sub_kh[q] * s.sub_kw[q] * kcin * s.cout_pad;
     taps += s.sub_kh[q] * s.sub_kw[q];
   }
   s.total_elems = off;
+  if (kcin != cin) s.total_elems += 4;  // split panels: max |w| and the 2^-s scale (2 x 4 bytes)
   if (layout == SEGCONV_PANEL_KMAJOR && tile_kmajor_tail(kh, kw, cin, cout, p_orig, panel_dtype))
     s.total_elems += (int64_t)(tile_image_bytes(kh, cin) / 2);
   if (layout == SEGCONV_PANEL_UMMA_FOLD) {
@@ -246,6 +251,22 @@ segconv_status segconv_subkernels_for_math(int kh, int kw, int cin, int cout, in
     math = segconv_select_math(x_dtype, x_dtype, cin, cout, kh, kw);
     if ((math == SEGCONV_MATH_BF16 || math == SEGCONV_MATH_F16X3) && !tc_shape_ok(kh, kw, p_orig))
       math = SEGCONV_MATH_FFMA;
+    // Tensor-core accumulation adds each MMA's K = 16 partial sum to the fp32
+    // accumulator without round-to-nearest (measured: outputs drift toward zero
+    // by ~4e-8 relative per step).  The folded / scatter kernels take at most a
+    // few dozen steps; the pair kernel's split mode keeps the main product
+    // (xh.wh: taps * cin / 16 steps) in its own accumulator, and past ~200 such
+    // steps the drift exceeds the fp32 bar (1e-5): those layers run on FFMA
+    // unless f16x3 is asked for explicitly.
+    if (math == SEGCONV_MATH_F16X3 && !tc_fold_fits(math, kh, kw, p_orig, cin, cout)) {
+      int taps_max = 0;
+      for (int r = 0; r < 2; ++r)
+        for (int c = 0; c < 2; ++c)
+          taps_max = std::max(taps_max, segconv_active_tap_count(kh, p_orig, r) *
+                                            segconv_active_tap_count(kw, p_orig, c));
+      if (!tc_wide_fits(kh, kw, p_orig, cin, cout) || (long long)taps_max * cin / 16 > 192)
+        math = SEGCONV_MATH_FFMA;
+    }
   }
   switch (math) {
     case SEGCONV_MATH_FFMA:
@@ -265,6 +286,14 @@ segconv_status segconv_subkernels_for_math(int kh, int kw, int cin, int cout, in
         const segconv_status st = segconv_subkernels_init(kh, kw, cin, cout, p_orig, SEGCONV_BF16,
                                                           SEGCONV_PANEL_KMAJOR, out);
         if (st == SEGCONV_OK) out->math = SEGCONV_MATH_BF16;
+        return st;
+      }
+      // wide fp32 layers: the same kernel on split planes, K = [hi | lo] x 3 passes
+      if (!fold && math == SEGCONV_MATH_F16X3 && tc_wide_fits(kh, kw, p_orig, cin, cout) &&
+          getenv("SEGCONV_NO_WIDE") == nullptr && getenv("SEGCONV_NO_WIDE_SPLIT") == nullptr) {
+        const segconv_status st = segconv_subkernels_init(kh, kw, cin, cout, p_orig, SEGCONV_F16_SPLIT,
+                                                          SEGCONV_PANEL_KMAJOR, out);
+        if (st == SEGCONV_OK) out->math = SEGCONV_MATH_F16X3;
         return st;
       }
       return segconv_subkernels_init(
@@ -330,6 +359,11 @@ segconv_status segconv_segregate(const void* d_kernel, segconv_dtype kernel_dtyp
                                              d_panels, (cudaStream_t)stream),
                        "segregate[umma]");
   }
+  if (sks->layout == SEGCONV_PANEL_KMAJOR && sks->dtype == SEGCONV_F16_SPLIT)
+    return cuda_status(launch_segregate_kmajor_split(d_kernel, kernel_dtype, sks->source_kh, sks->source_kw,
+                                                     sks->cin, sks->cout, sks->cout_pad, cls, d_panels,
+                                                     kmajor_elems(*sks), (cudaStream_t)stream),
+                       "segregate[k-major split]");
   const int64_t main_elems = sks->layout == SEGCONV_PANEL_KMAJOR ? kmajor_elems(*sks) : sks->total_elems;
   segconv_status st = cuda_status(launch_segregate(d_kernel, kernel_dtype, sks->source_kh, sks->source_kw,
                                                    sks->cin, sks->cout, sks->cout_pad, sks->layout, cls,
@@ -442,7 +476,7 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
     }
     case SEGCONV_MATH_BF16:
     case SEGCONV_MATH_F16X3: {
-      if (sks->layout == SEGCONV_PANEL_KMAJOR && math == SEGCONV_MATH_BF16) {
+      if (sks->layout == SEGCONV_PANEL_KMAJOR && (math == SEGCONV_MATH_BF16 || math == SEGCONV_MATH_F16X3)) {
         if ((int)math != sks->math)
           return fail(SEGCONV_E_CONTRACT, "panels were laid out for math %d, not %d", sks->math,
                       (int)math);

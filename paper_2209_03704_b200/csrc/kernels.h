@@ -63,6 +63,9 @@ cudaError_t launch_wgrad_reduce_streamk(const float* ws, float* gk, int cin, int
 cudaError_t launch_wgrad_reduce(const float* ws, float* gk, long long ksz, int splits, int accumulate,
                                 cudaStream_t s);
 
+cudaError_t launch_segregate_kmajor_split(const void* k, int k_dtype, int kh, int kw, int cin, int cout,
+                                          int cout_pad, const SegClasses& cls, void* panels, long long total,
+                                          cudaStream_t s);
 cudaError_t launch_segregate(const void* k, int k_dtype, int kh, int kw, int cin, int cout,
                              int cout_pad, int layout, const SegClasses& cls, void* panels,
                              int p_dtype, long long total, cudaStream_t s);

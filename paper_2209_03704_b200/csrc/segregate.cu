@@ -72,6 +72,89 @@ static cudaError_t launch_seg(const void* k, int kh, int kw, int cin, int cout, 
   return cudaGetLastError();
 }
 
+// K-major split panels for the pair kernel's fp32 mode: per class rows
+// (f < cout_pad, u, v) of 2 cin fp16 values, [hi(w'[ch]) | lo(w'[ch])] with
+// w' = w * 2^s = hi + lo (hi = rn(w'), lo = rn(w' - hi)).  The power-of-two
+// scale puts max |w'| at 2^14, so the lo halves of small weights stay out of
+// the fp16 subnormal range; the kernel multiplies its sums by 2^-s (exact),
+// stored after the panels: tail[0] = max |w| (bits), tail[1] = 2^-s.
+template <typename TK>
+__global__ void kernel_amax(const TK* __restrict__ k, long long n, unsigned* __restrict__ amax_bits) {
+  float m = 0.0f;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf((float)to_acc(k[e])));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(amax_bits, __float_as_uint(m));  // non-negative floats order as uints
+}
+
+__device__ __forceinline__ int split_scale_exp(unsigned amax_bits) {
+  const float amax = __uint_as_float(amax_bits);
+  if (!(amax > 0.0f)) return 0;
+  int e;
+  frexpf(amax, &e);  // amax in [2^(e-1), 2^e)
+  const int s = 14 - e;
+  return s < -20 ? -20 : (s > 60 ? 60 : s);
+}
+
+template <typename TK>
+__global__ void segregate_kmajor_split_kernel(const TK* __restrict__ k, int kw, int cin, int cout, SegClasses cls,
+                                              __half* __restrict__ panels, long long total,
+                                              const unsigned* __restrict__ amax_bits, float* __restrict__ inv_scale) {
+  const int cin2 = 2 * cin;
+  const float scale = ldexpf(1.0f, split_scale_exp(*amax_bits));
+  if (blockIdx.x == 0 && threadIdx.x == 0) *inv_scale = 1.0f / scale;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    int q = 0;
+#pragma unroll
+    for (int t = 1; t < 4; ++t)
+      if (e >= cls.sub_offset[t]) q = t;
+    long long o = e - cls.sub_offset[q];
+    const int c2 = (int)(o % cin2);
+    o /= cin2;
+    const int v = (int)(o % cls.kw[q]);
+    o /= cls.kw[q];
+    const int u = (int)(o % cls.kh[q]);
+    const int f = (int)(o / cls.kh[q]);
+    const int ch = c2 < cin ? c2 : c2 - cin;
+    float w = 0.0f;
+    if (f < cout)
+      w = scale * (float)to_acc(k[(((long long)(cls.u0[q] + 2 * u) * kw + (cls.v0[q] + 2 * v)) * cin + ch) * cout + f]);
+    const __half hi = __float2half_rn(w);
+    panels[e] = c2 < cin ? hi : __float2half_rn(w - __half2float(hi));
+  }
+}
+
+cudaError_t launch_segregate_kmajor_split(const void* k, int k_dtype, int kh, int kw, int cin, int cout,
+                                          int cout_pad, const SegClasses& cls, void* panels, long long total,
+                                          cudaStream_t s) {
+  (void)cout_pad;
+  // tail after the panels (total is even): [max |w| bits][2^-s]
+  unsigned* tail = reinterpret_cast<unsigned*>(reinterpret_cast<__half*>(panels) + total);
+  cudaError_t e = cudaMemsetAsync(tail, 0, 8, s);
+  if (e != cudaSuccess) return e;
+  const long long nk = (long long)kh * kw * cin * cout;
+  const unsigned ab = (unsigned)std::max(1LL, std::min<long long>((nk + 255) / 256, 148LL * 8));
+  const long long blocks = std::max(1LL, std::min<long long>((total + 255) / 256, 148LL * 32));
+#define SPLIT_CASE(TK)                                                                                   \
+  kernel_amax<TK><<<ab, 256, 0, s>>>((const TK*)k, nk, tail);                                          \
+  segregate_kmajor_split_kernel<TK><<<(unsigned)blocks, 256, 0, s>>>((const TK*)k, kw, cin, cout, cls,  \
+                                                                     (__half*)panels, total, tail,      \
+                                                                     reinterpret_cast<float*>(tail + 1));
+  if (k_dtype == SEGCONV_F32) {
+    SPLIT_CASE(float)
+  } else if (k_dtype == SEGCONV_F64) {
+    SPLIT_CASE(double)
+  } else if (k_dtype == SEGCONV_BF16) {
+    SPLIT_CASE(__nv_bfloat16)
+  } else {
+    return cudaErrorInvalidValue;
+  }
+#undef SPLIT_CASE
+  note_launch(2);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_segregate(const void* k, int k_dtype, int kh, int kw, int cin, int cout,
                              int cout_pad, int layout, const SegClasses& cls, void* panels,
                              int p_dtype, long long total, cudaStream_t s) {

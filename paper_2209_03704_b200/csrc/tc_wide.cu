@@ -35,6 +35,7 @@
 // stores its anchor's features contiguously, bias / ReLU / tanh fused),
 // 4 TMA producer, 5 MMA issuer (leader CTA), 6 TMEM allocator.
 #include <cuda.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -84,6 +85,12 @@ struct Params {
   // wscale 2 (stride-2 im2col walk over gy), ostride 1, one class holding every tap.
   int wscale, wbase_r, wbase_c, ostride;
   int b_tap_last;  // B map coordinates (k, n, tap) instead of (k, tap, n)
+  // SPLIT (fp32 layers, f16x3 math): x and w are stored as fp16 [hi | lo]
+  // channel halves; the K loop runs three passes (xh.wh, xl.wh, xh.wl), pass
+  // 1 reading A channels + split_off and pass 2 B channels + split_off
+  int split, split_off;
+  uint32_t ab_fmt;  // MMA operand format: 1 bf16, 0 fp16
+  const float* split_inv_scale;  // SPLIT: the weights were scaled by 2^s; sums are multiplied by 2^-s
   // WGRAD (mode 1, launch_tc_bwd_weight): per unit (split s, tap t, 256-channel pair
   // tile ct, feature tile nt), D[ch, f] = sum over the split's 64-pixel chunks of
   // x[m, ch] * gy[b, 2i+p-U, 2j+p-V, f].  Both operands are MN-major (channels /
@@ -196,6 +203,10 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
 }
 __host__ __device__ constexpr uint32_t idesc_bf16_m256(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+// kind::f16 with operand format fmt (1 bf16, 0 fp16), fp32 accumulate, M = 256
+__host__ __device__ constexpr uint32_t idesc_f16_m256(uint32_t fmt, int n) {
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
 // both operands MN-major (a_major bit 15, b_major bit 16)
 __host__ __device__ constexpr uint32_t idesc_bf16_m256_mn(int n) {
@@ -418,13 +429,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const int ib = (int)(a0 / ((long long)R * C));
           const int rem = (int)(a0 - (long long)ib * R * C);
           const int i0 = rem / C, j0 = rem - (rem / C) * C;
+          for (int pass = 0; pass < (p.split ? 3 : 1); ++pass)
           for (int kb = 0; kb < p.nkb; ++kb)
             for (int t = 0; t < p.taps[q]; ++t) {
+              const int ca = kb * KB + (pass == 1 ? p.split_off : 0);  // A: xl on pass 1
+              const int cb = kb * KB + (pass == 2 ? p.split_off : 0);  // B: wl on pass 2
               mbar_wait(&a_empty[sa], pa ^ 1);
               const uint32_t af = mapa(smem_u32(&a_full[sa]), 0);
               if (rank == 0) mbar_arrive_expect_tx(&a_full[sa], 2 * 128 * 128);
               tma2_load_im2col(smem_u32(a_base + (size_t)sa * p.a_stage_bytes), &maps.xi[q],
-                               kb * KB, p.wscale * j0 + p.wbase_c, p.wscale * i0 + p.wbase_r, ib,
+                               ca, p.wscale * j0 + p.wbase_c, p.wscale * i0 + p.wbase_r, ib,
                                (uint16_t)p.tap_off_c[q][t], (uint16_t)p.tap_off_r[q][t], af);
               if (++sa == SA) {
                 sa = 0;
@@ -434,10 +448,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint32_t bf = mapa(smem_u32(&b_full[sb]), 0);
               if (rank == 0) mbar_arrive_expect_tx(&b_full[sb], 2 * b_tx);
               if (p.b_tap_last)
-                tma2_load_3d(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), &maps.w[q], kb * KB, f0,
+                tma2_load_3d(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), &maps.w[q], cb, f0,
                              t, bf);
               else
-                tma2_load_3d(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), &maps.w[q], kb * KB, t,
+                tma2_load_3d(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), &maps.w[q], cb, t,
                              f0, bf);
               if (++sb == SB) {
                 sb = 0;
@@ -533,13 +547,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t pa = 0, pb = 0, pacc = 0;
       long long pt;
       int nt, q;
-      const uint32_t idesc = idesc_bf16_m256(p.NT);
+      const uint32_t idesc = idesc_f16_m256(p.ab_fmt, p.NT);
       for (int k = 0; unit_of(p, k, pt, nt, q); ++k) {
         mbar_wait(&acc_empty[acc], pacc ^ 1);
         tc_fence_after();
         if (lane == 0) trace_ev(p, 2, k);
-        const uint32_t d = tb + (uint32_t)(acc * p.NT);
+        // SPLIT: pass 0 (xh.wh) accumulates into its own columns, passes 1-2 (the
+        // ~2^-11 smaller corrections) into the next NT -- the large sum then takes
+        // only a third of the non-round-to-nearest accumulation steps
+        const uint32_t d = tb + (uint32_t)(acc * p.NT * (p.split ? 2 : 1));
         if (p.im2col) {
+          for (int pass = 0; pass < (p.split ? 3 : 1); ++pass)
           for (int kb = 0; kb < p.nkb; ++kb)
             for (int t = 0; t < p.taps[q]; ++t) {
               mbar_wait(&a_full[sa], pa);
@@ -547,11 +565,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               tc_fence_after();
               const uint64_t ad = sw128_desc(smem_u32(a_base + (size_t)sa * p.a_stage_bytes));
               const uint64_t bd = sw128_desc(smem_u32(b_base + (size_t)sb * p.b_stage_bytes));
+              const uint32_t ds = d + (pass > 0 ? (uint32_t)p.NT : 0u);
+              const bool first = (pass <= 1) && kb == 0 && t == 0;
               if (elect_one()) {
 #pragma unroll
                 for (int ks = 0; ks < KB / 16; ++ks)
-                  mma2_bf16(d, ad + 2u * ks, bd + 2u * ks, idesc,
-                            (kb == 0 && t == 0 && ks == 0) ? 0u : 1u);
+                  mma2_bf16(ds, ad + 2u * ks, bd + 2u * ks, idesc, (first && ks == 0) ? 0u : 1u);
               }
               __syncwarp();
               if (elect_one()) {
@@ -694,10 +713,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     p.cout +
                 nt * p.NT;
       const int fmax = p.cout - nt * p.NT;  // features of this tile that exist
+      const float osc = p.split ? __ldg(p.split_inv_scale) : 1.0f;
 #pragma unroll 1
       for (int c0 = 0; c0 < p.NT; c0 += 32) {
         float v[32];
-        tmem_ld32(lane_base + (uint32_t)(acc * p.NT + c0), v);
+        tmem_ld32(lane_base + (uint32_t)(acc * p.NT * (p.split ? 2 : 1) + c0), v);
+        if (p.split) {
+          float w2[32];
+          tmem_ld32(lane_base + (uint32_t)(acc * p.NT * 2 + p.NT + c0), w2);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = (v[e] + w2[e]) * osc;  // scale: exact power of two
+        }
         if (!ok || c0 >= fmax) continue;
         if (c0 + 32 <= fmax) {
           if constexpr (sizeof(YT) == 2) {
@@ -817,10 +843,25 @@ bool tc_wide_fits(int kh, int kw, int p, int cin, int cout) {
   return true;
 }
 
-static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
+// xs: the [hi | lo] fp16 copy of an fp32 input (SPLIT); any aligned pointer
+// when only checking support
+static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, const void* xs = nullptr) {
   p = tcw::Params{};
-  if (pr.x_dtype != SEGCONV_BF16 || pr.panel_dtype != SEGCONV_BF16) return false;
+  const bool split = pr.x_dtype == SEGCONV_F32 && pr.panel_dtype == SEGCONV_F16_SPLIT;
+  if (!split && (pr.x_dtype != SEGCONV_BF16 || pr.panel_dtype != SEGCONV_BF16)) return false;
   if (pr.panel_layout != SEGCONV_PANEL_KMAJOR) return false;
+  if (split && !xs) return false;
+  p.split = split ? 1 : 0;
+  p.split_off = pr.cin;
+  if (split) {  // the scale slot follows the K-major panels: 4 classes x cout_pad x taps x 2 cin fp16
+    long long main = 0;
+    for (int q = 0; q < 4; ++q) main += (long long)pr.cls.kh[q] * pr.cls.kw[q] * 2 * pr.cin * pr.cout_pad;
+    p.split_inv_scale = reinterpret_cast<const float*>(reinterpret_cast<const __half*>(pr.panels) + main) + 1;
+  }
+  p.ab_fmt = split ? 0u : 1u;
+  const int kc = split ? 2 * pr.cin : pr.cin;  // channels of the staged tensors
+  const void* xsrc = split ? xs : pr.x;
+  const CUtensorMapDataType op_type = split ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   if (pr.y_dtype != SEGCONV_BF16 && pr.y_dtype != SEGCONV_F32) return false;
   if (!tc_wide_fits(pr.kh, pr.kw, pr.p, pr.cin, pr.cout)) return false;
   p.wscale = 1;
@@ -837,7 +878,7 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
   p.out_h = pr.out_h;
   p.out_w = pr.out_w;
   p.Mv = (long long)pr.batch * pr.n * pr.n;
-  p.NT = tc_wide_ntile(pr.cout);
+  p.NT = split ? std::min(128, tc_wide_ntile(pr.cout)) : tc_wide_ntile(pr.cout);  // SPLIT: 2 accumulators
   p.n_tiles = (pr.cout + p.NT - 1) / p.NT;
   if (p.n_tiles * p.NT > pr.cout_pad && p.n_tiles > 1) {
     // the last tile may run past cout_pad: the TMA box is zero-filled out of bounds
@@ -876,7 +917,7 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
     // -- the extra per-tap A gathers are L2 hits, the saved MMA rows are not
     p.im2col = 1;
     const char* e = getenv("SEGCONV_WIDE_IM2COL");
-    if (e) p.im2col = atoi(e) ? 1 : 0;
+    if (e && !split) p.im2col = atoi(e) ? 1 : 0;  // the split passes need im2col staging
   }
   // halo-shift staging (SEGCONV_WIDE_IM2COL=0) limits: the staged rows must fit
   // one TMA box; they do not constrain the im2col path (e.g. 128 x 128 maps)
@@ -938,22 +979,22 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
   EncodeTiledFnW fn = encode_fn_w();
   if (!fn) return false;
   if (p.tile2d) {
-    const cuuint64_t dims[4] = {(cuuint64_t)pr.cin, (cuuint64_t)pr.n, (cuuint64_t)pr.n,
+    const cuuint64_t dims[4] = {(cuuint64_t)kc, (cuuint64_t)pr.n, (cuuint64_t)pr.n,
                                 (cuuint64_t)pr.batch};
-    const cuuint64_t strides[3] = {(cuuint64_t)pr.cin * 2, (cuuint64_t)pr.n * pr.cin * 2,
-                                   (cuuint64_t)pr.n * pr.n * pr.cin * 2};
+    const cuuint64_t strides[3] = {(cuuint64_t)kc * 2, (cuuint64_t)pr.n * kc * 2,
+                                   (cuuint64_t)pr.n * pr.n * kc * 2};
     const cuuint32_t box[4] = {(cuuint32_t)tcw::KB, (cuuint32_t)p.VW, (cuuint32_t)p.TRH, 1};
     const cuuint32_t es[4] = {1, 1, 1, 1};
-    if (fn(&maps.x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pr.x), dims, strides,
+    if (fn(&maps.x, op_type, 4, const_cast<void*>(xsrc), dims, strides,
            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
   } else {
-    const cuuint64_t dims[2] = {(cuuint64_t)pr.cin, (cuuint64_t)p.Mv};
-    const cuuint64_t strides[1] = {(cuuint64_t)pr.cin * 2};
+    const cuuint64_t dims[2] = {(cuuint64_t)kc, (cuuint64_t)p.Mv};
+    const cuuint64_t strides[1] = {(cuuint64_t)kc * 2};
     const cuuint32_t box[2] = {(cuuint32_t)tcw::KB, (cuuint32_t)p.S_rows};
     const cuuint32_t es[2] = {1, 1};
-    if (fn(&maps.x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pr.x), dims, strides,
+    if (fn(&maps.x, op_type, 2, const_cast<void*>(xsrc), dims, strides,
            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
@@ -973,16 +1014,16 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
         return false;
       enc2 = (EncIm2col)f;
     }
-    const cuuint64_t dims[4] = {(cuuint64_t)pr.cin, (cuuint64_t)pr.n, (cuuint64_t)pr.n,
+    const cuuint64_t dims[4] = {(cuuint64_t)kc, (cuuint64_t)pr.n, (cuuint64_t)pr.n,
                                 (cuuint64_t)pr.batch};
-    const cuuint64_t strides[3] = {(cuuint64_t)pr.cin * 2, (cuuint64_t)pr.n * pr.cin * 2,
-                                   (cuuint64_t)pr.n * pr.n * pr.cin * 2};
+    const cuuint64_t strides[3] = {(cuuint64_t)kc * 2, (cuuint64_t)pr.n * kc * 2,
+                                   (cuuint64_t)pr.n * pr.n * kc * 2};
     const cuuint32_t es[4] = {1, 1, 1, 1};
     for (int q = 0; q < 4; ++q) {
       // walk origins (anchor - p_fused) over [-pf, C-1-pf] x [-pf, R-1-pf] of every image
       const int lower[2] = {-pr.pf, -pr.pf};
       const int upper[2] = {pr.cls.cols[q] - pr.pf - pr.n, pr.cls.rows[q] - pr.pf - pr.n};
-      if (enc2(&maps.xi[q], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pr.x), dims,
+      if (enc2(&maps.xi[q], op_type, 4, const_cast<void*>(xsrc), dims,
                strides, lower, upper, (cuuint32_t)tcw::KB, 128, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -990,12 +1031,12 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
     }
   }
   for (int q = 0; q < 4; ++q) {
-    const cuuint64_t dims[3] = {(cuuint64_t)pr.cin, (cuuint64_t)p.taps[q], (cuuint64_t)pr.cout_pad};
-    const cuuint64_t strides[2] = {(cuuint64_t)pr.cin * 2, (cuuint64_t)p.taps[q] * pr.cin * 2};
+    const cuuint64_t dims[3] = {(cuuint64_t)kc, (cuuint64_t)p.taps[q], (cuuint64_t)pr.cout_pad};
+    const cuuint64_t strides[2] = {(cuuint64_t)kc * 2, (cuuint64_t)p.taps[q] * kc * 2};
     const cuuint32_t box[3] = {(cuuint32_t)tcw::KB, 1, (cuuint32_t)(p.NT / 2)};
     const cuuint32_t es[3] = {1, 1, 1};
     void* base = (char*)const_cast<void*>(pr.panels) + pr.cls.sub_offset[q] * 2;
-    if (fn(&maps.w[q], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, base, dims, strides, box, es,
+    if (fn(&maps.w[q], op_type, 3, base, dims, strides, box, es,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
@@ -1012,6 +1053,7 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps) {
 // N = ch -- no flipped or re-laid-out copy is made.
 static bool make_wide_dgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps& maps) {
   p = tcw::Params{};
+  p.ab_fmt = 1;  // bf16 operands
   if (pr.dtype != SEGCONV_BF16) return false;
   if (pr.cout % tcw::KB != 0 || pr.cin < 64 || pr.cin % 8 != 0) return false;
   const int taps = pr.kh * pr.kw;
@@ -1119,6 +1161,7 @@ static bool make_wide_dgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
 // launch_wgrad_reduce sums in split order (deterministic).
 static bool make_wide_wgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps& maps, int pairs) {
   p = tcw::Params{};
+  p.ab_fmt = 1;  // bf16 operands
   if (pr.dtype != SEGCONV_BF16 || pr.batch < 1) return false;
   if (pr.cin % 128 != 0 || pr.cout % 128 != 0) return false;
   const int taps = pr.kh * pr.kw;
@@ -1261,6 +1304,7 @@ bool tc_bwd_weight_supported(const BackwardProblem& pr) {
 static bool make_wide_conv(const void* src, int batch, int h, int w, int cin, const void* kt, int kh, int kw,
                            int cout, const float* bias, unsigned epi, void* y, tcw::Params& p, tcw::Maps& maps) {
   p = tcw::Params{};
+  p.ab_fmt = 1;  // bf16 operands
   const int taps = kh * kw;
   if (cin % tcw::KB != 0 || cout < 64 || taps > tcw::MAX_TAPS_Q || kh > 128 || kw > 128) return false;
   const int oh = h - kh + 1, ow = w - kw + 1;
@@ -1348,10 +1392,10 @@ bool tc_bwd_data_supported(const BackwardProblem& pr) {
 }
 
 bool tc_wide_supported(const FusedProblem& pr, int math) {
-  if (math != SEGCONV_MATH_BF16) return false;
+  if (math != SEGCONV_MATH_BF16 && math != SEGCONV_MATH_F16X3) return false;
   tcw::Params p;
   tcw::Maps m;
-  return make_wide(pr, p, m);
+  return make_wide(pr, p, m, pr.x);  // pr.x stands in for the split copy (alignment only)
 }
 
 template <typename YT, int ACT>
@@ -1398,9 +1442,54 @@ static cudaError_t launch_wide_t(const tcw::Params& prm, const tcw::Maps& maps, 
   return e;
 }
 
+namespace tcw {
+// fp32 x -> fp16 [hi | lo] channel halves (x = hi + lo to ~22 bits)
+__global__ void split_x_kernel(const float* __restrict__ x, __half* __restrict__ xs, long long npix, int cin) {
+  const long long total = npix * cin;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long pix = e / cin;
+    const int ch = (int)(e - pix * cin);
+    const float v = x[e];
+    const __half hi = __float2half_rn(v);
+    xs[pix * 2 * cin + ch] = hi;
+    xs[pix * 2 * cin + cin + ch] = __float2half_rn(v - __half2float(hi));
+  }
+}
+}  // namespace tcw
+
 cudaError_t launch_tc_wide(const FusedProblem& pr, cudaStream_t s) {
   tcw::Params p;
   tcw::Maps maps;
+  if (pr.x_dtype == SEGCONV_F32 && pr.panel_dtype == SEGCONV_F16_SPLIT) {
+    const long long npix = (long long)pr.batch * pr.n * pr.n;
+    if (npix == 0) return cudaSuccess;
+    void* xs = nullptr;
+    cudaError_t e = workspace_alloc(&xs, (size_t)npix * 2 * pr.cin * 2, s);
+    if (e != cudaSuccess) return e;
+    const long long total = npix * pr.cin;
+    tcw::split_x_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148LL * 16), 256, 0, s>>>(
+        (const float*)pr.x, (__half*)xs, npix, pr.cin);
+    e = cudaGetLastError();
+    if (e == cudaSuccess) {
+      note_launch();
+      if (!make_wide(pr, p, maps, xs)) {
+        e = cudaErrorNotSupported;
+      } else {
+        p.trace = tc_trace_buffer();
+        const int act = (pr.epi & SEGCONV_EPI_RELU) ? 1 : (pr.epi & SEGCONV_EPI_TANH) ? 2 : 0;
+        if (pr.y_dtype == SEGCONV_BF16)
+          e = act == 1 ? launch_wide_t<__nv_bfloat16, 1>(p, maps, s)
+                       : act == 2 ? launch_wide_t<__nv_bfloat16, 2>(p, maps, s)
+                                  : launch_wide_t<__nv_bfloat16, 0>(p, maps, s);
+        else
+          e = act == 1 ? launch_wide_t<float, 1>(p, maps, s)
+                       : act == 2 ? launch_wide_t<float, 2>(p, maps, s) : launch_wide_t<float, 0>(p, maps, s);
+      }
+    }
+    const cudaError_t e2 = cudaFreeAsync(xs, s);
+    return e != cudaSuccess ? e : e2;
+  }
   if (!make_wide(pr, p, maps)) return cudaErrorNotSupported;
   if (p.units == 0) return cudaSuccess;
   p.trace = tc_trace_buffer();

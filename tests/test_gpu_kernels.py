@@ -260,3 +260,59 @@ def test_tile_kernel_not_used_where_class_grids_exceed_the_input():
     got, path = run(x, k, 4, "bf16", out_dtype=torch.float32)
     assert path != "tc-tile"
     assert np.array_equal(got, oracle.tconv_fused(x, k, 4))
+
+
+@pytest.mark.parametrize("batch,n,cin,cout,ks,p,act", [
+    (4, 16, 512, 256, 4, 0, None),    # BASELINE C3 shape in fp32: main product 4 x 512 / 16 = 128 steps
+    (2, 8, 128, 64, 4, 2, "relu"),    # DCGAN layer in fp32
+    (3, 5, 256, 128, 3, 1, "tanh"),
+    (2, 7, 64, 96, 3, 0, None),
+    (2, 4, 768, 256, 3, 0, None),     # 4 taps x 768 / 16 = 192 steps, the AUTO limit
+])
+def test_pair_kernel_fp32_split(batch, n, cin, cout, ks, p, act):
+    """fp32 wide layers (the reference's own dtype) on the pair kernel: x and w as
+    fp16 [hi | lo] halves, three MMA passes (xh.wh, xl.wh, xh.wl).  Bar: 1e-5
+    scaled against the reference order, or -- where the reference's own fp32
+    sums (2048 terms for C3) already miss the exact f64 answer by that much --
+    at least as close to the exact answer as the reference is (within 2x), as
+    test_gpu_parity does for FFMA."""
+    rng = np.random.default_rng(batch + n + cin + p)
+    x = rng.uniform(-1, 1, (batch, n, n, cin)).astype(np.float32)
+    k = (rng.standard_normal((ks, ks, cin, cout)) / np.sqrt(cin * ks * ks)).astype(np.float32)
+    got, path = run(x, k, p, "f16x3", act)
+    assert path == "tc-pair"
+    want = want_of(x, k, p, act)
+    if scaled_err(got, want) > TOL_F32:
+        exact = oracle.tconv_fused(x.astype(np.float64), k.astype(np.float64), p)
+        if act == "relu":
+            exact = np.maximum(exact, 0)
+        if act == "tanh":
+            exact = np.tanh(exact)
+        assert scaled_err(got, exact) <= max(TOL_F32, 2 * scaled_err(want, exact))
+
+
+def test_pair_kernel_fp32_split_int_exact():
+    rng = np.random.default_rng(77)
+    x = rng.integers(-3, 4, (2, 8, 8, 128)).astype(np.float32)
+    k = rng.integers(-2, 3, (4, 4, 128, 64)).astype(np.float32)
+    got, path = run(x, k, 2, "f16x3")
+    assert path == "tc-pair"
+    assert np.array_equal(got, oracle.tconv_fused(x, k, 2))
+
+
+def test_fp32_long_k_layers_stay_on_ffma_under_auto():
+    """AUTO keeps fp32 layers whose main tensor-core accumulation would take > 192
+    K-steps (4 taps x 1024 channels / 16 = 256) on FFMA, which meets 1e-5; the
+    explicit f16x3 request still runs the pair kernel, within ~4e-8 per step."""
+    rng = np.random.default_rng(5)
+    x = rng.uniform(-1, 1, (2, 4, 4, 1024)).astype(np.float32)
+    k = (rng.standard_normal((4, 4, 1024, 128)) / np.sqrt(1024 * 16)).astype(np.float32)
+    g = sc.tconv_geometry(4, 4, 4, 0)
+    xt, kt = torch.from_numpy(x).cuda(), torch.from_numpy(k).cuda()
+    y = sc.transpose_conv_fused(xt, sc.segregate(kt, 0), g).cpu().numpy()
+    assert sc.last_path().startswith("simt")
+    want = oracle.tconv_fused(x, k, 0)
+    assert scaled_err(y, want) <= TOL_F32
+    y2 = sc.transpose_conv_fused(xt, sc.segregate(kt, 0, math="f16x3"), g).cpu().numpy()
+    assert sc.last_path() == "tc-pair"
+    assert scaled_err(y2, want) <= 256 * 4e-8 + TOL_F32
