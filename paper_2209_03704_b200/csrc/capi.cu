@@ -247,6 +247,7 @@ segconv_status segconv_subkernels_for_math(int kh, int kw, int cin, int cout, in
                                            segconv_dtype x_dtype, segconv_math math,
                                            segconv_subkernels* out) {
   if (!valid_dtype(x_dtype)) return fail(SEGCONV_E_CONTRACT, "unknown activation dtype");
+  bool fold_blocked = false;
   if (math == SEGCONV_MATH_AUTO) {
     math = segconv_select_math(x_dtype, x_dtype, cin, cout, kh, kw);
     if ((math == SEGCONV_MATH_BF16 || math == SEGCONV_MATH_F16X3) && !tc_shape_ok(kh, kw, p_orig))
@@ -258,14 +259,23 @@ segconv_status segconv_subkernels_for_math(int kh, int kw, int cin, int cout, in
     // (xh.wh: taps * cin / 16 steps) in its own accumulator, and past ~200 such
     // steps the drift exceeds the fp32 bar (1e-5): those layers run on FFMA
     // unless f16x3 is asked for explicitly.
-    if (math == SEGCONV_MATH_F16X3 && !tc_fold_fits(math, kh, kw, p_orig, cin, cout)) {
-      int taps_max = 0;
-      for (int r = 0; r < 2; ++r)
-        for (int c = 0; c < 2; ++c)
-          taps_max = std::max(taps_max, segconv_active_tap_count(kh, p_orig, r) *
-                                            segconv_active_tap_count(kw, p_orig, c));
-      if (!tc_wide_fits(kh, kw, p_orig, cin, cout) || (long long)taps_max * cin / 16 > 192)
-        math = SEGCONV_MATH_FFMA;
+    if (math == SEGCONV_MATH_F16X3) {
+      // the folded kernels accumulate all three products over the union window
+      int ur = 0, uc = 0;
+      fold_window(kh, kw, p_orig, &ur, &uc);
+      const bool fold_ok = tc_fold_fits(math, kh, kw, p_orig, cin, cout) && 3LL * ur * uc * cin / 16 <= 192;
+      if (!fold_ok) {
+        int taps_max = 0;
+        for (int r = 0; r < 2; ++r)
+          for (int c = 0; c < 2; ++c)
+            taps_max = std::max(taps_max, segconv_active_tap_count(kh, p_orig, r) *
+                                              segconv_active_tap_count(kw, p_orig, c));
+        const bool ring = kh == 5 && kw == 5 && cout == 3 && p_orig == 0 && cin % 32 == 0 && cin <= 256;
+        if (!ring && (!tc_wide_fits(kh, kw, p_orig, cin, cout) || (long long)taps_max * cin / 16 > 192))
+          math = SEGCONV_MATH_FFMA;
+        else if (!ring && tc_fold_fits(math, kh, kw, p_orig, cin, cout))
+          fold_blocked = true;  // too long for one accumulator: the pair kernel's split mode
+      }
     }
   }
   switch (math) {
@@ -279,7 +289,7 @@ segconv_status segconv_subkernels_for_math(int kh, int kw, int cin, int cout, in
     case SEGCONV_MATH_BF16:
     case SEGCONV_MATH_F16X3: {
       // narrow layers (cout <= 32, p_fused == 0): class-folded kernel
-      const bool fold = tc_fold_fits(math, kh, kw, p_orig, cin, cout);
+      const bool fold = !fold_blocked && tc_fold_fits(math, kh, kw, p_orig, cin, cout);
       // wide bf16 layers: CTA-pair kernel on K-major (class, f, u, v, ch) panels
       if (!fold && math == SEGCONV_MATH_BF16 && tc_wide_fits(kh, kw, p_orig, cin, cout) &&
           getenv("SEGCONV_NO_WIDE") == nullptr) {

@@ -316,3 +316,17 @@ def test_fp32_long_k_layers_stay_on_ffma_under_auto():
     y2 = sc.transpose_conv_fused(xt, sc.segregate(kt, 0, math="f16x3"), g).cpu().numpy()
     assert sc.last_path() == "tc-pair"
     assert scaled_err(y2, want) <= 256 * 4e-8 + TOL_F32
+
+
+@pytest.mark.parametrize("cin,cout,ks", [(512, 32, 3), (256, 16, 5)])
+def test_fp32_narrow_long_k_layers_leave_the_folded_kernel(cin, cout, ks):
+    """The folded kernels keep every product in one accumulator over the union
+    window; when that would take > 192 accumulation steps AUTO moves the layer to
+    the pair kernel's split mode (main product apart), which meets 1e-5."""
+    rng = np.random.default_rng(cin + ks)
+    x = rng.uniform(-1, 1, (2, 12, 12, cin)).astype(np.float32)
+    k = (rng.standard_normal((ks, ks, cin, cout)) / np.sqrt(cin * ks * ks)).astype(np.float32)
+    g = sc.tconv_geometry(12, ks, ks, 0)
+    y = sc.transpose_conv_fused(torch.from_numpy(x).cuda(), torch.from_numpy(k).cuda(), 0).cpu().numpy()
+    assert sc.last_path() == "tc-pair"
+    assert scaled_err(y, oracle.tconv_fused(x, k, 0)) <= TOL_F32
