@@ -62,7 +62,7 @@ typedef enum {
   SEGCONV_MATH_EXACT = 2,  /* SIMT, reference accumulation order, no FMA contraction:         */
                            /* bit-identical to the reference CPU path (slow; for parity)      */
   SEGCONV_MATH_BF16 = 3,   /* tcgen05 kind::f16: bf16 operands, fp32 accumulate in TMEM       */
-  SEGCONV_MATH_TF32 = 4,   /* reserved (kind::tf32); not built in this version                 */
+  SEGCONV_MATH_TF32 = 4,   /* tcgen05 kind::tf32 on fp32 data (10-bit mantissa; bar 1e-2 as bf16)  */
   SEGCONV_MATH_F16X3 = 5   /* tcgen05 kind::f16 on split operands: x = xh + xl, w = wh + wl     */
                            /* (fp16 each), y = xh*wh + xl*wh + xh*wl accumulated in fp32 TMEM;  */
                            /* ~22-bit operands, fp32-class accuracy for |x|,|w| < 2^15          */

@@ -310,6 +310,16 @@ segconv_status segconv_subkernels_for_math(int kh, int kw, int cin, int cout, in
           kh, kw, cin, cout, p_orig, math == SEGCONV_MATH_BF16 ? SEGCONV_BF16 : SEGCONV_F16_SPLIT,
           fold ? SEGCONV_PANEL_UMMA_FOLD : SEGCONV_PANEL_UMMA, out);
     }
+    case SEGCONV_MATH_TF32: {
+      // fp32 data on tf32 tensor cores (10-bit mantissa, the cuDNN default for fp32):
+      // the CTA-pair kernel on fp32 K-major panels
+      if (x_dtype != SEGCONV_F32 || !tc_wide_fits(kh, kw, p_orig, cin, cout))
+        return fail(SEGCONV_E_UNSUPPORTED, "TF32 math needs fp32 data, cin %% 64 == 0 and taps in every class");
+      const segconv_status st = segconv_subkernels_init(kh, kw, cin, cout, p_orig, SEGCONV_F32,
+                                                        SEGCONV_PANEL_KMAJOR, out);
+      if (st == SEGCONV_OK) out->math = SEGCONV_MATH_TF32;
+      return st;
+    }
     default:
       return fail(SEGCONV_E_UNSUPPORTED, "math mode %d has no kernels in this build", (int)math);
   }
@@ -485,8 +495,12 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
       return cuda_status(launch_direct_generic(pr, false, s), "transpose_conv_fused[ffma]");
     }
     case SEGCONV_MATH_BF16:
-    case SEGCONV_MATH_F16X3: {
-      if (sks->layout == SEGCONV_PANEL_KMAJOR && (math == SEGCONV_MATH_BF16 || math == SEGCONV_MATH_F16X3)) {
+    case SEGCONV_MATH_F16X3:
+    case SEGCONV_MATH_TF32: {
+      if (math == SEGCONV_MATH_TF32 && sks->layout != SEGCONV_PANEL_KMAJOR)
+        return fail(SEGCONV_E_CONTRACT, "TF32 math needs the K-major fp32 panels segregate builds for it");
+      if (sks->layout == SEGCONV_PANEL_KMAJOR &&
+          (math == SEGCONV_MATH_BF16 || math == SEGCONV_MATH_F16X3 || math == SEGCONV_MATH_TF32)) {
         if ((int)math != sks->math)
           return fail(SEGCONV_E_CONTRACT, "panels were laid out for math %d, not %d", sks->math,
                       (int)math);

@@ -91,6 +91,10 @@ struct Params {
   int split, split_off;
   uint32_t ab_fmt;  // MMA operand format: 1 bf16, 0 fp16
   const float* split_inv_scale;  // SPLIT: the weights were scaled by 2^s; sums are multiplied by 2^-s
+  // TF32 (fp32 data, math = tf32): fp32 operands, kind::tf32 MMAs (K = 8 per
+  // instruction -- the same 32 bytes per step), 32 channels per 128-byte row
+  int tf32;
+  int kbc;  // channels per k-block (one 128-byte TMA row): 64 16-bit, 32 fp32
   // WGRAD (mode 1, launch_tc_bwd_weight): per unit (split s, tap t, 256-channel pair
   // tile ct, feature tile nt), D[ch, f] = sum over the split's 64-pixel chunks of
   // x[m, ch] * gy[b, 2i+p-U, 2j+p-V, f].  Both operands are MN-major (channels /
@@ -185,6 +189,16 @@ __device__ __forceinline__ void mma2_bf16(uint32_t d_tmem, uint64_t a, uint64_t 
       ".reg .pred p;\n"
       "setp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma2_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n"
       "}\n" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
@@ -432,8 +446,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int pass = 0; pass < (p.split ? 3 : 1); ++pass)
           for (int kb = 0; kb < p.nkb; ++kb)
             for (int t = 0; t < p.taps[q]; ++t) {
-              const int ca = kb * KB + (pass == 1 ? p.split_off : 0);  // A: xl on pass 1
-              const int cb = kb * KB + (pass == 2 ? p.split_off : 0);  // B: wl on pass 2
+              const int ca = kb * p.kbc + (pass == 1 ? p.split_off : 0);  // A: xl on pass 1
+              const int cb = kb * p.kbc + (pass == 2 ? p.split_off : 0);  // B: wl on pass 2
               mbar_wait(&a_empty[sa], pa ^ 1);
               const uint32_t af = mapa(smem_u32(&a_full[sa]), 0);
               if (rank == 0) mbar_arrive_expect_tx(&a_full[sa], 2 * 128 * 128);
@@ -568,9 +582,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint32_t ds = d + (pass > 0 ? (uint32_t)p.NT : 0u);
               const bool first = (pass <= 1) && kb == 0 && t == 0;
               if (elect_one()) {
+                if (p.tf32) {
 #pragma unroll
-                for (int ks = 0; ks < KB / 16; ++ks)
-                  mma2_bf16(ds, ad + 2u * ks, bd + 2u * ks, idesc, (first && ks == 0) ? 0u : 1u);
+                  for (int ks = 0; ks < 4; ++ks)  // 4 x (K = 8 fp32) = one 128-byte row
+                    mma2_tf32(ds, ad + 2u * ks, bd + 2u * ks, idesc, (first && ks == 0) ? 0u : 1u);
+                } else {
+#pragma unroll
+                  for (int ks = 0; ks < KB / 16; ++ks)
+                    mma2_bf16(ds, ad + 2u * ks, bd + 2u * ks, idesc, (first && ks == 0) ? 0u : 1u);
+                }
               }
               __syncwarp();
               if (elect_one()) {
@@ -848,20 +868,26 @@ bool tc_wide_fits(int kh, int kw, int p, int cin, int cout) {
 static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, const void* xs = nullptr) {
   p = tcw::Params{};
   const bool split = pr.x_dtype == SEGCONV_F32 && pr.panel_dtype == SEGCONV_F16_SPLIT;
-  if (!split && (pr.x_dtype != SEGCONV_BF16 || pr.panel_dtype != SEGCONV_BF16)) return false;
+  const bool tf32 = pr.x_dtype == SEGCONV_F32 && pr.panel_dtype == SEGCONV_F32;
+  if (!split && !tf32 && (pr.x_dtype != SEGCONV_BF16 || pr.panel_dtype != SEGCONV_BF16)) return false;
   if (pr.panel_layout != SEGCONV_PANEL_KMAJOR) return false;
   if (split && !xs) return false;
   p.split = split ? 1 : 0;
+  p.tf32 = tf32 ? 1 : 0;
+  p.kbc = tf32 ? 32 : tcw::KB;
+  const int esz = tf32 ? 4 : 2;  // operand element bytes
   p.split_off = pr.cin;
   if (split) {  // the scale slot follows the K-major panels: 4 classes x cout_pad x taps x 2 cin fp16
     long long main = 0;
     for (int q = 0; q < 4; ++q) main += (long long)pr.cls.kh[q] * pr.cls.kw[q] * 2 * pr.cin * pr.cout_pad;
     p.split_inv_scale = reinterpret_cast<const float*>(reinterpret_cast<const __half*>(pr.panels) + main) + 1;
   }
-  p.ab_fmt = split ? 0u : 1u;
+  p.ab_fmt = tf32 ? 2u : split ? 0u : 1u;  // instruction-descriptor operand format: tf32 / f16 / bf16
   const int kc = split ? 2 * pr.cin : pr.cin;  // channels of the staged tensors
   const void* xsrc = split ? xs : pr.x;
-  const CUtensorMapDataType op_type = split ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const CUtensorMapDataType op_type = tf32    ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                      : split ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                              : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   if (pr.y_dtype != SEGCONV_BF16 && pr.y_dtype != SEGCONV_F32) return false;
   if (!tc_wide_fits(pr.kh, pr.kw, pr.p, pr.cin, pr.cout)) return false;
   p.wscale = 1;
@@ -883,7 +909,7 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
   if (p.n_tiles * p.NT > pr.cout_pad && p.n_tiles > 1) {
     // the last tile may run past cout_pad: the TMA box is zero-filled out of bounds
   }
-  p.nkb = pr.cin / tcw::KB;
+  p.nkb = pr.cin / p.kbc;
   p.pf = pr.pf;
   p.tile2d = pr.pf > 0 ? 1 : 0;
   p.VW = pr.n + 2 * pr.pf;  // pitch of the staged rows (the padded grid in TILE2D)
@@ -917,7 +943,7 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
     // -- the extra per-tap A gathers are L2 hits, the saved MMA rows are not
     p.im2col = 1;
     const char* e = getenv("SEGCONV_WIDE_IM2COL");
-    if (e && !split) p.im2col = atoi(e) ? 1 : 0;  // the split passes need im2col staging
+    if (e && !split && !tf32) p.im2col = atoi(e) ? 1 : 0;  // split / tf32 need im2col staging
   }
   // halo-shift staging (SEGCONV_WIDE_IM2COL=0) limits: the staged rows must fit
   // one TMA box; they do not constrain the im2col path (e.g. 128 x 128 maps)
@@ -981,9 +1007,9 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
   if (p.tile2d) {
     const cuuint64_t dims[4] = {(cuuint64_t)kc, (cuuint64_t)pr.n, (cuuint64_t)pr.n,
                                 (cuuint64_t)pr.batch};
-    const cuuint64_t strides[3] = {(cuuint64_t)kc * 2, (cuuint64_t)pr.n * kc * 2,
-                                   (cuuint64_t)pr.n * pr.n * kc * 2};
-    const cuuint32_t box[4] = {(cuuint32_t)tcw::KB, (cuuint32_t)p.VW, (cuuint32_t)p.TRH, 1};
+    const cuuint64_t strides[3] = {(cuuint64_t)kc * esz, (cuuint64_t)pr.n * kc * esz,
+                                   (cuuint64_t)pr.n * pr.n * kc * esz};
+    const cuuint32_t box[4] = {(cuuint32_t)p.kbc, (cuuint32_t)p.VW, (cuuint32_t)p.TRH, 1};
     const cuuint32_t es[4] = {1, 1, 1, 1};
     if (fn(&maps.x, op_type, 4, const_cast<void*>(xsrc), dims, strides,
            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -991,8 +1017,8 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
       return false;
   } else {
     const cuuint64_t dims[2] = {(cuuint64_t)kc, (cuuint64_t)p.Mv};
-    const cuuint64_t strides[1] = {(cuuint64_t)kc * 2};
-    const cuuint32_t box[2] = {(cuuint32_t)tcw::KB, (cuuint32_t)p.S_rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)kc * esz};
+    const cuuint32_t box[2] = {(cuuint32_t)p.kbc, (cuuint32_t)p.S_rows};
     const cuuint32_t es[2] = {1, 1};
     if (fn(&maps.x, op_type, 2, const_cast<void*>(xsrc), dims, strides,
            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -1016,15 +1042,15 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
     }
     const cuuint64_t dims[4] = {(cuuint64_t)kc, (cuuint64_t)pr.n, (cuuint64_t)pr.n,
                                 (cuuint64_t)pr.batch};
-    const cuuint64_t strides[3] = {(cuuint64_t)kc * 2, (cuuint64_t)pr.n * kc * 2,
-                                   (cuuint64_t)pr.n * pr.n * kc * 2};
+    const cuuint64_t strides[3] = {(cuuint64_t)kc * esz, (cuuint64_t)pr.n * kc * esz,
+                                   (cuuint64_t)pr.n * pr.n * kc * esz};
     const cuuint32_t es[4] = {1, 1, 1, 1};
     for (int q = 0; q < 4; ++q) {
       // walk origins (anchor - p_fused) over [-pf, C-1-pf] x [-pf, R-1-pf] of every image
       const int lower[2] = {-pr.pf, -pr.pf};
       const int upper[2] = {pr.cls.cols[q] - pr.pf - pr.n, pr.cls.rows[q] - pr.pf - pr.n};
       if (enc2(&maps.xi[q], op_type, 4, const_cast<void*>(xsrc), dims,
-               strides, lower, upper, (cuuint32_t)tcw::KB, 128, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               strides, lower, upper, (cuuint32_t)p.kbc, 128, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return false;
@@ -1032,10 +1058,10 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
   }
   for (int q = 0; q < 4; ++q) {
     const cuuint64_t dims[3] = {(cuuint64_t)kc, (cuuint64_t)p.taps[q], (cuuint64_t)pr.cout_pad};
-    const cuuint64_t strides[2] = {(cuuint64_t)kc * 2, (cuuint64_t)p.taps[q] * kc * 2};
-    const cuuint32_t box[3] = {(cuuint32_t)tcw::KB, 1, (cuuint32_t)(p.NT / 2)};
+    const cuuint64_t strides[2] = {(cuuint64_t)kc * esz, (cuuint64_t)p.taps[q] * kc * esz};
+    const cuuint32_t box[3] = {(cuuint32_t)p.kbc, 1, (cuuint32_t)(p.NT / 2)};
     const cuuint32_t es[3] = {1, 1, 1};
-    void* base = (char*)const_cast<void*>(pr.panels) + pr.cls.sub_offset[q] * 2;
+    void* base = (char*)const_cast<void*>(pr.panels) + pr.cls.sub_offset[q] * esz;
     if (fn(&maps.w[q], op_type, 3, base, dims, strides, box, es,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -1054,6 +1080,7 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
 static bool make_wide_dgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps& maps) {
   p = tcw::Params{};
   p.ab_fmt = 1;  // bf16 operands
+  p.kbc = tcw::KB;
   if (pr.dtype != SEGCONV_BF16) return false;
   if (pr.cout % tcw::KB != 0 || pr.cin < 64 || pr.cin % 8 != 0) return false;
   const int taps = pr.kh * pr.kw;
@@ -1162,6 +1189,7 @@ static bool make_wide_dgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
 static bool make_wide_wgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps& maps, int pairs) {
   p = tcw::Params{};
   p.ab_fmt = 1;  // bf16 operands
+  p.kbc = tcw::KB;
   if (pr.dtype != SEGCONV_BF16 || pr.batch < 1) return false;
   if (pr.cin % 128 != 0 || pr.cout % 128 != 0) return false;
   const int taps = pr.kh * pr.kw;
@@ -1305,6 +1333,7 @@ static bool make_wide_conv(const void* src, int batch, int h, int w, int cin, co
                            int cout, const float* bias, unsigned epi, void* y, tcw::Params& p, tcw::Maps& maps) {
   p = tcw::Params{};
   p.ab_fmt = 1;  // bf16 operands
+  p.kbc = tcw::KB;
   const int taps = kh * kw;
   if (cin % tcw::KB != 0 || cout < 64 || taps > tcw::MAX_TAPS_Q || kh > 128 || kw > 128) return false;
   const int oh = h - kh + 1, ow = w - kw + 1;
@@ -1392,7 +1421,7 @@ bool tc_bwd_data_supported(const BackwardProblem& pr) {
 }
 
 bool tc_wide_supported(const FusedProblem& pr, int math) {
-  if (math != SEGCONV_MATH_BF16 && math != SEGCONV_MATH_F16X3) return false;
+  if (math != SEGCONV_MATH_BF16 && math != SEGCONV_MATH_F16X3 && math != SEGCONV_MATH_TF32) return false;
   tcw::Params p;
   tcw::Maps m;
   return make_wide(pr, p, m, pr.x);  // pr.x stands in for the split copy (alignment only)

@@ -1,5 +1,6 @@
 """Times single layers (bf16 or fp32) through transpose_conv_fused: python
-scripts/layer_time.py B N CIN COUT K P [dtype]; prints path and us per call."""
+scripts/layer_time.py B N CIN COUT K P [dtype]; LAYER_MATH=tf32|f16x3|bf16|ffma picks
+the math (default auto); prints path and us per call."""
 import statistics
 import sys
 
@@ -13,7 +14,8 @@ dt = torch.float32 if (len(sys.argv) > 7 and sys.argv[7] == "f32") else torch.bf
 x = torch.randn((b, n, n, cin), device="cuda").to(dt)
 w = (torch.randn((k, k, cin, cout), device="cuda") * 0.02).to(dt)
 g = sc.tconv_geometry(n, k, k, p)
-sks = sc.segregate(w, p)
+import os  # noqa: E402
+sks = sc.segregate(w, p, math=os.environ.get("LAYER_MATH", "auto"))
 y = torch.empty((b, g.out_h, g.out_w, cout), device="cuda", dtype=dt)
 flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device="cuda")
 for _ in range(3):

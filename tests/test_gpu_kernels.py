@@ -330,3 +330,23 @@ def test_fp32_narrow_long_k_layers_leave_the_folded_kernel(cin, cout, ks):
     y = sc.transpose_conv_fused(torch.from_numpy(x).cuda(), torch.from_numpy(k).cuda(), 0).cpu().numpy()
     assert sc.last_path() == "tc-pair"
     assert scaled_err(y, oracle.tconv_fused(x, k, 0)) <= TOL_F32
+
+
+@pytest.mark.parametrize("batch,n,cin,cout,ks,p,act", [
+    (4, 16, 512, 256, 4, 0, None),    # C3 shape in fp32, tf32 tensor cores
+    (2, 8, 128, 64, 4, 2, "relu"),
+    (3, 5, 256, 96, 3, 1, "tanh"),
+])
+def test_pair_kernel_tf32(batch, n, cin, cout, ks, p, act):
+    """math="tf32" (explicit; AUTO keeps fp32 at the 1e-5 bar): fp32 operands on
+    kind::tf32 MMAs, 32 channels per 128-byte row; bar 1e-2 as the bf16 paths."""
+    rng = np.random.default_rng(batch * 9 + n + cin)
+    x = rng.uniform(-1, 1, (batch, n, n, cin)).astype(np.float32)
+    k = (rng.standard_normal((ks, ks, cin, cout)) / np.sqrt(cin * ks * ks)).astype(np.float32)
+    got, path = run(x, k, p, "tf32", act)
+    assert path == "tc-pair"
+    assert scaled_err(got, want_of(x, k, p, act)) <= TOL_TC
+    xi = rng.integers(-3, 4, (batch, n, n, cin)).astype(np.float32)
+    ki = rng.integers(-2, 3, (ks, ks, cin, cout)).astype(np.float32)
+    got, _ = run(xi, ki, p, "tf32")
+    assert np.array_equal(got, oracle.tconv_fused(xi, ki, p))  # small integers are exact in tf32
