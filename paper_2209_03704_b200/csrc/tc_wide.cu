@@ -52,6 +52,7 @@ using namespace tc;
 constexpr int NUM_THREADS = 224;
 constexpr int SMEM_LIMIT = 227 * 1024;
 constexpr int KB = 64;  // channels per stage: one 128-byte row
+constexpr int WCH = 128;  // WGRAD: pixels (K) per chunk
 constexpr int MAX_TAPS_Q = 25;  // 5x5: the input-gradient walk uses every tap as one class
 constexpr int MAX_STAGES_A = 8, MAX_STAGES_B = 12;
 
@@ -377,34 +378,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int t, ct, nt, slot;
       long long cb, ce;
       const int img = p.w_in_h * p.w_in_w;
-      const int di = 64 / p.w_in_w, dj = 64 - (64 / p.w_in_w) * p.w_in_w;  // a chunk = di rows + dj pixels
+      const int di = WCH / p.w_in_w, dj = WCH - (WCH / p.w_in_w) * p.w_in_w;  // a chunk = di rows + dj pixels
       for (int k = 0; wseg_of(p, k, t, ct, nt, cb, ce, slot); ++k) {
         const int ch0 = ct * 256 + (int)rank * 128, f0 = nt * p.NT + (int)rank * NT2;
         // first anchor of the segment's first chunk; then advanced by 64 pixels per
         // chunk without divisions (the single producer lane is on the critical path)
-        const long long mfirst = cb * 64;
+        const long long mfirst = cb * WCH;
         int b0 = (int)(mfirst / img);
         int i0 = (int)(mfirst - (long long)b0 * img);
         int j0 = i0 % p.w_in_w;
         i0 /= p.w_in_w;
         for (long long c = cb; c < ce; ++c) {
-          const long long m = c * 64;
+          const long long m = c * WCH;
           mbar_wait(&a_empty[sa], pa ^ 1);
           const uint32_t af = mapa(smem_u32(&a_full[sa]), 0);
-          if (rank == 0) mbar_arrive_expect_tx(&a_full[sa], 2 * 2 * 64 * 128);
+          if (rank == 0) mbar_arrive_expect_tx(&a_full[sa], 2 * 2 * WCH * 128);
           const uint32_t ad = smem_u32(a_base + (size_t)sa * p.a_stage_bytes);
           tma2_load_2d(ad, &maps.x, ch0, (int)m, af);
-          tma2_load_2d(ad + 8192, &maps.x, ch0 + 64, (int)m, af);
+          tma2_load_2d(ad + WCH * 128, &maps.x, ch0 + 64, (int)m, af);
           if (++sa == SA) {
             sa = 0;
             pa ^= 1;
           }
           mbar_wait(&b_empty[sb], pb ^ 1);
           const uint32_t bf = mapa(smem_u32(&b_full[sb]), 0);
-          if (rank == 0) mbar_arrive_expect_tx(&b_full[sb], 2 * (uint32_t)NT2 * 128);
+          if (rank == 0) mbar_arrive_expect_tx(&b_full[sb], 2 * (uint32_t)(NT2 / 64) * WCH * 128);
           const uint32_t bd = smem_u32(b_base + (size_t)sb * p.b_stage_bytes);
           for (int h = 0; h < NT2 / 64; ++h)
-            tma2_load_im2col(bd + h * 8192, &maps.xi[0], f0 + 64 * h, p.wscale * j0 + p.wbase_c,
+            tma2_load_im2col(bd + h * WCH * 128, &maps.xi[0], f0 + 64 * h, p.wscale * j0 + p.wbase_c,
                              p.wscale * i0 + p.wbase_r,
                              b0, (uint16_t)p.tap_off_c[0][t], (uint16_t)p.tap_off_r[0][t], bf);
           if (++sb == SB) {
@@ -526,11 +527,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&a_full[sa], pa);
           mbar_wait(&b_full[sb], pb);
           tc_fence_after();
-          const uint64_t ad = sw128_mn_desc(smem_u32(a_base + (size_t)sa * p.a_stage_bytes), 8192);
-          const uint64_t bd = sw128_mn_desc(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), 8192);
+          const uint64_t ad = sw128_mn_desc(smem_u32(a_base + (size_t)sa * p.a_stage_bytes), WCH * 128);
+          const uint64_t bd = sw128_mn_desc(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), WCH * 128);
           if (elect_one()) {
 #pragma unroll
-            for (int ks = 0; ks < 4; ++ks)  // K = 16 pixels = 2 atoms of 8 rows: +2048 bytes
+            for (int ks = 0; ks < WCH / 16; ++ks)  // K = 16 pixels = 2 atoms of 8 rows: +2048 bytes
               mma2_bf16(d, ad + 128u * ks, bd + 128u * ks, idesc, (c == c0 && ks == 0) ? 0u : 1u);
           }
           __syncwarp();
@@ -1224,12 +1225,12 @@ static bool make_wide_wgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
       p.tap_off_r[0][U * pr.kw + V] = pr.kh - 1 - U;
       p.tap_off_c[0][U * pr.kw + V] = pr.kw - 1 - V;
     }
-  p.w_chunks = (M + 63) / 64;
+  p.w_chunks = (M + tcw::WCH - 1) / tcw::WCH;
   // splits: minimise modelled time = waves x chunks per unit x t_chunk + the
   // split-K round trip of the partials (write + reduce read, ~5 TB/s, + launch);
   // t_chunk ~ 0.6 us for a 256 x 256 x 64 pair chunk (measured, B200)
   const long long base = (long long)taps * p.w_ch_pairs * p.n_tiles;
-  const double t_chunk = 0.6 * p.NT / 256.0;
+  const double t_chunk = 0.6 * p.NT / 256.0 * tcw::WCH / 64.0;
   const double t_split = (double)taps * pr.cin * pr.cout * 8.0 / 5e6;  // us per split
   int best = 1;
   double best_t = 1e300;
@@ -1269,8 +1270,8 @@ static bool make_wide_wgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
       p.units = base;  // tiles
     }
   }
-  p.a_stage_bytes = 2 * 64 * 128;
-  p.b_stage_bytes = (p.NT / 2) * 128;
+  p.a_stage_bytes = 2 * tcw::WCH * 128;
+  p.b_stage_bytes = (p.NT / 2 / 64) * tcw::WCH * 128;
   const int bar_bytes = (2 * tcw::MAX_STAGES_A + 2 * tcw::MAX_STAGES_B + 4) * 8 + 16;
   p.stages_a = p.stages_b =
       std::min(tcw::MAX_STAGES_A, (tcw::SMEM_LIMIT - bar_bytes) / (p.a_stage_bytes + p.b_stage_bytes));
@@ -1279,7 +1280,7 @@ static bool make_wide_wgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
   {
     const cuuint64_t dims[2] = {(cuuint64_t)pr.cin, (cuuint64_t)M};
     const cuuint64_t strides[1] = {(cuuint64_t)pr.cin * 2};
-    const cuuint32_t box[2] = {64, 64};
+    const cuuint32_t box[2] = {64, (cuuint32_t)tcw::WCH};
     const cuuint32_t es[2] = {1, 1};
     if (fn(&maps.x, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pr.x), dims, strides, box, es,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1297,7 +1298,7 @@ static bool make_wide_wgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
     const int upper[2] = {up_c, up_r};
     const cuuint32_t es[4] = {1, (cuuint32_t)pr.stride, (cuuint32_t)pr.stride, 1};
     if (enc2(&maps.xi[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pr.gy), dims, strides, lower,
-             upper, 64, 64, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             upper, 64, (cuuint32_t)tcw::WCH, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
   }
