@@ -66,10 +66,13 @@ struct Params {
   int NT, n_tiles, nkb;
   int S_rows;
   int a_stage_bytes, b_stage_bytes, stages_a, stages_b;
+  int bprod;  // IM2COL: warp 6 issues the B loads (A and B on separate lanes)
   int taps[4];
   int shift[4][MAX_TAPS_Q];
   int rows[4], cols[4];
   long long pair_tiles, units;
+  long long tail_full;  // IM2COL: units from here on are feature-tile halves (last partial wave)
+  int tail_on;
   // TILE2D (p_fused > 0): each CTA stages TR rows of the padded (virtual) grid,
   // VW = n + 2 p_fused wide, as one 4-D TMA box whose out-of-image part is
   // zero-filled -- the padding is never materialised
@@ -285,10 +288,16 @@ __device__ __forceinline__ void trace_ev(const Params& p, int ev, int local) {
 }
 
 // unit k of this pair -> (pair tile, feature tile, class)
-__device__ __forceinline__ bool unit_of(const Params& p, int k, long long& pt, int& nt, int& q) {
+// hf: 0 = whole feature tile; 1 / 2 = its first / second half (tail units)
+__device__ __forceinline__ bool unit_of(const Params& p, int k, long long& pt, int& nt, int& q, int& hf) {
   const long long pairs = gridDim.x / 2;
-  const long long u = (long long)(blockIdx.x / 2) + (long long)k * pairs;
+  long long u = (long long)(blockIdx.x / 2) + (long long)k * pairs;
   if (u >= p.units) return false;
+  hf = 0;
+  if (p.tail_on && u >= p.tail_full) {
+    hf = 1 + (int)((u - p.tail_full) & 1);
+    u = p.tail_full + ((u - p.tail_full) >> 1);
+  }
   if (p.im2col) {  // class-major: [class q][pair tile][feature tile]
     q = 0;
     while (u >= p.unit_base[q + 1]) ++q;
@@ -430,13 +439,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int sa = 0, sb = 0;
       uint32_t pa = 0, pb = 0;
       long long pt;
-      int nt, q;
-      for (int k = 0; unit_of(p, k, pt, nt, q); ++k) {
+      int nt, q, hf;
+      for (int k = 0; unit_of(p, k, pt, nt, q, hf); ++k) {
         const long long m0 = pt * 256 + (long long)rank * 128;
         const long long g = pt * 2 + rank;  // TILE2D: this CTA's row tile
         const int tb = p.tile2d ? (int)(g / p.tiles_per_img) : 0;
         const int tvi0 = p.tile2d ? (int)(g - (long long)tb * p.tiles_per_img) * p.TR : 0;
-        const int f0 = nt * p.NT + (int)rank * NT2;
+        const int f0 = hf ? nt * p.NT + (hf - 1) * NT2 + (int)rank * (NT2 / 2) : nt * p.NT + (int)rank * NT2;
         if (p.im2col) {
           // this CTA's first anchor of class q: (b, i, j) on the class's rows x cols grid
           const int R = p.rows[q], C = p.cols[q];
@@ -459,6 +468,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 sa = 0;
                 pa ^= 1;
               }
+              if (p.bprod) continue;  // warp 6 streams B
               mbar_wait(&b_empty[sb], pb ^ 1);
               const uint32_t bf = mapa(smem_u32(&b_full[sb]), 0);
               if (rank == 0) mbar_arrive_expect_tx(&b_full[sb], 2 * b_tx);
@@ -510,6 +520,36 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (rank == 0) trace_ev(p, 0, k);
       }
     }
+  } else if (warp == 6) {
+    // ===== IM2COL B producer (both CTAs): the weight tiles of every (pass, kb, tap)
+    // step, in the A producer's order -- two serial issue chains instead of one
+    if (lane == 0 && p.bprod) {
+      griddep_wait();
+      int sb = 0;
+      uint32_t pb = 0;
+      long long pt;
+      int nt, q, hf;
+      for (int k = 0; unit_of(p, k, pt, nt, q, hf); ++k) {
+        const int f0 = hf ? nt * p.NT + (hf - 1) * NT2 + (int)rank * (NT2 / 2) : nt * p.NT + (int)rank * NT2;
+        for (int pass = 0; pass < (p.split ? 3 : 1); ++pass)
+          for (int kb = 0; kb < p.nkb; ++kb)
+            for (int t = 0; t < p.taps[q]; ++t) {
+              const int cb = kb * p.kbc + (pass == 2 ? p.split_off : 0);  // B: wl on pass 2
+              mbar_wait(&b_empty[sb], pb ^ 1);
+              const uint32_t bf = mapa(smem_u32(&b_full[sb]), 0);
+              if (rank == 0) mbar_arrive_expect_tx(&b_full[sb], 2 * b_tx);
+              if (p.b_tap_last)
+                tma2_load_3d(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), &maps.w[q], cb, f0, t, bf);
+              else
+                tma2_load_3d(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), &maps.w[q], cb, t, f0, bf);
+              if (++sb == SB) {
+                sb = 0;
+                pb ^= 1;
+              }
+            }
+      }
+    }
+    __syncwarp();
   } else if (warp == 5) {
     // ===== MMA issuer (leader CTA; the whole warp runs the loop, one lane issues)
     if (rank == 0 && p.mode == 1) {
@@ -561,9 +601,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int sa = 0, sb = 0, acc = 0;
       uint32_t pa = 0, pb = 0, pacc = 0;
       long long pt;
-      int nt, q;
-      const uint32_t idesc = idesc_f16_m256(p.ab_fmt, p.NT);
-      for (int k = 0; unit_of(p, k, pt, nt, q); ++k) {
+      int nt, q, hf;
+      const uint32_t idesc_full = idesc_f16_m256(p.ab_fmt, p.NT), idesc_half = idesc_f16_m256(p.ab_fmt, p.NT / 2);
+      for (int k = 0; unit_of(p, k, pt, nt, q, hf); ++k) {
+        const uint32_t idesc = hf ? idesc_half : idesc_full;
         mbar_wait(&acc_empty[acc], pacc ^ 1);
         tc_fence_after();
         if (lane == 0) trace_ev(p, 2, k);
@@ -697,8 +738,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     int acc = 0;
     uint32_t pacc = 0;
     long long pt;
-    int nt, q;
-    for (int k = 0; unit_of(p, k, pt, nt, q); ++k) {
+    int nt, q, hf;
+    for (int k = 0; unit_of(p, k, pt, nt, q, hf); ++k) {
       mbar_wait(&acc_full[acc], pacc);
       tc_fence_after();
       if (threadIdx.x == 0 && rank == 0) trace_ev(p, 4, k);
@@ -728,15 +769,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         in_range = m < p.Mv;
       }
       const int r = q >> 1, c = q & 1;
+      const int fbase = nt * p.NT + (hf ? (hf - 1) * (p.NT / 2) : 0);
       const bool ok = in_range && i < p.rows[q] && j < p.cols[q] && !(p.debug & 1);
       YT* dst = reinterpret_cast<YT*>(p.y) +
                 ((long long)((long long)b * p.out_h + p.ostride * i + r) * p.out_w + p.ostride * j + c) *
                     p.cout +
-                nt * p.NT;
-      const int fmax = p.cout - nt * p.NT;  // features of this tile that exist
+                fbase;
+      const int fmax = p.cout - fbase;  // features of this tile that exist
       const float osc = p.split ? __ldg(p.split_inv_scale) : 1.0f;
 #pragma unroll 1
-      for (int c0 = 0; c0 < p.NT; c0 += 32) {
+      for (int c0 = 0; c0 < (hf ? p.NT / 2 : p.NT); c0 += 32) {
         float v[32];
         tmem_ld32(lane_base + (uint32_t)(acc * p.NT * (p.split ? 2 : 1) + c0), v);
         if (p.split) {
@@ -751,7 +793,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint32_t w[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
-              const int f = nt * p.NT + c0 + 2 * e;
+              const int f = fbase + c0 + 2 * e;
               const __nv_bfloat162 h = __floats2bfloat162_rn(finish<ACT>(v[2 * e], p.bias, p.epi, f),
                                                              finish<ACT>(v[2 * e + 1], p.bias, p.epi, f + 1));
               w[e] = *reinterpret_cast<const uint32_t*>(&h);
@@ -763,7 +805,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             float4* o = reinterpret_cast<float4*>(dst + c0);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-              const int f = nt * p.NT + c0 + 4 * e;
+              const int f = fbase + c0 + 4 * e;
               o[e] = make_float4(finish<ACT>(v[4 * e], p.bias, p.epi, f),
                                  finish<ACT>(v[4 * e + 1], p.bias, p.epi, f + 1),
                                  finish<ACT>(v[4 * e + 2], p.bias, p.epi, f + 2),
@@ -773,7 +815,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         } else {
 #pragma unroll
           for (int e = 0; e < 32; ++e)
-            if (c0 + e < fmax) dst[c0 + e] = from_f<YT>(finish<ACT>(v[e], p.bias, p.epi, nt * p.NT + c0 + e));
+            if (c0 + e < fmax) dst[c0 + e] = from_f<YT>(finish<ACT>(v[e], p.bias, p.epi, fbase + c0 + e));
         }
       }
       tc_fence_before();
@@ -866,6 +908,11 @@ bool tc_wide_fits(int kh, int kw, int p, int cin, int cout) {
 
 // xs: the [hi | lo] fp16 copy of an fp32 input (SPLIT); any aligned pointer
 // when only checking support
+static int wide_bprod() {
+  static const int v = getenv("SEGCONV_WIDE_BPROD") ? atoi(getenv("SEGCONV_WIDE_BPROD")) : 1;
+  return v ? 1 : 0;
+}
+
 static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, const void* xs = nullptr) {
   p = tcw::Params{};
   const bool split = pr.x_dtype == SEGCONV_F32 && pr.panel_dtype == SEGCONV_F16_SPLIT;
@@ -943,8 +990,10 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
     // BASELINE shape -- C3 89.7 -> 79.9 us (78 % useful rows), C5 237 -> 138 us
     // -- the extra per-tap A gathers are L2 hits, the saved MMA rows are not
     p.im2col = 1;
+  p.bprod = wide_bprod();
     const char* e = getenv("SEGCONV_WIDE_IM2COL");
     if (e && !split && !tf32) p.im2col = atoi(e) ? 1 : 0;  // split / tf32 need im2col staging
+    p.bprod = p.im2col ? wide_bprod() : 0;
   }
   // halo-shift staging (SEGCONV_WIDE_IM2COL=0) limits: the staged rows must fit
   // one TMA box; they do not constrain the im2col path (e.g. 128 x 128 maps)
@@ -1108,6 +1157,7 @@ static bool make_wide_dgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
   p.n_tiles = (pr.cin + p.NT - 1) / p.NT;
   p.nkb = pr.cout / tcw::KB;
   p.im2col = 1;
+  p.bprod = wide_bprod();
   p.S_rows = 128;
   p.taps[0] = taps;
   for (int U = 0; U < pr.kh; ++U)
@@ -1354,6 +1404,7 @@ static bool make_wide_conv(const void* src, int batch, int h, int w, int cin, co
   p.n_tiles = (cout + p.NT - 1) / p.NT;
   p.nkb = cin / tcw::KB;
   p.im2col = 1;
+  p.bprod = wide_bprod();
   p.S_rows = 128;
   p.taps[0] = taps;
   for (int u = 0; u < kh; ++u)
@@ -1450,6 +1501,18 @@ static cudaError_t launch_wide_t(const tcw::Params& prm, const tcw::Maps& maps, 
   long long pairs = std::min<long long>(prm.units, sms / 2);
   if (prm.mode == 1 && prm.w_share > 0)  // stream-K: every pair with a share of chunk-units
     pairs = (prm.units * prm.w_chunks + prm.w_share - 1) / prm.w_share;
+  tcw::Params pk = prm;
+  // last partial wave: when its T units fit twice over, run them as 2T feature
+  // half-tiles (N = NT/2) so the wave takes half a unit instead of a whole one
+  static const bool tail_split = !getenv("SEGCONV_WIDE_TAIL") || atoi(getenv("SEGCONV_WIDE_TAIL")) != 0;
+  if (tail_split && prm.mode == 0 && prm.im2col && prm.NT >= 128 && pairs > 0) {
+    const long long T = prm.units % pairs;
+    if (T > 0 && 2 * T <= pairs) {
+      pk.tail_on = 1;
+      pk.tail_full = prm.units - T;
+      pk.units = prm.units + T;
+    }
+  }
   const size_t smem = (size_t)prm.stages_a * prm.a_stage_bytes + (size_t)prm.stages_b * prm.b_stage_bytes +
                       (2 * tcw::MAX_STAGES_A + 2 * tcw::MAX_STAGES_B + 4) * 8 + 16;
   cudaLaunchConfig_t cfg = {};
@@ -1467,7 +1530,7 @@ static cudaError_t launch_wide_t(const tcw::Params& prm, const tcw::Maps& maps, 
   cfg.attrs = at;
   static const bool pdl = getenv("SEGCONV_NO_PDL") == nullptr;
   cfg.numAttrs = pdl ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm, maps);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, pk, maps);
   if (e == cudaSuccess) note_launch();
   return e;
 }

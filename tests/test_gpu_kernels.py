@@ -350,3 +350,22 @@ def test_pair_kernel_tf32(batch, n, cin, cout, ks, p, act):
     ki = rng.integers(-2, 3, (ks, ks, cin, cout)).astype(np.float32)
     got, _ = run(xi, ki, p, "tf32")
     assert np.array_equal(got, oracle.tconv_fused(xi, ki, p))  # small integers are exact in tf32
+
+
+@pytest.mark.parametrize("math,batch,cin,cout,ks,p", [
+    ("bf16", 24, 64, 128, 4, 0),    # 4 classes x 19 pair tiles = 76 units on 74 pairs: 2 split
+    ("bf16", 24, 64, 256, 4, 0),    # NT = 256 halves
+    ("bf16", 12, 64, 384, 4, 0),    # two feature tiles, the second one split
+    ("f16x3", 24, 64, 128, 4, 0),   # split-fp16 passes on half tiles
+    ("tf32", 24, 64, 128, 4, 0),
+])
+def test_pair_kernel_tail_half_tiles(math, batch, cin, cout, ks, p):
+    """The pair kernel runs the units of a last, partial wave as feature half-tiles
+    (N = NT / 2, two pairs per unit) when they fit twice over: every output
+    feature of those units must still be written once, exactly."""
+    rng = np.random.default_rng(batch + cout)
+    x = rng.integers(-3, 4, (batch, 16, 16, cin)).astype(np.float32)
+    k = rng.integers(-2, 3, (ks, ks, cin, cout)).astype(np.float32)
+    got, path = run(x, k, p, math, out_dtype=torch.float32)
+    assert path == "tc-pair"
+    assert np.array_equal(got, oracle.tconv_fused(x, k, p))
