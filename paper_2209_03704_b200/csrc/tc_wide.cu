@@ -378,8 +378,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int NT2 = p.NT / 2;
   const uint32_t a_tx = (uint32_t)p.S_rows * 128, b_tx = (uint32_t)NT2 * 128;
 
-  if (warp == 4) {
+  if (warp == 4 || (warp == 6 && p.mode == 1 && p.bprod)) {
     // ===== TMA producer (both CTAs): own halo rows and own half of the features
+    // (WGRAD with bprod: warp 4 streams the x rows, warp 6 the gy im2col rows)
+    const bool doA = warp == 4, doB = warp == 6 || !p.bprod;
     if (lane == 0 && p.mode == 1) {
       griddep_wait();
       int sa = 0, sb = 0;
@@ -399,6 +401,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         i0 /= p.w_in_w;
         for (long long c = cb; c < ce; ++c) {
           const long long m = c * WCH;
+          if (doA) {
           mbar_wait(&a_empty[sa], pa ^ 1);
           const uint32_t af = mapa(smem_u32(&a_full[sa]), 0);
           if (rank == 0) mbar_arrive_expect_tx(&a_full[sa], 2 * 2 * WCH * 128);
@@ -409,6 +412,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             sa = 0;
             pa ^= 1;
           }
+          }
+          if (doB) {
           mbar_wait(&b_empty[sb], pb ^ 1);
           const uint32_t bf = mapa(smem_u32(&b_full[sb]), 0);
           if (rank == 0) mbar_arrive_expect_tx(&b_full[sb], 2 * (uint32_t)(NT2 / 64) * WCH * 128);
@@ -420,6 +425,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (++sb == SB) {
             sb = 0;
             pb ^= 1;
+          }
           }
           j0 += dj;
           i0 += di;
@@ -434,7 +440,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
-    } else if (lane == 0) {
+    } else if (lane == 0 && p.mode != 1) {
       griddep_wait();  // activations come from the previous kernel (stack layer)
       int sa = 0, sb = 0;
       uint32_t pa = 0, pb = 0;
@@ -520,7 +526,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (rank == 0) trace_ev(p, 0, k);
       }
     }
-  } else if (warp == 6) {
+  } else if (warp == 6 && p.mode != 1) {
     // ===== IM2COL B producer (both CTAs): the weight tiles of every (pass, kb, tap)
     // step, in the A producer's order -- two serial issue chains instead of one
     if (lane == 0 && p.bprod) {
@@ -1239,6 +1245,7 @@ static bool make_wide_dgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
 // launch_wgrad_reduce sums in split order (deterministic).
 static bool make_wide_wgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps& maps, int pairs) {
   p = tcw::Params{};
+  p.bprod = wide_bprod();
   p.ab_fmt = 1;  // bf16 operands
   p.kbc = tcw::KB;
   if (pr.dtype != SEGCONV_BF16 || pr.batch < 1) return false;
