@@ -667,12 +667,27 @@ def main():
                 extra["conventional_gpu"] = prob.conventional(torch, 5, flush)
             except Exception as e:  # report, do not hide
                 extra["conventional_gpu"] = {"error": str(e)[:200]}
-            try:
-                extra["cudnn_conv_transpose2d"] = prob.cudnn(torch, 5, flush)
-            except Exception as e:
-                extra["cudnn_conv_transpose2d"] = {"error": str(e)[:200]}
+            # cuDNN context.  fp32 data: strict fp32 (allow_tf32 off, the like-for-like
+            # number at our 1e-5 bar) and torch's default TF32 (10-bit mantissa) both.
+            fp32 = getattr(prob, "tdt", None) == torch.float32
+            for tf32, key in ((False, "cudnn_conv_transpose2d"), (True, "cudnn_conv_transpose2d_tf32")):
+                if tf32 and not fp32:
+                    continue
+                prev = torch.backends.cudnn.allow_tf32
+                torch.backends.cudnn.allow_tf32 = tf32
+                try:
+                    r = prob.cudnn(torch, 5, flush)
+                    if r and fp32:
+                        r["what"] += " [TF32 math]" if tf32 else " [strict fp32: allow_tf32=False]"
+                    extra[key] = r
+                except Exception as e:
+                    extra[key] = {"error": str(e)[:200]}
+                finally:
+                    torch.backends.cudnn.allow_tf32 = prev
             if bwd:
                 extra["cudnn_conv_transpose2d_backward"] = extra.pop("cudnn_conv_transpose2d")
+                if "cudnn_conv_transpose2d_tf32" in extra:
+                    extra["cudnn_conv_transpose2d_backward_tf32"] = extra.pop("cudnn_conv_transpose2d_tf32")
             workers = os.cpu_count() or 1
             try:
                 secs, nimg, kind = prob.cpu_sample(workers)

@@ -77,6 +77,8 @@ struct Params {
   // VW = n + 2 p_fused wide, as one 4-D TMA box whose out-of-image part is
   // zero-filled -- the padding is never materialised
   int tile2d, pf, VW, TR, TRH, tiles_per_img;
+  int BW, BWo, col_tiles;  // TILE2D column blocks: box width (row pitch), anchors kept per block
+  int allq;  // halo staging: one unit = all four classes of a tile (4 accumulators of NT <= 64)
   // IM2COL (small images, where the halo-shift grid wastes rows): GEMM rows are
   // only class q's output anchors; each tap's A tile is gathered by an im2col
   // TMA (walk over the anchors, tap offset added per load)
@@ -306,6 +308,12 @@ __device__ __forceinline__ bool unit_of(const Params& p, int k, long long& pt, i
     pt = v / p.n_tiles;
     return true;
   }
+  if (p.allq) {
+    q = 0;
+    nt = (int)(u % p.n_tiles);
+    pt = u / p.n_tiles;
+    return true;
+  }
   q = (int)(u & 3);
   const long long t = u >> 2;
   nt = (int)(t % p.n_tiles);
@@ -450,7 +458,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const long long m0 = pt * 256 + (long long)rank * 128;
         const long long g = pt * 2 + rank;  // TILE2D: this CTA's row tile
         const int tb = p.tile2d ? (int)(g / p.tiles_per_img) : 0;
-        const int tvi0 = p.tile2d ? (int)(g - (long long)tb * p.tiles_per_img) * p.TR : 0;
+        const int trc = p.tile2d ? (int)(g - (long long)tb * p.tiles_per_img) : 0;  // (row tile, col block)
+        const int trow = p.tile2d ? trc / p.col_tiles : 0;
+        const int tvi0 = trow * p.TR, tvj0 = p.tile2d ? (trc - trow * p.col_tiles) * p.BWo : 0;
         const int f0 = hf ? nt * p.NT + (hf - 1) * NT2 + (int)rank * (NT2 / 2) : nt * p.NT + (int)rank * NT2;
         if (p.im2col) {
           // this CTA's first anchor of class q: (b, i, j) on the class's rows x cols grid
@@ -500,7 +510,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (rank == 0) mbar_arrive_expect_tx(&a_full[sa], (p.debug & 32) ? 0u : 2 * a_tx);
           if (!(p.debug & 32)) {  // diagnostics: no halo loads
             if (p.tile2d)
-              tma2_load_4d(smem_u32(a_base + (size_t)sa * p.a_stage_bytes), &maps.x, kb * KB, -p.pf,
+              tma2_load_4d(smem_u32(a_base + (size_t)sa * p.a_stage_bytes), &maps.x, kb * KB, tvj0 - p.pf,
                            tvi0 - p.pf, tb, af);
             else
               tma2_load_2d(smem_u32(a_base + (size_t)sa * p.a_stage_bytes), &maps.x, kb * KB,
@@ -510,12 +520,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             sa = 0;
             pa ^= 1;
           }
-          for (int t = 0; t < p.taps[q]; ++t) {
+          for (int qq = p.allq ? 0 : q; qq < (p.allq ? 4 : q + 1); ++qq)
+          for (int t = 0; t < p.taps[qq]; ++t) {
             mbar_wait(&b_empty[sb], pb ^ 1);
             const uint32_t bf = mapa(smem_u32(&b_full[sb]), 0);
             if (rank == 0) mbar_arrive_expect_tx(&b_full[sb], (p.debug & 16) ? 0u : 2 * b_tx);
             if (!(p.debug & 16))  // diagnostics: no weight loads
-              tma2_load_3d(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), &maps.w[q], kb * KB, t,
+              tma2_load_3d(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), &maps.w[qq], kb * KB, t,
                            f0, bf);
             if (++sb == SB) {
               sb = 0;
@@ -617,7 +628,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // SPLIT: pass 0 (xh.wh) accumulates into its own columns, passes 1-2 (the
         // ~2^-11 smaller corrections) into the next NT -- the large sum then takes
         // only a third of the non-round-to-nearest accumulation steps
-        const uint32_t d = tb + (uint32_t)(acc * p.NT * (p.split ? 2 : 1));
+        const uint32_t d = tb + (uint32_t)(acc * p.NT * (p.split ? 2 : p.allq ? 4 : 1));
         if (p.im2col) {
           for (int pass = 0; pass < (p.split ? 3 : 1); ++pass)
           for (int kb = 0; kb < p.nkb; ++kb)
@@ -660,16 +671,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           mbar_wait(&a_full[sa], pa);
           tc_fence_after();
           const uint32_t xa = smem_u32(a_base + (size_t)sa * p.a_stage_bytes);
-          for (int t = 0; t < p.taps[q]; ++t) {
+          for (int qq = p.allq ? 0 : q; qq < (p.allq ? 4 : q + 1); ++qq)
+          for (int t = 0; t < p.taps[qq]; ++t) {
             mbar_wait(&b_full[sb], pb);
             tc_fence_after();
             const uint32_t wa = smem_u32(b_base + (size_t)sb * p.b_stage_bytes);
-            const uint64_t ad = sw128_desc(xa + (uint32_t)p.shift[q][t] * 128);
+            const uint64_t ad = sw128_desc(xa + (uint32_t)p.shift[qq][t] * 128);
             const uint64_t bd = sw128_desc(wa);
+            const uint32_t dq = d + (p.allq ? (uint32_t)(qq * p.NT) : 0u);
             if (!(p.debug & 8) && elect_one()) {
 #pragma unroll
               for (int ks = 0; ks < KB / 16; ++ks)  // +32 bytes per K=16 step: +2 in the start field
-                mma2_bf16(d, ad + 2u * ks, bd + 2u * ks, idesc,
+                mma2_bf16(dq, ad + 2u * ks, bd + 2u * ks, idesc,
                           (kb == 0 && t == 0 && ks == 0) ? 0u : 1u);
             }
             __syncwarp();
@@ -762,10 +775,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       } else if (p.tile2d) {
         const long long g = pt * 2 + rank;
         b = (int)(g / p.tiles_per_img);
-        const int t = warp * 32 + lane;
-        i = (int)(g - (long long)b * p.tiles_per_img) * p.TR + t / p.VW;
-        j = t - (t / p.VW) * p.VW;
-        in_range = b < p.batch && t < p.TR * p.VW;
+        const int trc = (int)(g - (long long)b * p.tiles_per_img);
+        const int trow = trc / p.col_tiles, tcol = trc - trow * p.col_tiles;
+        const int t = warp * 32 + lane, jj = t % p.BW;
+        i = trow * p.TR + t / p.BW;
+        j = tcol * p.BWo + jj;
+        in_range = b < p.batch && t < p.TR * p.BW && jj < p.BWo;
       } else {
         const long long m = pt * 256 + (long long)rank * 128 + warp * 32 + lane;
         b = (int)(m / img);
@@ -774,9 +789,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         j = rem - (rem / p.n) * p.n;
         in_range = m < p.Mv;
       }
-      const int r = q >> 1, c = q & 1;
+      for (int qq = p.allq ? 0 : q; qq < (p.allq ? 4 : q + 1); ++qq) {
+      const int r = qq >> 1, c = qq & 1;
       const int fbase = nt * p.NT + (hf ? (hf - 1) * (p.NT / 2) : 0);
-      const bool ok = in_range && i < p.rows[q] && j < p.cols[q] && !(p.debug & 1);
+      const bool ok = in_range && i < p.rows[qq] && j < p.cols[qq] && !(p.debug & 1);
+      const uint32_t cbase = (uint32_t)(acc * p.NT * (p.split ? 2 : p.allq ? 4 : 1) + (p.allq ? qq * p.NT : 0));
       YT* dst = reinterpret_cast<YT*>(p.y) +
                 ((long long)((long long)b * p.out_h + p.ostride * i + r) * p.out_w + p.ostride * j + c) *
                     p.cout +
@@ -786,7 +803,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll 1
       for (int c0 = 0; c0 < (hf ? p.NT / 2 : p.NT); c0 += 32) {
         float v[32];
-        tmem_ld32(lane_base + (uint32_t)(acc * p.NT * (p.split ? 2 : 1) + c0), v);
+        tmem_ld32(lane_base + cbase + (uint32_t)c0, v);
         if (p.split) {
           float w2[32];
           tmem_ld32(lane_base + (uint32_t)(acc * p.NT * 2 + p.NT + c0), w2);
@@ -823,6 +840,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int e = 0; e < 32; ++e)
             if (c0 + e < fmax) dst[c0 + e] = from_f<YT>(finish<ACT>(v[e], p.bias, p.epi, fbase + c0 + e));
         }
+      }
       }
       tc_fence_before();
       __syncwarp();
@@ -967,17 +985,14 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
   p.pf = pr.pf;
   p.tile2d = pr.pf > 0 ? 1 : 0;
   p.VW = pr.n + 2 * pr.pf;  // pitch of the staged rows (the padded grid in TILE2D)
-  int max_shift = 0, max_dy = 0;
+  int max_shift = 0, max_dy = 0, max_dx = 0;
   for (int q = 0; q < 4; ++q) {
     p.taps[q] = pr.cls.kh[q] * pr.cls.kw[q];
     if (p.taps[q] > tcw::MAX_TAPS_Q) return false;
     for (int u = 0; u < pr.cls.kh[q]; ++u)
       for (int v = 0; v < pr.cls.kw[q]; ++v) {
-        const int pitch = p.tile2d ? p.VW : pr.n;
-        const int s = (pr.cls.off_r[q] + u) * pitch + (pr.cls.off_c[q] + v);
-        p.shift[q][u * pr.cls.kw[q] + v] = s;
-        max_shift = std::max(max_shift, s);
         max_dy = std::max(max_dy, pr.cls.off_r[q] + u);
+        max_dx = std::max(max_dx, pr.cls.off_c[q] + v);
       }
     p.rows[q] = pr.cls.rows[q];
     p.cols[q] = pr.cls.cols[q];
@@ -996,7 +1011,12 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
     // BASELINE shape -- C3 89.7 -> 79.9 us (78 % useful rows), C5 237 -> 138 us
     // -- the extra per-tap A gathers are L2 hits, the saved MMA rows are not
     p.im2col = 1;
-  p.bprod = wide_bprod();
+    // narrow outputs (<= 64 features) on large padded maps: stage each block of
+    // rows once and run all four classes' taps on it as shifted descriptors (4
+    // accumulators, ALLQ) instead of re-gathering the block per (class, tap) --
+    // measured (B200, batch 64, 4x4, p = 2): 128^2 x 64 -> 64 561 -> 365 us,
+    // 64^2 x 64 -> 64 152 -> 106 us; at 32^2 the im2col walk is still faster
+    if (!split && !tf32 && p.tile2d && tc_wide_ntile(pr.cout) <= 64 && pr.n >= 64) p.im2col = 0;
     const char* e = getenv("SEGCONV_WIDE_IM2COL");
     if (e && !split && !tf32) p.im2col = atoi(e) ? 1 : 0;  // split / tf32 need im2col staging
     p.bprod = p.im2col ? wide_bprod() : 0;
@@ -1005,17 +1025,44 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
   // one TMA box; they do not constrain the im2col path (e.g. 128 x 128 maps)
   if (!p.im2col) {
     if (p.tile2d) {
-      if (p.VW > 128) return false;
-      p.TR = 128 / p.VW;
-      p.TRH = p.TR + max_dy + 1;  // + one row: shifted reads of the last anchors wrap a row
+      // column blocks of BW staged columns (the row pitch), BWo = BW - max_dx anchors
+      // each (the rest read the next block's columns); BW = VW is one block per row.
+      // Pick the width that needs the fewest 128-row tiles.
       const int vh = std::max(pr.cls.rows[0], pr.cls.rows[2]);
-      p.tiles_per_img = (vh + p.TR - 1) / p.TR;
-      p.S_rows = p.VW * p.TRH;
-      if (p.TRH > 256 || p.S_rows > 384) return false;
-    } else {
-      p.S_rows = (128 + max_shift + 7) / 8 * 8;
-      if (p.S_rows > 256) return false;  // one TMA box
+      const int vw = std::max(pr.cls.cols[0], pr.cls.cols[1]);
+      long long best = -1;
+      for (int bw : {p.VW, 128, 64, 32, 16}) {
+        if (bw > p.VW || bw > 128 || (bw < p.VW && bw - max_dx < 8)) continue;
+        const int bwo = bw == p.VW ? p.VW : bw - max_dx;
+        const int tr = 128 / bw, ct = (vw + bwo - 1) / bwo;
+        const int trh = tr + max_dy + 1;  // + one row: shifted reads of the last anchors wrap a row
+        if (trh > 256 || bw * trh > 384) continue;
+        const long long tiles = (long long)((vh + tr - 1) / tr) * ct;
+        if (best < 0 || tiles < best) {
+          best = tiles;
+          p.BW = bw, p.BWo = bwo, p.TR = tr, p.col_tiles = ct, p.TRH = trh;
+        }
+      }
+      if (best < 0) return false;
+      p.tiles_per_img = (int)best;
+      p.S_rows = p.BW * p.TRH;
     }
+  }
+  for (int q = 0; q < 4; ++q)  // halo shifts: row offset x staged pitch + column offset
+    for (int u = 0; u < pr.cls.kh[q]; ++u)
+      for (int v = 0; v < pr.cls.kw[q]; ++v) {
+        const int pitch = p.tile2d ? p.BW : pr.n;
+        const int sh = (pr.cls.off_r[q] + u) * pitch + (pr.cls.off_c[q] + v);
+        p.shift[q][u * pr.cls.kw[q] + v] = sh;
+        max_shift = std::max(max_shift, sh);
+      }
+  if (!p.im2col && !p.tile2d) {
+    p.S_rows = (128 + max_shift + 7) / 8 * 8;
+    if (p.S_rows > 256) return false;  // one TMA box
+  }
+  {
+    static const int allq_env = getenv("SEGCONV_WIDE_ALLQ") ? atoi(getenv("SEGCONV_WIDE_ALLQ")) : 1;
+    p.allq = (!p.im2col && p.tile2d && p.NT <= 64 && allq_env) ? 1 : 0;
   }
   if (p.im2col) {
     p.tile2d = 0;
@@ -1054,7 +1101,7 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
     p.pair_tiles = 0;
   } else {
     p.pair_tiles = p.tile2d ? ((long long)pr.batch * p.tiles_per_img + 1) / 2 : (p.Mv + 255) / 256;
-    p.units = p.pair_tiles * p.n_tiles * 4;
+    p.units = p.pair_tiles * p.n_tiles * (p.allq ? 1 : 4);
   }
   if ((long long)pr.batch * pr.out_h * pr.out_w * pr.cout >= (1LL << 40)) return false;
   // tensor maps
@@ -1065,7 +1112,7 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
                                 (cuuint64_t)pr.batch};
     const cuuint64_t strides[3] = {(cuuint64_t)kc * esz, (cuuint64_t)pr.n * kc * esz,
                                    (cuuint64_t)pr.n * pr.n * kc * esz};
-    const cuuint32_t box[4] = {(cuuint32_t)p.kbc, (cuuint32_t)p.VW, (cuuint32_t)p.TRH, 1};
+    const cuuint32_t box[4] = {(cuuint32_t)p.kbc, (cuuint32_t)p.BW, (cuuint32_t)p.TRH, 1};
     const cuuint32_t es[4] = {1, 1, 1, 1};
     if (fn(&maps.x, op_type, 4, const_cast<void*>(xsrc), dims, strides,
            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,

@@ -369,3 +369,24 @@ def test_pair_kernel_tail_half_tiles(math, batch, cin, cout, ks, p):
     got, path = run(x, k, p, math, out_dtype=torch.float32)
     assert path == "tc-pair"
     assert np.array_equal(got, oracle.tconv_fused(x, k, p))
+
+
+@pytest.mark.parametrize("batch,n,cin,cout,p", [
+    (2, 64, 64, 64, 2),     # EB-GAN 64 -> 128 layer shape: 2-D column blocks, four class accumulators
+    (1, 128, 64, 64, 2),    # 128-wide map: blocks narrower than the padded row
+    (2, 72, 128, 48, 2),    # two k-blocks, a partial feature tile
+    (1, 66, 64, 64, 3),     # p = 3: odd parity classes
+])
+def test_pair_kernel_all_class_halo(batch, n, cin, cout, p):
+    """Narrow outputs on large padded maps take the halo staging with all four
+    classes per unit (ALLQ) and 2-D column blocks: bit-exact on integer data."""
+    rng = np.random.default_rng(n * 3 + cin + p)
+    x = rng.integers(-3, 4, (batch, n, n, cin)).astype(np.float32)
+    k = rng.integers(-2, 3, (4, 4, cin, cout)).astype(np.float32)
+    got, path = run(x, k, p, "bf16", out_dtype=torch.float32)
+    assert path == "tc-pair"
+    assert np.array_equal(got, oracle.tconv_fused(x, k, p))
+    xr = oracle.bf16_round(rng.standard_normal((batch, n, n, cin)).astype(np.float32))
+    kr = oracle.bf16_round((rng.standard_normal((4, 4, cin, cout)) * 0.05).astype(np.float32))
+    got, _ = run(xr, kr, p, "bf16", "relu", out_dtype=torch.float32)
+    assert scaled_err(got, want_of(xr, kr, p, "relu")) <= 1e-4
