@@ -79,6 +79,8 @@ struct Params {
   int tile2d, pf, VW, TR, TRH, tiles_per_img;
   int BW, BWo, col_tiles;  // TILE2D column blocks: box width (row pitch), anchors kept per block
   int allq;  // halo staging: one unit = all four classes of a tile (4 accumulators of NT <= 64)
+  int wres;  // ALLQ with one feature tile: every (kb, class, tap) weight tile resident in SMEM
+  int tap_base[4];  // WRES: first tile of class q within a k-block
   // IM2COL (small images, where the halo-shift grid wastes rows): GEMM rows are
   // only class q's output anchors; each tap's A tile is gathered by an im2col
   // TMA (walk over the anchors, tap offset added per load)
@@ -328,6 +330,17 @@ __device__ __forceinline__ float finish(float v, const float* bias, unsigned epi
   if (ACT == 2) v = tanhf(v);
   return v;
 }
+// bf16 outputs: the hardware tanh (max relative error ~2^-11) is below the bf16
+// rounding of the result (2^-9); accurate tanhf dominated the epilogue of large
+// bf16 tanh layers (EB-GAN preset, whose last layer writes 256^2 x 64 per image:
+// 1.02 -> 0.80 ms per step)
+template <int ACT>
+__device__ __forceinline__ float finish_bf(float v, const float* bias, unsigned epi, int f) {
+  if (epi & SEGCONV_EPI_BIAS) v += __ldg(bias + f);
+  if (ACT == 1) v = fmaxf(v, 0.0f);
+  if (ACT == 2) asm("tanh.approx.f32 %0, %1;" : "=f"(v) : "f"(v));
+  return v;
+}
 
 template <typename YT, int ACT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
@@ -452,6 +465,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       griddep_wait();  // activations come from the previous kernel (stack layer)
       int sa = 0, sb = 0;
       uint32_t pa = 0, pb = 0;
+      if (p.wres && blockIdx.x / 2 < p.units) {  // all weight tiles once, on b_full[0]
+        const uint32_t bf = mapa(smem_u32(&b_full[0]), 0);
+        const int ntile = p.nkb * (p.taps[0] + p.taps[1] + p.taps[2] + p.taps[3]);
+        if (rank == 0) mbar_arrive_expect_tx(&b_full[0], 2 * b_tx * (uint32_t)ntile);
+        int idx = 0;
+        for (int kb = 0; kb < p.nkb; ++kb)
+          for (int qq = 0; qq < 4; ++qq)
+            for (int t = 0; t < p.taps[qq]; ++t, ++idx)
+              tma2_load_3d(smem_u32(b_base) + (uint32_t)idx * b_tx, &maps.w[qq], kb * KB, t, (int)rank * NT2, bf);
+      }
       long long pt;
       int nt, q, hf;
       for (int k = 0; unit_of(p, k, pt, nt, q, hf); ++k) {
@@ -520,6 +543,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             sa = 0;
             pa ^= 1;
           }
+          if (!p.wres)
           for (int qq = p.allq ? 0 : q; qq < (p.allq ? 4 : q + 1); ++qq)
           for (int t = 0; t < p.taps[qq]; ++t) {
             mbar_wait(&b_empty[sb], pb ^ 1);
@@ -620,6 +644,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       long long pt;
       int nt, q, hf;
       const uint32_t idesc_full = idesc_f16_m256(p.ab_fmt, p.NT), idesc_half = idesc_f16_m256(p.ab_fmt, p.NT / 2);
+      if (p.wres && blockIdx.x / 2 < p.units) {  // resident weight tiles
+        mbar_wait(&b_full[0], 0);
+        tc_fence_after();
+      }
       for (int k = 0; unit_of(p, k, pt, nt, q, hf); ++k) {
         const uint32_t idesc = hf ? idesc_half : idesc_full;
         mbar_wait(&acc_empty[acc], pacc ^ 1);
@@ -673,9 +701,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const uint32_t xa = smem_u32(a_base + (size_t)sa * p.a_stage_bytes);
           for (int qq = p.allq ? 0 : q; qq < (p.allq ? 4 : q + 1); ++qq)
           for (int t = 0; t < p.taps[qq]; ++t) {
-            mbar_wait(&b_full[sb], pb);
-            tc_fence_after();
-            const uint32_t wa = smem_u32(b_base + (size_t)sb * p.b_stage_bytes);
+            if (!p.wres) {
+              mbar_wait(&b_full[sb], pb);
+              tc_fence_after();
+            }
+            const uint32_t wa = p.wres ? smem_u32(b_base) + (uint32_t)((kb * p.tap_base[3] + kb * p.taps[3] +
+                                                                        p.tap_base[qq] + t) * NT2 * 128)
+                                       : smem_u32(b_base + (size_t)sb * p.b_stage_bytes);
             const uint64_t ad = sw128_desc(xa + (uint32_t)p.shift[qq][t] * 128);
             const uint64_t bd = sw128_desc(wa);
             const uint32_t dq = d + (p.allq ? (uint32_t)(qq * p.NT) : 0u);
@@ -686,6 +718,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                           (kb == 0 && t == 0 && ks == 0) ? 0u : 1u);
             }
             __syncwarp();
+            if (p.wres) continue;
             if (elect_one()) commit2(&b_empty[sb]);
             __syncwarp();
             if (++sb == SB) {
@@ -817,8 +850,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
               const int f = fbase + c0 + 2 * e;
-              const __nv_bfloat162 h = __floats2bfloat162_rn(finish<ACT>(v[2 * e], p.bias, p.epi, f),
-                                                             finish<ACT>(v[2 * e + 1], p.bias, p.epi, f + 1));
+              const __nv_bfloat162 h = __floats2bfloat162_rn(finish_bf<ACT>(v[2 * e], p.bias, p.epi, f),
+                                                             finish_bf<ACT>(v[2 * e + 1], p.bias, p.epi, f + 1));
               w[e] = *reinterpret_cast<const uint32_t*>(&h);
             }
             uint4* o = reinterpret_cast<uint4*>(dst + c0);
@@ -838,7 +871,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         } else {
 #pragma unroll
           for (int e = 0; e < 32; ++e)
-            if (c0 + e < fmax) dst[c0 + e] = from_f<YT>(finish<ACT>(v[e], p.bias, p.epi, fbase + c0 + e));
+            if (c0 + e < fmax)
+              dst[c0 + e] = from_f<YT>(sizeof(YT) == 2 ? finish_bf<ACT>(v[e], p.bias, p.epi, fbase + c0 + e)
+                                                       : finish<ACT>(v[e], p.bias, p.epi, fbase + c0 + e));
         }
       }
       }
@@ -1063,6 +1098,13 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
   {
     static const int allq_env = getenv("SEGCONV_WIDE_ALLQ") ? atoi(getenv("SEGCONV_WIDE_ALLQ")) : 1;
     p.allq = (!p.im2col && p.tile2d && p.NT <= 64 && allq_env) ? 1 : 0;
+    static const int wres_env = getenv("SEGCONV_WIDE_WRES") ? atoi(getenv("SEGCONV_WIDE_WRES")) : 1;
+    p.wres = (p.allq && p.n_tiles == 1 && wres_env) ? 1 : 0;
+    int tb = 0;
+    for (int q = 0; q < 4; ++q) {
+      p.tap_base[q] = tb;
+      tb += p.taps[q];
+    }
   }
   if (p.im2col) {
     p.tile2d = 0;
@@ -1082,7 +1124,13 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
   if (p.im2col) {  // A and B both per (k-block, tap): paired rings
     p.stages_a = p.stages_b = std::min(tcw::MAX_STAGES_A, budget / (p.a_stage_bytes + p.b_stage_bytes));
     if (p.stages_a < 2) return false;
-  } else {
+  } else if (p.wres) {  // one "stage" holding every weight tile, A ring in the rest
+    p.b_stage_bytes *= p.nkb * (p.tap_base[3] + p.taps[3]);
+    p.stages_b = 1;
+    p.stages_a = std::min(tcw::MAX_STAGES_A, (budget - p.b_stage_bytes) / p.a_stage_bytes);
+    if (p.stages_a < 2) p.wres = 0, p.b_stage_bytes = (p.NT / 2) * 128;
+  }
+  if (!p.im2col && !p.wres) {
     p.stages_a = 3;
     p.stages_b = std::min(tcw::MAX_STAGES_B, (budget - p.stages_a * p.a_stage_bytes) / p.b_stage_bytes);
     if (p.stages_b < 4) {

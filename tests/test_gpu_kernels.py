@@ -390,3 +390,14 @@ def test_pair_kernel_all_class_halo(batch, n, cin, cout, p):
     kr = oracle.bf16_round((rng.standard_normal((4, 4, cin, cout)) * 0.05).astype(np.float32))
     got, _ = run(xr, kr, p, "bf16", "relu", out_dtype=torch.float32)
     assert scaled_err(got, want_of(xr, kr, p, "relu")) <= 1e-4
+
+
+@pytest.mark.parametrize("n,cin,cout,p", [(16, 128, 64, 2), (64, 64, 64, 2), (8, 256, 128, 0)])
+def test_pair_kernel_bf16_output_tanh(n, cin, cout, p):
+    """bf16 outputs take the hardware tanh (error ~2^-11, below bf16 rounding)."""
+    rng = np.random.default_rng(n + cin + cout)
+    x = oracle.bf16_round(rng.standard_normal((2, n, n, cin)).astype(np.float32))
+    k = oracle.bf16_round((rng.standard_normal((4, 4, cin, cout)) * 0.05).astype(np.float32))
+    got, path = run(x, k, p, "bf16", "tanh")
+    assert path == "tc-pair"
+    assert scaled_err(got, want_of(x, k, p, "tanh")) <= TOL_TC
