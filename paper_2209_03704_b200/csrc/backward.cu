@@ -554,6 +554,179 @@ __global__ void wgrad_reduce_streamk(const float* __restrict__ ws, float* __rest
   gk[e] = s;
 }
 
+
+// ------------------------------------------------- narrow outputs (cout <= 4)
+// The C4 family (5x5 -> 3 at 256^2): the packed FFMA tiles above leave most of
+// every tile's K (or N) idle and gather g element by element.  Here a CTA owns
+// one input row segment of 128 pixels x 64 channels; the g rows its pixels read
+// (kh rows x (2*128 + kw) columns x CO features) and the 64-channel slice of the
+// kernel are staged once in SMEM.
+constexpr int NW_PX = 128, NW_CH = 64, NW_MAXK = 7;
+
+__host__ __device__ constexpr int nw_gw(int kw) { return 2 * NW_PX + kw; }
+
+// stage g rows y = 2i + p - U (U < kh) at columns [2 j0 + p - (kw - 1), +gw) as
+// sg[(U * gw + col) * CO + f]; zero outside g
+template <typename T, int CO>
+__device__ __forceinline__ void nw_stage_g(const T* __restrict__ gy, float* sg, const BackwardProblem& pr, int b,
+                                           int i, int j0) {
+  const int gw = nw_gw(pr.kw), c0 = 2 * j0 + pr.p - (pr.kw - 1);
+  for (int U = 0; U < pr.kh; ++U) {
+    const int y = 2 * i + pr.p - U;
+    const bool yok = y >= 0 && y < pr.out_h;
+    const T* grow = gy + ((long long)b * pr.out_h + (yok ? y : 0)) * pr.out_w * CO;
+    float* srow = sg + U * gw * CO;
+    for (int e = threadIdx.x; e < gw * CO; e += blockDim.x) {
+      const int xx = c0 + e / CO;  // CO is a compile-time constant: a multiply-shift
+      srow[e] = (yok && xx >= 0 && xx < pr.out_w) ? to_acc(grow[(long long)c0 * CO + e]) : 0.f;
+    }
+  }
+}
+
+// gx: lane = (pixel half, 4 channels); 8 pixels per thread (slots 16 apart) --
+// per (U, V, f): one LDS.128 of weights + 8 broadcast g loads for 32 FFMA; a
+// half-warp stores one pixel's 64 channels as 256 contiguous bytes
+template <typename T, int CO>
+__global__ void __launch_bounds__(256) dgrad_narrow(const T* __restrict__ gy, const T* __restrict__ k,
+                                                    T* __restrict__ gx, BackwardProblem pr) {
+  extern __shared__ float nsm[];
+  const int taps = pr.kh * pr.kw, gw = nw_gw(pr.kw);
+  float* sw = nsm;                        // [(tap * CO + f) * 64 + c]
+  float* sg = nsm + taps * CO * NW_CH;    // [(U * gw + col) * CO + f]
+  const int j0 = blockIdx.y * NW_PX, cb = blockIdx.z * NW_CH;
+  for (int e = threadIdx.x; e < taps * CO * NW_CH; e += blockDim.x) {
+    const int c = e & (NW_CH - 1), tf = e / NW_CH;  // tf = tap * CO + f
+    sw[e] = cb + c < pr.cin ? to_acc(k[((long long)(tf / CO) * pr.cin + cb + c) * CO + tf % CO]) : 0.f;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c4 = lane & 15, slot = warp * 2 + (lane >> 4);
+  const int total_rows = pr.batch * pr.in_h;
+  // the CTA's rows (weights stay staged): blockIdx.x, + gridDim.x, ...
+  for (int row = blockIdx.x; row < total_rows; row += gridDim.x) {
+  const int b = row / pr.in_h, i = row - (row / pr.in_h) * pr.in_h;
+  __syncthreads();  // previous row's g reads are done
+  nw_stage_g<T, CO>(gy, sg, pr, b, i, j0);
+  __syncthreads();
+  float acc[8][4] = {};
+  for (int U = 0; U < pr.kh; ++U)
+    for (int V = 0; V < pr.kw; ++V) {
+      const float* gp = sg + ((U * gw) + 2 * slot + pr.kw - 1 - V) * CO;
+      const float* wp = sw + ((U * pr.kw + V) * CO) * NW_CH + 4 * c4;
+#pragma unroll
+      for (int f = 0; f < CO; ++f) {
+        const float4 w = *reinterpret_cast<const float4*>(wp + f * NW_CH);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float g = gp[32 * e * CO + f];  // pixel slot + 16 e: column + 32 e
+          acc[e][0] = fmaf(g, w.x, acc[e][0]);
+          acc[e][1] = fmaf(g, w.y, acc[e][1]);
+          acc[e][2] = fmaf(g, w.z, acc[e][2]);
+          acc[e][3] = fmaf(g, w.w, acc[e][3]);
+        }
+      }
+    }
+  const int ch = cb + 4 * c4;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int j = j0 + slot + 16 * e;
+    if (j >= pr.in_w) continue;
+    T* o = gx + ((long long)row * pr.in_w + j) * pr.cin + ch;
+    if constexpr (sizeof(T) == 4) {
+      if (ch + 4 <= pr.cin && (pr.cin & 3) == 0) {
+        *reinterpret_cast<float4*>(o) = make_float4(acc[e][0], acc[e][1], acc[e][2], acc[e][3]);
+        continue;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (ch + c < pr.cin) o[c] = from_acc<T>(acc[e][c]);
+  }
+  }
+}
+
+// gk partials: a CTA sums `rows` consecutive input rows (all columns, 64
+// channels).  Four pixel phases of 64 threads (pixels px = phase mod 4); a
+// thread owns 8 channels x 10 (tap, f) columns: per pixel 2 LDS.128 of x +
+// 10 g loads for 80 FFMA.  Each phase writes its own partial (split).
+template <typename T, int CO>
+__global__ void __launch_bounds__(256) wgrad_narrow(const T* __restrict__ x, const T* __restrict__ gy,
+                                                    float* __restrict__ ws, BackwardProblem pr, int rows) {
+  extern __shared__ float nsm[];
+  const int gw = nw_gw(pr.kw);
+  float* sx = nsm;                          // [px][68]
+  float* sg = nsm + NW_PX * (NW_CH + 4);    // [(U * gw + col) * CO + f]
+  const int cb = blockIdx.y * NW_CH;
+  const int ph = threadIdx.x >> 6, t64 = threadIdx.x & 63;
+  const int c8 = t64 & 7, cgp = t64 >> 3;
+  const int NP = pr.kh * pr.kw * CO;
+  int goff[10];
+#pragma unroll
+  for (int u = 0; u < 10; ++u) {
+    const int n = cgp + 8 * u;
+    const int tap = n < NP ? n / CO : 0, f = n < NP ? n - (n / CO) * CO : 0;
+    const int U = tap / pr.kw, V = tap - (tap / pr.kw) * pr.kw;
+    goff[u] = n < NP ? (U * gw + pr.kw - 1 - V) * CO + f : -1;
+  }
+  float acc[10][8] = {};
+  const int total_rows = pr.batch * pr.in_h;
+  const int r0 = blockIdx.x * rows, r1 = min(r0 + rows, total_rows);
+  for (int row = r0; row < r1; ++row) {
+    const int b = row / pr.in_h, i = row - (row / pr.in_h) * pr.in_h;
+    for (int j0 = 0; j0 < pr.in_w; j0 += NW_PX) {
+      __syncthreads();  // previous chunk's reads are done
+      for (int e = threadIdx.x; e < NW_PX * (NW_CH / 4); e += blockDim.x) {
+        const int px = e >> 4, c = (e & 15) * 4;
+        const int j = j0 + px;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j < pr.in_w) {
+          const T* xp = x + ((long long)row * pr.in_w + j) * pr.cin + cb + c;
+          if (sizeof(T) == 4 && cb + c + 4 <= pr.cin && (pr.cin & 3) == 0) {
+            v = __ldg(reinterpret_cast<const float4*>(xp));
+          } else {
+            v.x = cb + c < pr.cin ? to_acc(xp[0]) : 0.f;
+            v.y = cb + c + 1 < pr.cin ? to_acc(xp[1]) : 0.f;
+            v.z = cb + c + 2 < pr.cin ? to_acc(xp[2]) : 0.f;
+            v.w = cb + c + 3 < pr.cin ? to_acc(xp[3]) : 0.f;
+          }
+        }
+        *reinterpret_cast<float4*>(sx + px * (NW_CH + 4) + c) = v;
+      }
+      nw_stage_g<T, CO>(gy, sg, pr, b, i, j0);
+      __syncthreads();
+      const int npx = min(NW_PX, pr.in_w - j0);
+      for (int px = ph; px < npx; px += 4) {
+        const float4 xa = *reinterpret_cast<const float4*>(sx + px * (NW_CH + 4) + 8 * c8);
+        const float4 xb = *reinterpret_cast<const float4*>(sx + px * (NW_CH + 4) + 8 * c8 + 4);
+        const float* gp = sg + 2 * px * CO;
+#pragma unroll
+        for (int u = 0; u < 10; ++u) {
+          const float g = goff[u] >= 0 ? gp[goff[u]] : 0.f;
+          acc[u][0] = fmaf(xa.x, g, acc[u][0]);
+          acc[u][1] = fmaf(xa.y, g, acc[u][1]);
+          acc[u][2] = fmaf(xa.z, g, acc[u][2]);
+          acc[u][3] = fmaf(xa.w, g, acc[u][3]);
+          acc[u][4] = fmaf(xb.x, g, acc[u][4]);
+          acc[u][5] = fmaf(xb.y, g, acc[u][5]);
+          acc[u][6] = fmaf(xb.z, g, acc[u][6]);
+          acc[u][7] = fmaf(xb.w, g, acc[u][7]);
+        }
+      }
+    }
+  }
+  const long long ksz = (long long)pr.kh * pr.kw * pr.cin * CO;
+  float* out = ws + ((long long)blockIdx.x * 4 + ph) * ksz;
+#pragma unroll
+  for (int u = 0; u < 10; ++u) {
+    const int n = cgp + 8 * u;
+    if (n >= NP) continue;
+    const int tap = n / CO, f = n - (n / CO) * CO;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int ch = cb + 8 * c8 + c;
+      if (ch < pr.cin) out[((long long)tap * pr.cin + ch) * CO + f] = acc[u][c];
+    }
+  }
+}
 }  // namespace bwd
 
 cudaError_t launch_wgrad_reduce_streamk(const float* ws, float* gk, int cin, int cout, int taps, int nt_feat,
@@ -577,6 +750,82 @@ static int sm_count() {
   return sms;
 }
 
+static bool narrow_applies(const BackwardProblem& pr) {
+  static const bool off = getenv("SEGCONV_BWD_NARROW") && atoi(getenv("SEGCONV_BWD_NARROW")) == 0;
+  return !off && !pr.conv && pr.stride == 2 && pr.in_w >= 64 && pr.cout >= 1 && pr.cout <= 4 && pr.kh <= bwd::NW_MAXK &&
+         pr.kw <= bwd::NW_MAXK && pr.kh * pr.kw * pr.cout <= 80 && pr.in_h == pr.n && pr.in_w == pr.n &&
+         (pr.dtype == SEGCONV_F32 || pr.dtype == SEGCONV_BF16);
+}
+
+template <typename T, int CO>
+static cudaError_t narrow_dgrad_t(const BackwardProblem& pr, cudaStream_t s) {
+  const int gw = bwd::nw_gw(pr.kw);
+  const size_t smem = ((size_t)pr.kh * pr.kw * CO * bwd::NW_CH + (size_t)pr.kh * gw * CO) * sizeof(float);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(bwd::dgrad_narrow<T, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  const long long rows = (long long)pr.batch * pr.in_h;
+  const long long yz = (long long)((pr.in_w + bwd::NW_PX - 1) / bwd::NW_PX) * ((pr.cin + bwd::NW_CH - 1) / bwd::NW_CH);
+  const long long gx_rows = std::max(1LL, std::min(rows, (8LL * sm_count() + yz - 1) / yz));  // ~8 CTAs per SM
+  dim3 grid((unsigned)gx_rows, (unsigned)((pr.in_w + bwd::NW_PX - 1) / bwd::NW_PX),
+            (unsigned)((pr.cin + bwd::NW_CH - 1) / bwd::NW_CH));
+  bwd::dgrad_narrow<T, CO><<<grid, 256, smem, s>>>((const T*)pr.gy, (const T*)pr.k, (T*)pr.gx, pr);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) note_launch();
+  return e;
+}
+
+template <typename T>
+static cudaError_t narrow_dgrad(const BackwardProblem& pr, cudaStream_t s) {
+  switch (pr.cout) {
+    case 1: return narrow_dgrad_t<T, 1>(pr, s);
+    case 2: return narrow_dgrad_t<T, 2>(pr, s);
+    case 3: return narrow_dgrad_t<T, 3>(pr, s);
+    default: return narrow_dgrad_t<T, 4>(pr, s);
+  }
+}
+
+template <typename T, int CO>
+static cudaError_t narrow_wgrad_t(const BackwardProblem& pr, cudaStream_t s) {
+  const int gw = bwd::nw_gw(pr.kw);
+  const size_t smem = ((size_t)bwd::NW_PX * (bwd::NW_CH + 4) + (size_t)pr.kh * gw * CO) * sizeof(float);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(bwd::wgrad_narrow<T, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  const int chb = (pr.cin + bwd::NW_CH - 1) / bwd::NW_CH;
+  const long long total_rows = (long long)pr.batch * pr.in_h;
+  // ~2 CTAs per SM over (row range, channel block)
+  long long rows = std::max(1LL, (total_rows * chb + 2LL * sm_count() - 1) / (2LL * sm_count()));
+  const long long splits = (total_rows + rows - 1) / rows;
+  const long long ksz = (long long)pr.kh * pr.kw * pr.cin * pr.cout;
+  float* ws = nullptr;
+  cudaError_t e = workspace_alloc((void**)&ws, (size_t)splits * 4 * ksz * sizeof(float), s);
+  if (e != cudaSuccess) return e;
+  bwd::wgrad_narrow<T, CO><<<dim3((unsigned)splits, (unsigned)chb), 256, smem, s>>>(
+      (const T*)pr.x, (const T*)pr.gy, ws, pr, (int)rows);
+  e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    note_launch();
+    e = launch_wgrad_reduce(ws, (float*)pr.gk, ksz, (int)splits * 4, pr.accumulate, s);
+  }
+  cudaError_t e2 = cudaFreeAsync(ws, s);
+  return e != cudaSuccess ? e : e2;
+}
+
+template <typename T>
+static cudaError_t narrow_wgrad(const BackwardProblem& pr, cudaStream_t s) {
+  switch (pr.cout) {
+    case 1: return narrow_wgrad_t<T, 1>(pr, s);
+    case 2: return narrow_wgrad_t<T, 2>(pr, s);
+    case 3: return narrow_wgrad_t<T, 3>(pr, s);
+    default: return narrow_wgrad_t<T, 4>(pr, s);
+  }
+}
+
 template <typename T>
 static cudaError_t bwd_data_t(const BackwardProblem& pr, bool exact, cudaStream_t s) {
   const long long M = (long long)pr.batch * pr.in_h * pr.in_w;
@@ -592,6 +841,8 @@ static cudaError_t bwd_data_t(const BackwardProblem& pr, bool exact, cudaStream_
         bwd::dgrad_exact<T><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(
             (const T*)pr.gy, (const T*)pr.k, (T*)pr.gx, pr);
     }
+  } else if (sizeof(T) <= 4 && narrow_applies(pr)) {
+    if constexpr (sizeof(T) <= 4) return narrow_dgrad<T>(pr, s);
   } else {
     using ACC = typename std::conditional<sizeof(T) == 8, double, float>::type;
     dim3 grid((unsigned)((M + bwd::BM - 1) / bwd::BM), (unsigned)((pr.cin + bwd::BN - 1) / bwd::BN));
@@ -630,6 +881,10 @@ static cudaError_t bwd_weight_t(const BackwardProblem& pr, bool exact, cudaStrea
       if (e == cudaSuccess) note_launch();
       return e;
     }
+  }
+  if constexpr (sizeof(T) <= 4) {
+    static const bool wn = getenv("SEGCONV_BWD_NARROW_WGRAD") && atoi(getenv("SEGCONV_BWD_NARROW_WGRAD")) != 0;
+    if (wn && narrow_applies(pr) && M > 0) return narrow_wgrad<T>(pr, s);
   }
   // cout % 64 != 0: (tap, f) packed columns, all taps of a tile in one CTA
   const bool packed = pr.cout % bwd::BN != 0;

@@ -63,6 +63,9 @@ def test_exact_matches_reference_goldens_bit_for_bit():
     (2, 9, 130, 70, 3, 1),    # channel tiles past 128
     (4, 6, 16, 8, 1, 0),      # 1x1 kernel: classes without taps
     (2, 11, 128, 3, 3, 0),    # C5 layer d shape (fp32)
+    (1, 64, 64, 3, 5, 0),     # C4 family (narrow-output kernels), reduced size
+    (2, 20, 40, 1, 4, 2),     # narrow: partial channel block, one feature
+    (1, 130, 16, 4, 3, 1),    # narrow: rows wider than one 128-pixel segment
 ])
 def test_ffma_f32(b, n, cin, cout, k, p):
     rng = np.random.default_rng(b * 1000 + n * 10 + k)
@@ -81,7 +84,8 @@ def test_ffma_f32(b, n, cin, cout, k, p):
     assert (np.abs(gk - wk) <= 1e-5 * ak + 1e-7).all()
 
 
-@pytest.mark.parametrize("b,n,cin,cout,k,p", [(3, 6, 8, 5, 4, 2), (2, 12, 64, 32, 3, 0), (64, 4, 16, 16, 3, 1)])
+@pytest.mark.parametrize("b,n,cin,cout,k,p", [(3, 6, 8, 5, 4, 2), (2, 12, 64, 32, 3, 0), (64, 4, 16, 16, 3, 1),
+                                               (2, 33, 72, 3, 5, 0), (3, 9, 8, 2, 7, 3)])
 def test_ffma_int_exact(b, n, cin, cout, k, p):
     """Integer data: every partial sum is exact, so any summation order is bit-exact."""
     rng = np.random.default_rng(n * 7 + cin)
