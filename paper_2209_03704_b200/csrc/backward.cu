@@ -665,7 +665,7 @@ __global__ void __launch_bounds__(256) wgrad_narrow(const T* __restrict__ x, con
     const int n = cgp + 8 * u;
     const int tap = n < NP ? n / CO : 0, f = n < NP ? n - (n / CO) * CO : 0;
     const int U = tap / pr.kw, V = tap - (tap / pr.kw) * pr.kw;
-    goff[u] = n < NP ? (U * gw + pr.kw - 1 - V) * CO + f : -1;
+    goff[u] = (U * gw + pr.kw - 1 - V) * CO + f;  // columns past NP read a valid slot, never stored
   }
   float acc[10][8] = {};
   const int total_rows = pr.batch * pr.in_h;
@@ -694,13 +694,14 @@ __global__ void __launch_bounds__(256) wgrad_narrow(const T* __restrict__ x, con
       nw_stage_g<T, CO>(gy, sg, pr, b, i, j0);
       __syncthreads();
       const int npx = min(NW_PX, pr.in_w - j0);
+#pragma unroll 2
       for (int px = ph; px < npx; px += 4) {
         const float4 xa = *reinterpret_cast<const float4*>(sx + px * (NW_CH + 4) + 8 * c8);
         const float4 xb = *reinterpret_cast<const float4*>(sx + px * (NW_CH + 4) + 8 * c8 + 4);
         const float* gp = sg + 2 * px * CO;
 #pragma unroll
         for (int u = 0; u < 10; ++u) {
-          const float g = goff[u] >= 0 ? gp[goff[u]] : 0.f;
+          const float g = gp[goff[u]];
           acc[u][0] = fmaf(xa.x, g, acc[u][0]);
           acc[u][1] = fmaf(xa.y, g, acc[u][1]);
           acc[u][2] = fmaf(xa.z, g, acc[u][2]);
@@ -883,7 +884,7 @@ static cudaError_t bwd_weight_t(const BackwardProblem& pr, bool exact, cudaStrea
     }
   }
   if constexpr (sizeof(T) <= 4) {
-    static const bool wn = getenv("SEGCONV_BWD_NARROW_WGRAD") && atoi(getenv("SEGCONV_BWD_NARROW_WGRAD")) != 0;
+    static const bool wn = !getenv("SEGCONV_BWD_NARROW_WGRAD") || atoi(getenv("SEGCONV_BWD_NARROW_WGRAD")) != 0;
     if (wn && narrow_applies(pr) && M > 0) return narrow_wgrad<T>(pr, s);
   }
   // cout % 64 != 0: (tap, f) packed columns, all taps of a tile in one CTA
