@@ -751,7 +751,7 @@ static int sm_count() {
   return sms;
 }
 
-static bool narrow_applies(const BackwardProblem& pr) {
+bool bwd_narrow_applies(const BackwardProblem& pr) {
   static const bool off = getenv("SEGCONV_BWD_NARROW") && atoi(getenv("SEGCONV_BWD_NARROW")) == 0;
   return !off && !pr.conv && pr.stride == 2 && pr.in_w >= 64 && pr.cout >= 1 && pr.cout <= 4 && pr.kh <= bwd::NW_MAXK &&
          pr.kw <= bwd::NW_MAXK && pr.kh * pr.kw * pr.cout <= 80 && pr.in_h == pr.n && pr.in_w == pr.n &&
@@ -842,7 +842,7 @@ static cudaError_t bwd_data_t(const BackwardProblem& pr, bool exact, cudaStream_
         bwd::dgrad_exact<T><<<(unsigned)((total + 255) / 256), 256, 0, s>>>(
             (const T*)pr.gy, (const T*)pr.k, (T*)pr.gx, pr);
     }
-  } else if (sizeof(T) <= 4 && narrow_applies(pr)) {
+  } else if (sizeof(T) <= 4 && bwd_narrow_applies(pr)) {
     if constexpr (sizeof(T) <= 4) return narrow_dgrad<T>(pr, s);
   } else {
     using ACC = typename std::conditional<sizeof(T) == 8, double, float>::type;
@@ -885,7 +885,7 @@ static cudaError_t bwd_weight_t(const BackwardProblem& pr, bool exact, cudaStrea
   }
   if constexpr (sizeof(T) <= 4) {
     static const bool wn = !getenv("SEGCONV_BWD_NARROW_WGRAD") || atoi(getenv("SEGCONV_BWD_NARROW_WGRAD")) != 0;
-    if (wn && narrow_applies(pr) && M > 0) return narrow_wgrad<T>(pr, s);
+    if (wn && bwd_narrow_applies(pr) && M > 0) return narrow_wgrad<T>(pr, s);
   }
   // cout % 64 != 0: (tap, f) packed columns, all taps of a tile in one CTA
   const bool packed = pr.cout % bwd::BN != 0;

@@ -570,7 +570,7 @@ static segconv_status run_backward(const BackwardProblem& pr, segconv_math math,
       snprintf(msg, sizeof msg, "%s[input, tcgen05 pair]", what);
       st = cuda_status(launch_tc_bwd_data(pr, s), msg);
     } else {
-      dpath = exact ? "simt-exact" : "simt-ffma";
+      dpath = exact ? "simt-exact" : bwd_narrow_applies(pr) ? "simt-narrow" : "simt-ffma";
       snprintf(msg, sizeof msg, "%s[input]", what);
       st = cuda_status(launch_bwd_data_simt(pr, exact, s), msg);
     }
@@ -583,7 +583,7 @@ static segconv_status run_backward(const BackwardProblem& pr, segconv_math math,
       snprintf(msg, sizeof msg, "%s[kernel, tcgen05 pair]", what);
       st = cuda_status(launch_tc_bwd_weight(pr, s), msg);
     } else {
-      wpath = exact ? "simt-exact" : "simt-ffma";
+      wpath = exact ? "simt-exact" : bwd_narrow_applies(pr) ? "simt-narrow" : "simt-ffma";
       snprintf(msg, sizeof msg, "%s[kernel]", what);
       st = cuda_status(launch_bwd_weight_simt(pr, exact, s), msg);
     }

@@ -48,6 +48,8 @@ struct BackwardProblem {
   void* gk;
   int accumulate;  // gk += (the reference accumulates tap gradients across calls)
 };
+// the narrow-output (cout <= 4, wide rows) SIMT backward kernels take this problem
+bool bwd_narrow_applies(const BackwardProblem& pr);
 cudaError_t launch_bwd_data_simt(const BackwardProblem& pr, bool exact, cudaStream_t s);
 cudaError_t launch_bwd_weight_simt(const BackwardProblem& pr, bool exact, cudaStream_t s);
 bool tc_bwd_data_supported(const BackwardProblem& pr);
