@@ -80,6 +80,7 @@ struct Params {
   int BW, BWo, col_tiles;  // TILE2D column blocks: box width (row pitch), anchors kept per block
   int allq;  // halo staging: one unit = all four classes of a tile (4 accumulators of NT <= 64)
   int wres;  // ALLQ with one feature tile: every (kb, class, tap) weight tile resident in SMEM
+  int nacc;  // TMEM accumulator buffers (0 = 2; ALLQ with NT = 128 fills 512 columns with one)
   int tap_base[4];  // WRES: first tile of class q within a k-block
   // IM2COL (small images, where the halo-shift grid wastes rows): GEMM rows are
   // only class q's output anchors; each tap's A tile is gathered by an im2col
@@ -397,6 +398,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (threadIdx.x == 0) griddep_launch_dependents();  // next layer may start its prologue
 
   const int NT2 = p.NT / 2;
+  const int NACC = p.nacc > 0 ? p.nacc : 2;
   const uint32_t a_tx = (uint32_t)p.S_rows * 128, b_tx = (uint32_t)NT2 * 128;
 
   if (warp == 4 || (warp == 6 && p.mode == 1 && p.bprod)) {
@@ -543,7 +545,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             sa = 0;
             pa ^= 1;
           }
-          if (!p.wres)
+          if (!p.wres && !p.bprod)
           for (int qq = p.allq ? 0 : q; qq < (p.allq ? 4 : q + 1); ++qq)
           for (int t = 0; t < p.taps[qq]; ++t) {
             mbar_wait(&b_empty[sb], pb ^ 1);
@@ -572,6 +574,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int nt, q, hf;
       for (int k = 0; unit_of(p, k, pt, nt, q, hf); ++k) {
         const int f0 = hf ? nt * p.NT + (hf - 1) * NT2 + (int)rank * (NT2 / 2) : nt * p.NT + (int)rank * NT2;
+        if (!p.im2col) {  // halo staging: (kb, class, tap) weight tiles in the MMA order
+          for (int kb = 0; kb < p.nkb; ++kb)
+            for (int qq = p.allq ? 0 : q; qq < (p.allq ? 4 : q + 1); ++qq)
+              for (int t = 0; t < p.taps[qq]; ++t) {
+                mbar_wait(&b_empty[sb], pb ^ 1);
+                const uint32_t bf = mapa(smem_u32(&b_full[sb]), 0);
+                if (rank == 0) mbar_arrive_expect_tx(&b_full[sb], 2 * b_tx);
+                tma2_load_3d(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), &maps.w[qq], kb * KB, t, f0, bf);
+                if (++sb == SB) {
+                  sb = 0;
+                  pb ^= 1;
+                }
+              }
+          continue;
+        }
         for (int pass = 0; pass < (p.split ? 3 : 1); ++pass)
           for (int kb = 0; kb < p.nkb; ++kb)
             for (int t = 0; t < p.taps[q]; ++t) {
@@ -632,7 +649,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (elect_one()) commit2(&acc_full[acc]);
         __syncwarp();
-        if (++acc == 2) {
+        if (++acc == NACC) {
           acc = 0;
           pacc ^= 1;
         }
@@ -736,7 +753,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (elect_one()) commit2(&acc_full[acc]);
         __syncwarp();
         if (lane == 0) trace_ev(p, 3, k);
-        if (++acc == 2) {
+        if (++acc == NACC) {
           acc = 0;
           pacc ^= 1;
         }
@@ -777,7 +794,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cl(acc_empty_leader0 + (uint32_t)acc * 8);
-      if (++acc == 2) {
+      if (++acc == NACC) {
         acc = 0;
         pacc ^= 1;
       }
@@ -880,7 +897,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cl(acc_empty_leader0 + (uint32_t)acc * 8);
-      if (++acc == 2) {
+      if (++acc == NACC) {
         acc = 0;
         pacc ^= 1;
       }
@@ -1052,6 +1069,10 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
     // measured (B200, batch 64, 4x4, p = 2): 128^2 x 64 -> 64 561 -> 365 us,
     // 64^2 x 64 -> 64 152 -> 106 us; at 32^2 the im2col walk is still faster
     if (!split && !tf32 && p.tile2d && tc_wide_ntile(pr.cout) <= 64 && pr.n >= 64) p.im2col = 0;
+    // tiny maps (C5 c: 7 x 7): 128-row im2col boxes span several images and run
+    // slowly; linear halo rows with all classes per unit instead (one accumulator)
+    static const int small_env = getenv("SEGCONV_WIDE_ALLQ_SMALL") ? atoi(getenv("SEGCONV_WIDE_ALLQ_SMALL")) : 0;
+    if (!split && !tf32 && !p.tile2d && tc_wide_ntile(pr.cout) == 128 && pr.n <= small_env) p.im2col = 0;
     const char* e = getenv("SEGCONV_WIDE_IM2COL");
     if (e && !split && !tf32) p.im2col = atoi(e) ? 1 : 0;  // split / tf32 need im2col staging
     p.bprod = p.im2col ? wide_bprod() : 0;
@@ -1097,9 +1118,11 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
   }
   {
     static const int allq_env = getenv("SEGCONV_WIDE_ALLQ") ? atoi(getenv("SEGCONV_WIDE_ALLQ")) : 1;
-    p.allq = (!p.im2col && p.tile2d && p.NT <= 64 && allq_env) ? 1 : 0;
+    p.allq = (!p.im2col && p.NT <= 128 && allq_env) ? 1 : 0;
+    p.nacc = p.allq && 4 * p.NT > 256 ? 1 : 2;
     static const int wres_env = getenv("SEGCONV_WIDE_WRES") ? atoi(getenv("SEGCONV_WIDE_WRES")) : 1;
     p.wres = (p.allq && p.n_tiles == 1 && wres_env) ? 1 : 0;
+    p.bprod = (!p.im2col && !p.wres) ? wide_bprod() : p.bprod;
     int tb = 0;
     for (int q = 0; q < 4; ++q) {
       p.tap_base[q] = tb;
@@ -1128,7 +1151,7 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
     p.b_stage_bytes *= p.nkb * (p.tap_base[3] + p.taps[3]);
     p.stages_b = 1;
     p.stages_a = std::min(tcw::MAX_STAGES_A, (budget - p.b_stage_bytes) / p.a_stage_bytes);
-    if (p.stages_a < 2) p.wres = 0, p.b_stage_bytes = (p.NT / 2) * 128;
+    if (p.stages_a < 2) p.wres = 0, p.b_stage_bytes = (p.NT / 2) * 128, p.bprod = wide_bprod();
   }
   if (!p.im2col && !p.wres) {
     p.stages_a = 3;
