@@ -296,3 +296,18 @@ def test_full_size_tensor_core_backward_equals_simt(b, n, cin, cout, k):
     _, gk12 = sc.transpose_conv_fused_backward(x, kk, 0, (gy1.float() + gy2.float()).bfloat16(), math="bf16",
                                                input_grad=False)
     assert torch.equal(gk12, gk_tc + gk2)  # linear in the output gradient, exact
+
+
+def test_bf16_narrow_output_backward():
+    """bf16 layers with 3-feature outputs on wide maps take the narrow-output SIMT
+    kernels (no tensor-core mode for cout < 64): bf16 input gradient within the
+    bf16 bar, fp32 kernel gradient within 1e-4."""
+    rng = np.random.default_rng(21)
+    x = oracle.bf16_round(rng.standard_normal((1, 64, 64, 64)).astype(np.float32))
+    kk = oracle.bf16_round((rng.standard_normal((5, 5, 64, 3)) * 0.05).astype(np.float32))
+    g = oracle.geometry(64, 5, 5, 0)
+    gy = oracle.bf16_round(rng.standard_normal((1, g.out_h, g.out_w, 3)).astype(np.float32))
+    wx, wk = oracle.tconv_backward(x, kk, 0, gy)
+    gx, gk, path = gpu_bwd(x, kk, 0, gy, math="bf16", dtype=torch.bfloat16)
+    assert path == "bwd:simt-narrow+simt-narrow"
+    assert scaled_err(gx, wx) <= 1e-2 and scaled_err(gk, wk) <= 1e-4
