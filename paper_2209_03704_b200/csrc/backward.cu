@@ -645,29 +645,32 @@ __global__ void __launch_bounds__(256) dgrad_narrow(const T* __restrict__ gy, co
 }
 
 // gk partials: a CTA sums `rows` consecutive input rows (all columns, 64
-// channels).  Four pixel phases of 64 threads (pixels px = phase mod 4); a
-// thread owns 8 channels x 10 (tap, f) columns: per pixel 2 LDS.128 of x +
-// 10 g loads for 80 FFMA.  Each phase writes its own partial (split).
-template <typename T, int CO>
-__global__ void __launch_bounds__(256) wgrad_narrow(const T* __restrict__ x, const T* __restrict__ gy,
+// channels).  PH pixel phases (pixels px = phase mod PH); a thread owns 8
+// channels x COLS (tap, f) columns: per pixel 2 LDS.128 of x + COLS g loads for
+// 8 COLS FFMA.  Each phase writes its own partial (split).  COLS = 5 (two
+// phases, 80 registers, three CTAs per SM so one CTA's staging overlaps the
+// others' math) measured fastest on C4: 1031 us vs 1110 with COLS = 10.
+template <typename T, int CO, int COLS>
+__global__ void __launch_bounds__(256, COLS == 5 ? 3 : 2) wgrad_narrow(const T* __restrict__ x, const T* __restrict__ gy,
                                                     float* __restrict__ ws, BackwardProblem pr, int rows) {
+  constexpr int NG = 80 / COLS, TPP = 8 * NG, PH = 256 / TPP;  // column groups, threads and phases
   extern __shared__ float nsm[];
   const int gw = nw_gw(pr.kw);
   float* sx = nsm;                          // [px][68]
   float* sg = nsm + NW_PX * (NW_CH + 4);    // [(U * gw + col) * CO + f]
   const int cb = blockIdx.y * NW_CH;
-  const int ph = threadIdx.x >> 6, t64 = threadIdx.x & 63;
-  const int c8 = t64 & 7, cgp = t64 >> 3;
+  const int ph = threadIdx.x / TPP, tl = threadIdx.x - ph * TPP;
+  const int c8 = tl & 7, cgp = tl >> 3;
   const int NP = pr.kh * pr.kw * CO;
-  int goff[10];
+  int goff[COLS];
 #pragma unroll
-  for (int u = 0; u < 10; ++u) {
-    const int n = cgp + 8 * u;
+  for (int u = 0; u < COLS; ++u) {
+    const int n = cgp + NG * u;
     const int tap = n < NP ? n / CO : 0, f = n < NP ? n - (n / CO) * CO : 0;
     const int U = tap / pr.kw, V = tap - (tap / pr.kw) * pr.kw;
     goff[u] = (U * gw + pr.kw - 1 - V) * CO + f;  // columns past NP read a valid slot, never stored
   }
-  float acc[10][8] = {};
+  float acc[COLS][8] = {};
   const int total_rows = pr.batch * pr.in_h;
   const int r0 = blockIdx.x * rows, r1 = min(r0 + rows, total_rows);
   for (int row = r0; row < r1; ++row) {
@@ -695,12 +698,12 @@ __global__ void __launch_bounds__(256) wgrad_narrow(const T* __restrict__ x, con
       __syncthreads();
       const int npx = min(NW_PX, pr.in_w - j0);
 #pragma unroll 2
-      for (int px = ph; px < npx; px += 4) {
+      for (int px = ph; px < npx; px += PH) {
         const float4 xa = *reinterpret_cast<const float4*>(sx + px * (NW_CH + 4) + 8 * c8);
         const float4 xb = *reinterpret_cast<const float4*>(sx + px * (NW_CH + 4) + 8 * c8 + 4);
         const float* gp = sg + 2 * px * CO;
 #pragma unroll
-        for (int u = 0; u < 10; ++u) {
+        for (int u = 0; u < COLS; ++u) {
           const float g = gp[goff[u]];
           acc[u][0] = fmaf(xa.x, g, acc[u][0]);
           acc[u][1] = fmaf(xa.y, g, acc[u][1]);
@@ -715,10 +718,10 @@ __global__ void __launch_bounds__(256) wgrad_narrow(const T* __restrict__ x, con
     }
   }
   const long long ksz = (long long)pr.kh * pr.kw * pr.cin * CO;
-  float* out = ws + ((long long)blockIdx.x * 4 + ph) * ksz;
+  float* out = ws + ((long long)blockIdx.x * PH + ph) * ksz;
 #pragma unroll
-  for (int u = 0; u < 10; ++u) {
-    const int n = cgp + 8 * u;
+  for (int u = 0; u < COLS; ++u) {
+    const int n = cgp + NG * u;
     if (n >= NP) continue;
     const int tap = n / CO, f = n - (n / CO) * CO;
 #pragma unroll
@@ -794,24 +797,32 @@ static cudaError_t narrow_wgrad_t(const BackwardProblem& pr, cudaStream_t s) {
   const size_t smem = ((size_t)bwd::NW_PX * (bwd::NW_CH + 4) + (size_t)pr.kh * gw * CO) * sizeof(float);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(bwd::wgrad_narrow<T, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(bwd::wgrad_narrow<T, CO, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(bwd::wgrad_narrow<T, CO, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
   }
   const int chb = (pr.cin + bwd::NW_CH - 1) / bwd::NW_CH;
   const long long total_rows = (long long)pr.batch * pr.in_h;
-  // ~2 CTAs per SM over (row range, channel block)
-  long long rows = std::max(1LL, (total_rows * chb + 2LL * sm_count() - 1) / (2LL * sm_count()));
+  // a few CTAs per SM over (row range, channel block)
+  static const int cps = getenv("SEGCONV_WGRAD_NARROW_CPS") ? atoi(getenv("SEGCONV_WGRAD_NARROW_CPS")) : 3;
+  long long rows = std::max(1LL, (total_rows * chb + (long long)cps * sm_count() - 1) / ((long long)cps * sm_count()));
   const long long splits = (total_rows + rows - 1) / rows;
   const long long ksz = (long long)pr.kh * pr.kw * pr.cin * pr.cout;
   float* ws = nullptr;
-  cudaError_t e = workspace_alloc((void**)&ws, (size_t)splits * 4 * ksz * sizeof(float), s);
+  static const int cols = getenv("SEGCONV_WGRAD_NARROW_COLS") ? atoi(getenv("SEGCONV_WGRAD_NARROW_COLS")) : 5;
+  const int phases = cols == 5 ? 2 : 4;
+  cudaError_t e = workspace_alloc((void**)&ws, (size_t)splits * phases * ksz * sizeof(float), s);
   if (e != cudaSuccess) return e;
-  bwd::wgrad_narrow<T, CO><<<dim3((unsigned)splits, (unsigned)chb), 256, smem, s>>>(
-      (const T*)pr.x, (const T*)pr.gy, ws, pr, (int)rows);
+  if (cols == 5)
+    bwd::wgrad_narrow<T, CO, 5><<<dim3((unsigned)splits, (unsigned)chb), 256, smem, s>>>(
+        (const T*)pr.x, (const T*)pr.gy, ws, pr, (int)rows);
+  else
+    bwd::wgrad_narrow<T, CO, 10><<<dim3((unsigned)splits, (unsigned)chb), 256, smem, s>>>(
+        (const T*)pr.x, (const T*)pr.gy, ws, pr, (int)rows);
   e = cudaGetLastError();
   if (e == cudaSuccess) {
     note_launch();
-    e = launch_wgrad_reduce(ws, (float*)pr.gk, ksz, (int)splits * 4, pr.accumulate, s);
+    e = launch_wgrad_reduce(ws, (float*)pr.gk, ksz, (int)splits * phases, pr.accumulate, s);
   }
   cudaError_t e2 = cudaFreeAsync(ws, s);
   return e != cudaSuccess ? e : e2;
