@@ -989,6 +989,8 @@ static int wide_bprod() {
   return v ? 1 : 0;
 }
 
+static int wide_pairs();
+
 static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, const void* xs = nullptr) {
   p = tcw::Params{};
   const bool split = pr.x_dtype == SEGCONV_F32 && pr.panel_dtype == SEGCONV_F16_SPLIT;
@@ -1029,6 +1031,15 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
   p.out_w = pr.out_w;
   p.Mv = (long long)pr.batch * pr.n * pr.n;
   p.NT = split ? std::min(128, tc_wide_ntile(pr.cout)) : tc_wide_ntile(pr.cout);  // SPLIT: 2 accumulators
+  {
+    // small batches of small maps (GAN generators' first layers): fewer 256-wide
+    // units than CTA pairs leaves SMs idle -- halve the feature tile when the
+    // doubled unit count still fits one wave (DCGAN 4x4 x 1024 -> 512: 34.8 -> 32.2 us)
+    static const bool adapt = !getenv("SEGCONV_WIDE_NT_ADAPT") || atoi(getenv("SEGCONV_WIDE_NT_ADAPT")) != 0;
+    long long u = 0;
+    for (int q = 0; q < 4; ++q) u += ((long long)pr.batch * pr.cls.rows[q] * pr.cls.cols[q] + 255) / 256;
+    if (adapt && p.NT > 128 && 2 * u * ((pr.cout + p.NT - 1) / p.NT) <= wide_pairs()) p.NT = 128;
+  }
   p.n_tiles = (pr.cout + p.NT - 1) / p.NT;
   if (p.n_tiles * p.NT > pr.cout_pad && p.n_tiles > 1) {
     // the last tile may run past cout_pad: the TMA box is zero-filled out of bounds
