@@ -66,6 +66,8 @@ def test_exact_matches_reference_goldens_bit_for_bit():
     (1, 64, 64, 3, 5, 0),     # C4 family (narrow-output kernels), reduced size
     (2, 20, 40, 1, 4, 2),     # narrow: partial channel block, one feature
     (1, 130, 16, 4, 3, 1),    # narrow: rows wider than one 128-pixel segment
+    (1, 64, 10, 2, 3, 1),     # narrow: channels not a multiple of 4 (scalar loads / stores)
+    (2, 64, 72, 3, 4, 2),     # narrow: two channel blocks, p_fused = 1, two images
 ])
 def test_ffma_f32(b, n, cin, cout, k, p):
     rng = np.random.default_rng(b * 1000 + n * 10 + k)
