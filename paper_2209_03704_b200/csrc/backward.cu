@@ -534,6 +534,38 @@ __global__ void wgrad_reduce4(const float4* __restrict__ ws, float4* __restrict_
   gk[e] = s;
 }
 
+// Many splits of a small gradient (the narrow kernels' hundreds of partials of
+// a 4800-element gk): 8 float4 elements per CTA, 32 split groups of 8 threads
+// each summing every 32nd split, then a fixed-order combine of the 32 group
+// sums (deterministic) -- instead of one thread walking all splits serially.
+__global__ void __launch_bounds__(256) wgrad_reduce4_wide(const float4* __restrict__ ws, float4* __restrict__ gk,
+                                                          long long n4, int splits, int accumulate) {
+  __shared__ float4 part[32][8];
+  const int el = threadIdx.x & 7, grp = threadIdx.x >> 3;
+  const long long e = (long long)blockIdx.x * 8 + el;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (e < n4)
+    for (int i = grp; i < splits; i += 32) {
+      const float4 v = __ldcs(ws + (long long)i * n4 + e);
+      s.x += v.x;
+      s.y += v.y;
+      s.z += v.z;
+      s.w += v.w;
+    }
+  part[grp][el] = s;
+  __syncthreads();
+  if (grp == 0 && e < n4) {
+    float4 t = accumulate ? gk[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int g = 0; g < 32; ++g) {
+      t.x += part[g][el].x;
+      t.y += part[g][el].y;
+      t.z += part[g][el].z;
+      t.w += part[g][el].w;
+    }
+    gk[e] = t;
+  }
+}
+
 // stream-K pieces: element idx of gk belongs to tile T = ((t * ch_pairs + ch / 256)
 // * n_tiles + f / NT); its pieces are the pairs overlapping [T*chunks, (T+1)*chunks)
 // in slot order 0, 1, ... (deterministic)
@@ -975,8 +1007,12 @@ cudaError_t launch_wgrad_reduce(const float* ws, float* gk, long long ksz, int s
                                 cudaStream_t s) {
   if (ksz % 4 == 0 && ((uintptr_t)ws & 15) == 0 && ((uintptr_t)gk & 15) == 0) {
     const long long n4 = ksz / 4;
-    bwd::wgrad_reduce4<<<(unsigned)((n4 + 255) / 256), 256, 0, s>>>((const float4*)ws, (float4*)gk, n4, splits,
-                                                                     accumulate);
+    if (splits >= 64 && (n4 + 255) / 256 < 2LL * sm_count())  // too few threads to walk the splits
+      bwd::wgrad_reduce4_wide<<<(unsigned)((n4 + 7) / 8), 256, 0, s>>>((const float4*)ws, (float4*)gk, n4,
+                                                                        splits, accumulate);
+    else
+      bwd::wgrad_reduce4<<<(unsigned)((n4 + 255) / 256), 256, 0, s>>>((const float4*)ws, (float4*)gk, n4, splits,
+                                                                       accumulate);
   } else {
     bwd::wgrad_reduce<float><<<(unsigned)((ksz + 255) / 256), 256, 0, s>>>(ws, gk, ksz, splits, accumulate);
   }
