@@ -776,13 +776,7 @@ cudaError_t launch_wgrad_reduce_streamk(const float* ws, float* gk, int cin, int
 }
 
 static int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      sms = 148;
-  }
+  const int sms = device_sm_count();
   return sms;
 }
 
@@ -797,10 +791,10 @@ template <typename T, int CO>
 static cudaError_t narrow_dgrad_t(const BackwardProblem& pr, cudaStream_t s) {
   const int gw = bwd::nw_gw(pr.kw);
   const size_t smem = ((size_t)pr.kh * pr.kw * CO * bwd::NW_CH + (size_t)pr.kh * gw * CO) * sizeof(float);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(bwd::dgrad_narrow<T, CO>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
+  static PerDeviceOnce once;
+  {
+    const cudaError_t e = smem_attr_once(once, bwd::dgrad_narrow<T, CO>, 200 * 1024);
+    if (e != cudaSuccess) return e;
   }
   const long long rows = (long long)pr.batch * pr.in_h;
   const long long yz = (long long)((pr.in_w + bwd::NW_PX - 1) / bwd::NW_PX) * ((pr.cin + bwd::NW_CH - 1) / bwd::NW_CH);
@@ -827,11 +821,11 @@ template <typename T, int CO>
 static cudaError_t narrow_wgrad_t(const BackwardProblem& pr, cudaStream_t s) {
   const int gw = bwd::nw_gw(pr.kw);
   const size_t smem = ((size_t)bwd::NW_PX * (bwd::NW_CH + 4) + (size_t)pr.kh * gw * CO) * sizeof(float);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(bwd::wgrad_narrow<T, CO, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(bwd::wgrad_narrow<T, CO, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
+  static PerDeviceOnce once10, once5;
+  {
+    cudaError_t e = smem_attr_once(once10, bwd::wgrad_narrow<T, CO, 10>, 200 * 1024);
+    if (e == cudaSuccess) e = smem_attr_once(once5, bwd::wgrad_narrow<T, CO, 5>, 200 * 1024);
+    if (e != cudaSuccess) return e;
   }
   const int chb = (pr.cin + bwd::NW_CH - 1) / bwd::NW_CH;
   const long long total_rows = (long long)pr.batch * pr.in_h;

@@ -5,9 +5,53 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "segconv_b200.h"
 
 namespace segconv_b200 {
+
+// ------------------------------------------------------- per-device state
+// Function attributes (dynamic shared memory size, cluster flags) and SM
+// counts are properties of a device, and one process may drive several GPUs
+// (the multi-GPU stack driver does, from one thread per device).  Each launch
+// site keeps one PerDeviceOnce per kernel instantiation: the setup runs once
+// per device id, lock-free; a concurrent duplicate run is harmless (the
+// attributes are idempotent).
+struct PerDeviceOnce {
+  std::atomic<uint64_t> done{0};
+  template <class F>
+  cudaError_t run(F&& f) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = f();
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+  }
+};
+
+// SM count of the current device (cached per device id; 148 on B200).
+inline int device_sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  int v = cache[dev & 63].load(std::memory_order_relaxed);
+  if (v > 0) return v;
+  if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+  cache[dev & 63].store(v, std::memory_order_relaxed);
+  return v;
+}
+
+// Sets the kernel's dynamic shared memory limit once per device.
+template <typename K>
+inline cudaError_t smem_attr_once(PerDeviceOnce& once, K kern, int bytes) {
+  return once.run([&] {
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  });
+}
 
 // ----------------------------------------------------------------- dtypes
 template <typename T>

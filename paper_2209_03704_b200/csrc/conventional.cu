@@ -204,12 +204,10 @@ static cudaError_t run_conv_tiled(const float* src, int batch, int h, int w, int
   constexpr int TH = WH * QH + K - 1, TW = QW + K - 1, TWP = (TW + 3) & ~3;
   const size_t smem = (size_t)(CI * TH * TWP + CI * K * K * 32) * sizeof(float);
   auto kern = conv_valid_tiled<K, QH, QW, WH, CI>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static PerDeviceOnce once;
+  {
+    const cudaError_t e = smem_attr_once(once, kern, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int oh = h - K + 1, ow = w - K + 1;
   const int tiles_h = (oh + WH * QH - 1) / (WH * QH), tiles_w = (ow + QW - 1) / QW;

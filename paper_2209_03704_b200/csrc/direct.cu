@@ -364,12 +364,10 @@ static cudaError_t run_pixlanes(const FusedProblem& pr, cudaStream_t s) {
   constexpr int TH = WH * QV + U - 1, TW = WW * 32 + U - 1, TWP = TW + 1;
   const size_t smem = (size_t)(((CI * TH * TWP + 3) & ~3) + CI * P::TAPS * 4) * sizeof(float);
   auto kern = tconv_pixlanes<K, PODD, CO, QV, WH, WW, CI, TX, TWt>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  static PerDeviceOnce once;
+  {
+    const cudaError_t e = smem_attr_once(once, kern, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int rows0 = pr.cls.rows[0] > pr.cls.rows[2] ? pr.cls.rows[0] : pr.cls.rows[2];
   const int cols0 = pr.cls.cols[0] > pr.cls.cols[1] ? pr.cls.cols[0] : pr.cls.cols[1];
@@ -391,12 +389,10 @@ static cudaError_t run_coutlanes(const FusedProblem& pr, cudaStream_t s) {
   constexpr int TH = WH * QH + U - 1, TW = WW * QW + U - 1, TWP = (TW + 3) & ~3;
   const size_t smem = (size_t)(CI * TH * TWP + CI * P::TAPS * 32) * sizeof(float);
   auto kern = tconv_coutlanes<K, PODD, QH, QW, WH, WW, CI, TX, TWt>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+  static PerDeviceOnce once;
+  {
+    const cudaError_t e = smem_attr_once(once, kern, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
   }
   const int rows0 = pr.cls.rows[0] > pr.cls.rows[2] ? pr.cls.rows[0] : pr.cls.rows[2];
   const int cols0 = pr.cls.cols[0] > pr.cls.cols[1] ? pr.cls.cols[0] : pr.cls.cols[1];

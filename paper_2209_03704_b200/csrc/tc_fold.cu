@@ -890,20 +890,12 @@ bool tc_fold_supported(const FusedProblem& pr, int math) {
 template <int MODE, int N, bool TMEM_A>
 static cudaError_t launch_fold_t(const FoldPlan& pl, cudaStream_t s) {
   auto kern = tcf::tc_fold_kernel<MODE, N, TMEM_A>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tcf::SMEM_LIMIT);
+  static PerDeviceOnce once;
+  {
+    const cudaError_t e = smem_attr_once(once, kern, tcf::SMEM_LIMIT);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      sms = 148;
-  }
+  const int sms = device_sm_count();
   const long long grid = std::min<long long>(pl.p.units, sms);
   tcf::Params prm = pl.p;
   prm.trace = tc_trace_buffer();

@@ -449,17 +449,17 @@ typedef CUresult (*EncodeTiledFnTS)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 static EncodeTiledFnTS encode_fn_ts() {
-  static EncodeTiledFnTS fn = nullptr;
-  static bool init = false;
-  if (!init) {
-    init = true;
+  // magic static: thread-safe one-time lookup of the driver entry point
+  static const EncodeTiledFnTS fn = [] {
+    EncodeTiledFnTS fn = nullptr;
     void* f = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
             cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       fn = (EncodeTiledFnTS)f;
-  }
+    return fn;
+  }();
   return fn;
 }
 
@@ -627,20 +627,12 @@ static cudaError_t launch_fold_ts_t(const tcfs::Params& prm, const CUtensorMap& 
   // the MMA issue is unrolled over the union window; n = 3 (4 shifts) is the
   // instantiated shape (make_fold_ts_params admits only it)
   auto kern = tcfs::fold_ts_kernel<YT, ACT, 4>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tcfs::SMEM_LIMIT);
+  static PerDeviceOnce once;
+  {
+    const cudaError_t e = smem_attr_once(once, kern, tcfs::SMEM_LIMIT);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      sms = 148;
-  }
+  const int sms = device_sm_count();
   const long long units = (prm.Mv + 127) / 128;
   long long grid = std::min<long long>(units, sms);
   const size_t smem = (size_t)tcfs::STAGES * prm.stage_bytes + (3 * tcfs::STAGES + 6) * 8 + 16;

@@ -707,20 +707,12 @@ const unsigned long long* tc_trace_ptr() { return g_trace; }
 template <int MODE, int NT, int G>
 static cudaError_t launch_t(const Plan& pl, cudaStream_t s) {
   auto kern = tc::tc_halo_kernel<MODE, NT, G>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_LIMIT);
+  static PerDeviceOnce once;
+  {
+    const cudaError_t e = smem_attr_once(once, kern, tc::SMEM_LIMIT);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      sms = 148;
-  }
+  const int sms = device_sm_count();
   const long long grid = std::min<long long>(pl.p.total_units, sms);
   tc::Params prm = pl.p;
   prm.trace = tc_trace_buffer();

@@ -520,13 +520,7 @@ cudaError_t launch_tc_ring(const FusedProblem& pr, const void* ring_img, cudaStr
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorNotSupported;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      sms = 148;
-  }
+  const int sms = device_sm_count();
   const long long grid = std::min<long long>(p.g_total, sms);
   const size_t smem = (size_t)p.stages * p.stage_bytes + fixed;
   const int act = (pr.epi & SEGCONV_EPI_RELU) ? 1 : (pr.epi & SEGCONV_EPI_TANH) ? 2 : 0;
@@ -534,12 +528,9 @@ cudaError_t launch_tc_ring(const FusedProblem& pr, const void* ring_img, cudaStr
 #define RING_LAUNCH(A)                                                                           \
   {                                                                                              \
     auto kern = tcr::ring_kernel<5, 3, A>;                                                       \
-    static bool cfg = false;                                                                     \
-    if (!cfg) {                                                                                  \
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tcr::SMEM_LIMIT); \
-      if (e != cudaSuccess) return e;                                                            \
-      cfg = true;                                                                                \
-    }                                                                                            \
+    static PerDeviceOnce once;                                                                   \
+    e = smem_attr_once(once, kern, tcr::SMEM_LIMIT);                                              \
+    if (e != cudaSuccess) return e;                                                              \
     kern<<<(unsigned)grid, tcr::NUM_THREADS, smem, s>>>(p, tmap);                                \
   }
   if (act == 1)

@@ -124,10 +124,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 8) {
     // ===== TMA producer: weights once, then {64 ch, 128 pixels} boxes per tile
     if (lane == 0) {
+      // Both the activations and the weight image may come from the kernel
+      // this one overlaps under programmatic dependent launch (the previous
+      // stack layer, or segregate's image kernel right before a first call):
+      // wait for it before the first global read.
+      griddep_wait();
       mbar_arrive_expect_tx(w_full, (uint32_t)p.w_bytes);
       for (uint32_t off = 0; off < (uint32_t)p.w_bytes; off += 32768)
         bulk_g2s(w_base + off, p.panels + off, min(32768u, (uint32_t)p.w_bytes - off), w_full);
-      griddep_wait();  // activations come from the previous kernel (stack layer)
       int st = 0;
       uint32_t ph = 0;
       int k = 0;
@@ -443,13 +447,7 @@ static cudaError_t launch_tile_t(const FusedProblem& pr, const void* img, cudaSt
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorNotSupported;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      sms = 148;
-  }
+  const int sms = device_sm_count();
   const long long grid = std::min<long long>(p.tiles, sms);
   const size_t smem = (size_t)p.stages * p.stage_bytes + fixed;
   const int act = (pr.epi & SEGCONV_EPI_RELU) ? 1 : (pr.epi & SEGCONV_EPI_TANH) ? 2 : 0;
@@ -457,12 +455,9 @@ static cudaError_t launch_tile_t(const FusedProblem& pr, const void* img, cudaSt
 #define TILE_LAUNCH(A, YT)                                                                       \
   {                                                                                              \
     auto kern = tct::tile_kernel<KH, 3, A, YT>;                                                  \
-    static bool cfg = false;                                                                     \
-    if (!cfg) {                                                                                  \
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tct::SMEM_LIMIT); \
-      if (e != cudaSuccess) return e;                                                            \
-      cfg = true;                                                                                \
-    }                                                                                            \
+    static PerDeviceOnce once;                                                                   \
+    e = smem_attr_once(once, kern, tct::SMEM_LIMIT);                                              \
+    if (e != cudaSuccess) return e;                                                              \
     cudaLaunchConfig_t lc = {};                                                                 \
     lc.gridDim = dim3((unsigned)grid);                                                           \
     lc.blockDim = dim3(tct::NUM_THREADS);                                                        \

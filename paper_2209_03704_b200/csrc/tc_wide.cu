@@ -922,17 +922,17 @@ typedef CUresult (*EncodeTiledFnW)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 static EncodeTiledFnW encode_fn_w() {
-  static EncodeTiledFnW fn = nullptr;
-  static bool init = false;
-  if (!init) {
-    init = true;
+  // magic static: thread-safe one-time lookup of the driver entry point
+  static const EncodeTiledFnW fn = [] {
+    EncodeTiledFnW fn = nullptr;
     void* f = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
             cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       fn = (EncodeTiledFnW)f;
-  }
+    return fn;
+  }();
   return fn;
 }
 
@@ -941,16 +941,16 @@ typedef CUresult (*EncIm2colW)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, vo
                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 static EncIm2colW encode_im2col_w() {
-  static EncIm2colW fn = nullptr;
-  static bool init = false;
-  if (!init) {
-    init = true;
+  // magic static: thread-safe one-time lookup of the driver entry point
+  static const EncIm2colW fn = [] {
+    EncIm2colW fn = nullptr;
     void* f = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &f, cudaEnableDefault, &q) == cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       fn = (EncIm2colW)f;
-  }
+    return fn;
+  }();
   return fn;
 }
 
@@ -1496,13 +1496,7 @@ static bool make_wide_wgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
 }
 
 static int wide_pairs() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      sms = 148;
-  }
+  const int sms = device_sm_count();
   return sms / 2;
 }
 
@@ -1618,22 +1612,12 @@ bool tc_wide_supported(const FusedProblem& pr, int math) {
 template <typename YT, int ACT>
 static cudaError_t launch_wide_t(const tcw::Params& prm, const tcw::Maps& maps, cudaStream_t s) {
   auto kern = tcw::wide_kernel<YT, ACT>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tcw::SMEM_LIMIT);
+  static PerDeviceOnce once;
+  {
+    const cudaError_t e = smem_attr_once(once, kern, tcw::SMEM_LIMIT);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 0);
-    (void)e;
-    configured = true;
   }
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      sms = 148;
-  }
+  const int sms = device_sm_count();
   long long pairs = std::min<long long>(prm.units, sms / 2);
   if (prm.mode == 1 && prm.w_share > 0)  // stream-K: every pair with a share of chunk-units
     pairs = (prm.units * prm.w_chunks + prm.w_share - 1) / prm.w_share;

@@ -1,3 +1,4 @@
+#include <cmath>
 // tensor_io.cu -- SGC1 tensor container (reference tensor_io.hpp:12-103), host
 // side of the boundary: the format the reference's tools exchange tensors in
 // (tools/segconv.cpp apply/verify read and write it).  Same header checks, error
@@ -70,6 +71,13 @@ segconv_status peek(const char* path, segconv_tensor_file_info* info) {
 
 size_t elem_size(int dtype) { return dtype == SEGCONV_F64 ? 8 : 4; }
 
+template <typename T>
+bool all_finite(const T* v, size_t n) {
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(v[i])) return false;
+  return true;
+}
+
 // reference tensor_io.hpp:76-91; the payload is read straight into dst
 segconv_status load(const char* path, segconv_dtype dtype, void* dst, size_t dst_bytes,
                     segconv_tensor_file_info* out_info) {
@@ -97,6 +105,11 @@ segconv_status load(const char* path, segconv_dtype dtype, void* dst, size_t dst
     return set_error(SEGCONV_E_CONTRACT, "destination buffer is too small");
   if (fseek(in.f, 20, SEEK_SET) != 0 || fread(dst, 1, count * elem_size(dtype), in.f) != count * elem_size(dtype))
     return set_error(SEGCONV_E_IO, (std::string("read failure on ") + path).c_str());
+  // the reference builds the result through Tensor::from_data, which rejects
+  // non-finite payloads (tensor.hpp:87-88)
+  const bool finite = dtype == SEGCONV_F64 ? all_finite((const double*)dst, count)
+                                           : all_finite((const float*)dst, count);
+  if (!finite) return set_error(SEGCONV_E_CONTRACT, "tensor data contains a non-finite element");
   if (out_info) *out_info = info;
   return SEGCONV_OK;
 }

@@ -111,6 +111,27 @@ def test_error_kinds_and_offsets_match_the_reference_live(tmp_path):
             assert got[:2] == want[:2] and (want[1] != 6 or got[2] == want[2]), data
 
 
+def test_non_finite_payload_is_a_contract_error(tmp_path):
+    """reference load_tensor builds its result through Tensor::from_data, which
+    throws ContractError("tensor data contains a non-finite element")
+    (tensor.hpp:87-88); the loaders here do the same, the batch loader too."""
+    import struct
+    cases = [(_hdr(1, 2, 1, 0) + struct.pack("<ff", 1.0, float("nan")), False),
+             (_hdr(2, 1, 1, 0) + struct.pack("<ff", float("-inf"), 0.5), False),
+             (_hdr(1, 1, 2, 1) + struct.pack("<dd", float("inf"), 2.0), True)]
+    for i, (data, f64) in enumerate(cases):
+        p = str(tmp_path / f"nf{i}.sgc")
+        _bytes(p, data)
+        with pytest.raises(sc.ContractError, match="non-finite"):
+            sc.load_tensor(p)
+        with pytest.raises(sc.ContractError, match="non-finite"):
+            sc.load_tensor_batch([p])
+        if oracle.ref_available():
+            with pytest.raises(oracle.OracleError) as e:
+                oracle.ref_load_tensor(p, f64=f64)
+            assert e.value.code == 2 and "non-finite" in str(e.value)
+
+
 def test_batch_loader_host(tmp_path):
     rng = np.random.default_rng(2)
     imgs = [rng.standard_normal((4, 4, 3)).astype(np.float32) for _ in range(5)]
