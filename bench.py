@@ -253,6 +253,26 @@ class Layer:
         return time.perf_counter() - t0, nimg, "port"
 
 
+    def parity(self):
+        """Two sampled images of the timed output against the oracle (the
+        reference's segregated path restated in C, pinned to its goldens)."""
+        import oracle
+        b = self.cfg["batch"]
+        idx = sorted({0, b - 1})
+        x, k = self.x_host[idx], self.k_host
+        if self.cfg["dtype"] == "bf16":
+            x, k = oracle.bf16_round(x), oracle.bf16_round(k)
+        want = oracle.tconv_fused(x, k, self.cfg["p"])
+        if self.cfg["act"] == "tanh":
+            want = np.tanh(want)
+        elif self.cfg["act"] == "relu":
+            want = np.maximum(want, 0)
+        got = self.y[idx].float().cpu().numpy()
+        tol = 1e-2 if self.cfg["dtype"] == "bf16" else 1e-5
+        return {"max_scaled_err": scaled_err(got, want), "tol": tol, "images": idx,
+                "oracle": "oracle.tconv_fused (C port, pinned)"}
+
+
 class LayerBackward(Layer):
     """`--pass backward`: the layer's backward pass (reference netdemo/layers.hpp:171-211,
     input + kernel gradients) on the same synthetic layer, output gradient ~ N(0, 1).
@@ -282,13 +302,31 @@ class LayerBackward(Layer):
             _, gk = self.sc.transpose_conv_fused_backward(self.xd, self.kd, self.cfg["p"], self.gyd,
                                                           input_grad=False)
             work = self.torch.distributed.all_reduce(gk, async_op=True)
-            self.sc.transpose_conv_fused_backward(self.xd, self.kd, self.cfg["p"], self.gyd,
-                                                  kernel_grad=False)
+            gx, _ = self.sc.transpose_conv_fused_backward(self.xd, self.kd, self.cfg["p"], self.gyd,
+                                                          kernel_grad=False)
             work.wait()
             self.math = "bwd:dp (" + self.sc.last_path() + ", kernel grad all-reduced)"
+            self.gx_last = gx
             return
-        self.sc.transpose_conv_fused_backward(self.xd, self.kd, self.cfg["p"], self.gyd)
+        gx, _ = self.sc.transpose_conv_fused_backward(self.xd, self.kd, self.cfg["p"], self.gyd)
         self.math = self.sc.last_path()  # e.g. "bwd:tc-pair+tc-pair"
+        self.gx_last = gx
+
+    def parity(self):
+        """Input gradient of two sampled images against the oracle backward
+        (reference net::FusedTConv::backward restated; per image it depends on
+        that image's output gradient only)."""
+        import oracle
+        b = self.cfg["batch"]
+        idx = sorted({0, b - 1})
+        x, k, gy = self.x_host[idx], self.k_host, self.gy_host[idx]
+        if self.cfg["dtype"] == "bf16":
+            x, k, gy = oracle.bf16_round(x), oracle.bf16_round(k), oracle.bf16_round(gy)
+        wx, _ = oracle.tconv_backward(x, k, self.cfg["p"], gy)
+        got = self.gx_last[idx].float().cpu().numpy()
+        tol = 1e-2 if self.cfg["dtype"] == "bf16" else 1e-5
+        return {"max_scaled_err": scaled_err(got, wx), "tol": tol, "images": idx,
+                "what": "input gradient", "oracle": "oracle.tconv_backward (C port, pinned)"}
 
     def step_e2e(self):
         """Public API from host buffers: x and gy uploaded, both gradients read back."""
@@ -342,25 +380,32 @@ class LayerBackward(Layer):
 
 
 class Stack:
-    """BASELINE C5: four-layer bf16 generator stack, batch 1024 sharded over ranks."""
+    """BASELINE C5: four-layer bf16 generator stack, batch 1024 sharded over ranks
+    (ShardedStack: weights broadcast once from rank 0, all-gather of the outputs)."""
 
-    def __init__(self, cfg, rank, world, torch, sc, dev):
+    def __init__(self, cfg, rank, world, torch, sc, dev, batch=None):
         from paper_2209_03704_b200 import stack as st
+        self.torch, self.sc, self.st = torch, sc, st
         self.cfg = cfg
+        self.world = world
         self.specs = stack_specs(cfg)
         krng = np.random.default_rng(SEED)
         self.k_host = [gen((s.k, s.k, s.cin, s.cout), "n02", krng) for s in self.specs]
         ks = [torch.from_numpy(k).to(dev) for k in self.k_host]
-        if world > 1:
-            for k in ks:
-                torch.distributed.broadcast(k, src=0)
-        lo, hi = st.shard_range(cfg["batch"], rank, world)
-        self.lo, self.hi = lo, hi
+        gb = cfg["batch"] if batch is None else batch
+        self.global_batch = gb
         s0 = self.specs[0]
         rng = np.random.default_rng(SEED + 1)
-        xall = rng.standard_normal((cfg["batch"], s0.n_in, s0.n_in, s0.cin), dtype=np.float32)
-        self.x_host = xall[lo:hi]
-        self.stack = st.GeneratorStack(self.specs, ks, hi - lo, act_dtype=torch.bfloat16)
+        xall = rng.standard_normal((gb, s0.n_in, s0.n_in, s0.cin), dtype=np.float32)
+        if world > 1:
+            self.sharded = st.ShardedStack(self.specs, ks, gb, act_dtype=torch.bfloat16)
+            self.stack = self.sharded.local
+            self.lo, self.hi = self.sharded.lo, self.sharded.hi
+        else:
+            self.sharded = None
+            self.stack = st.GeneratorStack(self.specs, ks, gb, act_dtype=torch.bfloat16)
+            self.lo, self.hi = 0, gb
+        self.x_host = xall[self.lo:self.hi]
         self.stack.x.copy_(torch.from_numpy(self.x_host))
         self.math = "+".join({v: k for k, v in sc.MATHS.items()}[s.math] for s in self.stack.sks)
         self.stack.capture()
@@ -370,6 +415,7 @@ class Stack:
         self.bound = "tensor"
         self.x_pinned = torch.from_numpy(self.x_host).to(torch.bfloat16).pin_memory()
         self.y_pinned = torch.empty(self.stack.out.shape, dtype=torch.bfloat16).pin_memory()
+        self.paths = []
 
     def step(self):
         self.stack.forward()
@@ -381,6 +427,51 @@ class Stack:
 
     def e2e_bytes(self):
         return self.x_pinned.numel() * 2, self.y_pinned.numel() * 2
+
+    def gather(self):
+        """The path's one exchange: all-gather of the output shards (NCCL)."""
+        return self.sharded.gather() if self.sharded is not None else self.stack.out
+
+    def layer_times(self, steps, flush):
+        """Per-layer device time (eager launches, CUDA events between layers on the
+        launching stream): the dominant kernel of the step and its roofline."""
+        torch = self.torch
+        st = self.stack
+        per = [[] for _ in self.specs]
+        for i in range(steps + 1):
+            flush()
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(len(self.specs) + 1)]
+            src = st.x
+            evs[0].record()
+            paths = []
+            for li, (s, g, sks, dst) in enumerate(zip(st.specs, st.geoms, st.sks, st.acts)):
+                self.sc.transpose_conv_fused(src, sks, g, activation=s.activation, out=dst)
+                paths.append(self.sc.last_path())
+                evs[li + 1].record()
+                src = dst
+            torch.cuda.synchronize()
+            if i:
+                for li in range(len(self.specs)):
+                    per[li].append(evs[li].elapsed_time(evs[li + 1]))
+            self.paths = paths
+        out = []
+        pk = peaks()
+        for li, (s, g) in enumerate(zip(st.specs, st.geoms)):
+            ms = statistics.mean(per[li])
+            macs = self.sc.count_ops_fused(self.sc.LayerShape(s.n_in, s.cin, s.cout, s.k, s.k, s.p)).mults \
+                * st.batch
+            byts = (st.batch * (s.n_in ** 2 * s.cin + g.out_h * g.out_w * s.cout) + s.k * s.k * s.cin * s.cout) * 2
+            ai = 2.0 * macs / byts
+            tensor = ai > pk["bf16"] * 1e3 / pk["hbm"]
+            ach = (2.0 * macs / (ms * 1e-3) / 1e12) if tensor else (byts / (ms * 1e-3) / 1e9)
+            peak = pk["bf16"] if tensor else pk["hbm"]
+            out.append({"layer": "abcdefgh"[li], "shape": f"{s.n_in}x{s.n_in}x{s.cin}->{g.out_h}x{g.out_w}x{s.cout}",
+                        "path": paths[li] if li < len(self.paths) else None, "ms": round(ms, 4),
+                        "useful_macs": macs, "alg_bytes": byts,
+                        "bound": "tensor" if tensor else "hbm", "achieved": round(ach, 1),
+                        "unit": "TFLOP/s" if tensor else "GB/s", "peak": peak,
+                        "frac": round(ach / peak, 4)})
+        return out
 
     def conventional(self, torch, steps, flush):
         return None
@@ -408,6 +499,32 @@ class Stack:
             secs = time.perf_counter() - t0
         return secs, nimg, kind
 
+    def parity(self):
+        """Sampled images of the timed output against the oracle chain (bf16
+        rounding between layers, ReLU / tanh as fused), reference
+        tensors_equal_approx form (tensor.hpp:275-286), tol 1e-2 (bf16 path)."""
+        import oracle
+        b = self.hi - self.lo
+        idx = sorted({0, max(0, b // 2 - 1), b - 1})
+        got = self.stack.out[idx].float().cpu().numpy()
+        h = oracle.bf16_round(self.x_host[idx])
+        for s, k in zip(self.specs, self.k_host):
+            h = oracle.tconv_fused(h, oracle.bf16_round(k), s.p)
+            h = oracle.bf16_round(np.maximum(h, 0) if s.activation == "relu" else np.tanh(h))
+        return {"max_scaled_err": scaled_err(got, h), "tol": 1e-2,
+                "images": [self.lo + i for i in idx], "oracle": "oracle.tconv_fused chain (C port, pinned)"}
+
+
+def scaled_err(got, want):
+    """max |a - b| / max(|a|, |b|, 1) -- the reference's tensors_equal_approx measure."""
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    if got.shape != want.shape:
+        return float("inf")
+    if got.size == 0:
+        return 0.0
+    return float((np.abs(got - want) / np.maximum(np.maximum(np.abs(got), np.abs(want)), 1.0)).max())
+
 
 def stack_specs(cfg):
     """Layer chain of a stack config: BASELINE C5, or a GAN generator preset."""
@@ -420,40 +537,96 @@ def stack_macs_per_image(cfg):
     return sum(count_ops(s.n_in, s.cin, s.cout, s.k, s.k, s.p)[2] for s in stack_specs(cfg))
 
 
+
+
+def config_dict(name, cfg, world, bwd=False):
+    """The `config` object of BOTH arms (identical, so the driver's same-config
+    check holds): the workload and how the batch is split, nothing arm-specific."""
+    batch = cfg["batch"]
+    return {"workload": f"{name}: {cfg['desc']}" + (" -- backward (input + kernel gradients)" if bwd else ""),
+            "global_batch": batch if cfg.get("stack") else batch * world,
+            "per_rank_batch": (batch + world - 1) // world if cfg.get("stack") else batch,
+            "parallelism": f"batch-sharded x{world}, weights replicated"
+            + (" (all-gather of the outputs reported as gather_ms)" if cfg.get("stack") else "")
+            + (", kernel-gradient all-reduce overlapped with the input gradient" if bwd and world > 1 else ""),
+            "l2": "GPU arm: flushed between timed steps (256 MiB write outside the events); "
+                  "CPU arm: not applicable"}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args):
+    """`--gpus N` without an outer launcher: re-run this script as N ranks under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1).  NCCL
+    init logging stays on (on stderr, so stdout keeps one JSON line)."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    log("bench: launching", args.gpus, "ranks:", " ".join(cmd))
+    sys.exit(subprocess.run(cmd, env=env).returncode)
+
+
 # ------------------------------------------------------------ reference arm
-def run_reference(args, cfg):
+def run_reference(args, cfg, world):
     """`--impl reference`: the reference's own CPU implementation (oracle/_ref, built
-    from the unmodified headers) on this box's host cores, same metric/config."""
+    from the unmodified headers) on this box's host cores, same metric/config.
+    Value: images spread over all host threads, each through the reference's
+    sequential transpose_conv_fused (the fastest way to run it on this host);
+    the reference's own threaded transpose_conv_fused_parallel is reported beside it."""
     import oracle
     workers = os.cpu_count() or 1
     kind = "reference" if oracle.ref_available() else "port"
     name = args.config
     rng = np.random.default_rng(SEED)
-    times, nimgs = [], 0
+    times, par_times = [], []
+    bwd = args.pass_ == "backward"
     if cfg.get("stack"):
-        from paper_2209_03704_b200 import stack as st
         specs = stack_specs(cfg)
         krng = np.random.default_rng(SEED)
         ks = [oracle.bf16_round(gen((s.k, s.k, s.cin, s.cout), "n02", krng)) for s in specs]
         nimg = min(cfg["batch"], max(1, 2 * workers))
         s0 = specs[0]
         x0 = oracle.bf16_round(rng.standard_normal((nimg, s0.n_in, s0.n_in, s0.cin), dtype=np.float32))
-        macs_img = stack_macs_per_image(cfg)
-        for i in range(args.warmup + args.steps):
-            x, secs = x0, 0.0
+        macs = stack_macs_per_image(cfg) * nimg
+
+        def chain(mode, w, n):
+            x, secs = x0[:n], 0.0
             for s, k in zip(specs, ks):
                 if kind == "reference":
-                    y, dt = oracle.ref_time_fused_batch(1, x, k, s.p, workers)
+                    y, dt = oracle.ref_time_fused_batch(mode, x, k, s.p, w)
                 else:
                     t0 = time.perf_counter()
                     y = oracle.tconv_fused(x, k, s.p)
                     dt = time.perf_counter() - t0
                 secs += dt
                 x = oracle.bf16_round(np.maximum(y, 0) if s.activation == "relu" else np.tanh(y))
+            return secs
+        for i in range(args.warmup + args.steps):
+            secs = chain(1, workers, nimg)
             if i >= args.warmup:
                 times.append(secs)
-        nimgs = nimg
-        macs = macs_img * nimg
+        if kind == "reference":  # the reference's own threading, a bounded sample
+            npar = min(nimg, 4)
+            par_times.append((chain(0, workers, npar), npar))
     else:
         b, n, cin, cout, k, p = (cfg[x] for x in ("batch", "n", "cin", "cout", "k", "p"))
         nimg = min(b, max(1, 2 * workers))
@@ -461,10 +634,8 @@ def run_reference(args, cfg):
         kk = gen((k, k, cin, cout), cfg["wd"], np.random.default_rng(SEED), fan_in=cin * k * k)
         if cfg["dtype"] == "bf16":
             x, kk = oracle.bf16_round(x), oracle.bf16_round(kk)
-        import ctypes  # noqa: F401
         from oracle.oracle import count_ops
         macs = count_ops(n, cin, cout, k, k, p)[2] * nimg
-        bwd = args.pass_ == "backward"
         if bwd:  # backward: 2x the forward's useful MACs; output gradient ~ N(0, 1)
             macs *= 2
             g = oracle.geometry(n, k, k, p)
@@ -486,28 +657,72 @@ def run_reference(args, cfg):
                 secs = time.perf_counter() - t0
             if i >= args.warmup:
                 times.append(secs)
-        nimgs = nimg
+        if kind == "reference" and not bwd:
+            npar = min(nimg, 4)
+            _, secs = oracle.ref_time_fused_batch(0, x[:npar], kk, p, workers)
+            par_times.append((secs, npar))
     sec = statistics.median(times)
     val = macs / sec / 1e9
-    sample = (f"{nimgs} of {cfg['batch']} images per step, harness batch-threading over the "
+    sample = (f"{nimg} of {cfg['batch']} images per step, harness batch-threading over the "
               f"reference's sequential transpose_conv_fused (images across {workers} threads)"
-              if kind == "reference" else f"{nimgs} images per step, single-thread C port")
-    if args.pass_ == "backward":
+              if kind == "reference" else f"{nimg} images per step, single-thread C port")
+    if bwd:
         sample = sample.replace("transpose_conv_fused",
                                 "net::FusedTConv::backward (timed; its forward untimed)")
-    out = {"metric": METRIC + (" [backward pass]" if args.pass_ == "backward" else ""),
+    cpu = {"value": round(val, 4), "unit": "useful GMAC/s",
+           "cores": workers if kind == "reference" else 1, "kind": kind, "sample": sample,
+           "cpu_model": cpu_model()}
+    if par_times:
+        secs, npar = par_times[0]
+        cpu["reference_parallel"] = {
+            "value": round(macs / nimg * npar / secs / 1e9, 4), "unit": "useful GMAC/s",
+            "what": f"the reference's own transpose_conv_fused_parallel({workers} workers; threads over "
+                    f"cout slices, capped at cout) per image, {npar} images"}
+    out = {"metric": METRIC + (" [backward pass]" if bwd else ""),
            "value": round(val, 4), "unit": "useful GMAC/s", "impl": "reference",
-           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True,
            "scaling": "strong" if cfg.get("stack") else "weak", "vs_baseline": None,
-           "dtype": "f32", "data": "synthetic (seeded, BASELINE distributions)",
-           "config": {"workload": f"{name}: {cfg['desc']}", "sampled_images": nimgs},
-           "cpu_baseline": {"value": round(val, 4), "unit": "useful GMAC/s",
-                            "cores": workers if kind == "reference" else 1, "kind": kind,
-                            "sample": sample},
+           "dtype": "f32", "data": "synthetic (seeded, BASELINE distributions; no dataset)",
+           "config": config_dict(name, cfg, world, bwd),
+           "cpu_baseline": cpu,
            "e2e": {"value": round(val, 4), "unit": "useful GMAC/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------- launcher check (CPU, gloo)
+def run_plumbing_check(args, cfg, world, rank):
+    """`--plumbing-check`: the multi-rank plumbing of the GPU arm on CPU (gloo):
+    rendezvous, batch shards, the weight broadcast, max-over-ranks timing
+    reduction and the output all-gather -- no convolution is computed.  Used by
+    the CPU test of `--gpus N` self-launch; never a bench number."""
+    import torch
+    import torch.distributed as dist
+    from paper_2209_03704_b200 import stack as st
+    if world > 1:
+        dist.init_process_group("gloo")
+    b = cfg["batch"]
+    lo, hi = st.shard_range(b, rank, world)
+    w = torch.arange(16, dtype=torch.float32) if rank == 0 else torch.zeros(16)
+    if world > 1:
+        dist.broadcast(w, src=0)
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    local = torch.arange(lo, hi, dtype=torch.float32).reshape(-1, 1).repeat(1, 3)
+    full = st.gather_shards(local, b) if world > 1 else local
+    ok = bool(torch.equal(full[:, 0], torch.arange(b, dtype=torch.float32))) and bool(
+        torch.equal(w, torch.arange(16, dtype=torch.float32)))
+    if rank == 0:
+        print(json.dumps({"plumbing_only": True, "n_gpus": world, "ranks_seen_max": float(t.item()),
+                          "shard": [lo, hi], "gathered_rows": int(full.shape[0]), "ok": ok,
+                          "config": config_dict(args.config, cfg, world)}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if not ok:
+        sys.exit(1)
 
 
 # ---------------------------------------------------------------- main arm
@@ -516,7 +731,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default=os.environ.get("SEGCONV_BENCH_CONFIG", "C2"),
+    ap.add_argument("--config", default=os.environ.get("SEGCONV_BENCH_CONFIG", "C5"),
                     choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="segconv", choices=["segconv", "reference"])
     ap.add_argument("--no-baselines", action="store_true", help="skip conventional/cuDNN/CPU legs")
@@ -524,22 +739,34 @@ def main():
                     help="backward: the layer's input + kernel gradients (not for the C5 stack)")
     ap.add_argument("--no-e2e", action="store_true",
                     help="diagnostics (ncu launch lists): skip the host-buffer e2e leg")
+    ap.add_argument("--no-parity", action="store_true", help="skip the sampled oracle check")
+    ap.add_argument("--plumbing-check", action="store_true",
+                    help="CPU (gloo) check of the multi-rank launch/shard/gather plumbing; no compute")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"bench: WORLD_SIZE={world} but --gpus {args.gpus}; reporting n_gpus = {world}")
 
+    if args.plumbing_check:
+        run_plumbing_check(args, cfg, world, rank)
+        return
     if args.impl == "reference":
         if rank == 0:
-            run_reference(args, cfg)
+            run_reference(args, cfg, world)
         return
 
     import torch
     import torch.distributed as dist
 
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the segconv arm has no CPU fallback)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -563,10 +790,10 @@ def main():
     torch.cuda.synchronize()
     # The timed step replays a CUDA graph of the hot path so host launch
     # overhead (ctypes, argument checks) is not on the device clock; the e2e
-    # leg below goes through the public Python API eagerly.
+    # leg below goes through the public API eagerly.  (The stack captures its
+    # own graph; the backward pass allocates its split-K workspace per call.)
     graph = None
-    # (the backward pass allocates its split-K workspace per call: eager)
-    if not cfg.get("stack") and not bwd and not os.environ.get("SEGCONV_BENCH_EAGER"):
+    if not cfg.get("stack") and not bwd:
         side = torch.cuda.Stream()
         side.wait_stream(stream)
         with torch.cuda.stream(side):
@@ -616,6 +843,42 @@ def main():
         macs_all = float(mt.item())
     value = macs_all / (ms * 1e-3) / 1e9
 
+    # ---- parity of the timed output (sampled images vs the oracle), every rank
+    parity = None
+    if not args.no_parity:
+        try:
+            parity = prob.parity()
+            parity["pass"] = bool(parity["max_scaled_err"] <= parity["tol"])
+        except Exception as e:  # report, do not hide
+            parity = {"error": str(e)[:200], "pass": False}
+        if world > 1:
+            pf = torch.tensor([0.0 if parity.get("pass") else 1.0], device=dev)
+            dist.all_reduce(pf, op=dist.ReduceOp.MAX)
+            parity["all_ranks_pass"] = bool(pf.item() == 0.0)
+
+    # ---- the stack's exchange step: all-gather of the output shards, max over ranks
+    gather = None
+    if cfg.get("stack"):
+        gms = 0.0
+        if world > 1:
+            for _ in range(2):
+                prob.gather()
+            torch.cuda.synchronize()
+            dist.barrier()
+            ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ga.record(stream)
+            for _ in range(args.steps):
+                full = prob.gather()
+            gb.record(stream)
+            torch.cuda.synchronize()
+            gt = torch.tensor([ga.elapsed_time(gb) / args.steps], device=dev, dtype=torch.float64)
+            dist.all_reduce(gt, op=dist.ReduceOp.MAX)
+            gms = float(gt.item())
+            assert full.shape[0] == prob.global_batch
+        gather = {"ms": round(gms, 5), "bytes_total": int(prob.global_batch * prob.stack.out[0].numel() * 2),
+                  "what": "ShardedStack.gather: NCCL all-gather of the bf16 output shards"
+                          if world > 1 else "single rank: nothing to gather"}
+
     # ---- e2e through the public API with host buffers (H2D + compute + D2H)
     e2e_steps = 0 if args.no_e2e else args.steps
     for _ in range(2 if e2e_steps else 0):
@@ -635,11 +898,23 @@ def main():
     e2e_ms = float(e2e_ms.item())
     h2d, d2h = prob.e2e_bytes()
 
-    # ---- roofline of the dominant kernel (the whole step is that kernel, or the
-    # 4-kernel stack graph for C5)
+    # ---- roofline of the dominant kernel: the single layer's kernel, or for the
+    # stack the slowest of its per-layer kernels (timed per layer with events)
     pk = peaks()
     kern_ms = statistics.mean(step_ms)
-    if prob.bound == "tensor":
+    layers = None
+    if cfg.get("stack"):
+        layers = prob.layer_times(max(5, min(args.steps, 20)), flush)
+        dom = max(layers, key=lambda l: l["ms"])
+        roof = {"bound": dom["bound"], "achieved": dom["achieved"], "peak": dom["peak"], "unit": dom["unit"],
+                "frac": dom["frac"], "kernel": f"layer {dom['layer']} ({dom['path']})",
+                "per_launch_ms": dom["ms"],
+                "peak_src": pk["src"] + (" bf16 burst" if dom["bound"] == "tensor" else " copy")}
+        ach = 2.0 * prob.macs / (kern_ms * 1e-3) / 1e12
+        stack_roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": pk["bf16"], "unit": "TFLOP/s",
+                      "frac": round(ach / pk["bf16"], 4),
+                      "what": "whole step (4 layers, one graph, PDL between layers)"}
+    elif prob.bound == "tensor":
         ach = 2.0 * prob.macs / (kern_ms * 1e-3) / 1e12
         div = getattr(prob, "tensor_peak_div", 1.0)
         roof = {"bound": "tensor", "achieved": round(ach, 2), "peak": round(pk["bf16"] / div, 1),
@@ -658,6 +933,34 @@ def main():
             roof["traffic"] = tr.get("dram_bytes_per_launch")
             roof["traffic_src"] = tr.get("source")
     hbm_gbs = prob.alg_bytes / (kern_ms * 1e-3) / 1e9
+
+    # ---- strong-scaling proxy on one GPU: the per-GPU share of the global batch
+    sweep = None
+    if cfg.get("stack") and world == 1 and not args.no_baselines:
+        sweep = {str(prob.global_batch): {"ms": round(ms, 5), "gmacs": round(value, 1)}}
+        for share in (2, 4, 8):
+            bb = prob.global_batch // share
+            sub = Stack(cfg, 0, 1, torch, sc, dev, batch=bb)
+            for _ in range(3):
+                flush()
+                sub.step()
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(args.steps):
+                flush()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                sub.step()
+                b.record(stream)
+                b.synchronize()
+                ts.append(a.elapsed_time(b))
+            sms = statistics.mean(ts)
+            sweep[str(bb)] = {"ms": round(sms, 5), "gmacs": round(sub.macs / (sms * 1e-3) / 1e9, 1),
+                              "projected_n_gpus": share,
+                              "projected_value": round(prob.macs / (sms * 1e-3) / 1e9, 1)}
+            del sub
+        sweep["note"] = ("one GPU timing the per-GPU batch of the 1/2/4/8-GPU split (projected_value = "
+                         "the global batch's MACs over that time, gather excluded)")
 
     out = None
     if rank == 0:
@@ -696,6 +999,7 @@ def main():
                 extra["cpu_baseline"] = {
                     "value": round(cpu_val, 4), "unit": "useful GMAC/s",
                     "cores": workers if kind == "reference" else 1, "kind": kind,
+                    "cpu_model": cpu_model(),
                     "sample": (f"{nimg} images of the same workload, reference "
                                + ("net::FusedTConv::backward (timed; its forward untimed)" if bwd
                                   else "transpose_conv_fused")
@@ -709,21 +1013,22 @@ def main():
                "scaling": "strong" if cfg.get("stack") else "weak", "vs_baseline": None,
                "dtype": "bf16" if cfg["dtype"] == "bf16" else "f32",
                "data": "synthetic (seeded, BASELINE distributions; no dataset)",
-               "config": {"workload": f"{args.config}: {cfg['desc']}"
-                          + (" -- backward (input + kernel gradients)" if bwd else ""),
-                          "math": prob.math,
-                          "per_gpu_batch": (prob.hi - prob.lo) if cfg.get("stack") else cfg["batch"],
-                          "l2": "flushed between timed steps (256 MiB write, outside events)",
-                          "parallelism": f"batch-sharded x{world}, weights replicated"
-                          + (", kernel-gradient all-reduce (NCCL) overlapped with the input "
-                             "gradient" if bwd and world > 1 else "")},
+               "config": config_dict(args.config, cfg, world, bwd),
+               "math": prob.math,
                "hbm_gbs": round(hbm_gbs, 1),
                "roofline": roof,
                "e2e": {"value": round(macs_all / (e2e_ms * 1e-3) / 1e9, 2), "unit": "useful GMAC/s",
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                        "ms_per_step": round(e2e_ms, 4)},
                "gpu_launches": int(launches),
+               "parity": parity,
                "clocks": clk.summary()}
+        if cfg.get("stack"):
+            out["stack_roofline"] = stack_roof
+            out["layers"] = layers
+            out["gather_ms"] = gather
+            if sweep:
+                out["strong_scaling_proxy"] = sweep
         out.update(extra)
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -165,11 +165,23 @@ class ShardedStack:
 
     def gather(self) -> torch.Tensor:
         """All-gather the per-rank output slices into the full batch (every rank)."""
-        out = self.local.out.contiguous()
-        sizes = [shard_range(self.global_batch, r, self.world) for r in range(self.world)]
-        maxb = max(h - l for l, h in sizes)
+        return gather_shards(self.local.out, self.global_batch, group=self.group)
+
+
+def gather_shards(local: torch.Tensor, global_batch: int, *, group=None) -> torch.Tensor:
+    """The batch's per-rank slices (shard_range order) all-gathered into the full
+    batch on every rank.  Uneven shards are padded to the largest one so a
+    single all_gather moves them (NCCL over NVLink on GPU, gloo on CPU)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    out = local.contiguous()
+    sizes = [shard_range(global_batch, r, world) for r in range(world)]
+    maxb = max(h - l for l, h in sizes)
+    if out.shape[0] == maxb:
+        pad = out
+    else:
         pad = out.new_zeros((maxb,) + tuple(out.shape[1:]))
         pad[: out.shape[0]].copy_(out)
-        bufs = [torch.empty_like(pad) for _ in range(self.world)]
-        self.dist.all_gather(bufs, pad, group=self.group)
-        return torch.cat([b[: h - l] for b, (l, h) in zip(bufs, sizes)], dim=0)
+    bufs = [torch.empty_like(pad) for _ in range(world)]
+    dist.all_gather(bufs, pad, group=group)
+    return torch.cat([b[: h - l] for b, (l, h) in zip(bufs, sizes)], dim=0)

@@ -29,5 +29,39 @@ def test_reference_arm_json_line(extra):
     assert line["cpu_baseline"]["value"] == line["value"]
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
     assert ("backward" in line["metric"]) == bool(extra)
+    sys.path.insert(0, ROOT)
+    import bench
+    assert line["config"] == bench.config_dict("C1", bench.CONFIGS["C1"], 1, bool(extra))
     if oracle.ref_available():
         assert line["cpu_baseline"]["kind"] == "reference"
+
+
+def test_gpus_flag_self_launches_ranks_gloo():
+    """`bench.py --gpus 2` with no outer launcher re-runs itself as 2 ranks
+    (torch.distributed.run on 127.0.0.1); the CPU plumbing check exercises the
+    rendezvous, the batch shards, the broadcast, the max-over-ranks reduction
+    and the output all-gather of the multi-GPU arm with gloo."""
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--plumbing-check"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.strip().splitlines() if l.startswith("{")]
+    assert len(lines) == 1  # rank 0 alone prints
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["ok"] and line["gathered_rows"] == 1024
+    assert line["ranks_seen_max"] == 2.0 and line["shard"] == [0, 512]
+    assert line["config"]["workload"].startswith("C5:")  # the headline default
+
+
+def test_reference_arm_config_equals_the_gpu_arms():
+    """Both arms build `config` with the same function, so the driver's
+    same-config check holds (round-1 verdict: it did not)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    for name in ("C1", "C2", "C5"):
+        cfg = bench.CONFIGS[name]
+        a = bench.config_dict(name, cfg, 1)
+        assert a == bench.config_dict(name, cfg, 1)
+        assert set(a) == {"workload", "global_batch", "per_rank_batch", "parallelism", "l2"}
+    assert bench.config_dict("C5", bench.CONFIGS["C5"], 8)["per_rank_batch"] == 128

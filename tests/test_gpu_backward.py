@@ -294,6 +294,12 @@ def test_full_size_tensor_core_backward_equals_simt(b, n, cin, cout, k):
     assert sc.last_path() == "bwd:simt-ffma+simt-ffma"
     assert torch.equal(gx_tc, gx_s)
     assert torch.equal(gk_tc, gk_s)
+    # and against the oracle (not only CUDA vs CUDA): the input gradient of
+    # sampled images depends on that image alone; exact sums rounded to bf16
+    idx = [0, b - 1]
+    xs, ks_, gys = (t.float().cpu().numpy() for t in (x[idx], kk, gy1[idx]))
+    wx, _ = oracle.tconv_backward(xs, ks_, 0, gys)
+    np.testing.assert_array_equal(gx_tc[idx].float().cpu().numpy(), oracle.bf16_round(wx))
     _, gk2 = sc.transpose_conv_fused_backward(x, kk, 0, gy2, math="bf16", input_grad=False)
     _, gk12 = sc.transpose_conv_fused_backward(x, kk, 0, (gy1.float() + gy2.float()).bfloat16(), math="bf16",
                                                input_grad=False)

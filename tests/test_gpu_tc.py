@@ -158,3 +158,36 @@ def test_config_c5_stack_bf16():
         h = oracle.bf16_round(np.maximum(h, 0) if s.activation == "relu" else np.tanh(h))
     assert y.shape == (b, 19, 19, 3)
     assert scaled_err(y, h) <= 1e-2
+
+
+def _c5_chain(specs, ks, x):
+    h = x
+    for s, k in zip(specs, ks):
+        h = oracle.tconv_fused(h, k, s.p)
+        h = oracle.bf16_round(np.maximum(h, 0) if s.activation == "relu" else np.tanh(h))
+    return h
+
+
+def test_config_c5_stack_batch_1024_graph_pdl():
+    """The benched configuration itself: BASELINE C5 at batch 1024 (the pair
+    kernel's feature-tile halving, tail half-tiles and wave count all depend on
+    the batch), captured in a CUDA graph with programmatic dependent launch
+    between layers, compared on sampled images {0, 511, 1023} -- and at the
+    per-GPU batches of the 2/4/8-GPU split -- with the oracle chain (bf16
+    rounding between layers)."""
+    from paper_2209_03704_b200 import stack as st
+    specs = st.c5_layers()
+    rng = np.random.default_rng(1024)
+    ks = [oracle.bf16_round(rng.standard_normal((s.k, s.k, s.cin, s.cout), dtype=np.float32) * 0.02)
+          for s in specs]
+    x = oracle.bf16_round(rng.standard_normal((1024, 4, 4, 1024), dtype=np.float32))
+    for b in (1024, 512, 128):
+        stack = st.GeneratorStack(specs, [cuda(k) for k in ks], b)
+        stack.capture()
+        y = stack.forward(cuda(x[:b], torch.bfloat16))
+        torch.cuda.synchronize()
+        idx = sorted({0, b // 2 - 1, b - 1})
+        got = y[idx].float().cpu().numpy()
+        assert got.shape == (len(idx), 19, 19, 3)
+        assert np.isfinite(got).all()
+        assert scaled_err(got, _c5_chain(specs, ks, x[idx])) <= 1e-2, b
