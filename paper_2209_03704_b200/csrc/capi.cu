@@ -13,6 +13,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "segconv_b200.h"
+#include "tc_guard.cuh"
 
 namespace segconv_b200 {
 
@@ -75,6 +76,22 @@ static int64_t fold_image_elems(const segconv_subkernels& s) {
   const int planes = s.dtype == SEGCONV_F16_SPLIT ? 2 : 1;
   return (int64_t)planes * nkb * (s.k_block / 8) *
          fold_rows(s.source_kh, s.source_kw, s.p_orig, s.cout) * 8;
+}
+
+// Split-fp16 panels of the folded / scatter / halo kernels end in the range
+// guard (tc_guard.cuh): header + fp32 kernel, 16-byte aligned.
+static bool split_guarded(int layout, int dtype) {
+  return dtype == SEGCONV_F16_SPLIT && (layout == SEGCONV_PANEL_UMMA_FOLD || layout == SEGCONV_PANEL_UMMA);
+}
+static int64_t guard_elems(const segconv_subkernels& s) {
+  return split_guarded(s.layout, s.dtype)
+             ? (int64_t)(split_guard_bytes(s.source_kh, s.source_kw, s.cin, s.cout) / 2)
+             : 0;
+}
+// elements of every image the kernels read (the guard follows them)
+static int64_t image_elems(const segconv_subkernels& s) { return s.total_elems - guard_elems(s); }
+static const void* guard_of(const segconv_subkernels& s, const void* panels) {
+  return split_guarded(s.layout, s.dtype) ? (const void*)((const uint16_t*)panels + image_elems(s)) : nullptr;
 }
 
 static SegClasses classes_of(const segconv_subkernels& s, const segconv_geometry& g) {
@@ -231,6 +248,8 @@ segconv_status segconv_subkernels_init(int kh, int kw, int cin, int cout, int p_
     s.cout_pad = n_tiles * s.n_tile;
     s.total_elems = (int64_t)n_tiles * nkb * taps * planes * s.k_block * s.n_tile;
   }
+  if (split_guarded(s.layout, s.dtype))
+    s.total_elems = (s.total_elems + 7) / 8 * 8 + (int64_t)(split_guard_bytes(kh, kw, cin, cout) / 2);
   *out = s;
   return SEGCONV_OK;
 }
@@ -338,6 +357,15 @@ segconv_status segconv_segregate(const void* d_kernel, segconv_dtype kernel_dtyp
     cls.sub_offset[q] = sks->sub_offset[q];
   }
   if (sks->total_elems == 0) return SEGCONV_OK;
+  // split-fp16 images read the weight scale from the guard header: write it first
+  void* guard = const_cast<void*>(guard_of(*sks, d_panels));
+  if (guard) {
+    const segconv_status gst = cuda_status(
+        launch_split_guard(d_kernel, kernel_dtype, sks->source_kh, sks->source_kw, sks->cin, sks->cout, cls,
+                           guard, (cudaStream_t)stream),
+        "segregate[guard]");
+    if (gst != SEGCONV_OK) return gst;
+  }
   if (sks->layout == SEGCONV_PANEL_UMMA_FOLD) {
     cls.off_r[0] = cls.off_r[1] = 0;
     for (int q = 0; q < 4; ++q) {
@@ -347,18 +375,18 @@ segconv_status segconv_segregate(const void* d_kernel, segconv_dtype kernel_dtyp
     segconv_status st = cuda_status(
         launch_segregate_fold(d_kernel, kernel_dtype, sks->source_kh, sks->source_kw, sks->cin,
                               sks->cout, sks->p_orig, cls, sks->dtype == SEGCONV_F16_SPLIT,
-                              d_panels, (cudaStream_t)stream),
+                              d_panels, guard, (cudaStream_t)stream),
         "segregate[fold]");
-    if (st == SEGCONV_OK && sks->total_elems > fold_image_elems(*sks)) {
+    if (st == SEGCONV_OK && image_elems(*sks) > fold_image_elems(*sks)) {
       uint16_t* tail = (uint16_t*)d_panels + fold_image_elems(*sks);
       if (fold_ts_panels_apply(sks->source_kh, sks->source_kw, sks->cin, sks->cout, sks->p_orig,
                                sks->dtype))
         st = cuda_status(launch_fold_ts_image(d_kernel, kernel_dtype, sks->source_kh,
                                               sks->source_kw, sks->cin, sks->cout, sks->p_orig,
-                                              cls, tail, (cudaStream_t)stream),
+                                              cls, tail, guard, (cudaStream_t)stream),
                          "segregate[fold-ts]");
       else if (sks->dtype == SEGCONV_F16_SPLIT)
-        st = cuda_status(launch_ring_image(d_kernel, kernel_dtype, sks->cin, cls, tail,
+        st = cuda_status(launch_ring_image(d_kernel, kernel_dtype, sks->cin, cls, tail, guard,
                                            (cudaStream_t)stream),
                          "segregate[ring]");
       else
@@ -376,7 +404,7 @@ segconv_status segconv_segregate(const void* d_kernel, segconv_dtype kernel_dtyp
     return cuda_status(launch_segregate_umma(d_kernel, kernel_dtype, sks->source_kw, sks->cin,
                                              sks->cout, cls, sks->n_tile, sks->k_block, nkb,
                                              n_tiles, taps, sks->dtype == SEGCONV_F16_SPLIT,
-                                             d_panels, (cudaStream_t)stream),
+                                             d_panels, guard, (cudaStream_t)stream),
                        "segregate[umma]");
   }
   if (sks->layout == SEGCONV_PANEL_KMAJOR && sks->dtype == SEGCONV_F16_SPLIT)
@@ -474,6 +502,7 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
   pr.epi = epilogue;
   pr.y = d_y;
   pr.y_dtype = y_dtype;
+  pr.guard = guard_of(*sks, d_panels);
   cudaStream_t s = (cudaStream_t)stream;
 
   if (math == SEGCONV_MATH_AUTO) math = (segconv_math)sks->math;  // what the panels were built for
@@ -526,13 +555,13 @@ segconv_status segconv_transpose_conv_fused(const void* d_x, segconv_dtype x_dty
           return fail(SEGCONV_E_UNSUPPORTED,
                       "class-folded tensor-core path: needs p_fused == 0, cin a multiple of the "
                       "channel block and a halo that fits shared memory");
-        if (sks->total_elems > fold_image_elems(*sks) && tc_tile_supported(pr, math) && (g_path = "tc-tile"))
+        if (image_elems(*sks) > fold_image_elems(*sks) && tc_tile_supported(pr, math) && (g_path = "tc-tile"))
           return cuda_status(launch_tc_tile(pr, (const uint16_t*)d_panels + fold_image_elems(*sks), s),
                              "transpose_conv_fused[tcgen05 tile]");
-        if (sks->total_elems > fold_image_elems(*sks) && tc_ring_supported(pr, math) && (g_path = "tc-ring"))
+        if (image_elems(*sks) > fold_image_elems(*sks) && tc_ring_supported(pr, math) && (g_path = "tc-ring"))
           return cuda_status(launch_tc_ring(pr, (const uint16_t*)d_panels + fold_image_elems(*sks), s),
                              "transpose_conv_fused[tcgen05 ring]");
-        if (sks->total_elems > fold_image_elems(*sks) &&
+        if (image_elems(*sks) > fold_image_elems(*sks) &&
             fold_ts_panels_apply(sks->source_kh, sks->source_kw, sks->cin, sks->cout, sks->p_orig,
                                  sks->dtype) &&
             tc_fold_ts_supported(pr, math) && (g_path = "tc-fold-ts"))

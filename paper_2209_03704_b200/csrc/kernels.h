@@ -30,6 +30,9 @@ struct FusedProblem {
   unsigned epi;
   void* y;
   int y_dtype;
+  // split-fp16 panels: the range-guard header (tc_guard.cuh) -- weight scale,
+  // fp32 kernel for the CTA-local FFMA fallback; nullptr otherwise
+  const void* guard;
 };
 
 // Backward pass of the fused layer (reference netdemo/layers.hpp:171-211).
@@ -74,7 +77,7 @@ cudaError_t launch_segregate(const void* k, int k_dtype, int kh, int kw, int cin
 
 cudaError_t launch_segregate_umma(const void* k, int k_dtype, int kw, int cin, int cout,
                                   const SegClasses& cls, int NT, int KB, int nkb, int n_tiles,
-                                  int taps, bool split, void* panels, cudaStream_t s);
+                                  int taps, bool split, void* panels, const void* guard, cudaStream_t s);
 int tc_n_tile(int math, int cout);
 // class-folded tcgen05 kernel for narrow layers (tc_fold.cu)
 cudaError_t launch_tc_fold(const FusedProblem& pr, int math, cudaStream_t s);
@@ -88,7 +91,7 @@ int tc_wide_ntile(int cout);
 bool tc_ring_supported(const FusedProblem& pr, int math);
 cudaError_t launch_tc_ring(const FusedProblem& pr, const void* ring_img, cudaStream_t s);
 cudaError_t launch_ring_image(const void* k, int k_dtype, int cin, const SegClasses& cls, void* out,
-                              cudaStream_t s);
+                              const void* guard, cudaStream_t s);
 size_t ring_image_bytes(int cin);
 // pixel-scatter kernel for 3x3 -> 3-channel bf16 layers on small images (tc_tile.cu)
 bool tc_tile_supported(const FusedProblem& pr, int math);
@@ -102,7 +105,8 @@ cudaError_t launch_tc_fold_ts(const FusedProblem& pr, const void* img, cudaStrea
 bool fold_ts_panels_apply(int kh, int kw, int cin, int cout, int p_orig, int panel_dtype);
 size_t fold_ts_image_bytes_for(int kh, int kw, int cin, int p_orig);
 cudaError_t launch_fold_ts_image(const void* k, int k_dtype, int kh, int kw, int cin, int cout,
-                                 int p_orig, const SegClasses& cls, void* out, cudaStream_t s);
+                                 int p_orig, const SegClasses& cls, void* out, const void* guard,
+                                 cudaStream_t s);
 bool tc_fold_ts_supported(const FusedProblem& pr, int math);
 bool tc_fold_available(int math, int cin, int cout);
 bool tc_fold_fits(int math, int kh, int kw, int p, int cin, int cout);
@@ -112,7 +116,7 @@ int fold_kb(int math, int cin);
 int fold_rows(int kh, int kw, int p, int cout);
 cudaError_t launch_segregate_fold(const void* k, int k_dtype, int kh, int kw, int cin, int cout,
                                   int p, const SegClasses& cls, bool split, void* panels,
-                                  cudaStream_t s);
+                                  const void* guard, cudaStream_t s);
 int tc_k_block(int cin, int cout);
 
 // SIMT kernels (direct.cu).  Return cudaErrorNotSupported when no

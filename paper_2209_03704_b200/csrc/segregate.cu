@@ -12,6 +12,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_guard.cuh"
 
 namespace segconv_b200 {
 
@@ -87,14 +88,6 @@ __global__ void kernel_amax(const TK* __restrict__ k, long long n, unsigned* __r
   if ((threadIdx.x & 31) == 0) atomicMax(amax_bits, __float_as_uint(m));  // non-negative floats order as uints
 }
 
-__device__ __forceinline__ int split_scale_exp(unsigned amax_bits) {
-  const float amax = __uint_as_float(amax_bits);
-  if (!(amax > 0.0f)) return 0;
-  int e;
-  frexpf(amax, &e);  // amax in [2^(e-1), 2^e)
-  const int s = 14 - e;
-  return s < -20 ? -20 : (s > 60 ? 60 : s);
-}
 
 template <typename TK>
 __global__ void segregate_kmajor_split_kernel(const TK* __restrict__ k, int kw, int cin, int cout, SegClasses cls,
@@ -183,9 +176,11 @@ cudaError_t launch_segregate(const void* k, int k_dtype, int kh, int kw, int cin
 template <typename TK, bool SPLIT>
 __global__ void segregate_umma_kernel(const TK* __restrict__ k, int kw, int cin, int cout,
                                       SegClasses cls, int NT, int KB, int nkb, int taps,
-                                      uint16_t* __restrict__ out, long long rows_total) {
+                                      uint16_t* __restrict__ out, long long rows_total,
+                                      const SplitGuard* __restrict__ guard) {
   const int CH = KB / 8;
   constexpr int PLANES = SPLIT ? 2 : 1;
+  const float wscale = SPLIT ? ldexpf(1.0f, split_scale_exp(guard->amax_bits)) : 1.0f;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < rows_total;
        e += (long long)gridDim.x * blockDim.x) {
     const int n = (int)(e % NT);
@@ -209,8 +204,8 @@ __global__ void segregate_umma_kernel(const TK* __restrict__ k, int kw, int cin,
       const int ci = kb * KB + j * 8 + x;
       float w = 0.0f;
       if (f < cout && ci < cin)
-        w = (float)to_acc(k[(((long long)(cls.u0[q] + 2 * u) * kw + (cls.v0[q] + 2 * v)) * cin + ci) *
-                                cout + f]);
+        w = wscale * (float)to_acc(k[(((long long)(cls.u0[q] + 2 * u) * kw + (cls.v0[q] + 2 * v)) * cin + ci) *
+                                         cout + f]);
       if constexpr (SPLIT) {
         const __half h = __float2half_rn(w);
         hi[x] = __half_as_ushort(h);
@@ -232,7 +227,8 @@ __global__ void segregate_umma_kernel(const TK* __restrict__ k, int kw, int cin,
 
 cudaError_t launch_segregate_umma(const void* k, int k_dtype, int kw, int cin, int cout,
                                   const SegClasses& cls, int NT, int KB, int nkb, int n_tiles,
-                                  int taps, bool split, void* panels, cudaStream_t s) {
+                                  int taps, bool split, void* panels, const void* guard, cudaStream_t s) {
+  if (split && !guard) return cudaErrorInvalidValue;
   const long long rows_total = (long long)n_tiles * nkb * taps * (KB / 8) * NT;
   const int threads = 256;
   const unsigned blocks = (unsigned)std::min<long long>((rows_total + threads - 1) / threads, 148LL * 32);
@@ -240,10 +236,12 @@ cudaError_t launch_segregate_umma(const void* k, int k_dtype, int kw, int cin, i
   do {                                                                                         \
     if (split)                                                                                 \
       segregate_umma_kernel<KT, true><<<blocks, threads, 0, s>>>(                              \
-          (const KT*)k, kw, cin, cout, cls, NT, KB, nkb, taps, (uint16_t*)panels, rows_total); \
+          (const KT*)k, kw, cin, cout, cls, NT, KB, nkb, taps, (uint16_t*)panels, rows_total, \
+          (const SplitGuard*)guard);                                                           \
     else                                                                                       \
       segregate_umma_kernel<KT, false><<<blocks, threads, 0, s>>>(                             \
-          (const KT*)k, kw, cin, cout, cls, NT, KB, nkb, taps, (uint16_t*)panels, rows_total); \
+          (const KT*)k, kw, cin, cout, cls, NT, KB, nkb, taps, (uint16_t*)panels, rows_total, \
+          nullptr);                                                                            \
   } while (0)
   if (k_dtype == SEGCONV_F32)
     SEGU(float);
@@ -265,8 +263,10 @@ template <typename TK, bool SPLIT>
 __global__ void segregate_fold_kernel(const TK* __restrict__ k, int kw, int cin, int cout,
                                       SegClasses cls, int CP, int KB, int uc, int rows_per_col,
                                       int nshift_rows, uint16_t* __restrict__ out,
-                                      long long chunks_total, long long plane_elems) {
+                                      long long chunks_total, long long plane_elems,
+                                      const SplitGuard* __restrict__ guard) {
   const int CH = KB / 8;
+  const float wscale = SPLIT ? ldexpf(1.0f, split_scale_exp(guard->amax_bits)) : 1.0f;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < chunks_total;
        e += (long long)gridDim.x * blockDim.x) {
     const int row = (int)(e % rows_per_col);
@@ -284,8 +284,8 @@ __global__ void segregate_fold_kernel(const TK* __restrict__ k, int kw, int cin,
       const int ci = kb * KB + j * 8 + x;
       float w = 0.0f;
       if (tap && ci < cin)
-        w = (float)to_acc(
-            k[(((long long)(cls.u0[q] + 2 * u) * kw + (cls.v0[q] + 2 * v)) * cin + ci) * cout + f]);
+        w = wscale * (float)to_acc(
+                         k[(((long long)(cls.u0[q] + 2 * u) * kw + (cls.v0[q] + 2 * v)) * cin + ci) * cout + f]);
       if constexpr (SPLIT) {
         const __half h = __float2half_rn(w);
         hi[x] = __half_as_ushort(h);
@@ -306,7 +306,8 @@ __global__ void segregate_fold_kernel(const TK* __restrict__ k, int kw, int cin,
 
 cudaError_t launch_segregate_fold(const void* k, int k_dtype, int kh, int kw, int cin, int cout,
                                   int p, const SegClasses& cls, bool split, void* panels,
-                                  cudaStream_t s) {
+                                  const void* guard, cudaStream_t s) {
+  if (split && !guard) return cudaErrorInvalidValue;
   int ur, uc;
   fold_window(kh, kw, p, &ur, &uc);
   const int CP = fold_cp(cout);
@@ -322,12 +323,12 @@ cudaError_t launch_segregate_fold(const void* k, int k_dtype, int kh, int kw, in
       segregate_fold_kernel<KT, true><<<blocks, 256, 0, s>>>((const KT*)k, kw, cin, cout, cls,  \
                                                              CP, KB, uc, rows, ur * uc * 4 * CP, \
                                                              (uint16_t*)panels, chunks_total,  \
-                                                             plane_elems);                     \
+                                                             plane_elems, (const SplitGuard*)guard); \
     else                                                                                       \
       segregate_fold_kernel<KT, false><<<blocks, 256, 0, s>>>((const KT*)k, kw, cin, cout, cls, \
                                                               CP, KB, uc, rows, ur * uc * 4 * CP, \
                                                               (uint16_t*)panels, chunks_total, \
-                                                              plane_elems);                    \
+                                                              plane_elems, nullptr);           \
   } while (0)
   if (k_dtype == SEGCONV_F32)
     SEGF(float);
@@ -339,6 +340,60 @@ cudaError_t launch_segregate_fold(const void* k, int k_dtype, int kh, int kw, in
     return cudaErrorInvalidValue;
 #undef SEGF
   note_launch();
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------- split guard
+// Header of the split-fp16 panels (tc_guard.cuh): max |w|, W1 = max over
+// (class, feature) of sum |w| over the class's taps and channels, 2^-s; then
+// the kernel in fp32 (reference layout) for the CTA-local FFMA fallback.
+template <typename TK>
+__global__ void guard_w1_kernel(const TK* __restrict__ k, int kw, int cin, int cout, SegClasses cls,
+                                unsigned* __restrict__ w1_bits) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 4 * cout) return;
+  const int q = t / cout, f = t % cout;
+  float sum = 0.0f;
+  for (int u = 0; u < cls.kh[q]; ++u)
+    for (int v = 0; v < cls.kw[q]; ++v)
+      for (int ch = 0; ch < cin; ++ch)
+        sum += fabsf((float)to_acc(k[(((long long)(cls.u0[q] + 2 * u) * kw + (cls.v0[q] + 2 * v)) * cin + ch) *
+                                         cout + f]));
+  atomicMax(w1_bits, __float_as_uint(sum));  // non-negative floats order as uints
+}
+
+template <typename TK>
+__global__ void guard_copy_kernel(const TK* __restrict__ k, long long n, SplitGuard* __restrict__ g) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) g->inv_scale = ldexpf(1.0f, -split_scale_exp(g->amax_bits));
+  float* dst = reinterpret_cast<float*>(g + 1);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    dst[e] = (float)to_acc(k[e]);
+}
+
+cudaError_t launch_split_guard(const void* k, int k_dtype, int kh, int kw, int cin, int cout,
+                               const SegClasses& cls, void* guard, cudaStream_t s) {
+  SplitGuard* g = static_cast<SplitGuard*>(guard);
+  if (!g || ((uintptr_t)g & 15)) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemsetAsync(g, 0, sizeof(SplitGuard), s);
+  if (e != cudaSuccess) return e;
+  const long long nk = (long long)kh * kw * cin * cout;
+  const unsigned ab = (unsigned)std::max(1LL, std::min<long long>((nk + 255) / 256, 148LL * 8));
+  const unsigned wb = (unsigned)((4 * cout + 127) / 128);
+#define GUARD_CASE(TK)                                                                        \
+  kernel_amax<TK><<<ab, 256, 0, s>>>((const TK*)k, nk, &g->amax_bits);                        \
+  guard_w1_kernel<TK><<<wb, 128, 0, s>>>((const TK*)k, kw, cin, cout, cls, &g->w1_bits);      \
+  guard_copy_kernel<TK><<<ab, 256, 0, s>>>((const TK*)k, nk, g);
+  if (k_dtype == SEGCONV_F32) {
+    GUARD_CASE(float)
+  } else if (k_dtype == SEGCONV_F64) {
+    GUARD_CASE(double)
+  } else if (k_dtype == SEGCONV_BF16) {
+    GUARD_CASE(__nv_bfloat16)
+  } else {
+    return cudaErrorInvalidValue;
+  }
+#undef GUARD_CASE
+  note_launch(3);
   return cudaGetLastError();
 }
 

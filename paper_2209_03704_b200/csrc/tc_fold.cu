@@ -40,6 +40,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_ptx.cuh"
+#include "tc_guard.cuh"
 
 namespace segconv_b200 {
 namespace tcf {
@@ -81,6 +82,7 @@ struct Params {
   int debug_nostore;               // diagnostics (SEGCONV_TC_DEBUG bits): 1 skip global
                                    // stores, 2 skip the fp16 split, 4 skip epilogue body,
                                    // 8 skip the MMAs
+  FallbackArgs fb;                 // split-fp16 range guard (tc_guard.cuh)
 };
 
 __device__ __forceinline__ void trace_ev(const Params& p, int ev, int local) {
@@ -135,7 +137,7 @@ __device__ __forceinline__ YT cvt_out(float v) {
 template <typename YT, int ACT>
 __device__ __forceinline__ void fold_epilogue_block(const Params& p, const float (&v)[32],
                                                     float* tile, const Walk& w, int warp,
-                                                    int lane, int ncols) {
+                                                    int lane, int ncols, float wsc, float& chk) {
   // write: thread = row, column k -> tile[k][row]
 #pragma unroll
   for (int k = 0; k < 32; ++k) tile[k * 36 + lane] = v[k];
@@ -158,6 +160,8 @@ __device__ __forceinline__ void fold_epilogue_block(const Params& p, const float
   const int q0 = (warp * 32) / CP;                 // first class in this quadrant
   const int nq = min(4 - q0, max(1, 32 / CP));     // classes held by these 32 rows
   auto fin = [&](float x, int f) {
+    guard_check(chk, x);  // range guard: the raw sum of a stored output
+    x *= wsc;  // split-fp16 images hold w * 2^s (1 otherwise)
     if (p.epi & SEGCONV_EPI_BIAS) x += __ldg(p.bias + f);
     if (ACT == 1) x = fmaxf(x, 0.0f);
     if (ACT == 2) x = tanhf(x);
@@ -266,8 +270,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* l_empty = l_full + SL;
   uint64_t* w_free = l_empty + SL;  // TMEM-A: weight image copied out of SMEM
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_free + 1);
+  // a converter saw x outside the split's range (the word after the TMEM slot)
+  volatile int& guard_bad = *reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) guard_bad = 0;
   if (warp == 12 && lane == 0) {
     for (int s = 0; s < SA; ++s) {
       mbar_init(&a_land[s], 1);
@@ -378,6 +385,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t pa = 0, pl = 0;
       const uint32_t lrow = (uint32_t)p.kb * 4;
       if (TMEM_A) mbar_wait(w_free, 0);  // operand stages hold the staged weights until then
+      GuardTrack gt;
+      gt.init(p.fb.guard);
       long long m0;
       int nu, b, i0, j0;
       for (int k = 0; next_unit(p, k, m0, nu, b, i0, j0); ++k) {
@@ -398,6 +407,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const uint32_t src = lbase + (uint32_t)r * lrow + (uint32_t)j * 32;
                 ld_shared_v4f(src, v[u][0]);
                 ld_shared_v4f(src + 16, v[u][1]);
+                gt.add(v[u][0]);
+                gt.add(v[u][1]);
               }
             }
 #pragma unroll
@@ -428,6 +439,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+      if (gt.bad()) guard_bad = 1;
     } else if constexpr (MODE == MODE_F16X3) {
       const int pt = threadIdx.x - 256;
       int st = 0;
@@ -435,6 +447,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int rows_staged = p.block_mode ? p.P * p.TRH : p.pieces * p.piece_rows;
       // RPC row slots of 128 per chunk column; RPT_MAX = 4 chunks x RPC slots
       constexpr int RPC = 3, RPT_MAX = 4 * RPC;  // <= 384 rows x 4 chunks per stage
+      GuardTrack gt;
+      gt.init(p.fb.guard);
       long long m0;
       int nu, b, i0, j0;
       for (int k = 0; next_unit(p, k, m0, nu, b, i0, j0); ++k) {
@@ -460,6 +474,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint32_t src = sbase + (uint32_t)j * 2 * COL + (uint32_t)s * 32;
               ld_shared_v4f(src, v[q][0]);
               ld_shared_v4f(src + 16, v[q][1]);
+              gt.add(v[q][0]);
+              gt.add(v[q][1]);
             }
           }
           named_bar(1, 128);
@@ -483,6 +499,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+      if (gt.bad()) guard_bad = 1;
     }
   } else if (warp == 13) {
     // ================= resident weights in SMEM: one bulk-copy pass
@@ -591,6 +608,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int q = row / p.CP, f = row - (row / p.CP) * p.CP;
     const bool row_ok = row < p.R && f < p.cout;
     const bool warp_live = quad * 32 < p.R;
+    const float wsc = MODE == MODE_F16X3 ? guard_inv_scale(p.fb.guard) : 1.0f;
+    float chk = 0.0f;  // range guard: NaN once a stored sum is not finite
     (void)q;
     (void)row_ok;
     const long long img = (long long)p.n * p.n;
@@ -632,12 +651,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tmem_ld32(tbase + (uint32_t)c0, v);
           if (!(p.debug_nostore & 4)) {
             switch (sel) {
-              case 0: fold_epilogue_block<float, 0>(p, v, tile, w, quad, lane, nu - c0); break;
-              case 1: fold_epilogue_block<float, 1>(p, v, tile, w, quad, lane, nu - c0); break;
-              case 2: fold_epilogue_block<float, 2>(p, v, tile, w, quad, lane, nu - c0); break;
-              case 3: fold_epilogue_block<__nv_bfloat16, 0>(p, v, tile, w, quad, lane, nu - c0); break;
-              case 4: fold_epilogue_block<__nv_bfloat16, 1>(p, v, tile, w, quad, lane, nu - c0); break;
-              default: fold_epilogue_block<__nv_bfloat16, 2>(p, v, tile, w, quad, lane, nu - c0); break;
+              case 0: fold_epilogue_block<float, 0>(p, v, tile, w, quad, lane, nu - c0, wsc, chk); break;
+              case 1: fold_epilogue_block<float, 1>(p, v, tile, w, quad, lane, nu - c0, wsc, chk); break;
+              case 2: fold_epilogue_block<float, 2>(p, v, tile, w, quad, lane, nu - c0, wsc, chk); break;
+              case 3: fold_epilogue_block<__nv_bfloat16, 0>(p, v, tile, w, quad, lane, nu - c0, wsc, chk); break;
+              case 4: fold_epilogue_block<__nv_bfloat16, 1>(p, v, tile, w, quad, lane, nu - c0, wsc, chk); break;
+              default: fold_epilogue_block<__nv_bfloat16, 2>(p, v, tile, w, quad, lane, nu - c0, wsc, chk); break;
             }
           }
           walk_advance(w, 64);
@@ -652,6 +671,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         pacc ^= 1;
       }
     }
+    if (MODE == MODE_F16X3 && guard_check_bad(chk)) guard_bad = 1;
   }
 
   tc_fence_before();
@@ -660,6 +680,34 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
                  : "memory");
+  }
+  if (MODE == MODE_F16X3 && guard_bad) {
+    // x left the split-fp16 range in this CTA's halos: recompute the anchors
+    // of its units with FFMA (this CTA wrote them; the barrier orders the rewrite)
+    if (!p.block_mode) {
+      const long long g16 = (p.Mv + 15) / 16;
+      const long long a0 = g16 * blockIdx.x / gridDim.x * 16;
+      const long long a1 = min(p.Mv, g16 * (blockIdx.x + 1) / gridDim.x * 16);
+      const int img = p.n * p.n;
+      guard_fallback(p.fb, a1 - a0, 0, p.cout, [&](long long idx, int& b, int& i, int& j) {
+        const long long m = a0 + idx;
+        b = (int)(m / img);
+        const int rem = (int)(m - (long long)b * img);
+        i = rem / p.n;
+        j = rem - i * p.n;
+        return true;
+      });
+    } else {
+      long long m0;
+      int nu, b0, i0, j0;
+      for (int k = 0; next_unit(p, k, m0, nu, b0, i0, j0); ++k)
+        guard_fallback(p.fb, (long long)p.TR * p.TC, 0, p.cout, [&](long long idx, int& b, int& i, int& j) {
+          b = b0;
+          i = i0 + (int)(idx / p.TC);
+          j = j0 + (int)(idx % p.TC);
+          return true;
+        });
+    }
   }
 }
 
@@ -761,6 +809,8 @@ static FoldPlan make_fold_plan_n(const FusedProblem& pr, int math, int block_n) 
   p.y_dtype = pr.y_dtype;
   p.bias = pr.bias;
   p.epi = pr.epi;
+  p.fb = make_fallback_args(pr, split ? pr.guard : nullptr);
+  if (split && !pr.guard) return pl;
   for (int q = 0; q < 4; ++q) {
     p.rows[q] = pr.cls.rows[q];
     p.cols[q] = pr.cls.cols[q];

@@ -41,6 +41,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_ptx.cuh"
+#include "tc_guard.cuh"
 
 namespace segconv_b200 {
 namespace tcfs {
@@ -74,7 +75,7 @@ struct Params {
   const uint8_t* panels;  // UMMA_FOLD image, split planes
   unsigned long long* trace;
   int debug;
-  int cluster;  // CTAs per cluster sharing the weight image load (1, 2 or 4)
+  FallbackArgs fb;  // range guard (tc_guard.cuh): weight scale, FFMA fallback
 };
 
 __device__ __forceinline__ void trace_ev(const Params& p, int ev, int local) {
@@ -94,21 +95,10 @@ __device__ __forceinline__ bool next_unit(const Params& p, int k, long long& m0,
   return true;
 }
 
-// The weight image lands at the top stages of every CTA.  With clusters, CTA
-// r of the cluster fetches slice r of the image and multicasts it to all, so
-// L2 serves each weight byte once per cluster rather than once per SM.
+// The weight image lands at the top stages of every CTA.
 __device__ __forceinline__ void issue_weights(const Params& p, uint8_t* smem, uint64_t* w_full) {
   mbar_arrive_expect_tx(w_full, (uint32_t)p.w_img_bytes);
   uint8_t* dst = smem + (size_t)p.w_stage0 * p.stage_bytes;
-  if (p.cluster > 1) {
-    const uint32_t r = cluster_ctarank();
-    const uint32_t slice = (uint32_t)p.w_img_bytes / (uint32_t)p.cluster;  // 16-byte multiple
-    const uint16_t mask = (uint16_t)((1u << p.cluster) - 1);
-    constexpr uint32_t CHUNK = 16384;
-    for (uint32_t off = r * slice; off < (r + 1) * slice; off += CHUNK)
-      bulk_g2s_multicast(dst + off, p.panels + off, min(CHUNK, (r + 1) * slice - off), w_full, mask);
-    return;
-  }
   constexpr uint32_t CHUNK = 32768;
   for (uint32_t off = 0; off < (uint32_t)p.w_img_bytes; off += CHUNK)
     bulk_g2s(dst + off, p.panels + off, min(CHUNK, (uint32_t)p.w_img_bytes - off), w_full);
@@ -148,9 +138,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* w_full = acc_empty + 2;  // weight image landed in SMEM
   uint64_t* w_free = w_full + 1;     // weights copied into TMEM, staging area free
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_free + 1);
+  // a converter saw x outside the split's range (the word after the TMEM slot)
+  volatile int& guard_bad = *reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
+    guard_bad = 0;
     trace_ev(p, 9, 0);  // kernel entry
     if (p.trace && blockIdx.x < 160) p.trace[(blockIdx.x * 16 + 12) * 64] = clock64();
   }
@@ -179,7 +172,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (p.cluster > 1) cluster_sync();  // peers' mbarriers exist before any multicast lands
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) trace_ev(p, 10, 0);  // prologue done
 
@@ -233,6 +225,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t ph = 0;
     long long m0;
     int nu;
+    GuardTrack gt;
+    gt.init(p.fb.guard);
     for (int k = 0; next_unit(p, k, m0, nu); ++k) {
       const int rows_live = min(p.S_pad, nu + p.max_shift);
       for (int h = 0; h < NKB; ++h) {
@@ -249,6 +243,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int j = 0; j < CH; ++j) {
                 ld_shared_v4f(rb + ((((uint32_t)(2 * j)) ^ sw) << 4), v[t][j][0]);
                 ld_shared_v4f(rb + ((((uint32_t)(2 * j + 1)) ^ sw) << 4), v[t][j][1]);
+                gt.add(v[t][j][0]);
+                gt.add(v[t][j][1]);
               }
             }
           }
@@ -261,6 +257,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int j = 0; j < CH; ++j) {
                 uint32_t hi[4], lo[4];
                 split8x2(v[t][j][0], v[t][j][1], hi, lo);
+                gt.add_hi(hi);  // range guard: fp16 overflow shows as an inf hi half
                 const uint32_t dst = sbase + (uint32_t)j * 2 * COL + (uint32_t)r * 16;
                 st_shared_v4(dst, hi[0], hi[1], hi[2], hi[3]);
                 st_shared_v4(dst + COL, lo[0], lo[1], lo[2], lo[3]);
@@ -277,6 +274,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
+    if (gt.bad()) guard_bad = 1;
   } else if (warp == 12) {
     // ===== MMA issuer (the whole warp runs the loop; one elected lane issues)
     {
@@ -383,6 +381,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     const bool f_ok = f < p.cout;
     const float bias = (f_ok && (p.epi & SEGCONV_EPI_BIAS)) ? __ldg(p.bias + f) : 0.0f;
+    const float wsc = guard_inv_scale(p.fb.guard);  // the weight image holds w * 2^s
     YT* __restrict__ y = reinterpret_cast<YT*>(p.y);
     const int img = p.n * p.n;
     const int qrows = p.rows[q], qcols = p.cols[q];
@@ -413,7 +412,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           const bool st_ok = f_ok && !(p.debug & 1);
 #pragma unroll
           for (int t = 0; t < 32; ++t)
-            st_global_pred(y + (long long)po[t] * p.cout + f, finish<ACT>(v[t], bias),
+            st_global_pred(y + (long long)po[t] * p.cout + f, finish<ACT>(v[t] * wsc, bias),
                            st_ok && po[t] >= 0);
         }
       }
@@ -429,7 +428,6 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (p.cluster > 1) cluster_sync();  // no CTA leaves while a peer's multicast may target it
   if (threadIdx.x == 0) {
     trace_ev(p, 11, 0);  // all roles done
     if (p.trace && blockIdx.x < 160) p.trace[(blockIdx.x * 16 + 13) * 64] = clock64();
@@ -438,6 +436,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
                  : "memory");
+  }
+  if (guard_bad) {
+    // x left the split-fp16 range in this CTA's halo: recompute its anchors
+    // [s16 * 16, e16 * 16) with FFMA (this CTA wrote them; the barrier above
+    // orders the rewrite)
+    const long long g16 = (p.Mv + 15) / 16;
+    const long long a0 = g16 * blockIdx.x / gridDim.x * 16;
+    const long long a1 = min(p.Mv, g16 * (blockIdx.x + 1) / gridDim.x * 16);
+    const int img = p.n * p.n;
+    guard_fallback(p.fb, a1 - a0, 0, p.cout, [&](long long idx, int& b, int& i, int& j) {
+      const long long m = a0 + idx;
+      b = (int)(m / img);
+      const int rem = (int)(m - (long long)b * img);
+      i = rem / p.n;
+      j = rem - i * p.n;
+      return true;
+    });
   }
 }
 
@@ -481,7 +496,8 @@ size_t fold_ts_image_bytes(int cin, int nblk) { return (size_t)2 * (cin / 8) * n
 // Compact image: [plane hi/lo][k-chunk][block (shift, class)][32 rows f][8 fp16].
 __global__ void fold_ts_image_kernel(const float* __restrict__ k, int kw, int cin, int cout,
                                      SegClasses cls, int ur, int uc, uint16_t* __restrict__ out,
-                                     long long total) {
+                                     long long total, const SplitGuard* __restrict__ guard) {
+  const float wscale = ldexpf(1.0f, split_scale_exp(guard->amax_bits));
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const int f = (int)(e % 32);
@@ -516,7 +532,7 @@ __global__ void fold_ts_image_kernel(const float* __restrict__ k, int kw, int ci
       const int ci = J * 8 + x;
       float w = 0.0f;
       if (f < cout)
-        w = k[(((long long)(cls.u0[qq] + 2 * uu) * kw + (cls.v0[qq] + 2 * vv)) * cin + ci) * cout + f];
+        w = wscale * k[(((long long)(cls.u0[qq] + 2 * uu) * kw + (cls.v0[qq] + 2 * vv)) * cin + ci) * cout + f];
       const __half h = __float2half_rn(w);
       hi[x] = __half_as_ushort(h);
       lo[x] = __half_as_ushort(__float2half_rn(w - __half2float(h)));
@@ -530,15 +546,16 @@ __global__ void fold_ts_image_kernel(const float* __restrict__ k, int kw, int ci
 }
 
 cudaError_t launch_fold_ts_image(const void* k, int k_dtype, int kh, int kw, int cin, int cout,
-                                 int p_orig, const SegClasses& cls, void* out, cudaStream_t s) {
-  if (k_dtype != SEGCONV_F32) return cudaErrorNotSupported;
+                                 int p_orig, const SegClasses& cls, void* out, const void* guard,
+                                 cudaStream_t s) {
+  if (k_dtype != SEGCONV_F32 || !guard) return cudaErrorNotSupported;
   int ur, uc;
   fold_window(kh, kw, p_orig, &ur, &uc);
   const int nb = fold_ts_blocks(cls, ur, uc, nullptr);
   const long long total = (long long)(cin / 8) * nb * 32;
   const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 1024);
   fold_ts_image_kernel<<<blocks, 256, 0, s>>>((const float*)k, kw, cin, cout, cls, ur, uc,
-                                               (uint16_t*)out, total);
+                                               (uint16_t*)out, total, (const SplitGuard*)guard);
   note_launch();
   return cudaGetLastError();
 }
@@ -615,8 +632,7 @@ static bool make_fold_ts_params(const FusedProblem& pr, tcfs::Params& p) {
 }
 
 bool tc_fold_ts_supported(const FusedProblem& pr, int math) {
-  if (math != SEGCONV_MATH_F16X3 || pr.panel_layout != SEGCONV_PANEL_UMMA_FOLD) return false;
-  if (getenv("SEGCONV_NO_FOLD_TS")) return false;
+  if (math != SEGCONV_MATH_F16X3 || pr.panel_layout != SEGCONV_PANEL_UMMA_FOLD || !pr.guard) return false;
   tcfs::Params p;
   return make_fold_ts_params(pr, p) && encode_fn_ts() != nullptr;
 }
@@ -636,44 +652,7 @@ static cudaError_t launch_fold_ts_t(const tcfs::Params& prm, const CUtensorMap& 
   const long long units = (prm.Mv + 127) / 128;
   long long grid = std::min<long long>(units, sms);
   const size_t smem = (size_t)tcfs::STAGES * prm.stage_bytes + (3 * tcfs::STAGES + 6) * 8 + 16;
-  tcfs::Params pc = prm;
-  static const char* cl_env = getenv("SEGCONV_FOLD_TS_CLUSTER");
-  pc.cluster = cl_env ? atoi(cl_env) : 1;  // measured: 2- and 4-CTA clusters of this
-                                            // 205 KB-SMEM kernel do not all fit at once
-  if (pc.cluster != 1 && pc.cluster != 2 && pc.cluster != 4) pc.cluster = 1;
-  while (pc.cluster > 1 && ((uint32_t)prm.w_img_bytes % (16u * pc.cluster) != 0 || grid < pc.cluster))
-    pc.cluster /= 2;
-  if (pc.cluster > 1) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.blockDim = dim3(tcfs::NUM_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = (unsigned)pc.cluster;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    // whole clusters, and no more than can be co-resident (GPCs with an odd
-    // number of free SMs would otherwise push a cluster into a second wave);
-    // the anchor ranges are re-split over the grid
-    cfg.gridDim = dim3((unsigned)(grid / pc.cluster * pc.cluster));
-    int max_clusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&max_clusters, (void*)kern, &cfg) == cudaSuccess && max_clusters > 0)
-      grid = std::min<long long>(grid / pc.cluster, max_clusters) * pc.cluster;
-    else
-      grid = grid / pc.cluster * pc.cluster;
-    cfg.gridDim = dim3((unsigned)grid);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, pc, tmap);
-    if (e == cudaSuccess) {
-      note_launch();
-      return cudaSuccess;
-    }
-    cudaGetLastError();  // cluster launch refused: plain launch below
-    pc.cluster = 1;
-    grid = std::min<long long>(units, sms);
-  }
+  const tcfs::Params& pc = prm;
   kern<<<(unsigned)grid, tcfs::NUM_THREADS, smem, s>>>(pc, tmap);
   note_launch();
   return cudaGetLastError();
@@ -683,6 +662,7 @@ cudaError_t launch_tc_fold_ts(const FusedProblem& pr, const void* img, cudaStrea
   tcfs::Params p;
   if (!make_fold_ts_params(pr, p)) return cudaErrorNotSupported;
   p.panels = (const uint8_t*)img;  // the compact image appended to the folded panels
+  p.fb = make_fallback_args(pr, pr.guard);
   if (p.Mv == 0) return cudaSuccess;
   EncodeTiledFnTS fn = encode_fn_ts();
   if (!fn) return cudaErrorNotSupported;

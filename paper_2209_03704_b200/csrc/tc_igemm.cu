@@ -50,6 +50,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_ptx.cuh"
+#include "tc_guard.cuh"
 
 namespace segconv_b200 {
 namespace tc {
@@ -86,6 +87,7 @@ struct Params {
   int first_tap[4];
   int rows[4], cols[4];
   unsigned long long* trace;  // optional event trace (SEGCONV_TC_TRACE), CTAs 0..3
+  FallbackArgs fb;            // split-fp16 range guard (tc_guard.cuh)
 };
 
 // Debug trace: trace[(cta * 8 + event) * 64 + local_unit] = globaltimer (ns).
@@ -127,8 +129,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* acc_full = b_empty + NB;
   uint64_t* acc_empty = acc_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  // a converter saw x outside the split's range (the word after the TMEM slot)
+  volatile int& guard_bad = *reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) guard_bad = 0;
   // a_full arrivals: the TMA itself (bf16), or the 128 converter/gather threads.
   const uint32_t a_full_count = (p.tma_mode && MODE == MODE_BF16) ? 1u : 128u;
   if (warp == 8 && lane == 0) {
@@ -202,6 +207,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int pt = threadIdx.x - 128;
     int st = 0;
     uint32_t ph = 0;
+    GuardTrack gt;
+    gt.init(p.fb.guard);
     if (p.tma_mode) {
       if constexpr (MODE == MODE_F16X3) {
         // ======================= converter: fp32 chunk column j (32-byte rows)
@@ -221,6 +228,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 if (s < p.S) {
                   ld_shared_v4f(cbase + (uint32_t)s * 32, v[k][0]);
                   ld_shared_v4f(cbase + (uint32_t)s * 32 + 16, v[k][1]);
+                  gt.add(v[k][0]);
+                  gt.add(v[k][1]);
                 }
               }
               named_bar(1, 128);
@@ -278,6 +287,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 const float4* xp = reinterpret_cast<const float4*>((const float*)p.x + src);
                 v0 = __ldg(xp);
                 v1 = __ldg(xp + 1);
+                gt.add(v0);
+                gt.add(v1);
               }
               uint32_t hi[4], lo[4];
               split8(v0, v1, hi, lo);
@@ -299,6 +310,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
+    if (gt.bad()) guard_bad = 1;
   } else if (warp == 9) {
     // =========================== B loader: weight blocks by bulk copy
     if (lane == 0) {
@@ -413,6 +425,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t pacc = 0;
     const long long img = (long long)p.VH * p.VW;
     constexpr int CW = NT >= 32 ? 32 : NT;
+    const float wsc = MODE == MODE_F16X3 ? guard_inv_scale(p.fb.guard) : 1.0f;  // images hold w * 2^s
+    float chk = 0.0f;  // range guard: NaN once a stored sum is not finite
     for (long long u = blockIdx.x; u < p.total_units; u += gridDim.x) {
       long long mg;
       int nt;
@@ -444,8 +458,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const int f0 = nt * NT + c0;
             const bool full = f0 + CW <= p.cout;
 #pragma unroll
-            for (int k = 0; k < CW; ++k)
-              v[k] = epilogue_apply(v[k], p.epi, p.bias, min(f0 + k, p.cout - 1));
+            for (int k = 0; k < CW; ++k) {
+              if (f0 + k < p.cout) guard_check(chk, v[k]);
+              v[k] = epilogue_apply(v[k] * wsc, p.epi, p.bias, min(f0 + k, p.cout - 1));
+            }
             if (full && p.y_dtype == SEGCONV_F32 && (p.cout & 3) == 0) {
               float4* dst = reinterpret_cast<float4*>((float*)p.y + pix * p.cout + f0);
 #pragma unroll
@@ -480,6 +496,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         pacc ^= 1;
       }
     }
+    if (MODE == MODE_F16X3 && guard_check_bad(chk)) guard_bad = 1;
   }
 
   tc_fence_before();
@@ -489,6 +506,27 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "n"(TMEM_COLS)
                  : "memory");
+  }
+  if (MODE == MODE_F16X3 && guard_bad) {
+    // x left the split-fp16 range in this CTA's halos: recompute its units
+    // (anchors x feature tile) with FFMA; this CTA wrote them
+    const long long img = (long long)p.VH * p.VW;
+    for (long long u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+      long long mg;
+      int nt;
+      unit_coords(p, u, mg, nt);
+      const long long m0 = mg * MPG;
+      guard_fallback(p.fb, MPG, nt * NT, min(p.cout, (nt + 1) * NT),
+                     [&](long long idx, int& b, int& i, int& j) {
+                       const long long m = m0 + idx;
+                       if (m >= p.Mv) return false;
+                       b = (int)(m / img);
+                       const int rem = (int)(m - (long long)b * img);
+                       i = rem / p.VW;
+                       j = rem - i * p.VW;
+                       return true;
+                     });
+    }
   }
 }
 
@@ -587,6 +625,8 @@ static Plan make_plan_g(const FusedProblem& pr, int math, int G) {
   p.y_dtype = pr.y_dtype;
   p.bias = pr.bias;
   p.epi = pr.epi;
+  p.fb = make_fallback_args(pr, mode == tc::MODE_F16X3 ? pr.guard : nullptr);
+  if (mode == tc::MODE_F16X3 && !pr.guard) return pl;
   int t = 0, max_shift = 0;
   for (int q = 0; q < 4; ++q) {
     p.first_tap[q] = t;

@@ -40,6 +40,7 @@
 #include "kernels.h"
 #include "tc_ptx.cuh"
 #include "tc_scatter.cuh"
+#include "tc_guard.cuh"
 
 namespace segconv_b200 {
 namespace tcr {
@@ -67,6 +68,7 @@ struct Params {
   int stage_bytes, stages, w_bytes;
   unsigned long long* trace;
   int debug;
+  FallbackArgs fb;  // range guard (tc_guard.cuh): weight scale, FFMA fallback
 };
 
 __device__ __forceinline__ void trace_ev(const Params& p, int ev, int local) {
@@ -123,8 +125,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* acc_empty = acc_full + 2;
   uint64_t* w_full = acc_empty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_full + 1);
+  // a converter saw x outside the split's range (the word after the TMEM slot)
+  volatile int& guard_bad = *reinterpret_cast<volatile int*>(tmem_slot + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) guard_bad = 0;
   if (warp == 12 && lane == 0) {
     for (int s = 0; s < SA; ++s) {
       mbar_init(&a_land[s], 1);
@@ -189,6 +194,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     uint32_t ph = 0;
     int b, R, a;
     bool s0;
+    GuardTrack gt;
+    gt.init(p.fb.guard);
     for (int k = 0; unit_at<U>(p, k, b, R, a, s0); ++k) {
       for (int h = 0; h < NH; ++h) {
         mbar_wait(&a_land[st], ph);
@@ -204,6 +211,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int j = 0; j < CH; ++j) {
                 ld_shared_v4f(rb + ((((uint32_t)(2 * j)) ^ sw) << 4), v[t][j][0]);
                 ld_shared_v4f(rb + ((((uint32_t)(2 * j + 1)) ^ sw) << 4), v[t][j][1]);
+                gt.add(v[t][j][0]);
+                gt.add(v[t][j][1]);
               }
             }
           }
@@ -232,6 +241,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
+    if (gt.bad()) guard_bad = 1;
   } else if (warp == 12) {
     // ===== MMA issuer (whole warp in the loop; one elected lane issues)
     const uint32_t tb = __shfl_sync(0xffffffffu, tmem_base, 0);
@@ -300,6 +310,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     float bias[COUT];
 #pragma unroll
     for (int f = 0; f < COUT; ++f) bias[f] = (p.epi & SEGCONV_EPI_BIAS) ? __ldg(p.bias + f) : 0.0f;
+    const float wsc = guard_inv_scale(p.fb.guard);  // the weight image holds w * 2^s
+    float chk = 0.0f;  // range guard: NaN once a stored sum is not finite
     float* y = reinterpret_cast<float*>(p.y);
     float* xw = xchg + warp * (2 * 33);          // this warp's exchange rows (lanes 0, 1)
     const float* xn = xchg + (warp + 1) * (2 * 33);  // next warp's
@@ -372,7 +384,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             float* o = y + (row0 + 2 * j + c) * COUT;
 #pragma unroll
             for (int f = 0; f < COUT; ++f) {
-              float x = ring[0][q][f] + bias[f];
+              guard_check(chk, ring[0][q][f]);
+              float x = ring[0][q][f] * wsc + bias[f];
               if (ACT == 1) x = fmaxf(x, 0.0f);
               if (ACT == 2) x = tanhf(x);
               o[f] = x;
@@ -392,6 +405,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 #pragma unroll
         for (int f = 0; f < COUT; ++f) ring[U - 1][q][f] = 0.0f;
     }
+    if (guard_check_bad(chk)) guard_bad = 1;
   }
 
   tc_fence_before();
@@ -400,6 +414,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
                  : "memory");
+  }
+  if (guard_bad) {
+    // x left the split-fp16 range in this CTA's rows: recompute its anchor
+    // rows [g0, g1) x all columns with FFMA (this CTA wrote them)
+    const long long g0 = p.g_total * blockIdx.x / gridDim.x;
+    const long long g1 = p.g_total * (blockIdx.x + 1) / gridDim.x;
+    guard_fallback(p.fb, (g1 - g0) * p.n, 0, p.cout, [&](long long idx, int& b, int& i, int& j) {
+      const long long g = g0 + idx / p.n;
+      j = (int)(idx - (idx / p.n) * p.n);
+      b = (int)(g / p.rm);
+      i = (int)(g - (long long)b * p.rm);
+      return true;
+    });
   }
 }
 
@@ -410,8 +437,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 // of Layout<KH, COUT>, K-major no-swizzle: [plane hi/lo][k-chunk][N rows][8 fp16].
 template <int KH, int COUT>
 static __global__ void ring_image_kernel(const float* __restrict__ k, int cin, SegClasses cls,
-                                         uint16_t* __restrict__ out) {
+                                         uint16_t* __restrict__ out, const SplitGuard* __restrict__ guard) {
   using L = tcr::Layout<KH, COUT>;
+  const float wscale = ldexpf(1.0f, split_scale_exp(guard->amax_bits));
   const int CHT = cin / 8;
   const long long total = (long long)CHT * L::N;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -437,7 +465,7 @@ static __global__ void ring_image_kernel(const float* __restrict__ k, int cin, S
       if (qq >= 0) {
         const int u = dy - cls.off_r[qq], v = dxx - cls.off_c[qq];
         const int ci = chunk * 8 + x;
-        w = k[(((long long)(cls.u0[qq] + 2 * u) * KH + (cls.v0[qq] + 2 * v)) * cin + ci) * COUT + ff];
+        w = wscale * k[(((long long)(cls.u0[qq] + 2 * u) * KH + (cls.v0[qq] + 2 * v)) * cin + ci) * COUT + ff];
       }
       const __half h = __float2half_rn(w);
       hi[x] = __half_as_ushort(h);
@@ -464,7 +492,7 @@ static bool ring_shape(const FusedProblem& pr) {
 size_t ring_image_bytes(int cin) { return (size_t)2 * (cin / 8) * tcr::Layout<5, 3>::N * 16; }
 
 bool tc_ring_supported(const FusedProblem& pr, int math) {
-  if (math != SEGCONV_MATH_F16X3 || getenv("SEGCONV_NO_RING")) return false;
+  if (math != SEGCONV_MATH_F16X3 || !pr.guard) return false;
   return ring_shape(pr);
 }
 
@@ -497,6 +525,7 @@ cudaError_t launch_tc_ring(const FusedProblem& pr, const void* ring_img, cudaStr
   static const int dbg = getenv("SEGCONV_TC_DEBUG") ? atoi(getenv("SEGCONV_TC_DEBUG")) : 0;
   p.debug = dbg;
   p.trace = tc_trace_buffer();
+  p.fb = make_fallback_args(pr, pr.guard);
   // halo-free input view: (cin, batch * n * n) fp32, box {32 ch, n pixels}, 128B swizzle
   typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
@@ -546,11 +575,12 @@ cudaError_t launch_tc_ring(const FusedProblem& pr, const void* ring_img, cudaStr
 }
 
 cudaError_t launch_ring_image(const void* k, int k_dtype, int cin, const SegClasses& cls,
-                              void* out, cudaStream_t s) {
-  if (k_dtype != SEGCONV_F32) return cudaErrorNotSupported;
+                              void* out, const void* guard, cudaStream_t s) {
+  if (k_dtype != SEGCONV_F32 || !guard) return cudaErrorNotSupported;
   const long long total = (long long)(cin / 8) * tcr::Layout<5, 3>::N;
   const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 1024);
-  ring_image_kernel<5, 3><<<blocks, 256, 0, s>>>((const float*)k, cin, cls, (uint16_t*)out);
+  ring_image_kernel<5, 3><<<blocks, 256, 0, s>>>((const float*)k, cin, cls, (uint16_t*)out,
+                                                 (const SplitGuard*)guard);
   note_launch();
   return cudaGetLastError();
 }

@@ -43,6 +43,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_ptx.cuh"
+#include "tc_guard.cuh"
 
 namespace segconv_b200 {
 namespace tcw {
@@ -1656,14 +1657,31 @@ static cudaError_t launch_wide_t(const tcw::Params& prm, const tcw::Maps& maps, 
 }
 
 namespace tcw {
-// fp32 x -> fp16 [hi | lo] channel halves (x = hi + lo to ~22 bits)
-__global__ void split_x_kernel(const float* __restrict__ x, __half* __restrict__ xs, long long npix, int cin) {
+// fp32 x -> fp16 [hi | lo] channel halves, x * 2^t = hi + lo to ~22 bits.
+// fp16 has a 5-bit exponent: a power of two t puts max |x * 2^t| at 2^14, so
+// no finite input overflows and the split's subnormal floor (2^-25) sits 39
+// binades below the largest activation (range guard, tc_guard.cuh).  The sums
+// are of (x 2^t)(w 2^s): inv_out = 2^-s * 2^-t, applied in the epilogue.
+__global__ void x_amax_kernel(const float* __restrict__ x, long long n, unsigned* __restrict__ amax_bits) {
+  float m = 0.0f;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
+    m = fmaxf(m, fabsf(__ldg(x + e)));
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(amax_bits, __float_as_uint(m));
+}
+
+__global__ void split_x_kernel(const float* __restrict__ x, __half* __restrict__ xs, long long npix, int cin,
+                               const unsigned* __restrict__ amax_bits, const float* __restrict__ w_inv,
+                               float* __restrict__ inv_out) {
+  const int t = split_scale_exp(*amax_bits);
+  const float scale = ldexpf(1.0f, t);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *inv_out = *w_inv * ldexpf(1.0f, -t);
   const long long total = npix * cin;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
     const long long pix = e / cin;
     const int ch = (int)(e - pix * cin);
-    const float v = x[e];
+    const float v = x[e] * scale;
     const __half hi = __float2half_rn(v);
     xs[pix * 2 * cin + ch] = hi;
     xs[pix * 2 * cin + cin + ch] = __float2half_rn(v - __half2float(hi));
@@ -1678,17 +1696,25 @@ cudaError_t launch_tc_wide(const FusedProblem& pr, cudaStream_t s) {
     const long long npix = (long long)pr.batch * pr.n * pr.n;
     if (npix == 0) return cudaSuccess;
     void* xs = nullptr;
-    cudaError_t e = workspace_alloc(&xs, (size_t)npix * 2 * pr.cin * 2, s);
+    const size_t xs_bytes = ((size_t)npix * 2 * pr.cin * 2 + 15) / 16 * 16;
+    cudaError_t e = workspace_alloc(&xs, xs_bytes + 16, s);
     if (e != cudaSuccess) return e;
+    // after the halves: [max |x| bits][2^-s 2^-t]
+    unsigned* xtail = reinterpret_cast<unsigned*>(static_cast<char*>(xs) + xs_bytes);
     const long long total = npix * pr.cin;
-    tcw::split_x_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 148LL * 16), 256, 0, s>>>(
-        (const float*)pr.x, (__half*)xs, npix, pr.cin);
-    e = cudaGetLastError();
+    const bool ok = make_wide(pr, p, maps, xs);
+    e = ok ? cudaMemsetAsync(xtail, 0, 4, s) : cudaErrorNotSupported;
     if (e == cudaSuccess) {
-      note_launch();
-      if (!make_wide(pr, p, maps, xs)) {
-        e = cudaErrorNotSupported;
-      } else {
+      const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 148LL * 16);
+      tcw::x_amax_kernel<<<std::min(blocks, 148u * 8), 256, 0, s>>>((const float*)pr.x, total, xtail);
+      tcw::split_x_kernel<<<blocks, 256, 0, s>>>((const float*)pr.x, (__half*)xs, npix, pr.cin, xtail,
+                                                  p.split_inv_scale, reinterpret_cast<float*>(xtail + 1));
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) {
+      note_launch(2);
+      p.split_inv_scale = reinterpret_cast<const float*>(xtail + 1);
+      {
         p.trace = tc_trace_buffer();
         const int act = (pr.epi & SEGCONV_EPI_RELU) ? 1 : (pr.epi & SEGCONV_EPI_TANH) ? 2 : 0;
         if (pr.y_dtype == SEGCONV_BF16)

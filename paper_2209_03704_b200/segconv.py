@@ -220,6 +220,9 @@ class SubKernelSet:
             flat = self.panels[d.sub_offset[q]: d.sub_offset[q] + n]
             return flat.view(d.cout_pad, kh, kw, d.cin).permute(1, 2, 3, 0)[..., : d.cout]
         planes = 2 if d.dtype == A.F16_SPLIT else 1
+        # split-fp16 images hold w * 2^s; the range-guard header after the
+        # images stores 2^-s (csrc/tc_guard.cuh)
+        inv = self._guard_inv_scale() if d.dtype == A.F16_SPLIT else 1.0
         if d.layout == A.PANEL_UMMA_FOLD:
             # [plane][k_block][chunk][shift*4*cp + q*cp + f][8] over the union window
             CP, KB = d.n_tile, d.k_block
@@ -227,8 +230,9 @@ class SubKernelSet:
             uc = max(d.off_c[i] + d.sub_kw[i] for i in range(4))
             ur = max(d.off_r[i] + d.sub_kh[i] for i in range(4))
             rows = ur * uc * 4 * CP + (128 - 4 * CP)
-            blk = self.panels.view(planes, nkb, KB // 8, rows, 8).float()
-            w = blk[0] + (blk[1] if planes == 2 else 0)          # (nkb, CH, rows, 8)
+            n_img = planes * nkb * (KB // 8) * rows * 8
+            blk = self.panels[:n_img].view(planes, nkb, KB // 8, rows, 8).float()
+            w = (blk[0] + (blk[1] if planes == 2 else 0)) * inv  # (nkb, CH, rows, 8)
             w = w.permute(2, 0, 1, 3).reshape(rows, nkb * KB)     # (rows, cin_pad)
             out = torch.zeros(kh, kw, d.cin, d.cout, device=w.device)
             for u in range(kh):
@@ -242,12 +246,20 @@ class SubKernelSet:
         nkb = (d.cin + KB - 1) // KB
         ntl = d.cout_pad // NT
         taps = sum(d.sub_kh[i] * d.sub_kw[i] for i in range(4))
-        blk = self.panels.view(ntl, nkb, taps, planes, KB // 8, NT, 8).float()
-        w = blk[:, :, :, 0] + (blk[:, :, :, 1] if planes == 2 else 0)
+        n_img = ntl * nkb * taps * planes * (KB // 8) * NT * 8
+        blk = self.panels[:n_img].view(ntl, nkb, taps, planes, KB // 8, NT, 8).float()
+        w = (blk[:, :, :, 0] + (blk[:, :, :, 1] if planes == 2 else 0)) * inv
         # -> (tap, kb, chunk, e, nt, n) -> (tap, cin_pad, cout_pad)
         w = w.permute(2, 1, 3, 5, 0, 4).reshape(taps, nkb * KB, ntl * NT)
         t0 = int(d.sub_offset[q])
         return w[t0: t0 + kh * kw, : d.cin, : d.cout].reshape(kh, kw, d.cin, d.cout)
+
+    def _guard_inv_scale(self) -> float:
+        d = self.desc
+        if d.layout not in (A.PANEL_UMMA_FOLD, A.PANEL_UMMA):
+            return 1.0
+        off = d.total_elems - (16 + d.source_kh * d.source_kw * d.cin * d.cout * 4) // 2
+        return float(self.panels[off: off + 2].view(torch.float32)[0])
 
     @property
     def subs(self):
