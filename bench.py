@@ -740,11 +740,15 @@ def main():
     ap.add_argument("--no-e2e", action="store_true",
                     help="diagnostics (ncu launch lists): skip the host-buffer e2e leg")
     ap.add_argument("--no-parity", action="store_true", help="skip the sampled oracle check")
+    ap.add_argument("--batch", type=int, default=None,
+                    help="diagnostics: override the config's batch (not a headline line)")
     ap.add_argument("--plumbing-check", action="store_true",
                     help="CPU (gloo) check of the multi-rank launch/shard/gather plumbing; no compute")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
+    if args.batch is not None:
+        cfg = dict(cfg, batch=args.batch, desc=cfg["desc"] + f" [batch overridden: {args.batch}]")
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         self_launch(args)
