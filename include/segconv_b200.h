@@ -42,8 +42,9 @@ typedef enum {
   SEGCONV_E_CUDA = 3,        /* CUDA runtime / launch failure, no device, ...         */
   SEGCONV_E_UNSUPPORTED = 4, /* valid request this build has no kernel for            */
   SEGCONV_E_IO = 5,          /* == segconv::IoError       (reference errors.hpp:34-37) */
-  SEGCONV_E_PARSE = 6        /* == segconv::ParseError    (reference errors.hpp:25-31); */
+  SEGCONV_E_PARSE = 6,       /* == segconv::ParseError    (reference errors.hpp:25-31); */
                              /*    segconv_last_error_offset() = its byte_offset        */
+  SEGCONV_E_NCCL = 7         /* NCCL missing or a collective failed (multi-GPU stack)   */
 } segconv_status;
 
 /* Element types.  The reference supports float and double (tensor.hpp:65,154);
@@ -268,6 +269,64 @@ segconv_status segconv_transpose_conv_naive(const void* d_x, segconv_dtype dtype
                                             int kw, int cout, int p_orig, void* d_workspace,
                                             size_t workspace_bytes, const float* d_bias,
                                             unsigned epilogue, void* d_y, void* stream);
+
+/* ------------------------------------------------- multi-GPU layer stack */
+/* Batch-sharded driver for a chain of segregated layers (BASELINE C5: a GAN
+ * generator).  The reference has no parallelism across images -- its only
+ * threading is cout slices inside one image (fused_tconv.hpp:101-147) -- and
+ * no layer chain; this is the "segconv_stack_run" of SURVEY.md 8(b)/(e).
+ *
+ * One process drives `n_gpus` devices (0..n_gpus-1; 0 = every visible one),
+ * one stream each.  At creation the host weights go to GPU 0 and are
+ * ncclBroadcast to the others once, then each GPU segregates its replica.
+ * A forward call gives GPU g the contiguous image slice
+ * [g B / G + min(g, B % G), ...) (balanced, remainder first), copies its shard
+ * host->device in up to 4 slices on a copy stream while the chain runs on the
+ * slices already landed (no data-path collective; ReLU / tanh / bias fused per
+ * layer), ncclAllGather-s the output shards so every GPU holds the
+ * full batch, and copies GPU 0's copy to h_y.  NCCL (libnccl.so.2) is loaded
+ * on first use; without it a multi-GPU handle fails with SEGCONV_E_NCCL (a
+ * single-GPU one needs no collective). */
+typedef struct {
+  int n_in, cin, cout, kh, kw, p_orig; /* input n_in x n_in x cin, kernel kh x kw, padding */
+  const void* h_kernel;                /* host (kh, kw, cin, cout) of kernel_dtype            */
+  segconv_dtype kernel_dtype;          /* F32 / F64 / BF16                                     */
+  const float* h_bias;                 /* host cout floats, or NULL                            */
+  unsigned epilogue;                   /* SEGCONV_EPI_* (BIAS needs h_bias)                   */
+  segconv_math math;                   /* per-layer math (AUTO: from the activation dtype)     */
+} segconv_layer;
+
+typedef struct {
+  int n_gpus;
+  double h2d_ms;      /* max over GPUs: shard host->device copy (all slices)          */
+  double compute_ms;  /* max over GPUs: first slice landed -> last layer done (device */
+                      /* time; overlaps the upload of the later slices)               */
+  double gather_ms;   /* max over GPUs: ncclAllGather of the output shards            */
+  double d2h_ms;      /* GPU 0: full output device->host                              */
+  double total_ms;    /* host wall time of the call                                   */
+} segconv_timing;
+
+typedef struct segconv_stack segconv_stack;
+
+/* Validates the chain (each layer's tconv_geometry output and cout feed the
+ * next layer: ShapeError otherwise), allocates activations for up to
+ * max_batch images, broadcasts and segregates the weights.  dtype is the
+ * activation dtype (F32 or BF16) of every layer. */
+segconv_status segconv_stack_create(const segconv_layer* layers, int n_layers, segconv_dtype dtype,
+                                    int max_batch, int n_gpus, segconv_stack** out);
+/* h_x: (batch, n_in0, n_in0, cin0) host, h_y: (batch, out, out, cout_last)
+ * host, both of dtype (page-locked memory lets the copies run at full speed).
+ * Synchronous.  timing may be NULL. */
+segconv_status segconv_stack_forward(segconv_stack* st, const void* h_x, int batch, void* h_y,
+                                     segconv_timing* timing);
+/* Device pointer of GPU g's full-batch (all-gathered) output of the last forward. */
+const void* segconv_stack_output(const segconv_stack* st, int gpu);
+int segconv_stack_gpus(const segconv_stack* st);
+void segconv_stack_destroy(segconv_stack* st);
+/* create + forward + destroy. */
+segconv_status segconv_stack_run(const segconv_layer* layers, int n_layers, segconv_dtype dtype,
+                                 const void* h_x, int batch, int n_gpus, void* h_y,
+                                 segconv_timing* timing);
 
 /* ------------------------------------------------------------ accounting */
 /* reference analysis.hpp:31-41,48-67: out = {naive mults, naive adds, fused

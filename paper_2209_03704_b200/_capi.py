@@ -13,7 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libsegconv_b200.so")
 
 # segconv_status
-OK, E_SHAPE, E_CONTRACT, E_CUDA, E_UNSUPPORTED, E_IO, E_PARSE = range(7)
+OK, E_SHAPE, E_CONTRACT, E_CUDA, E_UNSUPPORTED, E_IO, E_PARSE, E_NCCL = range(8)
 # segconv_dtype
 F32, F64, BF16, F16_SPLIT = 0, 1, 2, 3
 # segconv_math
@@ -49,6 +49,18 @@ class TensorFileInfo(C.Structure):
                 ("precision", C.c_int)]
 
 
+class Layer(C.Structure):
+    """segconv_layer: one layer of a multi-GPU stack."""
+    _fields_ = [("n_in", C.c_int), ("cin", C.c_int), ("cout", C.c_int), ("kh", C.c_int), ("kw", C.c_int),
+                ("p_orig", C.c_int), ("h_kernel", C.c_void_p), ("kernel_dtype", C.c_int),
+                ("h_bias", C.c_void_p), ("epilogue", C.c_uint), ("math", C.c_int)]
+
+
+class Timing(C.Structure):
+    _fields_ = [("n_gpus", C.c_int), ("h2d_ms", C.c_double), ("compute_ms", C.c_double),
+                ("gather_ms", C.c_double), ("d2h_ms", C.c_double), ("total_ms", C.c_double)]
+
+
 # (name, restype, argtypes) for every symbol include/segconv_b200.h declares.
 _vp, _i, _u, _sz = C.c_void_p, C.c_int, C.c_uint, C.c_size_t
 SIGNATURES = {
@@ -81,6 +93,12 @@ SIGNATURES = {
     "segconv_transpose_conv_naive": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _vp, _sz,
                                           _vp, _u, _vp, _vp]),
     "segconv_count_ops": (_i, [_i, _i, _i, _i, _i, _i, C.POINTER(C.c_uint64)]),
+    "segconv_stack_create": (_i, [C.POINTER(Layer), _i, _i, _i, _i, C.POINTER(_vp)]),
+    "segconv_stack_forward": (_i, [_vp, _vp, _i, _vp, C.POINTER(Timing)]),
+    "segconv_stack_output": (_vp, [_vp, _i]),
+    "segconv_stack_gpus": (_i, [_vp]),
+    "segconv_stack_destroy": (None, [_vp]),
+    "segconv_stack_run": (_i, [C.POINTER(Layer), _i, _i, _vp, _i, _i, _vp, C.POINTER(Timing)]),
     "segconv_last_error": (C.c_char_p, []),
     "segconv_last_path": (C.c_char_p, []),
     "segconv_version": (C.c_char_p, []),

@@ -75,8 +75,12 @@ class UnsupportedError(SegconvError):
     """Valid request with no kernel in this build."""
 
 
+class NcclError(SegconvError):
+    """NCCL missing, or a collective of the multi-GPU stack failed."""
+
+
 _ERR = {A.E_SHAPE: ShapeError, A.E_CONTRACT: ContractError, A.E_CUDA: CudaError,
-        A.E_UNSUPPORTED: UnsupportedError, A.E_IO: IoError}
+        A.E_UNSUPPORTED: UnsupportedError, A.E_IO: IoError, A.E_NCCL: NcclError}
 
 
 def _check(status: int) -> None:

@@ -185,3 +185,70 @@ def gather_shards(local: torch.Tensor, global_batch: int, *, group=None) -> torc
     bufs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(bufs, pad, group=group)
     return torch.cat([b[: h - l] for b, (l, h) in zip(bufs, sizes)], dim=0)
+
+
+class MultiGPUStack:
+    """The C ABI's single-process multi-GPU driver (segconv_stack_*,
+    csrc/stack.cu): one host thread, one stream per GPU, weights
+    ncclBroadcast once at creation, each GPU a contiguous batch shard, the
+    output shards ncclAllGather-ed; host tensors in, host tensor out.
+
+    ``kernels`` are host (kh, kw, cin, cout) tensors; activations are
+    ``act_dtype`` (bfloat16 or float32).  ``forward(x)`` takes a host
+    (B, N, N, cin) tensor (page-locked for full-speed copies) and returns the
+    host output plus the per-phase timing (max over GPUs)."""
+
+    def __init__(self, specs: Sequence[LayerSpec], kernels: Sequence[torch.Tensor], max_batch: int, *,
+                 n_gpus: int = 0, act_dtype=torch.bfloat16, biases=None):
+        import ctypes as C
+        from . import _capi as A
+        if len(specs) != len(kernels) or not specs:
+            raise sc.ContractError("one kernel per layer spec is required")
+        self._A, self._C = A, C
+        self.specs = list(specs)
+        self.act_dtype = act_dtype
+        self._keep = []
+        arr = (A.Layer * len(specs))()
+        for i, (s, k) in enumerate(zip(specs, kernels)):
+            kh = k.detach().to("cpu").contiguous()
+            self._keep.append(kh)
+            b = None
+            if biases is not None and biases[i] is not None:
+                b = biases[i].detach().to("cpu", torch.float32).contiguous()
+                self._keep.append(b)
+            epi = sc._ACT[s.activation] | (A.EPI_BIAS if b is not None else 0)
+            arr[i] = A.Layer(s.n_in, s.cin, s.cout, s.k, s.k, s.p, kh.data_ptr(), sc._DT[kh.dtype],
+                             b.data_ptr() if b is not None else None, epi, A.MATH_AUTO)
+        h = C.c_void_p()
+        sc._check(A.lib().segconv_stack_create(arr, len(specs), sc._DT[act_dtype], int(max_batch), int(n_gpus),
+                                               C.byref(h)))
+        self._h = h
+        self.n_gpus = int(A.lib().segconv_stack_gpus(h))
+        g = sc.tconv_geometry(specs[-1].n_in, specs[-1].k, specs[-1].k, specs[-1].p)
+        self.out_shape = (g.out_h, g.out_w, specs[-1].cout)
+        self.last_timing = None
+
+    def forward(self, x: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        A, C = self._A, self._C
+        s0 = self.specs[0]
+        if x.dim() != 4 or tuple(x.shape[1:]) != (s0.n_in, s0.n_in, s0.cin) or x.dtype != self.act_dtype:
+            raise sc.ContractError(f"stack input must be (B, {s0.n_in}, {s0.n_in}, {s0.cin}) {self.act_dtype}")
+        x = x.contiguous()
+        if out is None:
+            out = torch.empty((x.shape[0],) + self.out_shape, dtype=self.act_dtype)
+        t = A.Timing()
+        sc._check(A.lib().segconv_stack_forward(self._h, x.data_ptr(), int(x.shape[0]), out.data_ptr(),
+                                                C.byref(t)))
+        self.last_timing = {k: getattr(t, k) for k, _ in A.Timing._fields_}
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._A.lib().segconv_stack_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

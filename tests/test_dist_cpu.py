@@ -153,3 +153,15 @@ def test_sharded_backward_gloo_world2(batch):
     np.testing.assert_array_equal(np.concatenate([gx0, gx1]), wx)  # input grads: per shard
     np.testing.assert_array_equal(gk0, gk1)  # every rank holds the all-reduced sum
     np.testing.assert_allclose(gk0, wk, rtol=0, atol=1e-5)  # == the full-batch kernel grad
+
+
+def test_multi_gpu_stack_checks_the_chain_on_the_host():
+    """segconv_stack_create validates the layer chain before touching a device
+    (ShapeError like the reference's geometry checks), so it fails the same way
+    with or without a GPU."""
+    from paper_2209_03704_b200 import segconv as sc
+    from paper_2209_03704_b200 import stack as st
+    specs = [st.LayerSpec(64, 32, 4, 3), st.LayerSpec(31, 16, 5, 3)]  # 5x5x32 does not feed cin 31
+    ks = [torch.zeros((3, 3, 64, 32)), torch.zeros((3, 3, 31, 16))]
+    with pytest.raises(sc.ShapeError, match="does not feed"):
+        st.MultiGPUStack(specs, ks, 4, act_dtype=torch.float32)

@@ -191,3 +191,26 @@ def test_config_c5_stack_batch_1024_graph_pdl():
         assert got.shape == (len(idx), 19, 19, 3)
         assert np.isfinite(got).all()
         assert scaled_err(got, _c5_chain(specs, ks, x[idx])) <= 1e-2, b
+
+
+def test_multi_gpu_stack_c_abi_equals_generator_stack():
+    """The C ABI's multi-GPU driver (segconv_stack_*, host buffers in and out,
+    NCCL broadcast / all-gather when more than one GPU is visible) runs the same
+    kernels as GeneratorStack: identical bits on one GPU, and the timing of each
+    phase is reported."""
+    from paper_2209_03704_b200 import stack as st
+    specs = st.c5_layers()
+    rng = np.random.default_rng(55)
+    ks = [torch.from_numpy(rng.standard_normal((s.k, s.k, s.cin, s.cout), dtype=np.float32) * 0.02)
+          for s in specs]
+    b = 64
+    x = torch.from_numpy(rng.standard_normal((b, 4, 4, 1024), dtype=np.float32)).bfloat16()
+    ref = st.GeneratorStack(specs, [k.cuda() for k in ks], b).forward(x.cuda()).cpu()
+    ms = st.MultiGPUStack(specs, ks, b, n_gpus=1)
+    y = ms.forward(x.pin_memory())
+    assert torch.equal(y, ref)
+    t = ms.last_timing
+    assert t["n_gpus"] == 1 and t["compute_ms"] > 0 and t["h2d_ms"] > 0 and t["d2h_ms"] > 0
+    y7 = ms.forward(x[:7].contiguous())
+    assert torch.equal(y7, ref[:7])
+    ms.close()
