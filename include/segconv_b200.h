@@ -243,11 +243,14 @@ segconv_status segconv_upsample2x_pad_backward(const void* d_gy, segconv_dtype d
                                                int n_in, int cin, int p_orig, void* d_gx,
                                                void* stream);
 /* reference reference_ops.hpp:86-108 (conv2d_valid), batched over `batch`
- * (h, w, cin) maps; output (batch, h-kh+1, w-kw+1, cout). */
+ * (h, w, cin) maps; output (batch, h-kh+1, w-kw+1, cout).  math: AUTO (bf16:
+ * tensor cores; fp32 / fp64: FFMA), FFMA, or EXACT -- the reference's (u, v,
+ * ch) accumulation order without FMA contraction, bit-identical to its CPU
+ * conv2d_valid and hence (zeros added exactly) to transpose_conv_fused EXACT. */
 segconv_status segconv_conv2d_valid(const void* d_src, segconv_dtype dtype, int batch, int h,
                                     int w, int cin, const void* d_kernel, int kh, int kw,
-                                    int cout, const float* d_bias, unsigned epilogue, void* d_y,
-                                    void* stream);
+                                    int cout, const float* d_bias, unsigned epilogue,
+                                    segconv_math math, void* d_y, void* stream);
 /* reference netdemo/layers.hpp:98-122 (net::ConvValid<T>::backward), batched:
  * gradients of conv2d_valid.  d_src (batch, h, w, cin) is the forward input,
  * d_gy (batch, h-kh+1, w-kw+1, cout) the output gradient, d_kernel (kh, kw,
@@ -268,7 +271,8 @@ segconv_status segconv_transpose_conv_naive(const void* d_x, segconv_dtype dtype
                                             int n_in, int cin, const void* d_kernel, int kh,
                                             int kw, int cout, int p_orig, void* d_workspace,
                                             size_t workspace_bytes, const float* d_bias,
-                                            unsigned epilogue, void* d_y, void* stream);
+                                            unsigned epilogue, segconv_math math, void* d_y,
+                                            void* stream);
 
 /* ------------------------------------------------- multi-GPU layer stack */
 /* Batch-sharded driver for a chain of segregated layers (BASELINE C5: a GAN

@@ -13,7 +13,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
+#include <cstdint>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -61,6 +63,46 @@ inline void throw_on(segconv_status st) {
   throw CudaError(msg);
 }
 
+// Arithmetic of the value-semantics operators.  AUTO: the tensor-core kernels
+// where the layer suits them (fp32 data: split-fp16, within 1e-5 of the
+// reference).  Build with -DSEGCONV_B200_DEFAULT_MATH=SEGCONV_MATH_EXACT to get
+// the reference's bit-for-bit results everywhere (its accumulation order, no
+// FMA contraction), e.g. to run the reference's samples unchanged.
+#ifndef SEGCONV_B200_DEFAULT_MATH
+#define SEGCONV_B200_DEFAULT_MATH SEGCONV_MATH_AUTO
+#endif
+
+// ------------------------------------------------------------- allocation accounting
+// reference tensor.hpp:22-55: Tensor / Kernel host storage allocated inside an
+// active AllocScope is tallied into its AllocStats.  The device work of the
+// operators allocates no host tensors, so a fused call records only its output
+// (the reference's also records its padded input copy).
+struct AllocStats {
+  std::size_t total_bytes = 0;
+  std::size_t peak_single = 0;
+  std::size_t allocations = 0;
+  void note(std::size_t bytes) {
+    total_bytes += bytes;
+    peak_single = std::max(peak_single, bytes);
+    ++allocations;
+  }
+};
+
+class AllocScope {
+ public:
+  explicit AllocScope(AllocStats& stats) : prev_(current_) { current_ = &stats; }
+  ~AllocScope() { current_ = prev_; }
+  AllocScope(const AllocScope&) = delete;
+  AllocScope& operator=(const AllocScope&) = delete;
+  static void note(std::size_t bytes) {
+    if (current_ != nullptr) current_->note(bytes);
+  }
+
+ private:
+  AllocStats* prev_;
+  static inline thread_local AllocStats* current_ = nullptr;
+};
+
 template <typename T>
 struct dtype_of;
 template <>
@@ -81,30 +123,63 @@ class Tensor {
  public:
   Tensor() = default;
   Tensor(int h, int w, int c) : h_(h), w_(w), c_(c) {
-    if (h < 1 || w < 1 || c < 1)
-      throw ShapeError("tensor dims must be positive, got " + std::to_string(h) + "x" +
-                       std::to_string(w) + "x" + std::to_string(c));
+    check_dims(h, w, c);
     data_.assign(size(), T(0));
+    AllocScope::note(size() * sizeof(T));
   }
   static Tensor from_data(int h, int w, int c, std::vector<T> values) {
-    Tensor t(h, w, c);
-    if (values.size() != t.size()) throw ContractError("tensor data length does not match dims");
+    check_dims(h, w, c);
+    const std::size_t expect = (std::size_t)h * (std::size_t)w * (std::size_t)c;
+    if (values.size() != expect)
+      throw ContractError("tensor data length " + std::to_string(values.size()) + " does not match dims (" +
+                          std::to_string(h) + "x" + std::to_string(w) + "x" + std::to_string(c) + ")");
     for (const T v : values)
       if (!std::isfinite(v)) throw ContractError("tensor data contains a non-finite element");
+    Tensor t;
+    t.h_ = h;
+    t.w_ = w;
+    t.c_ = c;
     t.data_ = std::move(values);
+    AllocScope::note(t.size() * sizeof(T));
     return t;
   }
+  Tensor(const Tensor& o) : h_(o.h_), w_(o.w_), c_(o.c_), data_(o.data_) {
+    AllocScope::note(data_.size() * sizeof(T));
+  }
+  Tensor& operator=(const Tensor& o) {
+    if (this != &o) {
+      h_ = o.h_;
+      w_ = o.w_;
+      c_ = o.c_;
+      data_ = o.data_;
+      AllocScope::note(data_.size() * sizeof(T));
+    }
+    return *this;
+  }
+  Tensor(Tensor&&) noexcept = default;
+  Tensor& operator=(Tensor&&) noexcept = default;
+
   int height() const { return h_; }
   int width() const { return w_; }
   int channels() const { return c_; }
   size_t size() const { return (size_t)h_ * w_ * c_; }
-  T operator()(int i, int j, int ch) const { return data_[((size_t)i * w_ + j) * c_ + ch]; }
-  T& operator()(int i, int j, int ch) { return data_[((size_t)i * w_ + j) * c_ + ch]; }
+  bool empty() const { return data_.empty(); }
+  size_t index(int i, int j, int ch) const { return ((size_t)i * w_ + j) * c_ + ch; }
+  T operator()(int i, int j, int ch) const { return data_[index(i, j, ch)]; }
+  T& operator()(int i, int j, int ch) { return data_[index(i, j, ch)]; }
+  const T* pixel(int i, int j) const { return data_.data() + index(i, j, 0); }
+  T* pixel(int i, int j) { return data_.data() + index(i, j, 0); }
   const T* data() const { return data_.data(); }
   T* data() { return data_.data(); }
+  const std::vector<T>& storage() const { return data_; }
   bool same_shape(const Tensor& o) const { return h_ == o.h_ && w_ == o.w_ && c_ == o.c_; }
 
  private:
+  static void check_dims(int h, int w, int c) {
+    if (h < 1 || w < 1 || c < 1)
+      throw ShapeError("tensor dims must be positive, got " + std::to_string(h) + "x" + std::to_string(w) + "x" +
+                       std::to_string(c));
+  }
   int h_ = 0, w_ = 0, c_ = 0;
   std::vector<T> data_;
 };
@@ -112,19 +187,31 @@ class Tensor {
 // (kh, kw, cin, cout), cout innermost (reference tensor.hpp:152-217)
 template <typename T>
 class Kernel {
+  static_assert(std::is_floating_point_v<T>, "Kernel requires float or double");
+
  public:
   Kernel() = default;
+  // spatial dims may be zero: segregation produces legal empty sub-kernels
   Kernel(int kh, int kw, int cin, int cout) : kh_(kh), kw_(kw), cin_(cin), cout_(cout) {
-    if (kh < 0 || kw < 0 || cin < 1 || cout < 1) throw ShapeError("bad kernel dims");
+    if (kh < 0 || kw < 0 || cin < 1 || cout < 1) throw ShapeError("bad kernel dims " + dims(kh, kw, cin, cout));
     data_.assign(size(), T(0));
+    AllocScope::note(size() * sizeof(T));
   }
   static Kernel from_data(int kh, int kw, int cin, int cout, std::vector<T> values) {
-    if (kh < 1 || kw < 1 || cin < 1 || cout < 1) throw ShapeError("bad kernel dims");
-    Kernel k(kh, kw, cin, cout);
-    if (values.size() != k.size()) throw ContractError("kernel data length does not match dims");
+    if (kh < 1 || kw < 1 || cin < 1 || cout < 1) throw ShapeError("bad kernel dims " + dims(kh, kw, cin, cout));
+    const std::size_t expect = (std::size_t)kh * kw * cin * cout;
+    if (values.size() != expect)
+      throw ContractError("kernel data length " + std::to_string(values.size()) + " does not match dims " +
+                          dims(kh, kw, cin, cout));
     for (const T v : values)
       if (!std::isfinite(v)) throw ContractError("kernel data contains a non-finite element");
+    Kernel k;
+    k.kh_ = kh;
+    k.kw_ = kw;
+    k.cin_ = cin;
+    k.cout_ = cout;
     k.data_ = std::move(values);
+    AllocScope::note(k.size() * sizeof(T));
     return k;
   }
   int kh() const { return kh_; }
@@ -133,18 +220,49 @@ class Kernel {
   int cout() const { return cout_; }
   size_t size() const { return (size_t)kh_ * kw_ * cin_ * cout_; }
   bool spatially_empty() const { return kh_ == 0 || kw_ == 0; }
-  T operator()(int u, int v, int ch, int f) const {
-    return data_[(((size_t)u * kw_ + v) * cin_ + ch) * cout_ + f];
-  }
-  T& operator()(int u, int v, int ch, int f) {
-    return data_[(((size_t)u * kw_ + v) * cin_ + ch) * cout_ + f];
-  }
+  size_t index(int u, int v, int ch, int f) const { return (((size_t)u * kw_ + v) * cin_ + ch) * cout_ + f; }
+  T operator()(int u, int v, int ch, int f) const { return data_[index(u, v, ch, f)]; }
+  T& operator()(int u, int v, int ch, int f) { return data_[index(u, v, ch, f)]; }
+  // the cout values of tap (u, v, ch)
+  const T* tap(int u, int v, int ch) const { return data_.data() + index(u, v, ch, 0); }
   const T* data() const { return data_.data(); }
   T* data() { return data_.data(); }
 
  private:
+  static std::string dims(int kh, int kw, int cin, int cout) {
+    return std::to_string(kh) + "x" + std::to_string(kw) + "x" + std::to_string(cin) + "x" + std::to_string(cout);
+  }
   int kh_ = 0, kw_ = 0, cin_ = 0, cout_ = 0;
   std::vector<T> data_;
+};
+
+// ------------------------------------------------------------- op counts
+// reference op_counts.hpp:9-41: multiply / add tallies; the counting hooks of
+// the TallyT overloads below.  The device kernels do not count as they go: a
+// TallyT overload adds the analytic totals of the call (the reference's
+// dots(count, len) per output pixel summed over the pixels -- equal totals).
+struct OpCounts {
+  std::uint64_t mults = 0;
+  std::uint64_t adds = 0;
+  OpCounts& operator+=(const OpCounts& o) {
+    mults += o.mults;
+    adds += o.adds;
+    return *this;
+  }
+  friend OpCounts operator+(OpCounts a, const OpCounts& b) { return a += b; }
+  friend bool operator==(const OpCounts& a, const OpCounts& b) { return a.mults == b.mults && a.adds == b.adds; }
+};
+struct NoTally {
+  static constexpr bool counting = false;
+  void dots(std::uint64_t, std::uint64_t) {}
+};
+struct Tally {
+  static constexpr bool counting = true;
+  OpCounts counts;
+  void dots(std::uint64_t count, std::uint64_t len) {
+    counts.mults += count * len;
+    if (len > 0) counts.adds += count * (len - 1);
+  }
 };
 
 // ------------------------------------------------------------- device memory
@@ -236,23 +354,36 @@ inline int active_tap_count(int n, int p, int r) { return segconv_active_tap_cou
 inline int class_input_offset(int p, int r) { return segconv_class_input_offset(p, r); }
 
 // ------------------------------------------------------------- segregation
-// Device counterpart of SubKernelSet<T> (reference segregation.hpp:43-55).
+// reference segregation.hpp:91-101: sub-kernel sizes of an odd n x n kernel,
+// largest class first.
+inline std::array<std::pair<int, int>, 4> sub_kernel_dims(int n) {
+  if (n < 1) throw ContractError("kernel size must be >= 1");
+  if (n % 2 == 0) throw ContractError("sub_kernel_dims is defined for odd sizes only");
+  const int hi = (n + 1) / 2, lo = n / 2;
+  return {{{hi, hi}, {hi, lo}, {lo, hi}, {lo, lo}}};
+}
+
+// reference segregation.hpp:38-55.  `subs` / `class_input_offsets` are the
+// reference's host-visible members (class q = r*2 + c); `desc` + `panels`
+// are the device panels segconv_segregate wrote for the consumer kernel.
 template <typename T>
 struct SubKernelSet {
+  std::array<Kernel<T>, 4> subs;
+  std::array<std::pair<int, int>, 4> class_input_offsets;
+  int source_kh = 0, source_kw = 0, p_orig_parity = 0;
   segconv_subkernels desc{};
   std::shared_ptr<DeviceBuffer> panels;
-  int source_kh = 0, source_kw = 0, p_orig_parity = 0;
+  const Kernel<T>& sub(int r, int c) const { return subs[r * 2 + c]; }
+  std::pair<int, int> offset(int r, int c) const { return class_input_offsets[r * 2 + c]; }
   int cin() const { return desc.cin; }
   int cout() const { return desc.cout; }
-  std::pair<int, int> offset(int r, int c) const {
-    return {desc.off_r[r * 2 + c], desc.off_c[r * 2 + c]};
-  }
 };
 
-// reference segregation.hpp:61-89.  `math` picks the consumer kernel
-// (SEGCONV_MATH_AUTO: tensor cores where the layer suits them).
+// reference segregation.hpp:61-89.  The device panels come from one gather
+// kernel (segconv_segregate); the host `subs` are the same taps,
+// k[u0 + 2u][v0 + 2v][ch][f].  `math` picks the consumer kernel family.
 template <typename T>
-SubKernelSet<T> segregate(const Kernel<T>& k, int p_orig, segconv_math math = SEGCONV_MATH_AUTO) {
+SubKernelSet<T> segregate(const Kernel<T>& k, int p_orig, segconv_math math = SEGCONV_B200_DEFAULT_MATH) {
   if (k.spatially_empty()) throw ContractError("cannot segregate a spatially empty kernel");
   if (p_orig < 0) throw ContractError("padding must be non-negative");
   SubKernelSet<T> s;
@@ -266,26 +397,114 @@ SubKernelSet<T> segregate(const Kernel<T>& k, int p_orig, segconv_math math = SE
   s.source_kh = k.kh();
   s.source_kw = k.kw();
   s.p_orig_parity = p_orig & 1;
+  for (int q = 0; q < 4; ++q) {
+    const int u0 = s.desc.u0[q], v0 = s.desc.v0[q], skh = s.desc.sub_kh[q], skw = s.desc.sub_kw[q];
+    Kernel<T> sub(skh, skw, k.cin(), k.cout());
+    for (int u = 0; u < skh; ++u)
+      for (int v = 0; v < skw; ++v)
+        for (int ch = 0; ch < k.cin(); ++ch)
+          std::memcpy(&sub(u, v, ch, 0), k.tap(u0 + 2 * u, v0 + 2 * v, ch), k.cout() * sizeof(T));
+    s.subs[q] = std::move(sub);
+    s.class_input_offsets[q] = {s.desc.off_r[q], s.desc.off_c[q]};
+  }
   return s;
 }
 
-// ------------------------------------------------------------- operators
-// reference fused_tconv.hpp:69-82
+// ------------------------------------------------------------- tensor ops
+// reference tensor.hpp:224-259.  pad / crop are host copies (the device path
+// never materialises them: the kernels predicate their halo loads);
+// upsample2x runs the conventional path's device kernel (K5).
 template <typename T>
-Tensor<T> transpose_conv_fused(const Tensor<T>& input, const SubKernelSet<T>& sks,
-                               const TConvGeometry& geom) {
+Tensor<T> pad(const Tensor<T>& t, int p) {
+  if (p < 0) throw ContractError("pad factor must be non-negative");
+  Tensor<T> out(t.height() + 2 * p, t.width() + 2 * p, t.channels());
+  const size_t row = (size_t)t.width() * t.channels() * sizeof(T);
+  for (int i = 0; i < t.height(); ++i) std::memcpy(out.pixel(i + p, p), t.pixel(i, 0), row);
+  return out;
+}
+
+template <typename T>
+Tensor<T> crop(const Tensor<T>& t, int top, int left, int h, int w) {
+  if (top < 0 || left < 0 || h < 1 || w < 1 || top + h > t.height() || left + w > t.width())
+    throw ContractError("crop window out of range");
+  Tensor<T> out(h, w, t.channels());
+  const size_t row = (size_t)w * t.channels() * sizeof(T);
+  for (int i = 0; i < h; ++i) std::memcpy(out.pixel(i, 0), t.pixel(top + i, left), row);
+  return out;
+}
+
+template <typename T>
+Tensor<T> upsample2x(const Tensor<T>& t) {
+  Tensor<T> out(2 * t.height() - 1, 2 * t.width() - 1, t.channels());
+  if (t.height() != t.width()) {  // the device kernel takes square maps (the operators' inputs)
+    for (int i = 0; i < t.height(); ++i)
+      for (int j = 0; j < t.width(); ++j)
+        std::memcpy(out.pixel(2 * i, 2 * j), t.pixel(i, j), t.channels() * sizeof(T));
+    return out;
+  }
+  detail::Staged dx(0, t.data(), t.size() * sizeof(T)), dy(1, out.size() * sizeof(T));
+  throw_on(segconv_upsample2x_pad(dx.get(), dtype_of<T>::value, 1, t.height(), t.channels(), 0, dy.get(),
+                                  nullptr));
+  dy.to_host(out.data(), out.size() * sizeof(T));
+  return out;
+}
+
+// ------------------------------------------------------------- operators
+namespace detail {
+// reference fused_tconv.hpp:17-35 (same messages; the C ABI checks again)
+template <typename T>
+void check_fused_args(const Tensor<T>& input, const SubKernelSet<T>& sks, const TConvGeometry& geom) {
   if (input.height() != geom.n_in || input.width() != geom.n_in)
-    throw ContractError("input size does not match the geometry");
+    throw ContractError("input is " + std::to_string(input.height()) + "x" + std::to_string(input.width()) +
+                        " but geometry was built for " + std::to_string(geom.n_in) + "x" +
+                        std::to_string(geom.n_in));
+  if (input.channels() != sks.cin())
+    throw ContractError("channel mismatch: input has " + std::to_string(input.channels()) +
+                        ", sub-kernels expect " + std::to_string(sks.cin()));
+  if (sks.source_kh != geom.kh || sks.source_kw != geom.kw)
+    throw ContractError("sub-kernel set was built from a " + std::to_string(sks.source_kh) + "x" +
+                        std::to_string(sks.source_kw) + " kernel, geometry expects " + std::to_string(geom.kh) +
+                        "x" + std::to_string(geom.kw));
+  if (sks.p_orig_parity != (geom.p_orig & 1))
+    throw ContractError("sub-kernel set was segregated for padding parity " + std::to_string(sks.p_orig_parity) +
+                        ", geometry has p_orig " + std::to_string(geom.p_orig));
+}
+// the math of the conventional operators under SEGCONV_B200_DEFAULT_MATH
+constexpr segconv_math conventional_math() {
+  return SEGCONV_B200_DEFAULT_MATH == SEGCONV_MATH_EXACT || SEGCONV_B200_DEFAULT_MATH == SEGCONV_MATH_FFMA
+             ? SEGCONV_B200_DEFAULT_MATH
+             : SEGCONV_MATH_AUTO;
+}
+}  // namespace detail
+
+// reference fused_tconv.hpp:69-82; the TallyT overload adds the call's
+// multiply / add totals (reference fused_from_padded: dots(cout, taps * cin)
+// per output pixel of each class)
+template <typename T, typename TallyT>
+Tensor<T> transpose_conv_fused(const Tensor<T>& input, const SubKernelSet<T>& sks, const TConvGeometry& geom,
+                               TallyT& tally) {
+  detail::check_fused_args(input, sks, geom);
   Tensor<T> out(geom.out_h, geom.out_w, sks.cout());
   detail::Staged dx(0, input.data(), input.size() * sizeof(T));
   detail::Staged dy(1, out.size() * sizeof(T));
   const segconv_geometry g = geom.c();
-  throw_on(segconv_transpose_conv_fused(dx.get(), dtype_of<T>::value, 1, input.height(),
-                                        input.channels(), &sks.desc, sks.panels->get(), &g,
-                                        nullptr, SEGCONV_EPI_NONE, SEGCONV_MATH_AUTO, dy.get(),
-                                        dtype_of<T>::value, nullptr));
+  throw_on(segconv_transpose_conv_fused(dx.get(), dtype_of<T>::value, 1, input.height(), input.channels(),
+                                        &sks.desc, sks.panels->get(), &g, nullptr, SEGCONV_EPI_NONE,
+                                        SEGCONV_MATH_AUTO, dy.get(), dtype_of<T>::value, nullptr));
   dy.to_host(out.data(), out.size() * sizeof(T));
+  for (int q = 0; q < 4; ++q) {
+    const int r = q >> 1, c = q & 1;
+    const std::uint64_t pixels = (std::uint64_t)((geom.out_h - r + 1) / 2) * ((geom.out_w - c + 1) / 2);
+    tally.dots(pixels * (std::uint64_t)sks.cout(),
+               (std::uint64_t)sks.desc.sub_kh[q] * sks.desc.sub_kw[q] * sks.cin());
+  }
   return out;
+}
+
+template <typename T>
+Tensor<T> transpose_conv_fused(const Tensor<T>& input, const SubKernelSet<T>& sks, const TConvGeometry& geom) {
+  NoTally t;
+  return transpose_conv_fused(input, sks, geom, t);
 }
 
 // reference fused_tconv.hpp:85-92
@@ -293,13 +512,14 @@ template <typename T>
 Tensor<T> transpose_conv_fused(const Tensor<T>& input, const Kernel<T>& k, int p) {
   const TConvGeometry geom = tconv_geometry(input.height(), k.kh(), k.kw(), p);
   if (input.height() != input.width())
-    throw ContractError("transpose conv expects a square input");
+    throw ContractError("transpose conv expects a square input, got " + std::to_string(input.height()) + "x" +
+                        std::to_string(input.width()));
   return transpose_conv_fused(input, segregate(k, p), geom);
 }
 
 // reference fused_tconv.hpp:101-147: the GPU grid replaces the cout-slice
 // threads; `workers` is validated as in the reference and the result is
-// identical to transpose_conv_fused.
+// identical to transpose_conv_fused (as the reference's is for any count).
 template <typename T>
 Tensor<T> transpose_conv_fused_parallel(const Tensor<T>& input, const SubKernelSet<T>& sks,
                                         const TConvGeometry& geom, int workers) {
@@ -308,40 +528,85 @@ Tensor<T> transpose_conv_fused_parallel(const Tensor<T>& input, const SubKernelS
 }
 
 // reference reference_ops.hpp:86-108
-template <typename T>
-Tensor<T> conv2d_valid(const Tensor<T>& src, const Kernel<T>& k) {
+template <typename T, typename TallyT>
+Tensor<T> conv2d_valid(const Tensor<T>& src, const Kernel<T>& k, TallyT& tally) {
   if (k.spatially_empty()) throw ShapeError("conv2d_valid needs a non-empty kernel");
-  if (src.channels() != k.cin()) throw ContractError("channel mismatch");
+  if (src.channels() != k.cin())
+    throw ContractError("channel mismatch: input has " + std::to_string(src.channels()) + ", kernel expects " +
+                        std::to_string(k.cin()));
   const int oh = src.height() - k.kh() + 1, ow = src.width() - k.kw() + 1;
   if (oh < 1 || ow < 1) throw ShapeError("kernel does not fit input");
   Tensor<T> out(oh, ow, k.cout());
   detail::Staged ds(0, src.data(), src.size() * sizeof(T)), dk(2, k.data(), k.size() * sizeof(T));
   detail::Staged dy(1, out.size() * sizeof(T));
-  throw_on(segconv_conv2d_valid(ds.get(), dtype_of<T>::value, 1, src.height(), src.width(),
-                                src.channels(), dk.get(), k.kh(), k.kw(), k.cout(), nullptr,
-                                SEGCONV_EPI_NONE, dy.get(), nullptr));
+  throw_on(segconv_conv2d_valid(ds.get(), dtype_of<T>::value, 1, src.height(), src.width(), src.channels(),
+                                dk.get(), k.kh(), k.kw(), k.cout(), nullptr, SEGCONV_EPI_NONE,
+                                detail::conventional_math(), dy.get(), nullptr));
   dy.to_host(out.data(), out.size() * sizeof(T));
+  tally.dots((std::uint64_t)oh * ow * k.cout(), (std::uint64_t)k.kh() * k.kw() * k.cin());
   return out;
 }
 
-// reference reference_ops.hpp:116-133
 template <typename T>
-Tensor<T> transpose_conv_naive(const Tensor<T>& input, const Kernel<T>& k, int p) {
-  if (input.channels() != k.cin()) throw ContractError("channel mismatch");
+Tensor<T> conv2d_valid(const Tensor<T>& src, const Kernel<T>& k) {
+  NoTally t;
+  return conv2d_valid(src, k, t);
+}
+
+// reference reference_ops.hpp:116-133
+template <typename T, typename TallyT>
+Tensor<T> transpose_conv_naive(const Tensor<T>& input, const Kernel<T>& k, int p, TallyT& tally) {
+  if (input.channels() != k.cin())
+    throw ContractError("channel mismatch: input has " + std::to_string(input.channels()) + ", kernel expects " +
+                        std::to_string(k.cin()));
   const TConvGeometry geom = tconv_geometry(input.height(), k.kh(), k.kw(), p);
   if (input.height() != input.width())
-    throw ContractError("transpose conv expects a square input");
+    throw ContractError("transpose conv expects a square input, got " + std::to_string(input.height()) + "x" +
+                        std::to_string(input.width()));
   Tensor<T> out(geom.out_h, geom.out_w, k.cout());
-  const size_t ws = segconv_naive_workspace_bytes(dtype_of<T>::value, 1, input.height(),
-                                                  input.channels(), p);
+  const size_t ws = segconv_naive_workspace_bytes(dtype_of<T>::value, 1, input.height(), input.channels(), p);
   detail::Staged dx(0, input.data(), input.size() * sizeof(T)), dk(2, k.data(), k.size() * sizeof(T));
   detail::Staged dw(3, ws), dy(1, out.size() * sizeof(T));
-  throw_on(segconv_transpose_conv_naive(dx.get(), dtype_of<T>::value, 1, input.height(),
-                                        input.channels(), dk.get(), k.kh(), k.kw(), k.cout(), p,
-                                        dw.get(), ws, nullptr, SEGCONV_EPI_NONE, dy.get(),
-                                        nullptr));
+  throw_on(segconv_transpose_conv_naive(dx.get(), dtype_of<T>::value, 1, input.height(), input.channels(),
+                                        dk.get(), k.kh(), k.kw(), k.cout(), p, dw.get(), ws, nullptr,
+                                        SEGCONV_EPI_NONE, detail::conventional_math(), dy.get(), nullptr));
   dy.to_host(out.data(), out.size() * sizeof(T));
+  tally.dots((std::uint64_t)geom.out_h * geom.out_w * k.cout(), (std::uint64_t)k.kh() * k.kw() * k.cin());
   return out;
+}
+
+template <typename T>
+Tensor<T> transpose_conv_naive(const Tensor<T>& input, const Kernel<T>& k, int p) {
+  NoTally t;
+  return transpose_conv_naive(input, k, p, t);
+}
+
+// ------------------------------------------------------------- analysis
+// reference analysis.hpp:14-77
+struct LayerShape {
+  int n_in = 0, cin = 0, cout = 0, kh = 0, kw = 0, p_orig = 0;
+};
+inline TConvGeometry geometry_of(const LayerShape& s) {
+  if (s.cin < 1 || s.cout < 1)
+    throw ShapeError("channel counts must be positive, got cin=" + std::to_string(s.cin) +
+                     " cout=" + std::to_string(s.cout));
+  return tconv_geometry(s.n_in, s.kh, s.kw, s.p_orig);
+}
+inline OpCounts count_ops_naive(const LayerShape& s) {
+  uint64_t o[4];
+  throw_on(segconv_count_ops(s.n_in, s.cin, s.cout, s.kh, s.kw, s.p_orig, o));
+  return {o[0], o[1]};
+}
+inline OpCounts count_ops_fused(const LayerShape& s) {
+  uint64_t o[4];
+  throw_on(segconv_count_ops(s.n_in, s.cin, s.cout, s.kh, s.kw, s.p_orig, o));
+  return {o[2], o[3]};
+}
+inline std::uint64_t memory_saved_bytes(const LayerShape& s, int elem_bytes) {
+  const TConvGeometry g = geometry_of(s);
+  const std::uint64_t up = (std::uint64_t)g.up_h * g.up_w;
+  const std::uint64_t side = (std::uint64_t)s.n_in + 2 * g.p_fused;
+  return (std::uint64_t)elem_bytes * (std::uint64_t)s.cin * (up - side * side);
 }
 
 // ------------------------------------------------------------- SGC1 files

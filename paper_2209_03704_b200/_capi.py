@@ -86,12 +86,12 @@ SIGNATURES = {
     "segconv_last_error_offset": (_sz, []),
     "segconv_upsample2x_pad": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _vp]),
     "segconv_upsample2x_pad_backward": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _vp]),
-    "segconv_conv2d_valid": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _i, _vp, _u, _vp, _vp]),
+    "segconv_conv2d_valid": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _i, _i, _i, _vp, _u, _i, _vp, _vp]),
     "segconv_conv2d_valid_backward": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _vp,
                                            _vp, _i, _vp]),
     "segconv_naive_workspace_bytes": (_sz, [_i, _i, _i, _i, _i]),
     "segconv_transpose_conv_naive": (_i, [_vp, _i, _i, _i, _i, _vp, _i, _i, _i, _i, _vp, _sz,
-                                          _vp, _u, _vp, _vp]),
+                                          _vp, _u, _i, _vp, _vp]),
     "segconv_count_ops": (_i, [_i, _i, _i, _i, _i, _i, C.POINTER(C.c_uint64)]),
     "segconv_stack_create": (_i, [C.POINTER(Layer), _i, _i, _i, _i, C.POINTER(_vp)]),
     "segconv_stack_forward": (_i, [_vp, _vp, _i, _vp, C.POINTER(Timing)]),

@@ -782,8 +782,8 @@ segconv_status segconv_upsample2x_pad_backward(const void* d_gy, segconv_dtype d
 // reference reference_ops.hpp:86-102
 segconv_status segconv_conv2d_valid(const void* d_src, segconv_dtype dtype, int batch, int h, int w,
                                     int cin, const void* d_kernel, int kh, int kw, int cout,
-                                    const float* d_bias, unsigned epilogue, void* d_y,
-                                    void* stream) {
+                                    const float* d_bias, unsigned epilogue, segconv_math math,
+                                    void* d_y, void* stream) {
   if (kh < 1 || kw < 1) return fail(SEGCONV_E_SHAPE, "conv2d_valid needs a non-empty kernel");
   if (h < 1 || w < 1 || cin < 1 || cout < 1 || batch < 0)
     return fail(SEGCONV_E_SHAPE, "tensor dims must be positive");
@@ -792,16 +792,23 @@ segconv_status segconv_conv2d_valid(const void* d_src, segconv_dtype dtype, int 
   if (!valid_dtype(dtype)) return fail(SEGCONV_E_CONTRACT, "unknown dtype");
   if ((epilogue & SEGCONV_EPI_BIAS) && !d_bias)
     return fail(SEGCONV_E_CONTRACT, "bias epilogue requested without a bias pointer");
+  if (math != SEGCONV_MATH_AUTO && math != SEGCONV_MATH_FFMA && math != SEGCONV_MATH_EXACT &&
+      !(math == SEGCONV_MATH_BF16 && dtype == SEGCONV_BF16))
+    return fail(SEGCONV_E_UNSUPPORTED, "conv2d_valid runs AUTO, FFMA, EXACT (float/double) or BF16 (bf16) math");
+  if (math == SEGCONV_MATH_EXACT && dtype == SEGCONV_BF16)
+    return fail(SEGCONV_E_CONTRACT, "EXACT math is defined for float and double (the reference's types)");
   if (batch == 0) return SEGCONV_OK;
-  if (dtype == SEGCONV_BF16 && tc_conv_valid_supported(batch, h, w, cin, kh, kw, cout) &&
-      !getenv("SEGCONV_NO_TC_CONV"))
+  if (math == SEGCONV_MATH_EXACT)
+    g_path = "simt-exact";
+  else if (dtype == SEGCONV_BF16 && tc_conv_valid_supported(batch, h, w, cin, kh, kw, cout))
     g_path = "tc-pair";
   else if (dtype == SEGCONV_F32 && kh == kw && cout > 4 && kh >= 3 && kh <= 5)
     g_path = "simt-tiled";
   else
     g_path = "simt-generic";
   return cuda_status(launch_conv2d_valid(d_src, dtype, batch, h, w, cin, d_kernel, kh, kw, cout,
-                                         d_bias, epilogue, d_y, (cudaStream_t)stream),
+                                         d_bias, epilogue, math == SEGCONV_MATH_EXACT, d_y,
+                                         (cudaStream_t)stream),
                      "conv2d_valid");
 }
 
@@ -859,7 +866,8 @@ segconv_status segconv_transpose_conv_naive(const void* d_x, segconv_dtype dtype
                                             int n_in, int cin, const void* d_kernel, int kh,
                                             int kw, int cout, int p_orig, void* d_workspace,
                                             size_t workspace_bytes, const float* d_bias,
-                                            unsigned epilogue, void* d_y, void* stream) {
+                                            unsigned epilogue, segconv_math math, void* d_y,
+                                            void* stream) {
   if (cin < 1 || cout < 1) return fail(SEGCONV_E_SHAPE, "bad kernel dims");
   segconv_geometry g;
   segconv_status st = segconv_tconv_geometry(n_in, kh, kw, p_orig, &g);
@@ -872,7 +880,7 @@ segconv_status segconv_transpose_conv_naive(const void* d_x, segconv_dtype dtype
   st = segconv_upsample2x_pad(d_x, dtype, batch, n_in, cin, p_orig, d_workspace, stream);
   if (st != SEGCONV_OK) return st;
   return segconv_conv2d_valid(d_workspace, dtype, batch, g.up_h, g.up_w, cin, d_kernel, kh, kw,
-                              cout, d_bias, epilogue, d_y, stream);
+                              cout, d_bias, epilogue, math, d_y, stream);
 }
 
 // reference analysis.hpp:31-67

@@ -97,7 +97,9 @@ cudaError_t launch_upsample_pad_backward(const void* g, int dtype, int batch, in
 }
 
 // Generic valid correlation: one thread per output element (any shape/dtype).
-template <typename T, typename ACC>
+// EXACT: the reference's (u, v, ch) order with separate multiply and add
+// (accumulate_window, reference_ops.hpp:31-79, built with -ffp-contract=off).
+template <typename T, typename ACC, bool EXACT = false>
 __global__ void __launch_bounds__(256)
     conv_valid_generic(const T* __restrict__ src, int batch, int h, int w, int cin,
                        const T* __restrict__ k, int kh, int kw, int cout, const float* bias,
@@ -117,8 +119,15 @@ __global__ void __launch_bounds__(256)
       for (int v = 0; v < kw; ++v) {
         const T* sp = src + (((long long)b * h + oy + u) * w + ox + v) * cin;
         const T* kp = k + ((long long)(u * kw + v) * cin) * cout + f;
-        for (int ch = 0; ch < cin; ++ch)
-          acc = fma((ACC)to_acc(sp[ch]), (ACC)to_acc(kp[(long long)ch * cout]), acc);
+        for (int ch = 0; ch < cin; ++ch) {
+          const ACC a = (ACC)to_acc(sp[ch]), bw = (ACC)to_acc(kp[(long long)ch * cout]);
+          if constexpr (!EXACT)
+            acc = fma(a, bw, acc);
+          else if constexpr (sizeof(ACC) == 8)
+            acc = __dadd_rn(acc, __dmul_rn(a, bw));
+          else
+            acc = __fadd_rn(acc, __fmul_rn(a, bw));
+        }
       }
     y[e] = from_d<T>((double)epilogue_apply(acc, epi, bias, f));
   }
@@ -235,11 +244,23 @@ __global__ void kmajor_transpose(const __nv_bfloat16* __restrict__ k, int taps, 
 
 cudaError_t launch_conv2d_valid(const void* src, int dtype, int batch, int h, int w, int cin,
                                 const void* k, int kh, int kw, int cout, const float* bias,
-                                unsigned epi, void* y, cudaStream_t s) {
+                                unsigned epi, bool exact, void* y, cudaStream_t s) {
   const long long total = (long long)batch * (h - kh + 1) * (w - kw + 1) * cout;
   if (total <= 0) return cudaSuccess;
-  if (dtype == SEGCONV_BF16 && tc_conv_valid_supported(batch, h, w, cin, kh, kw, cout) &&
-      getenv("SEGCONV_NO_TC_CONV") == nullptr) {
+  if (exact) {
+    const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 148LL * 64);
+    if (dtype == SEGCONV_F32)
+      conv_valid_generic<float, float, true><<<blocks, 256, 0, s>>>(
+          (const float*)src, batch, h, w, cin, (const float*)k, kh, kw, cout, bias, epi, (float*)y);
+    else if (dtype == SEGCONV_F64)
+      conv_valid_generic<double, double, true><<<blocks, 256, 0, s>>>(
+          (const double*)src, batch, h, w, cin, (const double*)k, kh, kw, cout, bias, epi, (double*)y);
+    else
+      return cudaErrorInvalidValue;
+    note_launch();
+    return cudaGetLastError();
+  }
+  if (dtype == SEGCONV_BF16 && tc_conv_valid_supported(batch, h, w, cin, kh, kw, cout)) {
     const long long kn = (long long)kh * kw * cin * cout;
     void* kt = nullptr;
     cudaError_t e = workspace_alloc(&kt, (size_t)kn * 2, s);

@@ -138,7 +138,7 @@ cudaError_t launch_upsample_pad(const void* x, int dtype, int batch, int n, int 
                                 void* up, cudaStream_t s);
 cudaError_t launch_conv2d_valid(const void* src, int dtype, int batch, int h, int w, int cin,
                                 const void* k, int kh, int kw, int cout, const float* bias,
-                                unsigned epi, void* y, cudaStream_t s);
+                                unsigned epi, bool exact, void* y, cudaStream_t s);
 
 void note_launch(int n = 1);
 

@@ -759,8 +759,10 @@ def upsample2x_pad_backward(grad_up: torch.Tensor, n_in: int, p: int) -> torch.T
     return gx[0] if squeeze else gx
 
 
-def conv2d_valid(src: torch.Tensor, k: torch.Tensor, *, bias=None, activation=None) -> torch.Tensor:
-    """reference reference_ops.hpp:86-108."""
+def conv2d_valid(src: torch.Tensor, k: torch.Tensor, *, bias=None, activation=None,
+                 math: Optional[str] = None) -> torch.Tensor:
+    """reference reference_ops.hpp:86-108.  ``math="exact"`` (float/double):
+    the reference's accumulation order, bit-identical to its CPU result."""
     sb, squeeze = _as_batch(src)
     dev = _device()
     host = not sb.is_cuda
@@ -781,8 +783,8 @@ def conv2d_valid(src: torch.Tensor, k: torch.Tensor, *, bias=None, activation=No
     epi = _epilogue(bias, activation)
     bptr = bias.to(dev, torch.float32).contiguous().data_ptr() if bias is not None else None
     _check(A.lib().segconv_conv2d_valid(sd.data_ptr(), _dtype_code(sd), b, h, w, cin,
-                                        kd.data_ptr(), kh, kw, cout, bptr, epi, y.data_ptr(),
-                                        _stream()))
+                                        kd.data_ptr(), kh, kw, cout, bptr, epi,
+                                        MATHS[math or "auto"], y.data_ptr(), _stream()))
     if host:
         y = y.cpu()
     return y[0] if squeeze else y
@@ -836,9 +838,12 @@ def conv2d_valid_backward(src: torch.Tensor, kernel: torch.Tensor, grad_out: tor
 
 
 def transpose_conv_naive(x: torch.Tensor, k: torch.Tensor, p: int, *, bias=None,
-                         activation=None, workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+                         activation=None, workspace: Optional[torch.Tensor] = None,
+                         math: Optional[str] = None) -> torch.Tensor:
     """reference reference_ops.hpp:116-133: upsample, pad, valid-correlate
-    (the conventional baseline; materialises the (2N-1+2p)^2 map)."""
+    (the conventional baseline; materialises the (2N-1+2p)^2 map).
+    ``math="exact"``: bit-identical to the reference (and to the fused op's
+    EXACT mode, the reference's fused == naive guarantee)."""
     xb, squeeze = _as_batch(x)
     dev = _device()
     host = not xb.is_cuda
@@ -862,7 +867,7 @@ def transpose_conv_naive(x: torch.Tensor, k: torch.Tensor, p: int, *, bias=None,
     _check(A.lib().segconv_transpose_conv_naive(
         xd.data_ptr(), _dtype_code(xd), b, h, cin, kd.data_ptr(), kh, kw, cout, int(p),
         workspace.data_ptr(), workspace.numel() * workspace.element_size(), bptr, epi,
-        y.data_ptr(), _stream()))
+        MATHS[math or "auto"], y.data_ptr(), _stream()))
     if host:
         y = y.cpu()
     return y[0] if squeeze else y

@@ -134,11 +134,11 @@ def test_naive_and_conv_contract_checks():
     L = A.lib()
     # workspace too small
     assert L.segconv_transpose_conv_naive(None, A.F32, 1, 4, 2, None, 3, 3, 1, 1, None, 0, None,
-                                          0, None, None) == A.E_CONTRACT
+                                          0, 0, None, None) == A.E_CONTRACT
     # kernel exceeds upsampled extent
     assert L.segconv_transpose_conv_naive(None, A.F32, 1, 4, 2, None, 9, 9, 1, 0, None, 0, None,
-                                          0, None, None) == A.E_SHAPE
-    assert L.segconv_conv2d_valid(None, A.F32, 1, 3, 3, 2, None, 4, 1, 1, None, 0, None,
+                                          0, 0, None, None) == A.E_SHAPE
+    assert L.segconv_conv2d_valid(None, A.F32, 1, 3, 3, 2, None, 4, 1, 1, None, 0, 0, None,
                                   None) == A.E_SHAPE
     assert L.segconv_naive_workspace_bytes(A.F32, 32, 256, 64, 0) == 32 * 511 * 511 * 64 * 4
 

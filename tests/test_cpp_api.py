@@ -48,3 +48,30 @@ def test_cpp_stack_runs(tmp_path):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failure(s)" in r.stdout
+
+
+REF_SAMPLE = "/root/reference/proj/samples/minimal_tconv.cpp"
+SAMPLE_BIN = os.path.join(ROOT, "tests", "cpp", "_samples", "minimal_tconv")
+
+
+@pytest.mark.skipif(not os.path.exists(REF_SAMPLE), reason="reference sources absent (GPU box)")
+def test_reference_sample_compiles_unchanged(tmp_path):
+    """The reference's own samples/minimal_tconv.cpp (its includes
+    <segconv/fused_tconv.hpp> etc., AllocStats / AllocScope, SubKernelSet,
+    transpose_conv_fused_parallel) compiles unchanged against include/."""
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I" + os.path.join(ROOT, "include"),
+                        "-I/usr/local/cuda/include", REF_SAMPLE], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.gpu
+def test_reference_sample_runs_bit_exact():
+    """The unchanged reference sample, built by __graft_entry__.build() with the
+    EXACT default math: fused == naive == parallel bit for bit on the GPU, as the
+    reference asserts on its CPU (exit code 0)."""
+    if not os.path.exists(SAMPLE_BIN):
+        pytest.skip("sample binary not built (needs the reference sources at build time)")
+    r = subprocess.run([SAMPLE_BIN], capture_output=True, text=True, timeout=120)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "bit for bit: yes" in r.stdout

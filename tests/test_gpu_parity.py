@@ -372,3 +372,19 @@ def test_host_buffer_pipeline_matches_device_call(batch, chunks):
     assert np.array_equal(got.numpy(), want)
     # and against the oracle at the fp32 tolerance (first image)
     approx_ok(got.numpy()[0], oracle.tconv_fused(x[:1], k, 0)[0], TOL_F32)
+
+
+def test_exact_naive_equals_exact_fused_and_the_reference():
+    """The reference's central guarantee (README: fused == naive bit for bit on
+    real data, one accumulation order, no FMA contraction) holds on the GPU in
+    EXACT math: the conventional path (upsample + pad + conv2d_valid) and the
+    segregated one agree bit for bit with each other and with the reference."""
+    rng = np.random.default_rng(77)
+    for (n, cin, cout, k, p) in [(16, 3, 8, 5, 2), (9, 4, 1, 3, 0), (7, 5, 6, 4, 1)]:
+        x = rng.uniform(-1, 1, (2, n, n, cin)).astype(np.float32)
+        kk = rng.uniform(-1, 1, (k, k, cin, cout)).astype(np.float32)
+        fused = run_fused(x, kk, p, "exact")
+        naive = sc.transpose_conv_naive(cuda(x), cuda(kk), p, math="exact").cpu().numpy()
+        np.testing.assert_array_equal(naive, fused)
+        np.testing.assert_array_equal(naive, oracle.tconv_naive(x, kk, p))
+        assert sc.last_path() == "simt-exact"
