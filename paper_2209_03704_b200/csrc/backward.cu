@@ -566,27 +566,6 @@ __global__ void __launch_bounds__(256) wgrad_reduce4_wide(const float4* __restri
   }
 }
 
-// stream-K pieces: element idx of gk belongs to tile T = ((t * ch_pairs + ch / 256)
-// * n_tiles + f / NT); its pieces are the pairs overlapping [T*chunks, (T+1)*chunks)
-// in slot order 0, 1, ... (deterministic)
-__global__ void wgrad_reduce_streamk(const float* __restrict__ ws, float* __restrict__ gk, int cin, int cout,
-                                     int taps, int nt_feat, long long chunks, long long share, int accumulate) {
-  const long long ksz = (long long)taps * cin * cout;
-  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= ksz) return;
-  const int f = (int)(e % cout);
-  const int ch = (int)((e / cout) % cin);
-  const int t = (int)(e / ((long long)cout * cin));
-  const int ch_pairs = (cin + 255) / 256, n_tiles = cout / nt_feat;
-  const long long T = ((long long)t * ch_pairs + ch / 256) * n_tiles + f / nt_feat;
-  const long long ts = T * chunks;
-  const int pieces = (int)((ts + chunks - 1) / share - ts / share) + 1;
-  float s = accumulate ? gk[e] : 0.f;
-  for (int i = 0; i < pieces; ++i) s += __ldcs(ws + (long long)i * ksz + e);
-  gk[e] = s;
-}
-
-
 // ------------------------------------------------- narrow outputs (cout <= 4)
 // The C4 family (5x5 -> 3 at 256^2): the packed FFMA tiles above leave most of
 // every tile's K (or N) idle and gather g element by element.  Here a CTA owns
@@ -765,24 +744,13 @@ __global__ void __launch_bounds__(256, COLS == 5 ? 3 : 2) wgrad_narrow(const T* 
 }
 }  // namespace bwd
 
-cudaError_t launch_wgrad_reduce_streamk(const float* ws, float* gk, int cin, int cout, int taps, int nt_feat,
-                                        long long chunks, long long share, int accumulate, cudaStream_t s) {
-  const long long ksz = (long long)taps * cin * cout;
-  bwd::wgrad_reduce_streamk<<<(unsigned)((ksz + 255) / 256), 256, 0, s>>>(ws, gk, cin, cout, taps, nt_feat, chunks,
-                                                                          share, accumulate);
-  cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess) note_launch();
-  return e;
-}
-
 static int sm_count() {
   const int sms = device_sm_count();
   return sms;
 }
 
 bool bwd_narrow_applies(const BackwardProblem& pr) {
-  static const bool off = getenv("SEGCONV_BWD_NARROW") && atoi(getenv("SEGCONV_BWD_NARROW")) == 0;
-  return !off && !pr.conv && pr.stride == 2 && pr.in_w >= 64 && pr.cout >= 1 && pr.cout <= 4 && pr.kh <= bwd::NW_MAXK &&
+  return !pr.conv && pr.stride == 2 && pr.in_w >= 64 && pr.cout >= 1 && pr.cout <= 4 && pr.kh <= bwd::NW_MAXK &&
          pr.kw <= bwd::NW_MAXK && pr.kh * pr.kw * pr.cout <= 80 && pr.in_h == pr.n && pr.in_w == pr.n &&
          (pr.dtype == SEGCONV_F32 || pr.dtype == SEGCONV_BF16);
 }
@@ -821,30 +789,24 @@ template <typename T, int CO>
 static cudaError_t narrow_wgrad_t(const BackwardProblem& pr, cudaStream_t s) {
   const int gw = bwd::nw_gw(pr.kw);
   const size_t smem = ((size_t)bwd::NW_PX * (bwd::NW_CH + 4) + (size_t)pr.kh * gw * CO) * sizeof(float);
-  static PerDeviceOnce once10, once5;
+  static PerDeviceOnce once5;
   {
-    cudaError_t e = smem_attr_once(once10, bwd::wgrad_narrow<T, CO, 10>, 200 * 1024);
-    if (e == cudaSuccess) e = smem_attr_once(once5, bwd::wgrad_narrow<T, CO, 5>, 200 * 1024);
+    const cudaError_t e = smem_attr_once(once5, bwd::wgrad_narrow<T, CO, 5>, 200 * 1024);
     if (e != cudaSuccess) return e;
   }
   const int chb = (pr.cin + bwd::NW_CH - 1) / bwd::NW_CH;
   const long long total_rows = (long long)pr.batch * pr.in_h;
   // a few CTAs per SM over (row range, channel block)
-  static const int cps = getenv("SEGCONV_WGRAD_NARROW_CPS") ? atoi(getenv("SEGCONV_WGRAD_NARROW_CPS")) : 3;
+  constexpr int cps = 3;
   long long rows = std::max(1LL, (total_rows * chb + (long long)cps * sm_count() - 1) / ((long long)cps * sm_count()));
   const long long splits = (total_rows + rows - 1) / rows;
   const long long ksz = (long long)pr.kh * pr.kw * pr.cin * pr.cout;
   float* ws = nullptr;
-  static const int cols = getenv("SEGCONV_WGRAD_NARROW_COLS") ? atoi(getenv("SEGCONV_WGRAD_NARROW_COLS")) : 5;
-  const int phases = cols == 5 ? 2 : 4;
+  constexpr int phases = 2;  // 5 (tap, f) columns per thread, two pixel phases
   cudaError_t e = workspace_alloc((void**)&ws, (size_t)splits * phases * ksz * sizeof(float), s);
   if (e != cudaSuccess) return e;
-  if (cols == 5)
-    bwd::wgrad_narrow<T, CO, 5><<<dim3((unsigned)splits, (unsigned)chb), 256, smem, s>>>(
-        (const T*)pr.x, (const T*)pr.gy, ws, pr, (int)rows);
-  else
-    bwd::wgrad_narrow<T, CO, 10><<<dim3((unsigned)splits, (unsigned)chb), 256, smem, s>>>(
-        (const T*)pr.x, (const T*)pr.gy, ws, pr, (int)rows);
+  bwd::wgrad_narrow<T, CO, 5><<<dim3((unsigned)splits, (unsigned)chb), 256, smem, s>>>(
+      (const T*)pr.x, (const T*)pr.gy, ws, pr, (int)rows);
   e = cudaGetLastError();
   if (e == cudaSuccess) {
     note_launch();
@@ -921,8 +883,7 @@ static cudaError_t bwd_weight_t(const BackwardProblem& pr, bool exact, cudaStrea
     }
   }
   if constexpr (sizeof(T) <= 4) {
-    static const bool wn = !getenv("SEGCONV_BWD_NARROW_WGRAD") || atoi(getenv("SEGCONV_BWD_NARROW_WGRAD")) != 0;
-    if (wn && bwd_narrow_applies(pr) && M > 0) return narrow_wgrad<T>(pr, s);
+    if (bwd_narrow_applies(pr) && M > 0) return narrow_wgrad<T>(pr, s);
   }
   // cout % 64 != 0: (tap, f) packed columns, all taps of a tile in one CTA
   const bool packed = pr.cout % bwd::BN != 0;
@@ -931,7 +892,7 @@ static cudaError_t bwd_weight_t(const BackwardProblem& pr, bool exact, cudaStrea
   const int tiles = ((pr.cin + bwd::BM - 1) / bwd::BM) * ntile * (packed ? 1 : taps);
   // split the pixel reduction until ~CPS CTAs per SM (latency hiding for the
   // gathers), keeping >= 256 pixels per split
-  static const int cps = getenv("SEGCONV_WGRAD_CPS") ? std::max(1, atoi(getenv("SEGCONV_WGRAD_CPS"))) : 4;
+  constexpr int cps = 4;
   long long splits = std::max(1LL, ((long long)cps * sm_count() + tiles - 1) / tiles);
   splits = std::min(splits, std::max(1LL, M / 256));
   if (M == 0) splits = 1;

@@ -310,16 +310,14 @@ segconv_status segconv_subkernels_for_math(int kh, int kw, int cin, int cout, in
       // narrow layers (cout <= 32, p_fused == 0): class-folded kernel
       const bool fold = !fold_blocked && tc_fold_fits(math, kh, kw, p_orig, cin, cout);
       // wide bf16 layers: CTA-pair kernel on K-major (class, f, u, v, ch) panels
-      if (!fold && math == SEGCONV_MATH_BF16 && tc_wide_fits(kh, kw, p_orig, cin, cout) &&
-          getenv("SEGCONV_NO_WIDE") == nullptr) {
+      if (!fold && math == SEGCONV_MATH_BF16 && tc_wide_fits(kh, kw, p_orig, cin, cout)) {
         const segconv_status st = segconv_subkernels_init(kh, kw, cin, cout, p_orig, SEGCONV_BF16,
                                                           SEGCONV_PANEL_KMAJOR, out);
         if (st == SEGCONV_OK) out->math = SEGCONV_MATH_BF16;
         return st;
       }
       // wide fp32 layers: the same kernel on split planes, K = [hi | lo] x 3 passes
-      if (!fold && math == SEGCONV_MATH_F16X3 && tc_wide_fits(kh, kw, p_orig, cin, cout) &&
-          getenv("SEGCONV_NO_WIDE") == nullptr && getenv("SEGCONV_NO_WIDE_SPLIT") == nullptr) {
+      if (!fold && math == SEGCONV_MATH_F16X3 && tc_wide_fits(kh, kw, p_orig, cin, cout)) {
         const segconv_status st = segconv_subkernels_init(kh, kw, cin, cout, p_orig, SEGCONV_F16_SPLIT,
                                                           SEGCONV_PANEL_KMAJOR, out);
         if (st == SEGCONV_OK) out->math = SEGCONV_MATH_F16X3;

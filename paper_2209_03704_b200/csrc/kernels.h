@@ -63,8 +63,6 @@ cudaError_t launch_tc_conv_valid(const void* src, int batch, int h, int w, int c
                                  int kw, int cout, const float* bias, unsigned epi, void* y, cudaStream_t s);
 cudaError_t launch_tc_bwd_weight(const BackwardProblem& pr, cudaStream_t s);
 cudaError_t workspace_alloc(void** p, size_t bytes, cudaStream_t s);
-cudaError_t launch_wgrad_reduce_streamk(const float* ws, float* gk, int cin, int cout, int taps, int nt_feat,
-                                        long long chunks, long long share, int accumulate, cudaStream_t s);
 cudaError_t launch_wgrad_reduce(const float* ws, float* gk, long long ksz, int splits, int accumulate,
                                 cudaStream_t s);
 

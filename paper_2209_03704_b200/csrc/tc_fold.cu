@@ -855,8 +855,7 @@ static FoldPlan make_fold_plan_n(const FusedProblem& pr, int math, int block_n) 
   // TMEM-A variant: when the four classes fill all 128 MMA rows and the weights
   // fit 256 TMEM columns (shifts * planes * cin / 2), the weights become the
   // MMA A operand in TMEM and all of shared memory goes to halo stages.
-  pl.tmem_a = p.R == 128 && p.N <= 128 && p.shifts * planes * pr.cin / 2 <= 256 &&
-              getenv("SEGCONV_FOLD_NO_TMEM_A") == nullptr;
+  pl.tmem_a = p.R == 128 && p.N <= 128 && p.shifts * planes * pr.cin / 2 <= 256;
   p.a_tmem_col = 256;
   p.w_img_bytes = planes * p.nkb * CH * p.w_rows * 16;
   p.w_bytes = pl.tmem_a ? 0 : p.w_img_bytes;
@@ -868,7 +867,7 @@ static FoldPlan make_fold_plan_n(const FusedProblem& pr, int math, int block_n) 
   // LAND (split math, LINEAR staging): the fp32 halo lands as {kb, rows} TMA
   // boxes (4*kb-byte rows: 128-byte requests at kb = 32, against 32-byte ones
   // for per-chunk boxes) and the converters write the operand stages.
-  p.land = split && !p.block_mode && getenv("SEGCONV_FOLD_NO_LAND") == nullptr ? 1 : 0;
+  p.land = split && !p.block_mode ? 1 : 0;
   if (p.land) {
     p.l_stage_bytes = (p.pieces * p.piece_rows * p.kb * 4 + 1023) / 1024 * 1024;
     const int pair = p.a_stage_bytes + p.l_stage_bytes;

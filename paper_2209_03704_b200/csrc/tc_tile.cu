@@ -366,7 +366,7 @@ static bool tile_shape(const FusedProblem& pr) {
 }
 
 bool tc_tile_supported(const FusedProblem& pr, int math) {
-  if (math != SEGCONV_MATH_BF16 || getenv("SEGCONV_NO_TILE")) return false;
+  if (math != SEGCONV_MATH_BF16) return false;
   return tile_shape(pr);
 }
 
@@ -467,7 +467,7 @@ static cudaError_t launch_tile_t(const FusedProblem& pr, const void* img, cudaSt
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                               \
     at[0].val.programmaticStreamSerializationAllowed = 1;                                        \
     lc.attrs = at;                                                                               \
-    lc.numAttrs = getenv("SEGCONV_NO_PDL") ? 0 : 1;                                              \
+    lc.numAttrs = 1;                                                                             \
     e = cudaLaunchKernelEx(&lc, kern, p, tmap);                                                  \
     if (e != cudaSuccess) return e;                                                              \
   }

@@ -114,10 +114,6 @@ struct Params {
   int w_kw, w_taps, w_ch_pairs, w_splits, w_cin, w_cout, w_direct, w_accumulate;
   int w_in_h, w_in_w;  // input map (anchor grid) of the kernel-gradient walk
   long long w_chunks, w_cps, w_ksz;
-  // stream-K schedule (w_share > 0): pair P takes chunk-units [P * share, (P+1) * share)
-  // of the (tile, chunk) space, cutting tiles into pieces; piece i of a tile goes
-  // to slot i of the workspace (launch_wgrad_reduce_streamk sums them in order)
-  long long w_share;
   float* wout;
   unsigned long long* trace;
   int debug;
@@ -256,33 +252,15 @@ __device__ __forceinline__ bool wunit_of(const Params& p, int k, int& s, int& t,
   return true;
 }
 
-// WGRAD segment k of this pair: tile (t, ct, nt), chunk range [c0, c1), output slot
+// WGRAD segment k of this pair: tile (t, ct, nt), chunk range [c0, c1) of
+// pixel split s, output slot s (0 when the sum is not split)
 __device__ __forceinline__ bool wseg_of(const Params& p, int k, int& t, int& ct, int& nt, long long& c0,
                                         long long& c1, int& slot) {
-  long long tile;
-  if (p.w_share > 0) {
-    const long long pair = blockIdx.x / 2;
-    const long long total = p.units * p.w_chunks;
-    const long long g0 = pair * p.w_share, g1 = min(total, g0 + p.w_share);
-    tile = g0 / p.w_chunks + k;
-    const long long ts = tile * p.w_chunks;
-    const long long s0 = max(g0, ts), s1 = min(g1, ts + p.w_chunks);
-    if (s0 >= s1) return false;
-    c0 = s0 - ts;
-    c1 = s1 - ts;
-    slot = (int)(pair - ts / p.w_share);
-  } else {
-    int s;
-    if (!wunit_of(p, k, s, t, ct, nt)) return false;
-    c0 = (long long)s * p.w_cps;
-    c1 = min(p.w_chunks, c0 + p.w_cps);
-    slot = p.w_direct ? 0 : s;
-    return true;
-  }
-  nt = (int)(tile % p.n_tiles);
-  tile /= p.n_tiles;
-  ct = (int)(tile % p.w_ch_pairs);
-  t = (int)(tile / p.w_ch_pairs);
+  int s;
+  if (!wunit_of(p, k, s, t, ct, nt)) return false;
+  c0 = (long long)s * p.w_cps;
+  c1 = min(p.w_chunks, c0 + p.w_cps);
+  slot = p.w_direct ? 0 : s;
   return true;
 }
 
@@ -985,10 +963,8 @@ bool tc_wide_fits(int kh, int kw, int p, int cin, int cout) {
 
 // xs: the [hi | lo] fp16 copy of an fp32 input (SPLIT); any aligned pointer
 // when only checking support
-static int wide_bprod() {
-  static const int v = getenv("SEGCONV_WIDE_BPROD") ? atoi(getenv("SEGCONV_WIDE_BPROD")) : 1;
-  return v ? 1 : 0;
-}
+// A and B streams on two producer lanes (measured: C3 81.3 -> 78.9 us)
+static int wide_bprod() { return 1; }
 
 static int wide_pairs();
 
@@ -1036,10 +1012,9 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
     // small batches of small maps (GAN generators' first layers): fewer 256-wide
     // units than CTA pairs leaves SMs idle -- halve the feature tile when the
     // doubled unit count still fits one wave (DCGAN 4x4 x 1024 -> 512: 34.8 -> 32.2 us)
-    static const bool adapt = !getenv("SEGCONV_WIDE_NT_ADAPT") || atoi(getenv("SEGCONV_WIDE_NT_ADAPT")) != 0;
     long long u = 0;
     for (int q = 0; q < 4; ++q) u += ((long long)pr.batch * pr.cls.rows[q] * pr.cls.cols[q] + 255) / 256;
-    if (adapt && p.NT > 128 && 2 * u * ((pr.cout + p.NT - 1) / p.NT) <= wide_pairs()) p.NT = 128;
+    if (p.NT > 128 && 2 * u * ((pr.cout + p.NT - 1) / p.NT) <= wide_pairs()) p.NT = 128;
   }
   p.n_tiles = (pr.cout + p.NT - 1) / p.NT;
   if (p.n_tiles * p.NT > pr.cout_pad && p.n_tiles > 1) {
@@ -1081,12 +1056,6 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
     // measured (B200, batch 64, 4x4, p = 2): 128^2 x 64 -> 64 561 -> 365 us,
     // 64^2 x 64 -> 64 152 -> 106 us; at 32^2 the im2col walk is still faster
     if (!split && !tf32 && p.tile2d && tc_wide_ntile(pr.cout) <= 64 && pr.n >= 64) p.im2col = 0;
-    // tiny maps (C5 c: 7 x 7): 128-row im2col boxes span several images and run
-    // slowly; linear halo rows with all classes per unit instead (one accumulator)
-    static const int small_env = getenv("SEGCONV_WIDE_ALLQ_SMALL") ? atoi(getenv("SEGCONV_WIDE_ALLQ_SMALL")) : 0;
-    if (!split && !tf32 && !p.tile2d && tc_wide_ntile(pr.cout) == 128 && pr.n <= small_env) p.im2col = 0;
-    const char* e = getenv("SEGCONV_WIDE_IM2COL");
-    if (e && !split && !tf32) p.im2col = atoi(e) ? 1 : 0;  // split / tf32 need im2col staging
     p.bprod = p.im2col ? wide_bprod() : 0;
   }
   // halo-shift staging (SEGCONV_WIDE_IM2COL=0) limits: the staged rows must fit
@@ -1129,11 +1098,9 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
     if (p.S_rows > 256) return false;  // one TMA box
   }
   {
-    static const int allq_env = getenv("SEGCONV_WIDE_ALLQ") ? atoi(getenv("SEGCONV_WIDE_ALLQ")) : 1;
-    p.allq = (!p.im2col && p.NT <= 128 && allq_env) ? 1 : 0;
+    p.allq = (!p.im2col && p.NT <= 128) ? 1 : 0;
     p.nacc = p.allq && 4 * p.NT > 256 ? 1 : 2;
-    static const int wres_env = getenv("SEGCONV_WIDE_WRES") ? atoi(getenv("SEGCONV_WIDE_WRES")) : 1;
-    p.wres = (p.allq && p.n_tiles == 1 && wres_env) ? 1 : 0;
+    p.wres = (p.allq && p.n_tiles == 1) ? 1 : 0;
     p.bprod = (!p.im2col && !p.wres) ? wide_bprod() : p.bprod;
     int tb = 0;
     for (int q = 0; q < 4; ++q) {
@@ -1432,31 +1399,10 @@ static bool make_wide_wgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
       best = sp;
     }
   }
-  if (const char* e = getenv("SEGCONV_WGRAD_SPLITS"))  // diagnostics
-    if (*e) best = std::max(1, atoi(e));
   p.w_cps = (p.w_chunks + best - 1) / best;
   p.w_splits = (int)((p.w_chunks + p.w_cps - 1) / p.w_cps);
   p.w_direct = p.w_splits == 1;
   p.units = base * p.w_splits;
-  // stream-K alternative: every pair the same number of chunk-units; a tile is
-  // cut into at most ceil(chunks / share) + 1 pieces
-  {
-    const long long share = (base * p.w_chunks + pairs - 1) / pairs;
-    const int maxp = (int)((p.w_chunks + share - 1) / share) + 1;
-    const double t_sk = (double)share * t_chunk + maxp * t_split + 3.0;
-    const char* e = getenv("SEGCONV_WGRAD_STREAMK");
-    // measured (B200): the pieces' extra reduction and the busier L2 with every
-    // pair active make it slower than the pixel splits on C3 / C5 (152 vs 144 us
-    // on C3), so it is opt-in (SEGCONV_WGRAD_STREAMK=1)
-    (void)t_sk;
-    const bool want = e && *e && atoi(e) != 0;
-    if (want && share >= 8) {
-      p.w_share = share;
-      p.w_splits = maxp;  // workspace slots
-      p.w_direct = 0;
-      p.units = base;  // tiles
-    }
-  }
   p.a_stage_bytes = 2 * tcw::WCH * 128;
   p.b_stage_bytes = (p.NT / 2 / 64) * tcw::WCH * 128;
   const int bar_bytes = (2 * tcw::MAX_STAGES_A + 2 * tcw::MAX_STAGES_B + 4) * 8 + 16;
@@ -1620,13 +1566,10 @@ static cudaError_t launch_wide_t(const tcw::Params& prm, const tcw::Maps& maps, 
   }
   const int sms = device_sm_count();
   long long pairs = std::min<long long>(prm.units, sms / 2);
-  if (prm.mode == 1 && prm.w_share > 0)  // stream-K: every pair with a share of chunk-units
-    pairs = (prm.units * prm.w_chunks + prm.w_share - 1) / prm.w_share;
   tcw::Params pk = prm;
   // last partial wave: when its T units fit twice over, run them as 2T feature
   // half-tiles (N = NT/2) so the wave takes half a unit instead of a whole one
-  static const bool tail_split = !getenv("SEGCONV_WIDE_TAIL") || atoi(getenv("SEGCONV_WIDE_TAIL")) != 0;
-  if (tail_split && prm.mode == 0 && prm.im2col && prm.NT >= 128 && pairs > 0) {
+  if (prm.mode == 0 && prm.im2col && prm.NT >= 128 && pairs > 0) {
     const long long T = prm.units % pairs;
     if (T > 0 && 2 * T <= pairs) {
       pk.tail_on = 1;
@@ -1649,8 +1592,7 @@ static cudaError_t launch_wide_t(const tcw::Params& prm, const tcw::Maps& maps, 
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap the previous
   at[1].val.programmaticStreamSerializationAllowed = 1;              // kernel's tail
   cfg.attrs = at;
-  static const bool pdl = getenv("SEGCONV_NO_PDL") == nullptr;
-  cfg.numAttrs = pdl ? 2 : 1;
+  cfg.numAttrs = 2;
   cudaError_t e = cudaLaunchKernelEx(&cfg, kern, pk, maps);
   if (e == cudaSuccess) note_launch();
   return e;
@@ -1760,11 +1702,7 @@ cudaError_t launch_tc_bwd_weight(const BackwardProblem& pr, cudaStream_t s) {
   p.wout = ws;
   e = launch_wide_t<float, 0>(p, maps, s);
   if (e == cudaSuccess) {
-    if (p.w_share > 0)
-      e = launch_wgrad_reduce_streamk(ws, (float*)pr.gk, pr.cin, pr.cout, p.w_taps, p.NT, p.w_chunks,
-                                      p.w_share, pr.accumulate, s);
-    else
-      e = launch_wgrad_reduce(ws, (float*)pr.gk, p.w_ksz, p.w_splits, pr.accumulate, s);
+    e = launch_wgrad_reduce(ws, (float*)pr.gk, p.w_ksz, p.w_splits, pr.accumulate, s);
   }
   cudaError_t e2 = cudaFreeAsync(ws, s);
   return e != cudaSuccess ? e : e2;

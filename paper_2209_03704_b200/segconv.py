@@ -411,7 +411,8 @@ def transpose_conv_fused(x: torch.Tensor, k: Union[SubKernelSet, torch.Tensor],
 def transpose_conv_fused_backward(x: torch.Tensor, kernel: torch.Tensor, p_orig: int,
                                   grad_out: torch.Tensor, *, math: Optional[str] = None,
                                   input_grad: bool = True, kernel_grad: bool = True,
-                                  grad_kernel: Optional[torch.Tensor] = None):
+                                  grad_kernel: Optional[torch.Tensor] = None,
+                                  grad_input: Optional[torch.Tensor] = None):
     """Gradients of the fused layer -- reference netdemo/layers.hpp:171-211
     (net::FusedTConv::backward), batched.
 
@@ -420,7 +421,9 @@ def transpose_conv_fused_backward(x: torch.Tensor, kernel: torch.Tensor, p_orig:
     Returns ``(grad_input, grad_kernel)`` (either None when not requested);
     grad_input has x's dtype, grad_kernel is float32 (float64 for double data)
     and summed over the batch.  Passing ``grad_kernel`` accumulates into it, as
-    the reference's grad_ does across backward calls.  ``math``: "exact"
+    the reference's grad_ does across backward calls; ``grad_input`` (a
+    contiguous CUDA tensor of x's batched shape and dtype) receives the input
+    gradient in place.  ``math``: "exact"
     (bit-identical to the reference, float/double), "ffma", "bf16", None (auto).
     """
     xb, squeeze = _as_batch(x)
@@ -443,7 +446,13 @@ def transpose_conv_fused_backward(x: torch.Tensor, kernel: torch.Tensor, p_orig:
     xd = xb.to(dev).contiguous()
     gd = gb.to(dev, dt).contiguous()
     kd = kernel.to(dev, dt).contiguous()
-    gx = torch.empty_like(xd) if input_grad else None
+    if input_grad and grad_input is not None:
+        if tuple(grad_input.shape) != tuple(xd.shape) or grad_input.dtype != dt or \
+                not grad_input.is_cuda or not grad_input.is_contiguous():
+            raise ContractError("grad_input must be a contiguous CUDA tensor of the input's shape and dtype")
+        gx = grad_input
+    else:
+        gx = torch.empty_like(xd) if input_grad else None
     acc_dt = torch.float64 if dt == torch.float64 else torch.float32
     acc = 0
     if kernel_grad:
