@@ -50,7 +50,29 @@ def build(verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+    build_cli()
     return LIB
+
+
+CLI_SRC = os.path.join(ROOT, "tools", "segconv_b200.cpp")
+CLI = os.path.join(ROOT, "tools", "segconv_b200")
+
+
+def build_cli() -> str:
+    """The command-line caller (tools/segconv_b200.cpp: verify / bench / apply
+    over the drop-in C++ API), linked against the in-tree library; the
+    reference's bit-for-bit default math (EXACT), as its CLI's ops are."""
+    if os.path.exists(CLI) and os.path.getmtime(CLI) >= max(
+            os.path.getmtime(p) for p in (CLI_SRC, LIB, os.path.join(ROOT, "include", "segconv_b200.hpp"))):
+        return CLI
+    cmd = ["g++", "-std=c++17", "-O2", "-DSEGCONV_B200_DEFAULT_MATH=SEGCONV_MATH_EXACT",
+           "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include", CLI_SRC, "-o", CLI,
+           "-L" + PKG, "-lsegconv_b200", "-L/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath," + PKG,
+           "-Wl,-rpath,/usr/local/cuda/lib64"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"CLI build failed:\n{r.stderr}")
+    return CLI
 
 
 if __name__ == "__main__":
