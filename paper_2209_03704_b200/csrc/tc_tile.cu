@@ -42,6 +42,12 @@ using namespace tc;
 
 constexpr int NUM_THREADS = 320;
 constexpr int SMEM_LIMIT = 227 * 1024;
+// Two CTAs per SM: a tile's epilogue (TMEM drain -> SMEM tile -> shift sums,
+// two named barriers) is serial within a CTA, so a second CTA's MMA and loads
+// run under it (measured: C5 layer d at one CTA per SM spent ~3.6k cycles per
+// 128-pixel tile, issue slots 28 % busy)
+constexpr int CTAS_PER_SM = 2;
+constexpr int SMEM_PER_CTA = 113 * 1024;
 constexpr int KB = 64;  // bf16 channels per stage: one 128-byte row
 constexpr int MAX_STAGES = 8;
 constexpr int TILE = 128;
@@ -75,7 +81,7 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
 }
 
 template <int KH, int COUT, int ACT, typename YT>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
     tile_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmap) {
   using L = ScatterLayout<KH, COUT>;
   constexpr int U = L::U, N = L::N, TP = N + 1;  // SMEM tile pitch (floats)
@@ -420,7 +426,7 @@ static cudaError_t launch_tile_t(const FusedProblem& pr, const void* img, cudaSt
   p.stage_bytes = tct::TILE * 128;
   p.w_bytes = (int)tile_image_bytes(KH, pr.cin);
   const int fixed = p.w_bytes + (tct::TILE * (L::N + 1) + 2) * 4 + (2 * tct::MAX_STAGES + 5) * 8 + 16;
-  p.stages = std::min(tct::MAX_STAGES, (tct::SMEM_LIMIT - fixed) / p.stage_bytes);
+  p.stages = std::min(tct::MAX_STAGES, (tct::SMEM_PER_CTA - fixed) / p.stage_bytes);
   if (p.stages < 2) return cudaErrorNotSupported;
   static const int dbg = getenv("SEGCONV_TC_DEBUG") ? atoi(getenv("SEGCONV_TC_DEBUG")) : 0;
   p.debug = dbg;
@@ -448,7 +454,7 @@ static cudaError_t launch_tile_t(const FusedProblem& pr, const void* img, cudaSt
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorNotSupported;
   const int sms = device_sm_count();
-  const long long grid = std::min<long long>(p.tiles, sms);
+  const long long grid = std::min<long long>(p.tiles, (long long)tct::CTAS_PER_SM * sms);
   const size_t smem = (size_t)p.stages * p.stage_bytes + fixed;
   const int act = (pr.epi & SEGCONV_EPI_RELU) ? 1 : (pr.epi & SEGCONV_EPI_TANH) ? 2 : 0;
   cudaError_t e = cudaSuccess;
