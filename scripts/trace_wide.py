@@ -25,7 +25,9 @@ buf = np.zeros(160 * 16 * 64, dtype=np.uint64)
 A.lib().segconv_debug_trace(buf.ctypes.data_as(C.c_void_p), buf.nbytes)
 tr = buf.reshape(160, 16, 64).astype(np.int64)
 t0 = tr[tr > 0].min()
-for cta in (0, 2):
+import os
+ctas = [int(c) for c in os.environ.get("TRACE_CTAS", "0,2").split(",")]
+for cta in ctas:
     print("CTA", cta, sc.last_path())
     for u in range(20):
         row = tr[cta, :6, u]
