@@ -303,6 +303,13 @@ __device__ __forceinline__ bool unit_of(const Params& p, int k, long long& pt, i
   return true;
 }
 
+// 32-byte global store (sm_100 STG.E.256); the address must be 32-byte aligned
+__device__ __forceinline__ void st_global_v8(void* ptr, const uint32_t* w) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(ptr), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+               "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
+}
+
 template <int ACT>
 __device__ __forceinline__ float finish(float v, const float* bias, unsigned epi, int f) {
   if (epi & SEGCONV_EPI_BIAS) v += __ldg(bias + f);
@@ -850,9 +857,16 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                                              finish_bf<ACT>(v[2 * e + 1], p.bias, p.epi, f + 1));
               w[e] = *reinterpret_cast<const uint32_t*>(&h);
             }
-            uint4* o = reinterpret_cast<uint4*>(dst + c0);
+            if ((reinterpret_cast<uintptr_t>(dst + c0) & 31) == 0) {
+              // 256-bit stores (sm_100 STG.256): half the store instructions of
+              // the scattered per-anchor epilogue writes
 #pragma unroll
-            for (int e = 0; e < 4; ++e) o[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+              for (int e = 0; e < 2; ++e) st_global_v8(dst + c0 + 16 * e, &w[8 * e]);
+            } else {
+              uint4* o = reinterpret_cast<uint4*>(dst + c0);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) o[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+            }
           } else {
             float4* o = reinterpret_cast<float4*>(dst + c0);
 #pragma unroll
@@ -875,6 +889,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       tc_fence_before();
       __syncwarp();
+      if (threadIdx.x == 0 && rank == 0) trace_ev(p, 5, k);  // epilogue of the unit done (warp 0)
       if (lane == 0) mbar_arrive_cl(acc_empty_leader0 + (uint32_t)acc * 8);
       if (++acc == NACC) {
         acc = 0;
