@@ -95,6 +95,27 @@ __device__ __forceinline__ __nv_bfloat16 from_d<__nv_bfloat16>(double v) {
   return __float2bfloat16_rn((float)v);
 }
 
+// 32-byte global accesses (sm_100 STG.E.256 / LDG.E.256); the address must be
+// 32-byte aligned.  Epilogues writing one anchor's features per thread are
+// bound by the number of scattered store instructions, so wider is faster.
+__device__ __forceinline__ void st_global_v8(void* ptr, const uint32_t* w) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(ptr), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+               "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
+}
+__device__ __forceinline__ void st_global_v8f(float* ptr, const float* v) {
+  asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(ptr), "f"(v[0]), "f"(v[1]), "f"(v[2]),
+               "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void ld_global_v8f(const float* ptr, float* v) {
+  asm volatile("ld.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+               : "l"(ptr)
+               : "memory");
+}
+__device__ __forceinline__ bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; }
+
 // --------------------------------------------------------------- epilogue
 // Order: + bias[f], then ReLU or tanh (SEGCONV_EPI_* flags).
 __device__ __forceinline__ float epilogue_apply(float v, unsigned epi, const float* bias, int f) {

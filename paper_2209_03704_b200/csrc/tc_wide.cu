@@ -303,13 +303,6 @@ __device__ __forceinline__ bool unit_of(const Params& p, int k, long long& pt, i
   return true;
 }
 
-// 32-byte global store (sm_100 STG.E.256); the address must be 32-byte aligned
-__device__ __forceinline__ void st_global_v8(void* ptr, const uint32_t* w) {
-  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(ptr), "r"(w[0]), "r"(w[1]), "r"(w[2]),
-               "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
-               : "memory");
-}
-
 template <int ACT>
 __device__ __forceinline__ float finish(float v, const float* bias, unsigned epi, int f) {
   if (epi & SEGCONV_EPI_BIAS) v += __ldg(bias + f);
@@ -767,11 +760,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (!ok) continue;
         float4* o = reinterpret_cast<float4*>(dst + c0);
         if (p.w_direct && p.w_accumulate) {
+          if (aligned32(dst + c0)) {
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float4 a = o[e];
-            o[e] = make_float4(a.x + v[4 * e], a.y + v[4 * e + 1], a.z + v[4 * e + 2], a.w + v[4 * e + 3]);
+            for (int e = 0; e < 4; ++e) {
+              float a[8];
+              ld_global_v8f(dst + c0 + 8 * e, a);
+#pragma unroll
+              for (int u = 0; u < 8; ++u) a[u] += v[8 * e + u];
+              st_global_v8f(dst + c0 + 8 * e, a);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float4 a = o[e];
+              o[e] = make_float4(a.x + v[4 * e], a.y + v[4 * e + 1], a.z + v[4 * e + 2], a.w + v[4 * e + 3]);
+            }
           }
+        } else if (aligned32(dst + c0)) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) st_global_v8f(dst + c0 + 8 * e, &v[8 * e]);
         } else {
 #pragma unroll
           for (int e = 0; e < 8; ++e) o[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
@@ -857,7 +864,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                                                              finish_bf<ACT>(v[2 * e + 1], p.bias, p.epi, f + 1));
               w[e] = *reinterpret_cast<const uint32_t*>(&h);
             }
-            if ((reinterpret_cast<uintptr_t>(dst + c0) & 31) == 0) {
+            if (aligned32(dst + c0)) {
               // 256-bit stores (sm_100 STG.256): half the store instructions of
               // the scattered per-anchor epilogue writes
 #pragma unroll
@@ -868,14 +875,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               for (int e = 0; e < 4; ++e) o[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
             }
           } else {
-            float4* o = reinterpret_cast<float4*>(dst + c0);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int f = fbase + c0 + 4 * e;
-              o[e] = make_float4(finish<ACT>(v[4 * e], p.bias, p.epi, f),
-                                 finish<ACT>(v[4 * e + 1], p.bias, p.epi, f + 1),
-                                 finish<ACT>(v[4 * e + 2], p.bias, p.epi, f + 2),
-                                 finish<ACT>(v[4 * e + 3], p.bias, p.epi, f + 3));
+            for (int e = 0; e < 32; ++e) v[e] = finish<ACT>(v[e], p.bias, p.epi, fbase + c0 + e);
+            if (aligned32(dst + c0)) {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) st_global_v8f(reinterpret_cast<float*>(dst + c0 + 8 * e), &v[8 * e]);
+            } else {
+              float4* o = reinterpret_cast<float4*>(dst + c0);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) o[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
             }
           }
         } else {
