@@ -67,6 +67,27 @@ def test_fold_ts_split_fp16(batch, n, act):
     assert scaled_err(got, want_of(x, k, 0, act, b)) <= TOL_F32
 
 
+# other shapes the anchors-on-M fold kernel takes: cout < 32 (per-element
+# stores), cin = 32 (one stage per unit), p = 1 and k = 4 (other class / shift
+# sets: the column order search), bf16 output, bias + activation
+@pytest.mark.parametrize("batch,n,cin,cout,k,p,act,odt", [
+    (2, 33, 64, 20, 3, 0, "relu", None),
+    (3, 30, 32, 32, 3, 0, None, None),
+    (2, 31, 64, 32, 3, 1, "tanh", None),
+    (2, 24, 64, 24, 4, 1, None, None),
+    (2, 40, 64, 32, 3, 0, "relu", torch.bfloat16),
+])
+def test_fold_ts_shapes(batch, n, cin, cout, k, p, act, odt):
+    rng = np.random.default_rng(batch * 1000 + n * 10 + cout + k)
+    x = rng.uniform(-1, 1, (batch, n, n, cin)).astype(np.float32)
+    w = (rng.standard_normal((k, k, cin, cout)) * 0.06).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, cout).astype(np.float32) if act else None
+    got, path = run(x, w, p, "f16x3", act, b, out_dtype=odt)
+    assert path == "tc-fold-ts", path
+    want = want_of(x, w, p, act, b)
+    assert scaled_err(got, want) <= (1e-2 if odt is not None else TOL_F32)
+
+
 # ---- wide bf16 layers (C3, C5 a-c): CTA-pair kernel
 @pytest.mark.parametrize("batch,n,cin,cout,ks,act", [
     (4, 16, 512, 256, 4, None),   # C3 shape (reduced batch)
