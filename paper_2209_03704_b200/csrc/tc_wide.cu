@@ -111,6 +111,7 @@ struct Params {
   // features contiguous, pixels = K): A from a 2-D map over x, B from the
   // stride-2 im2col walk over gy.  Results go to wout (+ s * ksz when split).
   int mode;
+  int kstage;  // IM2COL forward: 64-channel k-blocks per pipeline stage (2 halves the handshakes)
   int w_kw, w_taps, w_ch_pairs, w_splits, w_cin, w_cout, w_direct, w_accumulate;
   int w_in_h, w_in_w;  // input map (anchor grid) of the kernel-gradient walk
   long long w_chunks, w_cps, w_ksz;
@@ -340,9 +341,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
+  const int kst = p.kstage > 0 ? p.kstage : 1;  // k-blocks per stage
   if (warp == 5 && lane == 0) {
+    // IM2COL forward: one barrier pair per stage for A and B (both producers
+    // arrive on a_full, both wait on a_empty) -- one wait and one commit per
+    // stage in the MMA issuer
+    const uint32_t full_count = (p.im2col && p.mode != 1 && p.bprod) ? 2u : 1u;
     for (int s = 0; s < SA; ++s) {
-      mbar_init(&a_full[s], 1);
+      mbar_init(&a_full[s], full_count);
       mbar_init(&a_empty[s], 1);
     }
     for (int s = 0; s < SB; ++s) {
@@ -442,6 +448,50 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           }
         }
       }
+    } else if (p.mode != 1 && p.im2col && p.bprod && !p.wres) {
+      // ===== IM2COL A producer, whole warp: the operands stay warp-uniform
+      // (uniform registers, no per-lane R2UR / single-lane issue loop) and one
+      // elected lane arrives and issues -- the single-lane form of this loop
+      // took ~300 cycles per stage, more than a stage of N = 128 MMAs
+      griddep_wait();
+      int sa = 0, gsa = 0;
+      uint32_t pa = 0;
+      long long pt;
+      int nt, q, hf;
+      for (int k = 0; unit_of(p, k, pt, nt, q, hf); ++k) {
+        const int R = p.rows[q], C = p.cols[q];
+        const long long a0 = pt * 256 + (long long)rank * 128;
+        const int ib = (int)(a0 / ((long long)R * C));
+        const int rem = (int)(a0 - (long long)ib * R * C);
+        const int i0 = rem / C, j0 = rem - (rem / C) * C;
+        const int xw = p.wscale * j0 + p.wbase_c, xh = p.wscale * i0 + p.wbase_r;
+        const CUtensorMap* map = &maps.xi[q];
+        const int taps = p.taps[q];
+        for (int pass = 0; pass < (p.split ? 3 : 1); ++pass)
+          for (int kb = 0; kb < p.nkb; ++kb) {
+            const int ca = kb * p.kbc * kst + (pass == 1 ? p.split_off : 0);  // A: xl on pass 1
+            for (int t = 0; t < taps; ++t) {
+              mbar_wait(&a_empty[sa], pa ^ 1);
+              if (lane == 0 && rank == 0) trace_ev(p, 10, gsa);
+              ++gsa;
+              if (elect_one()) {
+                const uint32_t af = mapa(smem_u32(&a_full[sa]), 0);
+                if (rank == 0)
+                  mbar_arrive_expect_tx(&a_full[sa], (p.debug & 32) ? 0u : 2u * 128 * 128 * (uint32_t)kst);
+                if (!(p.debug & 32))
+                  for (int j = 0; j < kst; ++j)
+                    tma2_load_im2col(smem_u32(a_base + (size_t)sa * p.a_stage_bytes) + (uint32_t)j * 16384u, map,
+                                     ca + j * p.kbc, xw, xh, ib, (uint16_t)p.tap_off_c[q][t],
+                                     (uint16_t)p.tap_off_r[q][t], af);
+              }
+              __syncwarp();
+              if (++sa == SA) {
+                sa = 0;
+                pa ^= 1;
+              }
+            }
+          }
+      }
     } else if (lane == 0 && p.mode != 1) {
       griddep_wait();  // activations come from the previous kernel (stack layer)
       int sa = 0, sb = 0;
@@ -458,6 +508,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       long long pt;
       int nt, q, hf;
+      int gsa = 0;  // trace: global stage index
       for (int k = 0; unit_of(p, k, pt, nt, q, hf); ++k) {
         const long long m0 = pt * 256 + (long long)rank * 128;
         const long long g = pt * 2 + rank;  // TILE2D: this CTA's row tile
@@ -479,8 +530,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const int ca = kb * p.kbc + (pass == 1 ? p.split_off : 0);  // A: xl on pass 1
               const int cb = kb * p.kbc + (pass == 2 ? p.split_off : 0);  // B: wl on pass 2
               mbar_wait(&a_empty[sa], pa ^ 1);
+              if (rank == 0) trace_ev(p, 10, gsa++);
               const uint32_t af = mapa(smem_u32(&a_full[sa]), 0);
-              if (rank == 0) mbar_arrive_expect_tx(&a_full[sa], 2 * 128 * 128);
+              if (rank == 0) mbar_arrive_expect_tx(&a_full[sa], (p.debug & 32) ? 0u : 2 * 128 * 128);
+              if (!(p.debug & 32))  // diagnostics: no activation loads
               tma2_load_im2col(smem_u32(a_base + (size_t)sa * p.a_stage_bytes), &maps.xi[q],
                                ca, p.wscale * j0 + p.wbase_c, p.wscale * i0 + p.wbase_r, ib,
                                (uint16_t)p.tap_off_c[q][t], (uint16_t)p.tap_off_r[q][t], af);
@@ -545,9 +598,48 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   } else if (warp == 6 && p.mode != 1) {
     // ===== IM2COL B producer (both CTAs): the weight tiles of every (pass, kb, tap)
     // step, in the A producer's order -- two serial issue chains instead of one
-    if (lane == 0 && p.bprod) {
+    if (p.im2col && p.bprod) {
+      // whole warp, one elected lane issues (see the A producer)
       griddep_wait();
-      int sb = 0;
+      int sb = 0, gsb = 0;
+      uint32_t pb = 0;
+      long long pt;
+      int nt, q, hf;
+      for (int k = 0; unit_of(p, k, pt, nt, q, hf); ++k) {
+        const int f0 = hf ? nt * p.NT + (hf - 1) * NT2 + (int)rank * (NT2 / 2) : nt * p.NT + (int)rank * NT2;
+        const CUtensorMap* map = &maps.w[q];
+        const int taps = p.taps[q];
+        for (int pass = 0; pass < (p.split ? 3 : 1); ++pass)
+          for (int kb = 0; kb < p.nkb; ++kb) {
+            const int cb = kb * p.kbc * kst + (pass == 2 ? p.split_off : 0);  // B: wl on pass 2
+            for (int t = 0; t < taps; ++t) {
+              // the stage's A and B share a_full / a_empty (SA == SB, lockstep)
+              mbar_wait(&a_empty[sb], pb ^ 1);
+              if (lane == 0 && rank == 0) trace_ev(p, 11, gsb);
+              ++gsb;
+              if (elect_one()) {
+                const uint32_t bf = mapa(smem_u32(&a_full[sb]), 0);
+                if (rank == 0) mbar_arrive_expect_tx(&a_full[sb], (p.debug & 16) ? 0u : 2 * b_tx * (uint32_t)kst);
+                const uint32_t dst = smem_u32(b_base + (size_t)sb * p.b_stage_bytes);
+                if (!(p.debug & 16))
+                  for (int j = 0; j < kst; ++j) {
+                    if (p.b_tap_last)
+                      tma2_load_3d(dst + (uint32_t)j * b_tx, map, cb + j * p.kbc, f0, t, bf);
+                    else
+                      tma2_load_3d(dst + (uint32_t)j * b_tx, map, cb + j * p.kbc, t, f0, bf);
+                  }
+              }
+              __syncwarp();
+              if (++sb == SB) {
+                sb = 0;
+                pb ^= 1;
+              }
+            }
+          }
+      }
+    } else if (lane == 0 && p.bprod) {
+      griddep_wait();
+      int sb = 0, gsb = 0;
       uint32_t pb = 0;
       long long pt;
       int nt, q, hf;
@@ -572,9 +664,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           for (int kb = 0; kb < p.nkb; ++kb)
             for (int t = 0; t < p.taps[q]; ++t) {
               const int cb = kb * p.kbc + (pass == 2 ? p.split_off : 0);  // B: wl on pass 2
-              mbar_wait(&b_empty[sb], pb ^ 1);
-              const uint32_t bf = mapa(smem_u32(&b_full[sb]), 0);
-              if (rank == 0) mbar_arrive_expect_tx(&b_full[sb], 2 * b_tx);
+              // the stage's A and B share a_full / a_empty (SA == SB, lockstep)
+              mbar_wait(&a_empty[sb], pb ^ 1);
+              if (rank == 0) trace_ev(p, 11, gsb++);
+              const uint32_t bf = mapa(smem_u32(&a_full[sb]), 0);
+              if (rank == 0) mbar_arrive_expect_tx(&a_full[sb], (p.debug & 16) ? 0u : 2 * b_tx);
+              if (p.debug & 16) {  // diagnostics: no weight loads
+                if (++sb == SB) {
+                  sb = 0;
+                  pb ^= 1;
+                }
+                continue;
+              }
               if (p.b_tap_last)
                 tma2_load_3d(smem_u32(b_base + (size_t)sb * p.b_stage_bytes), &maps.w[q], cb, f0, t, bf);
               else
@@ -640,6 +741,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       long long pt;
       int nt, q, hf;
       const uint32_t idesc_full = idesc_f16_m256(p.ab_fmt, p.NT), idesc_half = idesc_f16_m256(p.ab_fmt, p.NT / 2);
+      int gst = 0;  // trace: global stage index
       if (p.wres && blockIdx.x / 2 < p.units) {  // resident weight tiles
         mbar_wait(&b_full[0], 0);
         tc_fence_after();
@@ -654,42 +756,59 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         // only a third of the non-round-to-nearest accumulation steps
         const uint32_t d = tb + (uint32_t)(acc * p.NT * (p.split ? 2 : p.allq ? 4 : 1));
         if (p.im2col) {
-          for (int pass = 0; pass < (p.split ? 3 : 1); ++pass)
-          for (int kb = 0; kb < p.nkb; ++kb)
-            for (int t = 0; t < p.taps[q]; ++t) {
-              mbar_wait(&a_full[sa], pa);
-              mbar_wait(&b_full[sb], pb);
-              tc_fence_after();
-              const uint64_t ad = sw128_desc(smem_u32(a_base + (size_t)sa * p.a_stage_bytes));
-              const uint64_t bd = sw128_desc(smem_u32(b_base + (size_t)sb * p.b_stage_bytes));
-              const uint32_t ds = d + (pass > 0 ? (uint32_t)p.NT : 0u);
-              const bool first = (pass <= 1) && kb == 0 && t == 0;
-              if (elect_one()) {
-                if (p.tf32) {
+          // Tight issue loop -- one barrier wait, the stage's MMAs, one commit,
+          // descriptors advanced by constant strides.  A warp-uniform issue
+          // loop costs ~370 cycles per stage before any MMA (wait 80, commit
+          // 70, loop / elect / syncwarp ~220: scripts/mma2_bench.cu) and the
+          // tensor pipe queues only about one MMA ahead, so a stage must hold
+          // more MMA time than that: four N = 256 MMAs (512 cycles) do, four
+          // N = 128 ones (276) do not -- hence two k-blocks per stage (kst).
+          const int per_pass = p.nkb * p.taps[q];
+          const int nst = (p.split ? 3 : 1) * per_pass;
+          const uint64_t ad0 = sw128_desc(smem_u32(a_base)), bd0 = sw128_desc(smem_u32(b_base));
+          const uint32_t astep = (uint32_t)p.a_stage_bytes >> 4, bstep = (uint32_t)p.b_stage_bytes >> 4;
+          int in_pass = 0, pass = 0;
+          for (int s = 0; s < nst; ++s) {
+            mbar_wait(&a_full[sa], pa);
+            tc_fence_after();
+            if (lane == 0) trace_ev(p, 6, gst);
+            const uint64_t ad = ad0 + (uint64_t)((uint32_t)sa * astep);
+            const uint64_t bd = bd0 + (uint64_t)((uint32_t)sa * bstep);
+            const uint32_t ds = d + (pass > 0 ? (uint32_t)p.NT : 0u);
+            const uint32_t acc0 = (pass <= 1 && in_pass == 0) ? 0u : 1u;
+            if (elect_one()) {
+              if (p.debug & 8) {  // diagnostics: no MMAs
+              } else if (p.tf32) {
 #pragma unroll
-                  for (int ks = 0; ks < 4; ++ks)  // 4 x (K = 8 fp32) = one 128-byte row
-                    mma2_tf32(ds, ad + 2u * ks, bd + 2u * ks, idesc, (first && ks == 0) ? 0u : 1u);
-                } else {
+                for (int ks = 0; ks < 4; ++ks)  // 4 x (K = 8 fp32) = one 128-byte row
+                  mma2_tf32(ds, ad + 2u * ks, bd + 2u * ks, idesc, ks == 0 ? acc0 : 1u);
+              } else if (kst == 2) {
+                // two 64-channel blocks: A 16 KB, B b_tx apart
 #pragma unroll
-                  for (int ks = 0; ks < KB / 16; ++ks)
-                    mma2_bf16(ds, ad + 2u * ks, bd + 2u * ks, idesc, (first && ks == 0) ? 0u : 1u);
-                }
+                for (int ks = 0; ks < KB / 16; ++ks)
+                  mma2_bf16(ds, ad + 2u * ks, bd + 2u * ks, idesc, ks == 0 ? acc0 : 1u);
+#pragma unroll
+                for (int ks = 0; ks < KB / 16; ++ks)
+                  mma2_bf16(ds, ad + (16384u >> 4) + 2u * ks, bd + (b_tx >> 4) + 2u * ks, idesc, 1u);
+              } else {
+#pragma unroll
+                for (int ks = 0; ks < KB / 16; ++ks)
+                  mma2_bf16(ds, ad + 2u * ks, bd + 2u * ks, idesc, ks == 0 ? acc0 : 1u);
               }
-              __syncwarp();
-              if (elect_one()) {
-                commit2(&a_empty[sa]);
-                commit2(&b_empty[sb]);
-              }
-              __syncwarp();
-              if (++sa == SA) {
-                sa = 0;
-                pa ^= 1;
-              }
-              if (++sb == SB) {
-                sb = 0;
-                pb ^= 1;
-              }
+              commit2(&a_empty[sa]);
             }
+            __syncwarp();
+            if (lane == 0) trace_ev(p, 8, gst);
+            ++gst;
+            if (++sa == SA) {
+              sa = 0;
+              pa ^= 1;
+            }
+            if (++in_pass == per_pass) {
+              in_pass = 0;
+              ++pass;
+            }
+          }
         } else
         for (int kb = 0; kb < p.nkb; ++kb) {
           mbar_wait(&a_full[sa], pa);
@@ -844,7 +963,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const int fmax = p.cout - fbase;  // features of this tile that exist
       const float osc = p.split ? __ldg(p.split_inv_scale) : 1.0f;
 #pragma unroll 1
-      for (int c0 = 0; c0 < (hf ? p.NT / 2 : p.NT); c0 += 32) {
+      for (int c0 = 0; c0 < ((p.debug & 4) ? 0 : hf ? p.NT / 2 : p.NT); c0 += 32) {  // 4: diagnostics, no epilogue
         float v[32];
         tmem_ld32(lane_base + cbase + (uint32_t)c0, v);
         if (p.split) {
@@ -1147,6 +1266,16 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
   const int bar_bytes = (2 * tcw::MAX_STAGES_A + 2 * tcw::MAX_STAGES_B + 4) * 8 + 16;
   const int budget = tcw::SMEM_LIMIT - bar_bytes;
   if (p.im2col) {  // A and B both per (k-block, tap): paired rings
+    // two 64-channel k-blocks per stage where cin allows: the producer / MMA
+    // handshake costs a few hundred cycles per stage whatever its size, as
+    // much as a stage of N = 128 MMAs (measured: the empty pipeline alone,
+    // no loads / MMAs / epilogue, takes 27 us for C5 layer c at one k-block
+    // per stage)
+    p.kstage = (!split && !tf32 && p.mode == 0 && pr.cin % (2 * tcw::KB) == 0 &&
+                2 * (p.a_stage_bytes + p.b_stage_bytes) * 3 <= budget) ? 2 : 1;
+    p.nkb = pr.cin / (p.kbc * p.kstage);
+    p.a_stage_bytes *= p.kstage;
+    p.b_stage_bytes *= p.kstage;
     p.stages_a = p.stages_b = std::min(tcw::MAX_STAGES_A, budget / (p.a_stage_bytes + p.b_stage_bytes));
     if (p.stages_a < 2) return false;
   } else if (p.wres) {  // one "stage" holding every weight tile, A ring in the rest

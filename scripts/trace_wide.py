@@ -34,3 +34,26 @@ for cta in ctas:
         if not row.any():
             break
         print(f"  unit {u}: " + " ".join(f"ev{e}={(v - t0) / 1000:7.2f}" for e, v in enumerate(row) if v))
+
+# per stage (im2col path, CTA 0): 10 A producer slot free, 11 B producer slot free, 6 MMA saw data, 8 MMA committed
+if os.environ.get("TRACE_STAGES"):
+    print("stage: A slot free / B slot free / MMA data ready / committed (us)")
+    for g in range(64):
+        row = [tr[0, e, g] for e in (10, 11, 6, 8)]
+        if not row[2]:
+            break
+        print("  g=%2d " % g + " ".join(f"{(v - t0) / 1000:7.2f}" if v else "   -   " for v in row))
+
+# start / end of every CTA (unit 0 MMA start, last epilogue end): a second wave
+# of clusters shows as CTAs that start when others finish
+if os.environ.get("TRACE_WAVES"):
+    st, en = [], []
+    for cta in range(160):
+        row = tr[cta]
+        if not row[2].any():
+            continue
+        st.append((row[2][row[2] > 0].min() - t0) / 1000)
+        en.append((row[5][row[5] > 0].max() - t0) / 1000 if row[5].any() else 0)
+    st, en = np.array(st), np.array(en)
+    print(f"CTAs with events {len(st)}; start min {st.min():.2f} max {st.max():.2f}; end min {en.min():.2f} max {en.max():.2f}")
+    print("starts sorted:", np.round(np.sort(st), 2)[-20:])
