@@ -14,3 +14,7 @@ for c in C5 C2 C4 C3 C1; do
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/r02/launches_$c.csv python bench.py --config $c --steps 2 --warmup 3 --no-baselines --no-e2e --no-parity > /dev/null 2>&1; echo launches $c=$?
 done
+# full captures of the pair kernel (layers a and c of the C5 stack) after the
+# im2col pipeline changes
+bash scripts/gpu_ncu2.sh c5a_r02b wide_kernel 3 -- --config C5a; mv gpurun_out/*_c5a_r02b.* gpurun_out/r02/ 2>/dev/null
+bash scripts/gpu_ncu2.sh c5c_r02b wide_kernel 3 -- --config C5c; mv gpurun_out/*_c5c_r02b.* gpurun_out/r02/ 2>/dev/null
