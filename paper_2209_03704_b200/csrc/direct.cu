@@ -438,28 +438,55 @@ static cudaError_t run_tiled_t(const FusedProblem& pr, cudaStream_t s) {
 // MACs (BASELINE C1: 1 x 32^2 x 1 -> 61^2 x 1) the tiled kernels' staging
 // is pure latency; this is one global read per tap.
 template <typename TX, typename TW>
-__global__ void __launch_bounds__(256) tconv_outputs(const FusedProblem pr, long long total) {
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) tconv_outputs(const FusedProblem pr, int total) {
+  // one thread per output (tiny layers, e.g. BASELINE C1: 3721 outputs of 1
+  // channel).  The class's taps are unrolled (<= 4 x 4 for kh <= 7) so that
+  // their loads issue back to back: after an L2 flush each is a DRAM round
+  // trip, and a runtime tap loop serialised them (6.3 us for C1).  32-bit
+  // index math (total < 2^16 outputs).
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= total) return;
-  const int f = (int)(e % pr.cout);
-  long long t = e / pr.cout;
-  const int ox = (int)(t % pr.out_w);
+  const int f = e % pr.cout;
+  int t = e / pr.cout;
+  const int ox = t % pr.out_w;
   t /= pr.out_w;
-  const int oy = (int)(t % pr.out_h);
-  const int b = (int)(t / pr.out_h);
+  const int oy = t % pr.out_h;
+  const int b = t / pr.out_h;
   const int r = oy & 1, c = ox & 1, q = r * 2 + c, i = oy >> 1, j = ox >> 1;
   const TX* __restrict__ x = (const TX*)pr.x;
   const TW* __restrict__ w = (const TW*)pr.panels + pr.cls.sub_offset[q];
-  const int kw = pr.cls.kw[q];
+  const int kh = pr.cls.kh[q], kw = pr.cls.kw[q], n = pr.n, cin = pr.cin, cout = pr.cout;
+  const int r0 = i + pr.cls.off_r[q] - pr.pf, c0 = j + pr.cls.off_c[q] - pr.pf;
   float acc = 0.0f;
-  for (int u = 0; u < pr.cls.kh[q]; ++u) {
-    const int gr = i + pr.cls.off_r[q] + u - pr.pf;
-    for (int v = 0; v < kw; ++v) {
-      const int gc = j + pr.cls.off_c[q] + v - pr.pf;
-      if (gr < 0 || gr >= pr.n || gc < 0 || gc >= pr.n) continue;  // zero padding
-      const TX* xp = x + (((long long)b * pr.n + gr) * pr.n + gc) * pr.cin;
-      const TW* wp = w + ((long long)(u * kw + v) * pr.cin) * pr.cout + f;
-      for (int ch = 0; ch < pr.cin; ++ch) acc = fmaf(to_acc(xp[ch]), to_acc(wp[(long long)ch * pr.cout]), acc);
+  if (cin == 1) {
+    float xv[4][4], wv[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int gr = r0 + u, gc = c0 + v;
+        const bool ok = u < kh && v < kw && gr >= 0 && gr < n && gc >= 0 && gc < n;  // zero padding
+        xv[u][v] = ok ? to_acc(x[(b * n + gr) * n + gc]) : 0.0f;
+        wv[u][v] = ok ? to_acc(w[(u * kw + v) * cout + f]) : 0.0f;
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)  // reference order: u, v
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        if (u < kh && v < kw) acc = fmaf(xv[u][v], wv[u][v], acc);
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (u >= kh) break;
+      const int gr = r0 + u;
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int gc = c0 + v;
+        if (v >= kw || gr < 0 || gr >= n || gc < 0 || gc >= n) continue;  // zero padding
+        const TX* xp = x + ((long long)(b * n + gr) * n + gc) * cin;
+        const TW* wp = w + ((long long)(u * kw + v) * cin) * cout + f;
+        for (int ch = 0; ch < cin; ++ch) acc = fmaf(to_acc(xp[ch]), to_acc(wp[(long long)ch * cout]), acc);
+      }
     }
   }
   store_out(pr.y, e, epilogue_apply(acc, pr.epi, pr.bias, f), pr.y_dtype);
@@ -475,7 +502,7 @@ cudaError_t launch_direct_tiled(const FusedProblem& pr, cudaStream_t s) {
   if (pr.panel_layout != SEGCONV_PANEL_REF) return cudaErrorNotSupported;
   if (tiny_layer(pr) && ((pr.x_dtype == SEGCONV_F32 && pr.panel_dtype == SEGCONV_F32) ||
                          (pr.x_dtype == SEGCONV_BF16 && pr.panel_dtype == SEGCONV_BF16))) {
-    const long long total = (long long)pr.batch * pr.out_h * pr.out_w * pr.cout;
+    const int total = (int)((long long)pr.batch * pr.out_h * pr.out_w * pr.cout);  // <= 2^16 (tiny_layer)
     if (total == 0) return cudaSuccess;
     const unsigned blocks = (unsigned)((total + 255) / 256);
     if (pr.x_dtype == SEGCONV_F32)
