@@ -95,6 +95,8 @@ def test_fold_ts_shapes(batch, n, cin, cout, k, p, act, odt):
     (2, 7, 256, 128, 3, "relu"),   # C5 layer c
     (5, 5, 512, 256, 3, None),     # odd image, partial pair tile
     (2, 9, 64, 96, 4, "tanh"),     # cout not a multiple of 64, single k-block
+    (2, 6, 192, 128, 3, "relu"),   # cin % 128 != 0: one k-block per pipeline stage
+    (3, 6, 128, 128, 3, None),     # two k-blocks per stage, a single stage per tap
 ])
 def test_pair_kernel_bf16(batch, n, cin, cout, ks, act):
     rng = np.random.default_rng(batch * 7 + n + cin)
@@ -422,3 +424,26 @@ def test_pair_kernel_bf16_output_tanh(n, cin, cout, p):
     got, path = run(x, k, p, "bf16", "tanh")
     assert path == "tc-pair"
     assert scaled_err(got, want_of(x, k, p, "tanh")) <= TOL_TC
+
+
+# ---- tiny layers (BASELINE C1 family): one thread per output, unrolled class taps
+@pytest.mark.parametrize("batch,n,cin,cout,k,p,dt", [
+    (1, 32, 1, 1, 3, 0, torch.float32),   # C1
+    (3, 17, 1, 2, 7, 2, torch.float32),   # 4 x 4 taps per class, padding
+    (2, 12, 2, 3, 5, 1, torch.float32),   # cin > 1: the channel-loop form
+    (2, 20, 1, 1, 4, 1, torch.bfloat16),  # bf16 storage
+])
+def test_tiny_layer_kernel(batch, n, cin, cout, k, p, dt):
+    rng = np.random.default_rng(n * 10 + k + cin)
+    x = rng.uniform(-1, 1, (batch, n, n, cin)).astype(np.float32)
+    w = rng.uniform(-1, 1, (k, k, cin, cout)).astype(np.float32)
+    if dt == torch.bfloat16:
+        x, w = oracle.bf16_round(x), oracle.bf16_round(w)
+    g = sc.tconv_geometry(n, k, k, p)
+    sks = sc.segregate(torch.from_numpy(w).cuda().to(dt), p, math="ffma")
+    y = sc.transpose_conv_fused(torch.from_numpy(x).cuda().to(dt), sks, g, math="ffma")
+    torch.cuda.synchronize()
+    assert sc.last_path() == "simt-tiled", sc.last_path()
+    want = oracle.tconv_fused(x, w, p)
+    tol = 1e-2 if dt == torch.bfloat16 else 1e-5
+    assert scaled_err(y.float().cpu().numpy(), want) <= tol
