@@ -608,6 +608,7 @@ def run_reference(args, cfg, world):
     name = args.config
     rng = np.random.default_rng(SEED)
     times, par_times = [], []
+    extra_times = {}  # sequential op, conventional naive path: (seconds, images)
     bwd = args.pass_ == "backward"
     if cfg.get("stack"):
         specs = stack_specs(cfg)
@@ -637,6 +638,8 @@ def run_reference(args, cfg, world):
         if kind == "reference":  # the reference's own threading, a bounded sample
             npar = min(nimg, 4)
             par_times.append((chain(0, workers, npar), npar))
+            extra_times["sequential"] = (chain(1, 1, 1), 1)
+            extra_times["naive"] = (chain(2, workers, min(nimg, workers)), min(nimg, workers))
     else:
         b, n, cin, cout, k, p = (cfg[x] for x in ("batch", "n", "cin", "cout", "k", "p"))
         nimg = min(b, max(1, 2 * workers))
@@ -671,6 +674,11 @@ def run_reference(args, cfg, world):
             npar = min(nimg, 4)
             _, secs = oracle.ref_time_fused_batch(0, x[:npar], kk, p, workers)
             par_times.append((secs, npar))
+            _, secs = oracle.ref_time_fused_batch(1, x[:1], kk, p, 1)
+            extra_times["sequential"] = (secs, 1)
+            nn = min(nimg, workers)
+            _, secs = oracle.ref_time_fused_batch(2, x[:nn], kk, p, workers)
+            extra_times["naive"] = (secs, nn)
     sec = statistics.median(times)
     val = macs / sec / 1e9
     sample = (f"{nimg} of {cfg['batch']} images per step, harness batch-threading over the "
@@ -688,6 +696,17 @@ def run_reference(args, cfg, world):
             "value": round(macs / nimg * npar / secs / 1e9, 4), "unit": "useful GMAC/s",
             "what": f"the reference's own transpose_conv_fused_parallel({workers} workers; threads over "
                     f"cout slices, capped at cout) per image, {npar} images"}
+    if "sequential" in extra_times:
+        secs, ni = extra_times["sequential"]
+        cpu["reference_sequential"] = {
+            "value": round(macs / nimg * ni / secs / 1e9, 4), "unit": "useful GMAC/s",
+            "what": "the reference's sequential transpose_conv_fused on one thread, 1 image"}
+    if "naive" in extra_times:
+        secs, ni = extra_times["naive"]
+        cpu["reference_naive"] = {
+            "value": round(macs / nimg * ni / secs / 1e9, 4), "unit": "useful GMAC/s (the fused op's MACs)",
+            "what": f"the conventional transpose_conv_naive (upsample + pad + valid conv, 4x the MACs), "
+                    f"{ni} images across {workers} threads"}
     out = {"metric": METRIC + (" [backward pass]" if bwd else ""),
            "value": round(val, 4), "unit": "useful GMAC/s", "impl": "reference",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

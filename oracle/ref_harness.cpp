@@ -297,7 +297,10 @@ int ref_verify_case(uint64_t seed, int want, int dims[5], float* x_out, float* k
 // mode 0: loop images through transpose_conv_fused_parallel(workers) (the
 //         reference's own threading: contiguous cout slices, capped at cout);
 // mode 1: harness-level batch threading -- `workers` threads each run the
-//         reference's sequential transpose_conv_fused on whole images.
+//         reference's sequential transpose_conv_fused on whole images
+//         (workers = 1: the sequential op alone);
+// mode 2: as mode 1 with the conventional transpose_conv_naive
+//         (reference_ops.hpp:116-133: upsample + pad + valid conv).
 // Segregation happens outside the timed region (proj/include/segconv/bench.hpp:83).
 // Returns wall seconds in *seconds.
 int ref_time_fused_batch_f32(int mode, const float* x, int batch, int n, int cin, const float* k,
@@ -322,7 +325,8 @@ int ref_time_fused_batch_f32(int mode, const float* x, int batch, int n, int cin
       std::atomic<int> next{0};
       auto work = [&] {
         for (int b = next++; b < batch; b = next++) {
-          const auto y = segconv::transpose_conv_fused(ins[b], sks, geom);
+          const auto y = mode == 2 ? segconv::transpose_conv_naive(ins[b], kk, p)
+                                   : segconv::transpose_conv_fused(ins[b], sks, geom);
           std::memcpy(out + b * osz, y.data(), osz * sizeof(float));
         }
       };
