@@ -328,6 +328,30 @@ class LayerBackward(Layer):
         return {"max_scaled_err": scaled_err(got, wx), "tol": tol, "images": idx,
                 "what": "input gradient", "oracle": "oracle.tconv_backward (C port, pinned)"}
 
+    def f16x3_leg(self, torch, steps, flush):
+        """fp32 layers: the same step with math="f16x3" (input gradient on the
+        tensor cores in split-fp16 math where the shape allows, kernel gradient
+        FFMA), timed like the main line, with its input-gradient parity."""
+        import oracle
+        ts = []
+        for i in range(steps + 2):
+            flush()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            gx, _ = self.sc.transpose_conv_fused_backward(self.xd, self.kd, self.cfg["p"], self.gyd, math="f16x3")
+            b.record()
+            b.synchronize()
+            if i >= 2:
+                ts.append(a.elapsed_time(b))
+        path = self.sc.last_path()
+        idx = sorted({0, self.cfg["batch"] - 1})
+        wx, _ = oracle.tconv_backward(self.x_host[idx], self.k_host, self.cfg["p"], self.gy_host[idx])
+        err = scaled_err(gx[idx].float().cpu().numpy(), wx)
+        ms = statistics.median(ts)
+        return {"ms": round(ms, 5), "value": round(self.macs / (ms * 1e-3) / 1e9, 2), "unit": "useful GMAC/s",
+                "path": path, "parity": {"max_scaled_err": err, "tol": 1e-5, "images": idx},
+                "what": "math=\"f16x3\": opt-in; AUTO keeps FFMA for the fp32 backward"}
+
     def step_e2e(self):
         """Public API from host buffers: x and gy uploaded, both gradients read back."""
         xd = self.x_pinned.to(self.xd.device, non_blocking=True)
@@ -1029,6 +1053,11 @@ def main():
                 extra["cudnn_conv_transpose2d_backward"] = extra.pop("cudnn_conv_transpose2d")
                 if "cudnn_conv_transpose2d_tf32" in extra:
                     extra["cudnn_conv_transpose2d_backward_tf32"] = extra.pop("cudnn_conv_transpose2d_tf32")
+                if fp32:
+                    try:
+                        extra["f16x3_backward"] = prob.f16x3_leg(torch, 10, flush)
+                    except Exception as e:
+                        extra["f16x3_backward"] = {"error": str(e)[:200]}
             workers = os.cpu_count() or 1
             try:
                 secs, nimg, kind = prob.cpu_sample(workers)

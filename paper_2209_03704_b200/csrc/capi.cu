@@ -596,6 +596,12 @@ static segconv_status run_backward(const BackwardProblem& pr, segconv_math math,
       dpath = "tc-pair";
       snprintf(msg, sizeof msg, "%s[input, tcgen05 pair]", what);
       st = cuda_status(launch_tc_bwd_data(pr, s), msg);
+    } else if (math == SEGCONV_MATH_F16X3 && tc_bwd_data_split_supported(pr)) {
+      // fp32 in split-fp16 math: K = taps x 2 cout x 2 copies / 16 accumulation
+      // steps (C2: 72), well inside the tensor-core accumulation bound (§5)
+      dpath = "tc-pair-split";
+      snprintf(msg, sizeof msg, "%s[input, tcgen05 pair, split fp16]", what);
+      st = cuda_status(launch_tc_bwd_data_split(pr, s), msg);
     } else {
       dpath = exact ? "simt-exact" : bwd_narrow_applies(pr) ? "simt-narrow" : "simt-ffma";
       snprintf(msg, sizeof msg, "%s[input]", what);
@@ -645,7 +651,10 @@ segconv_status segconv_transpose_conv_fused_backward(const void* d_x, const void
     return fail(SEGCONV_E_CONTRACT, "EXACT math is defined for float and double (the reference's types)");
   if (math == SEGCONV_MATH_BF16 && dtype != SEGCONV_BF16)
     return fail(SEGCONV_E_CONTRACT, "BF16 math needs bf16 tensors");
-  if (math != SEGCONV_MATH_EXACT && math != SEGCONV_MATH_FFMA && math != SEGCONV_MATH_BF16)
+  if (math == SEGCONV_MATH_F16X3 && dtype != SEGCONV_F32)
+    return fail(SEGCONV_E_CONTRACT, "F16X3 math needs fp32 tensors");
+  if (math != SEGCONV_MATH_EXACT && math != SEGCONV_MATH_FFMA && math != SEGCONV_MATH_BF16 &&
+      math != SEGCONV_MATH_F16X3)
     return fail(SEGCONV_E_UNSUPPORTED, "math mode %d has no backward kernels in this build", (int)math);
 
   BackwardProblem pr{};

@@ -56,6 +56,9 @@ bool bwd_narrow_applies(const BackwardProblem& pr);
 cudaError_t launch_bwd_data_simt(const BackwardProblem& pr, bool exact, cudaStream_t s);
 cudaError_t launch_bwd_weight_simt(const BackwardProblem& pr, bool exact, cudaStream_t s);
 bool tc_bwd_data_supported(const BackwardProblem& pr);
+// fp32 input gradient in split-fp16 math (f16x3) on the pair kernel (tc_wide.cu)
+bool tc_bwd_data_split_supported(const BackwardProblem& pr);
+cudaError_t launch_tc_bwd_data_split(const BackwardProblem& pr, cudaStream_t s);
 cudaError_t launch_tc_bwd_data(const BackwardProblem& pr, cudaStream_t s);
 bool tc_bwd_weight_supported(const BackwardProblem& pr);
 bool tc_conv_valid_supported(int batch, int h, int w, int cin, int kh, int kw, int cout);

@@ -101,6 +101,7 @@ struct Params {
   int split, split_off;
   uint32_t ab_fmt;  // MMA operand format: 1 bf16, 0 fp16
   const float* split_inv_scale;  // SPLIT: the weights were scaled by 2^s; sums are multiplied by 2^-s
+  int oscale;  // multiply the sums by *split_inv_scale without SPLIT's three passes (split-fp16 input gradient)
   // TF32 (fp32 data, math = tf32): fp32 operands, kind::tf32 MMAs (K = 8 per
   // instruction -- the same 32 bytes per step), 32 channels per 128-byte row
   int tf32;
@@ -112,6 +113,7 @@ struct Params {
   // stride-2 im2col walk over gy.  Results go to wout (+ s * ksz when split).
   int mode;
   int kstage;  // IM2COL forward: 64-channel k-blocks per pipeline stage (2 halves the handshakes)
+  int a_share;  // the stage's k-blocks multiply one A box (split-fp16 input gradient: [hi | lo] x two B halves)
   int w_kw, w_taps, w_ch_pairs, w_splits, w_cin, w_cout, w_direct, w_accumulate;
   int w_in_h, w_in_w;  // input map (anchor grid) of the kernel-gradient walk
   long long w_chunks, w_cps, w_ksz;
@@ -476,10 +478,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               ++gsa;
               if (elect_one()) {
                 const uint32_t af = mapa(smem_u32(&a_full[sa]), 0);
+                const int ka = p.a_share ? 1 : kst;  // A boxes per stage
                 if (rank == 0)
-                  mbar_arrive_expect_tx(&a_full[sa], (p.debug & 32) ? 0u : 2u * 128 * 128 * (uint32_t)kst);
+                  mbar_arrive_expect_tx(&a_full[sa], (p.debug & 32) ? 0u : 2u * 128 * 128 * (uint32_t)ka);
                 if (!(p.debug & 32))
-                  for (int j = 0; j < kst; ++j)
+                  for (int j = 0; j < ka; ++j)
                     tma2_load_im2col(smem_u32(a_base + (size_t)sa * p.a_stage_bytes) + (uint32_t)j * 16384u, map,
                                      ca + j * p.kbc, xw, xh, ib, (uint16_t)p.tap_off_c[q][t],
                                      (uint16_t)p.tap_off_r[q][t], af);
@@ -789,7 +792,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   mma2_bf16(ds, ad + 2u * ks, bd + 2u * ks, idesc, ks == 0 ? acc0 : 1u);
 #pragma unroll
                 for (int ks = 0; ks < KB / 16; ++ks)
-                  mma2_bf16(ds, ad + (16384u >> 4) + 2u * ks, bd + (b_tx >> 4) + 2u * ks, idesc, 1u);
+                  mma2_bf16(ds, ad + (p.a_share ? 0u : (16384u >> 4)) + 2u * ks, bd + (b_tx >> 4) + 2u * ks, idesc, 1u);
               } else {
 #pragma unroll
                 for (int ks = 0; ks < KB / 16; ++ks)
@@ -961,7 +964,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     p.cout +
                 fbase;
       const int fmax = p.cout - fbase;  // features of this tile that exist
-      const float osc = p.split ? __ldg(p.split_inv_scale) : 1.0f;
+      const float osc = (p.split || p.oscale) ? __ldg(p.split_inv_scale) : 1.0f;
 #pragma unroll 1
       for (int c0 = 0; c0 < ((p.debug & 4) ? 0 : hf ? p.NT / 2 : p.NT); c0 += 32) {  // 4: diagnostics, no epilogue
         float v[32];
@@ -971,6 +974,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           tmem_ld32(lane_base + (uint32_t)(acc * p.NT * 2 + p.NT + c0), w2);
 #pragma unroll
           for (int e = 0; e < 32; ++e) v[e] = (v[e] + w2[e]) * osc;  // scale: exact power of two
+        } else if (p.oscale) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] *= osc;
         }
         if (!ok || c0 >= fmax) continue;
         if (c0 + 32 <= fmax) {
@@ -1382,12 +1388,21 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
 // tap offset (kh-1-U, kw-1-V); positions outside gy are zero-filled by the TMA),
 // B = the original kernel, whose (U, V, ch, f) layout is already K-major for
 // N = ch -- no flipped or re-laid-out copy is made.
-static bool make_wide_dgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps& maps) {
+// Input gradient on the pair kernel (stride-2 im2col walk over gy).  bf16: gy
+// and the kernel as they are.  Split fp16 (fp32 data, f16x3, cout = 32):
+// gy16 = gy's [hi | lo] halves as 64 channels (scaled by 2^t) and per tap
+// w2 = [wh | wh | wl | 0] (scaled by 2^s): one stage per tap multiplies its A
+// box by both 64-channel B halves, gh.wh + gl.wh + gh.wl; gx = 2^-s-t (sum).
+static bool make_wide_dgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps& maps,
+                            const void* gy16 = nullptr, const void* w2 = nullptr) {
   p = tcw::Params{};
-  p.ab_fmt = 1;  // bf16 operands
+  const bool split = gy16 != nullptr;
+  p.ab_fmt = split ? 0 : 1;  // fp16 / bf16 operands
   p.kbc = tcw::KB;
-  if (pr.dtype != SEGCONV_BF16) return false;
-  if (pr.cout % tcw::KB != 0 || pr.cin < 64 || pr.cin % 8 != 0) return false;
+  if (pr.dtype != (split ? SEGCONV_F32 : SEGCONV_BF16)) return false;
+  const int kch = split ? 2 * pr.cout : pr.cout;  // A (gy) channels per tap
+  if (kch % tcw::KB != 0 || pr.cin < 64 || pr.cin % 8 != 0) return false;
+  if (split && kch != tcw::KB) return false;  // one A box of [hi | lo] per tap (cout = 32)
   const int taps = pr.kh * pr.kw;
   if (taps > tcw::MAX_TAPS_Q) return false;
   // walk origin of input pixel (i, j): (stride*i + lo_r, stride*j + lo_c); the
@@ -1400,17 +1415,21 @@ static bool make_wide_dgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
     return false;  // rank-4 im2col corner range
   if ((long long)pr.batch * pr.in_h * pr.in_w * pr.cin >= (1LL << 40)) return false;
   p.y = pr.gx;
-  p.y_dtype = SEGCONV_BF16;
+  p.y_dtype = split ? SEGCONV_F32 : SEGCONV_BF16;
   p.batch = pr.batch;
   p.n = pr.in_h;
-  p.cin = pr.cout;  // GEMM K channels
+  p.cin = split ? 2 * kch : kch;  // GEMM K channels
   p.cout = pr.cin;  // GEMM N: input-gradient channels
   p.out_h = pr.in_h;
   p.out_w = pr.in_w;
   p.Mv = (long long)pr.batch * pr.in_h * pr.in_w;
   p.NT = tc_wide_ntile(pr.cin);
   p.n_tiles = (pr.cin + p.NT - 1) / p.NT;
-  p.nkb = pr.cout / tcw::KB;
+  // split: one stage per tap, its A box [gh | gl] multiplied by the two B
+  // halves [wh | wh] and [wl | 0] (two k-blocks, one A box)
+  p.kstage = split ? 2 : 1;
+  p.a_share = split ? 1 : 0;
+  p.nkb = split ? 1 : kch / tcw::KB;
   p.im2col = 1;
   p.bprod = wide_bprod();
   p.S_rows = 128;
@@ -1428,7 +1447,7 @@ static bool make_wide_dgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
   p.ostride = 1;
   p.b_tap_last = 1;
   p.a_stage_bytes = 128 * 128;
-  p.b_stage_bytes = (p.NT / 2) * 128;
+  p.b_stage_bytes = (p.NT / 2) * 128 * p.kstage;
   if (p.b_stage_bytes % 1024) return false;
   const int bar_bytes = (2 * tcw::MAX_STAGES_A + 2 * tcw::MAX_STAGES_B + 4) * 8 + 16;
   p.stages_a = p.stages_b =
@@ -1453,26 +1472,28 @@ static bool make_wide_dgrad(const BackwardProblem& pr, tcw::Params& p, tcw::Maps
       return false;
     enc2 = (EncIm2col)f;
   }
+  const CUtensorMapDataType op = split ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   {
-    const cuuint64_t dims[4] = {(cuuint64_t)pr.cout, (cuuint64_t)pr.out_w, (cuuint64_t)pr.out_h,
+    const cuuint64_t dims[4] = {(cuuint64_t)kch, (cuuint64_t)pr.out_w, (cuuint64_t)pr.out_h,
                                 (cuuint64_t)pr.batch};
-    const cuuint64_t strides[3] = {(cuuint64_t)pr.cout * 2, (cuuint64_t)pr.out_w * pr.cout * 2,
-                                   (cuuint64_t)pr.out_h * pr.out_w * pr.cout * 2};
+    const cuuint64_t strides[3] = {(cuuint64_t)kch * 2, (cuuint64_t)pr.out_w * kch * 2,
+                                   (cuuint64_t)pr.out_h * pr.out_w * kch * 2};
     // walk: origins lo, lo + stride, ... (in_h x in_w per image); corners {W, H}
     const int lower[2] = {lo_c, lo_r};
     const int upper[2] = {up_c, up_r};
     const cuuint32_t es[4] = {1, (cuuint32_t)pr.stride, (cuuint32_t)pr.stride, 1};
-    if (enc2(&maps.xi[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(pr.gy), dims, strides, lower,
+    if (enc2(&maps.xi[0], op, 4, const_cast<void*>(split ? gy16 : pr.gy), dims, strides, lower,
              upper, (cuuint32_t)tcw::KB, 128, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
   }
   {
-    const cuuint64_t dims[3] = {(cuuint64_t)pr.cout, (cuuint64_t)pr.cin, (cuuint64_t)taps};
-    const cuuint64_t strides[2] = {(cuuint64_t)pr.cout * 2, (cuuint64_t)pr.cin * pr.cout * 2};
+    const int bch = p.cin;  // B channels per (tap, input channel): 2 kch for the split
+    const cuuint64_t dims[3] = {(cuuint64_t)bch, (cuuint64_t)pr.cin, (cuuint64_t)taps};
+    const cuuint64_t strides[2] = {(cuuint64_t)bch * 2, (cuuint64_t)pr.cin * bch * 2};
     const cuuint32_t box[3] = {(cuuint32_t)tcw::KB, (cuuint32_t)(p.NT / 2), 1};
     const cuuint32_t es[3] = {1, 1, 1};
-    if (fn(&maps.w[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(pr.k), dims, strides, box, es,
+    if (fn(&maps.w[0], op, 3, const_cast<void*>(split ? w2 : pr.k), dims, strides, box, es,
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
@@ -1758,10 +1779,39 @@ namespace tcw {
 // are of (x 2^t)(w 2^s): inv_out = 2^-s * 2^-t, applied in the epilogue.
 __global__ void x_amax_kernel(const float* __restrict__ x, long long n, unsigned* __restrict__ amax_bits) {
   float m = 0.0f;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x)
-    m = fmaxf(m, fabsf(__ldg(x + e)));
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long e0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {  // float4 body, scalar tail
+    const long long n4 = n / 4;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    long long e = e0;
+    for (; e + 3 * stride < n4; e += 4 * stride) {  // four loads in flight per thread
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = __ldcs(x4 + e + u * stride);  // read once: streaming
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(v[u].x), fabsf(v[u].y)), fmaxf(fabsf(v[u].z), fabsf(v[u].w))));
+    }
+    for (; e < n4; e += stride) {
+      const float4 v = __ldcs(x4 + e);
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+    e0 += n4 * 4;
+    if (e0 < n) m = fmaxf(m, fabsf(__ldg(x + e0)));  // < 4 left: the first threads take them
+  } else {
+    for (long long e = e0; e < n; e += stride) m = fmaxf(m, fabsf(__ldg(x + e)));
+  }
+  // one atomic per block: a thousand warps' atomics on one word serialise at L2
+  __shared__ float wm[32];
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(amax_bits, __float_as_uint(m));
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? wm[threadIdx.x] : 0.0f;
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) atomicMax(amax_bits, __float_as_uint(m));
+  }
 }
 
 __global__ void split_x_kernel(const float* __restrict__ x, __half* __restrict__ xs, long long npix, int cin,
@@ -1770,15 +1820,66 @@ __global__ void split_x_kernel(const float* __restrict__ x, __half* __restrict__
   const int t = split_scale_exp(*amax_bits);
   const float scale = ldexpf(1.0f, t);
   if (blockIdx.x == 0 && threadIdx.x == 0) *inv_out = *w_inv * ldexpf(1.0f, -t);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if (cin % 8 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 && (reinterpret_cast<uintptr_t>(xs) & 15) == 0) {
+    // 8 channels per thread: two float4 loads, two 16-byte stores (hi, lo)
+    const int c8 = cin / 8;
+    const long long total8 = npix * c8;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total8; e += stride) {
+      const long long pix = e / c8;
+      const int ch = (int)(e - pix * c8) * 8;
+      const float4* src = reinterpret_cast<const float4*>(x + pix * cin + ch);
+      const float4 a = __ldcs(src), b = __ldcs(src + 1);
+      const float v[8] = {a.x * scale, a.y * scale, a.z * scale, a.w * scale,
+                          b.x * scale, b.y * scale, b.z * scale, b.w * scale};
+      uint32_t hi[4], lo[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const __half2 h = __floats2half2_rn(v[2 * k], v[2 * k + 1]);
+        const float2 hf = __half22float2(h);
+        const __half2 l = __floats2half2_rn(v[2 * k] - hf.x, v[2 * k + 1] - hf.y);
+        hi[k] = *reinterpret_cast<const uint32_t*>(&h);
+        lo[k] = *reinterpret_cast<const uint32_t*>(&l);
+      }
+      __half* dst = xs + pix * 2 * cin + ch;
+      *reinterpret_cast<uint4*>(dst) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<uint4*>(dst + cin) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+    }
+    return;
+  }
   const long long total = npix * cin;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += stride) {
     const long long pix = e / cin;
     const int ch = (int)(e - pix * cin);
     const float v = x[e] * scale;
     const __half hi = __float2half_rn(v);
     xs[pix * 2 * cin + ch] = hi;
     xs[pix * 2 * cin + cin + ch] = __float2half_rn(v - __half2float(hi));
+  }
+}
+// Split-fp16 input gradient: w2[taps][cin][4 cout] fp16 = [wh | wh | wl | 0]
+// (make_wide_dgrad: two k-blocks against one A box [gh | gl]), weights scaled
+// by 2^s (max |w'| = 2^14); *w_inv = 2^-s.
+__global__ void split_w2_kernel(const float* __restrict__ k, int taps, int cin, int cout,
+                                const unsigned* __restrict__ amax_bits, __half* __restrict__ w2,
+                                float* __restrict__ w_inv) {
+  const int s = split_scale_exp(*amax_bits);
+  const float scale = ldexpf(1.0f, s);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *w_inv = ldexpf(1.0f, -s);
+  const int kch = 2 * cout;
+  const long long total = (long long)taps * cin * cout;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long row = e / cout;  // (tap, ci)
+    const int f = (int)(e - row * cout);
+    const float v = k[e] * scale;
+    const __half hi = __float2half_rn(v);
+    const __half lo = __float2half_rn(v - __half2float(hi));
+    __half* r = w2 + row * 2 * kch;  // [wh | wh | wl | 0]: k-block 0 x [gh | gl], k-block 1 x [gh | gl]
+    r[f] = hi;
+    r[cout + f] = hi;
+    r[2 * cout + f] = lo;
+    r[3 * cout + f] = __float2half_rn(0.0f);
   }
 }
 }  // namespace tcw
@@ -1867,6 +1968,54 @@ cudaError_t launch_tc_bwd_data(const BackwardProblem& pr, cudaStream_t s) {
   if (p.units == 0) return cudaSuccess;
   p.trace = nullptr;
   return launch_wide_t<__nv_bfloat16, 0>(p, maps, s);
+}
+
+bool tc_bwd_data_split_supported(const BackwardProblem& pr) {
+  tcw::Params p;
+  tcw::Maps m;
+  return make_wide_dgrad(pr, p, m, pr.gy, pr.k);  // stand-ins for the split copies (alignment only)
+}
+
+// fp32 input gradient in split-fp16 math on the pair kernel: pre-passes split gy
+// (scaled by 2^t) into [hi | lo] channel halves and build the doubled tap list
+// of the kernel (scaled by 2^s); the GEMM's sums are multiplied by 2^-s-t.
+cudaError_t launch_tc_bwd_data_split(const BackwardProblem& pr, cudaStream_t s) {
+  const long long npix = (long long)pr.batch * pr.out_h * pr.out_w;
+  const int taps = pr.kh * pr.kw, kch = 2 * pr.cout;
+  const size_t gy16_bytes = ((size_t)npix * kch * 2 + 255) / 256 * 256;
+  const size_t w2_bytes = ((size_t)taps * pr.cin * 2 * kch * 2 + 255) / 256 * 256;
+  void* ws = nullptr;
+  cudaError_t e = workspace_alloc(&ws, gy16_bytes + w2_bytes + 16, s);
+  if (e != cudaSuccess) return e;
+  void* gy16 = ws;
+  void* w2 = static_cast<char*>(ws) + gy16_bytes;
+  // tail: [max |gy| bits][max |w| bits][2^-s][2^-s 2^-t]
+  unsigned* tail = reinterpret_cast<unsigned*>(static_cast<char*>(w2) + w2_bytes);
+  float* tailf = reinterpret_cast<float*>(tail);
+  tcw::Params p;
+  tcw::Maps maps;
+  e = make_wide_dgrad(pr, p, maps, gy16, w2) ? cudaMemsetAsync(tail, 0, 8, s) : cudaErrorNotSupported;
+  if (e == cudaSuccess && p.units > 0) {
+    const long long ngy = npix * pr.cout, nk = (long long)taps * pr.cin * pr.cout;
+    const unsigned bg = (unsigned)std::min<long long>((ngy + 255) / 256, 148LL * 16);
+    const unsigned bk = (unsigned)std::min<long long>((nk + 255) / 256, 148LL * 4);
+    tcw::x_amax_kernel<<<std::min(bg, 148u * 8), 256, 0, s>>>((const float*)pr.gy, ngy, tail);
+    tcw::x_amax_kernel<<<bk, 256, 0, s>>>((const float*)pr.k, nk, tail + 1);
+    tcw::split_w2_kernel<<<bk, 256, 0, s>>>((const float*)pr.k, taps, pr.cin, pr.cout, tail + 1, (__half*)w2,
+                                            tailf + 2);
+    tcw::split_x_kernel<<<bg, 256, 0, s>>>((const float*)pr.gy, (__half*)gy16, npix, pr.cout, tail, tailf + 2,
+                                           tailf + 3);
+    e = cudaGetLastError();
+    note_launch(4);
+    if (e == cudaSuccess) {
+      p.split_inv_scale = tailf + 3;
+      p.oscale = 1;
+      p.trace = nullptr;
+      e = launch_wide_t<float, 0>(p, maps, s);
+    }
+  }
+  const cudaError_t e2 = cudaFreeAsync(ws, s);
+  return e != cudaSuccess ? e : e2;
 }
 
 cudaError_t launch_tc_conv_valid(const void* src, int batch, int h, int w, int cin, const void* kt, int kh,

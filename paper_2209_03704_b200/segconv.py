@@ -424,7 +424,11 @@ def transpose_conv_fused_backward(x: torch.Tensor, kernel: torch.Tensor, p_orig:
     the reference's grad_ does across backward calls; ``grad_input`` (a
     contiguous CUDA tensor of x's batched shape and dtype) receives the input
     gradient in place.  ``math``: "exact"
-    (bit-identical to the reference, float/double), "ffma", "bf16", None (auto).
+    (bit-identical to the reference, float/double), "ffma", "bf16", "f16x3"
+    (fp32: the input gradient on the tensor cores in split-fp16 math where the
+    shape allows -- 2 cout a multiple of 64, cin >= 64 -- the kernel gradient,
+    whose pixel sums are far longer than the tensor cores' accumulation bound,
+    on FFMA), None (auto: bf16 for bf16 data, ffma otherwise).
     """
     xb, squeeze = _as_batch(x)
     gb, _ = _as_batch(grad_out)

@@ -319,3 +319,58 @@ def test_bf16_narrow_output_backward():
     gx, gk, path = gpu_bwd(x, kk, 0, gy, math="bf16", dtype=torch.bfloat16)
     assert path == "bwd:simt-narrow+simt-narrow"
     assert scaled_err(gx, wx) <= 1e-2 and scaled_err(gk, wk) <= 1e-4
+
+
+# ---- fp32 input gradient in split-fp16 math on the pair kernel (math="f16x3")
+@pytest.mark.parametrize("b,n,cin,cout,k,p", [
+    (2, 64, 64, 32, 3, 0),    # C2 shape (reduced batch): one [hi | lo] box of 64 channels per tap
+    (3, 16, 128, 64, 4, 2),   # cout = 64: [hi | lo] is two boxes -> SIMT
+    (2, 9, 96, 32, 5, 1),     # 5x5, p = 1: 25 taps
+])
+def test_f16x3_input_grad_on_tensor_cores(b, n, cin, cout, k, p):
+    rng = np.random.default_rng(b * 31 + n + cin + k)
+    x = rng.uniform(-1, 1, (b, n, n, cin)).astype(np.float32)
+    kk = (rng.standard_normal((k, k, cin, cout)) * 0.059).astype(np.float32)
+    g = oracle.geometry(n, k, k, p)
+    gy = rng.uniform(-1, 1, (b, g.out_h, g.out_w, cout)).astype(np.float32)
+    wx, wk = oracle.tconv_backward(x, kk, p, gy)
+    gx, gk, path = gpu_bwd(x, kk, p, gy, math="f16x3")
+    dpath = "tc-pair-split" if cout == 32 and k * k <= 25 else "simt-ffma"
+    assert path == f"bwd:{dpath}+simt-ffma", path
+    # fp32 bar (reference tensors_equal_approx) on the input gradient; the
+    # kernel gradient runs FFMA
+    scaled = np.abs(gx - wx) / np.maximum(np.maximum(np.abs(gx), np.abs(wx)), 1.0)
+    assert scaled.max() <= 1e-5, scaled.max()
+    ak = oracle.tconv_backward(np.abs(x), np.abs(kk), p, np.abs(gy))[1]
+    assert (np.abs(gk - wk) <= 1e-5 * ak + 1e-7).all()
+
+
+def test_f16x3_input_grad_range():
+    """Large and small magnitudes: the split scales gy and the kernel by powers
+    of two (max 2^14), so nothing overflows fp16 and the result keeps the bar."""
+    rng = np.random.default_rng(77)
+    b, n, cin, cout, k, p = 1, 16, 64, 32, 3, 0
+    g = oracle.geometry(n, k, k, p)
+    x = rng.uniform(-1, 1, (b, n, n, cin)).astype(np.float32)
+    for gs, ws in [(1e6, 1e3), (1e-6, 1e-3), (3e4, 7e4)]:
+        kk = (rng.standard_normal((k, k, cin, cout)) * ws).astype(np.float32)
+        gy = (rng.uniform(-1, 1, (b, g.out_h, g.out_w, cout)) * gs).astype(np.float32)
+        wx, _ = oracle.tconv_backward(x, kk, p, gy)
+        gx, _, path = gpu_bwd(x, kk, p, gy, math="f16x3")
+        assert path.startswith("bwd:tc-pair-split"), path
+        assert np.isfinite(gx).all()
+        scaled = np.abs(gx - wx) / np.maximum(np.maximum(np.abs(gx), np.abs(wx)), 1.0)
+        if scaled.max() <= 1e-5:
+            continue
+        # ill-conditioned sums (1e9-sized products that cancel; the reference's
+        # own fp32 result is then far from the exact answer): the same criterion
+        # as the forward's range tests -- error against the exact (f64) answer
+        # in units of each output's conditioning sum sum |g||w|, at most 4x the
+        # reference's own (or 2^-20)
+        exact, _ = oracle.scatter_backward_f64(x, kk, p, gy)
+        cond, _ = oracle.scatter_backward_f64(np.abs(x), np.abs(kk), p, np.abs(gy))
+        live = cond > 0
+
+        def en(a):
+            return float((np.abs(a - exact)[live] / cond[live]).max())
+        assert en(gx) <= max(2.0 ** -20, 4 * en(wx)), (gs, ws, en(gx), en(wx))
