@@ -216,7 +216,11 @@ size_t segconv_last_error_offset(void);
  * bit-identical to the reference), FFMA (SIMT tiles), BF16 (bf16 data: the
  * input gradient on the tcgen05 CTA-pair kernel, a stride-2 im2col walk over
  * gy, when cout % 64 == 0 and cin >= 64; the kernel gradient on SIMT tiles
- * with fp32 accumulation), AUTO (BF16 for bf16 data, FFMA otherwise).
+ * with fp32 accumulation), F16X3 (fp32 data: the input gradient on the same
+ * kernel in split-fp16 math -- gy and w power-of-two scaled and split into
+ * fp16 hi/lo halves -- when cout == 32, cin >= 64, kh*kw <= 25; FFMA
+ * otherwise and for the kernel gradient), AUTO (BF16 for bf16 data, FFMA
+ * otherwise).
  * Errors: geometry ShapeError/ContractError as segconv_tconv_geometry; the
  * reference's "backward before forward" StateError has no counterpart (the
  * forward input is an argument). */
