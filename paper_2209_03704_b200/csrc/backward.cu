@@ -212,6 +212,7 @@ constexpr int BM = 64, BN = 64, BK = 16, NT = 256;
 template <typename T, typename ACC>
 __global__ void __launch_bounds__(NT) dgrad_ffma(const T* __restrict__ gy, const T* __restrict__ k,
                                                  T* __restrict__ gx, BackwardProblem pr) {
+  if (pr.run_if != nullptr && *pr.run_if == 0) return;  // the tensor-core path took it
   __shared__ ACC As[BK][BM + 4];
   __shared__ ACC Bs[BK][BN + 4];
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(NT) dgrad_ffma(const T* __restrict__ gy, const
 template <typename T, typename ACC>
 __global__ void __launch_bounds__(NT) dgrad_ffma_packed(const T* __restrict__ gy, const T* __restrict__ k,
                                                         T* __restrict__ gx, BackwardProblem pr) {
+  if (pr.run_if != nullptr && *pr.run_if == 0) return;  // the tensor-core path took it
   __shared__ ACC As[BK][BM + 4];
   __shared__ ACC Bs[BK][BN + 4];
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;

@@ -598,10 +598,11 @@ static segconv_status run_backward(const BackwardProblem& pr, segconv_math math,
       st = cuda_status(launch_tc_bwd_data(pr, s), msg);
     } else if (math == SEGCONV_MATH_F16X3 && tc_bwd_data_split_supported(pr)) {
       // fp32 in split-fp16 math: K = taps x 2 cout x 2 copies / 16 accumulation
-      // steps (C2: 72), well inside the tensor-core accumulation bound (§5)
+      // steps (C2: 72), well inside the tensor-core accumulation bound (§5);
+      // the range guard picks FFMA on the device for extreme dynamic ranges
       dpath = "tc-pair-split";
       snprintf(msg, sizeof msg, "%s[input, tcgen05 pair, split fp16]", what);
-      st = cuda_status(launch_tc_bwd_data_split(pr, s), msg);
+      st = cuda_status(launch_tc_bwd_data_split(pr, s, true), msg);
     } else {
       dpath = exact ? "simt-exact" : bwd_narrow_applies(pr) ? "simt-narrow" : "simt-ffma";
       snprintf(msg, sizeof msg, "%s[input]", what);
@@ -645,8 +646,11 @@ segconv_status segconv_transpose_conv_fused_backward(const void* d_x, const void
     if (d_gx && !d_kernel) return fail(SEGCONV_E_CONTRACT, "the input gradient needs the kernel");
     if (d_gk && !d_x) return fail(SEGCONV_E_CONTRACT, "the kernel gradient needs the forward input");
   }
+  // AUTO: bf16 tensor cores for bf16 data; fp32: split-fp16 tensor cores for
+  // the input gradient where the shape allows, behind a device-side range
+  // guard, FFMA otherwise
   if (math == SEGCONV_MATH_AUTO)
-    math = dtype == SEGCONV_BF16 ? SEGCONV_MATH_BF16 : SEGCONV_MATH_FFMA;
+    math = dtype == SEGCONV_BF16 ? SEGCONV_MATH_BF16 : dtype == SEGCONV_F32 ? SEGCONV_MATH_F16X3 : SEGCONV_MATH_FFMA;
   if (math == SEGCONV_MATH_EXACT && dtype == SEGCONV_BF16)
     return fail(SEGCONV_E_CONTRACT, "EXACT math is defined for float and double (the reference's types)");
   if (math == SEGCONV_MATH_BF16 && dtype != SEGCONV_BF16)

@@ -50,6 +50,9 @@ struct BackwardProblem {
   void* gx;
   void* gk;
   int accumulate;  // gk += (the reference accumulates tap gradients across calls)
+  // device flag: when set, the SIMT input-gradient kernels run only if *run_if
+  // != 0 (the split-fp16 tensor-core path's range guard decides on device)
+  const int* run_if;
 };
 // the narrow-output (cout <= 4, wide rows) SIMT backward kernels take this problem
 bool bwd_narrow_applies(const BackwardProblem& pr);
@@ -58,7 +61,9 @@ cudaError_t launch_bwd_weight_simt(const BackwardProblem& pr, bool exact, cudaSt
 bool tc_bwd_data_supported(const BackwardProblem& pr);
 // fp32 input gradient in split-fp16 math (f16x3) on the pair kernel (tc_wide.cu)
 bool tc_bwd_data_split_supported(const BackwardProblem& pr);
-cudaError_t launch_tc_bwd_data_split(const BackwardProblem& pr, cudaStream_t s);
+// guarded: a device-side range check picks the tensor-core or the SIMT (FFMA)
+// kernel (both launched, one exits at once) -- AUTO math for fp32 data
+cudaError_t launch_tc_bwd_data_split(const BackwardProblem& pr, cudaStream_t s, bool guarded);
 cudaError_t launch_tc_bwd_data(const BackwardProblem& pr, cudaStream_t s);
 bool tc_bwd_weight_supported(const BackwardProblem& pr);
 bool tc_conv_valid_supported(int batch, int h, int w, int cin, int kh, int kw, int cout);

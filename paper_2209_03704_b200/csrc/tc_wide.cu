@@ -102,6 +102,7 @@ struct Params {
   uint32_t ab_fmt;  // MMA operand format: 1 bf16, 0 fp16
   const float* split_inv_scale;  // SPLIT: the weights were scaled by 2^s; sums are multiplied by 2^-s
   int oscale;  // multiply the sums by *split_inv_scale without SPLIT's three passes (split-fp16 input gradient)
+  const int* run_if;  // non-null: the whole grid exits at once unless *run_if != 0 (device-side range guard)
   // TF32 (fp32 data, math = tf32): fp32 operands, kind::tf32 MMAs (K = 8 per
   // instruction -- the same 32 bytes per step), 32 channels per 128-byte row
   int tf32;
@@ -328,6 +329,7 @@ __device__ __forceinline__ float finish_bf(float v, const float* bias, unsigned 
 template <typename YT, int ACT>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     wide_kernel(const __grid_constant__ Params p, const __grid_constant__ Maps maps) {
+  if (p.run_if != nullptr && *p.run_if == 0) return;  // every CTA alike: before any barrier or TMEM
   extern __shared__ __align__(1024) uint8_t smem[];
   const int SA = p.stages_a, SB = p.stages_b;
   uint8_t* a_base = smem;
@@ -1862,10 +1864,24 @@ __global__ void split_x_kernel(const float* __restrict__ x, __half* __restrict__
 // by 2^s (max |w'| = 2^14); *w_inv = 2^-s.
 __global__ void split_w2_kernel(const float* __restrict__ k, int taps, int cin, int cout,
                                 const unsigned* __restrict__ amax_bits, __half* __restrict__ w2,
-                                float* __restrict__ w_inv) {
+                                float* __restrict__ w_inv, const unsigned* __restrict__ gy_amax_bits,
+                                int* __restrict__ guard) {
   const int s = split_scale_exp(*amax_bits);
   const float scale = ldexpf(1.0f, s);
-  if (blockIdx.x == 0 && threadIdx.x == 0) *w_inv = ldexpf(1.0f, -s);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *w_inv = ldexpf(1.0f, -s);
+    if (guard != nullptr) {
+      // accuracy bound of the split: each fp16 hi/lo pair is within 2^-25 of
+      // its scaled value (max 2^14), i.e. 2^-38 of the largest |gy| (|w|);
+      // over K = taps x cout products the absolute error stays under a
+      // quarter of the fp32 bar's 1e-5 floor when max|gy| max|w| K 2^-37
+      // does.  Past it (dynamic ranges of ~10^9 and more) the SIMT kernels run.
+      const float gmax = __uint_as_float(*gy_amax_bits), wmax = __uint_as_float(*amax_bits);
+      const bool ok = (double)gmax * wmax * taps * cout * 0x1p-37 <= 2.5e-6 && isfinite(gmax) && isfinite(wmax);
+      guard[0] = ok ? 1 : 0;
+      guard[1] = ok ? 0 : 1;
+    }
+  }
   const int kch = 2 * cout;
   const long long total = (long long)taps * cin * cout;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
@@ -1979,19 +1995,20 @@ bool tc_bwd_data_split_supported(const BackwardProblem& pr) {
 // fp32 input gradient in split-fp16 math on the pair kernel: pre-passes split gy
 // (scaled by 2^t) into [hi | lo] channel halves and build the doubled tap list
 // of the kernel (scaled by 2^s); the GEMM's sums are multiplied by 2^-s-t.
-cudaError_t launch_tc_bwd_data_split(const BackwardProblem& pr, cudaStream_t s) {
+cudaError_t launch_tc_bwd_data_split(const BackwardProblem& pr, cudaStream_t s, bool guarded) {
   const long long npix = (long long)pr.batch * pr.out_h * pr.out_w;
   const int taps = pr.kh * pr.kw, kch = 2 * pr.cout;
   const size_t gy16_bytes = ((size_t)npix * kch * 2 + 255) / 256 * 256;
   const size_t w2_bytes = ((size_t)taps * pr.cin * 2 * kch * 2 + 255) / 256 * 256;
   void* ws = nullptr;
-  cudaError_t e = workspace_alloc(&ws, gy16_bytes + w2_bytes + 16, s);
+  cudaError_t e = workspace_alloc(&ws, gy16_bytes + w2_bytes + 32, s);
   if (e != cudaSuccess) return e;
   void* gy16 = ws;
   void* w2 = static_cast<char*>(ws) + gy16_bytes;
-  // tail: [max |gy| bits][max |w| bits][2^-s][2^-s 2^-t]
+  // tail: [max |gy| bits][max |w| bits][2^-s][2^-s 2^-t][guard: tensor cores ran][SIMT must]
   unsigned* tail = reinterpret_cast<unsigned*>(static_cast<char*>(w2) + w2_bytes);
   float* tailf = reinterpret_cast<float*>(tail);
+  int* gflags = reinterpret_cast<int*>(tail + 4);
   tcw::Params p;
   tcw::Maps maps;
   e = make_wide_dgrad(pr, p, maps, gy16, w2) ? cudaMemsetAsync(tail, 0, 8, s) : cudaErrorNotSupported;
@@ -2002,7 +2019,7 @@ cudaError_t launch_tc_bwd_data_split(const BackwardProblem& pr, cudaStream_t s) 
     tcw::x_amax_kernel<<<std::min(bg, 148u * 8), 256, 0, s>>>((const float*)pr.gy, ngy, tail);
     tcw::x_amax_kernel<<<bk, 256, 0, s>>>((const float*)pr.k, nk, tail + 1);
     tcw::split_w2_kernel<<<bk, 256, 0, s>>>((const float*)pr.k, taps, pr.cin, pr.cout, tail + 1, (__half*)w2,
-                                            tailf + 2);
+                                            tailf + 2, tail, guarded ? gflags : nullptr);
     tcw::split_x_kernel<<<bg, 256, 0, s>>>((const float*)pr.gy, (__half*)gy16, npix, pr.cout, tail, tailf + 2,
                                            tailf + 3);
     e = cudaGetLastError();
@@ -2010,9 +2027,17 @@ cudaError_t launch_tc_bwd_data_split(const BackwardProblem& pr, cudaStream_t s) 
     if (e == cudaSuccess) {
       p.split_inv_scale = tailf + 3;
       p.oscale = 1;
+      p.run_if = guarded ? gflags : nullptr;
       p.trace = nullptr;
       e = launch_wide_t<float, 0>(p, maps, s);
     }
+  }
+  if (guarded && e == cudaSuccess && p.units > 0) {
+    // the SIMT kernels, gated on the other flag (exit at once when the tensor
+    // cores took the gradient) -- decided on the device, nothing synchronises
+    BackwardProblem pf = pr;
+    pf.run_if = gflags + 1;
+    e = launch_bwd_data_simt(pf, false, s);
   }
   const cudaError_t e2 = cudaFreeAsync(ws, s);
   return e != cudaSuccess ? e : e2;
