@@ -219,8 +219,9 @@ size_t segconv_last_error_offset(void);
  * with fp32 accumulation), F16X3 (fp32 data: the input gradient on the same
  * kernel in split-fp16 math -- gy and w power-of-two scaled and split into
  * fp16 hi/lo halves -- when cout == 32, cin >= 64, kh*kw <= 25; FFMA
- * otherwise and for the kernel gradient), AUTO (BF16 for bf16 data, FFMA
- * otherwise).
+ * otherwise and for the kernel gradient; a device-side range guard hands
+ * inputs whose products reach ~10^3 to FFMA), AUTO (BF16 for bf16 data,
+ * F16X3 for fp32, FFMA for double).
  * Errors: geometry ShapeError/ContractError as segconv_tconv_geometry; the
  * reference's "backward before forward" StateError has no counterpart (the
  * forward input is an argument). */

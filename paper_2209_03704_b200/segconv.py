@@ -428,7 +428,8 @@ def transpose_conv_fused_backward(x: torch.Tensor, kernel: torch.Tensor, p_orig:
     (fp32: the input gradient on the tensor cores in split-fp16 math where the
     shape allows -- 2 cout a multiple of 64, cin >= 64 -- the kernel gradient,
     whose pixel sums are far longer than the tensor cores' accumulation bound,
-    on FFMA), None (auto: bf16 for bf16 data, ffma otherwise).
+    on FFMA; a device-side range guard hands extreme dynamic ranges to FFMA),
+    None (auto: bf16 for bf16 data, f16x3 for float32, ffma for float64).
     """
     xb, squeeze = _as_batch(x)
     gb, _ = _as_batch(grad_out)
