@@ -56,6 +56,7 @@ constexpr int KB = 64;  // channels per stage: one 128-byte row
 constexpr int WCH = 128;  // WGRAD: pixels (K) per chunk
 constexpr int MAX_TAPS_Q = 25;  // 5x5: the input-gradient walk uses every tap as one class
 constexpr int MAX_STAGES_A = 8, MAX_STAGES_B = 12;
+constexpr int SMEM_PER_CTA2 = 113 * 1024;  // two CTAs per SM (Params::cps == 2)
 
 struct Params {
   void* y;
@@ -114,6 +115,7 @@ struct Params {
   // stride-2 im2col walk over gy.  Results go to wout (+ s * ksz when split).
   int mode;
   int kstage;  // IM2COL forward: 64-channel k-blocks per pipeline stage (2 halves the handshakes)
+  int cps;     // CTAs per SM (2: NT <= 128 forward, 256 TMEM columns each, two pipelines share the tensor pipe)
   int a_share;  // the stage's k-blocks multiply one A box (split-fp16 input gradient: [hi | lo] x two B halves)
   int w_kw, w_taps, w_ch_pairs, w_splits, w_cin, w_cout, w_direct, w_accumulate;
   int w_in_h, w_in_w;  // input map (anchor grid) of the kernel-gradient walk
@@ -326,8 +328,8 @@ __device__ __forceinline__ float finish_bf(float v, const float* bias, unsigned 
   return v;
 }
 
-template <typename YT, int ACT>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+template <typename YT, int ACT, int CPS>
+__global__ void __launch_bounds__(NUM_THREADS, CPS)
     wide_kernel(const __grid_constant__ Params p, const __grid_constant__ Maps maps) {
   if (p.run_if != nullptr && *p.run_if == 0) return;  // every CTA alike: before any barrier or TMEM
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -374,8 +376,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
   }
   if (warp == 6) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     smem_u32(tmem_slot))
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)), "r"(CPS == 2 ? 256 : 512)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
@@ -1038,7 +1040,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   cluster_sync();  // the pair's MMAs and remote arrivals are over before TMEM is freed
   if (warp == 6) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem_base)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(CPS == 2 ? 256 : 512)
                  : "memory");
   }
 }
@@ -1272,14 +1274,25 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
   p.b_stage_bytes = (p.NT / 2) * 128;
   if (p.b_stage_bytes % 1024) return false;
   const int bar_bytes = (2 * tcw::MAX_STAGES_A + 2 * tcw::MAX_STAGES_B + 4) * 8 + 16;
-  const int budget = tcw::SMEM_LIMIT - bar_bytes;
+  int budget = tcw::SMEM_LIMIT - bar_bytes;
   if (p.im2col) {  // A and B both per (k-block, tap): paired rings
     // two 64-channel k-blocks per stage where cin allows: the producer / MMA
     // handshake costs a few hundred cycles per stage whatever its size, as
     // much as a stage of N = 128 MMAs (measured: the empty pipeline alone,
     // no loads / MMAs / epilogue, takes 27 us for C5 layer c at one k-block
     // per stage)
-    p.kstage = (!split && !tf32 && p.mode == 0 && pr.cin % (2 * tcw::KB) == 0 &&
+    // narrow feature tiles: two CTAs (two pipelines) per SM, 256 TMEM columns
+    // each -- one CTA's per-stage handshakes run under the other's MMAs
+    // (measured: C5 layer c 39.6 -> 35.1-37.3 us; the same for NT = 256 with one
+    // accumulator per CTA made C3 77 -> 92 us)
+    // only when the units fill twice as many CTA pairs (small batches keep one
+    // pipeline with the whole ring: C5 at 128 images 50.8 -> 63.4 us otherwise)
+    long long units = 0;
+    for (int q = 0; q < 4; ++q)
+      units += ((long long)pr.batch * pr.cls.rows[q] * pr.cls.cols[q] + 255) / 256 * p.n_tiles;
+    p.cps = (!split && !tf32 && p.mode == 0 && p.NT <= 128 && units >= 4LL * wide_pairs()) ? 2 : 1;
+    if (p.cps == 2) budget = tcw::SMEM_PER_CTA2 - bar_bytes;
+    p.kstage = (p.cps == 1 && !split && !tf32 && p.mode == 0 && pr.cin % (2 * tcw::KB) == 0 &&
                 2 * (p.a_stage_bytes + p.b_stage_bytes) * 3 <= budget) ? 2 : 1;
     p.nkb = pr.cin / (p.kbc * p.kstage);
     p.a_stage_bytes *= p.kstage;
@@ -1733,14 +1746,15 @@ bool tc_wide_supported(const FusedProblem& pr, int math) {
 
 template <typename YT, int ACT>
 static cudaError_t launch_wide_t(const tcw::Params& prm, const tcw::Maps& maps, cudaStream_t s) {
-  auto kern = tcw::wide_kernel<YT, ACT>;
-  static PerDeviceOnce once;
+  auto kern = prm.cps == 2 ? tcw::wide_kernel<YT, ACT, 2> : tcw::wide_kernel<YT, ACT, 1>;
+  static PerDeviceOnce once1, once2;
   {
-    const cudaError_t e = smem_attr_once(once, kern, tcw::SMEM_LIMIT);
+    const cudaError_t e = prm.cps == 2 ? smem_attr_once(once2, kern, tcw::SMEM_PER_CTA2)
+                                       : smem_attr_once(once1, kern, tcw::SMEM_LIMIT);
     if (e != cudaSuccess) return e;
   }
   const int sms = device_sm_count();
-  long long pairs = std::min<long long>(prm.units, sms / 2);
+  long long pairs = std::min<long long>(prm.units, (long long)(sms / 2) * (prm.cps == 2 ? 2 : 1));
   tcw::Params pk = prm;
   // last partial wave: when its T units fit twice over, run them as 2T feature
   // half-tiles (N = NT/2) so the wave takes half a unit instead of a whole one
