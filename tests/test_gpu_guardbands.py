@@ -38,6 +38,8 @@ CASES = [
     ("pair-split", 2, 8, 128, 64, 4, 0, torch.float32, "auto", None, "tc-pair"),
     ("pair-tf32", 2, 8, 128, 64, 4, 0, torch.float32, "tf32", None, "tc-pair"),
     ("pair-allq", 1, 64, 128, 64, 4, 2, torch.bfloat16, "auto", "tanh", "tc-pair"),
+    # two CTAs per SM (NT <= 128, units for twice the pairs): 303 units
+    ("pair-2cta", 640, 7, 128, 128, 3, 0, torch.bfloat16, "auto", "relu", "tc-pair"),
     ("tile", 9, 11, 128, 3, 3, 0, torch.bfloat16, "auto", "tanh", "tc-tile"),
     ("tile-4x4", 3, 32, 128, 3, 4, 2, torch.bfloat16, "auto", "tanh", "tc-tile"),
     ("halo", 2, 6, 32, 48, 3, 2, torch.float32, "f16x3", None, "tc-halo"),
@@ -94,6 +96,7 @@ def test_guard_bands_and_determinism(case):
 def test_backward_guard_bands_and_determinism():
     rng = np.random.default_rng(11)
     for (b, n, cin, cout, k, p, dt, path) in [(2, 6, 128, 128, 4, 2, torch.bfloat16, "bwd:tc-pair+tc-pair"),
+                                               (2, 16, 64, 32, 3, 0, torch.float32, "bwd:tc-pair-split+simt-ffma"),
                                                (1, 64, 64, 3, 5, 0, torch.float32, "bwd:simt-narrow+simt-narrow"),
                                                (2, 9, 16, 24, 3, 1, torch.float32, "bwd:simt-ffma+simt-ffma")]:
         g = sc.tconv_geometry(n, k, k, p)
