@@ -79,7 +79,7 @@ void shard(int batch, int g, int G, int* lo, int* hi) {
 // on its own copy stream; the layer chain of slice c starts as soon as slice
 // c has landed, so the host->device copy (the e2e bound: 33.5 MB for C5 at
 // PCIe speed) overlaps the compute of the slices before it.
-constexpr int kMaxChunks = 4, kChunkImages = 128;
+constexpr int kMaxChunks = 8, kChunkImages = 128;
 int chunks_for(int b) { return std::max(1, std::min(kMaxChunks, b / kChunkImages)); }
 
 struct Layer {
@@ -92,8 +92,10 @@ struct Replica {
   int dev = 0;
   cudaStream_t stream = nullptr;  // compute (and collectives)
   cudaStream_t copy = nullptr;    // shard upload, chunk by chunk
+  cudaStream_t down = nullptr;    // one GPU: each chunk's output download, as soon as its chain ends
   cudaEvent_t ev[6] = {};      // h2d start, compute start, compute end, gather end, d2h end, h2d end
   cudaEvent_t chunk[kMaxChunks] = {};  // chunk c of the shard has landed
+  cudaEvent_t done[kMaxChunks] = {};   // chunk c's chain has finished (one GPU: its download may start)
   void* x = nullptr;           // shard input
   std::vector<void*> acts;     // per-layer outputs (shard)
   std::vector<void*> kern;     // raw kernels (kept for the broadcast source / re-segregation)
@@ -158,8 +160,11 @@ void segconv_stack_destroy(segconv_stack* st) {
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : r.chunk)
       if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : r.done)
+      if (e) cudaEventDestroy(e);
     if (r.stream) cudaStreamDestroy(r.stream);
     if (r.copy) cudaStreamDestroy(r.copy);
+    if (r.down) cudaStreamDestroy(r.down);
   }
   delete st;
 }
@@ -219,8 +224,10 @@ static segconv_status stack_build(segconv_stack* st, const segconv_layer* layers
     CK(cudaSetDevice(g), "stack: set device");
     CK(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking), "stack: stream");
     CK(cudaStreamCreateWithFlags(&r.copy, cudaStreamNonBlocking), "stack: copy stream");
+    CK(cudaStreamCreateWithFlags(&r.down, cudaStreamNonBlocking), "stack: download stream");
     for (cudaEvent_t& e : r.ev) CK(cudaEventCreate(&e), "stack: event");
     for (cudaEvent_t& e : r.chunk) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "stack: event");
+    for (cudaEvent_t& e : r.done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "stack: event");
     CK(cudaMalloc(&r.x, std::max<size_t>(1, st->max_shard * st->in_img * es)), "stack: input buffer");
     for (const Layer& L : st->layers) {
       void* a = nullptr;
@@ -356,6 +363,15 @@ static segconv_status stack_forward(segconv_stack* st, const void* h_x, int batc
         if (s != SEGCONV_OK) return s;
         src = dst;
       }
+      if (G == 1) {
+        // one GPU: download this chunk's output while the next chunks upload and
+        // compute (a third stream: the upload stream must not wait on compute)
+        CK(cudaEventRecord(r.done[c], r.stream), "stack: event");
+        CK(cudaStreamWaitEvent(r.down, r.done[c], 0), "stack: chunk done wait");
+        CK(cudaMemcpyAsync((char*)h_y + (size_t)(lo + c0) * st->out_img * es, src, (size_t)nb * st->out_img * es,
+                           cudaMemcpyDeviceToHost, r.down),
+           "stack: chunk output download");
+      }
     }
     if (b <= 0) CK(cudaEventRecord(r.ev[1], r.stream), "stack: event");
     CK(cudaEventRecord(r.ev[5], r.copy), "stack: event");
@@ -386,24 +402,29 @@ static segconv_status stack_forward(segconv_stack* st, const void* h_x, int batc
     CK(cudaEventRecord(r.ev[3], r.stream), "stack: event");
   }
   // GPU 0 holds every shard, each at g * pad images: compact them into h_y
+  // (one GPU: the chunks are already on their way, on the download stream)
   Replica& r0 = st->reps[0];
   CK(cudaSetDevice(r0.dev), "stack: set device");
-  for (int g = 0; g < G; ++g) {
-    int lo, hi;
-    shard(batch, g, G, &lo, &hi);
-    if (hi > lo)
-      CK(cudaMemcpyAsync((char*)h_y + (size_t)lo * st->out_img * es,
-                         (const char*)(G > 1 ? r0.gathered : r0.acts.back()) +
-                             (size_t)(G > 1 ? g * pad : lo) * st->out_img * es,
-                         (size_t)(hi - lo) * st->out_img * es, cudaMemcpyDeviceToHost, r0.stream),
-         "stack: output download");
+  if (G > 1) {
+    for (int g = 0; g < G; ++g) {
+      int lo, hi;
+      shard(batch, g, G, &lo, &hi);
+      if (hi > lo)
+        CK(cudaMemcpyAsync((char*)h_y + (size_t)lo * st->out_img * es,
+                           (const char*)r0.gathered + (size_t)g * pad * st->out_img * es,
+                           (size_t)(hi - lo) * st->out_img * es, cudaMemcpyDeviceToHost, r0.stream),
+           "stack: output download");
+    }
+    CK(cudaEventRecord(r0.ev[4], r0.stream), "stack: event");
+  } else {
+    CK(cudaEventRecord(r0.ev[4], r0.down), "stack: event");
   }
-  CK(cudaEventRecord(r0.ev[4], r0.stream), "stack: event");
   double h2d = 0, comp = 0, gat = 0, d2h = 0;
   for (Replica& r : st->reps) {
     CK(cudaSetDevice(r.dev), "stack: set device");
     CK(cudaStreamSynchronize(r.stream), "stack: forward");
     CK(cudaStreamSynchronize(r.copy), "stack: forward");
+    CK(cudaStreamSynchronize(r.down), "stack: forward");
     float a = 0, b = 0, c = 0;
     CK(cudaEventElapsedTime(&a, r.ev[0], r.ev[5]), "stack: timing");
     CK(cudaEventElapsedTime(&b, r.ev[1], r.ev[2]), "stack: timing");
@@ -416,7 +437,7 @@ static segconv_status stack_forward(segconv_stack* st, const void* h_x, int batc
     float d = 0;
     CK(cudaSetDevice(r0.dev), "stack: set device");
     CK(cudaEventElapsedTime(&d, r0.ev[3], r0.ev[4]), "stack: timing");
-    d2h = d;
+    d2h = std::max(0.0, (double)d);  // one GPU: the downloads overlap compute, this is the tail after it
   }
   if (tm) {
     tm->n_gpus = G;

@@ -210,7 +210,42 @@ def test_multi_gpu_stack_c_abi_equals_generator_stack():
     y = ms.forward(x.pin_memory())
     assert torch.equal(y, ref)
     t = ms.last_timing
-    assert t["n_gpus"] == 1 and t["compute_ms"] > 0 and t["h2d_ms"] > 0 and t["d2h_ms"] > 0
+    assert t["n_gpus"] == 1 and t["compute_ms"] > 0 and t["h2d_ms"] > 0 and t["d2h_ms"] >= 0
     y7 = ms.forward(x[:7].contiguous())
     assert torch.equal(y7, ref[:7])
+    ms.close()
+
+
+def test_multi_gpu_stack_chunked_upload_and_download():
+    """At the benched batch the C ABI driver uploads the shard in 8 chunks and
+    downloads each chunk's output as soon as its chain ends (one GPU): the
+    result must equal the one-shot graph path bit for bit."""
+    from paper_2209_03704_b200 import stack as st
+    specs = st.c5_layers()
+    rng = np.random.default_rng(57)
+    ks = [torch.from_numpy(rng.standard_normal((s.k, s.k, s.cin, s.cout), dtype=np.float32) * 0.02)
+          for s in specs]
+    b = 1024
+    x = torch.from_numpy(rng.standard_normal((b, 4, 4, 1024), dtype=np.float32)).bfloat16()
+    kd = [k.cuda() for k in ks]
+
+    def chunked_ref(xs, chunks):
+        # the kernels' configuration (feature tile, CTAs per SM, k-blocks per
+        # stage) depends on the batch, and with it a few bf16 roundings: the
+        # reference runs the same chunks (chunk c = images [c b / C, (c+1) b / C))
+        n = xs.shape[0]
+        outs = []
+        for c in range(chunks):
+            lo, hi = c * n // chunks, (c + 1) * n // chunks
+            outs.append(st.GeneratorStack(specs, kd, hi - lo).forward(xs[lo:hi].cuda()).cpu())
+        return torch.cat(outs)
+
+    ms = st.MultiGPUStack(specs, ks, b, n_gpus=1)
+    ref = chunked_ref(x, 8)
+    for _ in range(2):  # the second call reuses the buffers and streams
+        y = ms.forward(x.pin_memory())
+        assert torch.equal(y, ref)
+    assert ms.last_timing["d2h_ms"] >= 0
+    y3 = ms.forward(x[:300].contiguous())  # 2 uneven chunks
+    assert torch.equal(y3, chunked_ref(x[:300], 2))
     ms.close()
