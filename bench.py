@@ -353,6 +353,9 @@ class LayerBackward(Layer):
                 "path": path, "parity": {"max_scaled_err": err, "tol": 1e-5, "images": idx},
                 "what": "math=\"f16x3\" explicitly (AUTO takes the same guarded path)"}
 
+    e2e_what = ("segconv.transpose_conv_fused_backward from pinned host buffers: x and gy "
+                "uploaded, both gradients read back, all on the launching stream")
+
     def step_e2e(self):
         """Public API from host buffers: x and gy uploaded, both gradients read back."""
         xd = self.x_pinned.to(self.xd.device, non_blocking=True)
@@ -1085,13 +1088,14 @@ def main():
                "math": prob.math,
                "hbm_gbs": round(hbm_gbs, 1),
                "roofline": roof,
-               "e2e": {"value": round(macs_all / (e2e_ms * 1e-3) / 1e9, 2), "unit": "useful GMAC/s",
+               "e2e": None if not e2e_steps else {
+                       "value": round(macs_all / (e2e_ms * 1e-3) / 1e9, 2), "unit": "useful GMAC/s",
                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                        "ms_per_step": round(e2e_ms, 4),
                        "what": getattr(prob, "e2e_what", "C ABI segconv_transpose_conv_fused_host (pinned host "
                                        "buffers, batch slices pipelined over H2D / kernel / D2H streams)"),
                        **({"phases_ms": prob.capi.last_timing} if getattr(prob, "capi", None) is not None
-                          else {})},
+                          else {})},  # None: --no-e2e (diagnostic runs only)
                "gpu_launches": int(launches),
                "parity": parity,
                "clocks": clk.summary()}

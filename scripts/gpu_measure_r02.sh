@@ -8,7 +8,7 @@ for c in C5 C2 C4; do
   timeout 600 python bench.py --impl reference --config $c --steps 3 --warmup 1 > gpurun_out/r02/ref_$c.json 2> gpurun_out/r02/ref_$c.err; echo ref $c=$?
 done
 for c in C3 C5a C5b C5c C2 C4; do
-  timeout 600 python bench.py --config $c --pass backward --steps 10 --warmup 3 --no-e2e > gpurun_out/r02/bwd_$c.json 2> gpurun_out/r02/bwd_$c.err; echo bwd $c=$?
+  timeout 600 python bench.py --config $c --pass backward --steps 10 --warmup 3 > gpurun_out/r02/bwd_$c.json 2> gpurun_out/r02/bwd_$c.err; echo bwd $c=$?
 done
 for c in C5 C2 C4 C3 C1; do
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
