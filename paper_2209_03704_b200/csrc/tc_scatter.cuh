@@ -47,6 +47,24 @@ struct ScatterLayout {
         }
     return -1;
   }
+  // useful columns only (the tile kernel's SMEM copy of D): (dy, q, dx, f) ->
+  // column, group by group without the 16-column padding
+  static constexpr int useful_off(int dy) {
+    int o = 0;
+    for (int d = 0; d < dy; ++d) o += group_len(d);
+    return o;
+  }
+  static constexpr int NU = useful_off(U);
+  static constexpr int ucol(int dy, int q, int dx, int f) {
+    return has(q, dy, dx) ? useful_off(dy) + col_in_group(dy, q, dx, f) : -1;
+  }
+  // D (TMEM) column -> useful column, -1 for padding
+  static constexpr int compact(int c) {
+    int dy = 0;
+    while (dy + 1 < U && c >= group_off(dy + 1)) ++dy;
+    const int col = c - group_off(dy);
+    return col < group_len(dy) ? useful_off(dy) + col : -1;
+  }
 };
 
 }  // namespace segconv_b200

@@ -21,9 +21,9 @@
 // TMA (box {64 channels, 128 pixels}, 128-byte swizzle) and are the MMA A
 // operand directly; the weight image (rows = D columns) is resident in SMEM.
 //
-// Warp roles (320 threads): 0-7 epilogue (0-3 also drain TMEM; thread t sums
-// anchor t % 128 for output row parity t / 128), 8 TMA producer / TMEM
-// owner, 9 MMA issuer.
+// Warp roles (320 threads): 0-7 epilogue (warps w, w + 4 drain half of TMEM
+// lane quadrant w % 4 each; thread t sums anchor t % 128 for output row parity
+// t / 128), 8 TMA producer / TMEM owner, 9 MMA issuer.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -80,17 +80,39 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t addr) {
          (1ull << 46) | (2ull << 61);
 }
 
+// SMEM tile pitch (floats): the useful D columns, odd so that the drain's
+// row-per-lane stores and the gather's loads hit distinct banks
+template <int KH, int COUT>
+__host__ __device__ constexpr int tile_pitch() {
+  return ScatterLayout<KH, COUT>::NU | 1;
+}
+
+// TMEM columns [C0, C0 + CN) of this lane's D row -> its SMEM row (useful columns)
+template <typename L, int C0, int CN>
+__device__ __forceinline__ void drain_cols(uint32_t taddr, float* row) {
+  static_assert(CN % 8 == 0, "x8 loads");
+  uint32_t r[CN / 8][8];
+#pragma unroll
+  for (int c = 0; c < CN / 8; ++c) tmem_ld8_nw(taddr + (uint32_t)(C0 + 8 * c), r[c]);
+  tmem_wait_ld();
+#pragma unroll
+  for (int c = 0; c < CN; ++c) {
+    const int u = L::compact(C0 + c);
+    if (u >= 0) row[u] = __uint_as_float(r[c / 8][c % 8]);
+  }
+}
+
 template <int KH, int COUT, int ACT, typename YT>
 __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
     tile_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmap) {
   using L = ScatterLayout<KH, COUT>;
-  constexpr int U = L::U, N = L::N, TP = N + 1;  // SMEM tile pitch (floats)
+  constexpr int U = L::U, N = L::N, TP = tile_pitch<KH, COUT>();
   extern __shared__ __align__(1024) uint8_t smem[];
   const int SA = p.stages;
   uint8_t* a_base = smem;
   uint8_t* w_base = smem + (size_t)SA * p.stage_bytes;
-  float* dtile = reinterpret_cast<float*>(w_base + p.w_bytes);  // [TILE][TP]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(dtile + TILE * TP + (TILE * TP) % 2);
+  float* dtile = reinterpret_cast<float*>(w_base + p.w_bytes);  // 2 x [TILE][TP]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(dtile + 2 * TILE * TP + (2 * TILE * TP) % 2);
   uint64_t* a_full = bars;
   uint64_t* a_empty = a_full + SA;
   uint64_t* acc_full = a_empty + SA;
@@ -99,6 +121,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) trace_ev(p, 6, 0);
   if (warp == 9 && lane == 0) {
     for (int s = 0; s < SA; ++s) {
       mbar_init(&a_full[s], 1);
@@ -106,7 +129,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], 128);
+      mbar_init(&acc_empty[s], 256);
     }
     mbar_init(w_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -124,6 +147,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) griddep_launch_dependents();
+  if (threadIdx.x == 0) trace_ev(p, 8, 0);
   const int NKB = p.cin / KB;
   const uint32_t WCOL = (uint32_t)N * 16;
 
@@ -197,73 +221,78 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
       }
     }
   } else {
-    // ===== epilogue (warps 0-7): TMEM rows (pixels) -> SMEM tile (warps 0-3),
-    // then thread t sums anchor t % 128 for output rows of parity t / 128
+    // ===== epilogue (warps 0-7).  Warps w and w + 4 drain TMEM lane quadrant
+    // w % 4 (w < 4: D columns [0, N/2), else [N/2, N)) into a double-buffered
+    // SMEM tile of the useful columns; then thread t sums anchor t % 128 for
+    // output rows of parity t / 128.  One named barrier per tile: a drain into
+    // buffer k & 1 follows the barrier of tile k - 1, which every thread passes
+    // only after its gather from that buffer two tiles back.
     const int m = threadIdx.x & 127, rr = threadIdx.x >> 7;
-    const bool drain = warp < 4;
     const uint32_t lane_base = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
     float bias[COUT];
 #pragma unroll
     for (int f = 0; f < COUT; ++f) bias[f] = (p.epi & SEGCONV_EPI_BIAS) ? __ldg(p.bias + f) : 0.0f;
     YT* y = reinterpret_cast<YT*>(p.y);
-    const int img = p.n * p.n;
+    const unsigned img = (unsigned)(p.n * p.n);
+    // SMEM offset of shift (dy, dx) from the anchor's row (per-thread constant)
+    int soff[U][U];
+#pragma unroll
+    for (int dy = 0; dy < U; ++dy)
+#pragma unroll
+      for (int dx = 0; dx < U; ++dx) soff[dy][dx] = ((dy - p.pf) * p.n + (dx - p.pf)) * TP;
     int acc = 0;
     uint32_t pacc = 0;
     int k = 0;
     for (long long t = blockIdx.x; t < p.tiles; t += gridDim.x, ++k) {
-      if (drain) {
-        mbar_wait(&acc_full[acc], pacc);
-        tc_fence_after();
-        if (threadIdx.x == 0) trace_ev(p, 4, k);
-        float v[32];
+      // anchor geometry first: it overlaps the wait for the accumulator
+      const long long g = t * p.step + m;  // this thread's anchor, tile pixel p.back + m
+      const bool live = m < p.step && g < p.Mv && !(p.debug & 1);
+      const unsigned gu = live ? (unsigned)g : 0u;  // Mv < 2^31 (host check)
+      const int b = (int)(gu / img);
+      const int rem = (int)(gu - (unsigned)b * img);
+      const int i = rem / p.n, j = rem - (rem / p.n) * p.n;
+      bool inb[U][U];
 #pragma unroll
-        for (int c0 = 0; c0 + 32 <= N; c0 += 32) {
-          tmem_ld32(lane_base + (uint32_t)(acc * N + c0), v);
+      for (int dy = 0; dy < U; ++dy)
 #pragma unroll
-          for (int c = 0; c < 32; ++c) dtile[m * TP + c0 + c] = v[c];
-        }
-        if constexpr (N % 32 != 0) {  // N is a multiple of 16
-          tmem_ld16(lane_base + (uint32_t)(acc * N + N / 32 * 32), v);
-#pragma unroll
-          for (int c = 0; c < 16; ++c) dtile[m * TP + N / 32 * 32 + c] = v[c];
-        }
-        tc_fence_before();
-        mbar_arrive(&acc_empty[acc]);  // D is in SMEM now; the MMA may reuse the buffer
-      }
+        for (int dx = 0; dx < U; ++dx)
+          inb[dy][dx] = (unsigned)(i + dy - p.pf) < (unsigned)p.n && (unsigned)(j + dx - p.pf) < (unsigned)p.n;
+      float* dt = dtile + (k & 1) * (TILE * TP);
+      mbar_wait(&acc_full[acc], pacc);
+      tc_fence_after();
+      if (threadIdx.x == 0) trace_ev(p, 4, k);
+      if (warp < 4)
+        drain_cols<L, 0, N / 2>(lane_base + (uint32_t)(acc * N), dt + m * TP);
+      else
+        drain_cols<L, N / 2, N / 2>(lane_base + (uint32_t)(acc * N), dt + m * TP);
+      tc_fence_before();
+      mbar_arrive(&acc_empty[acc]);  // D is in SMEM now; the MMA may reuse the buffer
       if (++acc == 2) {
         acc = 0;
         pacc ^= 1;
       }
       named_bar(1, 256);
-      const long long g = t * p.step + m;  // this thread's anchor, tile pixel p.back + m
-      if (m < p.step && g < p.Mv && !(p.debug & 1)) {
-        // 32-bit index math (Mv < 2^31 is checked on the host)
-        const unsigned gu = (unsigned)g;
-        const int b = (int)(gu / (unsigned)img);
-        const int rem = (int)(gu - (unsigned)b * (unsigned)img);
-        const int i = rem / p.n, j = rem - (rem / p.n) * p.n;
+      if (live) {
+        const float* row = dt + (p.back + m) * TP;
         float out[2][COUT];
         bool okc[2];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
+          // classes of row parity rr: q = 2 rr + c, both compile-time below
           const int q = rr * 2 + c;
           okc[c] = i < p.rows[q] && j < p.cols[q];
 #pragma unroll
           for (int f = 0; f < COUT; ++f) {
-            float s = 0.0f;
+            float s = bias[f];
 #pragma unroll
             for (int dy = 0; dy < U; ++dy)
 #pragma unroll
               for (int dx = 0; dx < U; ++dx) {
-                // classes of row parity rr: q = 2 rr + c, both unrolled below
-                const int col0 = L::col_in_group(dy, 0 + c, dx, f), col2 = L::col_in_group(dy, 2 + c, dx, f);
+                const int col0 = L::ucol(dy, 0 + c, dx, f), col2 = L::ucol(dy, 2 + c, dx, f);
                 const int col = rr ? col2 : col0;
-                if ((rr ? col2 : col0) < 0) continue;
-                const int ii = i + dy - p.pf, jj = j + dx - p.pf;  // input pixel (padding: zero)
-                if (ii < 0 || ii >= p.n || jj < 0 || jj >= p.n) continue;
-                s += dtile[(p.back + m + (dy - p.pf) * p.n + (dx - p.pf)) * TP + L::group_off(dy) + col];
+                if (col < 0 || !inb[dy][dx]) continue;  // input pixel outside the image: zero
+                s += row[soff[dy][dx] + col];
               }
-            s += bias[f];
             if (ACT == 1) s = fmaxf(s, 0.0f);
             if (ACT == 2) {
               if constexpr (sizeof(YT) == 2) {
@@ -278,8 +307,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
         }
         // pixels (2i + rr, 2j) and (2i + rr, 2j + 1): 2 x COUT consecutive values
         YT* o = y + (((long long)b * p.out_h + 2 * i + rr) * p.out_w + 2 * j) * COUT;
-        if (sizeof(YT) == 2 && okc[0] && okc[1] && ((reinterpret_cast<uintptr_t>(o) & 3) == 0) &&
-            (COUT % 1 == 0) && (2 * COUT) % 2 == 0) {
+        if (sizeof(YT) == 2 && okc[0] && okc[1] && ((reinterpret_cast<uintptr_t>(o) & 3) == 0)) {
           const float* fl = &out[0][0];
 #pragma unroll
           for (int e = 0; e < COUT; ++e) {  // 2*COUT values as COUT bf16 pairs
@@ -294,13 +322,13 @@ __global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
               for (int f = 0; f < COUT; ++f) o[c * COUT + f] = from_f<YT>(out[c][f]);
         }
       }
-      named_bar(1, 256);  // the tile is rewritten by the next unit
       if (threadIdx.x == 0) trace_ev(p, 5, k);
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace_ev(p, 7, 0);
   if (warp == 8) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem_base)
@@ -425,7 +453,8 @@ static cudaError_t launch_tile_t(const FusedProblem& pr, const void* img, cudaSt
   if (p.tiles == 0) return cudaSuccess;
   p.stage_bytes = tct::TILE * 128;
   p.w_bytes = (int)tile_image_bytes(KH, pr.cin);
-  const int fixed = p.w_bytes + (tct::TILE * (L::N + 1) + 2) * 4 + (2 * tct::MAX_STAGES + 5) * 8 + 16;
+  const int fixed = p.w_bytes + (2 * tct::TILE * tct::tile_pitch<KH, 3>() + 2) * 4 +
+                    (2 * tct::MAX_STAGES + 5) * 8 + 16;
   p.stages = std::min(tct::MAX_STAGES, (tct::SMEM_PER_CTA - fixed) / p.stage_bytes);
   if (p.stages < 2) return cudaErrorNotSupported;
   static const int dbg = getenv("SEGCONV_TC_DEBUG") ? atoi(getenv("SEGCONV_TC_DEBUG")) : 0;

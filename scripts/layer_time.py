@@ -1,6 +1,6 @@
 """Times single layers (bf16 or fp32) through transpose_conv_fused: python
 scripts/layer_time.py B N CIN COUT K P [dtype]; LAYER_MATH=tf32|f16x3|bf16|ffma picks
-the math (default auto); prints path and us per call."""
+the math (default auto); NOFLUSH=1 skips the L2 flush; prints path and us per call."""
 import statistics
 import sys
 
@@ -22,7 +22,8 @@ for _ in range(3):
     sc.transpose_conv_fused(x, sks, g, out=y)
 ts = []
 for _ in range(20):
-    flush.fill_(1)
+    if not os.environ.get("NOFLUSH"):
+        flush.fill_(1)
     a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     sc.transpose_conv_fused(x, sks, g, out=y)
