@@ -39,6 +39,11 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <queue>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -57,6 +62,7 @@ constexpr int WCH = 128;  // WGRAD: pixels (K) per chunk
 constexpr int MAX_TAPS_Q = 25;  // 5x5: the input-gradient walk uses every tap as one class
 constexpr int MAX_STAGES_A = 8, MAX_STAGES_B = 12;
 constexpr int SMEM_PER_CTA2 = 113 * 1024;  // two CTAs per SM (Params::cps == 2)
+constexpr int SCHED_MAX = 1536;  // unit-schedule table entries (Params::sched)
 
 struct Params {
   void* y;
@@ -123,12 +129,19 @@ struct Params {
   float* wout;
   unsigned long long* trace;
   int debug;
+  // IM2COL forward: per-pair unit lists from the host's balanced schedule
+  // (launch_wide_t): entry = unit | (feature half << 14), 0xFFFF ends a list;
+  // sched_slots == 0 keeps the round-robin order
+  int sched_slots;
+  int wh_ok;  // Maps::wh (half-width weight boxes) are encoded: half units may be scheduled
+  uint16_t sched[SCHED_MAX];
 };
 
 struct Maps {
   CUtensorMap x;     // (cin, Mv) bf16, box {64, S_rows}; TILE2D: (cin, n, n, batch), box {64, VW, TRH, 1}
   CUtensorMap w[4];  // class q: (cin, taps_q, cout_pad) bf16, box {64, 1, NT/2}, 128B swizzle
   CUtensorMap xi[4]; // IM2COL class q: (cin, n, n, batch), walk over its anchors, 64 ch x 128 px
+  CUtensorMap wh[4]; // as w, box {64, 1, NT/4}: a feature half unit's weights (Params::wh_ok)
 };
 
 // ---------------------------------------------------------------- PTX (pair)
@@ -281,9 +294,18 @@ __device__ __forceinline__ void trace_ev(const Params& p, int ev, int local) {
 // hf: 0 = whole feature tile; 1 / 2 = its first / second half (tail units)
 __device__ __forceinline__ bool unit_of(const Params& p, int k, long long& pt, int& nt, int& q, int& hf) {
   const long long pairs = gridDim.x / 2;
-  long long u = (long long)(blockIdx.x / 2) + (long long)k * pairs;
-  if (u >= p.units) return false;
+  long long u;
   hf = 0;
+  if (p.sched_slots > 0) {
+    if (k >= p.sched_slots) return false;
+    const unsigned e = p.sched[(blockIdx.x >> 1) * p.sched_slots + k];
+    if (e == 0xFFFFu) return false;
+    u = e & 0x3FFFu;
+    hf = (int)(e >> 14);
+  } else {
+    u = (long long)(blockIdx.x / 2) + (long long)k * pairs;
+    if (u >= p.units) return false;
+  }
   if (p.tail_on && u >= p.tail_full) {
     hf = 1 + (int)((u - p.tail_full) & 1);
     u = p.tail_full + ((u - p.tail_full) >> 1);
@@ -373,6 +395,8 @@ __global__ void __launch_bounds__(NUM_THREADS, CPS)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.w[q])) : "memory");
       if (p.im2col)
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.xi[q])) : "memory");
+      if (p.wh_ok)
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.wh[q])) : "memory");
     }
   }
   if (warp == 6) {
@@ -387,6 +411,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CPS)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) griddep_launch_dependents();  // next layer may start its prologue
+  if (threadIdx.x == 0) trace_ev(p, 12, 0);
 
   const int NT2 = p.NT / 2;
   const int NACC = p.nacc > 0 ? p.nacc : 2;
@@ -614,7 +639,10 @@ __global__ void __launch_bounds__(NUM_THREADS, CPS)
       int nt, q, hf;
       for (int k = 0; unit_of(p, k, pt, nt, q, hf); ++k) {
         const int f0 = hf ? nt * p.NT + (hf - 1) * NT2 + (int)rank * (NT2 / 2) : nt * p.NT + (int)rank * NT2;
-        const CUtensorMap* map = &maps.w[q];
+        // a scheduled feature half loads half-width weight boxes (the tail halves keep full boxes)
+        const bool hb = hf && p.wh_ok && p.sched_slots > 0;
+        const CUtensorMap* map = hb ? &maps.wh[q] : &maps.w[q];
+        const uint32_t btx = hb ? b_tx / 2 : b_tx;
         const int taps = p.taps[q];
         for (int pass = 0; pass < (p.split ? 3 : 1); ++pass)
           for (int kb = 0; kb < p.nkb; ++kb) {
@@ -626,7 +654,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CPS)
               ++gsb;
               if (elect_one()) {
                 const uint32_t bf = mapa(smem_u32(&a_full[sb]), 0);
-                if (rank == 0) mbar_arrive_expect_tx(&a_full[sb], (p.debug & 16) ? 0u : 2 * b_tx * (uint32_t)kst);
+                if (rank == 0) mbar_arrive_expect_tx(&a_full[sb], (p.debug & 16) ? 0u : 2 * btx * (uint32_t)kst);
                 const uint32_t dst = smem_u32(b_base + (size_t)sb * p.b_stage_bytes);
                 if (!(p.debug & 16))
                   for (int j = 0; j < kst; ++j) {
@@ -1038,6 +1066,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CPS)
   tc_fence_before();
   __syncthreads();
   cluster_sync();  // the pair's MMAs and remote arrivals are over before TMEM is freed
+  if (threadIdx.x == 0) trace_ev(p, 13, 0);
   if (warp == 6) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(CPS == 2 ? 256 : 512)
@@ -1392,6 +1421,14 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return false;
+    if (p.im2col && p.mode == 0 && !split && p.NT == 256) {  // feature-half units (balanced schedule)
+      const cuuint32_t hbox[3] = {(cuuint32_t)p.kbc, 1, (cuuint32_t)(p.NT / 4)};
+      if (fn(&maps.wh[q], op_type, 3, base, dims, strides, hbox, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+      p.wh_ok = q == 3 ? 1 : 0;
+    }
   }
   return true;
 }
@@ -1744,6 +1781,105 @@ bool tc_wide_supported(const FusedProblem& pr, int math) {
   return make_wide(pr, p, m, pr.x);  // pr.x stands in for the split copy (alignment only)
 }
 
+// Balanced unit schedule for the im2col forward (Params::sched).  Units are
+// class-major and a unit's length is its class's taps x k-blocks, so the
+// round-robin order leaves pairs with one long unit more than others (C5
+// layer a: 128 k-steps on the busiest pair for a mean of 111).  Longest unit
+// first onto the least-loaded pair; a unit of >= 12 stages that would
+// overshoot the mean is run as two feature halves (N = NT/2, half-width weight
+// boxes) on the two least-loaded pairs, costed at 0.65 of the unit each (half
+// the MMAs, but the same A tile).  Used when it beats round-robin; cached per
+// shape.  Measured on the C5 stack (eager layer times, 30 steps): layer a
+// 60.6 -> 56.7 us; splitting shorter units (layer b's 4- and 8-stage ones)
+// cost 1 us there, and with two CTAs per SM (layer c) the pairs sharing an SM
+// already even out -- a balanced order was 1.5 us slower -- so neither is done.
+static bool balance_units(tcw::Params& pk, long long pairs) {
+  if (!(pk.mode == 0 && pk.im2col) || pk.cps == 2 || pk.units <= 0 || pk.units > 0x3FFF || pairs <= 0 ||
+      pk.units <= pairs)
+    return false;
+  struct Key {
+    long long units, pairs, base[5];
+    int taps[4], nkb, split, wh;
+    bool operator<(const Key& o) const { return std::memcmp(this, &o, sizeof(Key)) < 0; }
+  };
+  Key key;
+  std::memset(&key, 0, sizeof(key));
+  key.units = pk.units;
+  key.pairs = pairs;
+  for (int q = 0; q < 5; ++q) key.base[q] = pk.unit_base[q];
+  for (int q = 0; q < 4; ++q) key.taps[q] = pk.taps[q];
+  key.nkb = pk.nkb;
+  key.split = pk.split;
+  key.wh = pk.wh_ok;
+  static std::mutex mu;
+  static std::map<Key, std::vector<uint16_t>> cache;  // empty vector: round-robin is as good
+  std::vector<uint16_t> tab;
+  int slots = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      tab = it->second;
+    } else {
+      std::vector<std::pair<int, int>> us;  // (cost, unit)
+      long long total = 0;
+      for (int q = 0; q < 4; ++q)
+        for (long long u = pk.unit_base[q]; u < pk.unit_base[q + 1]; ++u) {
+          const int c = pk.taps[q] * pk.nkb * (pk.split ? 3 : 1) * 100;
+          us.emplace_back(c, (int)u);
+          total += c;
+        }
+      long long rr_max = 0;
+      for (long long i = 0; i < pairs; ++i) {
+        long long l = 0;
+        for (long long u = i; u < (long long)us.size(); u += pairs) l += us[u].first;  // class-major = unit order
+        rr_max = std::max(rr_max, l);
+      }
+      std::stable_sort(us.begin(), us.end(), [](const std::pair<int, int>& a, const std::pair<int, int>& b) {
+        return a.first > b.first;
+      });
+      const double target = 1.02 * (double)total / (double)pairs;
+      using LP = std::pair<double, long long>;
+      std::priority_queue<LP, std::vector<LP>, std::greater<LP>> heap;
+      for (long long i = 0; i < pairs; ++i) heap.emplace(0.0, i);
+      std::vector<std::vector<uint16_t>> lists((size_t)pairs);
+      for (const auto& cu : us) {
+        const LP a = heap.top();
+        heap.pop();
+        if (pk.wh_ok && cu.first >= 1200 && a.first + cu.first > target) {
+          const LP b = heap.top();
+          heap.pop();
+          lists[(size_t)a.second].push_back((uint16_t)(cu.second | (1 << 14)));
+          lists[(size_t)b.second].push_back((uint16_t)(cu.second | (2 << 14)));
+          heap.emplace(a.first + 0.65 * cu.first, a.second);
+          heap.emplace(b.first + 0.65 * cu.first, b.second);
+        } else {
+          lists[(size_t)a.second].push_back((uint16_t)cu.second);
+          heap.emplace(a.first + cu.first, a.second);
+        }
+      }
+      double mx = 0;
+      while (!heap.empty()) {
+        mx = std::max(mx, heap.top().first);
+        heap.pop();
+      }
+      size_t sl = 0;
+      for (const auto& l : lists) sl = std::max(sl, l.size());
+      if (mx < 0.99 * (double)rr_max && (long long)sl * pairs <= tcw::SCHED_MAX) {
+        tab.assign((size_t)pairs * sl, (uint16_t)0xFFFF);
+        for (size_t i = 0; i < lists.size(); ++i)
+          std::copy(lists[i].begin(), lists[i].end(), tab.begin() + (long long)i * (long long)sl);
+      }
+      cache.emplace(key, tab);
+    }
+  }
+  if (tab.empty()) return false;
+  slots = (int)(tab.size() / (size_t)pairs);
+  std::copy(tab.begin(), tab.end(), pk.sched);
+  pk.sched_slots = slots;
+  return true;
+}
+
 template <typename YT, int ACT>
 static cudaError_t launch_wide_t(const tcw::Params& prm, const tcw::Maps& maps, cudaStream_t s) {
   auto kern = prm.cps == 2 ? tcw::wide_kernel<YT, ACT, 2> : tcw::wide_kernel<YT, ACT, 1>;
@@ -1756,9 +1892,11 @@ static cudaError_t launch_wide_t(const tcw::Params& prm, const tcw::Maps& maps, 
   const int sms = device_sm_count();
   long long pairs = std::min<long long>(prm.units, (long long)(sms / 2) * (prm.cps == 2 ? 2 : 1));
   tcw::Params pk = prm;
+  const bool no_balance = (prm.debug & 64) != 0;  // diagnostics (SEGCONV_TC_DEBUG): round-robin order
   // last partial wave: when its T units fit twice over, run them as 2T feature
   // half-tiles (N = NT/2) so the wave takes half a unit instead of a whole one
-  if (prm.mode == 0 && prm.im2col && prm.NT >= 128 && pairs > 0) {
+  if (!no_balance && balance_units(pk, pairs)) {
+  } else if (prm.mode == 0 && prm.im2col && prm.NT >= 128 && pairs > 0) {
     const long long T = prm.units % pairs;
     if (T > 0 && 2 * T <= pairs) {
       pk.tail_on = 1;

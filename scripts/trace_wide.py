@@ -57,3 +57,14 @@ if os.environ.get("TRACE_WAVES"):
     st, en = np.array(st), np.array(en)
     print(f"CTAs with events {len(st)}; start min {st.min():.2f} max {st.max():.2f}; end min {en.min():.2f} max {en.max():.2f}")
     print("starts sorted:", np.round(np.sort(st), 2)[-20:])
+
+# CTA lifetimes (ev12 = setup done, ev13 = exit), all traced CTAs
+st, ex = tr[:, 12, 0], tr[:, 13, 0]
+ok = ex > 0
+if ok.any():
+    exs = np.sort((ex[ok] - t0) / 1000)
+    print(f"setup done: min {(st[ok].min() - t0) / 1000:.2f} max {(st[ok].max() - t0) / 1000:.2f} us")
+    print("exit percentiles (us): " + " ".join(f"p{q}={np.percentile(exs, q):.2f}" for q in (0, 10, 25, 50, 75, 90, 100)))
+    nun = [(tr[c, 5, :] > 0).sum() for c in range(160) if ex[c] > 0]
+    print("units per CTA:", sorted(set(nun)), "mean busy fraction:",
+          round(float(np.mean(exs) / exs.max()), 3))
