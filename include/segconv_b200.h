@@ -357,6 +357,14 @@ uint64_t segconv_launch_count(void);
  * up to `bytes` of the 160 x 16 x 64 uint64 trace to host memory.  Returns the
  * bytes copied (0 when tracing is off). */
 size_t segconv_debug_trace(void* host_out, size_t bytes);
+/* Diagnostics / host-logic tests: the pair kernel's balanced unit schedule for
+ * units in class-major order (unit_base[5]: first unit of each class, [4] =
+ * total), cost taps[q] x nkb per unit, over `pairs` CTA pairs.  Writes the
+ * [pairs][slots] table (entry = unit | half << 14, half 1 / 2 = feature half,
+ * 0xFFFF = end of a pair's list) and returns slots, or 0 when round-robin is
+ * as good (or the table exceeds `cap` entries). */
+size_t segconv_debug_wide_schedule(const long long* unit_base, const int* taps, int nkb, long long pairs,
+                                   int halves, uint16_t* out, size_t cap);
 
 #ifdef __cplusplus
 }  /* extern "C" */

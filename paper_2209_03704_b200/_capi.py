@@ -104,6 +104,8 @@ SIGNATURES = {
     "segconv_version": (C.c_char_p, []),
     "segconv_launch_count": (C.c_uint64, []),
     "segconv_debug_trace": (_sz, [_vp, _sz]),
+    "segconv_debug_wide_schedule": (_sz, [C.POINTER(C.c_longlong), C.POINTER(C.c_int), _i, C.c_longlong, _i,
+                                          C.POINTER(C.c_uint16), _sz]),
 }
 
 _lib = None

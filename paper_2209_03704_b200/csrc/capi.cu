@@ -130,6 +130,12 @@ size_t segconv_debug_trace(void* host_out, size_t bytes) {
   return n;
 }
 
+size_t segconv_debug_wide_schedule(const long long* unit_base, const int* taps, int nkb, long long pairs,
+                                   int halves, uint16_t* out, size_t cap) {
+  if (!unit_base || !taps) return 0;
+  return debug_wide_schedule(unit_base, taps, nkb, pairs, halves, out, cap);
+}
+
 // reference geometry.hpp:29-53
 segconv_status segconv_tconv_geometry(int n_in, int kh, int kw, int p_orig, segconv_geometry* g) {
   if (!g) return fail(SEGCONV_E_CONTRACT, "geometry output pointer is null");

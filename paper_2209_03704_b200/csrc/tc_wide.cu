@@ -1793,18 +1793,73 @@ bool tc_wide_supported(const FusedProblem& pr, int math) {
 // 60.6 -> 56.7 us; splitting shorter units (layer b's 4- and 8-stage ones)
 // cost 1 us there, and with two CTAs per SM (layer c) the pairs sharing an SM
 // already even out -- a balanced order was 1.5 us slower -- so neither is done.
+// unit_base: first unit of each class (class-major), cost = taps x k-block
+// stages; returns the [pairs][slots] table, or empty when round-robin is as good
+static std::vector<uint16_t> wide_schedule(const long long* unit_base, const int* taps, int nkb, int passes,
+                                           bool halves, long long pairs) {
+  std::vector<uint16_t> tab;
+  const long long units = unit_base[4];
+  if (units <= 0 || units > 0x3FFF || pairs <= 0 || units <= pairs) return tab;
+  std::vector<std::pair<int, int>> us;  // (cost, unit)
+  long long total = 0;
+  for (int q = 0; q < 4; ++q)
+    for (long long u = unit_base[q]; u < unit_base[q + 1]; ++u) {
+      const int c = taps[q] * nkb * passes * 100;
+      us.emplace_back(c, (int)u);
+      total += c;
+    }
+  long long rr_max = 0;
+  for (long long i = 0; i < pairs; ++i) {
+    long long l = 0;
+    for (long long u = i; u < (long long)us.size(); u += pairs) l += us[u].first;  // class-major = unit order
+    rr_max = std::max(rr_max, l);
+  }
+  std::stable_sort(us.begin(), us.end(),
+                   [](const std::pair<int, int>& a, const std::pair<int, int>& b) { return a.first > b.first; });
+  const double target = 1.02 * (double)total / (double)pairs;
+  using LP = std::pair<double, long long>;
+  std::priority_queue<LP, std::vector<LP>, std::greater<LP>> heap;
+  for (long long i = 0; i < pairs; ++i) heap.emplace(0.0, i);
+  std::vector<std::vector<uint16_t>> lists((size_t)pairs);
+  for (const auto& cu : us) {
+    const LP a = heap.top();
+    heap.pop();
+    if (halves && cu.first >= 1200 && a.first + cu.first > target) {
+      const LP b = heap.top();
+      heap.pop();
+      lists[(size_t)a.second].push_back((uint16_t)(cu.second | (1 << 14)));
+      lists[(size_t)b.second].push_back((uint16_t)(cu.second | (2 << 14)));
+      heap.emplace(a.first + 0.65 * cu.first, a.second);
+      heap.emplace(b.first + 0.65 * cu.first, b.second);
+    } else {
+      lists[(size_t)a.second].push_back((uint16_t)cu.second);
+      heap.emplace(a.first + cu.first, a.second);
+    }
+  }
+  double mx = 0;
+  while (!heap.empty()) {
+    mx = std::max(mx, heap.top().first);
+    heap.pop();
+  }
+  size_t sl = 0;
+  for (const auto& l : lists) sl = std::max(sl, l.size());
+  if (mx < 0.99 * (double)rr_max && (long long)sl * pairs <= tcw::SCHED_MAX) {
+    tab.assign((size_t)pairs * sl, (uint16_t)0xFFFF);
+    for (size_t i = 0; i < lists.size(); ++i)
+      std::copy(lists[i].begin(), lists[i].end(), tab.begin() + (long long)i * (long long)sl);
+  }
+  return tab;
+}
+
 static bool balance_units(tcw::Params& pk, long long pairs) {
-  if (!(pk.mode == 0 && pk.im2col) || pk.cps == 2 || pk.units <= 0 || pk.units > 0x3FFF || pairs <= 0 ||
-      pk.units <= pairs)
-    return false;
+  if (!(pk.mode == 0 && pk.im2col) || pk.cps == 2 || pk.unit_base[4] != pk.units) return false;
   struct Key {
-    long long units, pairs, base[5];
+    long long pairs, base[5];
     int taps[4], nkb, split, wh;
     bool operator<(const Key& o) const { return std::memcmp(this, &o, sizeof(Key)) < 0; }
   };
   Key key;
   std::memset(&key, 0, sizeof(key));
-  key.units = pk.units;
   key.pairs = pairs;
   for (int q = 0; q < 5; ++q) key.base[q] = pk.unit_base[q];
   for (int q = 0; q < 4; ++q) key.taps[q] = pk.taps[q];
@@ -1814,70 +1869,27 @@ static bool balance_units(tcw::Params& pk, long long pairs) {
   static std::mutex mu;
   static std::map<Key, std::vector<uint16_t>> cache;  // empty vector: round-robin is as good
   std::vector<uint16_t> tab;
-  int slots = 0;
   {
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
-    if (it != cache.end()) {
-      tab = it->second;
-    } else {
-      std::vector<std::pair<int, int>> us;  // (cost, unit)
-      long long total = 0;
-      for (int q = 0; q < 4; ++q)
-        for (long long u = pk.unit_base[q]; u < pk.unit_base[q + 1]; ++u) {
-          const int c = pk.taps[q] * pk.nkb * (pk.split ? 3 : 1) * 100;
-          us.emplace_back(c, (int)u);
-          total += c;
-        }
-      long long rr_max = 0;
-      for (long long i = 0; i < pairs; ++i) {
-        long long l = 0;
-        for (long long u = i; u < (long long)us.size(); u += pairs) l += us[u].first;  // class-major = unit order
-        rr_max = std::max(rr_max, l);
-      }
-      std::stable_sort(us.begin(), us.end(), [](const std::pair<int, int>& a, const std::pair<int, int>& b) {
-        return a.first > b.first;
-      });
-      const double target = 1.02 * (double)total / (double)pairs;
-      using LP = std::pair<double, long long>;
-      std::priority_queue<LP, std::vector<LP>, std::greater<LP>> heap;
-      for (long long i = 0; i < pairs; ++i) heap.emplace(0.0, i);
-      std::vector<std::vector<uint16_t>> lists((size_t)pairs);
-      for (const auto& cu : us) {
-        const LP a = heap.top();
-        heap.pop();
-        if (pk.wh_ok && cu.first >= 1200 && a.first + cu.first > target) {
-          const LP b = heap.top();
-          heap.pop();
-          lists[(size_t)a.second].push_back((uint16_t)(cu.second | (1 << 14)));
-          lists[(size_t)b.second].push_back((uint16_t)(cu.second | (2 << 14)));
-          heap.emplace(a.first + 0.65 * cu.first, a.second);
-          heap.emplace(b.first + 0.65 * cu.first, b.second);
-        } else {
-          lists[(size_t)a.second].push_back((uint16_t)cu.second);
-          heap.emplace(a.first + cu.first, a.second);
-        }
-      }
-      double mx = 0;
-      while (!heap.empty()) {
-        mx = std::max(mx, heap.top().first);
-        heap.pop();
-      }
-      size_t sl = 0;
-      for (const auto& l : lists) sl = std::max(sl, l.size());
-      if (mx < 0.99 * (double)rr_max && (long long)sl * pairs <= tcw::SCHED_MAX) {
-        tab.assign((size_t)pairs * sl, (uint16_t)0xFFFF);
-        for (size_t i = 0; i < lists.size(); ++i)
-          std::copy(lists[i].begin(), lists[i].end(), tab.begin() + (long long)i * (long long)sl);
-      }
-      cache.emplace(key, tab);
-    }
+    if (it == cache.end())
+      it = cache.emplace(key, wide_schedule(pk.unit_base, pk.taps, pk.nkb, pk.split ? 3 : 1, pk.wh_ok != 0, pairs))
+               .first;
+    tab = it->second;
   }
   if (tab.empty()) return false;
-  slots = (int)(tab.size() / (size_t)pairs);
   std::copy(tab.begin(), tab.end(), pk.sched);
-  pk.sched_slots = slots;
+  pk.sched_slots = (int)(tab.size() / (size_t)pairs);
   return true;
+}
+
+// diagnostics / host-logic tests (segconv_debug_wide_schedule)
+size_t debug_wide_schedule(const long long* unit_base, const int* taps, int nkb, long long pairs, int halves,
+                           uint16_t* out, size_t cap) {
+  const std::vector<uint16_t> t = wide_schedule(unit_base, taps, nkb, 1, halves != 0, pairs);
+  if (t.empty() || out == nullptr || t.size() > cap) return 0;
+  std::copy(t.begin(), t.end(), out);
+  return t.size() / (size_t)pairs;
 }
 
 template <typename YT, int ACT>
