@@ -42,12 +42,12 @@ using namespace tc;
 
 constexpr int NUM_THREADS = 320;
 constexpr int SMEM_LIMIT = 227 * 1024;
-// Two CTAs per SM: a tile's epilogue (TMEM drain -> SMEM tile -> shift sums,
-// two named barriers) is serial within a CTA, so a second CTA's MMA and loads
-// run under it (measured: C5 layer d at one CTA per SM spent ~3.6k cycles per
-// 128-pixel tile, issue slots 28 % busy)
-constexpr int CTAS_PER_SM = 2;
-constexpr int SMEM_PER_CTA = 113 * 1024;
+// Two CTAs per SM: a tile's epilogue (TMEM drain -> SMEM tile -> shift sums)
+// is serial within a CTA, so the other CTA's MMAs and loads run under it
+// (measured: C5 layer d at one CTA per SM spent ~3.6k cycles per 128-pixel
+// tile, issue slots 28 % busy).  One CTA per SM when the weight image, the two
+// D tiles and two stages do not fit half the shared memory (4x4, cin >= 256).
+__host__ __device__ constexpr int smem_per_cta(int cps) { return cps == 2 ? 113 * 1024 : 227 * 1024; }
 constexpr int KB = 64;  // bf16 channels per stage: one 128-byte row
 constexpr int MAX_STAGES = 8;
 constexpr int TILE = 128;
@@ -102,8 +102,8 @@ __device__ __forceinline__ void drain_cols(uint32_t taddr, float* row) {
   }
 }
 
-template <int KH, int COUT, int ACT, typename YT>
-__global__ void __launch_bounds__(NUM_THREADS, CTAS_PER_SM)
+template <int KH, int COUT, int ACT, typename YT, int CPS>
+__global__ void __launch_bounds__(NUM_THREADS, CPS)
     tile_kernel(const __grid_constant__ Params p, const __grid_constant__ CUtensorMap tmap) {
   using L = ScatterLayout<KH, COUT>;
   constexpr int U = L::U, N = L::N, TP = tile_pitch<KH, COUT>();
@@ -394,9 +394,16 @@ bool tile_applies(int kh, int kw, int p, int n, int cin, int cout) {
   return tct::TILE - (U - 1) * (n + 1) >= 32;
 }
 
+// shared memory besides the activation stages: weight image, two D tiles, barriers
+static int tile_fixed_bytes(int kh, int cin) {
+  const int pitch = kh == 4 ? tct::tile_pitch<4, 3>() : tct::tile_pitch<3, 3>();
+  return (int)tile_image_bytes(kh, cin) + (2 * tct::TILE * pitch + 2) * 4 + (2 * tct::MAX_STAGES + 5) * 8 + 16;
+}
+
 static bool tile_shape(const FusedProblem& pr) {
   return tile_applies(pr.kh, pr.kw, pr.p, pr.n, pr.cin, pr.cout) && pr.x_dtype == SEGCONV_BF16 &&
-         (pr.y_dtype == SEGCONV_BF16 || pr.y_dtype == SEGCONV_F32);
+         (pr.y_dtype == SEGCONV_BF16 || pr.y_dtype == SEGCONV_F32) &&
+         tile_fixed_bytes(pr.kh, pr.cin) + 2 * tct::TILE * 128 <= tct::smem_per_cta(1);
 }
 
 bool tc_tile_supported(const FusedProblem& pr, int math) {
@@ -453,12 +460,15 @@ static cudaError_t launch_tile_t(const FusedProblem& pr, const void* img, cudaSt
   if (p.tiles == 0) return cudaSuccess;
   p.stage_bytes = tct::TILE * 128;
   p.w_bytes = (int)tile_image_bytes(KH, pr.cin);
-  const int fixed = p.w_bytes + (2 * tct::TILE * tct::tile_pitch<KH, 3>() + 2) * 4 +
-                    (2 * tct::MAX_STAGES + 5) * 8 + 16;
-  p.stages = std::min(tct::MAX_STAGES, (tct::SMEM_PER_CTA - fixed) / p.stage_bytes);
-  if (p.stages < 2) return cudaErrorNotSupported;
+  const int fixed = tile_fixed_bytes(KH, pr.cin);
   static const int dbg = getenv("SEGCONV_TC_DEBUG") ? atoi(getenv("SEGCONV_TC_DEBUG")) : 0;
   p.debug = dbg;
+  // two CTAs per SM (three measured no faster on the C5 stack: 121.8 vs 121.3 us);
+  // one where the weight image of a wide 4x4 layer leaves no room for two
+  int cps = 2;
+  while (cps > 1 && (tct::smem_per_cta(cps) - fixed) / p.stage_bytes < 2) --cps;
+  p.stages = std::min(tct::MAX_STAGES, (tct::smem_per_cta(cps) - fixed) / p.stage_bytes);
+  if (p.stages < 2) return cudaErrorNotSupported;
   p.trace = tc_trace_buffer();
   typedef CUresult (*Enc)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                           const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
@@ -483,15 +493,15 @@ static cudaError_t launch_tile_t(const FusedProblem& pr, const void* img, cudaSt
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorNotSupported;
   const int sms = device_sm_count();
-  const long long grid = std::min<long long>(p.tiles, (long long)tct::CTAS_PER_SM * sms);
+  const long long grid = std::min<long long>(p.tiles, (long long)cps * sms);
   const size_t smem = (size_t)p.stages * p.stage_bytes + fixed;
   const int act = (pr.epi & SEGCONV_EPI_RELU) ? 1 : (pr.epi & SEGCONV_EPI_TANH) ? 2 : 0;
   cudaError_t e = cudaSuccess;
 #define TILE_LAUNCH(A, YT)                                                                       \
   {                                                                                              \
-    auto kern = tct::tile_kernel<KH, 3, A, YT>;                                                  \
-    static PerDeviceOnce once;                                                                   \
-    e = smem_attr_once(once, kern, tct::SMEM_LIMIT);                                              \
+    auto kern = cps == 2 ? tct::tile_kernel<KH, 3, A, YT, 2> : tct::tile_kernel<KH, 3, A, YT, 1>;  \
+    static PerDeviceOnce once[2];                                                                \
+    e = smem_attr_once(once[cps - 1], kern, tct::SMEM_LIMIT);                                     \
     if (e != cudaSuccess) return e;                                                              \
     cudaLaunchConfig_t lc = {};                                                                 \
     lc.gridDim = dim3((unsigned)grid);                                                           \

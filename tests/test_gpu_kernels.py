@@ -262,10 +262,12 @@ def test_narrow_outputs_at_padding(batch, n, cin, cout, p, act, path):
 
 
 @pytest.mark.parametrize("batch,n,cin,p,odt", [(5, 8, 64, 0, torch.float32), (3, 16, 128, 2, torch.bfloat16),
-                                               (2, 21, 192, 2, torch.float32), (7, 5, 64, 2, torch.float32)])
+                                               (2, 21, 192, 2, torch.float32), (7, 5, 64, 2, torch.float32),
+                                               (3, 8, 256, 2, torch.bfloat16), (2, 9, 512, 2, torch.float32)])
 def test_tile_kernel_4x4(batch, n, cin, p, odt):
     """4x4 -> 3 on the tile kernel: p = 0 (folded panels) and even p > 0 (K-major
-    panels with the tile image appended); bf16 real data, tolerance as C5 d."""
+    panels with the tile image appended); bf16 real data, tolerance as C5 d.
+    cin 256 / 512: the weight image leaves room for one CTA per SM only."""
     rng = np.random.default_rng(batch * 3 + n + p)
     x = oracle.bf16_round(rng.standard_normal((batch, n, n, cin)).astype(np.float32))
     k = oracle.bf16_round((rng.standard_normal((4, 4, cin, 3)) * 0.02).astype(np.float32))
