@@ -354,7 +354,8 @@ const char* segconv_version(void);
 uint64_t segconv_launch_count(void);
 /* Diagnostics: with SEGCONV_TC_TRACE=1 in the environment the tensor-core
  * kernels stamp per-role events (globaltimer ns) for their first 160 CTAs; copies
- * up to `bytes` of the 160 x 16 x 64 uint64 trace to host memory.  Returns the
+ * up to `bytes` of the 160 x 16 x 64 uint64 trace to host memory (with
+ * SEGCONV_TC_TRACE=2: eight such slots, one per launch in turn).  Returns the
  * bytes copied (0 when tracing is off). */
 size_t segconv_debug_trace(void* host_out, size_t bytes);
 /* Diagnostics / host-logic tests: the pair kernel's balanced unit schedule for

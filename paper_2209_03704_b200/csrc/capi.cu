@@ -125,7 +125,7 @@ uint64_t segconv_launch_count(void) { return g_launches.load(); }
 size_t segconv_debug_trace(void* host_out, size_t bytes) {
   const unsigned long long* t = tc_trace_ptr();
   if (!t || !host_out) return 0;
-  const size_t n = std::min(bytes, (size_t)160 * 16 * 64 * sizeof(unsigned long long));
+  const size_t n = std::min(bytes, tc_trace_bytes());
   if (cudaMemcpy(host_out, t, n, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
   return n;
 }

@@ -135,6 +135,7 @@ cudaError_t launch_tc_igemm(const FusedProblem& pr, int math, cudaStream_t s);
 bool tc_igemm_supported(const FusedProblem& pr, int math);
 bool tc_igemm_available(int math, int cin, int cout);
 const unsigned long long* tc_trace_ptr();
+size_t tc_trace_bytes();
 size_t debug_wide_schedule(const long long* unit_base, const int* taps, int nkb, long long pairs, int halves,
                            uint16_t* out, size_t cap);
 unsigned long long* tc_trace_buffer();

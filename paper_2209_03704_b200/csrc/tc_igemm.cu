@@ -729,19 +729,30 @@ bool tc_igemm_supported(const FusedProblem& pr, int math) {
   return make_plan(pr, math).ok;
 }
 
-// SEGCONV_TC_TRACE=1: a device buffer of 160 CTAs x 8 events x 64 units of
+// SEGCONV_TC_TRACE=1: a device buffer of 160 CTAs x 16 events x 64 units of
 // globaltimer stamps, readable through segconv_debug_trace() (diagnostics only).
+// SEGCONV_TC_TRACE=2: eight such slots, one per launch in turn (a stack's
+// layers, each captured into its graph with its own slot).
 static unsigned long long* g_trace = nullptr;
+static int g_trace_slots = 0, g_trace_next = 0;
+constexpr size_t kTraceSlot = 160 * 16 * 64;
 unsigned long long* tc_trace_buffer() {
   static bool init = false;
   if (!init) {
     init = true;
     const char* e = getenv("SEGCONV_TC_TRACE");
-    if (e && e[0] == '1' && cudaMalloc(&g_trace, 160 * 16 * 64 * sizeof(unsigned long long)) == cudaSuccess)
-      cudaMemset(g_trace, 0, 160 * 16 * 64 * sizeof(unsigned long long));
+    const int slots = (e && e[0] == '1') ? 1 : (e && e[0] == '2') ? 8 : 0;
+    if (slots && cudaMalloc(&g_trace, slots * kTraceSlot * sizeof(unsigned long long)) == cudaSuccess) {
+      cudaMemset(g_trace, 0, slots * kTraceSlot * sizeof(unsigned long long));
+      g_trace_slots = slots;
+    }
   }
-  return g_trace;
+  if (!g_trace) return nullptr;
+  unsigned long long* t = g_trace + (size_t)(g_trace_next % g_trace_slots) * kTraceSlot;
+  if (g_trace_slots > 1) ++g_trace_next;
+  return t;
 }
+size_t tc_trace_bytes() { return (size_t)g_trace_slots * kTraceSlot * sizeof(unsigned long long); }
 const unsigned long long* tc_trace_ptr() { return g_trace; }
 
 template <int MODE, int NT, int G>

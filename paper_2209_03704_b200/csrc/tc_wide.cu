@@ -62,7 +62,9 @@ constexpr int WCH = 128;  // WGRAD: pixels (K) per chunk
 constexpr int MAX_TAPS_Q = 25;  // 5x5: the input-gradient walk uses every tap as one class
 constexpr int MAX_STAGES_A = 8, MAX_STAGES_B = 12;
 constexpr int SMEM_PER_CTA2 = 113 * 1024;  // two CTAs per SM (Params::cps == 2)
-constexpr int SCHED_MAX = 1536;  // unit-schedule table entries (Params::sched)
+// unit-schedule table entries (Params::sched): the parameters live in the
+// constant bank, whose misses on a kernel's first reads are slow -- keep it small
+constexpr int SCHED_MAX = 640;
 
 struct Params {
   void* y;
@@ -353,6 +355,7 @@ __device__ __forceinline__ float finish_bf(float v, const float* bias, unsigned 
 template <typename YT, int ACT, int CPS>
 __global__ void __launch_bounds__(NUM_THREADS, CPS)
     wide_kernel(const __grid_constant__ Params p, const __grid_constant__ Maps maps) {
+  if (threadIdx.x == 0) trace_ev(p, 14, 0);  // kernel entry (diagnostics)
   if (p.run_if != nullptr && *p.run_if == 0) return;  // every CTA alike: before any barrier or TMEM
   extern __shared__ __align__(1024) uint8_t smem[];
   const int SA = p.stages_a, SB = p.stages_b;
@@ -388,6 +391,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CPS)
       mbar_init(&acc_empty[s], 8);  // one arrive per epilogue warp of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    trace_ev(p, 15, 1);
   }
   if (warp == 4 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.x)) : "memory");
@@ -404,10 +408,13 @@ __global__ void __launch_bounds__(NUM_THREADS, CPS)
                      smem_u32(tmem_slot)), "r"(CPS == 2 ? 256 : 512)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    if (lane == 0) trace_ev(p, 15, 0);
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) trace_ev(p, 15, 2);
   cluster_sync();  // both CTAs' barriers initialised before any remote arrive
+  if (threadIdx.x == 0) trace_ev(p, 15, 3);
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) griddep_launch_dependents();  // next layer may start its prologue
