@@ -1799,7 +1799,8 @@ bool tc_wide_supported(const FusedProblem& pr, int math) {
 // shape.  Measured on the C5 stack (eager layer times, 30 steps): layer a
 // 60.6 -> 56.7 us; splitting shorter units (layer b's 4- and 8-stage ones)
 // cost 1 us there, and with two CTAs per SM (layer c) the pairs sharing an SM
-// already even out -- a balanced order was 1.5 us slower -- so neither is done.
+// already even out -- a balanced order was 1.5 us slower -- so neither is done
+// (see balance_units for where it is used).
 // unit_base: first unit of each class (class-major), cost = taps x k-block
 // stages; returns the [pairs][slots] table, or empty when round-robin is as good
 static std::vector<uint16_t> wide_schedule(const long long* unit_base, const int* taps, int nkb, int passes,
@@ -1859,7 +1860,14 @@ static std::vector<uint16_t> wide_schedule(const long long* unit_base, const int
 }
 
 static bool balance_units(tcw::Params& pk, long long pairs) {
-  if (!(pk.mode == 0 && pk.im2col) || pk.cps == 2 || pk.unit_base[4] != pk.units) return false;
+  // only with feature halves available and >= 2.5 waves of units: a longest-first
+  // order without halves, or over fewer waves, measured slower than round-robin
+  // (C5 at 512 images: 87.8 -> 92.0 us; layer c at 512: 25.9 -> 27.7 us) --
+  // round-robin runs a pixel tile's feature tiles on neighbouring pairs at the
+  // same time, and their shared A tiles then cost the L2 once
+  if (!(pk.mode == 0 && pk.im2col) || pk.cps == 2 || pk.unit_base[4] != pk.units || !pk.wh_ok ||
+      2 * pk.units < 5 * pairs)
+    return false;
   struct Key {
     long long pairs, base[5];
     int taps[4], nkb, split, wh;
