@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CPS)
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) trace_ev(p, 15, 2);
-  cluster_sync();  // both CTAs' barriers initialised before any remote arrive
+  cluster_sync_relaxed();  // both CTAs' barriers initialised before any remote arrive
   if (threadIdx.x == 0) trace_ev(p, 15, 3);
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;

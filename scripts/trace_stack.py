@@ -54,7 +54,7 @@ for name, s in zip("abcd", last):
         line += f"  gap(prev last exit -> first load) {us(f.min()) - us(prev_exit):5.2f}"
     print(line)
     if t[:, 13, 0].any():  # pair-kernel prologue, CTA 0 and the latest-entering CTA
-        for c in (0, int(np.argmax(np.where(ok, ent, 0)))):
+        for c in (0, 1, int(np.argmax(np.where(ok, ent, 0)))):
             print(f"   CTA {c}: entry {us(ent[c]):.2f} barriers {us(t[c, 15, 1]) if t[c, 15, 1] else float('nan'):.2f}"
                   f" tmem {us(t[c, 15, 0]) if t[c, 15, 0] else float('nan'):.2f} sync {us(t[c, 15, 2]):.2f}"
                   f" cluster {us(t[c, 15, 3]):.2f} setup {us(setup[c]):.2f} first load {us(first[c]) if first[c] else float('nan'):.2f}")
