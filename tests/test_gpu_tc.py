@@ -213,6 +213,8 @@ def test_multi_gpu_stack_c_abi_equals_generator_stack():
     assert t["n_gpus"] == 1 and t["compute_ms"] > 0 and t["h2d_ms"] > 0 and t["d2h_ms"] >= 0
     y7 = ms.forward(x[:7].contiguous())
     assert torch.equal(y7, ref[:7])
+    y0 = ms.forward(x[:0].contiguous())  # empty batch: empty output, no work
+    assert tuple(y0.shape) == (0,) + tuple(ref.shape[1:])
     ms.close()
 
 
