@@ -163,6 +163,14 @@ __device__ __forceinline__ void mbar_arrive_cl(uint32_t bar_cl) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cl)
                : "memory");
 }
+// Relaxed form for the epilogue's "accumulator drained" arrive: only the TMEM
+// reads (complete after tcgen05.wait::ld, ordered by the tcgen05 fences) must
+// precede the MMA's reuse of the columns -- a release would also hold the warp
+// until its outstanding global stores are acknowledged (an ERRBAR / membar
+// stall in the epilogue, 4 % of the C5 layer-b samples)
+__device__ __forceinline__ void mbar_arrive_cl_relaxed(uint32_t bar_cl) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cl) : "memory");
+}
 __device__ __forceinline__ void mbar_wait_cl(uint64_t* b, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -947,7 +955,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CPS)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cl(acc_empty_leader0 + (uint32_t)acc * 8);
+      if (lane == 0) mbar_arrive_cl_relaxed(acc_empty_leader0 + (uint32_t)acc * 8);
       if (++acc == NACC) {
         acc = 0;
         pacc ^= 1;
@@ -1062,7 +1070,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CPS)
       tc_fence_before();
       __syncwarp();
       if (threadIdx.x == 0 && rank == 0) trace_ev(p, 5, k);  // epilogue of the unit done (warp 0)
-      if (lane == 0) mbar_arrive_cl(acc_empty_leader0 + (uint32_t)acc * 8);
+      if (lane == 0) mbar_arrive_cl_relaxed(acc_empty_leader0 + (uint32_t)acc * 8);
       if (++acc == NACC) {
         acc = 0;
         pacc ^= 1;
