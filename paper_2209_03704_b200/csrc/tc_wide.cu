@@ -55,7 +55,12 @@ namespace tcw {
 
 using namespace tc;
 
-constexpr int NUM_THREADS = 224;
+constexpr int NUM_THREADS = 224;  // 0-3 epilogue, 4 A producer, 5 MMA issuer, 6 B producer / TMEM owner
+// One CTA per SM: four more epilogue warps (7-10; warp w drains TMEM lane
+// quadrant w % 4 with warp w - 7 .. , alternate 32-column chunks each) -- a
+// 256 x 256 unit's epilogue took longer than the MMAs of the short units
+// queued behind it.  Two CTAs per SM keep 224 threads (register budget).
+__host__ __device__ constexpr int wide_threads(int cps) { return cps == 2 ? NUM_THREADS : NUM_THREADS + 128; }
 constexpr int SMEM_LIMIT = 227 * 1024;
 constexpr int KB = 64;  // channels per stage: one 128-byte row
 constexpr int WCH = 128;  // WGRAD: pixels (K) per chunk
@@ -361,7 +366,7 @@ __device__ __forceinline__ float finish_bf(float v, const float* bias, unsigned 
 }
 
 template <typename YT, int ACT, int CPS>
-__global__ void __launch_bounds__(NUM_THREADS, CPS)
+__global__ void __launch_bounds__(wide_threads(CPS), CPS)
     wide_kernel(const __grid_constant__ Params p, const __grid_constant__ Maps maps) {
   if (threadIdx.x == 0) trace_ev(p, 14, 0);  // kernel entry (diagnostics)
   if (p.run_if != nullptr && *p.run_if == 0) return;  // every CTA alike: before any barrier or TMEM
@@ -396,7 +401,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CPS)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], 8);  // one arrive per epilogue warp of both CTAs
+      mbar_init(&acc_empty[s], (CPS == 1 && p.mode != 1) ? 16 : 8);  // one arrive per epilogue warp of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     trace_ev(p, 15, 1);
@@ -961,9 +966,12 @@ __global__ void __launch_bounds__(NUM_THREADS, CPS)
         pacc ^= 1;
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < 4 || (CPS == 1 && warp >= 7 && p.mode != 1)) {
     // ===== epilogue: lane = anchor; each thread writes its anchor's features
-    const uint32_t lane_base = tmem_base + ((uint32_t)(warp * 32) << 16);
+    // (one CTA per SM: two warps per TMEM lane quadrant, alternate column chunks)
+    const int qd = warp & 3;
+    const int c_first = (CPS == 1 && warp >= 7) ? 32 : 0, c_step = CPS == 1 ? 64 : 32;
+    const uint32_t lane_base = tmem_base + ((uint32_t)(qd * 32) << 16);
     const uint32_t acc_empty_leader0 = mapa(smem_u32(&acc_empty[0]), 0);
     const int img = p.n * p.n;
     int acc = 0;
@@ -978,7 +986,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CPS)
       bool in_range;
       if (p.im2col) {
         const int R = p.rows[q], C = p.cols[q];
-        const long long a = pt * 256 + (long long)rank * 128 + warp * 32 + lane;
+        const long long a = pt * 256 + (long long)rank * 128 + qd * 32 + lane;
         b = (int)(a / ((long long)R * C));
         const int rem = (int)(a - (long long)b * R * C);
         i = rem / C;
@@ -989,12 +997,12 @@ __global__ void __launch_bounds__(NUM_THREADS, CPS)
         b = (int)(g / p.tiles_per_img);
         const int trc = (int)(g - (long long)b * p.tiles_per_img);
         const int trow = trc / p.col_tiles, tcol = trc - trow * p.col_tiles;
-        const int t = warp * 32 + lane, jj = t % p.BW;
+        const int t = qd * 32 + lane, jj = t % p.BW;
         i = trow * p.TR + t / p.BW;
         j = tcol * p.BWo + jj;
         in_range = b < p.batch && t < p.TR * p.BW && jj < p.BWo;
       } else {
-        const long long m = pt * 256 + (long long)rank * 128 + warp * 32 + lane;
+        const long long m = pt * 256 + (long long)rank * 128 + qd * 32 + lane;
         b = (int)(m / img);
         const int rem = (int)(m - (long long)b * img);
         i = rem / p.n;
@@ -1013,7 +1021,7 @@ __global__ void __launch_bounds__(NUM_THREADS, CPS)
       const int fmax = p.cout - fbase;  // features of this tile that exist
       const float osc = (p.split || p.oscale) ? __ldg(p.split_inv_scale) : 1.0f;
 #pragma unroll 1
-      for (int c0 = 0; c0 < ((p.debug & 4) ? 0 : hf ? p.NT / 2 : p.NT); c0 += 32) {  // 4: diagnostics, no epilogue
+      for (int c0 = c_first; c0 < ((p.debug & 4) ? 0 : hf ? p.NT / 2 : p.NT); c0 += c_step) {  // 4: diagnostics, no epilogue
         float v[32];
         tmem_ld32(lane_base + cbase + (uint32_t)c0, v);
         if (p.split) {
@@ -1943,7 +1951,7 @@ static cudaError_t launch_wide_t(const tcw::Params& prm, const tcw::Maps& maps, 
                       (2 * tcw::MAX_STAGES_A + 2 * tcw::MAX_STAGES_B + 4) * 8 + 16;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * pairs));
-  cfg.blockDim = dim3(tcw::NUM_THREADS);
+  cfg.blockDim = dim3(tcw::wide_threads(prm.cps == 2 ? 2 : 1));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
