@@ -139,6 +139,7 @@ struct Params {
   // IM2COL forward: per-pair unit lists from the host's balanced schedule
   // (launch_wide_t): entry = unit | (feature half << 14), 0xFFFF ends a list;
   // sched_slots == 0 keeps the round-robin order
+  int epi8;  // one CTA per SM, forward: warps 7-10 join the epilogue (wide_threads)
   int sched_slots;
   int wh_ok;  // Maps::wh (half-width weight boxes) are encoded: half units may be scheduled
   uint16_t sched[SCHED_MAX];
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(wide_threads(CPS), CPS)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&acc_full[s], 1);
-      mbar_init(&acc_empty[s], (CPS == 1 && p.mode != 1) ? 16 : 8);  // one arrive per epilogue warp of both CTAs
+      mbar_init(&acc_empty[s], (CPS == 1 && p.epi8) ? 16 : 8);  // one arrive per epilogue warp of both CTAs
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     trace_ev(p, 15, 1);
@@ -966,11 +967,12 @@ __global__ void __launch_bounds__(wide_threads(CPS), CPS)
         pacc ^= 1;
       }
     }
-  } else if (warp < 4 || (CPS == 1 && warp >= 7 && p.mode != 1)) {
+  } else if (warp < 4 || (CPS == 1 && warp >= 7 && p.epi8)) {
     // ===== epilogue: lane = anchor; each thread writes its anchor's features
     // (one CTA per SM: two warps per TMEM lane quadrant, alternate column chunks)
     const int qd = warp & 3;
-    const int c_first = (CPS == 1 && warp >= 7) ? 32 : 0, c_step = CPS == 1 ? 64 : 32;
+    const bool e8 = CPS == 1 && p.epi8;
+    const int c_first = (e8 && warp >= 7) ? 32 : 0, c_step = e8 ? 64 : 32;
     const uint32_t lane_base = tmem_base + ((uint32_t)(qd * 32) << 16);
     const uint32_t acc_empty_leader0 = mapa(smem_u32(&acc_empty[0]), 0);
     const int img = p.n * p.n;
@@ -1172,6 +1174,10 @@ static int wide_bprod() { return 1; }
 
 static int wide_pairs();
 
+static int wide_debug_bits() {
+  static const int dbg = getenv("SEGCONV_TC_DEBUG") ? atoi(getenv("SEGCONV_TC_DEBUG")) : 0;
+  return dbg;
+}
 static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, const void* xs = nullptr) {
   p = tcw::Params{};
   const bool split = pr.x_dtype == SEGCONV_F32 && pr.panel_dtype == SEGCONV_F16_SPLIT;
@@ -1347,6 +1353,14 @@ static bool make_wide(const FusedProblem& pr, tcw::Params& p, tcw::Maps& maps, c
     p.kstage = (p.cps == 1 && !split && !tf32 && p.mode == 0 && pr.cin % (2 * tcw::KB) == 0 &&
                 2 * (p.a_stage_bytes + p.b_stage_bytes) * 3 <= budget) ? 2 : 1;
     p.nkb = pr.cin / (p.kbc * p.kstage);
+    // eight epilogue warps where some class's units are short (< 12 stages), so
+    // a unit's epilogue would outlast the MMAs of the next: C5 115.7 vs 117.3 us;
+    // with only long units (C3: 16 stages each) four are faster (76.7 vs 77.2 us)
+    {
+      int min_st = 1 << 30;
+      for (int q = 0; q < 4; ++q) min_st = std::min(min_st, p.taps[q] * p.nkb * (split ? 3 : 1));
+      p.epi8 = (p.cps == 1 && p.mode == 0 && min_st < 12 && !(wide_debug_bits() & 256)) ? 1 : 0;  // debug 256: four
+    }
     p.a_stage_bytes *= p.kstage;
     p.b_stage_bytes *= p.kstage;
     p.stages_a = p.stages_b = std::min(tcw::MAX_STAGES_A, budget / (p.a_stage_bytes + p.b_stage_bytes));
