@@ -33,7 +33,9 @@
 //
 // Warp roles (224 threads per CTA): 0-3 epilogue (lane = anchor: each thread
 // stores its anchor's features contiguously, bias / ReLU / tanh fused),
-// 4 TMA producer, 5 MMA issuer (leader CTA), 6 TMEM allocator.
+// 4 A (activation) TMA producer, 5 MMA issuer (leader CTA), 6 B (weight) TMA
+// producer and TMEM allocator; at one CTA per SM 352 threads, warps 7-10 a
+// second set of epilogue warps (Params::epi8).
 #include <cuda.h>
 #include <cuda_fp16.h>
 
