@@ -174,6 +174,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   if (threadIdx.x == 0) trace_ev(p, 10, 0);  // prologue done
+  // launched with programmatic stream serialization: the barrier init, TMEM
+  // allocation and tensormap prefetch above overlap the previous kernel's tail;
+  // every global access (weights, halo loads, stores, guard fallback) follows
+  // this wait, so what the previous kernel wrote (the weight image of a
+  // just-segregated kernel, x) is visible and nothing it still reads is overwritten.
+  griddep_wait();
 
   const int NKB = p.cin / KB;                   // stages per unit
   const int KS = p.cin / 16;                    // K=16 steps over cin
@@ -652,10 +658,19 @@ static cudaError_t launch_fold_ts_t(const tcfs::Params& prm, const CUtensorMap& 
   const long long units = (prm.Mv + 127) / 128;
   long long grid = std::min<long long>(units, sms);
   const size_t smem = (size_t)tcfs::STAGES * prm.stage_bytes + (3 * tcfs::STAGES + 6) * 8 + 16;
-  const tcfs::Params& pc = prm;
-  kern<<<(unsigned)grid, tcfs::NUM_THREADS, smem, s>>>(pc, tmap);
-  note_launch();
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(tcfs::NUM_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // prologue overlaps the
+  at[0].val.programmaticStreamSerializationAllowed = 1;              // previous kernel's tail
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, prm, tmap);
+  if (e == cudaSuccess) note_launch();
+  return e;
 }
 
 cudaError_t launch_tc_fold_ts(const FusedProblem& pr, const void* img, cudaStream_t s) {

@@ -155,6 +155,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // programmatic stream serialization: the prologue above overlaps the previous
+  // kernel's tail; every global access (weight image, pixel rows, stores, guard
+  // fallback) follows this wait.
+  griddep_wait();
 
   const int NH = p.cin / KB;   // stages per pixel row
   const int TILES = p.n / 128;  // M-tiles per pixel row
@@ -560,7 +564,18 @@ cudaError_t launch_tc_ring(const FusedProblem& pr, const void* ring_img, cudaStr
     static PerDeviceOnce once;                                                                   \
     e = smem_attr_once(once, kern, tcr::SMEM_LIMIT);                                              \
     if (e != cudaSuccess) return e;                                                              \
-    kern<<<(unsigned)grid, tcr::NUM_THREADS, smem, s>>>(p, tmap);                                \
+    cudaLaunchConfig_t cfg = {};                                                                 \
+    cfg.gridDim = dim3((unsigned)grid);                                                          \
+    cfg.blockDim = dim3(tcr::NUM_THREADS);                                                       \
+    cfg.dynamicSmemBytes = smem;                                                                 \
+    cfg.stream = s;                                                                              \
+    cudaLaunchAttribute at[1];                                                                   \
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                               \
+    at[0].val.programmaticStreamSerializationAllowed = 1;                                        \
+    cfg.attrs = at;                                                                              \
+    cfg.numAttrs = 1;                                                                            \
+    e = cudaLaunchKernelEx(&cfg, kern, p, tmap);                                                 \
+    if (e != cudaSuccess) return e;                                                              \
   }
   if (act == 1)
     RING_LAUNCH(1)
