@@ -71,6 +71,17 @@ CONFIGS = {
 SEED = 20240911
 
 
+_DIST = [False]
+
+
+def dist_on():
+    """The GPU arm runs over a process group (NCCL): at world size > 1, or at
+    world size 1 under --dist (the driver's launch form exercised end to end on
+    a one-GPU box: NCCL init, the weight broadcast, the max-over-ranks
+    reduction and the all-gather, each a one-rank collective)."""
+    return _DIST[0]
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -154,7 +165,7 @@ class Layer:
         self.k_host = gen((k, k, cin, cout), cfg["wd"], krng, fan_in=cin * k * k)
         self.tdt = torch.bfloat16 if cfg["dtype"] == "bf16" else torch.float32
         kd = torch.from_numpy(self.k_host).to(dev)
-        if world > 1:  # weights replicated from rank 0 (NCCL broadcast, untimed)
+        if dist_on():  # weights replicated from rank 0 (NCCL broadcast, untimed)
             torch.distributed.broadcast(kd, src=0)
         self.kd = kd.to(self.tdt)
         self.xd = torch.from_numpy(self.x_host).to(dev, self.tdt)
@@ -296,7 +307,7 @@ class LayerBackward(Layer):
         self.gk_pinned = torch.empty(self.kd.shape, dtype=torch.float32).pin_memory()
 
     def step(self):
-        if self.world > 1:
+        if dist_on():
             # data-parallel step: the kernel gradient's all-reduce (NCCL) runs while
             # the input-gradient kernel computes (paper_2209_03704_b200/dp.py)
             _, gk = self.sc.transpose_conv_fused_backward(self.xd, self.kd, self.cfg["p"], self.gyd,
@@ -425,7 +436,7 @@ class Stack:
         s0 = self.specs[0]
         rng = np.random.default_rng(SEED + 1)
         xall = rng.standard_normal((gb, s0.n_in, s0.n_in, s0.cin), dtype=np.float32)
-        if world > 1:
+        if dist_on():
             self.sharded = st.ShardedStack(self.specs, ks, gb, act_dtype=torch.bfloat16)
             self.stack = self.sharded.local
             self.lo, self.hi = self.sharded.lo, self.sharded.hi
@@ -797,6 +808,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true",
                     help="diagnostics (ncu launch lists): skip the host-buffer e2e leg")
     ap.add_argument("--no-parity", action="store_true", help="skip the sampled oracle check")
+    ap.add_argument("--dist", action="store_true",
+                    help="use the NCCL process group even at world size 1 (launcher plumbing check)")
     ap.add_argument("--batch", type=int, default=None,
                     help="diagnostics: override the config's batch (not a headline line)")
     ap.add_argument("--plumbing-check", action="store_true",
@@ -830,7 +843,8 @@ def main():
         raise SystemExit("bench.py: no CUDA device (the segconv arm has no CPU fallback)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    _DIST[0] = world > 1 or args.dist
+    if dist_on():
         dist.init_process_group("nccl", device_id=dev)
     from paper_2209_03704_b200 import segconv as sc
 
@@ -871,7 +885,7 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, each bracketed by events; L2 flushed between steps
-    if world > 1:
+    if dist_on():
         dist.barrier()
     torch.cuda.synchronize()
     l0 = sc.launch_count()
@@ -888,17 +902,17 @@ def main():
     if graph is not None or cfg.get("stack"):
         # graph replays bypass the host-side counter: count the captured kernels
         launches = args.steps * prob.launches_per_step
-    if world > 1:
+    if dist_on():
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     tot_ms = sum(step_ms)
     t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
-    if world > 1:
+    if dist_on():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     tot_ms = float(t.item())
     ms = tot_ms / args.steps
     macs_all = prob.macs * world if not cfg.get("stack") else prob.macs
-    if cfg.get("stack") and world > 1:
+    if cfg.get("stack") and dist_on():
         mt = torch.tensor([prob.macs], device=dev, dtype=torch.float64)
         dist.all_reduce(mt)
         macs_all = float(mt.item())
@@ -912,7 +926,7 @@ def main():
             parity["pass"] = bool(parity["max_scaled_err"] <= parity["tol"])
         except Exception as e:  # report, do not hide
             parity = {"error": str(e)[:200], "pass": False}
-        if world > 1:
+        if dist_on():
             pf = torch.tensor([0.0 if parity.get("pass") else 1.0], device=dev)
             dist.all_reduce(pf, op=dist.ReduceOp.MAX)
             parity["all_ranks_pass"] = bool(pf.item() == 0.0)
@@ -921,7 +935,7 @@ def main():
     gather = None
     if cfg.get("stack"):
         gms = 0.0
-        if world > 1:
+        if dist_on():
             for _ in range(2):
                 prob.gather()
             torch.cuda.synchronize()
@@ -938,14 +952,14 @@ def main():
             assert full.shape[0] == prob.global_batch
         gather = {"ms": round(gms, 5), "bytes_total": int(prob.global_batch * prob.stack.out[0].numel() * 2),
                   "what": "ShardedStack.gather: NCCL all-gather of the bf16 output shards"
-                          if world > 1 else "single rank: nothing to gather"}
+                          if dist_on() else "single rank: nothing to gather"}
 
     # ---- e2e through the public API with host buffers (H2D + compute + D2H)
     e2e_steps = 0 if args.no_e2e else args.steps
     for _ in range(2 if e2e_steps else 0):
         prob.step_e2e()
     torch.cuda.synchronize()
-    if world > 1:
+    if dist_on():
         dist.barrier()
     ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
@@ -959,7 +973,7 @@ def main():
     # output is on the host: time it by the host clock (it is synchronous)
     per = (wall_ms if getattr(prob, "capi", None) is not None else ea.elapsed_time(eb)) / max(1, e2e_steps)
     e2e_ms = torch.tensor([per], device=dev, dtype=torch.float64)
-    if world > 1:
+    if dist_on():
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
     h2d, d2h = prob.e2e_bytes()
@@ -1107,7 +1121,7 @@ def main():
                 out["strong_scaling_proxy"] = sweep
         out.update(extra)
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if dist_on():
         dist.barrier()
         dist.destroy_process_group()
 
