@@ -65,3 +65,14 @@ def test_reference_arm_config_equals_the_gpu_arms():
         assert a == bench.config_dict(name, cfg, 1)
         assert set(a) == {"workload", "global_batch", "per_rank_batch", "parallelism", "l2"}
     assert bench.config_dict("C5", bench.CONFIGS["C5"], 8)["per_rank_batch"] == 128
+
+
+def test_dist_flag_is_off_by_default_and_accepted():
+    """`--dist` (NCCL process group at world size 1, the driver's torchrun form)
+    is opt-in: a plain one-rank run keeps no process group."""
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.dist_on() is False
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--help"],
+                       capture_output=True, text=True, timeout=120, cwd=ROOT)
+    assert r.returncode == 0 and "--dist" in r.stdout
